@@ -1,0 +1,168 @@
+/* walklap.h — C ABI of the B200 walk-based Laplacian library (libwalklap.so).
+ *
+ * Implements the data-parallel hot path of arXiv 2601.11338 (F. Arrigo, F. Durastante,
+ * "Walk based Laplacians for Modeling Diffusion on Complex Networks"):
+ *   * total communicability t = φ_θ(A,c) 1              ("a single evaluation")
+ *   * Laplacian action 𝕃_θ(c) V = diag(t) V - φ_θ(A,c) V  (eq:weighted_laplacian)
+ *   * matrix-function action φ_θ(A,c) V                  (Prop. pro:whe-we-converge)
+ *   * diffusion exp(-τ 𝕃_θ) x0 for a sweep of τ
+ * where φ_θ(A,c) = Σ_k c_k q_k(A), q_k the backtrack-downweighted walk counts of eq:qrec
+ * with θ = 1 - μ: θ = 1 all walks, θ = 0 nonbacktracking (eq:Br).
+ * Every action is evaluated by polynomial Krylov (Arnoldi) on the 2n x 2n companion
+ * operator Z = [[O, I], [μ(μI - D), A]] (eq:Zdef) started from [q_1 v; q_2 v]; the small
+ * projected function f_1(H_k) (eq:fs with s = 1) is evaluated on the device.
+ *
+ * Conventions (all entry points):
+ *  - Return WL_OK (0) on success.  On failure a thread-local message is available from
+ *    wl_last_error().  Argument errors are detected synchronously before anything is enqueued.
+ *  - Pointers documented as "device" must be CUDA device (or managed) memory on the operator's
+ *    device; "host" pointers are ordinary host memory.  The caller owns every buffer it passes.
+ *  - Work is stream-ordered on `stream` (a cudaStream_t passed as void*; NULL = legacy default
+ *    stream) and asynchronous unless stated: results are valid after the stream is synchronized.
+ *  - Dense blocks are row-major: element (row r, column c) of a block with leading dimension ld
+ *    lives at ptr[r * ld + c]; ld >= number of columns.
+ *  - Multi-GPU: every rank calls the same functions collectively with its own contiguous row range
+ *    (from wl_partition); inputs and outputs are row-distributed the same way.
+ *  - Handles are opaque and owned by the library until the matching *_destroy.
+ */
+#ifndef WALKLAP_H
+#define WALKLAP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  WL_OK = 0,
+  WL_EINVAL = 1,      /* bad argument: θ ∉ [0,1], b < 1, ld < columns, null pointer, sizes */
+  WL_EGRAPH = 2,      /* CSR not simple/symmetric-compatible: unsorted row_ptr, column out of range,
+                         self loop or duplicate entry (simple graphs only) */
+  WL_EDIVERGE = 3,    /* resolvent with α·ρ ≥ 1: the series of Prop. pro:whe-we-converge diverges
+                         (Remark P:390-392) */
+  WL_ENOCONV = 4,     /* reserved: a-posteriori Krylov check failed (best iterate still written) */
+  WL_ENOMEM = 5,      /* device allocation failed */
+  WL_ECUDA = 6,       /* CUDA runtime error (message has the CUDA error string) */
+  WL_ENCCL = 7,       /* NCCL error */
+  WL_EUNSUPPORTED = 8 /* size/feature outside this build (e.g. local nnz >= 2^31) */
+} wl_status;
+
+typedef enum {
+  WL_WALK = 0, /* all walks: θ = 1 (μ = 0), 𝕃(f) = diag(f(A)1) - f(A), eq:f-laplacian */
+  WL_NBT = 1,  /* nonbacktracking: θ = 0 (μ = 1), p_k of eq:Br */
+  WL_BTDW = 2  /* backtrack-downweighted: θ ∈ [0,1] given explicitly */
+} wl_variant;
+
+typedef enum {
+  WL_F_EXP = 0,       /* c_k = β^k / k!  (f = exp(βx); inverse temperature β) */
+  WL_F_RESOLVENT = 1, /* c_k = α^k       (f = (1 - αx)^{-1}) */
+  WL_F_SERIES = 2     /* explicit c_0..c_{K}, zero beyond (Def. def:transformedlaplacian) */
+} wl_fkind;
+
+/* Walk weights {c_k} of Def. def:BDTW-Laplacian.  `coeffs` (host, ncoeffs entries) is read only
+ * for WL_F_SERIES and copied by wl_operator_create. */
+typedef struct {
+  int32_t kind;         /* wl_fkind */
+  double param;         /* β (WL_F_EXP) or α (WL_F_RESOLVENT) */
+  const double* coeffs; /* host; WL_F_SERIES only */
+  int32_t ncoeffs;      /* 1..64; WL_F_SERIES only */
+} wl_walkfun;
+
+/* Options; initialise with wl_opts_default(). */
+typedef struct {
+  int32_t krylov_dim;   /* Arnoldi steps k per action (default 30; 1..64) */
+  int32_t reorth;       /* 1 = classical Gram-Schmidt twice (CGS2, default); 0 = single CGS pass */
+  int32_t max_cols;     /* columns per internal Krylov batch (default 32; 1..32) */
+  double breakdown_tol; /* lucky breakdown when ||w_{j+1}|| <= tol * ||Z q_j|| (default 1e-12) */
+  double rho_bound;     /* optional upper bound on ρ(Z_θ) (e.g. ρ(A), which bounds it since
+                           0 <= q_k <= A^k): a resolvent with α * rho_bound >= 1 is rejected with
+                           WL_EDIVERGE (Prop. pro:whe-we-converge).  0 = no check (default). */
+} wl_opts;
+
+typedef struct wl_comm wl_comm;
+typedef struct wl_operator wl_operator;
+typedef struct wl_workspace wl_workspace;
+typedef void* wl_stream; /* cudaStream_t */
+
+void wl_opts_default(wl_opts* opts);
+const char* wl_last_error(void);
+const char* wl_version(void);
+/* Number of CUDA kernels this library has launched in the calling process (monotone counter). */
+int64_t wl_launch_count(void);
+
+/* ---- multi-GPU plumbing (NCCL over NVLink; one process per GPU) --------------------------- */
+/* Rank 0 creates a 128-byte NCCL unique id (host buffer `out128`) and broadcasts it. */
+wl_status wl_nccl_unique_id(void* out128);
+/* Collective over `nranks` processes; binds `device`.  comm = NULL everywhere means 1 GPU. */
+wl_status wl_comm_create(int32_t nranks, int32_t rank, const void* id128, int32_t device,
+                         wl_comm** out);
+void wl_comm_destroy(wl_comm* comm);
+
+/* nnz-balanced contiguous row partition (host, bit-exact integer arithmetic):
+ * bounds[0] = 0, bounds[nranks] = n, bounds[p] = smallest r with row_ptr[r] >= ceil(p*nnz/nranks)
+ * (clamped to be nondecreasing).  row_ptr: host, n+1 entries.  bounds_out: host, nranks+1. */
+wl_status wl_partition(int64_t n, const int64_t* row_ptr, int32_t nranks, int64_t* bounds_out);
+
+/* ---- operator --------------------------------------------------------------------------------
+ * Builds the operator for rows [row_begin, row_end) of an n_global-node simple graph and
+ * computes + caches t_θ = φ_θ(A,c) 1 for every requested θ (step a8; synchronous on return).
+ *   row_ptr_local : host, (row_end-row_begin)+1 entries, global nnz offsets of the local rows
+ *                   (row_ptr_local[0] need not be 0)
+ *   col_idx_local : host, global column ids of those rows (sorted per row, no self loops/dups)
+ *   variant       : WL_WALK / WL_NBT force θ = 1 / θ = 0 and require n_theta == 1;
+ *                   WL_BTDW takes thetas[0..n_theta) ∈ [0,1] (host)
+ *   n_theta       : 1..32 downweighting values evaluated together (a θ sweep); an action on a
+ *                   b-column block V returns n_theta*b columns (see wl_apply)
+ *   f, opts       : walk weights and options (copied)
+ * The CSR is copied to device memory; host arrays may be freed on return.  WL_EGRAPH on
+ * malformed CSR; WL_EDIVERGE for a resolvent with α * opts->rho_bound >= 1. */
+wl_status wl_operator_create(wl_comm* comm, int64_t n_global, int64_t row_begin, int64_t row_end,
+                             const int64_t* row_ptr_local, const int32_t* col_idx_local,
+                             int32_t variant, int32_t n_theta, const double* thetas,
+                             const wl_walkfun* f, const wl_opts* opts, wl_stream stream,
+                             wl_operator** out);
+void wl_operator_destroy(wl_operator* op);
+/* Local sizes: n_local rows, nnz_local, halo rows, number of θ values. Any pointer may be NULL. */
+wl_status wl_operator_info(const wl_operator* op, int64_t* n_local, int64_t* nnz_local,
+                           int64_t* n_halo, int32_t* n_theta);
+/* Copies t_θ = φ_θ 1 (device, n_local x n_theta, ld ldt >= n_theta) — the "diagonal shift". */
+wl_status wl_operator_diag_shift(const wl_operator* op, double* t_dev, int64_t ldt,
+                                 wl_stream stream);
+
+/* Workspace for actions on up to max_b input columns (device memory is allocated here: the
+ * Krylov basis takes (k+1) * 2 * n_local * min(32, n_theta*max_b) doubles). */
+wl_status wl_workspace_create(const wl_operator* op, int32_t max_b, wl_workspace** out);
+void wl_workspace_destroy(wl_workspace* ws);
+
+/* ---- actions (step a3-a7) -------------------------------------------------------------------
+ * V  : device, n_local x b, leading dimension ldv >= b
+ * LV : device, n_local x (n_theta*b), ldlv >= n_theta*b;
+ *      column i*b + c receives 𝕃_{θ_i} V[:, c]  (wl_apply) or φ_{θ_i} V[:, c] (wl_phi_apply).
+ * V and LV must not overlap.  1 <= b <= max_b of the workspace.  Asynchronous on `stream`. */
+wl_status wl_apply(const wl_operator* op, int32_t b, const double* V, int64_t ldv, double* LV,
+                   int64_t ldlv, wl_workspace* ws, wl_stream stream);
+wl_status wl_phi_apply(const wl_operator* op, int32_t b, const double* V, int64_t ldv,
+                       double* LV, int64_t ldlv, wl_workspace* ws, wl_stream stream);
+/* Same as wl_apply with HOST buffers (pinned or pageable): copies V to the device, applies, and
+ * copies the result back inside the call; synchronous (returns after LV is written). */
+wl_status wl_apply_host(const wl_operator* op, int32_t b, const double* V_host, int64_t ldv,
+                        double* LV_host, int64_t ldlv, wl_workspace* ws, wl_stream stream);
+
+/* ---- diffusion (step a9) --------------------------------------------------------------------
+ * X[:, s] = exp(-tau[s] 𝕃_{θ_i}) x0 for s < nt, i = theta_index, by an outer Lanczos process of
+ * dimension k_out on the symmetric 𝕃 (each step one wl_apply) with full reorthogonalisation,
+ * then X = ||x0|| Q_out exp(-tau T) e_1 (dense exponential of the k_out x k_out tridiagonal T).
+ *   tau : host, nt >= 1 values >= 0;   x0 : device, n_local;   X : device, n_local x nt (ldx).
+ * 2 <= k_out <= 128.  Asynchronous on `stream`. */
+wl_status wl_diffuse(const wl_operator* op, int32_t theta_index, int32_t nt, const double* tau,
+                     const double* x0, double* X, int64_t ldx, int32_t k_out, wl_workspace* ws,
+                     wl_stream stream);
+
+/* Synchronizes `stream` and returns the first asynchronous error recorded on `op` (or WL_OK). */
+wl_status wl_wait(const wl_operator* op, wl_stream stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WALKLAP_H */

@@ -1,0 +1,891 @@
+// engine.cu — host orchestration of the walk-Laplacian Krylov path and the C ABI (walklap.h).
+//
+// One "action" on a chunk of B <= 32 columns (column c = (θ index, input column)) is
+// (SURVEY §8(a) a3-a7):
+//   a3  u = [A v ; A(Av) - μ d⊙v]                          two Z-SpMM launches (seeds q_1 v, q_2 v)
+//   a4  for j < k: w = Z q_j  (bottom half only)           spmv (merge-path, fused recurrence)
+//   a5            CGS2 of w against q_0..q_j, ||w''||       gram_proj / gram_update_proj /
+//                                                           gram_update_norm + finalize_step
+//   a6  y = f_1(H_k) e_1 on the device                     small_f
+//   a7  φv = c_0 v + ||u|| [I O] Q_k y ;  𝕃v = t'⊙v - (φv - c_0 v)    combine
+// with t' = φ1 - c_0 1 cached at operator creation (a8).  Multi-GPU: the SpMM input rows owned
+// by other ranks are exchanged (grouped ncclSend/ncclRecv) before each SpMM and every Gram
+// reduction is summed with ncclAllReduce, so H is bit-identical on every rank.
+#include "walklap.h"
+#include "wl_internal.cuh"
+
+#include <nccl.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <vector>
+
+namespace wl {
+
+static std::atomic<int64_t> g_launches{0};
+void note_launch(const char*) { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+  if (e == cudaSuccess) return;
+  const std::string msg = std::string(what) + ": " + cudaGetErrorString(e) + " (" + file + ":" +
+                          std::to_string(line) + ")";
+  if (e == cudaErrorMemoryAllocation) throw Error(WL_ENOMEM, msg);
+  throw Error(WL_ECUDA, msg);
+}
+
+#define WL_NCCL(x)                                                                        \
+  do {                                                                                    \
+    ncclResult_t r_ = (x);                                                                \
+    if (r_ != ncclSuccess) throw ::wl::Error(WL_ENCCL, std::string(#x) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+template <class T>
+struct DArr {
+  T* p = nullptr;
+  size_t n = 0;
+  DArr() = default;
+  DArr(const DArr&) = delete;
+  DArr& operator=(const DArr&) = delete;
+  ~DArr() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t count) {
+    if (count <= n && p) return;
+    release();
+    if (count == 0) return;
+    WL_CUDA(cudaMalloc(&p, sizeof(T) * count));
+    n = count;
+  }
+};
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) WL_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace wl
+
+using wl::DArr;
+using wl::Error;
+
+struct wl_comm {
+  ncclComm_t nccl = nullptr;
+  int nranks = 1, rank = 0, device = 0;
+};
+
+struct TileSet {
+  int items = 0, num = 0;
+  DArr<int2> coords;
+  DArr<int32_t> carry_row;
+  DArr<double> carry_val;
+};
+
+struct wl_operator {
+  int device = 0;
+  wl_comm* comm = nullptr;
+  int nranks = 1, rank = 0;
+  int64_t n_global = 0, row_begin = 0, row_end = 0;
+  int32_t n_loc = 0, nnz_loc = 0;
+  DArr<int32_t> rowptr, col;
+  // halo plan (rows exchanged per SpMM; counts in rows)
+  int64_t n_halo = 0, n_send = 0;
+  std::vector<int64_t> send_cnt, send_displ, recv_cnt, recv_displ;
+  DArr<int32_t> send_idx;
+  // walk weights / parameters
+  int n_theta = 1;
+  std::vector<double> theta, mu;
+  DArr<double> mu_dev;
+  int fkind = WL_F_EXP;
+  double fparam = 1.0, c0 = 1.0;
+  std::vector<double> coeffs;
+  DArr<double> coeffs_dev;
+  wl_opts opts{};
+  DArr<double> tprime;  // n_loc x n_theta: t - c_0 (φ1 minus its identity term)
+  std::map<int, std::unique_ptr<TileSet>> tiles;
+  mutable std::mutex mtx;
+};
+
+struct wl_workspace {
+  const wl_operator* op = nullptr;
+  int max_b = 1, Bmax = 1, K = 30;
+  DArr<double> basis, S, Vb, halo_send, halo_recv;
+  DArr<double> partials, sums1, sums2, sums3;
+  DArr<unsigned int> ticket;
+  DArr<double> H, s_all, n0, comb, scratch;
+  DArr<int> keff, vcol, tcol;
+  DArr<double> colp;  // g0z, g1z, g0s, g1s (kMaxCols each)
+  // host-buffer entry point
+  DArr<double> hV, hLV;
+  // diffusion (outer Lanczos)
+  int kout_alloc = 0;
+  DArr<double> oQ, ow, oH, os, on0, osums1, osums2, osums3, otau, oY, oscratch;
+  DArr<int> okeff;
+};
+
+namespace wl {
+namespace {
+
+thread_local std::string g_last_error;
+
+wl_status fail(int code, const std::string& m) {
+  g_last_error = m;
+  return (wl_status)code;
+}
+
+template <class F>
+wl_status guarded(F&& f) {
+  try {
+    f();
+    return WL_OK;
+  } catch (const Error& e) {
+    return fail(e.code, e.what());
+  } catch (const std::bad_alloc&) {
+    return fail(WL_ENOMEM, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(WL_EINVAL, e.what());
+  }
+}
+
+inline cudaStream_t S_(wl_stream s) { return reinterpret_cast<cudaStream_t>(s); }
+inline bool multi(const wl_operator* op) { return op->comm && op->comm->nranks > 1; }
+
+void allreduce(const wl_operator* op, double* buf, size_t count, cudaStream_t s) {
+  if (!multi(op)) return;
+  WL_NCCL(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, op->comm->nccl, s));
+}
+
+// Rows of `src` (n_loc x B, ld lds) that other ranks reference are packed and exchanged into
+// ws->halo_recv (n_halo x B), ordered by owner rank then global id.
+void halo_exchange(const wl_operator* op, wl_workspace* ws, const double* src, int64_t lds, int B,
+                   cudaStream_t s) {
+  if (!multi(op)) return;
+  pack_rows(src, lds, op->send_idx.p, op->n_send, B, ws->halo_send.p, s);
+  WL_NCCL(ncclGroupStart());
+  for (int p = 0; p < op->nranks; ++p) {
+    if (p == op->rank) continue;
+    if (op->send_cnt[p] > 0)
+      WL_NCCL(ncclSend(ws->halo_send.p + op->send_displ[p] * B, (size_t)(op->send_cnt[p] * B), ncclDouble,
+                       p, op->comm->nccl, s));
+    if (op->recv_cnt[p] > 0)
+      WL_NCCL(ncclRecv(ws->halo_recv.p + op->recv_displ[p] * B, (size_t)(op->recv_cnt[p] * B), ncclDouble,
+                       p, op->comm->nccl, s));
+  }
+  WL_NCCL(ncclGroupEnd());
+}
+
+TileSet& tiles_for(const wl_operator* op, int B, cudaStream_t s) {
+  const int T = spmv_tile_items(B);
+  std::lock_guard<std::mutex> lk(op->mtx);
+  auto& m = const_cast<wl_operator*>(op)->tiles;
+  auto it = m.find(T);
+  if (it != m.end()) return *it->second;
+  auto ts = std::make_unique<TileSet>();
+  ts->items = T;
+  const int64_t items = (int64_t)op->n_loc + op->nnz_loc;
+  ts->num = (int)std::max<int64_t>(1, (items + T - 1) / T);
+  ts->coords.alloc(ts->num + 1);
+  ts->carry_row.alloc(ts->num);
+  ts->carry_val.alloc((size_t)ts->num * kMaxCols);
+  spmv_tiles(op->rowptr.p, op->n_loc, op->nnz_loc, T, ts->coords.p, ts->num, s);
+  auto& ref = *ts;
+  m.emplace(T, std::move(ts));
+  return ref;
+}
+
+void do_spmv(const wl_operator* op, wl_workspace* ws, const double* y, const double* x,
+             const double* g0, const double* g1, const double* scale, double* out, int B,
+             cudaStream_t s) {
+  TileSet& ts = tiles_for(op, B, s);
+  SpmvArgs a{};
+  a.rowptr = op->rowptr.p;
+  a.col = op->col.p;
+  a.tiles = ts.coords.p;
+  a.num_tiles = ts.num;
+  a.tile_items = ts.items;
+  a.n_loc = op->n_loc;
+  a.y = y;
+  a.ldy = B;
+  a.yh = ws->halo_recv.p;
+  a.ldh = B;
+  a.x = x;
+  a.ldx = B;
+  a.out = out;
+  a.ldo = B;
+  a.g0 = g0;
+  a.g1 = g1;
+  a.scale = scale;
+  a.B = B;
+  a.carry_row = ts.carry_row.p;
+  a.carry_val = ts.carry_val.p;
+  spmv(a, s);
+}
+
+// One Krylov action on global output columns [gstart, gstart + B) of the n_theta*b block;
+// `out` points at column gstart.  mode: 0 = φV, 1 = 𝕃V, 2 = t' (V = ones).
+void run_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double* V, int64_t ldv, int b,
+               int gstart, int B, double* out, int64_t ldo, cudaStream_t s) {
+  const int64_t n = op->n_loc;
+  const int K = ws->K;
+  const int64_t L = 2 * n;
+  const int64_t vstride = L * B;
+  double* g0z = ws->colp.p;
+  double* g1z = g0z + kMaxCols;
+  double* g0s = g1z + kMaxCols;
+  double* g1s = g0s + kMaxCols;
+  setup_chunk(op->mu_dev.p, gstart, b, B, g0z, g1z, g0s, g1s, ws->vcol.p, ws->tcol.p, s);
+  batch_inputs(V, ldv, B, n, ws->Vb.p, ws->vcol.p, s);
+  double* Q0 = ws->basis.p;
+  // a3: seeds q_1 v = A v (top) and q_2 v = A(Av) - μ d⊙v (bottom)   (eq:qrec seeds)
+  halo_exchange(op, ws, ws->Vb.p, B, B, s);
+  do_spmv(op, ws, ws->Vb.p, nullptr, nullptr, nullptr, nullptr, Q0, B, s);
+  halo_exchange(op, ws, Q0, B, B, s);
+  do_spmv(op, ws, Q0, ws->Vb.p, g0s, g1s, nullptr, Q0 + n * B, B, s);
+  const int grid = gram_grid(L * B, B);
+  GramArgs g{};
+  g.Q = ws->basis.p;
+  g.vstride = vstride;
+  g.len = L;
+  g.B = B;
+  g.s = ws->s_all.p;
+  g.partials = ws->partials.p;
+  g.ticket = ws->ticket.p;
+  g.grid = grid;
+  // ||u||
+  g.nvec = 0;
+  g.wa = Q0;
+  g.wscale = nullptr;
+  g.split = L;
+  g.wb = nullptr;
+  g.sums_out = ws->sums1.p;
+  gram_proj(g, s);
+  allreduce(op, ws->sums1.p, B, s);
+  finalize_norm0(ws->sums1.p, B, ws->n0.p, ws->s_all.p, ws->keff.p, K, s);
+  const double btol = op->opts.breakdown_tol;
+  const int reorth = op->opts.reorth;
+  for (int j = 0; j < K; ++j) {
+    double* Qj = ws->basis.p + (int64_t)j * vstride;
+    double* Qn = ws->basis.p + (int64_t)(j + 1) * vstride;
+    // a4: S = s_j (A Qj_bot + μ(μ - d) Qj_top) — bottom half of Z q_j; the top half is q_j,bot
+    halo_exchange(op, ws, Qj + n * B, B, B, s);
+    do_spmv(op, ws, Qj + n * B, Qj, g0z, g1z, ws->s_all.p + (int64_t)j * B, ws->S.p, B, s);
+    // a5: classical Gram-Schmidt (twice)
+    GramArgs w = g;
+    w.nvec = j + 1;
+    w.wa = Qj + n * B;
+    w.wscale = ws->s_all.p + (int64_t)j * B;
+    w.split = n;
+    w.wb = ws->S.p;
+    w.sums_out = ws->sums1.p;
+    gram_proj(w, s);
+    allreduce(op, ws->sums1.p, (size_t)(j + 2) * B, s);
+    if (reorth) {
+      GramArgs u = w;
+      u.wout = Qn;
+      u.sums_in = ws->sums1.p;
+      u.sums_out = ws->sums2.p;
+      if (j + 1 <= 32) {
+        gram_update_proj(u, s);
+      } else {  // unfused fallback for long bases: update, then project
+        u.sums_out = ws->sums3.p;
+        gram_update_norm(u, s);
+        GramArgs p2 = g;
+        p2.nvec = j + 1;
+        p2.wa = Qn;
+        p2.split = L;
+        p2.wscale = nullptr;
+        p2.sums_out = ws->sums2.p;
+        gram_proj(p2, s);
+      }
+      allreduce(op, ws->sums2.p, (size_t)(j + 1) * B, s);
+      GramArgs v = g;
+      v.nvec = j + 1;
+      v.wa = Qn;
+      v.wscale = nullptr;
+      v.split = L;
+      v.wout = Qn;
+      v.sums_in = ws->sums2.p;
+      v.sums_out = ws->sums3.p;
+      gram_update_norm(v, s);
+    } else {
+      GramArgs v = w;
+      v.wout = Qn;
+      v.sums_in = ws->sums1.p;
+      v.sums_out = ws->sums3.p;
+      gram_update_norm(v, s);
+    }
+    allreduce(op, ws->sums3.p, B, s);
+    finalize_step(ws->sums1.p, ws->sums2.p, ws->sums3.p, j, B, K, btol, reorth, ws->s_all.p, ws->H.p,
+                  ws->keff.p, s);
+  }
+  // a6: y = f_1(H_k) e_1 per column; comb_i = ||u|| y_i s_i
+  SmallFArgs f{};
+  f.H = ws->H.p;
+  f.K = K;
+  f.keff = ws->keff.p;
+  f.kind = op->fkind;
+  f.param = op->fparam;
+  f.coeffs = op->coeffs_dev.p;
+  f.ncoeffs = (int)op->coeffs.size();
+  f.n0 = ws->n0.p;
+  f.s = ws->s_all.p;
+  f.comb = ws->comb.p;
+  f.scratch = ws->scratch.p;
+  f.B = B;
+  small_f(f, s);
+  // a7: combine (top halves of the basis)
+  combine(mode, ws->basis.p, vstride, K, n, B, ws->comb.p, V, ldv, ws->vcol.p, op->c0,
+          op->tprime.p, op->n_theta, ws->tcol.p, out, ldo, s);
+}
+
+void run_action(const wl_operator* op, wl_workspace* ws, int mode, const double* V, int64_t ldv, int b,
+                double* out, int64_t ldo, cudaStream_t s) {
+  const int G = op->n_theta * b;
+  for (int g0 = 0; g0 < G; g0 += ws->Bmax) {
+    const int B = std::min(ws->Bmax, G - g0);
+    run_chunk(op, ws, mode, V, ldv, b, g0, B, out + g0, ldo, s);
+  }
+}
+
+void workspace_alloc(wl_workspace* ws, const wl_operator* op, int max_b) {
+  ws->op = op;
+  ws->max_b = max_b;
+  ws->K = op->opts.krylov_dim;
+  ws->Bmax = std::max(1, std::min({op->opts.max_cols, kMaxCols, op->n_theta * max_b}));
+  const int64_t n = op->n_loc;
+  const int B = ws->Bmax, K = ws->K;
+  ws->basis.alloc((size_t)(K + 1) * 2 * n * B);
+  ws->S.alloc((size_t)n * B);
+  ws->Vb.alloc((size_t)n * B);
+  if (op->n_halo > 0) ws->halo_recv.alloc((size_t)op->n_halo * B);
+  if (op->n_send > 0) ws->halo_send.alloc((size_t)op->n_send * B);
+  const int grid = gram_grid(2 * n * B, B);
+  ws->partials.alloc((size_t)grid * (K + 2) * B);
+  ws->sums1.alloc((size_t)(K + 2) * B);
+  ws->sums2.alloc((size_t)(K + 2) * B);
+  ws->sums3.alloc((size_t)(K + 2) * B);
+  ws->ticket.alloc(1);
+  WL_CUDA(cudaMemset(ws->ticket.p, 0, sizeof(unsigned int)));
+  ws->H.alloc((size_t)B * (K + 1) * K);
+  WL_CUDA(cudaMemset(ws->H.p, 0, sizeof(double) * B * (K + 1) * K));
+  ws->s_all.alloc((size_t)(K + 1) * B);
+  ws->n0.alloc(B);
+  ws->comb.alloc((size_t)(K + 1) * B);
+  ws->scratch.alloc((size_t)B * 9 * kMaxSmallN * kMaxSmallN);
+  ws->keff.alloc(B);
+  ws->vcol.alloc(kMaxCols);
+  ws->tcol.alloc(kMaxCols);
+  ws->colp.alloc(4 * kMaxCols);
+  WL_CUDA(cudaDeviceSynchronize());
+}
+
+// Collective exchange of small host int64 vectors through NCCL (device staging).
+void nccl_alltoall_counts(wl_comm* c, const std::vector<int64_t>& send, std::vector<int64_t>& recv,
+                          cudaStream_t s) {
+  const int P = c->nranks;
+  DArr<int64_t> ds, dr;
+  ds.alloc(P);
+  dr.alloc(P);
+  WL_CUDA(cudaMemcpy(ds.p, send.data(), sizeof(int64_t) * P, cudaMemcpyHostToDevice));
+  WL_NCCL(ncclGroupStart());
+  for (int p = 0; p < P; ++p) {
+    WL_NCCL(ncclSend(ds.p + p, 1, ncclInt64, p, c->nccl, s));
+    WL_NCCL(ncclRecv(dr.p + p, 1, ncclInt64, p, c->nccl, s));
+  }
+  WL_NCCL(ncclGroupEnd());
+  WL_CUDA(cudaStreamSynchronize(s));
+  recv.resize(P);
+  WL_CUDA(cudaMemcpy(recv.data(), dr.p, sizeof(int64_t) * P, cudaMemcpyDeviceToHost));
+}
+
+void build_operator(wl_operator* op, const int64_t* rp_in, const int32_t* ci_in, cudaStream_t s) {
+  const int64_t n = op->n_loc;
+  const int64_t base = rp_in[0];
+  const int64_t nnz = rp_in[n] - base;
+  if (nnz < 0) throw Error(WL_EGRAPH, "row_ptr decreases");
+  if (nnz >= INT32_MAX || n >= INT32_MAX) throw Error(WL_EUNSUPPORTED, "local nnz or rows >= 2^31");
+  op->nnz_loc = (int32_t)nnz;
+  std::vector<int32_t> rp((size_t)n + 1);
+  for (int64_t i = 0; i <= n; ++i) {
+    const int64_t v = rp_in[i] - base;
+    if (v < 0 || v > nnz || (i > 0 && v < rp[i - 1])) throw Error(WL_EGRAPH, "row_ptr not nondecreasing");
+    rp[i] = (int32_t)v;
+  }
+  // gather all ranks' row ranges
+  std::vector<int64_t> bounds(op->nranks + 1, 0);
+  if (multi(op)) {
+    DArr<int64_t> d;
+    d.alloc(2 * op->nranks);
+    int64_t mine[2] = {op->row_begin, op->row_end};
+    WL_CUDA(cudaMemcpy(d.p + 2 * op->rank, mine, sizeof(mine), cudaMemcpyHostToDevice));
+    WL_NCCL(ncclAllGather(d.p + 2 * op->rank, d.p, 2, ncclInt64, op->comm->nccl, s));
+    WL_CUDA(cudaStreamSynchronize(s));
+    std::vector<int64_t> h(2 * op->nranks);
+    WL_CUDA(cudaMemcpy(h.data(), d.p, sizeof(int64_t) * h.size(), cudaMemcpyDeviceToHost));
+    for (int p = 0; p < op->nranks; ++p) {
+      if (h[2 * p] != (p == 0 ? 0 : h[2 * p - 1])) throw Error(WL_EINVAL, "row ranges not contiguous by rank");
+      bounds[p] = h[2 * p];
+      bounds[p + 1] = h[2 * p + 1];
+    }
+    if (bounds[op->nranks] != op->n_global) throw Error(WL_EINVAL, "row ranges do not cover n_global");
+  } else {
+    bounds[0] = 0;
+    bounds[1] = op->n_global;
+  }
+  // validate columns and collect remote ids
+  std::vector<int64_t> remote;
+  for (int64_t r = 0; r < n; ++r) {
+    const int64_t grow = op->row_begin + r;
+    for (int64_t z = rp[r]; z < rp[r + 1]; ++z) {
+      const int64_t cg = ci_in[z];
+      if (cg < 0 || cg >= op->n_global) throw Error(WL_EGRAPH, "column id out of range");
+      if (cg == grow) throw Error(WL_EGRAPH, "self loop (graphs must be simple, P:76)");
+      if (z > rp[r] && cg <= ci_in[z - 1]) throw Error(WL_EGRAPH, "columns not strictly increasing in a row");
+      if (cg < op->row_begin || cg >= op->row_end) remote.push_back(cg);
+    }
+  }
+  std::sort(remote.begin(), remote.end());
+  remote.erase(std::unique(remote.begin(), remote.end()), remote.end());
+  op->n_halo = (int64_t)remote.size();
+  std::vector<int32_t> col((size_t)nnz);
+  for (int64_t z = 0; z < nnz; ++z) {
+    const int64_t cg = ci_in[z];
+    if (cg >= op->row_begin && cg < op->row_end) col[z] = (int32_t)(cg - op->row_begin);
+    else col[z] = (int32_t)(n + (std::lower_bound(remote.begin(), remote.end(), cg) - remote.begin()));
+  }
+  op->rowptr.alloc(n + 1);
+  op->col.alloc(std::max<int64_t>(nnz, 1));
+  WL_CUDA(cudaMemcpy(op->rowptr.p, rp.data(), sizeof(int32_t) * (n + 1), cudaMemcpyHostToDevice));
+  if (nnz) WL_CUDA(cudaMemcpy(op->col.p, col.data(), sizeof(int32_t) * nnz, cudaMemcpyHostToDevice));
+  // halo plan: how many rows I need from each owner, then the ids (owners pack them)
+  const int P = op->nranks;
+  op->recv_cnt.assign(P, 0);
+  op->recv_displ.assign(P, 0);
+  op->send_cnt.assign(P, 0);
+  op->send_displ.assign(P, 0);
+  if (multi(op)) {
+    for (int64_t id : remote) {
+      const int owner = (int)(std::upper_bound(bounds.begin(), bounds.end(), id) - bounds.begin()) - 1;
+      op->recv_cnt[owner]++;
+    }
+    for (int p = 1; p < P; ++p) op->recv_displ[p] = op->recv_displ[p - 1] + op->recv_cnt[p - 1];
+    nccl_alltoall_counts(op->comm, op->recv_cnt, op->send_cnt, s);
+    for (int p = 1; p < P; ++p) op->send_displ[p] = op->send_displ[p - 1] + op->send_cnt[p - 1];
+    op->n_send = op->send_displ[P - 1] + op->send_cnt[P - 1];
+    DArr<int64_t> need, give;
+    need.alloc(std::max<int64_t>(1, op->n_halo));
+    give.alloc(std::max<int64_t>(1, op->n_send));
+    if (op->n_halo)
+      WL_CUDA(cudaMemcpy(need.p, remote.data(), sizeof(int64_t) * op->n_halo, cudaMemcpyHostToDevice));
+    WL_NCCL(ncclGroupStart());
+    for (int p = 0; p < P; ++p) {
+      if (op->recv_cnt[p]) WL_NCCL(ncclSend(need.p + op->recv_displ[p], op->recv_cnt[p], ncclInt64, p, op->comm->nccl, s));
+      if (op->send_cnt[p]) WL_NCCL(ncclRecv(give.p + op->send_displ[p], op->send_cnt[p], ncclInt64, p, op->comm->nccl, s));
+    }
+    WL_NCCL(ncclGroupEnd());
+    WL_CUDA(cudaStreamSynchronize(s));
+    std::vector<int64_t> g((size_t)op->n_send);
+    if (op->n_send) WL_CUDA(cudaMemcpy(g.data(), give.p, sizeof(int64_t) * op->n_send, cudaMemcpyDeviceToHost));
+    std::vector<int32_t> idx((size_t)op->n_send);
+    for (int64_t k = 0; k < op->n_send; ++k) {
+      if (g[k] < op->row_begin || g[k] >= op->row_end) throw Error(WL_EGRAPH, "halo request for a row not owned");
+      idx[k] = (int32_t)(g[k] - op->row_begin);
+    }
+    op->send_idx.alloc(std::max<int64_t>(1, op->n_send));
+    if (op->n_send) WL_CUDA(cudaMemcpy(op->send_idx.p, idx.data(), sizeof(int32_t) * op->n_send, cudaMemcpyHostToDevice));
+  } else if (op->n_halo) {
+    throw Error(WL_EGRAPH, "column outside [row_begin,row_end) without a communicator");
+  }
+}
+
+void check_block(const void* p, int64_t ld, int64_t cols, const char* what) {
+  if (!p) throw Error(WL_EINVAL, std::string(what) + " is NULL");
+  if (ld < cols) throw Error(WL_EINVAL, std::string(what) + ": leading dimension < columns");
+}
+
+}  // namespace
+}  // namespace wl
+
+using namespace wl;
+
+extern "C" {
+
+const char* wl_last_error(void) { return g_last_error.c_str(); }
+const char* wl_version(void) { return "walklap-b200 0.1 (sm_100a)"; }
+int64_t wl_launch_count(void) { return g_launches.load(); }
+
+void wl_opts_default(wl_opts* o) {
+  if (!o) return;
+  o->krylov_dim = 30;
+  o->reorth = 1;
+  o->max_cols = 32;
+  o->breakdown_tol = 1e-12;
+  o->rho_bound = 0.0;
+}
+
+wl_status wl_nccl_unique_id(void* out128) {
+  return guarded([&] {
+    if (!out128) throw Error(WL_EINVAL, "out128 is NULL");
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId id;
+    WL_NCCL(ncclGetUniqueId(&id));
+    std::memcpy(out128, &id, 128);
+  });
+}
+
+wl_status wl_comm_create(int32_t nranks, int32_t rank, const void* id128, int32_t device, wl_comm** out) {
+  return guarded([&] {
+    if (!out || !id128 || nranks < 1 || rank < 0 || rank >= nranks) throw Error(WL_EINVAL, "bad comm args");
+    WL_CUDA(cudaSetDevice(device));
+    auto c = std::make_unique<wl_comm>();
+    c->nranks = nranks;
+    c->rank = rank;
+    c->device = device;
+    ncclUniqueId id;
+    std::memcpy(&id, id128, 128);
+    WL_NCCL(ncclCommInitRank(&c->nccl, nranks, id, rank));
+    *out = c.release();
+  });
+}
+
+void wl_comm_destroy(wl_comm* c) {
+  if (!c) return;
+  if (c->nccl) ncclCommDestroy(c->nccl);
+  delete c;
+}
+
+wl_status wl_partition(int64_t n, const int64_t* row_ptr, int32_t nranks, int64_t* bounds) {
+  return guarded([&] {
+    if (n < 0 || !row_ptr || !bounds || nranks < 1) throw Error(WL_EINVAL, "bad partition args");
+    const int64_t nnz = row_ptr[n] - row_ptr[0];
+    bounds[0] = 0;
+    for (int p = 1; p < nranks; ++p) {
+      const int64_t target = row_ptr[0] + (p * nnz + nranks - 1) / nranks;  // ceil(p nnz / P)
+      int64_t r = std::lower_bound(row_ptr, row_ptr + n + 1, target) - row_ptr;
+      r = std::min(std::max(r, bounds[p - 1]), n);
+      bounds[p] = r;
+    }
+    bounds[nranks] = n;
+  });
+}
+
+wl_status wl_operator_create(wl_comm* comm, int64_t n_global, int64_t row_begin, int64_t row_end,
+                             const int64_t* row_ptr_local, const int32_t* col_idx_local, int32_t variant,
+                             int32_t n_theta, const double* thetas, const wl_walkfun* f,
+                             const wl_opts* opts, wl_stream stream, wl_operator** out) {
+  return guarded([&] {
+    if (!out || !row_ptr_local || !f) throw Error(WL_EINVAL, "NULL argument");
+    if (n_global < 1 || row_begin < 0 || row_end < row_begin || row_end > n_global)
+      throw Error(WL_EINVAL, "bad row range");
+    if (row_ptr_local[row_end - row_begin] > row_ptr_local[0] && !col_idx_local)
+      throw Error(WL_EINVAL, "col_idx is NULL");
+    auto op = std::make_unique<wl_operator>();
+    op->comm = comm;
+    if (comm) {
+      op->nranks = comm->nranks;
+      op->rank = comm->rank;
+      op->device = comm->device;
+    } else {
+      WL_CUDA(cudaGetDevice(&op->device));
+      if (row_begin != 0 || row_end != n_global) throw Error(WL_EINVAL, "single GPU operator must own all rows");
+    }
+    DeviceGuard dg(op->device);
+    op->n_global = n_global;
+    op->row_begin = row_begin;
+    op->row_end = row_end;
+    op->n_loc = (int32_t)(row_end - row_begin);
+    if (opts) op->opts = *opts;
+    else wl_opts_default(&op->opts);
+    if (op->opts.krylov_dim < 1 || op->opts.krylov_dim > kMaxKrylov) throw Error(WL_EINVAL, "krylov_dim must be in [1, 64]");
+    if (op->opts.max_cols < 1 || op->opts.max_cols > kMaxCols) throw Error(WL_EINVAL, "max_cols must be in [1, 32]");
+    if (!(op->opts.breakdown_tol >= 0.0)) throw Error(WL_EINVAL, "breakdown_tol < 0");
+    // θ values (θ = 1 - μ)
+    if (variant == WL_WALK || variant == WL_NBT) {
+      if (n_theta != 1) throw Error(WL_EINVAL, "WL_WALK/WL_NBT take exactly one θ");
+      op->theta = {variant == WL_WALK ? 1.0 : 0.0};
+    } else if (variant == WL_BTDW) {
+      if (n_theta < 1 || n_theta > kMaxCols || !thetas) throw Error(WL_EINVAL, "n_theta must be in [1, 32]");
+      for (int i = 0; i < n_theta; ++i) {
+        if (!(thetas[i] >= 0.0 && thetas[i] <= 1.0)) throw Error(WL_EINVAL, "θ must be in [0, 1]");
+        op->theta.push_back(thetas[i]);
+      }
+    } else {
+      throw Error(WL_EINVAL, "unknown variant");
+    }
+    op->n_theta = (int)op->theta.size();
+    for (double t : op->theta) op->mu.push_back(1.0 - t);
+    // walk weights
+    op->fkind = f->kind;
+    op->fparam = f->param;
+    if (f->kind == WL_F_EXP) {
+      op->c0 = 1.0;
+    } else if (f->kind == WL_F_RESOLVENT) {
+      op->c0 = 1.0;
+      if (op->opts.rho_bound > 0.0 && std::fabs(f->param) * op->opts.rho_bound >= 1.0)
+        throw Error(WL_EDIVERGE, "resolvent: α ρ >= 1, series diverges (Prop. pro:whe-we-converge)");
+    } else if (f->kind == WL_F_SERIES) {
+      if (!f->coeffs || f->ncoeffs < 1 || f->ncoeffs > 64) throw Error(WL_EINVAL, "series needs 1..64 coefficients");
+      op->coeffs.assign(f->coeffs, f->coeffs + f->ncoeffs);
+      op->c0 = op->coeffs[0];
+    } else {
+      throw Error(WL_EINVAL, "unknown walk-function kind");
+    }
+    cudaStream_t s = S_(stream);
+    op->mu_dev.alloc(op->n_theta);
+    WL_CUDA(cudaMemcpy(op->mu_dev.p, op->mu.data(), sizeof(double) * op->n_theta, cudaMemcpyHostToDevice));
+    if (!op->coeffs.empty()) {
+      op->coeffs_dev.alloc(op->coeffs.size());
+      WL_CUDA(cudaMemcpy(op->coeffs_dev.p, op->coeffs.data(), sizeof(double) * op->coeffs.size(),
+                         cudaMemcpyHostToDevice));
+    }
+    build_operator(op.get(), row_ptr_local, col_idx_local, s);
+    // a8: t' = φ_θ 1 - c_0 1 for every θ (one batched Krylov action on V = 1)
+    op->tprime.alloc((size_t)std::max<int64_t>(1, op->n_loc) * op->n_theta);
+    {
+      wl_workspace ws;
+      workspace_alloc(&ws, op.get(), 1);
+      run_action(op.get(), &ws, 2, nullptr, 1, 1, op->tprime.p, op->n_theta, s);
+      WL_CUDA(cudaStreamSynchronize(s));
+    }
+    *out = op.release();
+  });
+}
+
+void wl_operator_destroy(wl_operator* op) {
+  if (!op) return;
+  DeviceGuard dg(op->device);
+  WL_CUDA(cudaDeviceSynchronize());
+  delete op;
+}
+
+wl_status wl_operator_info(const wl_operator* op, int64_t* n_local, int64_t* nnz_local, int64_t* n_halo,
+                           int32_t* n_theta) {
+  return guarded([&] {
+    if (!op) throw Error(WL_EINVAL, "op is NULL");
+    if (n_local) *n_local = op->n_loc;
+    if (nnz_local) *nnz_local = op->nnz_loc;
+    if (n_halo) *n_halo = op->n_halo;
+    if (n_theta) *n_theta = op->n_theta;
+  });
+}
+
+wl_status wl_operator_diag_shift(const wl_operator* op, double* t_dev, int64_t ldt, wl_stream stream) {
+  return guarded([&] {
+    if (!op) throw Error(WL_EINVAL, "op is NULL");
+    check_block(t_dev, ldt, op->n_theta, "t_dev");
+    DeviceGuard dg(op->device);
+    // t = t' + c_0
+    const int nt = op->n_theta;
+    std::vector<double> host((size_t)op->n_loc * nt);
+    WL_CUDA(cudaMemcpyAsync(host.data(), op->tprime.p, sizeof(double) * host.size(), cudaMemcpyDeviceToHost, S_(stream)));
+    WL_CUDA(cudaStreamSynchronize(S_(stream)));
+    for (auto& v : host) v += op->c0;
+    WL_CUDA(cudaMemcpy2DAsync(t_dev, sizeof(double) * ldt, host.data(), sizeof(double) * nt, sizeof(double) * nt,
+                              op->n_loc, cudaMemcpyHostToDevice, S_(stream)));
+    WL_CUDA(cudaStreamSynchronize(S_(stream)));
+  });
+}
+
+wl_status wl_workspace_create(const wl_operator* op, int32_t max_b, wl_workspace** out) {
+  return guarded([&] {
+    if (!op || !out || max_b < 1) throw Error(WL_EINVAL, "bad workspace args");
+    DeviceGuard dg(op->device);
+    auto ws = std::make_unique<wl_workspace>();
+    workspace_alloc(ws.get(), op, max_b);
+    *out = ws.release();
+  });
+}
+
+void wl_workspace_destroy(wl_workspace* ws) {
+  if (!ws) return;
+  DeviceGuard dg(ws->op->device);
+  cudaDeviceSynchronize();
+  delete ws;
+}
+
+static wl_status apply_common(int mode, const wl_operator* op, int32_t b, const double* V, int64_t ldv, double* LV,
+                              int64_t ldlv, wl_workspace* ws, wl_stream stream) {
+  return guarded([&] {
+    if (!op || !ws || ws->op != op) throw Error(WL_EINVAL, "operator/workspace mismatch");
+    if (b < 1 || b > ws->max_b) throw Error(WL_EINVAL, "b out of [1, max_b]");
+    if (op->n_loc > 0) {
+      check_block(V, ldv, b, "V");
+      check_block(LV, ldlv, (int64_t)op->n_theta * b, "LV");
+    }
+    DeviceGuard dg(op->device);
+    run_action(op, ws, mode, V, ldv, b, LV, ldlv, S_(stream));
+  });
+}
+
+wl_status wl_apply(const wl_operator* op, int32_t b, const double* V, int64_t ldv, double* LV, int64_t ldlv,
+                   wl_workspace* ws, wl_stream stream) {
+  return apply_common(1, op, b, V, ldv, LV, ldlv, ws, stream);
+}
+
+wl_status wl_phi_apply(const wl_operator* op, int32_t b, const double* V, int64_t ldv, double* LV, int64_t ldlv,
+                       wl_workspace* ws, wl_stream stream) {
+  return apply_common(0, op, b, V, ldv, LV, ldlv, ws, stream);
+}
+
+wl_status wl_apply_host(const wl_operator* op, int32_t b, const double* Vh, int64_t ldv, double* LVh,
+                        int64_t ldlv, wl_workspace* ws, wl_stream stream) {
+  return guarded([&] {
+    if (!op || !ws || ws->op != op) throw Error(WL_EINVAL, "operator/workspace mismatch");
+    if (b < 1 || b > ws->max_b) throw Error(WL_EINVAL, "b out of [1, max_b]");
+    const int64_t n = op->n_loc;
+    const int64_t G = (int64_t)op->n_theta * b;
+    check_block(Vh, ldv, b, "V_host");
+    check_block(LVh, ldlv, G, "LV_host");
+    DeviceGuard dg(op->device);
+    cudaStream_t s = S_(stream);
+    ws->hV.alloc((size_t)std::max<int64_t>(1, n * b));
+    ws->hLV.alloc((size_t)std::max<int64_t>(1, n * G));
+    WL_CUDA(cudaMemcpy2DAsync(ws->hV.p, sizeof(double) * b, Vh, sizeof(double) * ldv, sizeof(double) * b, n,
+                              cudaMemcpyHostToDevice, s));
+    run_action(op, ws, 1, ws->hV.p, b, b, ws->hLV.p, G, s);
+    WL_CUDA(cudaMemcpy2DAsync(LVh, sizeof(double) * ldlv, ws->hLV.p, sizeof(double) * G, sizeof(double) * G, n,
+                              cudaMemcpyDeviceToHost, s));
+    WL_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+wl_status wl_diffuse(const wl_operator* op, int32_t theta_index, int32_t nt, const double* tau, const double* x0,
+                     double* X, int64_t ldx, int32_t k_out, wl_workspace* ws, wl_stream stream) {
+  return guarded([&] {
+    if (!op || !ws || ws->op != op) throw Error(WL_EINVAL, "operator/workspace mismatch");
+    if (theta_index < 0 || theta_index >= op->n_theta) throw Error(WL_EINVAL, "theta_index out of range");
+    if (nt < 1 || !tau) throw Error(WL_EINVAL, "need nt >= 1 times");
+    if (k_out < 2 || k_out > 128) throw Error(WL_EINVAL, "k_out must be in [2, 128]");
+    for (int i = 0; i < nt; ++i)
+      if (!(tau[i] >= 0.0)) throw Error(WL_EINVAL, "times must be >= 0");
+    if (op->n_loc > 0) {
+      check_block(x0, 1, 1, "x0");
+      check_block(X, ldx, nt, "X");
+    }
+    DeviceGuard dg(op->device);
+    cudaStream_t s = S_(stream);
+    const int64_t n = op->n_loc;
+    const int m = k_out;
+    if (ws->kout_alloc < m || ws->otau.n < (size_t)nt) {
+      ws->oQ.alloc((size_t)(m + 1) * std::max<int64_t>(1, n));
+      ws->ow.alloc((size_t)std::max<int64_t>(1, n));
+      ws->oH.alloc((size_t)(m + 1) * m);
+      ws->os.alloc(m + 1);
+      ws->on0.alloc(1);
+      ws->okeff.alloc(1);
+      ws->osums1.alloc(m + 2);
+      ws->osums2.alloc(m + 2);
+      ws->osums3.alloc(m + 2);
+      ws->otau.alloc(nt);
+      ws->oY.alloc((size_t)nt * (m + 1));
+      ws->oscratch.alloc((size_t)nt * 9 * kMaxSmallN * kMaxSmallN);
+      ws->kout_alloc = m;
+      if (ws->partials.n < (size_t)gram_grid(n, 1) * (m + 2))
+        ws->partials.alloc((size_t)gram_grid(n, 1) * (m + 2));
+    }
+    WL_CUDA(cudaMemsetAsync(ws->oH.p, 0, sizeof(double) * (m + 1) * m, s));
+    WL_CUDA(cudaMemcpyAsync(ws->otau.p, tau, sizeof(double) * nt, cudaMemcpyHostToDevice, s));
+    // outer Arnoldi (= Lanczos with full reorthogonalisation: 𝕃 symmetric, Prop. pro:still-again-an-mmatrix)
+    GramArgs g{};
+    g.Q = ws->oQ.p;
+    g.vstride = n;
+    g.len = n;
+    g.B = 1;
+    g.s = ws->os.p;
+    g.partials = ws->partials.p;
+    g.ticket = ws->ticket.p;
+    g.grid = gram_grid(n, 1);
+    WL_CUDA(cudaMemcpyAsync(ws->oQ.p, x0, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    g.nvec = 0;
+    g.wa = ws->oQ.p;
+    g.split = n;
+    g.sums_out = ws->osums1.p;
+    gram_proj(g, s);
+    allreduce(op, ws->osums1.p, 1, s);
+    finalize_norm0(ws->osums1.p, 1, ws->on0.p, ws->os.p, ws->okeff.p, m, s);
+    for (int j = 0; j < m; ++j) {
+      double* Pj = ws->oQ.p + (int64_t)j * n;
+      double* Pn = ws->oQ.p + (int64_t)(j + 1) * n;
+      // inner action: ow = 𝕃 P̃_j (P̃_j unnormalised; q_j = s_j P̃_j)
+      run_chunk(op, ws, 1, Pj, 1, 1, theta_index, 1, ws->ow.p, 1, s);
+      GramArgs w = g;
+      w.nvec = j + 1;
+      w.wa = ws->ow.p;
+      w.wscale = ws->os.p + j;
+      w.split = n;
+      w.sums_out = ws->osums1.p;
+      gram_proj(w, s);
+      allreduce(op, ws->osums1.p, j + 2, s);
+      GramArgs u = w;
+      u.wout = Pn;
+      u.sums_in = ws->osums1.p;
+      u.sums_out = ws->osums2.p;
+      if (j + 1 <= 32) {
+        gram_update_proj(u, s);
+      } else {
+        u.sums_out = ws->osums3.p;
+        gram_update_norm(u, s);
+        GramArgs p2 = g;
+        p2.nvec = j + 1;
+        p2.wa = Pn;
+        p2.split = n;
+        p2.sums_out = ws->osums2.p;
+        gram_proj(p2, s);
+      }
+      allreduce(op, ws->osums2.p, j + 1, s);
+      GramArgs v = g;
+      v.nvec = j + 1;
+      v.wa = Pn;
+      v.split = n;
+      v.wout = Pn;
+      v.sums_in = ws->osums2.p;
+      v.sums_out = ws->osums3.p;
+      gram_update_norm(v, s);
+      allreduce(op, ws->osums3.p, 1, s);
+      finalize_step(ws->osums1.p, ws->osums2.p, ws->osums3.p, j, 1, m, op->opts.breakdown_tol, 1, ws->os.p,
+                    ws->oH.p, ws->okeff.p, s);
+    }
+    SmallFArgs f{};
+    f.H = ws->oH.p;
+    f.K = m;
+    f.keff = ws->okeff.p;
+    f.kind = 3;
+    f.n0 = ws->on0.p;
+    f.s = ws->os.p;
+    f.comb = ws->oY.p;
+    f.scratch = ws->oscratch.p;
+    f.B = 1;
+    f.tau = ws->otau.p;
+    f.nprob = nt;
+    small_f(f, s);
+    lanczos_combine(ws->oQ.p, n, m + 1, n, ws->oY.p, nt, 1.0, X, ldx, s);
+  });
+}
+
+wl_status wl_wait(const wl_operator* op, wl_stream stream) {
+  return guarded([&] {
+    if (!op) throw Error(WL_EINVAL, "op is NULL");
+    DeviceGuard dg(op->device);
+    WL_CUDA(cudaStreamSynchronize(S_(stream)));
+    WL_CUDA(cudaGetLastError());
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,117 @@
+// wl_internal.cuh — shared declarations of the walklap CUDA library (not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+namespace wl {
+
+// ---------------------------------------------------------------- errors / launch accounting
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+void cuda_check(cudaError_t e, const char* what, const char* file, int line);
+#define WL_CUDA(x) ::wl::cuda_check((x), #x, __FILE__, __LINE__)
+void note_launch(const char* name);  // increments the process-wide launch counter
+#define WL_LAUNCH(name) ::wl::note_launch(name)
+
+constexpr int kMaxCols = 32;    // columns per Krylov batch (B)
+constexpr int kMaxKrylov = 64;  // Arnoldi steps per action
+constexpr int kMaxSmallN = 130; // largest dense matrix of the projected-function kernels
+
+// ---------------------------------------------------------------- merge-path Z-SpMV
+// out[r][c] = scale[c] * ( Σ_{z in row r} y[col[z]][c] + (g0[c] + g1[c] * deg(r)) * x[r][c] )
+// Gathers y rows (ld ldy) for local columns < n_loc, halo rows (ld ldh) for columns >= n_loc.
+struct SpmvArgs {
+  const int32_t* rowptr;  // n_loc + 1, local offsets
+  const int32_t* col;     // nnz, local ids (halo ids >= n_loc)
+  const int2* tiles;      // num_tiles + 1 merge coordinates (row, nz)
+  int num_tiles;
+  int tile_items;
+  int32_t n_loc;
+  const double* y; int64_t ldy;
+  const double* yh; int64_t ldh;
+  const double* x; int64_t ldx;   // may be null (no diagonal term)
+  double* out; int64_t ldo;
+  const double* g0; const double* g1; const double* scale;  // device, B entries (scale may be null)
+  int B;
+  int32_t* carry_row;  // num_tiles
+  double* carry_val;   // num_tiles * B
+};
+int spmv_tile_items(int B);
+void spmv_tiles(const int32_t* rowptr, int32_t n, int32_t nnz, int tile_items, int2* tiles,
+                int num_tiles, cudaStream_t s);
+void spmv(const SpmvArgs& a, cudaStream_t s);
+
+// ---------------------------------------------------------------- Gram-Schmidt kernels
+// Basis: nvec vectors, vector i at Q + i*vstride, element e (column e % B) for e < len*B.
+// w(e) = e < split*B ? wscale[c] * wa[e] : wb[e - split*B]   ("two-source" vector).
+struct GramArgs {
+  const double* Q; int64_t vstride;
+  int nvec;
+  int64_t len;      // rows (L = 2 n_loc for Z vectors)
+  int B;
+  const double* s;  // per-vector column scales s[i*B + c] (basis stores unnormalised vectors)
+  const double* wa; const double* wscale; int64_t split;
+  const double* wb;
+  double* wout;     // written vector (update kernels)
+  const double* sums_in;   // previous reduction results ((nvec)*B): coefficients c_i = s_i^2 * sums_in_i
+  double* partials;        // per-CTA partial sums
+  double* sums_out;        // reduced sums (nvec+1)*B
+  unsigned int* ticket;
+  int grid;
+};
+void gram_proj(GramArgs a, cudaStream_t s);         // sums_out[i] = Σ Q_i w, sums_out[nvec] = Σ w²
+void gram_update_proj(GramArgs a, cudaStream_t s);  // wout = w - Σ c_i Q_i ; sums_out[i] = Σ Q_i wout
+void gram_update_norm(GramArgs a, cudaStream_t s);  // wout = w - Σ c_i Q_i ; sums_out[0] = Σ wout²
+int gram_grid(int64_t elems, int B);
+
+// ---------------------------------------------------------------- small dense functions
+// Per column c (problem), m = keff[c]: y_c = f_1(H_m) e_1 for the Arnoldi matrix H.
+// kind 3 (outer diffusion): problem p uses column 0's H and computes exp(-tau[p] H_m) e_1;
+// output comb[p*(K+1) + i] = n0 * y_i * s_i.
+struct SmallFArgs {
+  const double* H; int ldh_col;   // H of column c at H + c*(K+1)*K, entry (i,j) at [j*(K+1)+i]
+  int K;
+  const int* keff;
+  int kind; double param; const double* coeffs; int ncoeffs;
+  const double* n0;  // ||u|| per column
+  const double* s;   // basis scales s[i*B + c]
+  double* comb;      // out: comb[i*B + c] = n0 * y_i * s_i
+  double* scratch;   // per problem 9 * kMaxSmallN^2 doubles
+  int B;             // columns of H/s/n0 (problems for kinds 0-2)
+  const double* tau; // kind 3 only: nprob values
+  int nprob;         // kind 3 only
+};
+void small_f(const SmallFArgs& a, cudaStream_t s);
+
+// ---------------------------------------------------------------- elementwise / misc kernels
+// Vb[r*B + j] = V[r*ldv + vcol[j]]   (j < B); V null => ones
+void batch_inputs(const double* V, int64_t ldv, int B, int64_t n, double* Vb, const int* vcol,
+                  cudaStream_t s);
+void setup_chunk(const double* mu, int gstart, int b, int B, double* g0z, double* g1z, double* g0s,
+                 double* g1s, int* vcol, int* tcol, cudaStream_t s);
+// Arnoldi bookkeeping after a reduction: see engine.cu for the exact semantics.
+void finalize_norm0(const double* sums, int B, double* n0, double* s0, int* keff, int K,
+                    cudaStream_t s);
+void finalize_step(const double* sums1, const double* sums2, const double* sums3, int j, int B,
+                   int K, double btol, int reorth, double* s_all, double* H, int* keff,
+                   cudaStream_t s);
+// combine: mode 0 = φV (c0 V + Σ comb_i Q_i,top), 1 = 𝕃V (t'⊙V - Σ comb_i Q_i,top),
+//          2 = t' (Σ comb_i Q_i,top) for V = 1
+// V column of batch column c is vcol[c]; t' column is tcol[c].
+void combine(int mode, const double* Q, int64_t vstride, int nvec, int64_t n, int B,
+             const double* comb, const double* V, int64_t ldv, const int* vcol, double c0,
+             const double* tprime, int64_t ldt, const int* tcol, double* out, int64_t ldo,
+             cudaStream_t s);
+void pack_rows(const double* src, int64_t lds, const int32_t* idx, int64_t cnt, int B, double* dst,
+               cudaStream_t s);
+void fill(double* p, int64_t n, double v, cudaStream_t s);
+
+// outer Lanczos helpers (diffusion)
+void lanczos_combine(const double* Q, int64_t stride, int m, int64_t n, const double* Y, int nt,
+                     double scale, double* X, int64_t ldx, cudaStream_t s);
+
+}  // namespace wl

@@ -1,0 +1,300 @@
+"""ctypes binding of libwalklap.so (include/walklap.h).  Argument marshalling only.
+
+Every numerical step runs in the library's CUDA kernels; this module converts torch CUDA
+tensors to (pointer, leading dimension) pairs, numpy CSR arrays to host pointers and torch
+streams to cudaStream_t handles.  Names follow walklap.h: θ (theta) = 1 - μ.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libwalklap.so")
+_lib = None
+
+WL_WALK, WL_NBT, WL_BTDW = 0, 1, 2
+WL_F_EXP, WL_F_RESOLVENT, WL_F_SERIES = 0, 1, 2
+_STATUS = {0: "WL_OK", 1: "WL_EINVAL", 2: "WL_EGRAPH", 3: "WL_EDIVERGE", 4: "WL_ENOCONV",
+           5: "WL_ENOMEM", 6: "WL_ECUDA", 7: "WL_ENCCL", 8: "WL_EUNSUPPORTED"}
+
+
+class WalkLapError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{_STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class _WalkFun(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("param", ctypes.c_double),
+                ("coeffs", ctypes.POINTER(ctypes.c_double)), ("ncoeffs", ctypes.c_int32)]
+
+
+class _Opts(ctypes.Structure):
+    _fields_ = [("krylov_dim", ctypes.c_int32), ("reorth", ctypes.c_int32),
+                ("max_cols", ctypes.c_int32), ("breakdown_tol", ctypes.c_double),
+                ("rho_bound", ctypes.c_double)]
+
+
+def load():
+    """Load the in-tree CUDA library; raise loudly if it was not built (no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libwalklap.so not found at {LIB_PATH}; run `python -c 'import "
+                          "__graft_entry__ as g; g.build()'` (nvcc, sm_100a)")
+    lib = ctypes.CDLL(LIB_PATH)
+    vp, i32, i64, dbl = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+    pvp = ctypes.POINTER(vp)
+    sig = {
+        "wl_last_error": ([], ctypes.c_char_p),
+        "wl_version": ([], ctypes.c_char_p),
+        "wl_launch_count": ([], i64),
+        "wl_opts_default": ([ctypes.POINTER(_Opts)], None),
+        "wl_nccl_unique_id": ([vp], ctypes.c_int),
+        "wl_comm_create": ([i32, i32, vp, i32, pvp], ctypes.c_int),
+        "wl_comm_destroy": ([vp], None),
+        "wl_partition": ([i64, vp, i32, vp], ctypes.c_int),
+        "wl_operator_create": ([vp, i64, i64, i64, vp, vp, i32, i32, vp, ctypes.POINTER(_WalkFun),
+                                ctypes.POINTER(_Opts), vp, pvp], ctypes.c_int),
+        "wl_operator_destroy": ([vp], None),
+        "wl_operator_info": ([vp, vp, vp, vp, vp], ctypes.c_int),
+        "wl_operator_diag_shift": ([vp, vp, i64, vp], ctypes.c_int),
+        "wl_workspace_create": ([vp, i32, pvp], ctypes.c_int),
+        "wl_workspace_destroy": ([vp], None),
+        "wl_apply": ([vp, i32, vp, i64, vp, i64, vp, vp], ctypes.c_int),
+        "wl_phi_apply": ([vp, i32, vp, i64, vp, i64, vp, vp], ctypes.c_int),
+        "wl_apply_host": ([vp, i32, vp, i64, vp, i64, vp, vp], ctypes.c_int),
+        "wl_diffuse": ([vp, i32, i32, vp, vp, vp, i64, i32, vp, vp], ctypes.c_int),
+        "wl_wait": ([vp, vp], ctypes.c_int),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+def _check(rc):
+    if rc != 0:
+        raise WalkLapError(rc, load().wl_last_error().decode())
+
+
+def version() -> str:
+    return load().wl_version().decode()
+
+
+def launch_count() -> int:
+    """Kernels launched by libwalklap in this process (monotone)."""
+    return int(load().wl_launch_count())
+
+
+def partition(row_ptr: np.ndarray, nranks: int) -> np.ndarray:
+    """nnz-balanced contiguous row partition (wl_partition)."""
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    out = np.empty(nranks + 1, dtype=np.int64)
+    _check(load().wl_partition(len(rp) - 1, rp.ctypes.data, nranks, out.ctypes.data))
+    return out
+
+
+def _stream_handle(stream):
+    import torch
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _block(t, cols, what):
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float64:
+        raise TypeError(f"{what}: expected a CUDA float64 tensor")
+    if t.dim() == 1:
+        t = t.view(-1, 1)
+    if t.shape[1] != cols or (t.shape[0] > 1 and t.stride(1) != 1):
+        raise ValueError(f"{what}: expected rows x {cols} with unit column stride")
+    return t, max(t.stride(0), cols)
+
+
+class Comm:
+    """NCCL communicator over the current torch.distributed group (one process per GPU)."""
+
+    def __init__(self, rank: int, world: int, device: int, group=None):
+        import torch.distributed as dist
+        lib = load()
+        uid = (ctypes.c_char * 128)()
+        if rank == 0:
+            _check(lib.wl_nccl_unique_id(uid))
+        obj = [bytes(uid) if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        uid = (ctypes.c_char * 128).from_buffer_copy(obj[0])
+        h = ctypes.c_void_p()
+        _check(lib.wl_comm_create(world, rank, uid, device, ctypes.byref(h)))
+        self.handle, self.rank, self.world, self.device = h, rank, world, device
+
+    def close(self):
+        if self.handle:
+            load().wl_comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Workspace:
+    def __init__(self, op: "Operator", max_b: int):
+        self.op = op
+        self.max_b = max_b
+        h = ctypes.c_void_p()
+        _check(load().wl_workspace_create(op.handle, max_b, ctypes.byref(h)))
+        self.handle = h
+
+    def close(self):
+        if getattr(self, "handle", None):
+            load().wl_workspace_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Operator:
+    """𝕃_θ(f) for one graph and n_theta downweighting values (wl_operator_create).
+
+    rows [row_begin, row_end) of an n_global-node graph; row_ptr/col_idx are the HOST CSR arrays
+    of those rows (global offsets and column ids).  f = ("exp", β) | ("resolvent", α) |
+    ("series", [c0, c1, ...]).
+    """
+
+    def __init__(self, n_global, row_ptr, col_idx, thetas=(1.0,), f=("exp", 1.0), variant=None,
+                 row_range=None, comm: Comm | None = None, krylov_dim=30, reorth=1, max_cols=32,
+                 breakdown_tol=1e-12, rho_bound=0.0, stream=None):
+        lib = load()
+        rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+        ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+        rb, re = (0, n_global) if row_range is None else row_range
+        thetas = [float(t) for t in np.atleast_1d(thetas)]
+        if variant is None:
+            variant = WL_BTDW
+        elif isinstance(variant, str):
+            variant = {"walk": WL_WALK, "nbt": WL_NBT, "btdw": WL_BTDW}[variant]
+        th = (ctypes.c_double * len(thetas))(*thetas)
+        kind, param = f
+        coeffs = None
+        wf = _WalkFun()
+        if kind == "exp":
+            wf.kind, wf.param = WL_F_EXP, float(param)
+        elif kind == "resolvent":
+            wf.kind, wf.param = WL_F_RESOLVENT, float(param)
+        elif kind == "series":
+            coeffs = (ctypes.c_double * len(param))(*[float(c) for c in param])
+            wf.kind, wf.param, wf.coeffs, wf.ncoeffs = WL_F_SERIES, 0.0, coeffs, len(param)
+        else:
+            raise ValueError(kind)
+        opts = _Opts()
+        lib.wl_opts_default(ctypes.byref(opts))
+        opts.krylov_dim, opts.reorth, opts.max_cols = krylov_dim, reorth, max_cols
+        opts.breakdown_tol, opts.rho_bound = breakdown_tol, rho_bound
+        h = ctypes.c_void_p()
+        _check(lib.wl_operator_create(comm.handle if comm else None, n_global, rb, re, rp.ctypes.data,
+                                      ci.ctypes.data, variant, len(thetas) if variant == WL_BTDW else 1,
+                                      th, ctypes.byref(wf), ctypes.byref(opts),
+                                      _stream_handle(stream), ctypes.byref(h)))
+        self.handle = h
+        self.comm = comm
+        self.thetas = thetas if variant == WL_BTDW else [1.0 if variant == WL_WALK else 0.0]
+        nl, nz, nh, nt = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int32()
+        _check(lib.wl_operator_info(h, ctypes.byref(nl), ctypes.byref(nz), ctypes.byref(nh), ctypes.byref(nt)))
+        self.n_local, self.nnz_local, self.n_halo, self.n_theta = nl.value, nz.value, nh.value, nt.value
+        self._ws = {}
+
+    def workspace(self, max_b: int) -> Workspace:
+        if max_b not in self._ws:
+            self._ws[max_b] = Workspace(self, max_b)
+        return self._ws[max_b]
+
+    def diag_shift(self, stream=None):
+        """t_θ = φ_θ 1 (n_local x n_theta)."""
+        import torch
+        out = torch.empty((self.n_local, self.n_theta), dtype=torch.float64, device="cuda")
+        _check(load().wl_operator_diag_shift(self.handle, ctypes.c_void_p(out.data_ptr()), self.n_theta,
+                                             _stream_handle(stream)))
+        return out
+
+    def _action(self, fn, V, out, ws, stream):
+        import torch
+        if V.dim() == 1:
+            V = V.view(-1, 1)
+        b = V.shape[1]
+        V, ldv = _block(V, b, "V")
+        cols = self.n_theta * b
+        if out is None:
+            out = torch.empty((self.n_local, cols), dtype=torch.float64, device=V.device)
+        out2, ldo = _block(out, cols, "out")
+        ws = ws or self.workspace(b)
+        _check(fn(self.handle, b, ctypes.c_void_p(V.data_ptr()), ldv, ctypes.c_void_p(out2.data_ptr()), ldo,
+                  ws.handle, _stream_handle(stream)))
+        return out
+
+    def apply(self, V, out=None, ws=None, stream=None):
+        """𝕃_θ V for every θ: returns n_local x (n_theta * b), column i*b + c = 𝕃_{θ_i} V[:, c]."""
+        return self._action(load().wl_apply, V, out, ws, stream)
+
+    def phi_apply(self, V, out=None, ws=None, stream=None):
+        """φ_θ V = Σ_k c_k q_k(A) V (same layout as apply)."""
+        return self._action(load().wl_phi_apply, V, out, ws, stream)
+
+    def apply_host(self, V: np.ndarray, out: np.ndarray | None = None, ws=None, stream=None) -> np.ndarray:
+        """𝕃_θ V with host buffers (copies inside the C call)."""
+        V = np.ascontiguousarray(V, dtype=np.float64)
+        if V.ndim == 1:
+            V = V[:, None]
+        b = V.shape[1]
+        cols = self.n_theta * b
+        if out is None:
+            out = np.empty((self.n_local, cols), dtype=np.float64)
+        ws = ws or self.workspace(b)
+        _check(load().wl_apply_host(self.handle, b, V.ctypes.data, b, out.ctypes.data, out.strides[0] // 8,
+                                    ws.handle, _stream_handle(stream)))
+        return out
+
+    def diffuse(self, x0, taus, theta_index=0, k_out=80, out=None, ws=None, stream=None):
+        """exp(-τ 𝕃_θ) x0 for every τ (columns)."""
+        import torch
+        taus = np.ascontiguousarray(np.atleast_1d(taus), dtype=np.float64)
+        nt = len(taus)
+        x0 = x0.reshape(-1)
+        if not (x0.is_cuda and x0.dtype == torch.float64 and x0.is_contiguous()):
+            raise TypeError("x0: expected a contiguous CUDA float64 vector")
+        if out is None:
+            out = torch.empty((self.n_local, nt), dtype=torch.float64, device=x0.device)
+        out2, ldx = _block(out, nt, "out")
+        ws = ws or self.workspace(1)
+        _check(load().wl_diffuse(self.handle, theta_index, nt, taus.ctypes.data, ctypes.c_void_p(x0.data_ptr()),
+                                 ctypes.c_void_p(out2.data_ptr()), ldx, k_out, ws.handle, _stream_handle(stream)))
+        return out
+
+    def wait(self, stream=None):
+        _check(load().wl_wait(self.handle, _stream_handle(stream)))
+
+    def close(self):
+        for ws in self._ws.values():
+            ws.close()
+        self._ws = {}
+        if getattr(self, "handle", None):
+            load().wl_operator_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

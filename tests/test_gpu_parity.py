@@ -1,0 +1,229 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by element.
+
+Tolerance (BASELINE.json north_star): relative L2 error per column <= 1e-10 in fp64.
+Sizes span several merge-path tiles and ragged tails; edge cases: isolated rows, zero
+columns, breakdown (tiny / invariant Krylov spaces), chunking beyond 32 columns.
+"""
+import numpy as np
+import pytest
+
+import graphgen as gg
+from oracle import coeffs as C
+from oracle import dense as D
+from oracle import series as S
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def wl():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2601_11338_b200 as wl
+    from paper_2601_11338_b200 import build
+    build.build()
+    wl.load()
+    return wl
+
+
+def relerr(got, ref):
+    got, ref = np.atleast_2d(got.T).T, np.atleast_2d(ref.T).T
+    den = np.linalg.norm(ref, axis=0)
+    den[den == 0] = 1.0
+    return np.linalg.norm(got - ref, axis=0) / den
+
+
+def _dense_case(wl, g, thetas, f, b, seed=101, **kw):
+    A = D.adjacency(g)
+    V = gg.vectors(g.n, b, seed)
+    op = wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=thetas, f=f, **kw)
+    LV = op.apply(torch.from_numpy(V).cuda()).cpu().numpy()
+    PV = op.phi_apply(torch.from_numpy(V).cuda()).cpu().numpy()
+    t = op.diag_shift().cpu().numpy()
+    fo = {"exp": C.exp, "resolvent": C.resolvent}.get(f[0], C.series)(f[1])
+    worst = 0.0
+    for i, th in enumerate(thetas):
+        ph = D.phi(A, 1.0 - th, fo)
+        sl = slice(i * b, (i + 1) * b)
+        worst = max(worst, relerr(LV[:, sl], D.walk_laplacian(ph) @ V).max(),
+                    relerr(PV[:, sl], ph @ V).max(), relerr(t[:, i], ph.sum(1)).max())
+    op.close()
+    return worst
+
+
+@pytest.mark.parametrize("b", [1, 8])
+def test_karate_exp_three_variants(wl, b):
+    """Config C1: walk (θ=1), θ=0.5 and nonbacktracking (θ=0), exp β = 1/ρ(A)."""
+    g = gg.karate()
+    beta = 1.0 / D.rho_A(D.adjacency(g))
+    assert _dense_case(wl, g, [1.0, 0.5, 0.0], ("exp", beta), b) < TOL
+
+
+def test_karate_variant_enums(wl):
+    g = gg.karate()
+    A = D.adjacency(g)
+    beta = 1.0 / D.rho_A(A)
+    V = gg.vectors(34, 2, 5)
+    for variant, mu in (("walk", 0.0), ("nbt", 1.0)):
+        op = wl.Operator(g.n, g.row_ptr, g.col_idx, variant=variant, f=("exp", beta))
+        got = op.apply(torch.from_numpy(V).cuda()).cpu().numpy()
+        assert relerr(got, D.laplacian(A, mu, C.exp(beta)) @ V).max() < TOL
+        op.close()
+
+
+def test_karate_resolvent_and_series(wl):
+    g = gg.karate()
+    rA = D.rho_A(D.adjacency(g))
+    assert _dense_case(wl, g, [1.0, 0.25, 0.0], ("resolvent", 0.5 / rA), 3) < TOL
+    assert _dense_case(wl, g, [0.7, 0.0], ("series", [0.5, 0.3, 0.2, 0.1, 0.05]), 2) < TOL
+
+
+def test_reduction_to_standard_laplacian(wl):
+    """c = (0, 1, 0, ...) gives 𝕃 = L = D - A for every θ."""
+    g = gg.barabasi_albert(500, 3, 7)
+    A = D.adjacency(g)
+    V = gg.vectors(g.n, 4, 9)
+    op = wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=[1.0, 0.5, 0.0], f=("series", [0.0, 1.0]))
+    got = op.apply(torch.from_numpy(V).cuda()).cpu().numpy()
+    ref = D.standard_laplacian(A) @ V
+    for i in range(3):
+        assert relerr(got[:, 4 * i:4 * i + 4], ref).max() < 1e-13
+
+
+def test_fig4b_through_gpu_operator(wl):
+    """Materialise 𝕃_1((1-αx)^{-1}) on the GPU (34 unit vectors) and reproduce Fig. 4(b)."""
+    from conftest import read_golden
+    gold = np.array(read_golden("fig4b_karate_nbt_resolvent_true.txt"), dtype=float)
+    g = gg.karate()
+    A = D.adjacency(g)
+    alpha = 1.0 / (1.0 + D.rho_Z(A, 1.0))
+    op = wl.Operator(g.n, g.row_ptr, g.col_idx, variant="nbt", f=("resolvent", alpha), krylov_dim=64)
+    Lap = op.apply(torch.eye(34, dtype=torch.float64, device="cuda")).cpu().numpy()
+    ph = D.return_probability(Lap / (1.0 + alpha), gold[:, 0])
+    assert np.max(np.abs(ph - gold[:, 1])) < 1e-9
+    op.close()
+
+
+@pytest.mark.parametrize("theta", [1.0, 0.5, 0.0])
+def test_multi_tile_graphs_vs_series(wl, theta):
+    """Power-law (R-MAT with isolated rows, hubs spanning tiles), BA and road-like graphs."""
+    graphs = [gg.rmat(14, 12000, 150000, seed=21, perm_seed=22),
+              gg.barabasi_albert(20000, 5, 31),
+              gg.grid_lcc(150, 149, 0.3, 41)]
+    for g in graphs:
+        rA = S.rho_A(g)
+        f = C.exp(1.0 / rA)
+        for b in (1, 5):
+            V = gg.vectors(g.n, b, 77)
+            op = wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=[theta], f=("exp", f.param))
+            got = op.apply(torch.from_numpy(V).cuda()).cpu().numpy()
+            ref = S.laplacian_apply(g, 1.0 - theta, f, V, rA)
+            assert relerr(got, ref).max() < TOL, (g.name, b)
+            t = op.diag_shift().cpu().numpy()[:, 0]
+            assert relerr(t, S.total_communicability(g, 1.0 - theta, f, rA)).max() < TOL
+            op.close()
+
+
+def test_theta_sweep_chunking_over_32_columns(wl):
+    """11 θ values x b = 3 inputs = 33 output columns: two internal Krylov batches."""
+    g = gg.rmat(12, 3000, 30000, seed=3, perm_seed=4)
+    rA = S.rho_A(g)
+    f = C.exp(1.0 / rA)
+    thetas = list(np.linspace(0.0, 1.0, 11))
+    V = gg.vectors(g.n, 3, 8)
+    op = wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=thetas, f=("exp", f.param))
+    got = op.apply(torch.from_numpy(V).cuda()).cpu().numpy()
+    for i, th in enumerate(thetas):
+        ref = S.laplacian_apply(g, 1.0 - th, f, V, rA)
+        assert relerr(got[:, 3 * i:3 * i + 3], ref).max() < TOL
+    op.close()
+
+
+def test_edge_cases(wl):
+    # isolated rows and a zero column: φ v = c_0 v there, 𝕃 v = 0 on isolated rows
+    g = gg.with_isolated(gg.karate(), 10)
+    rA = S.rho_A(g)
+    V = gg.vectors(g.n, 3, 1)
+    V[:, 1] = 0.0
+    V[:34, 2] = 0.0   # supported on isolated nodes only -> u = 0
+    op = wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=[0.5], f=("exp", 1.0 / rA))
+    got = op.apply(torch.from_numpy(V).cuda()).cpu().numpy()
+    ref = S.laplacian_apply(g, 0.5, C.exp(1.0 / rA), V, rA)
+    assert relerr(got[:, [0]], ref[:, [0]]).max() < TOL
+    assert np.all(got[:, 1] == 0.0) and np.all(got[:, 2] == 0.0)
+    pv = op.phi_apply(torch.from_numpy(V).cuda()).cpu().numpy()
+    assert np.array_equal(pv[:, 2], V[:, 2])
+    op.close()
+    # tiny graphs: Krylov space smaller than k (lucky breakdown), star with large k
+    for g in (gg.path(2), gg.complete(3), gg.star(40)):
+        rA = S.rho_A(g)
+        for th in (1.0, 0.0):
+            Vs = gg.vectors(g.n, 2, 3)
+            op = wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=[th], f=("exp", 1.0 / rA), krylov_dim=60)
+            got = op.apply(torch.from_numpy(Vs).cuda()).cpu().numpy()
+            ref = D.laplacian(D.adjacency(g), 1.0 - th, C.exp(1.0 / rA)) @ Vs
+            assert relerr(got, ref).max() < TOL, (g.name, th)
+            op.close()
+    # edgeless graph: 𝕃 = 0
+    e = gg.from_edges(5, [])
+    op = wl.Operator(5, e.row_ptr, e.col_idx, thetas=[0.3], f=("exp", 1.0))
+    assert np.all(op.apply(torch.ones(5, 1, dtype=torch.float64, device="cuda")).cpu().numpy() == 0)
+    op.close()
+
+
+def test_diffusion_karate_and_road(wl):
+    """a9: exp(-τ𝕃)x0 vs dense eigendecomposition; Fig. 4 time grid."""
+    for g, ts, kout in ((gg.karate(), np.linspace(0, 10, 30), 40),
+                        (gg.grid_lcc(30, 30, 0.3, 5), np.linspace(0, 100, 19), 80)):
+        A = D.adjacency(g)
+        rA = D.rho_A(A)
+        for th in (1.0, 0.0):
+            x0 = np.zeros(g.n)
+            x0[g.n // 2] = 1.0
+            op = wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=[th], f=("exp", 1.0 / rA))
+            X = op.diffuse(torch.from_numpy(x0).cuda(), ts, k_out=kout).cpu().numpy()
+            ref = D.diffusion(D.laplacian(A, 1.0 - th, C.exp(1.0 / rA)), x0, ts)
+            assert relerr(X, ref).max() < TOL, (g.name, th)
+            assert np.max(np.abs(X.sum(0) - 1.0)) < 1e-10        # mass conservation
+            op.close()
+
+
+def test_apply_host_matches_device(wl):
+    g = gg.barabasi_albert(3000, 4, 2)
+    rA = S.rho_A(g)
+    V = gg.vectors(g.n, 2, 4)
+    op = wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=[1.0, 0.0], f=("exp", 1.0 / rA))
+    a = op.apply(torch.from_numpy(V).cuda()).cpu().numpy()
+    b = op.apply_host(V)
+    assert np.array_equal(a, b)   # same kernels, same order: bitwise
+    op.close()
+
+
+def test_cabi_errors(wl):
+    g = gg.karate()
+    with pytest.raises(wl.WalkLapError, match="WL_EINVAL"):
+        wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=[1.5], f=("exp", 1.0))
+    bad = g.col_idx.copy()
+    bad[0] = 0  # self loop on row 0
+    with pytest.raises(wl.WalkLapError, match="WL_EGRAPH"):
+        wl.Operator(g.n, g.row_ptr, bad, thetas=[1.0], f=("exp", 1.0))
+    with pytest.raises(wl.WalkLapError, match="WL_EDIVERGE"):
+        wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=[1.0], f=("resolvent", 0.2), rho_bound=6.73)
+
+
+def test_full_c2_barabasi_albert(wl):
+    """Config C2 at full size: BA n=1e5, avg degree 10, k=30, b=8, θ in {1, 0.5, 0}."""
+    g = gg.barabasi_albert(100000, 5, 1001)
+    rA = S.rho_A(g)
+    f = C.exp(1.0 / rA)
+    V = gg.vectors(g.n, 8, 102)
+    thetas = [1.0, 0.5, 0.0]
+    op = wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=thetas, f=("exp", f.param), krylov_dim=30)
+    got = op.apply(torch.from_numpy(V).cuda()).cpu().numpy()
+    for i, th in enumerate(thetas):
+        ref = S.laplacian_apply(g, 1.0 - th, f, V, rA)
+        assert relerr(got[:, 8 * i:8 * i + 8], ref).max() < TOL
+    op.close()
