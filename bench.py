@@ -1,0 +1,374 @@
+#!/usr/bin/env python
+"""Benchmark: walk-based Laplacian actions/s (𝕃·v, fp64) on BASELINE.json config C4.
+
+Workload (N=1 and every N): config C4 — R-MAT n = 1e7, m = 2e8 (nnz 4e8), θ sweep
+{0, 0.1, ..., 1} of the backtrack-downweighted Laplacian 𝕃_θ(exp(βx)), β = 1/ρ(A).
+One step = 𝕃_θ v for all 11 θ (steps a3-a7, one batched Krylov action of 11 columns,
+k = 30 Arnoldi steps on the companion operator Z); t_θ = φ_θ 1 (a8) is built once at operator
+creation, outside the timed region (like the CSR upload a1).  Row-partitioned across N GPUs
+(nnz-balanced), NCCL halo exchange + allreduce: strong scaling.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl walklap|reference] [--config c4]
+
+Prints ONE JSON line (rank 0).  --impl reference times the CPU oracle (oracle/, fp64 series) on
+the same workload, on the host cores, one action per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import graphgen as gg  # noqa: E402
+from graphgen import configs  # noqa: E402
+
+METRIC = "Laplacian actions/sec (L·v, fp64) and SpMV HBM GB/s vs peak"
+
+
+def log(*a):
+    print("[bench]", *a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200", "-i", str(self.dev)], stdout=subprocess.PIPE,
+                                      stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.p:
+            self.p.terminate()
+            try:
+                out, _ = self.p.communicate(timeout=5)
+            except Exception:
+                out = ""
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup(ngpus):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != ngpus:
+        if world == 1 and ngpus > 1:
+            raise SystemExit("--gpus N>1 must be launched with torchrun (one process per GPU)")
+    return world, rank, local
+
+
+def load_graph(cfg, world, rank, torch, dist):
+    """Rank 0 generates the seeded graph; N>1 broadcasts it over NCCL (setup, untimed)."""
+    t0 = time.time()
+    if rank == 0:
+        g = cfg["make"]()
+    if world > 1:
+        meta = torch.tensor([g.n, g.nnz] if rank == 0 else [0, 0], dtype=torch.int64, device="cuda")
+        dist.broadcast(meta, 0)
+        n, nnz = int(meta[0]), int(meta[1])
+        rp = torch.from_numpy(g.row_ptr).cuda() if rank == 0 else torch.empty(n + 1, dtype=torch.int64, device="cuda")
+        ci = torch.from_numpy(g.col_idx).cuda() if rank == 0 else torch.empty(nnz, dtype=torch.int32, device="cuda")
+        dist.broadcast(rp, 0)
+        dist.broadcast(ci, 0)
+        if rank != 0:
+            g = gg.Graph(n, rp.cpu().numpy(), ci.cpu().numpy(), "broadcast")
+        del rp, ci
+    return g, time.time() - t0
+
+
+def algorithmic_bytes(n, nnz, n_halo, G, K, Bmax, b, n_theta):
+    """Bytes each kernel must move per step, by kernel name."""
+    out = {}
+    def add(k, v):
+        out[k] = out.get(k, 0) + v
+    for g0 in range(0, G, Bmax):
+        B = min(Bmax, G - g0)
+        L = 2 * n
+        vec = 8 * L * B
+        blk = 8 * n * B
+        csr = 4 * nnz + 4 * (n + 1)
+        add("spmv_merge", (csr + 2 * blk + 8 * n_halo * B))          # seed 1: gather y + write
+        add("spmv_merge", (csr + 3 * blk + 8 * n_halo * B))          # seed 2: + x
+        add("spmv_merge", K * (csr + 3 * blk + 8 * n_halo * B))      # Z steps
+        add("gram_proj", vec)                                         # ||u||
+        for j in range(K):
+            add("gram_proj", (j + 2) * vec)
+            add("gram_update_proj" if j + 1 <= 32 else "gram_update_norm", (j + 3) * vec)
+            add("gram_update_norm", (j + 3) * vec)
+        add("combine", K * blk + blk + 8 * n * b + 8 * n * n_theta)
+        add("batch_inputs", 8 * n * b + blk)
+    return out
+
+
+def run_walklap(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2601_11338_b200 as wl
+
+    world, rank, local = dist_setup(args.gpus)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = configs.get(args.config)
+    g, t_gen = load_graph(cfg, world, rank, torch, dist)
+    bounds = wl.partition(g.row_ptr, world)
+    rb, re = int(bounds[rank]), int(bounds[rank + 1])
+    rp = g.row_ptr[rb:re + 1]
+    ci = g.col_idx[g.row_ptr[rb]:g.row_ptr[re]]
+    comm = wl.Comm(rank, world, local) if world > 1 else None
+    t0 = time.time()
+    # β = 1/ρ(A) (inverse temperature) — ρ(A) by the library's Lanczos on A
+    probe = wl.Operator(g.n, rp, ci, thetas=[1.0], f=("series", [0.0, 1.0]), row_range=(rb, re), comm=comm,
+                        krylov_dim=2)
+    rho = probe.spectral_radius(k=args.rho_k)
+    probe.close()
+    beta = 1.0 / rho
+    thetas = cfg["thetas"]
+    K = args.krylov if args.krylov else cfg["krylov_dim"]
+    op = wl.Operator(g.n, rp, ci, thetas=thetas, f=("exp", beta), row_range=(rb, re), comm=comm, krylov_dim=K)
+    torch.cuda.synchronize()
+    t_create = time.time() - t0
+    b = args.b if args.b else cfg["b"]
+    n_loc = op.n_local
+    Vfull = gg.vectors(g.n, b, cfg["vec_seed"] or 103)
+    V = torch.from_numpy(np.ascontiguousarray(Vfull[rb:re])).cuda()
+    del Vfull
+    G = op.n_theta * b
+    out = torch.empty((n_loc, G), dtype=torch.float64, device="cuda")
+    ws = op.workspace(b)
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        op.apply(V, out=out, ws=ws)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    wl.profile_enable(True)
+    l0 = wl.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            op.apply(V, out=out, ws=ws)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = wl.launch_count() - l0
+    wl.profile_enable(False)
+    prof = wl.profile_collect()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    actions = G  # every step applies 𝕃_θ to b vectors for each θ (whole job, all ranks together)
+    value = actions / (ms / 1e3)
+
+    # ---- end to end through the public C ABI with host buffers (pinned), H2D + D2H inside ----
+    e2e = None
+    if not args.no_e2e:
+        Vh = torch.from_numpy(np.ascontiguousarray(V.cpu().numpy())).pin_memory().numpy()
+        LVh = torch.empty((n_loc, G), dtype=torch.float64).pin_memory().numpy()
+        op.apply_host(Vh, out=LVh, ws=ws)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        for _ in range(args.steps):
+            op.apply_host(Vh, out=LVh, ws=ws)
+        e_ms = (time.perf_counter() - t1) * 1e3 / args.steps
+        if world > 1:
+            t = torch.tensor([e_ms], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e2e = {"value": actions / (e_ms / 1e3), "unit": "actions/s", "ms_per_step": e_ms,
+               "h2d_bytes_per_step": int(Vh.nbytes) * world, "d2h_bytes_per_step": int(LVh.nbytes) * world}
+
+    # ---- roofline of the dominant kernel (rank 0's kernels; live CUDA-event timing) ----
+    peak, peak_src = peaks()
+    nnz_loc = int(ci.shape[0])
+    ab = algorithmic_bytes(n_loc, nnz_loc, op.n_halo, G, K, ws_bmax(op, b), b, op.n_theta)
+    kernels = {}
+    for name, (tot_ms, cnt) in prof.items():
+        per_step_ms = tot_ms / args.steps
+        bytes_ = ab.get(name)
+        kernels[name] = {"ms_per_step": per_step_ms, "launches_per_step": cnt / args.steps,
+                         "share": per_step_ms / ms}
+        if bytes_:
+            gbs = bytes_ / (per_step_ms / 1e3) / 1e9
+            kernels[name].update({"alg_bytes_per_step": bytes_, "achieved_gbs": gbs, "frac": gbs / peak})
+    top = max((k for k in kernels if "alg_bytes_per_step" in kernels[k]), key=lambda k: kernels[k]["ms_per_step"])
+    ncu = ncu_traffic()
+    roof = {"kernel": top, "bound": "hbm", "achieved": kernels[top]["achieved_gbs"], "peak": peak,
+            "unit": "GB/s", "frac": kernels[top]["frac"], "peak_source": peak_src,
+            "traffic": ncu.get(top), "alg_bytes_per_launch": ab[top] / max(1, kernels[top]["launches_per_step"])}
+    spmv = kernels.get("spmv_merge", {})
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(g, cfg, beta, args)
+
+    if rank == 0:
+        clocks = clk.summary()
+        line = {
+            "metric": METRIC, "value": value, "unit": "actions/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded R-MAT, graphgen)",
+            "config": {"workload": f"{args.config}: {cfg['desc']}", "n": g.n, "nnz": g.nnz,
+                       "thetas": thetas, "b": b, "actions_per_step": actions, "krylov_dim": K,
+                       "f": f"exp(beta x), beta=1/rho(A)={beta:.6g}", "global_batch": actions,
+                       "parallelism": f"row-partition x{world} (NCCL halo + allreduce)",
+                       "l2": "inputs larger than L2 (col_idx 1.6 GB, basis tens of GB): no flush",
+                       "setup_s": {"generate": round(t_gen, 2), "operator_create_incl_t": round(t_create, 2)}},
+            "roofline": roof,
+            "spmv": {"achieved_gbs": spmv.get("achieved_gbs"), "frac": spmv.get("frac"), "peak": peak,
+                     "share": spmv.get("share")},
+            "kernels": {k: {kk: (round(vv, 6) if isinstance(vv, float) else vv) for kk, vv in v.items()}
+                        for k, v in sorted(kernels.items(), key=lambda kv: -kv[1]["ms_per_step"])},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    op.close()
+    if comm:
+        comm.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def ws_bmax(op, b):
+    return max(1, min(32, op.n_theta * b))
+
+
+def ncu_traffic():
+    """dram bytes per launch from the committed ncu --set full summary (profiles/), if present."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        return {k: v["dram_bytes_per_launch"] for k, v in json.load(open(p)).items()}
+    except Exception:
+        return {}
+
+
+def _oracle_sample(g, cfg, beta):
+    """Bounded oracle sample: one action 𝕃_θ v at θ = 0.5 by the fp64 series (t precomputed, untimed)."""
+    from oracle import coeffs as C
+    from oracle import series as S
+    import threadpoolctl
+    A = S.csr(g)
+    f = C.exp(beta)
+    rho = 1.0 / beta
+    v = gg.vectors(g.n, 1, cfg["vec_seed"] or 103)[:, 0]
+    t = S.total_communicability(g, 0.5, f, rho, A=A)
+    with threadpoolctl.threadpool_limits(1):
+        t0 = time.perf_counter()
+        _ = t * v - S.phi_apply(g, 0.5, f, v, rho, A=A)
+        dt = time.perf_counter() - t0
+    return dt
+
+
+def cpu_baseline(g, cfg, beta, args):
+    dt = _oracle_sample(g, cfg, beta)
+    return {"value": 1.0 / dt, "unit": "actions/s", "cores": 1, "kind": "oracle",
+            "sample": "one action L_theta v at theta=0.5 on the full graph (fp64 series oracle, "
+                      "scipy CSR SpMV, 1 thread; t precomputed outside the timing)",
+            "seconds": dt}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = configs.get(args.config)
+    g = cfg["make"]()
+    from oracle import series as S
+    rho = S.rho_A(g)
+    beta = 1.0 / rho
+    for _ in range(args.warmup):
+        _oracle_sample(g, cfg, beta)
+    times = [_oracle_sample(g, cfg, beta) for _ in range(args.steps)]
+    ms = 1e3 * sum(times) / len(times)
+    value = 1e3 / ms
+    sample = ("one action L_theta v at theta=0.5 per step on the full graph (fp64 series oracle, "
+              "scipy CSR SpMV, 1 thread; t precomputed outside the timing)")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "actions/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded R-MAT, graphgen)",
+        "config": {"workload": f"{args.config}: {cfg['desc']}", "n": g.n, "nnz": g.nnz,
+                   "f": f"exp(beta x), beta=1/rho(A)={beta:.6g}"},
+        "cpu_baseline": {"value": value, "unit": "actions/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": "actions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="walklap", choices=["walklap", "reference"])
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--b", type=int, default=0)
+    ap.add_argument("--krylov", type=int, default=0)
+    ap.add_argument("--rho-k", type=int, default=60)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("warning: contract requires >= 3 warm-up steps")
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_walklap(args)
+
+
+if __name__ == "__main__":
+    main()

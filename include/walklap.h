@@ -159,6 +159,23 @@ wl_status wl_diffuse(const wl_operator* op, int32_t theta_index, int32_t nt, con
                      const double* x0, double* X, int64_t ldx, int32_t k_out, wl_workspace* ws,
                      wl_stream stream);
 
+/* ---- spectral radius (helper for β = 1/ρ(A); convergence checks, Prop. pro:whe-we-converge)
+ * ρ(A) of the operator's graph by k steps of Lanczos on A (full reorthogonalisation) started from
+ * the all-ones vector (positive overlap with the Perron vector of the nonnegative symmetric A);
+ * returns the largest eigenvalue of the k x k tridiagonal (a lower bound converging to ρ(A)).
+ * Synchronous.  2 <= k <= 128. */
+wl_status wl_spectral_radius(const wl_operator* op, int32_t k, double* rho_out, wl_stream stream);
+
+/* ---- live per-kernel timing (benchmarking) ----------------------------------------------------
+ * When enabled, every kernel launch scope is bracketed by CUDA events on its stream (small
+ * overhead).  wl_profile_collect() synchronizes on the recorded events, aggregates elapsed time
+ * per kernel name and clears the session; wl_profile_get(i) reads entry i < wl_profile_count().
+ * `name` points to library-owned storage valid until the next collect. */
+void wl_profile_enable(int32_t on);
+wl_status wl_profile_collect(void);
+int32_t wl_profile_count(void);
+wl_status wl_profile_get(int32_t i, const char** name, double* total_ms, int64_t* launches);
+
 /* Synchronizes `stream` and returns the first asynchronous error recorded on `op` (or WL_OK). */
 wl_status wl_wait(const wl_operator* op, wl_stream stream);
 

@@ -12,5 +12,7 @@ from .walklap import (  # noqa: F401
     launch_count,
     load,
     partition,
+    profile_collect,
+    profile_enable,
     version,
 )

@@ -32,6 +32,44 @@ namespace wl {
 static std::atomic<int64_t> g_launches{0};
 void note_launch(const char*) { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+// ---- live per-kernel timing (bench.py): CUDA events around every launch scope ----------------
+struct ProfRec {
+  std::string name;
+  cudaEvent_t a, b;
+};
+static std::mutex g_prof_mtx;
+static bool g_prof_on = false;
+static std::vector<ProfRec> g_prof;          // events of the current session
+static std::vector<cudaEvent_t> g_prof_pool;  // recycled events
+static std::vector<std::pair<std::string, std::pair<double, int64_t>>> g_prof_result;
+
+static cudaEvent_t prof_event() {
+  if (!g_prof_pool.empty()) {
+    cudaEvent_t e = g_prof_pool.back();
+    g_prof_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  WL_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+LaunchScope::LaunchScope(const char* name, cudaStream_t st) : s(st) {
+  note_launch(name);
+  if (!g_prof_on) return;
+  std::lock_guard<std::mutex> lk(g_prof_mtx);
+  ProfRec r{name, prof_event(), prof_event()};
+  WL_CUDA(cudaEventRecord(r.a, s));
+  slot = (int)g_prof.size();
+  g_prof.push_back(r);
+}
+
+LaunchScope::~LaunchScope() {
+  if (slot < 0) return;
+  std::lock_guard<std::mutex> lk(g_prof_mtx);
+  cudaEventRecord(g_prof[slot].b, s);
+}
+
 void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
   if (e == cudaSuccess) return;
   const std::string msg = std::string(what) + ": " + cudaGetErrorString(e) + " (" + file + ":" +
@@ -515,6 +553,124 @@ void build_operator(wl_operator* op, const int64_t* rp_in, const int32_t* ci_in,
   }
 }
 
+
+// Outer Arnoldi with CGS2 on unit-stride n-vectors (B = 1), basis ws->oQ (vector 0 preset by the
+// caller), Hessenberg ws->oH (layout (m+1) x m), scales ws->os, ||P_0|| in ws->on0.
+// `apply(P̃_j, out)` writes the operator applied to the UNNORMALISED basis vector P̃_j.
+template <class Apply>
+void outer_arnoldi(const wl_operator* op, wl_workspace* ws, int m, Apply&& apply, cudaStream_t s) {
+  const int64_t n = op->n_loc;
+  WL_CUDA(cudaMemsetAsync(ws->oH.p, 0, sizeof(double) * (m + 1) * m, s));
+  GramArgs g{};
+  g.Q = ws->oQ.p;
+  g.vstride = n;
+  g.len = n;
+  g.B = 1;
+  g.s = ws->os.p;
+  g.partials = ws->partials.p;
+  g.ticket = ws->ticket.p;
+  g.grid = gram_grid(n, 1);
+  g.nvec = 0;
+  g.wa = ws->oQ.p;
+  g.split = n;
+  g.sums_out = ws->osums1.p;
+  gram_proj(g, s);
+  allreduce(op, ws->osums1.p, 1, s);
+  finalize_norm0(ws->osums1.p, 1, ws->on0.p, ws->os.p, ws->okeff.p, m, s);
+  for (int j = 0; j < m; ++j) {
+    double* Pj = ws->oQ.p + (int64_t)j * n;
+    double* Pn = ws->oQ.p + (int64_t)(j + 1) * n;
+    apply(Pj, ws->ow.p);
+    GramArgs w = g;
+    w.nvec = j + 1;
+    w.wa = ws->ow.p;
+    w.wscale = ws->os.p + j;  // q_j = s_j P̃_j, so Z q_j = s_j * apply(P̃_j)
+    w.split = n;
+    w.sums_out = ws->osums1.p;
+    gram_proj(w, s);
+    allreduce(op, ws->osums1.p, j + 2, s);
+    GramArgs u = w;
+    u.wout = Pn;
+    u.sums_in = ws->osums1.p;
+    u.sums_out = ws->osums2.p;
+    if (j + 1 <= 32) {
+      gram_update_proj(u, s);
+    } else {
+      u.sums_out = ws->osums3.p;
+      gram_update_norm(u, s);
+      GramArgs p2 = g;
+      p2.nvec = j + 1;
+      p2.wa = Pn;
+      p2.split = n;
+      p2.sums_out = ws->osums2.p;
+      gram_proj(p2, s);
+    }
+    allreduce(op, ws->osums2.p, j + 1, s);
+    GramArgs v = g;
+    v.nvec = j + 1;
+    v.wa = Pn;
+    v.split = n;
+    v.wout = Pn;
+    v.sums_in = ws->osums2.p;
+    v.sums_out = ws->osums3.p;
+    gram_update_norm(v, s);
+    allreduce(op, ws->osums3.p, 1, s);
+    finalize_step(ws->osums1.p, ws->osums2.p, ws->osums3.p, j, 1, m, op->opts.breakdown_tol, 1, ws->os.p,
+                  ws->oH.p, ws->okeff.p, s);
+  }
+}
+
+void outer_alloc(const wl_operator* op, wl_workspace* ws, int m, int nt) {
+  const int64_t n = op->n_loc;
+  if (ws->kout_alloc >= m && ws->otau.n >= (size_t)nt) return;
+  ws->oQ.alloc((size_t)(m + 1) * std::max<int64_t>(1, n));
+  ws->ow.alloc((size_t)std::max<int64_t>(1, n));
+  ws->oH.alloc((size_t)(m + 1) * m);
+  ws->os.alloc(m + 1);
+  ws->on0.alloc(1);
+  ws->okeff.alloc(1);
+  ws->osums1.alloc(m + 2);
+  ws->osums2.alloc(m + 2);
+  ws->osums3.alloc(m + 2);
+  ws->otau.alloc(std::max(1, nt));
+  ws->oY.alloc((size_t)std::max(1, nt) * (m + 1));
+  ws->oscratch.alloc((size_t)std::max(1, nt) * 9 * kMaxSmallN * kMaxSmallN);
+  ws->kout_alloc = m;
+  const size_t need = (size_t)gram_grid(n, 1) * (m + 2);
+  if (ws->partials.n < need) ws->partials.alloc(need);
+  if (!ws->ticket.p) {
+    ws->ticket.alloc(1);
+    WL_CUDA(cudaMemset(ws->ticket.p, 0, sizeof(unsigned int)));
+  }
+}
+
+// Largest eigenvalue of the symmetric tridiagonal (a, b) by bisection on Sturm counts.
+double tridiag_max_eig(const std::vector<double>& a, const std::vector<double>& b) {
+  const int m = (int)a.size();
+  double lo = 1e300, hi = -1e300;
+  for (int i = 0; i < m; ++i) {  // Gershgorin interval
+    const double r = (i > 0 ? std::fabs(b[i - 1]) : 0.0) + (i + 1 < m ? std::fabs(b[i]) : 0.0);
+    lo = std::min(lo, a[i] - r);
+    hi = std::max(hi, a[i] + r);
+  }
+  auto count_below = [&](double x) {  // number of eigenvalues < x
+    int c = 0;
+    double d = 1.0;
+    for (int i = 0; i < m; ++i) {
+      d = a[i] - x - (i > 0 ? b[i - 1] * b[i - 1] / d : 0.0);
+      if (d == 0.0) d = -1e-300;
+      if (d < 0) ++c;
+    }
+    return c;
+  };
+  for (int it = 0; it < 200 && hi - lo > 1e-15 * std::max(1.0, std::fabs(hi)); ++it) {
+    const double mid = 0.5 * (lo + hi);
+    if (count_below(mid) >= m) hi = mid;  // all eigenvalues below mid
+    else lo = mid;
+  }
+  return hi;
+}
+
 void check_block(const void* p, int64_t ld, int64_t cols, const char* what) {
   if (!p) throw Error(WL_EINVAL, std::string(what) + " is NULL");
   if (ld < cols) throw Error(WL_EINVAL, std::string(what) + ": leading dimension < columns");
@@ -783,85 +939,13 @@ wl_status wl_diffuse(const wl_operator* op, int32_t theta_index, int32_t nt, con
     cudaStream_t s = S_(stream);
     const int64_t n = op->n_loc;
     const int m = k_out;
-    if (ws->kout_alloc < m || ws->otau.n < (size_t)nt) {
-      ws->oQ.alloc((size_t)(m + 1) * std::max<int64_t>(1, n));
-      ws->ow.alloc((size_t)std::max<int64_t>(1, n));
-      ws->oH.alloc((size_t)(m + 1) * m);
-      ws->os.alloc(m + 1);
-      ws->on0.alloc(1);
-      ws->okeff.alloc(1);
-      ws->osums1.alloc(m + 2);
-      ws->osums2.alloc(m + 2);
-      ws->osums3.alloc(m + 2);
-      ws->otau.alloc(nt);
-      ws->oY.alloc((size_t)nt * (m + 1));
-      ws->oscratch.alloc((size_t)nt * 9 * kMaxSmallN * kMaxSmallN);
-      ws->kout_alloc = m;
-      if (ws->partials.n < (size_t)gram_grid(n, 1) * (m + 2))
-        ws->partials.alloc((size_t)gram_grid(n, 1) * (m + 2));
-    }
-    WL_CUDA(cudaMemsetAsync(ws->oH.p, 0, sizeof(double) * (m + 1) * m, s));
+    outer_alloc(op, ws, m, nt);
     WL_CUDA(cudaMemcpyAsync(ws->otau.p, tau, sizeof(double) * nt, cudaMemcpyHostToDevice, s));
-    // outer Arnoldi (= Lanczos with full reorthogonalisation: 𝕃 symmetric, Prop. pro:still-again-an-mmatrix)
-    GramArgs g{};
-    g.Q = ws->oQ.p;
-    g.vstride = n;
-    g.len = n;
-    g.B = 1;
-    g.s = ws->os.p;
-    g.partials = ws->partials.p;
-    g.ticket = ws->ticket.p;
-    g.grid = gram_grid(n, 1);
     WL_CUDA(cudaMemcpyAsync(ws->oQ.p, x0, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
-    g.nvec = 0;
-    g.wa = ws->oQ.p;
-    g.split = n;
-    g.sums_out = ws->osums1.p;
-    gram_proj(g, s);
-    allreduce(op, ws->osums1.p, 1, s);
-    finalize_norm0(ws->osums1.p, 1, ws->on0.p, ws->os.p, ws->okeff.p, m, s);
-    for (int j = 0; j < m; ++j) {
-      double* Pj = ws->oQ.p + (int64_t)j * n;
-      double* Pn = ws->oQ.p + (int64_t)(j + 1) * n;
-      // inner action: ow = 𝕃 P̃_j (P̃_j unnormalised; q_j = s_j P̃_j)
-      run_chunk(op, ws, 1, Pj, 1, 1, theta_index, 1, ws->ow.p, 1, s);
-      GramArgs w = g;
-      w.nvec = j + 1;
-      w.wa = ws->ow.p;
-      w.wscale = ws->os.p + j;
-      w.split = n;
-      w.sums_out = ws->osums1.p;
-      gram_proj(w, s);
-      allreduce(op, ws->osums1.p, j + 2, s);
-      GramArgs u = w;
-      u.wout = Pn;
-      u.sums_in = ws->osums1.p;
-      u.sums_out = ws->osums2.p;
-      if (j + 1 <= 32) {
-        gram_update_proj(u, s);
-      } else {
-        u.sums_out = ws->osums3.p;
-        gram_update_norm(u, s);
-        GramArgs p2 = g;
-        p2.nvec = j + 1;
-        p2.wa = Pn;
-        p2.split = n;
-        p2.sums_out = ws->osums2.p;
-        gram_proj(p2, s);
-      }
-      allreduce(op, ws->osums2.p, j + 1, s);
-      GramArgs v = g;
-      v.nvec = j + 1;
-      v.wa = Pn;
-      v.split = n;
-      v.wout = Pn;
-      v.sums_in = ws->osums2.p;
-      v.sums_out = ws->osums3.p;
-      gram_update_norm(v, s);
-      allreduce(op, ws->osums3.p, 1, s);
-      finalize_step(ws->osums1.p, ws->osums2.p, ws->osums3.p, j, 1, m, op->opts.breakdown_tol, 1, ws->os.p,
-                    ws->oH.p, ws->okeff.p, s);
-    }
+    // outer Arnoldi (= Lanczos with full reorthogonalisation: 𝕃 symmetric, Prop. pro:still-again-an-mmatrix)
+    outer_arnoldi(op, ws, m, [&](const double* Pj, double* out) {
+      run_chunk(op, ws, 1, Pj, 1, 1, theta_index, 1, out, 1, s);  // inner action 𝕃 P̃_j
+    }, s);
     SmallFArgs f{};
     f.H = ws->oH.p;
     f.K = m;
@@ -876,6 +960,70 @@ wl_status wl_diffuse(const wl_operator* op, int32_t theta_index, int32_t nt, con
     f.nprob = nt;
     small_f(f, s);
     lanczos_combine(ws->oQ.p, n, m + 1, n, ws->oY.p, nt, 1.0, X, ldx, s);
+  });
+}
+
+wl_status wl_spectral_radius(const wl_operator* op, int32_t k, double* rho_out, wl_stream stream) {
+  return guarded([&] {
+    if (!op || !rho_out) throw Error(WL_EINVAL, "NULL argument");
+    if (k < 2 || k > 128) throw Error(WL_EINVAL, "k must be in [2, 128]");
+    DeviceGuard dg(op->device);
+    cudaStream_t s = S_(stream);
+    wl_workspace ws;
+    ws.op = op;
+    if (op->n_halo > 0) ws.halo_recv.alloc(op->n_halo);
+    if (op->n_send > 0) ws.halo_send.alloc(op->n_send);
+    outer_alloc(op, &ws, k, 1);
+    fill(ws.oQ.p, op->n_loc, 1.0, s);
+    outer_arnoldi(op, &ws, k, [&](const double* Pj, double* out) {
+      halo_exchange(op, &ws, Pj, 1, 1, s);
+      do_spmv(op, &ws, Pj, nullptr, nullptr, nullptr, nullptr, out, 1, s);  // A P̃_j
+    }, s);
+    std::vector<double> H((size_t)(k + 1) * k);
+    int keff = 0;
+    WL_CUDA(cudaMemcpyAsync(H.data(), ws.oH.p, sizeof(double) * H.size(), cudaMemcpyDeviceToHost, s));
+    WL_CUDA(cudaMemcpyAsync(&keff, ws.okeff.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    WL_CUDA(cudaStreamSynchronize(s));
+    if (keff <= 0) { *rho_out = 0.0; return; }
+    std::vector<double> a(keff), b(std::max(0, keff - 1));
+    for (int i = 0; i < keff; ++i) a[i] = H[(size_t)i * (k + 1) + i];
+    for (int i = 0; i + 1 < keff; ++i) b[i] = H[(size_t)i * (k + 1) + i + 1];
+    *rho_out = tridiag_max_eig(a, b);
+  });
+}
+
+void wl_profile_enable(int32_t on) {
+  std::lock_guard<std::mutex> lk(g_prof_mtx);
+  g_prof_on = on != 0;
+}
+
+wl_status wl_profile_collect(void) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(g_prof_mtx);
+    std::map<std::string, std::pair<double, int64_t>> acc;
+    for (auto& r : g_prof) {
+      WL_CUDA(cudaEventSynchronize(r.b));
+      float ms = 0.f;
+      WL_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+      auto& e = acc[r.name];
+      e.first += ms;
+      e.second += 1;
+      g_prof_pool.push_back(r.a);
+      g_prof_pool.push_back(r.b);
+    }
+    g_prof.clear();
+    g_prof_result.assign(acc.begin(), acc.end());
+  });
+}
+
+int32_t wl_profile_count(void) { return (int32_t)g_prof_result.size(); }
+
+wl_status wl_profile_get(int32_t i, const char** name, double* total_ms, int64_t* launches) {
+  return guarded([&] {
+    if (i < 0 || i >= (int32_t)g_prof_result.size()) throw Error(WL_EINVAL, "profile index out of range");
+    if (name) *name = g_prof_result[i].first.c_str();
+    if (total_ms) *total_ms = g_prof_result[i].second.first;
+    if (launches) *launches = g_prof_result[i].second.second;
   });
 }
 

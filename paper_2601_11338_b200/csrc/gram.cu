@@ -15,6 +15,7 @@
 // sums the partials in CTA order.  Threads own one column each (block = B * m threads and
 // a grid-stride that is a multiple of B), so column reductions never mix columns.
 #include "wl_internal.cuh"
+#include <algorithm>
 
 namespace wl {
 namespace {
@@ -177,8 +178,20 @@ int gram_grid(int64_t elems, int B) {
     else KERNEL<64><<<a.grid, bs_, 0, s>>>(__VA_ARGS__);                                    \
   } while (0)
 
+// Bases longer than 64 vectors (outer diffusion Lanczos) are processed in tiles of 64: tile
+// [i0, i1) writes its sums at sums_out + i0*B; its trailing w.w slot is overwritten by the next
+// tile, and the last tile leaves w.w at index nvec.
 void gram_proj(GramArgs a, cudaStream_t s) {
-  if (a.nvec > kMaxKrylov + 1) throw Error(1, "gram_proj: too many vectors");
+  if (a.nvec > 64) {
+    for (int i0 = 0; i0 < a.nvec; i0 += 64) {
+      GramArgs t = a;
+      t.nvec = std::min(64, a.nvec - i0);
+      t.Q = a.Q + (int64_t)i0 * a.vstride;
+      t.sums_out = a.sums_out + (int64_t)i0 * a.B;
+      gram_proj(t, s);
+    }
+    return;
+  }
   WL_LAUNCH("gram_proj");
   WL_GRAM_DISPATCH(gram_proj_kernel, a.nvec, a);
   WL_CUDA(cudaGetLastError());
@@ -195,7 +208,18 @@ void gram_update_proj(GramArgs a, cudaStream_t s) {
 }
 
 void gram_update_norm(GramArgs a, cudaStream_t s) {
-  if (a.nvec > kMaxKrylov + 1) throw Error(1, "gram_update_norm: too many vectors");
+  if (a.nvec > 64) {  // tiles of 64 basis vectors; tiles after the first update wout in place
+    for (int i0 = 0; i0 < a.nvec; i0 += 64) {
+      GramArgs t = a;
+      t.nvec = std::min(64, a.nvec - i0);
+      t.Q = a.Q + (int64_t)i0 * a.vstride;
+      t.s = a.s + (int64_t)i0 * a.B;
+      t.sums_in = a.sums_in + (int64_t)i0 * a.B;
+      if (i0 > 0) { t.wa = a.wout; t.wscale = nullptr; t.split = a.len; t.wb = nullptr; }
+      gram_update_norm(t, s);
+    }
+    return;
+  }
   WL_LAUNCH("gram_update_norm");
   WL_GRAM_DISPATCH(gram_update_norm_kernel, a.nvec, a);
   WL_CUDA(cudaGetLastError());

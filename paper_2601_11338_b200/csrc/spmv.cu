@@ -197,15 +197,19 @@ void spmv(const SpmvArgs& a, cudaStream_t s) {
   if (a.num_tiles <= 0) return;
   const size_t smem = sizeof(int) * (2 * (size_t)a.tile_items + 2);
   const int ipt = ipt_for(a.B);
-  WL_LAUNCH("spmv_merge");
-  if (ipt == 8) spmv_merge_kernel<8><<<a.num_tiles, kThreads, smem, s>>>(a);
-  else if (ipt == 16) spmv_merge_kernel<16><<<a.num_tiles, kThreads, smem, s>>>(a);
-  else spmv_merge_kernel<32><<<a.num_tiles, kThreads, smem, s>>>(a);
-  WL_CUDA(cudaGetLastError());
-  WL_LAUNCH("spmv_fixup");
-  spmv_fixup_kernel<<<(a.num_tiles + 7) / 8, 256, 0, s>>>(a.carry_row, a.carry_val, a.num_tiles, a.B,
-                                                          a.scale, a.out, a.ldo);
-  WL_CUDA(cudaGetLastError());
+  {
+    WL_LAUNCH("spmv_merge");
+    if (ipt == 8) spmv_merge_kernel<8><<<a.num_tiles, kThreads, smem, s>>>(a);
+    else if (ipt == 16) spmv_merge_kernel<16><<<a.num_tiles, kThreads, smem, s>>>(a);
+    else spmv_merge_kernel<32><<<a.num_tiles, kThreads, smem, s>>>(a);
+    WL_CUDA(cudaGetLastError());
+  }
+  {
+    WL_LAUNCH("spmv_fixup");
+    spmv_fixup_kernel<<<(a.num_tiles + 7) / 8, 256, 0, s>>>(a.carry_row, a.carry_val, a.num_tiles, a.B,
+                                                            a.scale, a.out, a.ldo);
+    WL_CUDA(cudaGetLastError());
+  }
 }
 
 }  // namespace wl

@@ -15,7 +15,15 @@ struct Error : std::runtime_error {
 void cuda_check(cudaError_t e, const char* what, const char* file, int line);
 #define WL_CUDA(x) ::wl::cuda_check((x), #x, __FILE__, __LINE__)
 void note_launch(const char* name);  // increments the process-wide launch counter
-#define WL_LAUNCH(name) ::wl::note_launch(name)
+// Scoped launch accounting: counts the launch and, when profiling is enabled (wl_profile_enable),
+// brackets the launch(es) in this scope with CUDA events on stream `s`, accumulated per name.
+struct LaunchScope {
+  int slot = -1;
+  cudaStream_t s;
+  LaunchScope(const char* name, cudaStream_t st);
+  ~LaunchScope();
+};
+#define WL_LAUNCH(name) ::wl::LaunchScope wl_launch_scope_(name, s)
 
 constexpr int kMaxCols = 32;    // columns per Krylov batch (B)
 constexpr int kMaxKrylov = 64;  // Arnoldi steps per action

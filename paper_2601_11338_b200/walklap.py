@@ -70,6 +70,12 @@ def load():
         "wl_apply_host": ([vp, i32, vp, i64, vp, i64, vp, vp], ctypes.c_int),
         "wl_diffuse": ([vp, i32, i32, vp, vp, vp, i64, i32, vp, vp], ctypes.c_int),
         "wl_wait": ([vp, vp], ctypes.c_int),
+        "wl_spectral_radius": ([vp, i32, ctypes.POINTER(dbl), vp], ctypes.c_int),
+        "wl_profile_enable": ([i32], None),
+        "wl_profile_collect": ([], ctypes.c_int),
+        "wl_profile_count": ([], i32),
+        "wl_profile_get": ([i32, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(dbl), ctypes.POINTER(i64)],
+                           ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -91,6 +97,23 @@ def version() -> str:
 def launch_count() -> int:
     """Kernels launched by libwalklap in this process (monotone)."""
     return int(load().wl_launch_count())
+
+
+def profile_enable(on: bool = True) -> None:
+    """Bracket every library launch with CUDA events on its stream (live per-kernel timing)."""
+    load().wl_profile_enable(1 if on else 0)
+
+
+def profile_collect() -> dict:
+    """Synchronize on the recorded events; {kernel name: (total ms, launches)}; clears the session."""
+    lib = load()
+    _check(lib.wl_profile_collect())
+    out = {}
+    for i in range(lib.wl_profile_count()):
+        name, ms, cnt = ctypes.c_char_p(), ctypes.c_double(), ctypes.c_int64()
+        _check(lib.wl_profile_get(i, ctypes.byref(name), ctypes.byref(ms), ctypes.byref(cnt)))
+        out[name.value.decode()] = (ms.value, cnt.value)
+    return out
 
 
 def partition(row_ptr: np.ndarray, nranks: int) -> np.ndarray:
@@ -281,6 +304,12 @@ class Operator:
         _check(load().wl_diffuse(self.handle, theta_index, nt, taus.ctypes.data, ctypes.c_void_p(x0.data_ptr()),
                                  ctypes.c_void_p(out2.data_ptr()), ldx, k_out, ws.handle, _stream_handle(stream)))
         return out
+
+    def spectral_radius(self, k: int = 60, stream=None) -> float:
+        """ρ(A) of the operator's graph (wl_spectral_radius: Lanczos on A from the ones vector)."""
+        rho = ctypes.c_double()
+        _check(load().wl_spectral_radius(self.handle, k, ctypes.byref(rho), _stream_handle(stream)))
+        return rho.value
 
     def wait(self, stream=None):
         _check(load().wl_wait(self.handle, _stream_handle(stream)))
