@@ -135,9 +135,9 @@ def algorithmic_bytes(n, nnz, n_halo, G, K, Bmax, b, n_theta):
         vec = 8 * L * B
         blk = 8 * n * B
         csr = 4 * nnz + 4 * (n + 1)
-        add("spmv_merge", (csr + 2 * blk + 8 * n_halo * B))          # seed 1: gather y + write
-        add("spmv_merge", (csr + 3 * blk + 8 * n_halo * B))          # seed 2: + x
-        add("spmv_merge", K * (csr + 3 * blk + 8 * n_halo * B))      # Z steps
+        add("spmv_binned", (csr + 2 * blk + 8 * n_halo * B))          # seed 1: gather y + write
+        add("spmv_binned", (csr + 3 * blk + 8 * n_halo * B))          # seed 2: + x
+        add("spmv_binned", K * (csr + 3 * blk + 8 * n_halo * B))      # Z steps
         add("gram_proj", vec)                                         # ||u||
         for j in range(K):
             add("gram_proj", (j + 2) * vec)
@@ -250,7 +250,7 @@ def run_walklap(args):
     roof = {"kernel": top, "bound": "hbm", "achieved": kernels[top]["achieved_gbs"], "peak": peak,
             "unit": "GB/s", "frac": kernels[top]["frac"], "peak_source": peak_src,
             "traffic": ncu.get(top), "alg_bytes_per_launch": ab[top] / max(1, kernels[top]["launches_per_step"])}
-    spmv = kernels.get("spmv_merge", {})
+    spmv = kernels.get("spmv_binned", {})
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -129,13 +129,6 @@ struct wl_comm {
   int nranks = 1, rank = 0, device = 0;
 };
 
-struct TileSet {
-  int items = 0, num = 0;
-  DArr<int2> coords;
-  DArr<int32_t> carry_row;
-  DArr<double> carry_val;
-};
-
 struct wl_operator {
   int device = 0;
   wl_comm* comm = nullptr;
@@ -157,8 +150,10 @@ struct wl_operator {
   DArr<double> coeffs_dev;
   wl_opts opts{};
   DArr<double> tprime;  // n_loc x n_theta: t - c_0 (φ1 minus its identity term)
-  std::map<int, std::unique_ptr<TileSet>> tiles;
-  mutable std::mutex mtx;
+  // degree bins of the SpMM (spmv.cu)
+  DArr<int32_t> small_rows, medium_rows;
+  DArr<int4> chunks;
+  int n_small = 0, n_medium = 0, n_chunks = 0;
 };
 
 struct wl_workspace {
@@ -170,6 +165,8 @@ struct wl_workspace {
   DArr<double> H, s_all, n0, comb, scratch;
   DArr<int> keff, vcol, tcol;
   DArr<double> colp;  // g0z, g1z, g0s, g1s (kMaxCols each)
+  DArr<double> chunk_part;
+  DArr<unsigned int> row_ticket;
   // host-buffer entry point
   DArr<double> hV, hLV;
   // diffusion (outer Lanczos)
@@ -229,36 +226,21 @@ void halo_exchange(const wl_operator* op, wl_workspace* ws, const double* src, i
   WL_NCCL(ncclGroupEnd());
 }
 
-TileSet& tiles_for(const wl_operator* op, int B, cudaStream_t s) {
-  const int T = spmv_tile_items(B);
-  std::lock_guard<std::mutex> lk(op->mtx);
-  auto& m = const_cast<wl_operator*>(op)->tiles;
-  auto it = m.find(T);
-  if (it != m.end()) return *it->second;
-  auto ts = std::make_unique<TileSet>();
-  ts->items = T;
-  const int64_t items = (int64_t)op->n_loc + op->nnz_loc;
-  ts->num = (int)std::max<int64_t>(1, (items + T - 1) / T);
-  ts->coords.alloc(ts->num + 1);
-  ts->carry_row.alloc(ts->num);
-  ts->carry_val.alloc((size_t)ts->num * kMaxCols);
-  spmv_tiles(op->rowptr.p, op->n_loc, op->nnz_loc, T, ts->coords.p, ts->num, s);
-  auto& ref = *ts;
-  m.emplace(T, std::move(ts));
-  return ref;
-}
-
 void do_spmv(const wl_operator* op, wl_workspace* ws, const double* y, const double* x,
              const double* g0, const double* g1, const double* scale, double* out, int B,
              cudaStream_t s) {
-  TileSet& ts = tiles_for(op, B, s);
   SpmvArgs a{};
   a.rowptr = op->rowptr.p;
   a.col = op->col.p;
-  a.tiles = ts.coords.p;
-  a.num_tiles = ts.num;
-  a.tile_items = ts.items;
   a.n_loc = op->n_loc;
+  a.small_rows = op->small_rows.p;
+  a.n_small = op->n_small;
+  a.medium_rows = op->medium_rows.p;
+  a.n_medium = op->n_medium;
+  a.chunks = op->chunks.p;
+  a.n_chunks = op->n_chunks;
+  a.chunk_part = ws->chunk_part.p;
+  a.row_ticket = ws->row_ticket.p;
   a.y = y;
   a.ldy = B;
   a.yh = ws->halo_recv.p;
@@ -271,9 +253,17 @@ void do_spmv(const wl_operator* op, wl_workspace* ws, const double* y, const dou
   a.g1 = g1;
   a.scale = scale;
   a.B = B;
-  a.carry_row = ts.carry_row.p;
-  a.carry_val = ts.carry_val.p;
   spmv(a, s);
+}
+
+// Scratch of the hub-row chunks (partials + tickets) for B columns.
+void spmv_scratch(const wl_operator* op, wl_workspace* ws, int B) {
+  if (op->n_chunks == 0) return;
+  if (ws->chunk_part.n < (size_t)op->n_chunks * B) ws->chunk_part.alloc((size_t)op->n_chunks * B);
+  if (ws->row_ticket.n < (size_t)op->n_chunks) {
+    ws->row_ticket.alloc(op->n_chunks);
+    WL_CUDA(cudaMemset(ws->row_ticket.p, 0, sizeof(unsigned int) * op->n_chunks));
+  }
 }
 
 // One Krylov action on global output columns [gstart, gstart + B) of the n_theta*b block;
@@ -431,6 +421,7 @@ void workspace_alloc(wl_workspace* ws, const wl_operator* op, int max_b) {
   ws->vcol.alloc(kMaxCols);
   ws->tcol.alloc(kMaxCols);
   ws->colp.alloc(4 * kMaxCols);
+  spmv_scratch(op, ws, B);
   WL_CUDA(cudaDeviceSynchronize());
 }
 
@@ -507,6 +498,29 @@ void build_operator(wl_operator* op, const int64_t* rp_in, const int32_t* ci_in,
     const int64_t cg = ci_in[z];
     if (cg >= op->row_begin && cg < op->row_end) col[z] = (int32_t)(cg - op->row_begin);
     else col[z] = (int32_t)(n + (std::lower_bound(remote.begin(), remote.end(), cg) - remote.begin()));
+  }
+  {  // degree bins (spmv.cu): small rows, medium rows, hub-row chunks
+    std::vector<int32_t> sm, md;
+    std::vector<int4> ch;
+    for (int64_t r = 0; r < n; ++r) {
+      const int32_t d = rp[r + 1] - rp[r];
+      if (d <= kSmallMax) sm.push_back((int32_t)r);
+      else if (d <= kHubChunk) md.push_back((int32_t)r);
+      else {
+        const int first = (int)ch.size();
+        for (int32_t z = rp[r]; z < rp[r + 1]; z += kHubChunk)
+          ch.push_back(make_int4((int)r, z, std::min(z + kHubChunk, rp[r + 1]), first));
+      }
+    }
+    op->n_small = (int)sm.size();
+    op->n_medium = (int)md.size();
+    op->n_chunks = (int)ch.size();
+    op->small_rows.alloc(std::max<size_t>(1, sm.size()));
+    op->medium_rows.alloc(std::max<size_t>(1, md.size()));
+    op->chunks.alloc(std::max<size_t>(1, ch.size()));
+    if (!sm.empty()) WL_CUDA(cudaMemcpy(op->small_rows.p, sm.data(), 4 * sm.size(), cudaMemcpyHostToDevice));
+    if (!md.empty()) WL_CUDA(cudaMemcpy(op->medium_rows.p, md.data(), 4 * md.size(), cudaMemcpyHostToDevice));
+    if (!ch.empty()) WL_CUDA(cudaMemcpy(op->chunks.p, ch.data(), sizeof(int4) * ch.size(), cudaMemcpyHostToDevice));
   }
   op->rowptr.alloc(n + 1);
   op->col.alloc(std::max<int64_t>(nnz, 1));
@@ -974,6 +988,7 @@ wl_status wl_spectral_radius(const wl_operator* op, int32_t k, double* rho_out, 
     if (op->n_halo > 0) ws.halo_recv.alloc(op->n_halo);
     if (op->n_send > 0) ws.halo_send.alloc(op->n_send);
     outer_alloc(op, &ws, k, 1);
+    spmv_scratch(op, &ws, 1);
     fill(ws.oQ.p, op->n_loc, 1.0, s);
     outer_arnoldi(op, &ws, k, [&](const double* Pj, double* out) {
       halo_exchange(op, &ws, Pj, 1, 1, s);

@@ -78,32 +78,53 @@ __device__ inline double load_w(const GramArgs& a, int64_t e, int64_t splitE, do
   return e < splitE ? wsc * __ldg(a.wa + e) : __ldg(a.wb + (e - splitE));
 }
 
-template <int JT>
+// Each thread owns column c = tid % B and visits U elements per iteration, e + u*bs
+// (u < U): all in column c, each a coalesced warp access, U independent loads per basis vector.
+template <int JT, int U>
 __global__ void __launch_bounds__(256) gram_proj_kernel(GramArgs a) {
   __shared__ double red[8 * 256];
   const int B = a.B, tid = threadIdx.x, bs = blockDim.x, c = tid % B;
   const int64_t total = a.len * B, splitE = a.split * B;
   const double wsc = a.wscale ? a.wscale[c] : 1.0;
+  const int nvec = a.nvec;
   double acc[JT + 1];
 #pragma unroll
   for (int i = 0; i <= JT; ++i) acc[i] = 0.0;
-  for (int64_t e = (int64_t)blockIdx.x * bs + tid; e < total; e += (int64_t)gridDim.x * bs) {
-    const double w = load_w(a, e, splitE, wsc);
+  const int64_t step = (int64_t)gridDim.x * bs * U;
+  for (int64_t base = (int64_t)blockIdx.x * bs * U + tid; base < total; base += step) {
+    double w[U];
 #pragma unroll
-    for (int i = 0; i < JT; ++i)
-      if (i < a.nvec) acc[i] += __ldg(a.Q + i * a.vstride + e) * w;
-    acc[JT] += w * w;
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = base + (int64_t)u * bs;
+      w[u] = e < total ? load_w(a, e, splitE, wsc) : 0.0;
+      acc[JT] += w[u] * w[u];
+    }
+    double q[JT][U];  // all loads of this iteration in flight before any FMA
+    const double* qp = a.Q + base;
+#pragma unroll
+    for (int i = 0; i < JT; ++i) {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        q[i][u] = (i < nvec && base + (int64_t)u * bs < total) ? __ldg(qp + (int64_t)u * bs) : 0.0;
+      qp += a.vstride;
+    }
+#pragma unroll
+    for (int i = 0; i < JT; ++i) {
+      double sum = 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) sum += q[i][u] * w[u];
+      acc[i] += sum;
+    }
   }
-  // move the w.w accumulator to slot nvec so partial layout is [i < nvec | ww]
   double v[JT + 1];
 #pragma unroll
-  for (int i = 0; i <= JT; ++i) v[i] = (i < a.nvec) ? acc[i] : (i == a.nvec ? acc[JT] : 0.0);
-  const int nout = (a.nvec + 1) * B;
-  block_partials<JT + 1>(v, a.nvec + 1, B, nout, a.partials, red);
+  for (int i = 0; i <= JT; ++i) v[i] = (i < nvec) ? acc[i] : (i == nvec ? acc[JT] : 0.0);
+  const int nout = (nvec + 1) * B;
+  block_partials<JT + 1>(v, nvec + 1, B, nout, a.partials, red);
   last_block_reduce(a.partials, nout, a.sums_out, a.ticket);
 }
 
-template <int JT>
+template <int JT, int U>
 __global__ void __launch_bounds__(256) gram_update_proj_kernel(GramArgs a) {
   __shared__ double red[8 * 256];
   __shared__ double coef[JT * kMaxCols];
@@ -115,27 +136,53 @@ __global__ void __launch_bounds__(256) gram_update_proj_kernel(GramArgs a) {
   __syncthreads();
   const int64_t total = a.len * B, splitE = a.split * B;
   const double wsc = a.wscale ? a.wscale[c] : 1.0;
+  const int nvec = a.nvec;
   double acc[JT];
 #pragma unroll
   for (int i = 0; i < JT; ++i) acc[i] = 0.0;
-  for (int64_t e = (int64_t)blockIdx.x * bs + tid; e < total; e += (int64_t)gridDim.x * bs) {
-    double q[JT];
+  const int64_t step = (int64_t)gridDim.x * bs * U;
+  for (int64_t base = (int64_t)blockIdx.x * bs * U + tid; base < total; base += step) {
+    double q[JT][U];
+    const double* qp = a.Q + base;
 #pragma unroll
-    for (int i = 0; i < JT; ++i) q[i] = (i < a.nvec) ? __ldg(a.Q + i * a.vstride + e) : 0.0;
-    double w = load_w(a, e, splitE, wsc);
+    for (int i = 0; i < JT; ++i) {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        q[i][u] = (i < nvec && base + (int64_t)u * bs < total) ? __ldg(qp + (int64_t)u * bs) : 0.0;
+      qp += a.vstride;
+    }
+    double w[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = base + (int64_t)u * bs;
+      w[u] = e < total ? load_w(a, e, splitE, wsc) : 0.0;
+    }
 #pragma unroll
     for (int i = 0; i < JT; ++i)
-      if (i < a.nvec) w -= coef[i * B + c] * q[i];
-    a.wout[e] = w;
+      if (i < nvec) {
+        const double ci = coef[i * B + c];
 #pragma unroll
-    for (int i = 0; i < JT; ++i) acc[i] += q[i] * w;
+        for (int u = 0; u < U; ++u) w[u] -= ci * q[i][u];
+      }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = base + (int64_t)u * bs;
+      if (e < total) a.wout[e] = w[u];
+    }
+#pragma unroll
+    for (int i = 0; i < JT; ++i) {
+      double sum = 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) sum += q[i][u] * w[u];
+      acc[i] += sum;
+    }
   }
-  const int nout = a.nvec * B;
-  block_partials<JT>(acc, a.nvec, B, nout, a.partials, red);
+  const int nout = nvec * B;
+  block_partials<JT>(acc, nvec, B, nout, a.partials, red);
   last_block_reduce(a.partials, nout, a.sums_out, a.ticket);
 }
 
-template <int JT>
+template <int JT, int U>
 __global__ void __launch_bounds__(256) gram_update_norm_kernel(GramArgs a) {
   __shared__ double red[8 * 256];
   __shared__ double coef[JT * kMaxCols];
@@ -147,14 +194,39 @@ __global__ void __launch_bounds__(256) gram_update_norm_kernel(GramArgs a) {
   __syncthreads();
   const int64_t total = a.len * B, splitE = a.split * B;
   const double wsc = a.wscale ? a.wscale[c] : 1.0;
+  const int nvec = a.nvec;
   double acc[1] = {0.0};
-  for (int64_t e = (int64_t)blockIdx.x * bs + tid; e < total; e += (int64_t)gridDim.x * bs) {
-    double w = e < splitE ? wsc * a.wa[e] : a.wb[e - splitE];  // may alias wout: plain loads
-#pragma unroll 8
-    for (int i = 0; i < JT; ++i)
-      if (i < a.nvec) w -= coef[i * B + c] * __ldg(a.Q + i * a.vstride + e);
-    a.wout[e] = w;
-    acc[0] += w * w;
+  const int64_t step = (int64_t)gridDim.x * bs * U;
+  for (int64_t base = (int64_t)blockIdx.x * bs * U + tid; base < total; base += step) {
+    double w[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {  // may alias wout: plain loads
+      const int64_t e = base + (int64_t)u * bs;
+      w[u] = e < total ? (e < splitE ? wsc * a.wa[e] : a.wb[e - splitE]) : 0.0;
+    }
+    double q[JT][U];
+    const double* qp = a.Q + base;
+#pragma unroll
+    for (int i = 0; i < JT; ++i) {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        q[i][u] = (i < nvec && base + (int64_t)u * bs < total) ? __ldg(qp + (int64_t)u * bs) : 0.0;
+      qp += a.vstride;
+    }
+#pragma unroll
+    for (int i = 0; i < JT; ++i) {
+      const double ci = (i < nvec) ? coef[i * B + c] : 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) w[u] -= ci * q[i][u];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = base + (int64_t)u * bs;
+      if (e < total) {
+        a.wout[e] = w[u];
+        acc[0] += w[u] * w[u];
+      }
+    }
   }
   const int nout = B;
   block_partials<1>(acc, 1, B, nout, a.partials, red);
@@ -165,17 +237,17 @@ __global__ void __launch_bounds__(256) gram_update_norm_kernel(GramArgs a) {
 
 int gram_grid(int64_t elems, int B) {
   const int bs = gram_block(B);
-  const int64_t blocks = (elems + bs - 1) / bs;
+  const int64_t blocks = (elems + 4 * bs - 1) / (4 * bs);
   return (int)std::max<int64_t>(1, std::min<int64_t>(blocks, 148 * 4));
 }
 
 #define WL_GRAM_DISPATCH(KERNEL, NV, ...)                                                   \
   do {                                                                                      \
     const int bs_ = gram_block(a.B);                                                        \
-    if ((NV) <= 8) KERNEL<8><<<a.grid, bs_, 0, s>>>(__VA_ARGS__);                           \
-    else if ((NV) <= 16) KERNEL<16><<<a.grid, bs_, 0, s>>>(__VA_ARGS__);                    \
-    else if ((NV) <= 32) KERNEL<32><<<a.grid, bs_, 0, s>>>(__VA_ARGS__);                    \
-    else KERNEL<64><<<a.grid, bs_, 0, s>>>(__VA_ARGS__);                                    \
+    if ((NV) <= 8) KERNEL<8, 4><<<a.grid, bs_, 0, s>>>(__VA_ARGS__);                        \
+    else if ((NV) <= 16) KERNEL<16, 4><<<a.grid, bs_, 0, s>>>(__VA_ARGS__);                 \
+    else if ((NV) <= 32) KERNEL<32, 2><<<a.grid, bs_, 0, s>>>(__VA_ARGS__);                 \
+    else KERNEL<64, 1><<<a.grid, bs_, 0, s>>>(__VA_ARGS__);                                 \
   } while (0)
 
 // Bases longer than 64 vectors (outer diffusion Lanczos) are processed in tiles of 64: tile
@@ -201,9 +273,9 @@ void gram_update_proj(GramArgs a, cudaStream_t s) {
   if (a.nvec > 32) throw Error(1, "gram_update_proj: nvec > 32 (use the unfused path)");
   WL_LAUNCH("gram_update_proj");
   const int bs_ = gram_block(a.B);
-  if (a.nvec <= 8) gram_update_proj_kernel<8><<<a.grid, bs_, 0, s>>>(a);
-  else if (a.nvec <= 16) gram_update_proj_kernel<16><<<a.grid, bs_, 0, s>>>(a);
-  else gram_update_proj_kernel<32><<<a.grid, bs_, 0, s>>>(a);
+  if (a.nvec <= 8) gram_update_proj_kernel<8, 4><<<a.grid, bs_, 0, s>>>(a);
+  else if (a.nvec <= 16) gram_update_proj_kernel<16, 4><<<a.grid, bs_, 0, s>>>(a);
+  else gram_update_proj_kernel<32, 2><<<a.grid, bs_, 0, s>>>(a);
   WL_CUDA(cudaGetLastError());
 }
 

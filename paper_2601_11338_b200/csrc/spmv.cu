@@ -7,209 +7,142 @@
 // kernel with (g0, g1) = (0, 0) / (0, -μ); the Z step uses (g0, g1) = (μ², -μ).  A has unit
 // values, so the kernel only adds gathered rows — no value array is read.
 //
-// Load balance: merge-path decomposition (Merrill & Garland) of the (row-end, nnz) sequence
-// into equal tiles of merge items, so a 300k-degree hub and a million isolated rows cost the
-// same per tile.  A CTA (256 threads) handles one tile; it is split into "lane groups" of B
-// lanes (lane c owns column c of the row-major n x B blocks), each group walking IPT
-// consecutive merge items.  Gathered rows are prefetched into registers (IPT independent loads
-// per lane) before the walk.  Rows split across groups are stitched in shared memory; rows
-// split across tiles are stitched deterministically by spmv_fixup_kernel.
+// Power-law load balance by degree binning (built once per operator, B-independent):
+//   small rows  (deg <= 32, incl. isolated rows): one lane group (B lanes, lane c = column c of the
+//               row-major n x B blocks) per row, rows in id order so neighbouring groups read
+//               neighbouring col_idx ranges;
+//   medium rows (32 < deg <= 1024): one warp per row, its lane groups split the nonzeros and are
+//               reduced with shuffles;
+//   hub rows    (deg > 1024): split into 1024-nonzero chunks, one warp per chunk; each chunk writes
+//               a partial and the last chunk to finish (per-row ticket) sums the row's partials in
+//               chunk order — deterministic, no second launch.
+// Every lane issues up to 8 independent gathers before consuming them (ILP), and all control flow
+// is uniform within a lane group.
 #include "wl_internal.cuh"
-#include <climits>
 
 namespace wl {
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kU = 8;  // gathers in flight per lane
 
-__host__ __device__ inline int groups_per_cta(int B) { return (kThreads / 32) * (32 / B); }
-inline int ipt_for(int B) { return B <= 2 ? 8 : (B <= 8 ? 16 : 32); }
-
-// merge-path search on the tile-local sequence: returns rows consumed at diagonal d
-__device__ inline int merge_search(int d, const int* s_rp, int nrows, int z0, int nnzt) {
-  int lo = max(0, d - nnzt), hi = min(d, nrows);
-  while (lo < hi) {
-    int mid = (lo + hi) >> 1;
-    if (s_rp[mid + 1] <= z0 + (d - mid - 1)) lo = mid + 1;
-    else hi = mid;
+struct Ctx {
+  const SpmvArgs& a;
+  int c;
+  double g0, g1, sc;
+  __device__ double gather(int cl) const {
+    return cl < a.n_loc ? __ldg(a.y + (int64_t)cl * a.ldy + c)
+                        : __ldg(a.yh + (int64_t)(cl - a.n_loc) * a.ldh + c);
   }
-  return lo;
+  __device__ void write(int r, int deg, double sum) const {
+    double o = sum;
+    if (a.x) o += (g0 + g1 * (double)deg) * a.x[(int64_t)r * a.ldx + c];
+    a.out[(int64_t)r * a.ldo + c] = sc * o;
+  }
+  // Σ y[col[z]] for z = z0 + first, z0 + first + step, ... < z1 (step = lane groups sharing the row)
+  __device__ double strided_sum(int z0, int z1, int first, int step) const {
+    double acc = 0.0;
+    for (int z = z0 + first; z < z1; z += kU * step) {  // kU predicated gathers in flight
+      int cl[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int zz = z + u * step;
+        cl[u] = zz < z1 ? __ldg(a.col + zz) : -1;
+      }
+      double v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) v[u] = cl[u] >= 0 ? gather(cl[u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < kU; ++u) acc += v[u];
+    }
+    return acc;
+  }
+};
+
+// sum of `v` over the lane groups of a warp, result valid in group 0 (lanes 0..B-1)
+__device__ inline double group_reduce(double v, int B, int gpw) {
+  if ((B & (B - 1)) == 0) {
+    for (int off = 16; off >= B; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+    return v;
+  }
+  const int lane = threadIdx.x & 31;
+  double s = v;
+  for (int g = 1; g < gpw; ++g) {
+    const double o = __shfl_sync(0xffffffffu, v, (lane + g * B) & 31);
+    s += o;
+  }
+  return s;
 }
 
-template <int IPT>
-__global__ void __launch_bounds__(kThreads) spmv_merge_kernel(SpmvArgs a) {
-  extern __shared__ int s_dyn[];
-  __shared__ double s_carry[kThreads];  // groups * B <= 256
-  __shared__ int s_crow[kThreads];
-  __shared__ int s_cdone[kThreads];
-
+__global__ void __launch_bounds__(kThreads) spmv_binned_kernel(SpmvArgs a) {
   const int B = a.B;
-  const int T = a.tile_items;
-  const int t = blockIdx.x;
-  const int2 c0 = a.tiles[t], c1 = a.tiles[t + 1];
-  const int r0 = c0.x, z0 = c0.y;
-  const int nrows = c1.x - r0, nnzt = c1.y - z0;
-  int* s_rp = s_dyn;           // s_rp[i] = rowptr[r0 + i], i in [0, nrows + 1]
-  int* s_col = s_dyn + T + 2;  // s_col[k] = col[z0 + k], k < nnzt
-
-  for (int i = threadIdx.x; i <= nrows + 1; i += kThreads)
-    s_rp[i] = (r0 + i <= a.n_loc) ? __ldg(a.rowptr + r0 + i) : INT_MAX;
-  for (int k = threadIdx.x; k < nnzt; k += kThreads) s_col[k] = __ldg(a.col + z0 + k);
-  __syncthreads();
-
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int gpw = 32 / B;
   const int gi = lane / B, c = lane - gi * B;
   const bool lane_ok = gi < gpw;
-  const int g = warp * gpw + (lane_ok ? gi : 0);
-  const int total = nrows + nnzt;
-  const int d0 = min(g * IPT, total), d1 = min(d0 + IPT, total);
-  const int x0 = merge_search(d0, s_rp, nrows, z0, nnzt), y0 = d0 - x0;
-  const int x1 = merge_search(d1, s_rp, nrows, z0, nnzt), y1 = d1 - x1;
-
-  // prefetch the gathered values of this group's nonzeros (independent loads in flight)
-  double v[IPT];
-#pragma unroll
-  for (int p = 0; p < IPT; ++p) {
-    v[p] = 0.0;
-    const int k = y0 + p;
-    if (lane_ok && k < y1) {
-      const int cl = s_col[k];
-      v[p] = cl < a.n_loc ? __ldg(a.y + (int64_t)cl * a.ldy + c)
-                          : __ldg(a.yh + (int64_t)(cl - a.n_loc) * a.ldh + c);
-    }
+  const int cc = lane_ok ? c : 0;
+  Ctx ctx{a, cc, a.g0 ? a.g0[cc] : 0.0, a.g1 ? a.g1[cc] : 0.0, a.scale ? a.scale[cc] : 1.0};
+  int blk = blockIdx.x;
+  if (blk < a.nblk_small) {  // ---- small rows: one lane group per row
+    const int idx = (blk * kWarps + warp) * gpw + gi;
+    if (!lane_ok || idx >= a.n_small) return;
+    const int r = a.small_rows[idx];
+    const int z0 = __ldg(a.rowptr + r), z1 = __ldg(a.rowptr + r + 1);
+    ctx.write(r, z1 - z0, ctx.strided_sum(z0, z1, 0, 1));
+    return;
   }
-  const double g0 = a.g0 ? a.g0[min(c, B - 1)] : 0.0;
-  const double g1 = a.g1 ? a.g1[min(c, B - 1)] : 0.0;
-  const double sc = a.scale ? a.scale[min(c, B - 1)] : 1.0;
-
-  auto write_row = [&](int row, double val) {  // row: tile-local
-    const int r = r0 + row;
-    double o = val;
-    if (a.x) {
-      const double deg = (double)(s_rp[row + 1] - s_rp[row]);
-      o += (g0 + g1 * deg) * a.x[(int64_t)r * a.ldx + c];
-    }
-    a.out[(int64_t)r * a.ldo + c] = sc * o;
-  };
-
-  // did earlier merge items (this or previous tiles) consume nonzeros of row x0?
-  const bool started_mid = lane_ok && (z0 + y0 > s_rp[x0]);
-  bool first = true, held = false;
-  double hold = 0.0, acc = 0.0;
-  int row = x0;
-  if (lane_ok) {
-#pragma unroll
-    for (int p = 0; p < IPT; ++p) {
-      if (y0 + p < y1) {
-        const int z = z0 + y0 + p;
-        while (s_rp[row + 1] <= z) {  // rows (possibly empty) that end before nonzero z
-          if (first && started_mid) { hold = acc; held = true; }
-          else write_row(row, acc);
-          first = false;
-          acc = 0.0;
-          ++row;
-        }
-        acc += v[p];
-      }
-    }
-    while (row < x1) {
-      if (first && started_mid) { hold = acc; held = true; }
-      else write_row(row, acc);
-      first = false;
-      acc = 0.0;
-      ++row;
-    }
-    s_carry[g * B + c] = acc;  // partial of the row open at the group's end (row x1)
-    if (c == 0) { s_crow[g] = x1; s_cdone[g] = (x1 > x0); }
+  blk -= a.nblk_small;
+  if (blk < a.nblk_medium) {  // ---- medium rows: one warp per row
+    const int idx = blk * kWarps + warp;
+    if (idx >= a.n_medium) return;
+    const int r = a.medium_rows[idx];
+    const int z0 = __ldg(a.rowptr + r), z1 = __ldg(a.rowptr + r + 1);
+    const double part = lane_ok ? ctx.strided_sum(z0, z1, gi, gpw) : 0.0;
+    const double sum = group_reduce(part, B, gpw);
+    if (gi == 0) ctx.write(r, z1 - z0, sum);
+    return;
   }
-  __syncthreads();
-
-  if (held) {  // stitch the first completed row with the carries of the preceding groups
-    double sum = hold;
-    for (int gp = g - 1; gp >= 0; --gp) {
-      sum += s_carry[gp * B + c];
-      if (s_cdone[gp]) break;
+  blk -= a.nblk_medium;
+  {  // ---- hub rows: one warp per 1024-nonzero chunk, last chunk of the row reduces in order
+    const int idx = blk * kWarps + warp;
+    if (idx >= a.n_chunks) return;
+    const int4 ch = a.chunks[idx];  // (row, z0, z1, first chunk index of the row)
+    const double part = lane_ok ? ctx.strided_sum(ch.y, ch.z, gi, gpw) : 0.0;
+    const double sum = group_reduce(part, B, gpw);
+    if (gi == 0) a.chunk_part[(int64_t)idx * B + c] = sum;
+    __threadfence();
+    __syncwarp();
+    unsigned ticket = 0;
+    const int z0r = __ldg(a.rowptr + ch.x), z1r = __ldg(a.rowptr + ch.x + 1);
+    const int nch = (z1r - z0r + kHubChunk - 1) / kHubChunk;
+    if (lane == 0) ticket = atomicAdd(a.row_ticket + ch.w, 1u);  // one ticket per hub row
+    ticket = __shfl_sync(0xffffffffu, ticket, 0);
+    if (ticket != (unsigned)(nch - 1)) return;
+    __threadfence();
+    if (gi == 0) {
+      double tot = 0.0;
+      for (int k = 0; k < nch; ++k) tot += __ldcg(a.chunk_part + (int64_t)(ch.w + k) * B + c);
+      ctx.write(ch.x, z1r - z0r, tot);
     }
-    write_row(x0, sum);
+    if (lane == 0) a.row_ticket[ch.w] = 0u;
   }
-  // tile carry-out: the open row at the tile end, accumulated over the trailing groups
-  const int G = groups_per_cta(B);
-  if (lane_ok && g == G - 1) {
-    const int r1 = c1.x;
-    int crow = -1;
-    double sum = 0.0;
-    if (r1 < a.n_loc && c1.y > max(z0, s_rp[nrows])) {
-      crow = r1;
-      for (int gp = G - 1; gp >= 0; --gp) {
-        sum += s_carry[gp * B + c];
-        if (s_cdone[gp]) break;
-      }
-    }
-    a.carry_val[(int64_t)t * B + c] = sum;
-    if (c == 0) a.carry_row[t] = crow;
-  }
-}
-
-// rows spanning several tiles: the first tile of each run adds the run's carries in order
-__global__ void spmv_fixup_kernel(const int32_t* carry_row, const double* carry_val, int num_tiles,
-                                  int B, const double* scale, double* out, int64_t ldo) {
-  const int t = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
-  const int c = threadIdx.x & 31;
-  if (t >= num_tiles || c >= B) return;
-  const int r = carry_row[t];
-  if (r < 0 || (t > 0 && carry_row[t - 1] == r)) return;
-  double sum = 0.0;
-  for (int u = t; u < num_tiles && carry_row[u] == r; ++u) sum += carry_val[(int64_t)u * B + c];
-  const double sc = scale ? scale[c] : 1.0;
-  out[(int64_t)r * ldo + c] += sc * sum;
-}
-
-__global__ void spmv_tiles_kernel(const int32_t* rowptr, int32_t n, int32_t nnz, int T, int2* tiles,
-                                  int num_tiles) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t > num_tiles) return;
-  const int64_t d = min((int64_t)t * T, (int64_t)n + nnz);
-  int64_t lo = max((int64_t)0, d - nnz), hi = min(d, (int64_t)n);
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) >> 1;
-    if ((int64_t)rowptr[mid + 1] <= d - mid - 1) lo = mid + 1;
-    else hi = mid;
-  }
-  tiles[t] = make_int2((int)lo, (int)(d - lo));
 }
 
 }  // namespace
 
-int spmv_tile_items(int B) { return groups_per_cta(B) * ipt_for(B); }
-
-void spmv_tiles(const int32_t* rowptr, int32_t n, int32_t nnz, int tile_items, int2* tiles,
-                int num_tiles, cudaStream_t s) {
-  WL_LAUNCH("spmv_tiles");
-  spmv_tiles_kernel<<<(num_tiles + 1 + 255) / 256, 256, 0, s>>>(rowptr, n, nnz, tile_items, tiles,
-                                                                 num_tiles);
+void spmv(const SpmvArgs& a0, cudaStream_t s) {
+  if (a0.B < 1 || a0.B > kMaxCols) throw Error(1, "spmv: B out of range");
+  SpmvArgs a = a0;
+  const int gpw = 32 / a.B;
+  a.nblk_small = (a.n_small + kWarps * gpw - 1) / (kWarps * gpw);
+  a.nblk_medium = (a.n_medium + kWarps - 1) / kWarps;
+  const int nblk_hub = (a.n_chunks + kWarps - 1) / kWarps;
+  const int grid = a.nblk_small + a.nblk_medium + nblk_hub;
+  if (grid <= 0) return;
+  WL_LAUNCH("spmv_binned");
+  spmv_binned_kernel<<<grid, kThreads, 0, s>>>(a);
   WL_CUDA(cudaGetLastError());
-}
-
-void spmv(const SpmvArgs& a, cudaStream_t s) {
-  if (a.B < 1 || a.B > kMaxCols) throw Error(1, "spmv: B out of range");
-  if (a.tile_items != spmv_tile_items(a.B)) throw Error(1, "spmv: tile size mismatch");
-  if (a.num_tiles <= 0) return;
-  const size_t smem = sizeof(int) * (2 * (size_t)a.tile_items + 2);
-  const int ipt = ipt_for(a.B);
-  {
-    WL_LAUNCH("spmv_merge");
-    if (ipt == 8) spmv_merge_kernel<8><<<a.num_tiles, kThreads, smem, s>>>(a);
-    else if (ipt == 16) spmv_merge_kernel<16><<<a.num_tiles, kThreads, smem, s>>>(a);
-    else spmv_merge_kernel<32><<<a.num_tiles, kThreads, smem, s>>>(a);
-    WL_CUDA(cudaGetLastError());
-  }
-  {
-    WL_LAUNCH("spmv_fixup");
-    spmv_fixup_kernel<<<(a.num_tiles + 7) / 8, 256, 0, s>>>(a.carry_row, a.carry_val, a.num_tiles, a.B,
-                                                            a.scale, a.out, a.ldo);
-    WL_CUDA(cudaGetLastError());
-  }
 }
 
 }  // namespace wl

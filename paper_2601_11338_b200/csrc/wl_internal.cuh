@@ -29,28 +29,28 @@ constexpr int kMaxCols = 32;    // columns per Krylov batch (B)
 constexpr int kMaxKrylov = 64;  // Arnoldi steps per action
 constexpr int kMaxSmallN = 130; // largest dense matrix of the projected-function kernels
 
-// ---------------------------------------------------------------- merge-path Z-SpMV
+// ---------------------------------------------------------------- degree-binned Z-SpMV
 // out[r][c] = scale[c] * ( Σ_{z in row r} y[col[z]][c] + (g0[c] + g1[c] * deg(r)) * x[r][c] )
 // Gathers y rows (ld ldy) for local columns < n_loc, halo rows (ld ldh) for columns >= n_loc.
+constexpr int kSmallMax = 32;    // rows with deg <= 32: one lane group per row
+constexpr int kHubChunk = 1024;  // rows with deg > 1024: split into chunks of 1024 nonzeros
 struct SpmvArgs {
   const int32_t* rowptr;  // n_loc + 1, local offsets
   const int32_t* col;     // nnz, local ids (halo ids >= n_loc)
-  const int2* tiles;      // num_tiles + 1 merge coordinates (row, nz)
-  int num_tiles;
-  int tile_items;
   int32_t n_loc;
+  const int32_t* small_rows; int n_small;
+  const int32_t* medium_rows; int n_medium;
+  const int4* chunks; int n_chunks;  // (row, z0, z1, first chunk index of that row)
+  double* chunk_part;                // n_chunks * B partial sums (scratch)
+  unsigned int* row_ticket;          // n_chunks, zero between launches
+  int nblk_small, nblk_medium;       // filled by spmv()
   const double* y; int64_t ldy;
   const double* yh; int64_t ldh;
   const double* x; int64_t ldx;   // may be null (no diagonal term)
   double* out; int64_t ldo;
-  const double* g0; const double* g1; const double* scale;  // device, B entries (scale may be null)
+  const double* g0; const double* g1; const double* scale;  // device, B entries (null = 0,0,1)
   int B;
-  int32_t* carry_row;  // num_tiles
-  double* carry_val;   // num_tiles * B
 };
-int spmv_tile_items(int B);
-void spmv_tiles(const int32_t* rowptr, int32_t n, int32_t nnz, int tile_items, int2* tiles,
-                int num_tiles, cudaStream_t s);
 void spmv(const SpmvArgs& a, cudaStream_t s);
 
 // ---------------------------------------------------------------- Gram-Schmidt kernels
