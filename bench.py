@@ -138,11 +138,12 @@ def algorithmic_bytes(n, nnz, n_halo, G, K, Bmax, b, n_theta):
         add("spmv_binned", (csr + 2 * blk + 8 * n_halo * B))          # seed 1: gather y + write
         add("spmv_binned", (csr + 3 * blk + 8 * n_halo * B))          # seed 2: + x
         add("spmv_binned", K * (csr + 3 * blk + 8 * n_halo * B))      # Z steps
-        add("gram_proj", vec)                                         # ||u||
+        # DCGS2 step j: dots read q_0..q_{j-1}, p_j and the SpMM output (w's top half IS p_j's
+        # bottom half, read once); update reads the same and writes q_j and p_{j+1}
         for j in range(K):
-            add("gram_proj", (j + 2) * vec)
-            add("gram_update_proj" if j + 1 <= 32 else "gram_update_norm", (j + 3) * vec)
-            add("gram_update_norm", (j + 3) * vec)
+            add("dcgs2_dots", (j + 1.5) * vec)   # (w top re-read from L2/HBM: not algorithmic)
+            add("dcgs2_update", (j + 3.5) * vec)
+        add("dcgs2_dots", (K + 1) * vec)                              # final delayed reorth.
         add("combine", K * blk + blk + 8 * n * b + 8 * n * n_theta)
         add("batch_inputs", 8 * n * b + blk)
     return out

@@ -162,7 +162,7 @@ struct wl_workspace {
   DArr<double> basis, S, Vb, halo_send, halo_recv;
   DArr<double> partials, sums1, sums2, sums3;
   DArr<unsigned int> ticket;
-  DArr<double> H, s_all, n0, comb, scratch;
+  DArr<double> H, s_all, n0, comb, scratch, ref, coef_v, coef_s;
   DArr<int> keff, vcol, tcol;
   DArr<double> colp;  // g0z, g1z, g0s, g1s (kMaxCols each)
   DArr<double> chunk_part;
@@ -286,84 +286,50 @@ void run_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double* 
   do_spmv(op, ws, ws->Vb.p, nullptr, nullptr, nullptr, nullptr, Q0, B, s);
   halo_exchange(op, ws, Q0, B, B, s);
   do_spmv(op, ws, Q0, ws->Vb.p, g0s, g1s, nullptr, Q0 + n * B, B, s);
-  const int grid = gram_grid(L * B, B);
-  GramArgs g{};
-  g.Q = ws->basis.p;
-  g.vstride = vstride;
-  g.len = L;
-  g.B = B;
-  g.s = ws->s_all.p;
-  g.partials = ws->partials.p;
-  g.ticket = ws->ticket.p;
-  g.grid = grid;
-  // ||u||
-  g.nvec = 0;
-  g.wa = Q0;
-  g.wscale = nullptr;
-  g.split = L;
-  g.wb = nullptr;
-  g.sums_out = ws->sums1.p;
-  gram_proj(g, s);
-  allreduce(op, ws->sums1.p, B, s);
-  finalize_norm0(ws->sums1.p, B, ws->n0.p, ws->s_all.p, ws->keff.p, K, s);
+  // a5: Arnoldi with delayed classical Gram-Schmidt (DCGS2): per step one SpMM, one fused dot
+  // pass (single reduction / allreduce) and one fused two-output update pass.
+  WL_CUDA(cudaMemsetAsync(ws->H.p, 0, sizeof(double) * B * (K + 1) * K, s));
+  Dcgs2Args d{};
+  d.Q = ws->basis.p;
+  d.vstride = vstride;
+  d.len = L;
+  d.B = B;
+  d.partials = ws->partials.p;
+  d.sums_out = ws->sums1.p;
+  d.coef_v = ws->coef_v.p;
+  d.coef_s = ws->coef_s.p;
   const double btol = op->opts.breakdown_tol;
-  const int reorth = op->opts.reorth;
   for (int j = 0; j < K; ++j) {
-    double* Qj = ws->basis.p + (int64_t)j * vstride;
-    double* Qn = ws->basis.p + (int64_t)(j + 1) * vstride;
-    // a4: S = s_j (A Qj_bot + μ(μ - d) Qj_top) — bottom half of Z q_j; the top half is q_j,bot
-    halo_exchange(op, ws, Qj + n * B, B, B, s);
-    do_spmv(op, ws, Qj + n * B, Qj, g0z, g1z, ws->s_all.p + (int64_t)j * B, ws->S.p, B, s);
-    // a5: classical Gram-Schmidt (twice)
-    GramArgs w = g;
-    w.nvec = j + 1;
-    w.wa = Qj + n * B;
-    w.wscale = ws->s_all.p + (int64_t)j * B;
-    w.split = n;
-    w.wb = ws->S.p;
-    w.sums_out = ws->sums1.p;
-    gram_proj(w, s);
-    allreduce(op, ws->sums1.p, (size_t)(j + 2) * B, s);
-    if (reorth) {
-      GramArgs u = w;
-      u.wout = Qn;
-      u.sums_in = ws->sums1.p;
-      u.sums_out = ws->sums2.p;
-      if (j + 1 <= 32) {
-        gram_update_proj(u, s);
-      } else {  // unfused fallback for long bases: update, then project
-        u.sums_out = ws->sums3.p;
-        gram_update_norm(u, s);
-        GramArgs p2 = g;
-        p2.nvec = j + 1;
-        p2.wa = Qn;
-        p2.split = L;
-        p2.wscale = nullptr;
-        p2.sums_out = ws->sums2.p;
-        gram_proj(p2, s);
-      }
-      allreduce(op, ws->sums2.p, (size_t)(j + 1) * B, s);
-      GramArgs v = g;
-      v.nvec = j + 1;
-      v.wa = Qn;
-      v.wscale = nullptr;
-      v.split = L;
-      v.wout = Qn;
-      v.sums_in = ws->sums2.p;
-      v.sums_out = ws->sums3.p;
-      gram_update_norm(v, s);
-    } else {
-      GramArgs v = w;
-      v.wout = Qn;
-      v.sums_in = ws->sums1.p;
-      v.sums_out = ws->sums3.p;
-      gram_update_norm(v, s);
-    }
-    allreduce(op, ws->sums3.p, B, s);
-    finalize_step(ws->sums1.p, ws->sums2.p, ws->sums3.p, j, B, K, btol, reorth, ws->s_all.p, ws->H.p,
-                  ws->keff.p, s);
+    double* Pj = ws->basis.p + (int64_t)j * vstride;
+    double* Pn = ws->basis.p + (int64_t)(j + 1) * vstride;
+    // a4: S = A Pj_bot + μ(μ - d) Pj_top — bottom half of Z p_j; its top half is Pj_bot
+    halo_exchange(op, ws, Pj + n * B, B, B, s);
+    do_spmv(op, ws, Pj + n * B, Pj, g0z, g1z, nullptr, ws->S.p, B, s);
+    d.nq = j;
+    d.P = Pj;
+    d.wa = Pj + n * B;
+    d.split = n;
+    d.wb = ws->S.p;
+    dcgs2_dots(d, s);
+    allreduce(op, ws->sums1.p, (size_t)(2 * j + 3) * B, s);
+    dcgs2_coeffs(ws->sums1.p, j, B, K, btol, 0, op->opts.reorth, ws->H.p, ws->ref.p, ws->n0.p, ws->keff.p,
+                 ws->coef_v.p, ws->coef_s.p, s);
+    d.Pnext = Pn;
+    d.accumulate = 0;
+    dcgs2_update(d, s);
   }
-  // a6: y = f_1(H_k) e_1 per column; comb_i = ||u|| y_i s_i
+  {  // delayed reorthogonalisation of p_K completes column K-1 of H
+    d.nq = K;
+    d.P = ws->basis.p + (int64_t)K * vstride;
+    d.wa = nullptr;
+    d.wb = nullptr;
+    d.split = n;
+    dcgs2_dots(d, s);
+    allreduce(op, ws->sums1.p, (size_t)(2 * K + 3) * B, s);
+    dcgs2_coeffs(ws->sums1.p, K, B, K, btol, 1, op->opts.reorth, ws->H.p, ws->ref.p, ws->n0.p, ws->keff.p,
+                 ws->coef_v.p, ws->coef_s.p, s);
+  }
+  // a6: y = f_1(H_k) e_1 per column; comb_i = ||u|| y_i  (q_i stored normalised)
   SmallFArgs f{};
   f.H = ws->H.p;
   f.K = K;
@@ -373,7 +339,7 @@ void run_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double* 
   f.coeffs = op->coeffs_dev.p;
   f.ncoeffs = (int)op->coeffs.size();
   f.n0 = ws->n0.p;
-  f.s = ws->s_all.p;
+  f.s = nullptr;
   f.comb = ws->comb.p;
   f.scratch = ws->scratch.p;
   f.B = B;
@@ -405,8 +371,11 @@ void workspace_alloc(wl_workspace* ws, const wl_operator* op, int max_b) {
   if (op->n_halo > 0) ws->halo_recv.alloc((size_t)op->n_halo * B);
   if (op->n_send > 0) ws->halo_send.alloc((size_t)op->n_send * B);
   const int grid = gram_grid(2 * n * B, B);
-  ws->partials.alloc((size_t)grid * (K + 2) * B);
-  ws->sums1.alloc((size_t)(K + 2) * B);
+  ws->partials.alloc((size_t)grid * (2 * K + 5) * B);
+  ws->ref.alloc(B);
+  ws->coef_v.alloc((size_t)2 * (K + 1) * B);
+  ws->coef_s.alloc((size_t)3 * B);
+  ws->sums1.alloc((size_t)(2 * K + 5) * B);
   ws->sums2.alloc((size_t)(K + 2) * B);
   ws->sums3.alloc((size_t)(K + 2) * B);
   ws->ticket.alloc(1);
@@ -568,12 +537,16 @@ void build_operator(wl_operator* op, const int64_t* rp_in, const int32_t* ci_in,
 }
 
 
+// Outer basis vectors are padded to an even length (16-byte aligned rows for the bulk-copy
+// Gram kernels); the pad entries are zero and never written.
+inline int64_t outer_stride(const wl_operator* op) { return std::max<int64_t>(2, op->n_loc + (op->n_loc & 1)); }
+
 // Outer Arnoldi with CGS2 on unit-stride n-vectors (B = 1), basis ws->oQ (vector 0 preset by the
 // caller), Hessenberg ws->oH (layout (m+1) x m), scales ws->os, ||P_0|| in ws->on0.
 // `apply(P̃_j, out)` writes the operator applied to the UNNORMALISED basis vector P̃_j.
 template <class Apply>
 void outer_arnoldi(const wl_operator* op, wl_workspace* ws, int m, Apply&& apply, cudaStream_t s) {
-  const int64_t n = op->n_loc;
+  const int64_t n = outer_stride(op);
   WL_CUDA(cudaMemsetAsync(ws->oH.p, 0, sizeof(double) * (m + 1) * m, s));
   GramArgs g{};
   g.Q = ws->oQ.p;
@@ -634,11 +607,14 @@ void outer_arnoldi(const wl_operator* op, wl_workspace* ws, int m, Apply&& apply
   }
 }
 
+
 void outer_alloc(const wl_operator* op, wl_workspace* ws, int m, int nt) {
-  const int64_t n = op->n_loc;
+  const int64_t np = outer_stride(op);
   if (ws->kout_alloc >= m && ws->otau.n >= (size_t)nt) return;
-  ws->oQ.alloc((size_t)(m + 1) * std::max<int64_t>(1, n));
-  ws->ow.alloc((size_t)std::max<int64_t>(1, n));
+  ws->oQ.alloc((size_t)(m + 1) * np);
+  ws->ow.alloc((size_t)np);
+  WL_CUDA(cudaMemset(ws->oQ.p, 0, sizeof(double) * (m + 1) * np));
+  WL_CUDA(cudaMemset(ws->ow.p, 0, sizeof(double) * np));
   ws->oH.alloc((size_t)(m + 1) * m);
   ws->os.alloc(m + 1);
   ws->on0.alloc(1);
@@ -650,7 +626,7 @@ void outer_alloc(const wl_operator* op, wl_workspace* ws, int m, int nt) {
   ws->oY.alloc((size_t)std::max(1, nt) * (m + 1));
   ws->oscratch.alloc((size_t)std::max(1, nt) * 9 * kMaxSmallN * kMaxSmallN);
   ws->kout_alloc = m;
-  const size_t need = (size_t)gram_grid(n, 1) * (m + 2);
+  const size_t need = (size_t)gram_grid(np, 1) * (m + 2);
   if (ws->partials.n < need) ws->partials.alloc(need);
   if (!ws->ticket.p) {
     ws->ticket.alloc(1);
@@ -973,7 +949,7 @@ wl_status wl_diffuse(const wl_operator* op, int32_t theta_index, int32_t nt, con
     f.tau = ws->otau.p;
     f.nprob = nt;
     small_f(f, s);
-    lanczos_combine(ws->oQ.p, n, m + 1, n, ws->oY.p, nt, 1.0, X, ldx, s);
+    lanczos_combine(ws->oQ.p, outer_stride(op), m + 1, n, ws->oY.p, nt, 1.0, X, ldx, s);
   });
 }
 

@@ -8,256 +8,342 @@
 //
 // Per Arnoldi step (w = Z q_j, nvec = j+1):
 //   gram_proj        sums1_i = Q_i . w,  sums1_nvec = w . w               (1 read of the basis)
-//   gram_update_proj w' = w - Σ s_i² sums1_i Q_i ;  sums2_i = Q_i . w'    (1 read; Q_i kept in
+//   gram_update_proj w' = w - Σ s_i² sums1_i Q_i ;  sums2_i = Q_i . w'    (1 read: Q_i stays in
 //                    registers between the update and the second projection)
 //   gram_update_norm w'' = w' - Σ s_i² sums2_i Q_i ; sums3 = w'' . w''    (1 read)
-// Reductions are deterministic: per-CTA partials, then the last CTA to finish (atomic ticket)
-// sums the partials in CTA order.  Threads own one column each (block = B * m threads and
-// a grid-stride that is a multiple of B), so column reductions never mix columns.
+//
+// These are pure HBM streams of nvec+2 vectors.  Design (measured, tools/stream_bench.cu on
+// B200: register streaming of 32 concurrent vectors reaches 7.3 TB/s, a 1-CTA/SM bulk-TMA ring is
+// capped near 4.6 TB/s by the bytes a 227 KB shared memory can keep in flight for 32 streams):
+// the basis vectors are split across thread groups — group g owns vectors [8g, 8g+8) — so a
+// thread holds at most 8 accumulators and 8 x U loads in flight at full occupancy.  Update
+// kernels combine the groups' partial sums Σ c_i Q_i with warp shuffles.  Threads own one column (slot % B, slots a multiple of B), so column
+// reductions never mix columns.  Reductions are deterministic: per-CTA partials, then a reduce kernel
+// sums them in a fixed order.
 #include "wl_internal.cuh"
+
 #include <algorithm>
+#include <cstdlib>
 
 namespace wl {
 namespace {
 
-inline int gram_block(int B) { return B * std::max(1, 256 / B); }
+constexpr int kVG = 8;             // basis vectors per thread group
+constexpr int kMaxGroups = 4;      // => <= 32 vectors per launch (larger sets are tiled)
+constexpr int kMaxVecPerLaunch = kVG * kMaxGroups;
+constexpr int kBS = 256;
 
-// Block-reduce per-thread values v[0..NV) (only the first nv meaningful) by column and write
-// this CTA's partial sums to partials[blockIdx.x * nout + i*B + c] (i < nv).
-template <int NV>
-__device__ inline void block_partials(const double (&v)[NV], int nv, int B, int nout,
-                                      double* partials, double* red /* 8 * blockDim */) {
-  const int bs = blockDim.x, tid = threadIdx.x, m = bs / B;
+inline int groups_for(int nvec) { return std::max(1, (nvec + kVG - 1) / kVG); }
+
+// sums_out[ic] = Σ_cta partials[ic * G + cta]: one warp per output, lanes stride over the CTAs
+// (coalesced), fixed-order shuffle tree — deterministic for a given grid.
+__global__ void reduce_partials_kernel(const double* partials, int nout, int G, double* sums_out) {
+  const int ic = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (ic >= nout) return;
+  const double* p = partials + (int64_t)ic * G;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int g = lane;
+  for (; g + 96 < G; g += 128) {
+    s0 += __ldcg(p + g);
+    s1 += __ldcg(p + g + 32);
+    s2 += __ldcg(p + g + 64);
+    s3 += __ldcg(p + g + 96);
+  }
+  for (; g < G; g += 32) s0 += __ldcg(p + g);
+  double v = (s0 + s1) + (s2 + s3);
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  if (lane == 0) sums_out[ic] = v;
+}
+
+// MODE 0: proj, 1: update_proj, 2: update_norm.
+//   block = ES slots x NG groups, interleaved: thread t -> group g = t % NG, slot = t / NG, so the
+//   NG groups of a slot are adjacent lanes of one warp and combine by __shfl_xor (an exact,
+//   commutative tree: every lane gets bitwise the same sum).  No barrier in the streaming loop.
+template <int MODE, int U>
+__global__ void __launch_bounds__(kBS) gram_vs_kernel(GramArgs a, int ES, int NG) {
+  __shared__ double red[(kVG + 1) * kBS];  // per-thread accumulators for the block reduce
+  const int B = a.B, tid = threadIdx.x;
+  const int g = tid % NG, slot = tid / NG, c = slot % B;
+  const unsigned mask = __activemask();
+  const int nvec = a.nvec, i0 = g * kVG;
+  const int nv_g = max(0, min(kVG, nvec - i0));
+  const int64_t total = a.len * B, splitE = a.split * B;
+  const double wsc = a.wscale ? a.wscale[c] : 1.0;
+  double cf[kVG];
 #pragma unroll
-  for (int i0 = 0; i0 < NV; i0 += 8) {
-    if (i0 < nv) {
+  for (int j = 0; j < kVG; ++j) {
+    cf[j] = 0.0;
+    if (MODE != 0 && j < nv_g) {
+      const double si = a.s[(i0 + j) * B + c];
+      cf[j] = si * si * a.sums_in[(i0 + j) * B + c];
+    }
+  }
+  double acc[kVG];
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (i0 + q < NV) red[q * bs + tid] = v[(i0 + q < NV) ? i0 + q : 0];
-      __syncthreads();
-      if (tid < 8 * B) {
-        const int q = tid / B, c = tid - q * B;
-        if (i0 + q < nv) {
-          double s = 0.0;
-          for (int k = 0; k < m; ++k) s += red[q * bs + c + k * B];
-          partials[(int64_t)blockIdx.x * nout + (i0 + q) * B + c] = s;
+  for (int j = 0; j < kVG; ++j) acc[j] = 0.0;
+  double accw = 0.0;  // w.w (proj) or w''.w'' (update_norm), group 0 only
+  const double* Qg = a.Q + (int64_t)i0 * a.vstride;
+  const int64_t step = (int64_t)gridDim.x * ES * U;
+  for (int64_t b0 = (int64_t)blockIdx.x * ES * U; b0 < total; b0 += step) {  // block-uniform bound
+    double w[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = b0 + slot + (int64_t)u * ES;
+      w[u] = 0.0;
+      if (e < total) {
+        if (MODE == 0) w[u] = e < splitE ? wsc * __ldg(a.wa + e) : __ldg(a.wb + (e - splitE));
+        else w[u] = e < splitE ? wsc * a.wa[e] : a.wb[e - splitE];  // wa may alias wout
+      }
+    }
+    double q[kVG][U];
+#pragma unroll
+    for (int j = 0; j < kVG; ++j)
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t e = b0 + slot + (int64_t)u * ES;
+        q[j][u] = (j < nv_g && e < total) ? __ldg(Qg + j * a.vstride + e) : 0.0;
+      }
+    if (MODE == 0) {
+#pragma unroll
+      for (int j = 0; j < kVG; ++j)
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc[j] += q[j][u] * w[u];
+      if (g == 0) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) accw += w[u] * w[u];
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        double p = 0.0;
+#pragma unroll
+        for (int j = 0; j < kVG; ++j) p += cf[j] * q[j][u];
+        for (int off = 1; off < NG; off <<= 1) p += __shfl_xor_sync(mask, p, off);
+        w[u] -= p;  // w' = w - Σ_i c_i Q_i
+        const int64_t e = b0 + slot + (int64_t)u * ES;
+        if (g == 0 && e < total) {
+          a.wout[e] = w[u];
+          if (MODE == 2) accw += w[u] * w[u];
         }
       }
-      __syncthreads();
-    }
-  }
-}
-
-// Last CTA: sums_out[ic] = Σ_cta partials[cta * nout + ic] (fixed order), then reset ticket.
-__device__ inline void last_block_reduce(const double* partials, int nout, double* sums_out,
-                                         unsigned int* ticket) {
-  __shared__ bool am_last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) am_last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
-  __syncthreads();
-  if (!am_last) return;
-  __threadfence();
-  const int G = gridDim.x;
-  for (int ic = threadIdx.x; ic < nout; ic += blockDim.x) {
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    int g = 0;
-    for (; g + 3 < G; g += 4) {
-      s0 += __ldcg(partials + (int64_t)(g + 0) * nout + ic);
-      s1 += __ldcg(partials + (int64_t)(g + 1) * nout + ic);
-      s2 += __ldcg(partials + (int64_t)(g + 2) * nout + ic);
-      s3 += __ldcg(partials + (int64_t)(g + 3) * nout + ic);
-    }
-    for (; g < G; ++g) s0 += __ldcg(partials + (int64_t)g * nout + ic);
-    sums_out[ic] = (s0 + s1) + (s2 + s3);
-  }
-  if (threadIdx.x == 0) *ticket = 0u;
-}
-
-__device__ inline double load_w(const GramArgs& a, int64_t e, int64_t splitE, double wsc) {
-  return e < splitE ? wsc * __ldg(a.wa + e) : __ldg(a.wb + (e - splitE));
-}
-
-// Each thread owns column c = tid % B and visits U elements per iteration, e + u*bs
-// (u < U): all in column c, each a coalesced warp access, U independent loads per basis vector.
-template <int JT, int U>
-__global__ void __launch_bounds__(256) gram_proj_kernel(GramArgs a) {
-  __shared__ double red[8 * 256];
-  const int B = a.B, tid = threadIdx.x, bs = blockDim.x, c = tid % B;
-  const int64_t total = a.len * B, splitE = a.split * B;
-  const double wsc = a.wscale ? a.wscale[c] : 1.0;
-  const int nvec = a.nvec;
-  double acc[JT + 1];
+      if (MODE == 1) {
 #pragma unroll
-  for (int i = 0; i <= JT; ++i) acc[i] = 0.0;
-  const int64_t step = (int64_t)gridDim.x * bs * U;
-  for (int64_t base = (int64_t)blockIdx.x * bs * U + tid; base < total; base += step) {
-    double w[U];
+        for (int j = 0; j < kVG; ++j)
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t e = base + (int64_t)u * bs;
-      w[u] = e < total ? load_w(a, e, splitE, wsc) : 0.0;
-      acc[JT] += w[u] * w[u];
-    }
-    double q[JT][U];  // all loads of this iteration in flight before any FMA
-    const double* qp = a.Q + base;
-#pragma unroll
-    for (int i = 0; i < JT; ++i) {
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        q[i][u] = (i < nvec && base + (int64_t)u * bs < total) ? __ldg(qp + (int64_t)u * bs) : 0.0;
-      qp += a.vstride;
-    }
-#pragma unroll
-    for (int i = 0; i < JT; ++i) {
-      double sum = 0.0;
-#pragma unroll
-      for (int u = 0; u < U; ++u) sum += q[i][u] * w[u];
-      acc[i] += sum;
-    }
-  }
-  double v[JT + 1];
-#pragma unroll
-  for (int i = 0; i <= JT; ++i) v[i] = (i < nvec) ? acc[i] : (i == nvec ? acc[JT] : 0.0);
-  const int nout = (nvec + 1) * B;
-  block_partials<JT + 1>(v, nvec + 1, B, nout, a.partials, red);
-  last_block_reduce(a.partials, nout, a.sums_out, a.ticket);
-}
-
-template <int JT, int U>
-__global__ void __launch_bounds__(256) gram_update_proj_kernel(GramArgs a) {
-  __shared__ double red[8 * 256];
-  __shared__ double coef[JT * kMaxCols];
-  const int B = a.B, tid = threadIdx.x, bs = blockDim.x, c = tid % B;
-  for (int idx = tid; idx < a.nvec * B; idx += bs) {
-    const double si = a.s[idx];
-    coef[idx] = si * si * a.sums_in[idx];
-  }
-  __syncthreads();
-  const int64_t total = a.len * B, splitE = a.split * B;
-  const double wsc = a.wscale ? a.wscale[c] : 1.0;
-  const int nvec = a.nvec;
-  double acc[JT];
-#pragma unroll
-  for (int i = 0; i < JT; ++i) acc[i] = 0.0;
-  const int64_t step = (int64_t)gridDim.x * bs * U;
-  for (int64_t base = (int64_t)blockIdx.x * bs * U + tid; base < total; base += step) {
-    double q[JT][U];
-    const double* qp = a.Q + base;
-#pragma unroll
-    for (int i = 0; i < JT; ++i) {
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        q[i][u] = (i < nvec && base + (int64_t)u * bs < total) ? __ldg(qp + (int64_t)u * bs) : 0.0;
-      qp += a.vstride;
-    }
-    double w[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t e = base + (int64_t)u * bs;
-      w[u] = e < total ? load_w(a, e, splitE, wsc) : 0.0;
-    }
-#pragma unroll
-    for (int i = 0; i < JT; ++i)
-      if (i < nvec) {
-        const double ci = coef[i * B + c];
-#pragma unroll
-        for (int u = 0; u < U; ++u) w[u] -= ci * q[i][u];
+          for (int u = 0; u < U; ++u) acc[j] += q[j][u] * w[u];
       }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t e = base + (int64_t)u * bs;
-      if (e < total) a.wout[e] = w[u];
-    }
-#pragma unroll
-    for (int i = 0; i < JT; ++i) {
-      double sum = 0.0;
-#pragma unroll
-      for (int u = 0; u < U; ++u) sum += q[i][u] * w[u];
-      acc[i] += sum;
     }
   }
-  const int nout = nvec * B;
-  block_partials<JT>(acc, nvec, B, nout, a.partials, red);
-  last_block_reduce(a.partials, nout, a.sums_out, a.ticket);
+  // block reduce by (vector, column): out index i*B + c; i = nvec is the w.w slot (proj)
+#pragma unroll
+  for (int j = 0; j < kVG; ++j) red[j * kBS + tid] = acc[j];
+  red[kVG * kBS + tid] = accw;
+  __syncthreads();
+  const int nrows = (MODE == 0) ? nvec + 1 : (MODE == 1 ? nvec : 1);
+  const int nout = nrows * B;
+  const int per = ES / B;
+  for (int idx = tid; idx < nout; idx += blockDim.x) {
+    const int i = idx / B, cc = idx - i * B;
+    const bool is_w = (MODE == 0 && i == nvec) || MODE == 2;
+    const int gg = is_w ? 0 : i / kVG, j = is_w ? kVG : i % kVG;
+    double sum = 0.0;
+    for (int k = 0; k < per; ++k) sum += red[j * kBS + (cc + k * B) * NG + gg];
+    a.partials[(int64_t)idx * gridDim.x + blockIdx.x] = sum;
+  }
 }
 
-template <int JT, int U>
-__global__ void __launch_bounds__(256) gram_update_norm_kernel(GramArgs a) {
-  __shared__ double red[8 * 256];
-  __shared__ double coef[JT * kMaxCols];
-  const int B = a.B, tid = threadIdx.x, bs = blockDim.x, c = tid % B;
-  for (int idx = tid; idx < a.nvec * B; idx += bs) {
-    const double si = a.s[idx];
-    coef[idx] = si * si * a.sums_in[idx];
-  }
-  __syncthreads();
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
+template <int MODE>
+void launch_vs(GramArgs a, cudaStream_t s) {
+  static const int U = env_int("WL_GRAM_U", 2);           // experiment knobs (defaults tuned)
+  static const int target = env_int("WL_GRAM_BS", 256);
+  int NG = groups_for(a.nvec);
+  if (NG == 3) NG = 4;
+  const int ES = std::max(a.B, (target / NG) / a.B * a.B);
+  const int64_t total = a.len * a.B;
+  const int64_t items = (total + (int64_t)ES * U - 1) / ((int64_t)ES * U);
+  a.grid = (int)std::max<int64_t>(1, std::min<int64_t>(items, gram_grid(total, a.B)));
+  if (U == 1) gram_vs_kernel<MODE, 1><<<a.grid, ES * NG, 0, s>>>(a, ES, NG);
+  else if (U == 4) gram_vs_kernel<MODE, 4><<<a.grid, ES * NG, 0, s>>>(a, ES, NG);
+  else gram_vs_kernel<MODE, 2><<<a.grid, ES * NG, 0, s>>>(a, ES, NG);
+  WL_CUDA(cudaGetLastError());
+  const int nout = (MODE == 0 ? a.nvec + 1 : (MODE == 1 ? a.nvec : 1)) * a.B;
+  note_launch("gram_reduce");  // second kernel of this launch scope (counted, timed with it)
+  reduce_partials_kernel<<<(nout + 7) / 8, 256, 0, s>>>(a.partials, nout, a.grid, a.sums_out);
+  WL_CUDA(cudaGetLastError());
+}
+
+// ---- DCGS2 passes ------------------------------------------------------------------------
+// Same thread layout as gram_vs_kernel.  Pass B handles PAIRS (e, e + nB) of a Z vector (top and
+// bottom half, same column): w = Z p_j has top half = bottom half of p_j, so the pair reads
+// p_b = P[e + nB] once and uses it both as p (bottom) and as w (top), and the in-place overwrite
+// of P (p_j -> q_j) is race-free: only the owner thread of the pair reads or writes P[e] and
+// P[e + nB].
+// pass A (read only, so no pairing needed): each thread takes U adjacent element chunks
+// (e, e + ES, ...) — measured faster than the (e, e + nB) pairs; w = (p_bot ; S) is read from
+// its two sources.  Per thread 2 x 8 dot accumulators (q_i.p, q_i.w) for its group's vectors;
+// group 0 also accumulates α, β, γ.
+template <int U>
+__global__ void __launch_bounds__(kBS) dcgs2_dots_kernel(Dcgs2Args a, int ES, int NG) {
+  __shared__ double red[(2 * kVG + 3) * kBS];
+  const int B = a.B, tid = threadIdx.x;
+  const int g = tid % NG, slot = tid / NG;
+  const int nq = a.nq, i0 = g * kVG;
+  const int nv_g = max(0, min(kVG, nq - i0));
+  const bool has_w = a.wa != nullptr;
   const int64_t total = a.len * B, splitE = a.split * B;
-  const double wsc = a.wscale ? a.wscale[c] : 1.0;
-  const int nvec = a.nvec;
-  double acc[1] = {0.0};
-  const int64_t step = (int64_t)gridDim.x * bs * U;
-  for (int64_t base = (int64_t)blockIdx.x * bs * U + tid; base < total; base += step) {
-    double w[U];
+  double acc[2 * kVG + 3];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {  // may alias wout: plain loads
-      const int64_t e = base + (int64_t)u * bs;
-      w[u] = e < total ? (e < splitE ? wsc * a.wa[e] : a.wb[e - splitE]) : 0.0;
-    }
-    double q[JT][U];
-    const double* qp = a.Q + base;
-#pragma unroll
-    for (int i = 0; i < JT; ++i) {
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        q[i][u] = (i < nvec && base + (int64_t)u * bs < total) ? __ldg(qp + (int64_t)u * bs) : 0.0;
-      qp += a.vstride;
-    }
-#pragma unroll
-    for (int i = 0; i < JT; ++i) {
-      const double ci = (i < nvec) ? coef[i * B + c] : 0.0;
-#pragma unroll
-      for (int u = 0; u < U; ++u) w[u] -= ci * q[i][u];
-    }
+  for (int j = 0; j < 2 * kVG + 3; ++j) acc[j] = 0.0;
+  const double* Qg = a.Q + (int64_t)i0 * a.vstride;
+  const int64_t step = (int64_t)gridDim.x * ES * U;
+  for (int64_t b0 = (int64_t)blockIdx.x * ES * U; b0 < total; b0 += step) {
+    double p[U], w[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int64_t e = base + (int64_t)u * bs;
+      const int64_t e = b0 + slot + (int64_t)u * ES;
+      p[u] = 0.0;
+      w[u] = 0.0;
       if (e < total) {
-        a.wout[e] = w[u];
-        acc[0] += w[u] * w[u];
+        p[u] = __ldg(a.P + e);
+        if (has_w) w[u] = e < splitE ? __ldg(a.wa + e) : __ldg(a.wb + (e - splitE));
+      }
+    }
+    double q[kVG][U];
+#pragma unroll
+    for (int j = 0; j < kVG; ++j)
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t e = b0 + slot + (int64_t)u * ES;
+        q[j][u] = (j < nv_g && e < total) ? __ldg(Qg + j * a.vstride + e) : 0.0;
+      }
+#pragma unroll
+    for (int j = 0; j < kVG; ++j)
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        acc[2 * j] += q[j][u] * p[u];
+        acc[2 * j + 1] += q[j][u] * w[u];
+      }
+    if (g == 0) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        acc[2 * kVG] += p[u] * p[u];
+        acc[2 * kVG + 1] += p[u] * w[u];
+        acc[2 * kVG + 2] += w[u] * w[u];
       }
     }
   }
-  const int nout = B;
-  block_partials<1>(acc, 1, B, nout, a.partials, red);
-  last_block_reduce(a.partials, nout, a.sums_out, a.ticket);
+#pragma unroll
+  for (int j = 0; j < 2 * kVG + 3; ++j) red[j * kBS + tid] = acc[j];
+  __syncthreads();
+  const int nout = (2 * nq + 3) * B;
+  const int per = ES / B;
+  for (int idx = tid; idx < nout; idx += blockDim.x) {
+    const int r = idx / B, cc = idx - r * B;
+    int gg, jj;
+    if (r < 2 * nq) { const int i = r / 2; gg = i / kVG; jj = 2 * (i % kVG) + (r & 1); }
+    else { gg = 0; jj = 2 * kVG + (r - 2 * nq); }
+    double sum = 0.0;
+    for (int k = 0; k < per; ++k) sum += red[jj * kBS + (cc + k * B) * NG + gg];
+    a.partials[(int64_t)idx * gridDim.x + blockIdx.x] = sum;
+  }
+}
+
+// pass B: group partial sums Σ cq_i q_i and Σ cp_i q_i combined by __shfl_xor; group 0 writes.
+__global__ void __launch_bounds__(kBS) dcgs2_update_kernel(Dcgs2Args a, int ES, int NG) {
+  const int B = a.B, tid = threadIdx.x;
+  const int g = tid % NG, slot = tid / NG, c = slot % B;
+  const unsigned mask = __activemask();
+  const int nq = a.nq, i0 = g * kVG;
+  const int nv_g = max(0, min(kVG, nq - i0));
+  const int64_t half = a.split * B;
+  double cq[kVG], cp[kVG];
+#pragma unroll
+  for (int j = 0; j < kVG; ++j) {
+    cq[j] = j < nv_g ? a.coef_v[(2 * (i0 + j)) * B + c] : 0.0;
+    cp[j] = j < nv_g ? a.coef_v[(2 * (i0 + j) + 1) * B + c] : 0.0;
+  }
+  const double cq_p = a.coef_s[c], cp_p = a.coef_s[B + c], cp_w = a.coef_s[2 * B + c];
+  const bool dead = !a.accumulate && cq_p == 0.0;  // broken-down column: exact zeros
+  const double* Qg = a.Q + (int64_t)i0 * a.vstride;
+  const int64_t step = (int64_t)gridDim.x * ES;
+  for (int64_t b0 = (int64_t)blockIdx.x * ES; b0 < half; b0 += step) {
+    const int64_t e = b0 + slot;
+    const bool ok = e < half;
+    double q[kVG][2];
+#pragma unroll
+    for (int j = 0; j < kVG; ++j) {
+      q[j][0] = (j < nv_g && ok) ? __ldg(Qg + j * a.vstride + e) : 0.0;
+      q[j][1] = (j < nv_g && ok) ? __ldg(Qg + j * a.vstride + e + half) : 0.0;
+    }
+    double bq[2] = {0.0, 0.0}, bp[2] = {0.0, 0.0};
+    if (g == 0 && ok) {
+      if (a.accumulate) {
+        bq[0] = a.P[e];
+        bq[1] = a.P[e + half];
+        bp[0] = a.Pnext[e];
+        bp[1] = a.Pnext[e + half];
+      } else {
+        const double pt = a.P[e], pb = a.P[e + half];
+        const double wb = a.wb[e];  // w = (p_b ; S)
+        bq[0] = cq_p * pt;
+        bq[1] = cq_p * pb;
+        bp[0] = cp_w * pb + cp_p * pt;
+        bp[1] = cp_w * wb + cp_p * pb;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      double sq = 0.0, sp = 0.0;
+#pragma unroll
+      for (int j = 0; j < kVG; ++j) {
+        sq += cq[j] * q[j][u];
+        sp += cp[j] * q[j][u];
+      }
+      for (int off = 1; off < NG; off <<= 1) {
+        sq += __shfl_xor_sync(mask, sq, off);
+        sp += __shfl_xor_sync(mask, sp, off);
+      }
+      bq[u] += sq;
+      bp[u] += sp;
+    }
+    if (g == 0 && ok) {
+      a.P[e] = dead ? 0.0 : bq[0];
+      a.P[e + half] = dead ? 0.0 : bq[1];
+      a.Pnext[e] = dead ? 0.0 : bp[0];
+      a.Pnext[e + half] = dead ? 0.0 : bp[1];
+    }
+  }
+}
+
+inline void vs_shape(int B, int nvec, int& ES, int& NG) {
+  static const int target = env_int("WL_GRAM_BS", 256);
+  NG = groups_for(nvec);
+  if (NG == 3) NG = 4;
+  ES = std::max(B, (target / NG) / B * B);
 }
 
 }  // namespace
 
 int gram_grid(int64_t elems, int B) {
-  const int bs = gram_block(B);
-  const int64_t blocks = (elems + 4 * bs - 1) / (4 * bs);
-  return (int)std::max<int64_t>(1, std::min<int64_t>(blocks, 148 * 4));
+  (void)elems;
+  (void)B;
+  return 148 * 6;  // enough resident CTAs for latency hiding; partial buffers are sized for this
 }
 
-#define WL_GRAM_DISPATCH(KERNEL, NV, ...)                                                   \
-  do {                                                                                      \
-    const int bs_ = gram_block(a.B);                                                        \
-    if ((NV) <= 8) KERNEL<8, 4><<<a.grid, bs_, 0, s>>>(__VA_ARGS__);                        \
-    else if ((NV) <= 16) KERNEL<16, 4><<<a.grid, bs_, 0, s>>>(__VA_ARGS__);                 \
-    else if ((NV) <= 32) KERNEL<32, 2><<<a.grid, bs_, 0, s>>>(__VA_ARGS__);                 \
-    else KERNEL<64, 1><<<a.grid, bs_, 0, s>>>(__VA_ARGS__);                                 \
-  } while (0)
-
-// Bases longer than 64 vectors (outer diffusion Lanczos) are processed in tiles of 64: tile
-// [i0, i1) writes its sums at sums_out + i0*B; its trailing w.w slot is overwritten by the next
-// tile, and the last tile leaves w.w at index nvec.
+// Bases longer than 32 vectors are processed in tiles of 32: tile [i0, i1) writes its sums at
+// sums_out + i0*B; its trailing w.w slot is overwritten by the next tile, and the last tile
+// leaves w.w at index nvec.
 void gram_proj(GramArgs a, cudaStream_t s) {
-  if (a.nvec > 64) {
-    for (int i0 = 0; i0 < a.nvec; i0 += 64) {
+  if (a.nvec > kMaxVecPerLaunch) {
+    for (int i0 = 0; i0 < a.nvec; i0 += kMaxVecPerLaunch) {
       GramArgs t = a;
-      t.nvec = std::min(64, a.nvec - i0);
+      t.nvec = std::min(kMaxVecPerLaunch, a.nvec - i0);
       t.Q = a.Q + (int64_t)i0 * a.vstride;
       t.sums_out = a.sums_out + (int64_t)i0 * a.B;
       gram_proj(t, s);
@@ -265,25 +351,20 @@ void gram_proj(GramArgs a, cudaStream_t s) {
     return;
   }
   WL_LAUNCH("gram_proj");
-  WL_GRAM_DISPATCH(gram_proj_kernel, a.nvec, a);
-  WL_CUDA(cudaGetLastError());
+  launch_vs<0>(a, s);
 }
 
 void gram_update_proj(GramArgs a, cudaStream_t s) {
-  if (a.nvec > 32) throw Error(1, "gram_update_proj: nvec > 32 (use the unfused path)");
+  if (a.nvec > kMaxVecPerLaunch) throw Error(1, "gram_update_proj: nvec > 32 (use the unfused path)");
   WL_LAUNCH("gram_update_proj");
-  const int bs_ = gram_block(a.B);
-  if (a.nvec <= 8) gram_update_proj_kernel<8, 4><<<a.grid, bs_, 0, s>>>(a);
-  else if (a.nvec <= 16) gram_update_proj_kernel<16, 4><<<a.grid, bs_, 0, s>>>(a);
-  else gram_update_proj_kernel<32, 2><<<a.grid, bs_, 0, s>>>(a);
-  WL_CUDA(cudaGetLastError());
+  launch_vs<1>(a, s);
 }
 
 void gram_update_norm(GramArgs a, cudaStream_t s) {
-  if (a.nvec > 64) {  // tiles of 64 basis vectors; tiles after the first update wout in place
-    for (int i0 = 0; i0 < a.nvec; i0 += 64) {
+  if (a.nvec > kMaxVecPerLaunch) {  // tiles of 32 vectors; tiles after the first update wout in place
+    for (int i0 = 0; i0 < a.nvec; i0 += kMaxVecPerLaunch) {
       GramArgs t = a;
-      t.nvec = std::min(64, a.nvec - i0);
+      t.nvec = std::min(kMaxVecPerLaunch, a.nvec - i0);
       t.Q = a.Q + (int64_t)i0 * a.vstride;
       t.s = a.s + (int64_t)i0 * a.B;
       t.sums_in = a.sums_in + (int64_t)i0 * a.B;
@@ -293,7 +374,57 @@ void gram_update_norm(GramArgs a, cudaStream_t s) {
     return;
   }
   WL_LAUNCH("gram_update_norm");
-  WL_GRAM_DISPATCH(gram_update_norm_kernel, a.nvec, a);
+  launch_vs<2>(a, s);
+}
+
+// pass A for nq <= 32 per launch; longer bases tile the vectors: tile [i0, i1) writes its a/b
+// pairs at offset 2*i0 and its trailing α/β/γ are overwritten by the next tile.
+void dcgs2_dots(Dcgs2Args a, cudaStream_t s) {
+  if (a.nq > kMaxVecPerLaunch) {
+    for (int i0 = 0; i0 < a.nq; i0 += kMaxVecPerLaunch) {
+      Dcgs2Args t = a;
+      t.nq = std::min(kMaxVecPerLaunch, a.nq - i0);
+      t.Q = a.Q + (int64_t)i0 * a.vstride;
+      t.sums_out = a.sums_out + (int64_t)2 * i0 * a.B;
+      dcgs2_dots(t, s);
+    }
+    return;
+  }
+  WL_LAUNCH("dcgs2_dots");
+  if (a.len != 2 * a.split) throw Error(1, "dcgs2: vectors must be stacked halves (len = 2 split)");
+  int ES, NG;
+  vs_shape(a.B, a.nq, ES, NG);
+  const int64_t total = a.len * a.B;
+  const int64_t items = (total + (int64_t)ES * 2 - 1) / ((int64_t)ES * 2);
+  a.grid = (int)std::max<int64_t>(1, std::min<int64_t>(items, gram_grid(total, a.B)));
+  dcgs2_dots_kernel<2><<<a.grid, ES * NG, 0, s>>>(a, ES, NG);
+  WL_CUDA(cudaGetLastError());
+  const int nout = (2 * a.nq + 3) * a.B;
+  note_launch("gram_reduce");
+  reduce_partials_kernel<<<(nout + 7) / 8, 256, 0, s>>>(a.partials, nout, a.grid, a.sums_out);
+  WL_CUDA(cudaGetLastError());
+}
+
+void dcgs2_update(Dcgs2Args a, cudaStream_t s) {
+  if (a.nq > kMaxVecPerLaunch) {
+    for (int i0 = 0; i0 < a.nq; i0 += kMaxVecPerLaunch) {
+      Dcgs2Args t = a;
+      t.nq = std::min(kMaxVecPerLaunch, a.nq - i0);
+      t.Q = a.Q + (int64_t)i0 * a.vstride;
+      t.coef_v = a.coef_v + (int64_t)2 * i0 * a.B;
+      t.accumulate = i0 > 0 ? 1 : a.accumulate;
+      dcgs2_update(t, s);
+    }
+    return;
+  }
+  WL_LAUNCH("dcgs2_update");
+  if (a.len != 2 * a.split) throw Error(1, "dcgs2: vectors must be stacked halves (len = 2 split)");
+  int ES, NG;
+  vs_shape(a.B, a.nq, ES, NG);
+  const int64_t half = a.split * a.B;
+  const int64_t items = (half + ES - 1) / ES;
+  a.grid = (int)std::max<int64_t>(1, std::min<int64_t>(items, gram_grid(half, a.B)));
+  dcgs2_update_kernel<<<a.grid, ES * NG, 0, s>>>(a, ES, NG);
   WL_CUDA(cudaGetLastError());
 }
 

@@ -142,6 +142,95 @@ __global__ void setup_chunk_kernel(const double* mu, int gstart, int b, int B, d
   tcol[c] = g / b;
 }
 
+// ---- DCGS2 Arnoldi bookkeeping (one thread per Krylov column) -----------------------------
+// Delayed reorthogonalisation (Świrydowicz et al. 2021; Bielich et al. 2022), derived for the
+// Arnoldi relation Z Q_k = Q_{k+1} H_k.  At step j the dots of pass A give, for p_j (the vector
+// orthogonalised once at step j-1) and w = Z p_j:
+//   a = Q_j^T p_j, b = Q_j^T w, α = p_j.p_j, β = p_j.w, γ = w.w.
+// Reorthogonalisation: q_j = (p_j - Q_j a)/ν, ν² = α - |a|²; it completes column j-1 of H:
+//   H(0:j, j-1) += a, H(j, j-1) = ν.
+// Then Z q_j = (w - Q_{j+1} H_j a)/ν, so its first-pass projection on Q_{j+1} is
+//   h = ([b ; (β - a.b)/ν] - H_j a)/ν   (stored as the provisional column j of H)
+// and p_{j+1} = Z q_j - Q_{j+1} h = (w - Q_{j+1} Q_{j+1}^T w)/ν
+//            = w/ν - (r_j/ν) p_j - Q_j (r_{0:j} - a r_j/ν),  r = Q_{j+1}^T w/ν = [b/ν ; (β - a.b)/ν²].
+// Pass B coefficients: q_j = cq_p p_j + Σ cq_i q_i, p_{j+1} = cp_w w + cp_p p_j + Σ cp_i q_i.
+// Breakdown (invariant Krylov space): ν <= btol ||Z q_{j-1}||  ->  keff = j, column zeroed after.
+// reorth = 0 drops the delayed correction (a := 0): single classical Gram-Schmidt.
+__global__ void dcgs2_coeffs_kernel(const double* sums, int j, int B, int K, double btol, int final_pass,
+                                    int reorth, double* H, double* ref, double* n0, int* keff, double* coef_v,
+                                    double* coef_s) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= B) return;
+  double* Hc = H + (int64_t)c * (K + 1) * K;  // (row i, col l) at Hc[l*(K+1) + i]
+  auto S = [&](int k) {  // a_i entries (even k < 2j) vanish without reorthogonalisation
+    return (!reorth && k < 2 * j && (k & 1) == 0) ? 0.0 : sums[(int64_t)k * B + c];
+  };
+  const double alpha = S(2 * j), beta = S(2 * j + 1), gamma = S(2 * j + 2);
+  bool alive;
+  double nu;
+  if (j == 0) {
+    nu = sqrt(alpha);
+    alive = nu > 0.0;
+    n0[c] = nu;
+    keff[c] = alive ? K : 0;
+  } else {
+    alive = keff[c] == K;
+    double aa = 0.0;
+    for (int i = 0; i < j; ++i) aa += S(2 * i) * S(2 * i);
+    nu = sqrt(fmax(alpha - aa, 0.0));
+    if (alive) {
+      for (int i = 0; i < j; ++i) Hc[(j - 1) * (K + 1) + i] += S(2 * i);
+      if (nu > btol * ref[c] && nu > 0.0) {
+        Hc[(j - 1) * (K + 1) + j] = nu;
+      } else {
+        Hc[(j - 1) * (K + 1) + j] = 0.0;
+        keff[c] = j;
+        alive = false;
+      }
+    }
+  }
+  const int nq = j;
+  auto zero = [&]() {
+    for (int i = 0; i < nq; ++i) {
+      coef_v[(2 * i) * B + c] = 0.0;
+      coef_v[(2 * i + 1) * B + c] = 0.0;
+    }
+    coef_s[c] = 0.0;
+    coef_s[B + c] = 0.0;
+    coef_s[2 * B + c] = 0.0;
+  };
+  if (final_pass) return;
+  if (!alive) {
+    zero();
+    return;
+  }
+  // (H_j a)_i for i <= j, H_j = columns 0..j-1 (rows 0..j)
+  double Ha[kMaxKrylov + 1];
+  double ab = 0.0;
+  for (int i = 0; i <= j; ++i) Ha[i] = 0.0;
+  for (int l = 0; l < j; ++l) {
+    const double al = S(2 * l);
+    ab += al * S(2 * l + 1);
+    for (int i = 0; i <= l + 1 && i <= j; ++i) Ha[i] += Hc[l * (K + 1) + i] * al;
+  }
+  const double inv = 1.0 / nu;
+  const double qw = (beta - ab) * inv;
+  double* hcol = Hc + (int64_t)j * (K + 1);
+  for (int i = 0; i <= j; ++i)  // provisional column j (completed by step j+1's correction)
+    if (j < K) hcol[i] = ((i < j ? S(2 * i + 1) : qw) - Ha[i]) * inv;
+  // r = H_j a/ν + h = Q_{j+1}^T w / ν = [b/ν ; qw/ν]:  p_{j+1} = (w - Q_{j+1} Q_{j+1}^T w)/ν
+  const double rj = qw * inv;
+  for (int i = 0; i < j; ++i) {
+    const double ai = S(2 * i);
+    coef_v[(2 * i) * B + c] = -ai * inv;
+    coef_v[(2 * i + 1) * B + c] = -(S(2 * i + 1) * inv - ai * rj * inv);
+  }
+  coef_s[c] = inv;
+  coef_s[B + c] = -rj * inv;
+  coef_s[2 * B + c] = inv;
+  ref[c] = sqrt(gamma) * inv;
+}
+
 inline int grid_for(int64_t total, int bs = 256) {
   int64_t g = (total + bs - 1) / bs;
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 8));
@@ -217,6 +306,14 @@ void lanczos_combine(const double* Q, int64_t stride, int m, int64_t n, const do
     WL_CUDA(cudaFuncSetAttribute(lanczos_combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
   lanczos_combine_kernel<<<grid_for(n), 256, smem, s>>>(Q, stride, m, n, Y, nt, scale, X, ldx);
+  WL_CUDA(cudaGetLastError());
+}
+
+void dcgs2_coeffs(const double* sums, int j, int B, int K, double btol, int final_pass, int reorth, double* H,
+                  double* ref, double* n0, int* keff, double* coef_v, double* coef_s, cudaStream_t s) {
+  WL_LAUNCH("dcgs2_coeffs");
+  dcgs2_coeffs_kernel<<<1, 32, 0, s>>>(sums, j, B, K, btol, final_pass, reorth, H, ref, n0, keff, coef_v,
+                                       coef_s);
   WL_CUDA(cudaGetLastError());
 }
 

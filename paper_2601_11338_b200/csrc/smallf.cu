@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(kBS) small_f_kernel(SmallFArgs a) {
   __syncthreads();
   const double n0 = a.n0[c];
   for (int i = threadIdx.x; i <= K; i += blockDim.x) {
-    const double v = (i < m) ? n0 * y[i] * a.s[i * B + c] : 0.0;
+    const double v = (i < m) ? n0 * y[i] * (a.s ? a.s[i * B + c] : 1.0) : 0.0;
     if (a.kind == 3) a.comb[(int64_t)p * (K + 1) + i] = v;
     else a.comb[i * B + c] = v;
   }

@@ -76,6 +76,29 @@ void gram_update_proj(GramArgs a, cudaStream_t s);  // wout = w - Σ c_i Q_i ; s
 void gram_update_norm(GramArgs a, cudaStream_t s);  // wout = w - Σ c_i Q_i ; sums_out[0] = Σ wout²
 int gram_grid(int64_t elems, int B);
 
+// DCGS2: delayed classical Gram-Schmidt (one reduction per Arnoldi step).  Step j holds the
+// finalised orthonormal q_0..q_{j-1} (Q) and p_j (P): once orthogonalised, unnormalised.
+//   pass A (dcgs2_dots):   a_i = q_i.p_j, b_i = q_i.w (i < j), α = p_j.p_j, β = p_j.w, γ = w.w,
+//                          w = Z p_j; sums layout [a_0 b_0 a_1 b_1 ... α β γ] x B (w null: b=β=γ=0)
+//   pass B (dcgs2_update): q_j = cq_p p_j + Σ cq_i q_i  (into P, in place),
+//                          p_{j+1} = cp_w w + cp_p p_j + Σ cp_i q_i  (into Pnext)
+struct Dcgs2Args {
+  const double* Q; int64_t vstride; int nq;
+  int64_t len; int B;
+  double* P;                          // p_j (pass B overwrites it with q_j)
+  const double* wa; int64_t split; const double* wb;   // w two-source (wa null: no w)
+  double* Pnext;                      // pass B: p_{j+1}
+  const double* coef_v;               // pass B: [cq_i, cp_i] interleaved per vector, x B
+  const double* coef_s;               // pass B: [cq_p, cp_p, cp_w] x B
+  int accumulate;                     // pass B vector tiles after the first: add to P / Pnext
+  double* partials; double* sums_out;
+  int grid;
+};
+void dcgs2_dots(Dcgs2Args a, cudaStream_t s);
+void dcgs2_update(Dcgs2Args a, cudaStream_t s);
+void dcgs2_coeffs(const double* sums, int j, int B, int K, double btol, int final_pass, int reorth, double* H,
+                  double* ref, double* n0, int* keff, double* coef_v, double* coef_s, cudaStream_t s);
+
 // ---------------------------------------------------------------- small dense functions
 // Per column c (problem), m = keff[c]: y_c = f_1(H_m) e_1 for the Arnoldi matrix H.
 // kind 3 (outer diffusion): problem p uses column 0's H and computes exp(-tau[p] H_m) e_1;
