@@ -72,12 +72,16 @@ typedef struct {
 /* Options; initialise with wl_opts_default(). */
 typedef struct {
   int32_t krylov_dim;   /* Arnoldi steps k per action (default 30; 1..64) */
-  int32_t reorth;       /* 1 = classical Gram-Schmidt twice (CGS2, default); 0 = single CGS pass */
+  int32_t reorth;       /* 1 = reorthogonalised classical Gram-Schmidt (DCGS2: the second pass is
+                           delayed and fused with the next step's projection; default);
+                           0 = single classical Gram-Schmidt pass */
   int32_t max_cols;     /* columns per internal Krylov batch (default 32; 1..32) */
   double breakdown_tol; /* lucky breakdown when ||w_{j+1}|| <= tol * ||Z q_j|| (default 1e-12) */
   double rho_bound;     /* optional upper bound on ρ(Z_θ) (e.g. ρ(A), which bounds it since
                            0 <= q_k <= A^k): a resolvent with α * rho_bound >= 1 is rejected with
                            WL_EDIVERGE (Prop. pro:whe-we-converge).  0 = no check (default). */
+  int32_t relabel;      /* 1 (default): relabel the local rows by decreasing degree internally
+                           (gather locality); results are returned in the caller's row order */
 } wl_opts;
 
 typedef struct wl_comm wl_comm;

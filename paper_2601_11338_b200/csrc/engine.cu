@@ -149,7 +149,8 @@ struct wl_operator {
   std::vector<double> coeffs;
   DArr<double> coeffs_dev;
   wl_opts opts{};
-  DArr<double> tprime;  // n_loc x n_theta: t - c_0 (φ1 minus its identity term)
+  DArr<double> tprime;  // n_loc x n_theta, internal row order: t - c_0 (φ1 minus its identity term)
+  DArr<int32_t> perm;   // internal row -> user row (degree-sorted relabelling); empty = identity
   // degree bins of the SpMM (spmv.cu)
   DArr<int32_t> small_rows, medium_rows;
   DArr<int4> chunks;
@@ -268,8 +269,11 @@ void spmv_scratch(const wl_operator* op, wl_workspace* ws, int B) {
 
 // One Krylov action on global output columns [gstart, gstart + B) of the n_theta*b block;
 // `out` points at column gstart.  mode: 0 = φV, 1 = 𝕃V, 2 = t' (V = ones).
+// user_order: V / out rows are in the caller's order (gathered / scattered through op->perm);
+// false for the internal-order vectors of the outer diffusion Lanczos.
 void run_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double* V, int64_t ldv, int b,
-               int gstart, int B, double* out, int64_t ldo, cudaStream_t s) {
+               int gstart, int B, double* out, int64_t ldo, cudaStream_t s, bool user_order = true) {
+  const int32_t* perm = user_order ? op->perm.p : nullptr;
   const int64_t n = op->n_loc;
   const int K = ws->K;
   const int64_t L = 2 * n;
@@ -279,7 +283,7 @@ void run_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double* 
   double* g0s = g1z + kMaxCols;
   double* g1s = g0s + kMaxCols;
   setup_chunk(op->mu_dev.p, gstart, b, B, g0z, g1z, g0s, g1s, ws->vcol.p, ws->tcol.p, s);
-  batch_inputs(V, ldv, B, n, ws->Vb.p, ws->vcol.p, s);
+  batch_inputs(V, ldv, B, n, ws->Vb.p, ws->vcol.p, perm, s);
   double* Q0 = ws->basis.p;
   // a3: seeds q_1 v = A v (top) and q_2 v = A(Av) - μ d⊙v (bottom)   (eq:qrec seeds)
   halo_exchange(op, ws, ws->Vb.p, B, B, s);
@@ -346,7 +350,7 @@ void run_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double* 
   small_f(f, s);
   // a7: combine (top halves of the basis)
   combine(mode, ws->basis.p, vstride, K, n, B, ws->comb.p, V, ldv, ws->vcol.p, op->c0,
-          op->tprime.p, op->n_theta, ws->tcol.p, out, ldo, s);
+          op->tprime.p, op->n_theta, ws->tcol.p, out, ldo, perm, s);
 }
 
 void run_action(const wl_operator* op, wl_workspace* ws, int mode, const double* V, int64_t ldv, int b,
@@ -468,6 +472,34 @@ void build_operator(wl_operator* op, const int64_t* rp_in, const int32_t* ci_in,
     if (cg >= op->row_begin && cg < op->row_end) col[z] = (int32_t)(cg - op->row_begin);
     else col[z] = (int32_t)(n + (std::lower_bound(remote.begin(), remote.end(), cg) - remote.begin()));
   }
+  // Degree-sorted relabelling of the local rows: internal row r' holds user row perm[r'], rows
+  // in decreasing degree (ties by id).  The hot gather set (high-degree rows, i.e. the columns
+  // most nonzeros point to) becomes a dense, L2-resident prefix of every gathered block instead
+  // of being scattered across random ids.  Halo ids (>= n) are unchanged; inputs are gathered and
+  // outputs scattered through perm at the boundary (batch_inputs / combine).
+  std::vector<int32_t> newid;
+  if (op->opts.relabel) {
+    std::vector<int32_t> perm((size_t)n);
+    std::iota(perm.begin(), perm.end(), 0);
+    std::stable_sort(perm.begin(), perm.end(), [&](int32_t x, int32_t y) {
+      return (rp[x + 1] - rp[x]) > (rp[y + 1] - rp[y]);
+    });
+    newid.assign((size_t)n, 0);
+    for (int64_t k = 0; k < n; ++k) newid[perm[k]] = (int32_t)k;
+    std::vector<int32_t> rp2((size_t)n + 1, 0), col2((size_t)nnz);
+    for (int64_t k = 0; k < n; ++k) rp2[k + 1] = rp2[k] + (rp[perm[k] + 1] - rp[perm[k]]);
+    for (int64_t k = 0; k < n; ++k) {
+      const int32_t src = rp[perm[k]], dst = rp2[k], d = rp[perm[k] + 1] - src;
+      for (int32_t t = 0; t < d; ++t) {
+        const int32_t cl = col[src + t];
+        col2[dst + t] = cl < n ? newid[cl] : cl;
+      }
+    }
+    rp.swap(rp2);
+    col.swap(col2);
+    op->perm.alloc(std::max<int64_t>(1, n));
+    if (n) WL_CUDA(cudaMemcpy(op->perm.p, perm.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+  }
   {  // degree bins (spmv.cu): small rows, medium rows, hub-row chunks
     std::vector<int32_t> sm, md;
     std::vector<int4> ch;
@@ -528,6 +560,7 @@ void build_operator(wl_operator* op, const int64_t* rp_in, const int32_t* ci_in,
     for (int64_t k = 0; k < op->n_send; ++k) {
       if (g[k] < op->row_begin || g[k] >= op->row_end) throw Error(WL_EGRAPH, "halo request for a row not owned");
       idx[k] = (int32_t)(g[k] - op->row_begin);
+      if (!newid.empty()) idx[k] = newid[idx[k]];
     }
     op->send_idx.alloc(std::max<int64_t>(1, op->n_send));
     if (op->n_send) WL_CUDA(cudaMemcpy(op->send_idx.p, idx.data(), sizeof(int32_t) * op->n_send, cudaMemcpyHostToDevice));
@@ -684,6 +717,7 @@ void wl_opts_default(wl_opts* o) {
   o->max_cols = 32;
   o->breakdown_tol = 1e-12;
   o->rho_bound = 0.0;
+  o->relabel = 1;
 }
 
 wl_status wl_nccl_unique_id(void* out128) {
@@ -843,6 +877,14 @@ wl_status wl_operator_diag_shift(const wl_operator* op, double* t_dev, int64_t l
     WL_CUDA(cudaMemcpyAsync(host.data(), op->tprime.p, sizeof(double) * host.size(), cudaMemcpyDeviceToHost, S_(stream)));
     WL_CUDA(cudaStreamSynchronize(S_(stream)));
     for (auto& v : host) v += op->c0;
+    if (op->perm.p) {  // internal -> user row order
+      std::vector<int32_t> perm((size_t)op->n_loc);
+      WL_CUDA(cudaMemcpy(perm.data(), op->perm.p, sizeof(int32_t) * op->n_loc, cudaMemcpyDeviceToHost));
+      std::vector<double> u(host.size());
+      for (int64_t r = 0; r < op->n_loc; ++r)
+        for (int i = 0; i < nt; ++i) u[(size_t)perm[r] * nt + i] = host[(size_t)r * nt + i];
+      host.swap(u);
+    }
     WL_CUDA(cudaMemcpy2DAsync(t_dev, sizeof(double) * ldt, host.data(), sizeof(double) * nt, sizeof(double) * nt,
                               op->n_loc, cudaMemcpyHostToDevice, S_(stream)));
     WL_CUDA(cudaStreamSynchronize(S_(stream)));
@@ -931,10 +973,11 @@ wl_status wl_diffuse(const wl_operator* op, int32_t theta_index, int32_t nt, con
     const int m = k_out;
     outer_alloc(op, ws, m, nt);
     WL_CUDA(cudaMemcpyAsync(ws->otau.p, tau, sizeof(double) * nt, cudaMemcpyHostToDevice, s));
-    WL_CUDA(cudaMemcpyAsync(ws->oQ.p, x0, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    if (op->perm.p) pack_rows(x0, 1, op->perm.p, n, 1, ws->oQ.p, s);  // user -> internal order
+    else WL_CUDA(cudaMemcpyAsync(ws->oQ.p, x0, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
     // outer Arnoldi (= Lanczos with full reorthogonalisation: 𝕃 symmetric, Prop. pro:still-again-an-mmatrix)
     outer_arnoldi(op, ws, m, [&](const double* Pj, double* out) {
-      run_chunk(op, ws, 1, Pj, 1, 1, theta_index, 1, out, 1, s);  // inner action 𝕃 P̃_j
+      run_chunk(op, ws, 1, Pj, 1, 1, theta_index, 1, out, 1, s, false);  // inner action 𝕃 P̃_j
     }, s);
     SmallFArgs f{};
     f.H = ws->oH.p;
@@ -949,7 +992,7 @@ wl_status wl_diffuse(const wl_operator* op, int32_t theta_index, int32_t nt, con
     f.tau = ws->otau.p;
     f.nprob = nt;
     small_f(f, s);
-    lanczos_combine(ws->oQ.p, outer_stride(op), m + 1, n, ws->oY.p, nt, 1.0, X, ldx, s);
+    lanczos_combine(ws->oQ.p, outer_stride(op), m + 1, n, ws->oY.p, nt, 1.0, X, ldx, op->perm.p, s);
   });
 }
 

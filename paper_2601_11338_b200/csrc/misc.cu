@@ -6,14 +6,16 @@
 namespace wl {
 namespace {
 
-__global__ void batch_inputs_kernel(const double* V, int64_t ldv, int b, int B, int64_t n, double* Vb,
-                                    const int* vcol) {
+// internal row r holds user row perm[r] (degree-sorted relabelling; perm null = identity)
+__global__ void batch_inputs_kernel(const double* V, int64_t ldv, int B, int64_t n, double* Vb,
+                                    const int* vcol, const int32_t* perm) {
   const int64_t total = n * B;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = e / B;
     const int j = (int)(e - r * B);
-    Vb[e] = V ? V[r * ldv + vcol[j]] : 1.0;
+    const int64_t ru = perm ? perm[r] : r;
+    Vb[e] = V ? V[ru * ldv + vcol[j]] : 1.0;
   }
 }
 
@@ -62,7 +64,7 @@ template <int NV>
 __global__ void combine_kernel(int mode, const double* Q, int64_t vstride, int nvec, int64_t n, int B,
                                const double* comb, const double* V, int64_t ldv, const int* vcol,
                                double c0, const double* tprime, int64_t ldt, const int* tcol,
-                               double* out, int64_t ldo) {
+                               double* out, int64_t ldo, const int32_t* perm) {
   __shared__ double s_comb[NV * kMaxCols];
   for (int idx = threadIdx.x; idx < nvec * B; idx += blockDim.x) s_comb[idx] = comb[idx];
   __syncthreads();
@@ -76,13 +78,15 @@ __global__ void combine_kernel(int mode, const double* Q, int64_t vstride, int n
     for (int i = 0; i < NV; ++i)
       if (i < nvec) acc += s_comb[i * B + c] * __ldg(Q + i * vstride + e);
     double o;
+    const int64_t ru = perm ? perm[r] : r;  // user row of internal row r
     if (mode == 2) {
       o = acc;
+      out[r * ldo + c] = o;  // t' stays in internal order
     } else {
-      const double v = V ? V[r * ldv + vcol[c]] : 1.0;
+      const double v = V ? V[ru * ldv + vcol[c]] : 1.0;
       o = (mode == 0) ? c0 * v + acc : tprime[r * ldt + tcol[c]] * v - acc;
+      out[ru * ldo + c] = o;
     }
-    out[r * ldo + c] = o;
   }
 }
 
@@ -104,7 +108,7 @@ __global__ void fill_kernel(double* p, int64_t n, double v) {
 
 // X[r, s] = scale * Σ_i Q_i[r] Y[s*m + i]   (outer Lanczos combine, Q_i unit-stride length n)
 __global__ void lanczos_combine_kernel(const double* Q, int64_t stride, int m, int64_t n, const double* Y,
-                                       int nt, double scale, double* X, int64_t ldx) {
+                                       int nt, double scale, double* X, int64_t ldx, const int32_t* perm) {
   extern __shared__ double s_Y[];  // m * nt
   for (int idx = threadIdx.x; idx < m * nt; idx += blockDim.x) s_Y[idx] = Y[idx];
   __syncthreads();
@@ -119,7 +123,7 @@ __global__ void lanczos_combine_kernel(const double* Q, int64_t stride, int m, i
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u)
-        if (s0 + u < nt) X[r * ldx + s0 + u] = scale * acc[u];
+        if (s0 + u < nt) X[(perm ? (int64_t)perm[r] : r) * ldx + s0 + u] = scale * acc[u];
     }
   }
 }
@@ -239,9 +243,9 @@ inline int grid_for(int64_t total, int bs = 256) {
 }  // namespace
 
 void batch_inputs(const double* V, int64_t ldv, int B, int64_t n, double* Vb, const int* vcol,
-                      cudaStream_t s) {
+                  const int32_t* perm, cudaStream_t s) {
   WL_LAUNCH("batch_inputs");
-  batch_inputs_kernel<<<grid_for(n * B), 256, 0, s>>>(V, ldv, 0, B, n, Vb, vcol);
+  batch_inputs_kernel<<<grid_for(n * B), 256, 0, s>>>(V, ldv, B, n, Vb, vcol, perm);
   WL_CUDA(cudaGetLastError());
 }
 
@@ -270,15 +274,15 @@ void finalize_step(const double* sums1, const double* sums2, const double* sums3
 void combine(int mode, const double* Q, int64_t vstride, int nvec, int64_t n, int B,
                  const double* comb, const double* V, int64_t ldv, const int* vcol, double c0,
                  const double* tprime, int64_t ldt, const int* tcol, double* out, int64_t ldo,
-                 cudaStream_t s) {
+                 const int32_t* perm, cudaStream_t s) {
   WL_LAUNCH("combine");
   const int g = grid_for(n * B);
   if (nvec <= 16)
-    combine_kernel<16><<<g, 256, 0, s>>>(mode, Q, vstride, nvec, n, B, comb, V, ldv, vcol, c0, tprime, ldt, tcol, out, ldo);
+    combine_kernel<16><<<g, 256, 0, s>>>(mode, Q, vstride, nvec, n, B, comb, V, ldv, vcol, c0, tprime, ldt, tcol, out, ldo, perm);
   else if (nvec <= 32)
-    combine_kernel<32><<<g, 256, 0, s>>>(mode, Q, vstride, nvec, n, B, comb, V, ldv, vcol, c0, tprime, ldt, tcol, out, ldo);
+    combine_kernel<32><<<g, 256, 0, s>>>(mode, Q, vstride, nvec, n, B, comb, V, ldv, vcol, c0, tprime, ldt, tcol, out, ldo, perm);
   else
-    combine_kernel<kMaxKrylov + 1><<<g, 256, 0, s>>>(mode, Q, vstride, nvec, n, B, comb, V, ldv, vcol, c0, tprime, ldt, tcol, out, ldo);
+    combine_kernel<kMaxKrylov + 1><<<g, 256, 0, s>>>(mode, Q, vstride, nvec, n, B, comb, V, ldv, vcol, c0, tprime, ldt, tcol, out, ldo, perm);
   WL_CUDA(cudaGetLastError());
 }
 
@@ -298,14 +302,14 @@ void fill(double* p, int64_t n, double v, cudaStream_t s) {
 }
 
 void lanczos_combine(const double* Q, int64_t stride, int m, int64_t n, const double* Y, int nt,
-                     double scale, double* X, int64_t ldx, cudaStream_t s) {
+                     double scale, double* X, int64_t ldx, const int32_t* perm, cudaStream_t s) {
   WL_LAUNCH("lanczos_combine");
   const size_t smem = sizeof(double) * (size_t)m * nt;
   if (smem > 200 * 1024) throw Error(1, "lanczos_combine: k_out * nt too large");
   if (smem > 48 * 1024)
     WL_CUDA(cudaFuncSetAttribute(lanczos_combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
-  lanczos_combine_kernel<<<grid_for(n), 256, smem, s>>>(Q, stride, m, n, Y, nt, scale, X, ldx);
+  lanczos_combine_kernel<<<grid_for(n), 256, smem, s>>>(Q, stride, m, n, Y, nt, scale, X, ldx, perm);
   WL_CUDA(cudaGetLastError());
 }
 

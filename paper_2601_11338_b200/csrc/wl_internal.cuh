@@ -121,7 +121,7 @@ void small_f(const SmallFArgs& a, cudaStream_t s);
 // ---------------------------------------------------------------- elementwise / misc kernels
 // Vb[r*B + j] = V[r*ldv + vcol[j]]   (j < B); V null => ones
 void batch_inputs(const double* V, int64_t ldv, int B, int64_t n, double* Vb, const int* vcol,
-                  cudaStream_t s);
+                  const int32_t* perm, cudaStream_t s);
 void setup_chunk(const double* mu, int gstart, int b, int B, double* g0z, double* g1z, double* g0s,
                  double* g1s, int* vcol, int* tcol, cudaStream_t s);
 // Arnoldi bookkeeping after a reduction: see engine.cu for the exact semantics.
@@ -132,17 +132,18 @@ void finalize_step(const double* sums1, const double* sums2, const double* sums3
                    cudaStream_t s);
 // combine: mode 0 = φV (c0 V + Σ comb_i Q_i,top), 1 = 𝕃V (t'⊙V - Σ comb_i Q_i,top),
 //          2 = t' (Σ comb_i Q_i,top) for V = 1
-// V column of batch column c is vcol[c]; t' column is tcol[c].
+// V column of batch column c is vcol[c]; t' column is tcol[c]; internal row r is user row
+// perm[r] (modes 0/1 read V and write out in user order; mode 2 writes t' in internal order).
 void combine(int mode, const double* Q, int64_t vstride, int nvec, int64_t n, int B,
              const double* comb, const double* V, int64_t ldv, const int* vcol, double c0,
              const double* tprime, int64_t ldt, const int* tcol, double* out, int64_t ldo,
-             cudaStream_t s);
+             const int32_t* perm, cudaStream_t s);
 void pack_rows(const double* src, int64_t lds, const int32_t* idx, int64_t cnt, int B, double* dst,
                cudaStream_t s);
 void fill(double* p, int64_t n, double v, cudaStream_t s);
 
 // outer Lanczos helpers (diffusion)
 void lanczos_combine(const double* Q, int64_t stride, int m, int64_t n, const double* Y, int nt,
-                     double scale, double* X, int64_t ldx, cudaStream_t s);
+                     double scale, double* X, int64_t ldx, const int32_t* perm, cudaStream_t s);
 
 }  // namespace wl

@@ -35,7 +35,7 @@ class _WalkFun(ctypes.Structure):
 class _Opts(ctypes.Structure):
     _fields_ = [("krylov_dim", ctypes.c_int32), ("reorth", ctypes.c_int32),
                 ("max_cols", ctypes.c_int32), ("breakdown_tol", ctypes.c_double),
-                ("rho_bound", ctypes.c_double)]
+                ("rho_bound", ctypes.c_double), ("relabel", ctypes.c_int32)]
 
 
 def load():
@@ -199,7 +199,7 @@ class Operator:
 
     def __init__(self, n_global, row_ptr, col_idx, thetas=(1.0,), f=("exp", 1.0), variant=None,
                  row_range=None, comm: Comm | None = None, krylov_dim=30, reorth=1, max_cols=32,
-                 breakdown_tol=1e-12, rho_bound=0.0, stream=None):
+                 breakdown_tol=1e-12, rho_bound=0.0, relabel=1, stream=None):
         lib = load()
         rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
         ci = np.ascontiguousarray(col_idx, dtype=np.int32)
@@ -225,7 +225,7 @@ class Operator:
         opts = _Opts()
         lib.wl_opts_default(ctypes.byref(opts))
         opts.krylov_dim, opts.reorth, opts.max_cols = krylov_dim, reorth, max_cols
-        opts.breakdown_tol, opts.rho_bound = breakdown_tol, rho_bound
+        opts.breakdown_tol, opts.rho_bound, opts.relabel = breakdown_tol, rho_bound, relabel
         h = ctypes.c_void_p()
         _check(lib.wl_operator_create(comm.handle if comm else None, n_global, rb, re, rp.ctypes.data,
                                       ci.ctypes.data, variant, len(thetas) if variant == WL_BTDW else 1,

@@ -227,3 +227,22 @@ def test_full_c2_barabasi_albert(wl):
         ref = S.laplacian_apply(g, 1.0 - th, f, V, rA)
         assert relerr(got[:, 8 * i:8 * i + 8], ref).max() < TOL
     op.close()
+
+
+def test_relabel_on_off_agree(wl):
+    """Degree-sorted internal relabelling is invisible at the boundary (results in user order)."""
+    g = gg.rmat(13, 6000, 60000, seed=5, perm_seed=6)
+    rA = S.rho_A(g)
+    V = gg.vectors(g.n, 3, 2)
+    outs = []
+    for rel in (0, 1):
+        op = wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=[0.3, 1.0], f=("exp", 1.0 / rA), relabel=rel)
+        outs.append((op.apply(torch.from_numpy(V).cuda()).cpu().numpy(), op.diag_shift().cpu().numpy()))
+        x0 = np.zeros(g.n)
+        x0[7] = 1.0
+        outs[-1] += (op.diffuse(torch.from_numpy(x0).cuda(), [0.5, 2.0], k_out=30).cpu().numpy(),)
+        op.close()
+    for a, b in zip(outs[0], outs[1]):
+        assert relerr(a, b).max() < 1e-12
+    ref = S.laplacian_apply(g, 0.7, C.exp(1.0 / rA), V, rA)
+    assert relerr(outs[1][0][:, :3], ref).max() < TOL
