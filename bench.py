@@ -169,7 +169,19 @@ def run_walklap(args):
     # β = 1/ρ(A) (inverse temperature) — ρ(A) by the library's Lanczos on A
     probe = wl.Operator(g.n, rp, ci, thetas=[1.0], f=("series", [0.0, 1.0]), row_range=(rb, re), comm=comm,
                         krylov_dim=2)
+    # the Lanczos of ρ(A) runs rho_k single-column SpMVs A·y: time them live (b = 1 SpMV roofline)
+    torch.cuda.synchronize()
+    wl.profile_enable(True)
     rho = probe.spectral_radius(k=args.rho_k)
+    wl.profile_enable(False)
+    prof_rho = wl.profile_collect()
+    spmv_b1 = None
+    if "spmv_binned" in prof_rho:
+        ms1, cnt1 = prof_rho["spmv_binned"]
+        nl, nz = probe.n_local, probe.nnz_local
+        by1 = 4 * nz + 4 * (nl + 1) + 8 * nl + 8 * probe.n_halo + 8 * nl  # col, rowptr, y (once), halo, out
+        spmv_b1 = {"alg_bytes_per_launch": by1, "ms_per_launch": ms1 / cnt1, "launches": cnt1,
+                   "achieved_gbs": by1 / (ms1 / cnt1 / 1e3) / 1e9}
     probe.close()
     beta = 1.0 / rho
     thetas = cfg["thetas"]
@@ -270,8 +282,9 @@ def run_walklap(args):
                        "l2": "inputs larger than L2 (col_idx 1.6 GB, basis tens of GB): no flush",
                        "setup_s": {"generate": round(t_gen, 2), "operator_create_incl_t": round(t_create, 2)}},
             "roofline": roof,
-            "spmv": {"achieved_gbs": spmv.get("achieved_gbs"), "frac": spmv.get("frac"), "peak": peak,
-                     "share": spmv.get("share")},
+            "spmv": {"b": G if G <= 32 else 32, "achieved_gbs": spmv.get("achieved_gbs"), "frac": spmv.get("frac"),
+                     "peak": peak, "share": spmv.get("share"), "traffic": ncu.get("spmv_binned"),
+                     "b1": (dict(spmv_b1, frac=spmv_b1["achieved_gbs"] / peak) if spmv_b1 else None)},
             "kernels": {k: {kk: (round(vv, 6) if isinstance(vv, float) else vv) for kk, vv in v.items()}
                         for k, v in sorted(kernels.items(), key=lambda kv: -kv[1]["ms_per_step"])},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,

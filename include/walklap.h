@@ -108,6 +108,18 @@ void wl_comm_destroy(wl_comm* comm);
  * (clamped to be nondecreasing).  row_ptr: host, n+1 entries.  bounds_out: host, nranks+1. */
 wl_status wl_partition(int64_t n, const int64_t* row_ptr, int32_t nranks, int64_t* bounds_out);
 
+/* Host-only halo plan of rank `rank` under the row partition `bounds` (nranks+1 entries), the
+ * plan wl_operator_create builds before its internal relabelling; needs no GPU.
+ *   col_local_out  : nnz_local int32 — owned column g -> g - bounds[rank]; every other column ->
+ *                    n_local + h, h its index in halo_ids_out
+ *   halo_ids_out   : capacity nnz_local int64 — sorted distinct global ids of the non-owned
+ *                    columns (grouped by owner, partitions being contiguous); *n_halo_out entries
+ *   recv_count_out : nranks int64 (may be NULL) — halo rows owned by each rank
+ * Validates the CSR like wl_operator_create (WL_EGRAPH). */
+wl_status wl_halo_plan(int64_t n_global, int32_t nranks, const int64_t* bounds, int32_t rank,
+                       const int64_t* row_ptr_local, const int32_t* col_idx_local, int32_t* col_local_out,
+                       int64_t* halo_ids_out, int64_t* n_halo_out, int64_t* recv_count_out);
+
 /* ---- operator --------------------------------------------------------------------------------
  * Builds the operator for rows [row_begin, row_end) of an n_global-node simple graph and
  * computes + caches t_θ = φ_θ(A,c) 1 for every requested θ (step a8; synchronous on return).

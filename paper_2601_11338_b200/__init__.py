@@ -9,6 +9,7 @@ from .walklap import (  # noqa: F401
     Operator,
     WalkLapError,
     Workspace,
+    halo_plan,
     launch_count,
     load,
     partition,

@@ -417,6 +417,36 @@ void nccl_alltoall_counts(wl_comm* c, const std::vector<int64_t>& send, std::vec
   WL_CUDA(cudaMemcpy(recv.data(), dr.p, sizeof(int64_t) * P, cudaMemcpyDeviceToHost));
 }
 
+// Column renumbering of a row block [row_begin, row_end): owned column g -> g - row_begin, other
+// columns -> n + (index of g in the sorted, deduplicated halo list).  Validates the CSR
+// (in-range, no self loops, strictly increasing columns per row: simple graphs).
+void halo_plan_host(int64_t n_global, int64_t row_begin, int64_t row_end, const int64_t* rp_in,
+                    const int32_t* ci_in, std::vector<int32_t>& col, std::vector<int64_t>& remote) {
+  const int64_t n = row_end - row_begin;
+  const int64_t base = rp_in[0];
+  const int64_t nnz = rp_in[n] - base;
+  col.assign((size_t)nnz, 0);
+  remote.clear();
+  for (int64_t r = 0; r < n; ++r) {
+    const int64_t grow = row_begin + r;
+    if (rp_in[r + 1] < rp_in[r]) throw Error(WL_EGRAPH, "row_ptr not nondecreasing");
+    for (int64_t z = rp_in[r] - base; z < rp_in[r + 1] - base; ++z) {
+      const int64_t cg = ci_in[z];
+      if (cg < 0 || cg >= n_global) throw Error(WL_EGRAPH, "column id out of range");
+      if (cg == grow) throw Error(WL_EGRAPH, "self loop (graphs must be simple, P:76)");
+      if (z > rp_in[r] - base && cg <= ci_in[z - 1]) throw Error(WL_EGRAPH, "columns not strictly increasing in a row");
+      if (cg < row_begin || cg >= row_end) remote.push_back(cg);
+    }
+  }
+  std::sort(remote.begin(), remote.end());
+  remote.erase(std::unique(remote.begin(), remote.end()), remote.end());
+  for (int64_t z = 0; z < nnz; ++z) {
+    const int64_t cg = ci_in[z];
+    if (cg >= row_begin && cg < row_end) col[z] = (int32_t)(cg - row_begin);
+    else col[z] = (int32_t)(n + (std::lower_bound(remote.begin(), remote.end(), cg) - remote.begin()));
+  }
+}
+
 void build_operator(wl_operator* op, const int64_t* rp_in, const int32_t* ci_in, cudaStream_t s) {
   const int64_t n = op->n_loc;
   const int64_t base = rp_in[0];
@@ -451,27 +481,11 @@ void build_operator(wl_operator* op, const int64_t* rp_in, const int32_t* ci_in,
     bounds[0] = 0;
     bounds[1] = op->n_global;
   }
-  // validate columns and collect remote ids
-  std::vector<int64_t> remote;
-  for (int64_t r = 0; r < n; ++r) {
-    const int64_t grow = op->row_begin + r;
-    for (int64_t z = rp[r]; z < rp[r + 1]; ++z) {
-      const int64_t cg = ci_in[z];
-      if (cg < 0 || cg >= op->n_global) throw Error(WL_EGRAPH, "column id out of range");
-      if (cg == grow) throw Error(WL_EGRAPH, "self loop (graphs must be simple, P:76)");
-      if (z > rp[r] && cg <= ci_in[z - 1]) throw Error(WL_EGRAPH, "columns not strictly increasing in a row");
-      if (cg < op->row_begin || cg >= op->row_end) remote.push_back(cg);
-    }
-  }
-  std::sort(remote.begin(), remote.end());
-  remote.erase(std::unique(remote.begin(), remote.end()), remote.end());
-  op->n_halo = (int64_t)remote.size();
+  // validate columns, renumber them (local ids, then halo ids n + h) and collect the halo
   std::vector<int32_t> col((size_t)nnz);
-  for (int64_t z = 0; z < nnz; ++z) {
-    const int64_t cg = ci_in[z];
-    if (cg >= op->row_begin && cg < op->row_end) col[z] = (int32_t)(cg - op->row_begin);
-    else col[z] = (int32_t)(n + (std::lower_bound(remote.begin(), remote.end(), cg) - remote.begin()));
-  }
+  std::vector<int64_t> remote;
+  halo_plan_host(op->n_global, op->row_begin, op->row_end, rp_in, ci_in, col, remote);
+  op->n_halo = (int64_t)remote.size();
   // Degree-sorted relabelling of the local rows: internal row r' holds user row perm[r'], rows
   // in decreasing degree (ties by id).  The hot gather set (high-degree rows, i.e. the columns
   // most nonzeros point to) becomes a dense, L2-resident prefix of every gathered block instead
@@ -763,6 +777,32 @@ wl_status wl_partition(int64_t n, const int64_t* row_ptr, int32_t nranks, int64_
       bounds[p] = r;
     }
     bounds[nranks] = n;
+  });
+}
+
+wl_status wl_halo_plan(int64_t n_global, int32_t nranks, const int64_t* bounds, int32_t rank,
+                       const int64_t* row_ptr_local, const int32_t* col_idx_local, int32_t* col_local_out,
+                       int64_t* halo_ids_out, int64_t* n_halo_out, int64_t* recv_count_out) {
+  return guarded([&] {
+    if (!bounds || !row_ptr_local || nranks < 1 || rank < 0 || rank >= nranks || !n_halo_out)
+      throw Error(WL_EINVAL, "bad halo plan args");
+    const int64_t rb = bounds[rank], re = bounds[rank + 1];
+    if (rb < 0 || re < rb || re > n_global) throw Error(WL_EINVAL, "bad bounds");
+    const int64_t nnz = row_ptr_local[re - rb] - row_ptr_local[0];
+    if (nnz > 0 && (!col_idx_local || !col_local_out || !halo_ids_out)) throw Error(WL_EINVAL, "NULL arrays");
+    std::vector<int32_t> col;
+    std::vector<int64_t> remote;
+    halo_plan_host(n_global, rb, re, row_ptr_local, col_idx_local, col, remote);
+    if (nnz > 0) std::memcpy(col_local_out, col.data(), sizeof(int32_t) * col.size());
+    if (!remote.empty()) std::memcpy(halo_ids_out, remote.data(), sizeof(int64_t) * remote.size());
+    *n_halo_out = (int64_t)remote.size();
+    if (recv_count_out) {
+      for (int p = 0; p < nranks; ++p) recv_count_out[p] = 0;
+      for (int64_t id : remote) {
+        const int owner = (int)(std::upper_bound(bounds, bounds + nranks + 1, id) - bounds) - 1;
+        recv_count_out[owner]++;
+      }
+    }
   });
 }
 

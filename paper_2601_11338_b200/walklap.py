@@ -58,6 +58,7 @@ def load():
         "wl_comm_create": ([i32, i32, vp, i32, pvp], ctypes.c_int),
         "wl_comm_destroy": ([vp], None),
         "wl_partition": ([i64, vp, i32, vp], ctypes.c_int),
+        "wl_halo_plan": ([i64, i32, vp, i32, vp, vp, vp, vp, vp, vp], ctypes.c_int),
         "wl_operator_create": ([vp, i64, i64, i64, vp, vp, i32, i32, vp, ctypes.POINTER(_WalkFun),
                                 ctypes.POINTER(_Opts), vp, pvp], ctypes.c_int),
         "wl_operator_destroy": ([vp], None),
@@ -122,6 +123,22 @@ def partition(row_ptr: np.ndarray, nranks: int) -> np.ndarray:
     out = np.empty(nranks + 1, dtype=np.int64)
     _check(load().wl_partition(len(rp) - 1, rp.ctypes.data, nranks, out.ctypes.data))
     return out
+
+
+def halo_plan(n_global: int, bounds: np.ndarray, rank: int, row_ptr_local: np.ndarray,
+              col_idx_local: np.ndarray):
+    """Host-only halo plan (wl_halo_plan): (local column ids, halo global ids, per-rank counts)."""
+    b = np.ascontiguousarray(bounds, dtype=np.int64)
+    rp = np.ascontiguousarray(row_ptr_local, dtype=np.int64)
+    ci = np.ascontiguousarray(col_idx_local, dtype=np.int32)
+    nnz = int(rp[-1] - rp[0])
+    col = np.empty(max(1, nnz), dtype=np.int32)
+    halo = np.empty(max(1, nnz), dtype=np.int64)
+    cnt = np.empty(len(b) - 1, dtype=np.int64)
+    nh = ctypes.c_int64()
+    _check(load().wl_halo_plan(n_global, len(b) - 1, b.ctypes.data, rank, rp.ctypes.data, ci.ctypes.data,
+                               col.ctypes.data, halo.ctypes.data, ctypes.byref(nh), cnt.ctypes.data))
+    return col[:nnz], halo[:nh.value], cnt
 
 
 def _stream_handle(stream):
