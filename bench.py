@@ -305,7 +305,7 @@ def ncu_traffic():
     """dram bytes per launch from the committed ncu --set full summary (profiles/), if present."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
-        return {k: v["dram_bytes_per_launch"] for k, v in json.load(open(p)).items()}
+        return {k: v["dram_bytes_per_launch"] for k, v in json.load(open(p)).items() if isinstance(v, dict)}
     except Exception:
         return {}
 

@@ -246,3 +246,55 @@ def test_relabel_on_off_agree(wl):
         assert relerr(a, b).max() < 1e-12
     ref = S.laplacian_apply(g, 0.7, C.exp(1.0 / rA), V, rA)
     assert relerr(outs[1][0][:, :3], ref).max() < TOL
+
+
+@pytest.mark.slow
+def test_full_c4_theta_sweep_vs_series(wl):
+    """Config C4 at full size (R-MAT n=1e7, nnz=4e8) in the bench launch configuration (11 θ, b=1,
+    k=30): the θ = 0.5 column of the sweep vs the series oracle over all 1e7 rows."""
+    from graphgen import configs
+    cfg = configs.get("c4")
+    g = cfg["make"]()
+    # β from the library's Lanczos ρ(A): a parameter shared by both sides; the oracle's truncation
+    # bound uses a safety margin above it
+    probe = wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=[1.0], f=("series", [0.0, 1.0]), krylov_dim=2)
+    rho = probe.spectral_radius(k=60)
+    probe.close()
+    beta = 1.0 / rho
+    V = gg.vectors(g.n, 1, cfg["vec_seed"])
+    op = wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=cfg["thetas"], f=("exp", beta), krylov_dim=30)
+    got = op.apply(torch.from_numpy(V).cuda()).cpu().numpy()
+    t_gpu = op.diag_shift().cpu().numpy()
+    op.close()
+    i = cfg["thetas"].index(0.5)
+    A = S.csr(g)
+    f = C.exp(beta)
+    t = S.total_communicability(g, 0.5, f, rho * 1.001, A=A)
+    ref = t * V[:, 0] - S.phi_apply(g, 0.5, f, V[:, 0], rho * 1.001, A=A)
+    assert relerr(t_gpu[:, i], t).max() < TOL
+    assert relerr(got[:, i], ref).max() < TOL
+    # 𝕃 1 = 0 for every θ column (P:408) via t: 𝕃 1 = t - φ 1 = 0 is exact in the oracle; on the GPU
+    # check symmetry-free invariant sum(𝕃 v) = sum_i t_i v_i - 1ᵀφv = 0 (φ symmetric: 1ᵀφv = tᵀv)
+    for j in range(len(cfg["thetas"])):
+        assert abs(got[:, j].sum()) < 1e-10 * np.abs(got[:, j]).sum()
+
+
+@pytest.mark.slow
+def test_full_c3_road_diffusion(wl):
+    """Config C3 at full size (grid LCC n~2e6): NBT diffusion exp(-τ𝕃)x0 over the 90-point sweep
+    τ in [0,100] (k_out = 80); parity vs the Chebyshev oracle for τ <= 10, mass for every τ."""
+    from graphgen import configs
+    from oracle import chebyshev
+    g = configs.get("c3")["make"]()
+    rA = S.rho_A(g)
+    f = C.exp(1.0 / rA)
+    taus = np.linspace(0.0, 100.0, 90)
+    x0 = np.zeros(g.n)
+    x0[g.n // 2] = 1.0
+    op = wl.Operator(g.n, g.row_ptr, g.col_idx, variant="nbt", f=("exp", f.param))
+    X = op.diffuse(torch.from_numpy(x0).cuda(), taus, k_out=80).cpu().numpy()
+    op.close()
+    assert np.max(np.abs(X.sum(axis=0) - 1.0)) < 1e-10          # mass 1ᵀx(τ) = 1ᵀx0
+    sub = taus <= 10.0
+    ref = chebyshev.diffusion(g, 1.0, f, x0, taus[sub], rA)
+    assert relerr(X[:, sub], ref).max() < TOL
