@@ -20,6 +20,7 @@
 // is uniform within a lane group.
 #include "wl_internal.cuh"
 
+#include <climits>
 #include <cstdlib>
 
 namespace wl {
@@ -28,14 +29,20 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 
-template <int kU>  // gathers in flight per lane
+// Per-lane gather context.  Offsets are 32-bit (n_loc * ld < 2^31 is checked on the host), the
+// halo select exists only in the HALO instantiation, and only the last round of a range is
+// predicated (ncu r3: 18 warp instructions per nonzero before, mostly address/predicate work).
+template <int kU, bool HALO>
 struct Ctx {
   const SpmvArgs& a;
   int c;
   double g0, g1, sc;
+  const double* yc;   // y + c
+  const double* yhc;  // yh + c
+  int ldy, ldh;
   __device__ double gather(int cl) const {
-    return cl < a.n_loc ? __ldg(a.y + (int64_t)cl * a.ldy + c)
-                        : __ldg(a.yh + (int64_t)(cl - a.n_loc) * a.ldh + c);
+    if (HALO && cl >= a.n_loc) return __ldg(yhc + (cl - a.n_loc) * ldh);
+    return __ldg(yc + cl * ldy);
   }
   __device__ void write(int r, int deg, double sum) const {
     double o = sum;
@@ -45,13 +52,22 @@ struct Ctx {
   // Σ y[col[z]] for z = z0 + first, z0 + first + step, ... < z1 (step = lane groups sharing the row)
   __device__ double strided_sum(int z0, int z1, int first, int step) const {
     double acc = 0.0;
-    for (int z = z0 + first; z < z1; z += kU * step) {  // kU predicated gathers in flight
+    int z = z0 + first;
+    const int full = z1 - (kU - 1) * step;  // rounds with all kU nonzeros present
+    for (; z < full; z += kU * step) {
       int cl[kU];
 #pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const int zz = z + u * step;
-        cl[u] = zz < z1 ? __ldg(a.col + zz) : -1;
-      }
+      for (int u = 0; u < kU; ++u) cl[u] = __ldg(a.col + z + u * step);
+      double v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) v[u] = gather(cl[u]);
+#pragma unroll
+      for (int u = 0; u < kU; ++u) acc += v[u];
+    }
+    if (z < z1) {  // predicated tail round
+      int cl[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) cl[u] = (z + u * step < z1) ? __ldg(a.col + z + u * step) : -1;
       double v[kU];
 #pragma unroll
       for (int u = 0; u < kU; ++u) v[u] = cl[u] >= 0 ? gather(cl[u]) : 0.0;
@@ -77,7 +93,7 @@ __device__ inline double group_reduce(double v, int B, int gpw) {
   return s;
 }
 
-template <int kU>
+template <int kU, bool HALO>
 __global__ void __launch_bounds__(kThreads) spmv_binned_kernel(SpmvArgs a) {
   const int B = a.B;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -85,7 +101,8 @@ __global__ void __launch_bounds__(kThreads) spmv_binned_kernel(SpmvArgs a) {
   const int gi = lane / B, c = lane - gi * B;
   const bool lane_ok = gi < gpw;
   const int cc = lane_ok ? c : 0;
-  Ctx<kU> ctx{a, cc, a.g0 ? a.g0[cc] : 0.0, a.g1 ? a.g1[cc] : 0.0, a.scale ? a.scale[cc] : 1.0};
+  Ctx<kU, HALO> ctx{a, cc, a.g0 ? a.g0[cc] : 0.0, a.g1 ? a.g1[cc] : 0.0, a.scale ? a.scale[cc] : 1.0,
+                    a.y + cc, a.yh + cc, (int)a.ldy, (int)a.ldh};
   int blk = blockIdx.x;
   if (blk < a.nblk_small) {  // ---- small rows: one lane group per row
     const int idx = (blk * kWarps + warp) * gpw + gi;
@@ -198,7 +215,8 @@ __global__ void __launch_bounds__(kThreads) spmv_async_kernel(SpmvArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* sbuf = s_dyn + (int64_t)warp * S * 32 * B;
   const int cc = lane < B ? lane : 0;
-  Ctx<8> ctx{a, cc, a.g0 ? a.g0[cc] : 0.0, a.g1 ? a.g1[cc] : 0.0, a.scale ? a.scale[cc] : 1.0};
+  Ctx<8, true> ctx{a, cc, a.g0 ? a.g0[cc] : 0.0, a.g1 ? a.g1[cc] : 0.0, a.scale ? a.scale[cc] : 1.0,
+                   a.y + cc, a.yh + cc, (int)a.ldy, (int)a.ldh};
   int blk = blockIdx.x;
   if (blk < a.nblk_medium) {
     const int idx = blk * kWarps + warp;
@@ -245,10 +263,17 @@ void spmv(const SpmvArgs& a0, cudaStream_t s) {
   if (grid <= 0) return;
   static const int U = [] { const char* v = getenv("WL_SPMV_U"); return v ? atoi(v) : 8; }();
   static const bool split = getenv("WL_SPMV_SPLIT") != nullptr;  // per-class timing experiment
+  if ((int64_t)(a.n_loc + 1) * a.ldy >= INT32_MAX || a.yh && (int64_t)a.ldh * a.n_loc >= INT32_MAX)
+    throw Error(8, "spmv: n_loc * ld must be < 2^31 (32-bit gather offsets)");
+  const bool halo = a.yh != nullptr;
   auto go = [&](const SpmvArgs& aa, int g) {
-    if (U >= 32) spmv_binned_kernel<32><<<g, kThreads, 0, s>>>(aa);
-    else if (U >= 16) spmv_binned_kernel<16><<<g, kThreads, 0, s>>>(aa);
-    else spmv_binned_kernel<8><<<g, kThreads, 0, s>>>(aa);
+    if (halo) {
+      if (U >= 16) spmv_binned_kernel<16, true><<<g, kThreads, 0, s>>>(aa);
+      else spmv_binned_kernel<8, true><<<g, kThreads, 0, s>>>(aa);
+    } else {
+      if (U >= 16) spmv_binned_kernel<16, false><<<g, kThreads, 0, s>>>(aa);
+      else spmv_binned_kernel<8, false><<<g, kThreads, 0, s>>>(aa);
+    }
     WL_CUDA(cudaGetLastError());
   };
   static const int async_min_b = [] { const char* v = getenv("WL_SPMV_ASYNC"); return v ? atoi(v) : 99; }();  // off by default: measured slower
