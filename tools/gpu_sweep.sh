@@ -1,5 +1,5 @@
 # parity tests, then the C4 bench under several experiment knobs (env assignments as args)
-timeout 900 python -m pytest tests -m gpu -q -x --timeout 180 -p no:cacheprovider 2>&1 | tail -${TESTLINES:-3}
+[ -z "$SKIPTESTS" ] && timeout 900 python -m pytest tests -m gpu -q -x --timeout 180 -p no:cacheprovider 2>&1 | tail -${TESTLINES:-3}
 for cfg in "$@"; do
   env $cfg timeout 900 python bench.py --steps ${STEPS:-3} --warmup 3 --no-cpu-baseline --no-e2e ${BENCHARGS} 2>gpurun_out/bench_sweep.err > gpurun_out/bench_sweep.json || tail -5 gpurun_out/bench_sweep.err
   python - "$cfg" <<'PY'
