@@ -1,0 +1,339 @@
+// dcgs2.cu — the two basis passes of the DCGS2 Arnoldi step (step a5): bulk-copy ring kernels.
+//
+// Per Arnoldi step j (see misc.cu dcgs2_coeffs_kernel for the algebra):
+//   pass A (dcgs2_dots):   a_i = q_i.p_j, b_i = q_i.w (i < j), α = p.p, β = p.w, γ = w.w
+//   pass B (dcgs2_update): q_j = cq_p p + Σ cq_i q_i      -> spare slot (never aliases p_j)
+//                          p_{j+1} = cp_w w + cp_p p + Σ cp_i q_i
+// with w = Z p_j = (p_j,bottom ; S), S the SpMM output.  Both passes stream the basis once: they
+// are HBM streams of j+2..j+4 vectors, nothing else.
+//
+// Design (measured on B200, tools/stream_bench.cu): a register-streaming kernel cannot keep the
+// ~190 KB per SM in flight that HBM3e needs once 30+ streams each want several loads in flight per
+// thread (best register variant: 4.2-4.9 TB/s here).  So both passes run ONE persistent CTA per SM
+// in which a producer warp streams every operand of a tile — 16 KB pieces of p_j, w and each basis
+// vector — into a 12-stage shared-memory ring with bulk copies (cp.async.bulk, completion on
+// per-stage mbarriers) and consumer warps fold each piece into registers and release the stage
+// (empty mbarrier, no block-wide barrier).  192 KB per SM are in flight without holding a register.
+// Tile = E = tpb * PER elements with tpb = floor(consumers / B) * B: consumer thread t owns the
+// elements t + i*tpb (i < PER) of every tile, all of column t % B (row-major n x B blocks), so its
+// accumulators never mix columns.  Bulk copies need 16-byte aligned, 16-byte multiple pieces:
+// the engine pads each half of a Z vector to an even element count (zero phantom row).
+// Basis vectors come from a pointer table in the kernel parameters, which lets the engine rotate
+// slots instead of overwriting p_j in place.  Reductions are deterministic: per-CTA partials in a
+// fixed order, then reduce_partials (gram.cu).
+#include "wl_internal.cuh"
+
+#include <algorithm>
+#include <cstdlib>
+
+namespace wl {
+namespace {
+
+constexpr int kMaxVecPerLaunch = 32;  // longer bases are tiled by the launchers
+
+// pass A keeps 2 x 32 dot accumulators per thread, so it runs 128 consumers x 16 elements (5 warps: 255 registers per thread);
+// pass B 512 consumers x 4 elements.
+constexpr int kDotsConsumers = 128, kDotsPer = 16;
+constexpr int kUpdConsumers = 512, kUpdPer = 4;
+constexpr int kStages = 12;
+constexpr int kStageElems = 2048;  // 16 KB
+constexpr int kRedBatch = 24;                       // dots epilogue: values per smem round
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t ph) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra WAIT_%=;\n}" ::"r"(bar),
+      "r"(ph)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const double* src, int bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
+// Producer: item sequence per tile = [X0, X1, q_0 .. q_{nq-1}]; X1 may be two-source (wa | wb).
+__device__ __forceinline__ void ring_produce(const Dcgs2Args& a, const double* X0, const double* X1a, const double* X1b,
+                             int64_t h, int E, double* ring, uint64_t* full, uint64_t* empty) {
+  const int64_t N = a.len * a.B;
+  int s = 0;
+  uint32_t ph = 0;
+  int64_t it = 0;
+  const int nitems = a.nq + (X0 ? 1 : 0) + (X1a ? 1 : 0);
+  for (int64_t e0 = (int64_t)blockIdx.x * E; e0 < N; e0 += (int64_t)gridDim.x * E) {
+    const int cnt = (int)min((int64_t)E, N - e0);
+    for (int item = 0; item < nitems; ++item, ++it) {
+      if (it >= kStages) mbar_wait(su32(&empty[s]), ph ^ 1);
+      const uint32_t bar = su32(&full[s]);
+      const uint32_t dst = su32(ring + (int64_t)s * kStageElems);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(cnt * 8) : "memory");
+      const int qi = item - (X0 ? 1 : 0) - (X1a ? 1 : 0);
+      if (X0 && item == 0) {
+        bulk_g2s(dst, X0 + e0, cnt * 8, bar);
+      } else if (qi < 0) {  // X1, possibly straddling the two sources at h
+        if (X1b == nullptr || e0 + cnt <= h) {
+          bulk_g2s(dst, X1a + e0, cnt * 8, bar);
+        } else if (e0 >= h) {
+          bulk_g2s(dst, X1b + (e0 - h), cnt * 8, bar);
+        } else {
+          const int c1 = (int)(h - e0);
+          bulk_g2s(dst, X1a + e0, c1 * 8, bar);
+          bulk_g2s(dst + c1 * 8, X1b, (cnt - c1) * 8, bar);
+        }
+      } else {
+        bulk_g2s(dst, a.Q.p[qi] + e0, cnt * 8, bar);
+      }
+      if (++s == kStages) { s = 0; ph ^= 1; }
+    }
+  }
+}
+
+struct RingCursor {
+  int s = 0;
+  uint32_t ph = 0;
+  __device__ const double* acquire(double* ring, uint64_t* full) {
+    mbar_wait(su32(&full[s]), ph);
+    return ring + (int64_t)s * kStageElems;
+  }
+  __device__ void release(uint64_t* empty, int lane) {
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&empty[s])) : "memory");
+    if (++s == kStages) { s = 0; ph ^= 1; }
+  }
+};
+
+__device__ __forceinline__ void ring_init(uint64_t* full, uint64_t* empty, int consumer_warps) {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&empty[s])), "r"(consumer_warps));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+}
+
+// pass A: items [P, w?, q_0..q_{nq-1}]
+__global__ void __launch_bounds__(kDotsConsumers + 32, 1) dcgs2_dots_ring(Dcgs2Args a, int tpb) {
+  extern __shared__ __align__(128) double ring[];
+  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, t = threadIdx.x;
+  const int B = a.B, nq = a.nq;
+  const int E = tpb * kDotsPer;
+  const int64_t N = a.len * a.B, h = a.split * a.B;
+  const bool has_w = a.wa != nullptr;
+  ring_init(full, empty, kDotsConsumers / 32);
+  __syncthreads();
+  double acc[2 * kMaxVecPerLaunch], alpha = 0.0, beta = 0.0, gamma = 0.0;
+#pragma unroll
+  for (int v = 0; v < 2 * kMaxVecPerLaunch; ++v) acc[v] = 0.0;
+  if (warp == kDotsConsumers / 32) {
+    if (lane == 0) ring_produce(a, a.P, has_w ? a.wa : nullptr, a.wb, h, E, ring, full, empty);
+  } else {
+    RingCursor cur;
+    const bool act = t < tpb;
+    for (int64_t e0 = (int64_t)blockIdx.x * E; e0 < N; e0 += (int64_t)gridDim.x * E) {
+      const int cnt = (int)min((int64_t)E, N - e0);
+      double pv[kDotsPer], wv[kDotsPer];
+      {
+        const double* st = cur.acquire(ring, full);
+#pragma unroll
+        for (int i = 0; i < kDotsPer; ++i) pv[i] = (act && t + i * tpb < cnt) ? st[t + i * tpb] : 0.0;
+        cur.release(empty, lane);
+      }
+      if (has_w) {
+        const double* st = cur.acquire(ring, full);
+#pragma unroll
+        for (int i = 0; i < kDotsPer; ++i) wv[i] = (act && t + i * tpb < cnt) ? st[t + i * tpb] : 0.0;
+        cur.release(empty, lane);
+      } else {
+#pragma unroll
+        for (int i = 0; i < kDotsPer; ++i) wv[i] = 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < kDotsPer; ++i) {
+        alpha += pv[i] * pv[i];
+        beta += pv[i] * wv[i];
+        gamma += wv[i] * wv[i];
+      }
+#pragma unroll 32
+      for (int j = 0; j < kMaxVecPerLaunch; ++j) {
+        if (j < nq) {
+          const double* st = cur.acquire(ring, full);
+#pragma unroll
+          for (int i = 0; i < kDotsPer; ++i) {
+            const double q = (act && t + i * tpb < cnt) ? st[t + i * tpb] : 0.0;
+            acc[2 * j] += q * pv[i];
+            acc[2 * j + 1] += q * wv[i];
+          }
+          cur.release(empty, lane);
+        }
+      }
+    }
+  }
+  __syncthreads();  // every copy has landed and been consumed: the ring is free
+  // epilogue: per (value, column) sum over the consumer threads of that column, fixed order
+  const int nval = 2 * nq + 3;
+  double* red = ring;  // [kRedBatch][kDotsConsumers]
+  for (int v0 = 0; v0 < nval; v0 += kRedBatch) {
+    if (t < kDotsConsumers) {
+#pragma unroll
+      for (int u = 0; u < 2 * kMaxVecPerLaunch; ++u)
+        if (u < 2 * nq && u >= v0 && u < v0 + kRedBatch) red[(u - v0) * kDotsConsumers + t] = acc[u];
+      if (2 * nq >= v0 && 2 * nq < v0 + kRedBatch) red[(2 * nq - v0) * kDotsConsumers + t] = alpha;
+      if (2 * nq + 1 >= v0 && 2 * nq + 1 < v0 + kRedBatch) red[(2 * nq + 1 - v0) * kDotsConsumers + t] = beta;
+      if (2 * nq + 2 >= v0 && 2 * nq + 2 < v0 + kRedBatch) red[(2 * nq + 2 - v0) * kDotsConsumers + t] = gamma;
+    }
+    __syncthreads();
+    const int nv = min(kRedBatch, nval - v0);
+    for (int idx = t; idx < nv * B; idx += blockDim.x) {
+      const int vv = idx / B, c = idx - vv * B;
+      double sum = 0.0;
+      for (int tt = c; tt < tpb; tt += B) sum += red[vv * kDotsConsumers + tt];
+      a.partials[(int64_t)((v0 + vv) * B + c) * gridDim.x + blockIdx.x] = sum;
+    }
+    __syncthreads();
+  }
+}
+
+// pass B: items [X0, X1, q_0..q_{nq-1}];  q_j = a0 X0 + Σ cq_i q_i,  p_{j+1} = a1 X0 + a2 X1 + Σ cp_i q_i
+// (X0, X1) = (p_j, w) with (a0, a1, a2) = (cq_p, cp_p, cp_w), or (Qout, Pnext) with (1, 0, 1)
+// for the vector tiles after the first (accumulate).
+__global__ void __launch_bounds__(kUpdConsumers + 32, 1) dcgs2_update_ring(Dcgs2Args a, int tpb) {
+  extern __shared__ __align__(128) double ring[];
+  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+  __shared__ double coef[2 * kMaxVecPerLaunch * kMaxCols];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, t = threadIdx.x;
+  const int B = a.B, nq = a.nq;
+  const int E = tpb * kUpdPer;
+  const int64_t N = a.len * a.B, h = a.split * a.B;
+  for (int i = t; i < 2 * nq * B; i += blockDim.x) coef[i] = a.coef_v[i];
+  ring_init(full, empty, kUpdConsumers / 32);
+  __syncthreads();
+  if (warp == kUpdConsumers / 32) {
+    if (lane == 0) {
+      if (a.accumulate) ring_produce(a, a.Qout, a.Pnext, nullptr, h, E, ring, full, empty);
+      else ring_produce(a, a.P, a.wa, a.wb, h, E, ring, full, empty);
+    }
+    return;
+  }
+  const bool act = t < tpb;
+  const int c = t % B;
+  double a0, a1, a2;
+  bool dead = false;
+  if (a.accumulate) { a0 = 1.0; a1 = 0.0; a2 = 1.0; }
+  else {
+    a0 = a.coef_s[c]; a1 = a.coef_s[B + c]; a2 = a.coef_s[2 * B + c];
+    dead = a0 == 0.0;
+  }
+  RingCursor cur;
+  for (int64_t e0 = (int64_t)blockIdx.x * E; e0 < N; e0 += (int64_t)gridDim.x * E) {
+    const int cnt = (int)min((int64_t)E, N - e0);
+    double sq[kUpdPer], sp[kUpdPer];
+    {
+      const double* st = cur.acquire(ring, full);
+#pragma unroll
+      for (int i = 0; i < kUpdPer; ++i) {
+        const double x = (act && t + i * tpb < cnt) ? st[t + i * tpb] : 0.0;
+        sq[i] = a0 * x;
+        sp[i] = a1 * x;
+      }
+      cur.release(empty, lane);
+    }
+    {
+      const double* st = cur.acquire(ring, full);
+#pragma unroll
+      for (int i = 0; i < kUpdPer; ++i) sp[i] += a2 * ((act && t + i * tpb < cnt) ? st[t + i * tpb] : 0.0);
+      cur.release(empty, lane);
+    }
+    for (int j = 0; j < nq; ++j) {
+      const double cq = coef[(2 * j) * B + c], cp = coef[(2 * j + 1) * B + c];
+      const double* st = cur.acquire(ring, full);
+#pragma unroll
+      for (int i = 0; i < kUpdPer; ++i) {
+        const double q = (act && t + i * tpb < cnt) ? st[t + i * tpb] : 0.0;
+        sq[i] += cq * q;
+        sp[i] += cp * q;
+      }
+      cur.release(empty, lane);
+    }
+    if (act) {
+#pragma unroll
+      for (int i = 0; i < kUpdPer; ++i)
+        if (t + i * tpb < cnt) {
+          a.Qout[e0 + t + i * tpb] = dead ? 0.0 : sq[i];
+          a.Pnext[e0 + t + i * tpb] = dead ? 0.0 : sp[i];
+        }
+    }
+  }
+}
+
+size_t ring_smem() { return (size_t)kStages * kStageElems * sizeof(double); }
+
+VecPtrs shifted(const VecPtrs& v, int i0) {
+  VecPtrs r{};
+  for (int k = 0; k + i0 < kMaxKrylov + 2; ++k) r.p[k] = v.p[k + i0];
+  return r;
+}
+
+}  // namespace
+
+// pass A for nq <= 32 per launch; longer bases tile the vectors: tile [i0, i1) writes its a/b
+// pairs at offset 2*i0 and its trailing α/β/γ are overwritten by the next tile.
+void dcgs2_dots(Dcgs2Args a, cudaStream_t s) {
+  if (a.nq > kMaxVecPerLaunch) {
+    for (int i0 = 0; i0 < a.nq; i0 += kMaxVecPerLaunch) {
+      Dcgs2Args t = a;
+      t.nq = std::min(kMaxVecPerLaunch, a.nq - i0);
+      t.Q = shifted(a.Q, i0);
+      t.sums_out = a.sums_out + (int64_t)2 * i0 * a.B;
+      dcgs2_dots(t, s);
+    }
+    return;
+  }
+  WL_LAUNCH("dcgs2_dots");
+  {
+    if ((a.split * a.B) % 2) throw Error(1, "dcgs2: half length must be even (phantom row)");
+    static bool attr = false;
+    if (!attr) {
+      WL_CUDA(cudaFuncSetAttribute(dcgs2_dots_ring, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ring_smem()));
+      attr = true;
+    }
+    const int tpb = kDotsConsumers / a.B * a.B;
+    const int64_t N = a.len * a.B;
+    a.grid = (int)std::min<int64_t>(148, (N + tpb * kDotsPer - 1) / (tpb * kDotsPer));
+    dcgs2_dots_ring<<<a.grid, kDotsConsumers + 32, ring_smem(), s>>>(a, tpb);
+    WL_CUDA(cudaGetLastError());
+    note_launch("gram_reduce");
+    reduce_partials(a.partials, (2 * a.nq + 3) * a.B, a.grid, a.sums_out, s);
+  }
+}
+
+void dcgs2_update(Dcgs2Args a, cudaStream_t s) {
+  if (a.nq > kMaxVecPerLaunch) {
+    for (int i0 = 0; i0 < a.nq; i0 += kMaxVecPerLaunch) {
+      Dcgs2Args t = a;
+      t.nq = std::min(kMaxVecPerLaunch, a.nq - i0);
+      t.Q = shifted(a.Q, i0);
+      t.coef_v = a.coef_v + (int64_t)2 * i0 * a.B;
+      t.accumulate = i0 > 0 ? 1 : a.accumulate;
+      dcgs2_update(t, s);
+    }
+    return;
+  }
+  WL_LAUNCH("dcgs2_update");
+  {
+    if ((a.split * a.B) % 2) throw Error(1, "dcgs2: half length must be even (phantom row)");
+    static bool attr = false;
+    if (!attr) {
+      WL_CUDA(cudaFuncSetAttribute(dcgs2_update_ring, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ring_smem()));
+      attr = true;
+    }
+    const int tpb = kUpdConsumers / a.B * a.B;
+    const int64_t N = a.len * a.B;
+    const int grid = (int)std::min<int64_t>(148, (N + tpb * kUpdPer - 1) / (tpb * kUpdPer));
+    dcgs2_update_ring<<<grid, kUpdConsumers + 32, ring_smem(), s>>>(a, tpb);
+    WL_CUDA(cudaGetLastError());
+  }
+}
+
+}  // namespace wl

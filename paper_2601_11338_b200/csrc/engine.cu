@@ -276,7 +276,10 @@ void run_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double* 
   const int32_t* perm = user_order ? op->perm.p : nullptr;
   const int64_t n = op->n_loc;
   const int K = ws->K;
-  const int64_t L = 2 * n;
+  // Z-vector halves hold n_pad >= n rows, n_pad * B even (a zero phantom row when n and B are
+  // both odd): every half starts 16-byte aligned for the bulk copies of the DCGS2 passes.
+  const int64_t n_pad = n + ((n * B) & 1);
+  const int64_t L = 2 * n_pad;
   const int64_t vstride = L * B;
   double* g0z = ws->colp.p;
   double* g1z = g0z + kMaxCols;
@@ -289,13 +292,20 @@ void run_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double* 
   halo_exchange(op, ws, ws->Vb.p, B, B, s);
   do_spmv(op, ws, ws->Vb.p, nullptr, nullptr, nullptr, nullptr, Q0, B, s);
   halo_exchange(op, ws, Q0, B, B, s);
-  do_spmv(op, ws, Q0, ws->Vb.p, g0s, g1s, nullptr, Q0 + n * B, B, s);
+  do_spmv(op, ws, Q0, ws->Vb.p, g0s, g1s, nullptr, Q0 + n_pad * B, B, s);
+  if (n_pad > n) {  // phantom rows of the seed vector and of S stay zero; the passes keep them so
+    fill(Q0 + n * B, B, 0.0, s);
+    fill(Q0 + (n_pad + n) * B, B, 0.0, s);
+    fill(ws->S.p + n * B, B, 0.0, s);
+  }
   // a5: Arnoldi with delayed classical Gram-Schmidt (DCGS2): per step one SpMM, one fused dot
   // pass (single reduction / allreduce) and one fused two-output update pass.
   WL_CUDA(cudaMemsetAsync(ws->H.p, 0, sizeof(double) * B * (K + 1) * K, s));
+  // Basis slots: vector slot i -> buffer; slot K+1 is the spare that receives q_j, after which the
+  // buffers of slots j and K+1 swap (q_j never overwrites p_j while pass B still reads it).
+  VecPtrs slot{};
+  for (int i = 0; i < K + 2; ++i) slot.p[i] = ws->basis.p + (int64_t)i * vstride;
   Dcgs2Args d{};
-  d.Q = ws->basis.p;
-  d.vstride = vstride;
   d.len = L;
   d.B = B;
   d.partials = ws->partials.p;
@@ -304,30 +314,33 @@ void run_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double* 
   d.coef_s = ws->coef_s.p;
   const double btol = op->opts.breakdown_tol;
   for (int j = 0; j < K; ++j) {
-    double* Pj = ws->basis.p + (int64_t)j * vstride;
-    double* Pn = ws->basis.p + (int64_t)(j + 1) * vstride;
+    double* Pj = const_cast<double*>(slot.p[j]);
     // a4: S = A Pj_bot + μ(μ - d) Pj_top — bottom half of Z p_j; its top half is Pj_bot
-    halo_exchange(op, ws, Pj + n * B, B, B, s);
-    do_spmv(op, ws, Pj + n * B, Pj, g0z, g1z, nullptr, ws->S.p, B, s);
+    halo_exchange(op, ws, Pj + n_pad * B, B, B, s);
+    do_spmv(op, ws, Pj + n_pad * B, Pj, g0z, g1z, nullptr, ws->S.p, B, s);
+    d.Q = slot;
     d.nq = j;
     d.P = Pj;
-    d.wa = Pj + n * B;
-    d.split = n;
+    d.wa = Pj + n_pad * B;
+    d.split = n_pad;
     d.wb = ws->S.p;
     dcgs2_dots(d, s);
     allreduce(op, ws->sums1.p, (size_t)(2 * j + 3) * B, s);
     dcgs2_coeffs(ws->sums1.p, j, B, K, btol, 0, op->opts.reorth, ws->H.p, ws->ref.p, ws->n0.p, ws->keff.p,
                  ws->coef_v.p, ws->coef_s.p, s);
-    d.Pnext = Pn;
+    d.Qout = const_cast<double*>(slot.p[K + 1]);
+    d.Pnext = const_cast<double*>(slot.p[j + 1]);
     d.accumulate = 0;
     dcgs2_update(d, s);
+    std::swap(slot.p[j], slot.p[K + 1]);
   }
   {  // delayed reorthogonalisation of p_K completes column K-1 of H
+    d.Q = slot;
     d.nq = K;
-    d.P = ws->basis.p + (int64_t)K * vstride;
+    d.P = slot.p[K];
     d.wa = nullptr;
     d.wb = nullptr;
-    d.split = n;
+    d.split = n_pad;
     dcgs2_dots(d, s);
     allreduce(op, ws->sums1.p, (size_t)(2 * K + 3) * B, s);
     dcgs2_coeffs(ws->sums1.p, K, B, K, btol, 1, op->opts.reorth, ws->H.p, ws->ref.p, ws->n0.p, ws->keff.p,
@@ -349,7 +362,7 @@ void run_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double* 
   f.B = B;
   small_f(f, s);
   // a7: combine (top halves of the basis)
-  combine(mode, ws->basis.p, vstride, K, n, B, ws->comb.p, V, ldv, ws->vcol.p, op->c0,
+  combine(mode, slot, K, n, B, ws->comb.p, V, ldv, ws->vcol.p, op->c0,
           op->tprime.p, op->n_theta, ws->tcol.p, out, ldo, perm, s);
 }
 
@@ -369,8 +382,8 @@ void workspace_alloc(wl_workspace* ws, const wl_operator* op, int max_b) {
   ws->Bmax = std::max(1, std::min({op->opts.max_cols, kMaxCols, op->n_theta * max_b}));
   const int64_t n = op->n_loc;
   const int B = ws->Bmax, K = ws->K;
-  ws->basis.alloc((size_t)(K + 1) * 2 * n * B);
-  ws->S.alloc((size_t)n * B);
+  ws->basis.alloc((size_t)(K + 2) * 2 * (n + 1) * B);  // halves padded by <= 1 phantom row
+  ws->S.alloc((size_t)(n + 1) * B);
   ws->Vb.alloc((size_t)n * B);
   if (op->n_halo > 0) ws->halo_recv.alloc((size_t)op->n_halo * B);
   if (op->n_send > 0) ws->halo_send.alloc((size_t)op->n_send * B);

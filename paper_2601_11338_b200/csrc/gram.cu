@@ -178,174 +178,6 @@ void launch_vs(GramArgs a, cudaStream_t s) {
   WL_CUDA(cudaGetLastError());
 }
 
-// ---- DCGS2 passes ------------------------------------------------------------------------
-// Same thread layout as gram_vs_kernel.  Pass B handles PAIRS (e, e + nB) of a Z vector (top and
-// bottom half, same column): w = Z p_j has top half = bottom half of p_j, so the pair reads
-// p_b = P[e + nB] once and uses it both as p (bottom) and as w (top), and the in-place overwrite
-// of P (p_j -> q_j) is race-free: only the owner thread of the pair reads or writes P[e] and
-// P[e + nB].
-// pass A (read only, so no pairing needed): each thread takes U adjacent element chunks
-// (e, e + ES, ...) — measured faster than the (e, e + nB) pairs; w = (p_bot ; S) is read from
-// its two sources.  Per thread 2 x 8 dot accumulators (q_i.p, q_i.w) for its group's vectors;
-// group 0 also accumulates α, β, γ.
-template <int VG, int U>
-__global__ void __launch_bounds__(kBS) dcgs2_dots_kernel(Dcgs2Args a, int ES, int NG) {
-  __shared__ double red[(2 * VG + 3) * kBS];
-  const int B = a.B, tid = threadIdx.x;
-  const int g = tid % NG, slot = tid / NG;
-  const int nq = a.nq, i0 = g * VG;
-  const int nv_g = max(0, min(VG, nq - i0));
-  const bool has_w = a.wa != nullptr;
-  const int64_t total = a.len * B, splitE = a.split * B;
-  double acc[2 * VG + 3];
-#pragma unroll
-  for (int j = 0; j < 2 * VG + 3; ++j) acc[j] = 0.0;
-  const double* Qg = a.Q + (int64_t)i0 * a.vstride;
-  const int64_t step = (int64_t)gridDim.x * ES * U;
-  for (int64_t b0 = (int64_t)blockIdx.x * ES * U; b0 < total; b0 += step) {
-    double p[U], w[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t e = b0 + slot + (int64_t)u * ES;
-      p[u] = 0.0;
-      w[u] = 0.0;
-      if (e < total) {
-        p[u] = __ldg(a.P + e);
-        if (has_w) w[u] = e < splitE ? __ldg(a.wa + e) : __ldg(a.wb + (e - splitE));
-      }
-    }
-    double q[VG][U];
-#pragma unroll
-    for (int j = 0; j < VG; ++j)
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t e = b0 + slot + (int64_t)u * ES;
-        q[j][u] = (j < nv_g && e < total) ? __ldg(Qg + j * a.vstride + e) : 0.0;
-      }
-#pragma unroll
-    for (int j = 0; j < VG; ++j)
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        acc[2 * j] += q[j][u] * p[u];
-        acc[2 * j + 1] += q[j][u] * w[u];
-      }
-    if (g == 0) {
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        acc[2 * VG] += p[u] * p[u];
-        acc[2 * VG + 1] += p[u] * w[u];
-        acc[2 * VG + 2] += w[u] * w[u];
-      }
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < 2 * VG + 3; ++j) red[j * kBS + tid] = acc[j];
-  __syncthreads();
-  const int nout = (2 * nq + 3) * B;
-  const int per = ES / B;
-  for (int idx = tid; idx < nout; idx += blockDim.x) {
-    const int r = idx / B, cc = idx - r * B;
-    int gg, jj;
-    if (r < 2 * nq) { const int i = r / 2; gg = i / VG; jj = 2 * (i % VG) + (r & 1); }
-    else { gg = 0; jj = 2 * VG + (r - 2 * nq); }
-    double sum = 0.0;
-    for (int k = 0; k < per; ++k) sum += red[jj * kBS + (cc + k * B) * NG + gg];
-    a.partials[(int64_t)idx * gridDim.x + blockIdx.x] = sum;
-  }
-}
-
-// pass B: group partial sums Σ cq_i q_i and Σ cp_i q_i combined by __shfl_xor; group 0 writes.
-template <int VG, int UP>
-__global__ void __launch_bounds__(kBS) dcgs2_update_kernel(Dcgs2Args a, int ES, int NG) {
-  const int B = a.B, tid = threadIdx.x;
-  const int g = tid % NG, slot = tid / NG, c = slot % B;
-  const unsigned mask = __activemask();
-  const int nq = a.nq, i0 = g * VG;
-  const int nv_g = max(0, min(VG, nq - i0));
-  const int64_t half = a.split * B;
-  double cq[VG], cp[VG];
-#pragma unroll
-  for (int j = 0; j < VG; ++j) {
-    cq[j] = j < nv_g ? a.coef_v[(2 * (i0 + j)) * B + c] : 0.0;
-    cp[j] = j < nv_g ? a.coef_v[(2 * (i0 + j) + 1) * B + c] : 0.0;
-  }
-  const double cq_p = a.coef_s[c], cp_p = a.coef_s[B + c], cp_w = a.coef_s[2 * B + c];
-  const bool dead = !a.accumulate && cq_p == 0.0;  // broken-down column: exact zeros
-  const double* Qg = a.Q + (int64_t)i0 * a.vstride;
-  const int64_t step = (int64_t)gridDim.x * ES * UP;
-  for (int64_t b0 = (int64_t)blockIdx.x * ES * UP; b0 < half; b0 += step) {
-    double q[VG][2 * UP];
-#pragma unroll
-    for (int u = 0; u < UP; ++u) {
-      const int64_t e = b0 + slot + (int64_t)u * ES;
-      const bool ok = e < half;
-#pragma unroll
-      for (int j = 0; j < VG; ++j) {
-        q[j][2 * u] = (j < nv_g && ok) ? __ldg(Qg + j * a.vstride + e) : 0.0;
-        q[j][2 * u + 1] = (j < nv_g && ok) ? __ldg(Qg + j * a.vstride + e + half) : 0.0;
-      }
-    }
-    double bq[2 * UP], bp[2 * UP];
-#pragma unroll
-    for (int u = 0; u < UP; ++u) {
-      const int64_t e = b0 + slot + (int64_t)u * ES;
-      bq[2 * u] = bq[2 * u + 1] = bp[2 * u] = bp[2 * u + 1] = 0.0;
-      if (g == 0 && e < half) {
-        if (a.accumulate) {
-          bq[2 * u] = a.P[e];
-          bq[2 * u + 1] = a.P[e + half];
-          bp[2 * u] = a.Pnext[e];
-          bp[2 * u + 1] = a.Pnext[e + half];
-        } else {
-          const double pt = a.P[e], pb = a.P[e + half];
-          const double wb = a.wb[e];  // w = (p_b ; S)
-          bq[2 * u] = cq_p * pt;
-          bq[2 * u + 1] = cq_p * pb;
-          bp[2 * u] = cp_w * pb + cp_p * pt;
-          bp[2 * u + 1] = cp_w * wb + cp_p * pb;
-        }
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < 2 * UP; ++k) {
-      double sq = 0.0, sp = 0.0;
-#pragma unroll
-      for (int j = 0; j < VG; ++j) {
-        sq += cq[j] * q[j][k];
-        sp += cp[j] * q[j][k];
-      }
-      for (int off = 1; off < NG; off <<= 1) {
-        sq += __shfl_xor_sync(mask, sq, off);
-        sp += __shfl_xor_sync(mask, sp, off);
-      }
-      bq[k] += sq;
-      bp[k] += sp;
-    }
-#pragma unroll
-    for (int u = 0; u < UP; ++u) {
-      const int64_t e = b0 + slot + (int64_t)u * ES;
-      if (g == 0 && e < half) {
-        a.P[e] = dead ? 0.0 : bq[2 * u];
-        a.P[e + half] = dead ? 0.0 : bq[2 * u + 1];
-        a.Pnext[e] = dead ? 0.0 : bp[2 * u];
-        a.Pnext[e + half] = dead ? 0.0 : bp[2 * u + 1];
-      }
-    }
-  }
-}
-
-inline int next_pow2(int x) {
-  int p = 1;
-  while (p < x) p <<= 1;
-  return p;
-}
-
-inline void vs_shape_vg(int B, int nvec, int VG, int& ES, int& NG) {
-  NG = next_pow2(std::max(1, (nvec + VG - 1) / VG));
-  ES = std::max(B, (kBS / NG) / B * B);
-}
-
-
 }  // namespace
 
 int gram_grid(int64_t elems, int B) {
@@ -395,70 +227,8 @@ void gram_update_norm(GramArgs a, cudaStream_t s) {
   launch_vs<2>(a, s);
 }
 
-// pass A for nq <= 32 per launch; longer bases tile the vectors: tile [i0, i1) writes its a/b
-// pairs at offset 2*i0 and its trailing α/β/γ are overwritten by the next tile.
-void dcgs2_dots(Dcgs2Args a, cudaStream_t s) {
-  if (a.nq > kMaxVecPerLaunch) {
-    for (int i0 = 0; i0 < a.nq; i0 += kMaxVecPerLaunch) {
-      Dcgs2Args t = a;
-      t.nq = std::min(kMaxVecPerLaunch, a.nq - i0);
-      t.Q = a.Q + (int64_t)i0 * a.vstride;
-      t.sums_out = a.sums_out + (int64_t)2 * i0 * a.B;
-      dcgs2_dots(t, s);
-    }
-    return;
-  }
-  WL_LAUNCH("dcgs2_dots");
-  if (a.len != 2 * a.split) throw Error(1, "dcgs2: vectors must be stacked halves (len = 2 split)");
-  static const int VG = env_int("WL_DOTS_VG", 8), U = env_int("WL_DOTS_U", 2);  // tuning knobs
-  int ES, NG;
-  vs_shape_vg(a.B, a.nq, VG, ES, NG);
-  const int64_t total = a.len * a.B;
-  const int64_t items = (total + (int64_t)ES * U - 1) / ((int64_t)ES * U);
-  a.grid = (int)std::max<int64_t>(1, std::min<int64_t>(items, gram_grid(total, a.B)));
-  if (VG == 4) {
-    if (U == 4) dcgs2_dots_kernel<4, 4><<<a.grid, ES * NG, 0, s>>>(a, ES, NG);
-    else if (U == 1) dcgs2_dots_kernel<4, 1><<<a.grid, ES * NG, 0, s>>>(a, ES, NG);
-    else dcgs2_dots_kernel<4, 2><<<a.grid, ES * NG, 0, s>>>(a, ES, NG);
-  } else {
-    if (U == 4) dcgs2_dots_kernel<8, 4><<<a.grid, ES * NG, 0, s>>>(a, ES, NG);
-    else if (U == 1) dcgs2_dots_kernel<8, 1><<<a.grid, ES * NG, 0, s>>>(a, ES, NG);
-    else dcgs2_dots_kernel<8, 2><<<a.grid, ES * NG, 0, s>>>(a, ES, NG);
-  }
-  WL_CUDA(cudaGetLastError());
-  const int nout = (2 * a.nq + 3) * a.B;
-  note_launch("gram_reduce");
-  reduce_partials_kernel<<<(nout + 7) / 8, 256, 0, s>>>(a.partials, nout, a.grid, a.sums_out);
-  WL_CUDA(cudaGetLastError());
-}
-
-void dcgs2_update(Dcgs2Args a, cudaStream_t s) {
-  if (a.nq > kMaxVecPerLaunch) {
-    for (int i0 = 0; i0 < a.nq; i0 += kMaxVecPerLaunch) {
-      Dcgs2Args t = a;
-      t.nq = std::min(kMaxVecPerLaunch, a.nq - i0);
-      t.Q = a.Q + (int64_t)i0 * a.vstride;
-      t.coef_v = a.coef_v + (int64_t)2 * i0 * a.B;
-      t.accumulate = i0 > 0 ? 1 : a.accumulate;
-      dcgs2_update(t, s);
-    }
-    return;
-  }
-  WL_LAUNCH("dcgs2_update");
-  if (a.len != 2 * a.split) throw Error(1, "dcgs2: vectors must be stacked halves (len = 2 split)");
-  static const int VG = env_int("WL_UPD_VG", 8), UP = env_int("WL_UPD_U", 1);  // tuning knobs
-  int ES, NG;
-  vs_shape_vg(a.B, a.nq, VG, ES, NG);
-  const int64_t half = a.split * a.B;
-  const int64_t items = (half + (int64_t)ES * UP - 1) / ((int64_t)ES * UP);
-  a.grid = (int)std::max<int64_t>(1, std::min<int64_t>(items, gram_grid(half, a.B)));
-  if (VG == 4) {
-    if (UP == 2) dcgs2_update_kernel<4, 2><<<a.grid, ES * NG, 0, s>>>(a, ES, NG);
-    else dcgs2_update_kernel<4, 1><<<a.grid, ES * NG, 0, s>>>(a, ES, NG);
-  } else {
-    if (UP == 2) dcgs2_update_kernel<8, 2><<<a.grid, ES * NG, 0, s>>>(a, ES, NG);
-    else dcgs2_update_kernel<8, 1><<<a.grid, ES * NG, 0, s>>>(a, ES, NG);
-  }
+void reduce_partials(const double* partials, int nout, int G, double* sums_out, cudaStream_t s) {
+  reduce_partials_kernel<<<(nout + 7) / 8, 256, 0, s>>>(partials, nout, G, sums_out);
   WL_CUDA(cudaGetLastError());
 }
 

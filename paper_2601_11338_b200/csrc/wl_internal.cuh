@@ -80,20 +80,26 @@ int gram_grid(int64_t elems, int B);
 // finalised orthonormal q_0..q_{j-1} (Q) and p_j (P): once orthogonalised, unnormalised.
 //   pass A (dcgs2_dots):   a_i = q_i.p_j, b_i = q_i.w (i < j), α = p_j.p_j, β = p_j.w, γ = w.w,
 //                          w = Z p_j; sums layout [a_0 b_0 a_1 b_1 ... α β γ] x B (w null: b=β=γ=0)
-//   pass B (dcgs2_update): q_j = cq_p p_j + Σ cq_i q_i  (into P, in place),
+//   pass B (dcgs2_update): q_j = cq_p p_j + Σ cq_i q_i  (into Qout, which must not alias P),
 //                          p_{j+1} = cp_w w + cp_p p_j + Σ cp_i q_i  (into Pnext)
+// Basis vectors are addressed through a pointer table (slot i -> vector), passed by value.
+struct VecPtrs {
+  const double* p[kMaxKrylov + 2];
+};
 struct Dcgs2Args {
-  const double* Q; int64_t vstride; int nq;
+  VecPtrs Q; int nq;                  // q_0 .. q_{nq-1}
   int64_t len; int B;
-  double* P;                          // p_j (pass B overwrites it with q_j)
+  const double* P;                    // p_j
   const double* wa; int64_t split; const double* wb;   // w two-source (wa null: no w)
+  double* Qout;                       // pass B: q_j
   double* Pnext;                      // pass B: p_{j+1}
   const double* coef_v;               // pass B: [cq_i, cp_i] interleaved per vector, x B
   const double* coef_s;               // pass B: [cq_p, cp_p, cp_w] x B
-  int accumulate;                     // pass B vector tiles after the first: add to P / Pnext
+  int accumulate;                     // pass B vector tiles after the first: add to Qout / Pnext
   double* partials; double* sums_out;
   int grid;
 };
+void reduce_partials(const double* partials, int nout, int G, double* sums_out, cudaStream_t s);
 void dcgs2_dots(Dcgs2Args a, cudaStream_t s);
 void dcgs2_update(Dcgs2Args a, cudaStream_t s);
 void dcgs2_coeffs(const double* sums, int j, int B, int K, double btol, int final_pass, int reorth, double* H,
@@ -134,7 +140,7 @@ void finalize_step(const double* sums1, const double* sums2, const double* sums3
 //          2 = t' (Σ comb_i Q_i,top) for V = 1
 // V column of batch column c is vcol[c]; t' column is tcol[c]; internal row r is user row
 // perm[r] (modes 0/1 read V and write out in user order; mode 2 writes t' in internal order).
-void combine(int mode, const double* Q, int64_t vstride, int nvec, int64_t n, int B,
+void combine(int mode, const VecPtrs& Q, int nvec, int64_t n, int B,
              const double* comb, const double* V, int64_t ldv, const int* vcol, double c0,
              const double* tprime, int64_t ldt, const int* tcol, double* out, int64_t ldo,
              const int32_t* perm, cudaStream_t s);
