@@ -155,6 +155,7 @@ struct wl_operator {
   DArr<int32_t> small_rows, medium_rows;
   DArr<int4> chunks;
   int n_small = 0, n_medium = 0, n_chunks = 0;
+  int small_first = -1;  // small rows form the contiguous id range [small_first, +n_small) (relabelled)
 };
 
 struct wl_workspace {
@@ -236,6 +237,7 @@ void do_spmv(const wl_operator* op, wl_workspace* ws, const double* y, const dou
   a.n_loc = op->n_loc;
   a.small_rows = op->small_rows.p;
   a.n_small = op->n_small;
+  a.small_first = op->small_first;
   a.medium_rows = op->medium_rows.p;
   a.n_medium = op->n_medium;
   a.chunks = op->chunks.p;
@@ -542,6 +544,7 @@ void build_operator(wl_operator* op, const int64_t* rp_in, const int32_t* ci_in,
     }
     op->n_small = (int)sm.size();
     op->n_medium = (int)md.size();
+    op->small_first = (!sm.empty() && sm.back() - sm.front() + 1 == (int32_t)sm.size()) ? sm.front() : -1;
     op->n_chunks = (int)ch.size();
     op->small_rows.alloc(std::max<size_t>(1, sm.size()));
     op->medium_rows.alloc(std::max<size_t>(1, md.size()));

@@ -20,6 +20,7 @@
 // is uniform within a lane group.
 #include "wl_internal.cuh"
 
+#include <algorithm>
 #include <climits>
 #include <cstdlib>
 
@@ -250,6 +251,81 @@ __global__ void __launch_bounds__(kThreads) spmv_async_kernel(SpmvArgs a) {
   if (lane == 0) a.row_ticket[ch.w] = 0u;
 }
 
+
+// ---- small rows with contiguous ids (the degree-sorted layout): one warp per batch of 32 rows ----
+// The per-row path above pays a chain of dependent memory latencies per row (row id -> rowptr ->
+// col -> gather).  Here a warp loads the batch's 33 row starts with one coalesced load, stages the
+// batch's nonzero column ids (contiguous) and its x rows in shared memory with a second, and
+// each lane group then walks its share of the batch's nonzeros in rounds of kU gathers,
+// flushing rows as their ranges end: ~1 latency per kU gathers instead of ~3 per row.
+template <int kU, bool HALO>
+__global__ void __launch_bounds__(kThreads) spmv_small_batched_kernel(SpmvArgs a) {
+  extern __shared__ __align__(16) int s_small[];
+  constexpr int kColCap = 32 * kSmallMax;  // max nonzeros of a 32-row batch
+  constexpr int kIntsPerWarp = kColCap + 40;
+  const int B = a.B, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gpw = 32 / B, gi = lane / B, c = lane - gi * B;
+  const bool lane_ok = gi < gpw;
+  const int cc = lane_ok ? c : 0;
+  int* scol = s_small + warp * kIntsPerWarp;
+  int* srow = scol + kColCap;
+  double* sx = reinterpret_cast<double*>(s_small + kWarps * kIntsPerWarp) + warp * 32 * B;
+  Ctx<kU, HALO> ctx{a, cc, a.g0 ? a.g0[cc] : 0.0, a.g1 ? a.g1[cc] : 0.0, a.scale ? a.scale[cc] : 1.0,
+                    a.y + cc, a.yh + cc, (int)a.ldy, (int)a.ldh};
+  const int nb = (a.n_small + 31) / 32;
+  for (int bt = blockIdx.x * kWarps + warp; bt < nb; bt += gridDim.x * kWarps) {
+    const int r0 = a.small_first + bt * 32;
+    const int nr = min(32, a.n_small - bt * 32);
+    const int zl = __ldg(a.rowptr + r0 + min(lane, nr));
+    const int Z1 = __ldg(a.rowptr + r0 + nr);
+    const int Z0 = __shfl_sync(0xffffffffu, zl, 0);
+    srow[lane] = zl - Z0;  // rows >= nr: empty ranges at the end
+    if (lane == 0) srow[32] = Z1 - Z0;
+    const int T = Z1 - Z0;
+#pragma unroll 4
+    for (int p = lane; p < T; p += 32) scol[p] = __ldg(a.col + Z0 + p);
+    if (a.x)
+      for (int e = lane; e < nr * B; e += 32) sx[e] = __ldg(a.x + (int64_t)r0 * B + e);
+    __syncwarp();
+    if (lane_ok) {
+      const int ia = gi * nr / gpw, ib = (gi + 1) * nr / gpw;  // this group's rows
+      auto flush = [&](int i, double acc) {
+        double o = acc;
+        if (a.x) o += (ctx.g0 + ctx.g1 * (double)(srow[i + 1] - srow[i])) * sx[i * B + c];
+        a.out[(int64_t)(r0 + i) * a.ldo + c] = ctx.sc * o;
+      };
+      int cur = ia, rend = srow[ia + 1];
+      const int P1 = srow[ib];
+      double acc = 0.0;
+      for (int p = srow[ia]; p < P1; p += kU) {
+        double v[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) v[u] = p + u < P1 ? ctx.gather(scol[p + u]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          if (p + u < P1) {
+            while (p + u >= rend) {
+              flush(cur, acc);
+              acc = 0.0;
+              rend = srow[++cur + 1];
+            }
+            acc += v[u];
+          }
+        }
+      }
+      for (; cur < ib; ++cur) {  // the last row with nonzeros and any empty rows after it
+        flush(cur, acc);
+        acc = 0.0;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+size_t small_batched_smem(int B) {
+  return (size_t)kWarps * ((32 * kSmallMax + 40) * sizeof(int) + 32 * B * sizeof(double));
+}
+
 }  // namespace
 
 void spmv(const SpmvArgs& a0, cudaStream_t s) {
@@ -299,6 +375,58 @@ void spmv(const SpmvArgs& a0, cudaStream_t s) {
       const int g = a.nblk_medium + nblk_hub;
       spmv_async_kernel<S><<<g, kThreads, smem, s>>>(t);
       WL_CUDA(cudaGetLastError());
+    }
+    return;
+  }
+  // small rows with contiguous ids (x rows contiguous too): the batched kernel takes them
+  static const bool batched_on = [] { const char* v = getenv("WL_SPMV_BATCHED"); return v ? atoi(v) != 0 : true; }();
+  const bool batched = batched_on && a.small_first >= 0 && a.n_small > 0 && (a.x == nullptr || a.ldx == a.B);
+  auto go_small = [&]() {
+    auto kern = halo ? spmv_small_batched_kernel<8, true> : spmv_small_batched_kernel<8, false>;
+    const size_t smem = small_batched_smem(a.B);
+    static bool attr[2] = {false, false};
+    if (!attr[halo]) {
+      WL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)small_batched_smem(kMaxCols)));
+      attr[halo] = true;
+    }
+    int occ = 0;
+    WL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem));
+    static int sms = 0;
+    if (!sms) {
+      int dev = 0;
+      WL_CUDA(cudaGetDevice(&dev));
+      WL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const int nb = (a.n_small + 31) / 32;
+    const int g = std::max(1, std::min((nb + kWarps - 1) / kWarps, sms * std::max(occ, 1)));
+    kern<<<g, kThreads, smem, s>>>(a);
+    WL_CUDA(cudaGetLastError());
+  };
+  if (batched) {
+    SpmvArgs t = a;
+    t.n_small = 0;
+    t.nblk_small = 0;
+    if (!split) {
+      WL_LAUNCH("spmv_binned");
+      go_small();
+      if (grid - a.nblk_small > 0) go(t, grid - a.nblk_small);
+      return;
+    }
+    {
+      WL_LAUNCH("spmv_small");
+      go_small();
+    }
+    {
+      WL_LAUNCH("spmv_medium");
+      SpmvArgs m = t;
+      m.n_chunks = 0;
+      if (m.nblk_medium) go(m, m.nblk_medium);
+    }
+    {
+      WL_LAUNCH("spmv_hub");
+      SpmvArgs h = t;
+      h.n_medium = 0; h.nblk_medium = 0;
+      if (nblk_hub) go(h, nblk_hub);
     }
     return;
   }
