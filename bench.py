@@ -204,7 +204,6 @@ def run_walklap(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    wl.profile_enable(True)
     l0 = wl.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
@@ -214,9 +213,32 @@ def run_walklap(args):
         ev1.record(stream)
         torch.cuda.synchronize()
     launches = wl.launch_count() - l0
+    ms = ev0.elapsed_time(ev1) / args.steps
+    # per-kernel table: the same K steps again with per-launch-scope CUDA events (kept out of the timed region)
+    torch.cuda.synchronize()
+    wl.profile_enable(True)
+    for _ in range(args.steps):
+        op.apply(V, out=out, ws=ws)
+    torch.cuda.synchronize()
     wl.profile_enable(False)
     prof = wl.profile_collect()
-    ms = ev0.elapsed_time(ev1) / args.steps
+    graph_info = None
+    if args.graph:
+        # the whole step captured as one CUDA graph (no host synchronisation inside an action)
+        cg = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(cg):
+            op.apply(V, out=out, ws=ws)
+        cg.replay()
+        torch.cuda.synchronize()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(args.steps):
+            cg.replay()
+        g1.record(stream)
+        torch.cuda.synchronize()
+        gms = g0.elapsed_time(g1) / args.steps
+        graph_info = {"ms_per_step": gms, "value": op.n_theta * b / (gms / 1e3)}
+        del cg
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -289,6 +311,8 @@ def run_walklap(args):
                         for k, v in sorted(kernels.items(), key=lambda kv: -kv[1]["ms_per_step"])},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
         }
+        if graph_info:
+            line["cuda_graph"] = graph_info
         print(json.dumps(line), flush=True)
     op.close()
     if comm:
@@ -375,6 +399,7 @@ def main():
     ap.add_argument("--rho-k", type=int, default=60)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--graph", action="store_true", help="also time the step captured as one CUDA graph")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warning: contract requires >= 3 warm-up steps")

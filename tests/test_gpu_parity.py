@@ -298,3 +298,35 @@ def test_full_c3_road_diffusion(wl):
     sub = taus <= 10.0
     ref = chebyshev.diffusion(g, 1.0, f, x0, taus[sub], rA)
     assert relerr(X[:, sub], ref).max() < TOL
+
+
+def test_apply_captured_in_cuda_graph(wl):
+    """The whole 𝕃·V action is stream-ordered with no host synchronisation, so it captures into one CUDA graph
+    (SURVEY §8(d) timing protocol); replays on new inputs match the oracle and the eager call bit for bit."""
+    g = gg.rmat(14, 12000, 150000, seed=21, perm_seed=22)
+    rA = S.rho_A(g)
+    f = C.exp(1.0 / rA)
+    thetas = [0.0, 0.5, 1.0]
+    b = 2
+    op = wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=thetas, f=("exp", f.param))
+    ws = op.workspace(b)
+    V = torch.from_numpy(gg.vectors(g.n, b, 5)).cuda()
+    out = torch.empty((g.n, len(thetas) * b), dtype=torch.float64, device="cuda")
+    op.apply(V, out=out, ws=ws)  # warm-up outside capture (one-time kernel attributes)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        op.apply(V, out=out, ws=ws)
+    for seed in (6, 7):
+        Vn = gg.vectors(g.n, b, seed)
+        V.copy_(torch.from_numpy(Vn))
+        graph.replay()
+        torch.cuda.synchronize()
+        got = out.cpu().numpy()
+        eager = op.apply(V, ws=ws).cpu().numpy()
+        assert np.array_equal(got, eager)
+        for i, th in enumerate(thetas):
+            ref = S.laplacian_apply(g, 1.0 - th, f, Vn, rA)
+            assert relerr(got[:, i * b:(i + 1) * b], ref).max() < TOL
+    ws.close()
+    op.close()
