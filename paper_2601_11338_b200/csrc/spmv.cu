@@ -150,108 +150,6 @@ __global__ void __launch_bounds__(kThreads) spmv_binned_kernel(SpmvArgs a) {
   }
 }
 
-// ---- medium rows and hub chunks through shared memory (cp.async / LDGSTS) -------------------
-// The register-gather path keeps every in-flight gather in a register, which caps the bytes in
-// flight per SM (~56 KB measured on C4 at B = 11, latency-bound).  Here a warp streams its
-// nonzero range in rounds of 32 nonzeros: for round k it issues cp.async copies of the 32 gathered
-// rows (32 x B doubles; lanes copy consecutive doubles of a row) into stage k % S of a per-warp
-// shared-memory ring, and accumulates round k - S + 1 from shared memory (lane c owns column c).
-// In-flight data lives in shared memory, not registers.
-__device__ inline void cp_async8(double* smem_dst, const double* gsrc) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(smem_dst)),
-               "l"(gsrc)
-               : "memory");
-}
-__device__ inline void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ inline void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-template <int S>
-__device__ inline double async_range_sum(const SpmvArgs& a, int z0, int z1, double* sbuf, int lane) {
-  const int B = a.B;
-  const int per = 32 * B;  // doubles per stage
-  const int nr = (z1 - z0 + 31) / 32;
-  const int q32 = 32 / B, r32 = 32 % B;
-  auto issue = [&](int k) {
-    if (k < nr) {
-      const int z = z0 + k * 32 + lane;
-      const int mycol = z < z1 ? __ldg(a.col + z) : -1;
-      double* st = sbuf + (k % S) * per;
-      int r = lane / B, c = lane - (lane / B) * B;  // element f = lane + 32 i -> (row r, column c)
-      for (int i = 0; i < B; ++i) {
-        const int cl = __shfl_sync(0xffffffffu, mycol, r);
-        double* dst = st + r * B + c;
-        if (cl < 0) *dst = 0.0;
-        else if (cl < a.n_loc) cp_async8(dst, a.y + (int64_t)cl * a.ldy + c);
-        else cp_async8(dst, a.yh + (int64_t)(cl - a.n_loc) * a.ldh + c);
-        r += q32;
-        c += r32;
-        if (c >= B) { c -= B; ++r; }
-      }
-    }
-    cp_async_commit();
-  };
-#pragma unroll
-  for (int k = 0; k < S - 1; ++k) issue(k);
-  double acc = 0.0;
-  for (int k = 0; k < nr; ++k) {
-    issue(k + S - 1);
-    cp_async_wait<S - 1>();
-    __syncwarp();
-    if (lane < B) {
-      const double* st = sbuf + (k % S) * per + lane;
-      const int rows = min(32, z1 - z0 - k * 32);
-      for (int r = 0; r < rows; ++r) acc += st[r * B];
-    }
-    __syncwarp();
-  }
-  cp_async_wait<0>();
-  return acc;  // valid in lanes < B
-}
-
-template <int S>
-__global__ void __launch_bounds__(kThreads) spmv_async_kernel(SpmvArgs a) {
-  extern __shared__ double s_dyn[];
-  const int B = a.B;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double* sbuf = s_dyn + (int64_t)warp * S * 32 * B;
-  const int cc = lane < B ? lane : 0;
-  Ctx<8, true> ctx{a, cc, a.g0 ? a.g0[cc] : 0.0, a.g1 ? a.g1[cc] : 0.0, a.scale ? a.scale[cc] : 1.0,
-                   a.y + cc, a.yh + cc, (int)a.ldy, (int)a.ldh};
-  int blk = blockIdx.x;
-  if (blk < a.nblk_medium) {
-    const int idx = blk * kWarps + warp;
-    if (idx >= a.n_medium) return;
-    const int r = a.medium_rows[idx];
-    const int z0 = __ldg(a.rowptr + r), z1 = __ldg(a.rowptr + r + 1);
-    const double sum = async_range_sum<S>(a, z0, z1, sbuf, lane);
-    if (lane < B) ctx.write(r, z1 - z0, sum);
-    return;
-  }
-  blk -= a.nblk_medium;
-  const int idx = blk * kWarps + warp;
-  if (idx >= a.n_chunks) return;
-  const int4 ch = a.chunks[idx];
-  const double sum = async_range_sum<S>(a, ch.y, ch.z, sbuf, lane);
-  if (lane < B) a.chunk_part[(int64_t)idx * B + lane] = sum;
-  __threadfence();
-  __syncwarp();
-  unsigned ticket = 0;
-  const int z0r = __ldg(a.rowptr + ch.x), z1r = __ldg(a.rowptr + ch.x + 1);
-  const int nch = (z1r - z0r + kHubChunk - 1) / kHubChunk;
-  if (lane == 0) ticket = atomicAdd(a.row_ticket + ch.w, 1u);
-  ticket = __shfl_sync(0xffffffffu, ticket, 0);
-  if (ticket != (unsigned)(nch - 1)) return;
-  __threadfence();
-  if (lane < B) {
-    double tot = 0.0;
-    for (int k = 0; k < nch; ++k) tot += __ldcg(a.chunk_part + (int64_t)(ch.w + k) * B + lane);
-    ctx.write(ch.x, z1r - z0r, tot);
-  }
-  if (lane == 0) a.row_ticket[ch.w] = 0u;
-}
-
-
 // ---- small rows with contiguous ids (the degree-sorted layout): one warp per batch of 32 rows ----
 // The per-row path above pays a chain of dependent memory latencies per row (row id -> rowptr ->
 // col -> gather).  Here a warp loads the batch's 33 row starts with one coalesced load, stages the
@@ -352,32 +250,6 @@ void spmv(const SpmvArgs& a0, cudaStream_t s) {
     }
     WL_CUDA(cudaGetLastError());
   };
-  static const int async_min_b = [] { const char* v = getenv("WL_SPMV_ASYNC"); return v ? atoi(v) : 99; }();  // off by default: measured slower
-  if (a.B >= async_min_b && (a.n_medium + a.n_chunks) > 0) {
-    // small rows: register path; medium rows + hub chunks: shared-memory async path
-    constexpr int S = 3;
-    const size_t smem = (size_t)kWarps * S * 32 * a.B * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-      WL_CUDA(cudaFuncSetAttribute(spmv_async_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      attr = true;
-    }
-    {
-      WL_LAUNCH(split ? "spmv_small" : "spmv_binned");
-      SpmvArgs t = a;
-      t.n_medium = 0; t.nblk_medium = 0; t.n_chunks = 0;
-      if (t.nblk_small) go(t, t.nblk_small);
-    }
-    {
-      WL_LAUNCH(split ? "spmv_async" : "spmv_binned");
-      SpmvArgs t = a;
-      t.n_small = 0; t.nblk_small = 0;
-      const int g = a.nblk_medium + nblk_hub;
-      spmv_async_kernel<S><<<g, kThreads, smem, s>>>(t);
-      WL_CUDA(cudaGetLastError());
-    }
-    return;
-  }
   // small rows with contiguous ids (x rows contiguous too): the batched kernel takes them
   static const bool batched_on = [] { const char* v = getenv("WL_SPMV_BATCHED"); return v ? atoi(v) != 0 : true; }();
   const bool batched = batched_on && a.small_first >= 0 && a.n_small > 0 && (a.x == nullptr || a.ldx == a.B);
