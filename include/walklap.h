@@ -40,8 +40,8 @@ typedef enum {
   WL_EGRAPH = 2,      /* CSR not simple/symmetric-compatible: unsorted row_ptr, column out of range,
                          self loop or duplicate entry (simple graphs only) */
   WL_EDIVERGE = 3,    /* resolvent with α·ρ ≥ 1: the series of Prop. pro:whe-we-converge diverges
-                         (Remark P:390-392) */
-  WL_ENOCONV = 4,     /* reserved: a-posteriori Krylov check failed (best iterate still written) */
+                         (Remark P:390-392); CG solver: 𝒜_θ(α) not positive definite */
+  WL_ENOCONV = 4,     /* CG solver: a column did not reach cg_tol within cg_maxit (best iterate written) */
   WL_ENOMEM = 5,      /* device allocation failed */
   WL_ECUDA = 6,       /* CUDA runtime error (message has the CUDA error string) */
   WL_ENCCL = 7,       /* NCCL error */
@@ -82,7 +82,19 @@ typedef struct {
                            WL_EDIVERGE (Prop. pro:whe-we-converge).  0 = no check (default). */
   int32_t relabel;      /* 1 (default): relabel the local rows by decreasing degree internally
                            (gather locality); results are returned in the caller's row order */
+  int32_t solver;       /* WL_SOLVER_KRYLOV (default): polynomial Krylov on Z for every f.
+                           WL_SOLVER_CG (resolvent only, α > 0): φ_θ = (1-μ²α²) 𝒜_θ(α)^{-1} with the
+                           deformed Laplacian 𝒜_θ(α) = (1-μ²α²)I - αA + μα²D (eq:deformed at μ = 1,
+                           P:436-441), solved by Jacobi-preconditioned conjugate gradients (§4.2 P:545-551;
+                           SPD when α ρ(Z_θ) < 1, Prop. prop:CGworks).  Actions then synchronize the
+                           stream every cg_check iterations; a non-SPD system returns WL_EDIVERGE and
+                           columns not converged after cg_maxit return WL_ENOCONV (best iterate written). */
+  double cg_tol;        /* relative residual ||b - 𝒜x|| <= cg_tol ||b|| per column (default 1e-9) */
+  int32_t cg_maxit;     /* iteration cap (default 1000) */
+  int32_t cg_check;     /* convergence is read back every cg_check iterations (default 8) */
 } wl_opts;
+
+typedef enum { WL_SOLVER_KRYLOV = 0, WL_SOLVER_CG = 1 } wl_solver;
 
 typedef struct wl_comm wl_comm;
 typedef struct wl_operator wl_operator;

@@ -169,12 +169,19 @@ struct wl_workspace {
   DArr<double> colp;  // g0z, g1z, g0s, g1s (kMaxCols each)
   DArr<double> chunk_part;
   DArr<unsigned int> row_ticket;
+  // conjugate-gradient solver state (cg.cu): per column constants, scalars, |b|², iterations, flags
+  DArr<double> cg_cs, cg_sc, cg_bb;
+  DArr<int> cg_iters, cg_flags;
+  int* cg_flags_host = nullptr;  // pinned
   // host-buffer entry point
   DArr<double> hV, hLV;
   // diffusion (outer Lanczos)
   int kout_alloc = 0;
   DArr<double> oQ, ow, oH, os, on0, osums1, osums2, osums3, otau, oY, oscratch;
   DArr<int> okeff;
+  ~wl_workspace() {
+    if (cg_flags_host) cudaFreeHost(cg_flags_host);
+  }
 };
 
 namespace wl {
@@ -273,8 +280,8 @@ void spmv_scratch(const wl_operator* op, wl_workspace* ws, int B) {
 // `out` points at column gstart.  mode: 0 = φV, 1 = 𝕃V, 2 = t' (V = ones).
 // user_order: V / out rows are in the caller's order (gathered / scattered through op->perm);
 // false for the internal-order vectors of the outer diffusion Lanczos.
-void run_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double* V, int64_t ldv, int b,
-               int gstart, int B, double* out, int64_t ldo, cudaStream_t s, bool user_order = true) {
+void krylov_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double* V, int64_t ldv, int b,
+                  int gstart, int B, double* out, int64_t ldo, cudaStream_t s, bool user_order) {
   const int32_t* perm = user_order ? op->perm.p : nullptr;
   const int64_t n = op->n_loc;
   const int K = ws->K;
@@ -368,6 +375,69 @@ void run_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double* 
           op->tprime.p, op->n_theta, ws->tcol.p, out, ldo, perm, s);
 }
 
+
+// Resolvent action by Jacobi-preconditioned CG on the deformed Laplacian (cg.cu; opts.solver ==
+// WL_SOLVER_CG): x = 𝒜_θ(α)^{-1} V per column, then φ V = (1-μ²α²) x.  Vector roles reuse the
+// Krylov basis memory: x, r, p, q.  Synchronizes every opts.cg_check iterations.
+void cg_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double* V, int64_t ldv, int b, int gstart,
+              int B, double* out, int64_t ldo, cudaStream_t s, bool user_order) {
+  const int32_t* perm = user_order ? op->perm.p : nullptr;
+  const int64_t n = op->n_loc;
+  double* g0 = ws->colp.p;
+  double* g1 = g0 + kMaxCols;
+  double* scale = g1 + kMaxCols;
+  cg_setup(op->mu_dev.p, op->fparam, op->opts.cg_tol, gstart, b, B, ws->cg_cs.p, g0, g1, scale, ws->vcol.p,
+           ws->tcol.p, s);
+  batch_inputs(V, ldv, B, n, ws->Vb.p, ws->vcol.p, perm, s);
+  CgArgs a{};
+  a.n = n;
+  a.B = B;
+  a.rowptr = op->rowptr.p;
+  a.cs = ws->cg_cs.p;
+  a.b = ws->Vb.p;
+  a.x = ws->basis.p;
+  a.r = a.x + n * B;
+  a.p = a.r + n * B;
+  a.q = a.p + n * B;
+  a.partials = ws->partials.p;
+  a.sums = ws->sums1.p;
+  a.sc = ws->cg_sc.p;
+  a.bb = ws->cg_bb.p;
+  a.iters = ws->cg_iters.p;
+  a.flags = ws->cg_flags.p;
+  WL_CUDA(cudaMemsetAsync(ws->cg_flags.p, 0, 2 * sizeof(int), s));
+  cg_init(a, s);
+  allreduce(op, a.sums, (size_t)2 * B, s);
+  cg_scalar(0, a, s);
+  bool done = false;
+  for (int it = 0; it < op->opts.cg_maxit && !done; ++it) {
+    halo_exchange(op, ws, a.p, B, B, s);
+    do_spmv(op, ws, a.p, a.p, g0, g1, scale, a.q, B, s);  // q = 𝒜 p
+    cg_dot(a, s);
+    allreduce(op, a.sums, (size_t)B, s);
+    cg_scalar(1, a, s);
+    cg_update(a, s);
+    allreduce(op, a.sums, (size_t)2 * B, s);
+    cg_scalar(2, a, s);
+    cg_direction(a, s);
+    if ((it + 1) % op->opts.cg_check == 0 || it + 1 == op->opts.cg_maxit) {
+      WL_CUDA(cudaMemcpyAsync(ws->cg_flags_host, ws->cg_flags.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+      WL_CUDA(cudaStreamSynchronize(s));
+      if (ws->cg_flags_host[0] & 1) throw Error(WL_EDIVERGE, "CG: deformed Laplacian not positive definite (α ρ(Z_θ) >= 1?)");
+      done = ws->cg_flags_host[1] == 0;
+    }
+  }
+  cg_combine(mode, a.x, n, B, ws->cg_cs.p, V, ldv, ws->vcol.p, op->c0, op->tprime.p, op->n_theta, ws->tcol.p, out,
+             ldo, perm, s);
+  if (!done) throw Error(WL_ENOCONV, "CG: residual above cg_tol after cg_maxit iterations (best iterate written)");
+}
+
+void run_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double* V, int64_t ldv, int b, int gstart,
+               int B, double* out, int64_t ldo, cudaStream_t s, bool user_order = true) {
+  if (op->opts.solver == WL_SOLVER_CG) cg_chunk(op, ws, mode, V, ldv, b, gstart, B, out, ldo, s, user_order);
+  else krylov_chunk(op, ws, mode, V, ldv, b, gstart, B, out, ldo, s, user_order);
+}
+
 void run_action(const wl_operator* op, wl_workspace* ws, int mode, const double* V, int64_t ldv, int b,
                 double* out, int64_t ldo, cudaStream_t s) {
   const int G = op->n_theta * b;
@@ -384,7 +454,8 @@ void workspace_alloc(wl_workspace* ws, const wl_operator* op, int max_b) {
   ws->Bmax = std::max(1, std::min({op->opts.max_cols, kMaxCols, op->n_theta * max_b}));
   const int64_t n = op->n_loc;
   const int B = ws->Bmax, K = ws->K;
-  ws->basis.alloc((size_t)(K + 2) * 2 * (n + 1) * B);  // halves padded by <= 1 phantom row
+  if (op->opts.solver == WL_SOLVER_CG) ws->basis.alloc((size_t)4 * (n + 1) * B);  // x, r, p, q
+  else ws->basis.alloc((size_t)(K + 2) * 2 * (n + 1) * B);  // halves padded by <= 1 phantom row
   ws->S.alloc((size_t)(n + 1) * B);
   ws->Vb.alloc((size_t)n * B);
   if (op->n_halo > 0) ws->halo_recv.alloc((size_t)op->n_halo * B);
@@ -409,6 +480,12 @@ void workspace_alloc(wl_workspace* ws, const wl_operator* op, int max_b) {
   ws->vcol.alloc(kMaxCols);
   ws->tcol.alloc(kMaxCols);
   ws->colp.alloc(4 * kMaxCols);
+  ws->cg_cs.alloc(8 * kMaxCols);
+  ws->cg_sc.alloc(4 * kMaxCols);
+  ws->cg_bb.alloc(kMaxCols);
+  ws->cg_iters.alloc(kMaxCols);
+  ws->cg_flags.alloc(2);
+  if (!ws->cg_flags_host) WL_CUDA(cudaMallocHost(&ws->cg_flags_host, 2 * sizeof(int)));
   spmv_scratch(op, ws, B);
   WL_CUDA(cudaDeviceSynchronize());
 }
@@ -748,6 +825,10 @@ void wl_opts_default(wl_opts* o) {
   o->breakdown_tol = 1e-12;
   o->rho_bound = 0.0;
   o->relabel = 1;
+  o->solver = WL_SOLVER_KRYLOV;
+  o->cg_tol = 1e-9;
+  o->cg_maxit = 1000;
+  o->cg_check = 8;
 }
 
 wl_status wl_nccl_unique_id(void* out128) {
@@ -852,6 +933,13 @@ wl_status wl_operator_create(wl_comm* comm, int64_t n_global, int64_t row_begin,
     if (op->opts.krylov_dim < 1 || op->opts.krylov_dim > kMaxKrylov) throw Error(WL_EINVAL, "krylov_dim must be in [1, 64]");
     if (op->opts.max_cols < 1 || op->opts.max_cols > kMaxCols) throw Error(WL_EINVAL, "max_cols must be in [1, 32]");
     if (!(op->opts.breakdown_tol >= 0.0)) throw Error(WL_EINVAL, "breakdown_tol < 0");
+    if (op->opts.solver != WL_SOLVER_KRYLOV && op->opts.solver != WL_SOLVER_CG) throw Error(WL_EINVAL, "unknown solver");
+    if (op->opts.solver == WL_SOLVER_CG) {
+      if (f->kind != WL_F_RESOLVENT || !(f->param > 0.0))
+        throw Error(WL_EINVAL, "WL_SOLVER_CG needs the resolvent with α > 0");
+      if (!(op->opts.cg_tol > 0.0) || op->opts.cg_maxit < 1 || op->opts.cg_check < 1)
+        throw Error(WL_EINVAL, "cg_tol > 0, cg_maxit >= 1, cg_check >= 1 required");
+    }
     // θ values (θ = 1 - μ)
     if (variant == WL_WALK || variant == WL_NBT) {
       if (n_theta != 1) throw Error(WL_EINVAL, "WL_WALK/WL_NBT take exactly one θ");

@@ -106,6 +106,30 @@ void dcgs2_update(Dcgs2Args a, cudaStream_t s);
 void dcgs2_coeffs(const double* sums, int j, int B, int K, double btol, int final_pass, int reorth, double* H,
                   double* ref, double* n0, int* keff, double* coef_v, double* coef_s, cudaStream_t s);
 
+// ---------------------------------------------------------------- resolvent by PCG (cg.cu)
+struct CgArgs {
+  int64_t n; int B;
+  const int32_t* rowptr;       // degrees for the Jacobi preconditioner
+  const double* cs;            // per column constants (cg_setup)
+  const double* b;             // right-hand sides, n x B
+  double *x, *r, *p, *q;       // n x B each
+  double* partials; double* sums;
+  double* sc;                  // per column scalars: rz, alpha, beta, active
+  double* bb;                  // per column ||b||^2
+  int* iters;                  // per column iteration counts
+  int* flags;                  // [0] bit 0: not positive definite; [1] active columns
+};
+void cg_setup(const double* mu, double alpha, double tol, int gstart, int b, int B, double* cs, double* g0,
+              double* g1, double* scale, int* vcol, int* tcol, cudaStream_t s);
+void cg_init(CgArgs a, cudaStream_t s);
+void cg_dot(CgArgs a, cudaStream_t s);
+void cg_update(CgArgs a, cudaStream_t s);
+void cg_direction(CgArgs a, cudaStream_t s);
+void cg_scalar(int which, const CgArgs& a, cudaStream_t s);
+void cg_combine(int mode, const double* x, int64_t n, int B, const double* cs, const double* V, int64_t ldv,
+                const int* vcol, double c0, const double* tprime, int64_t ldt, const int* tcol, double* out,
+                int64_t ldo, const int32_t* perm, cudaStream_t s);
+
 // ---------------------------------------------------------------- small dense functions
 // Per column c (problem), m = keff[c]: y_c = f_1(H_m) e_1 for the Arnoldi matrix H.
 // kind 3 (outer diffusion): problem p uses column 0's H and computes exp(-tau[p] H_m) e_1;

@@ -1,0 +1,147 @@
+"""GPU parity of the resolvent solver by preconditioned CG vs the CPU oracle.
+
+φ_θ = (1-μ²α²) 𝒜_θ(α)^{-1} with 𝒜_θ(α) = (1-μ²α²)I - αA + μα²D (eq:deformed at μ = 1);
+the oracle side is the dense closed form (oracle/dense.py, pinned to Fig. 4b and to the series) and
+the matrix-free series (oracle/series.py).  α follows §5.3: log-spaced in [1e-3, 10^-1/2]
+scaled by the dominant eigenvalue; here by ρ(A) ≥ ρ(Z_θ) (R8), so 𝒜 is SPD for every θ.
+Parity tests run CG to a relative residual of 1e-13 and compare at the north-star 1e-10; the
+paper's tolerance (1e-9) is checked against the residual bound it promises.
+"""
+import numpy as np
+import pytest
+
+import graphgen as gg
+from oracle import coeffs as C
+from oracle import dense as D
+from oracle import series as S
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+ALPHAS = np.logspace(-3, -0.5, 4)  # x ρ^{-1}
+
+
+@pytest.fixture(scope="module")
+def wl():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2601_11338_b200 as wl
+    from paper_2601_11338_b200 import build
+    build.build()
+    wl.load()
+    return wl
+
+
+def relerr(got, ref):
+    got, ref = np.atleast_2d(got.T).T, np.atleast_2d(ref.T).T
+    den = np.linalg.norm(ref, axis=0)
+    den[den == 0] = 1.0
+    return np.linalg.norm(got - ref, axis=0) / den
+
+
+@pytest.mark.parametrize("a", ALPHAS)
+def test_karate_cg_vs_dense_closed_form(wl, a):
+    g = gg.karate()
+    A = D.adjacency(g)
+    alpha = a / D.rho_A(A)
+    thetas = [1.0, 0.5, 0.0]
+    b = 3
+    V = gg.vectors(g.n, b, 101)
+    op = wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=thetas, f=("resolvent", alpha), solver="cg", cg_tol=1e-13)
+    LV = op.apply(torch.from_numpy(V).cuda()).cpu().numpy()
+    PV = op.phi_apply(torch.from_numpy(V).cuda()).cpu().numpy()
+    t = op.diag_shift().cpu().numpy()
+    for i, th in enumerate(thetas):
+        ph = D.phi_resolvent_closed(A, 1.0 - th, alpha)
+        sl = slice(i * b, (i + 1) * b)
+        assert relerr(LV[:, sl], D.walk_laplacian(ph) @ V).max() < TOL
+        assert relerr(PV[:, sl], ph @ V).max() < TOL
+        assert relerr(t[:, i], ph.sum(1)).max() < TOL
+    op.close()
+
+
+def test_cg_agrees_with_krylov_solver(wl):
+    """The two solvers of the library evaluate the same resolvent operator."""
+    g = gg.barabasi_albert(3000, 4, 7)
+    rA = S.rho_A(g)
+    alpha = 0.3 / rA
+    V = torch.from_numpy(gg.vectors(g.n, 4, 9)).cuda()
+    thetas = [0.0, 0.3, 1.0]
+    cg = wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=thetas, f=("resolvent", alpha), solver="cg", cg_tol=1e-13)
+    kr = wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=thetas, f=("resolvent", alpha), krylov_dim=40)
+    assert relerr(cg.apply(V).cpu().numpy(), kr.apply(V).cpu().numpy()).max() < TOL
+    cg.close()
+    kr.close()
+
+
+@pytest.mark.parametrize("theta", [1.0, 0.5, 0.0])
+def test_multi_tile_graphs_cg_vs_series(wl, theta):
+    graphs = [gg.rmat(14, 12000, 150000, seed=21, perm_seed=22),
+              gg.barabasi_albert(20000, 5, 31),
+              gg.grid_lcc(150, 149, 0.3, 41)]
+    for g in graphs:
+        rA = S.rho_A(g)
+        for a in (ALPHAS[0], ALPHAS[-1]):
+            alpha = a / rA
+            f = C.resolvent(alpha)
+            V = gg.vectors(g.n, 5, 77)
+            op = wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=[theta], f=("resolvent", alpha), solver="cg",
+                             cg_tol=1e-13)
+            got = op.apply(torch.from_numpy(V).cuda()).cpu().numpy()
+            ref = S.laplacian_apply(g, 1.0 - theta, f, V, rA)
+            assert relerr(got, ref).max() < TOL, (g.name, a)
+            op.close()
+
+
+def test_paper_tolerance_residual_bound(wl):
+    """At the paper's cg_tol = 1e-9 every column satisfies ||𝒜x - v|| <= 1e-9 ||v|| (checked through the
+    dense 𝒜 on the CPU: x = φ v / (1-μ²α²))."""
+    g = gg.barabasi_albert(2000, 3, 5)
+    A = D.adjacency(g)
+    d = A.sum(1)
+    alpha = ALPHAS[-1] / D.rho_A(A)
+    thetas = [0.0, 0.5, 1.0]
+    V = gg.vectors(g.n, 2, 3)
+    op = wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=thetas, f=("resolvent", alpha), solver="cg")
+    PV = op.phi_apply(torch.from_numpy(V).cuda()).cpu().numpy()
+    for i, th in enumerate(thetas):
+        mu = 1.0 - th
+        s = 1.0 - mu * mu * alpha * alpha
+        Adef = s * np.eye(g.n) - alpha * A + mu * alpha * alpha * np.diag(d)
+        X = PV[:, 2 * i:2 * i + 2] / s
+        res = np.linalg.norm(Adef @ X - V, axis=0) / np.linalg.norm(V, axis=0)
+        assert res.max() <= 1e-9 * (1 + 1e-6)
+    op.close()
+
+
+def test_cg_errors(wl):
+    g = gg.karate()
+    rA = D.rho_A(D.adjacency(g))
+    with pytest.raises(wl.WalkLapError) as e:  # CG needs the resolvent
+        wl.Operator(g.n, g.row_ptr, g.col_idx, f=("exp", 0.1), solver="cg")
+    assert e.value.code == 1
+    with pytest.raises(wl.WalkLapError) as e:  # α ρ >= 1 rejected up front with a ρ bound
+        wl.Operator(g.n, g.row_ptr, g.col_idx, f=("resolvent", 1.5 / rA), solver="cg", rho_bound=rA)
+    assert e.value.code == 3
+    # too few iterations: WL_ENOCONV (raised by operator creation, which solves for t)
+    with pytest.raises(wl.WalkLapError) as e:
+        wl.Operator(g.n, g.row_ptr, g.col_idx, f=("resolvent", 0.9 / rA), solver="cg", cg_maxit=2, cg_check=1,
+                    cg_tol=1e-14)
+    assert e.value.code == 4
+
+
+def test_cg_diffusion_karate(wl):
+    """Diffusion exp(-τ𝕃)x0 with the CG-evaluated resolvent Laplacian (outer Lanczos, step a9)."""
+    g = gg.karate()
+    A = D.adjacency(g)
+    alpha = 0.5 / D.rho_A(A)
+    Lap = D.walk_laplacian(D.phi_resolvent_closed(A, 1.0, alpha))
+    x0 = np.zeros(g.n)
+    x0[0] = 1.0
+    taus = np.linspace(0.0, 10.0, 7)
+    op = wl.Operator(g.n, g.row_ptr, g.col_idx, variant="nbt", f=("resolvent", alpha), solver="cg", cg_tol=1e-14)
+    X = op.diffuse(torch.from_numpy(x0).cuda(), taus, k_out=34).cpu().numpy()
+    ref = D.diffusion(Lap, x0, taus)
+    assert relerr(X, ref).max() < 1e-9
+    op.close()
