@@ -359,6 +359,130 @@ def cpu_baseline(g, cfg, beta, args):
             "seconds": dt}
 
 
+def run_cg(args):
+    """--solver cg: the paper's §5.3 workload on a config's graph — one resolvent NBT
+    Laplacian action 𝕃_1((1-αx)^{-1}) v for each of 4 α log-spaced in [1e-3, 10^-1/2]/ρ, CG to a
+    relative residual of 1e-9 (Jacobi preconditioner instead of the paper's AMG).  ρ(A) >= ρ(Z_1)
+    scales α (R8).  A step applies all four operators."""
+    import torch
+    import torch.distributed as dist
+    import paper_2601_11338_b200 as wl
+
+    world, rank, local = dist_setup(args.gpus)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = configs.get(args.config)
+    g, t_gen = load_graph(cfg, world, rank, torch, dist)
+    bounds = wl.partition(g.row_ptr, world)
+    rb, re = int(bounds[rank]), int(bounds[rank + 1])
+    rp = g.row_ptr[rb:re + 1]
+    ci = g.col_idx[g.row_ptr[rb]:g.row_ptr[re]]
+    comm = wl.Comm(rank, world, local) if world > 1 else None
+    t0 = time.time()
+    probe = wl.Operator(g.n, rp, ci, thetas=[1.0], f=("series", [0.0, 1.0]), row_range=(rb, re), comm=comm,
+                        krylov_dim=2)
+    rho = probe.spectral_radius(k=args.rho_k)
+    probe.close()
+    alphas = [a / rho for a in np.logspace(-3, -0.5, 4)]
+    ops = [wl.Operator(g.n, rp, ci, variant="nbt", f=("resolvent", a), row_range=(rb, re), comm=comm,
+                       solver="cg", cg_tol=1e-9, rho_bound=rho) for a in alphas]
+    torch.cuda.synchronize()
+    t_create = time.time() - t0
+    b = args.b if args.b else 1
+    Vfull = gg.vectors(g.n, b, cfg["vec_seed"] or 103)
+    V = torch.from_numpy(np.ascontiguousarray(Vfull[rb:re])).cuda()
+    del Vfull
+    outs = [torch.empty((op.n_local, b), dtype=torch.float64, device="cuda") for op in ops]
+    wss = [op.workspace(b) for op in ops]
+
+    def step():
+        for op, o, w in zip(ops, outs, wss):
+            op.apply(V, out=o, ws=w)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    l0 = wl.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = wl.launch_count() - l0
+    ms = ev0.elapsed_time(ev1) / args.steps
+    wl.profile_enable(True)
+    it0 = sum(w.cg_iterations() for w in wss)
+    for _ in range(args.steps):
+        step()
+    torch.cuda.synchronize()
+    wl.profile_enable(False)
+    prof = wl.profile_collect()
+    cg_iters = (sum(w.cg_iterations() for w in wss) - it0) / args.steps  # executed iterations per step
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    actions = len(alphas) * b
+    value = actions / (ms / 1e3)
+    # algorithmic bytes: SpMM as in §7 (y once, x = y here: 2 n b reads + write); CG vector kernels:
+    # init 4 blocks, each executed iteration dot 2 + update 6 + direction 3 blocks
+    n_loc, nnz_loc = ops[0].n_local, int(ci.shape[0])
+    blk = 8 * n_loc * b
+    peak, peak_src = peaks()
+    kernels = {}
+    for name, (tot, cnt) in prof.items():
+        per = tot / args.steps
+        kernels[name] = {"ms_per_step": per, "launches_per_step": cnt / args.steps, "share": per / ms}
+    if "spmv_binned" in kernels:
+        k = kernels["spmv_binned"]
+        by = cg_iters * (4 * nnz_loc + 4 * (n_loc + 1) + 2 * blk + 8 * ops[0].n_halo * b)
+        k.update({"alg_bytes_per_step": by, "achieved_gbs": by / (k["ms_per_step"] / 1e3) / 1e9})
+    if "cg_vec" in kernels:
+        k = kernels["cg_vec"]
+        inits = len(alphas)
+        iters = cg_iters  # launches past convergence inside a check interval exit at once: not counted
+        by = inits * 4 * blk + iters * 11 * blk
+        k.update({"alg_bytes_per_step": by, "achieved_gbs": by / (k["ms_per_step"] / 1e3) / 1e9,
+                  "cg_iterations_per_step": iters})
+    for k in kernels.values():
+        if "achieved_gbs" in k:
+            k["frac"] = k["achieved_gbs"] / peak
+    top = max((k for k in kernels if "alg_bytes_per_step" in kernels[k]), key=lambda k: kernels[k]["ms_per_step"])
+    tk = kernels[top]
+    roof = {"kernel": top, "bound": "hbm", "achieved": tk["achieved_gbs"], "peak": peak, "unit": "GB/s",
+            "frac": tk["frac"], "peak_source": peak_src, "traffic": None,
+            "alg_bytes_per_launch": tk["alg_bytes_per_step"] / max(1, tk["launches_per_step"])}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "actions/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded graphgen)",
+            "config": {"workload": f"{args.config}: {cfg['desc']}; resolvent NBT Laplacian by PCG (Jacobi), "
+                                   f"4 alpha log-spaced in [1e-3, 10^-0.5]/rho(A), rel. tol 1e-9 (paper 5.3)",
+                       "n": g.n, "nnz": g.nnz, "b": b, "alphas": alphas, "rho_A": rho,
+                       "actions_per_step": actions, "parallelism": f"row-partition x{world}",
+                       "setup_s": {"generate": round(t_gen, 2), "operators_incl_t": round(t_create, 2)}},
+            "roofline": roof,
+            "kernels": {k: {kk: (round(vv, 6) if isinstance(vv, float) else vv) for kk, vv in v.items()}
+                        for k, v in sorted(kernels.items(), key=lambda kv: -kv[1]["ms_per_step"])},
+            "cpu_baseline": None, "e2e": None, "gpu_launches": launches, "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    for op in ops:
+        op.close()
+    if comm:
+        comm.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def run_reference(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -400,11 +524,15 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--graph", action="store_true", help="also time the step captured as one CUDA graph")
+    ap.add_argument("--solver", default="krylov", choices=["krylov", "cg"],
+                    help="cg: the paper's 5.3 resolvent workload by PCG on --config's graph")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warning: contract requires >= 3 warm-up steps")
     if args.impl == "reference":
         run_reference(args)
+    elif args.solver == "cg":
+        run_cg(args)
     else:
         run_walklap(args)
 

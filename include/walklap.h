@@ -162,6 +162,9 @@ wl_status wl_operator_diag_shift(const wl_operator* op, double* t_dev, int64_t l
  * Krylov basis takes (k+1) * 2 * n_local * min(32, n_theta*max_b) doubles). */
 wl_status wl_workspace_create(const wl_operator* op, int32_t max_b, wl_workspace** out);
 void wl_workspace_destroy(wl_workspace* ws);
+/* Counters of a workspace (host): cg_iterations = CG iterations executed by actions on it so far
+ * (per solve, the largest count over its columns; WL_SOLVER_CG only).  Any pointer may be NULL. */
+wl_status wl_workspace_stats(const wl_workspace* ws, int64_t* cg_iterations);
 
 /* ---- actions (step a3-a7) -------------------------------------------------------------------
  * V  : device, n_local x b, leading dimension ldv >= b

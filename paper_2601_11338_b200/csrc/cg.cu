@@ -94,6 +94,7 @@ __global__ void __launch_bounds__(kThreads) cg_init_kernel(CgArgs a) {
 
 // sums: [p.q]
 __global__ void __launch_bounds__(kThreads) cg_dot_kernel(CgArgs a) {
+  if (a.flags[1] == 0) return;  // every column converged: the rest of the check interval is empty
   const Lane L(a.B);
   double v[1] = {0.0};
   const int64_t N = a.n * a.B;
@@ -104,6 +105,7 @@ __global__ void __launch_bounds__(kThreads) cg_dot_kernel(CgArgs a) {
 
 // x += α p, r -= α q;  sums: [r.z, r.r] with z = M^{-1} r
 __global__ void __launch_bounds__(kThreads) cg_update_kernel(CgArgs a) {
+  if (a.flags[1] == 0) return;
   const Lane L(a.B);
   double v[2] = {0.0, 0.0};
   const int64_t N = a.n * a.B;
@@ -122,6 +124,7 @@ __global__ void __launch_bounds__(kThreads) cg_update_kernel(CgArgs a) {
 
 // p = M^{-1} r + β p
 __global__ void __launch_bounds__(kThreads) cg_direction_kernel(CgArgs a) {
+  if (a.flags[1] == 0) return;
   const Lane L(a.B);
   const int64_t N = a.n * a.B;
   if (!L.act) return;
@@ -134,8 +137,8 @@ __global__ void __launch_bounds__(kThreads) cg_direction_kernel(CgArgs a) {
 //   which 0 (after init):   rz = sums[0], bb = sums[1]; active = bb > 0
 //   which 1 (after dot):    α = active ? rz / pq : 0 (pq <= 0: not SPD -> diverged flag)
 //   which 2 (after update): β = rz_new / rz, rz = rz_new; converged when r.r <= tol² b.b
-__global__ void cg_scalar_kernel(int which, const double* sums, int B, double* sc, double* bb, const double* cs,
-                                 int* iters, int* flags) {
+__device__ void scalar_step(int which, const double* sums, int B, double* sc, double* bb, const double* cs,
+                            int* iters, int* flags) {
   const int c = threadIdx.x;
   if (c < B) {
     double* s = sc + c * kSlots;
@@ -168,12 +171,44 @@ __global__ void cg_scalar_kernel(int which, const double* sums, int B, double* s
       }
     }
   }
-  __syncwarp();
-  if (c == 0) {  // number of still-active columns, for the host's periodic convergence check
+  __syncthreads();
+  if (threadIdx.x == 0) {  // number of still-active columns: read by the vector kernels and the host check
     int act = 0;
     for (int k = 0; k < B; ++k) act += sc[k * kSlots + 3] != 0.0;
     flags[1] = act;
   }
+}
+
+// scalar steps, one thread per column.
+//   which 0 (after init):   rz = sums[0], bb = sums[1]; active = bb > 0
+//   which 1 (after dot):    α = active ? rz / pq : 0 (pq <= 0: not SPD -> diverged flag)
+//   which 2 (after update): β = rz_new / rz, rz = rz_new; converged when r.r <= tol² b.b
+__global__ void cg_scalar_kernel(int which, const double* sums, int B, double* sc, double* bb, const double* cs,
+                                 int* iters, int* flags) {
+  if (which != 0 && flags[1] == 0) return;
+  scalar_step(which, sums, B, sc, bb, cs, iters, flags);
+}
+
+// single-GPU fusion of reduce_partials + cg_scalar: one CTA sums the <= 64 partial rows (warp per
+// row, lanes over the CTAs, fixed shuffle tree) and then takes the scalar step.
+__global__ void __launch_bounds__(256) cg_reduce_scalar_kernel(int which, int nout, int G, CgArgs a) {
+  if (which != 0 && a.flags[1] == 0) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int ic = warp; ic < nout; ic += blockDim.x / 32) {
+    const double* p = a.partials + (int64_t)ic * G;
+    double s0 = 0.0, s1 = 0.0;
+    int g = lane;
+    for (; g + 32 < G; g += 64) {
+      s0 += p[g];
+      s1 += p[g + 32];
+    }
+    if (g < G) s0 += p[g];
+    double v = s0 + s1;
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if (lane == 0) a.sums[ic] = v;
+  }
+  __syncthreads();
+  scalar_step(which, a.sums, a.B, a.sc, a.bb, a.cs, a.iters, a.flags);
 }
 
 // out (user order) from the solution x = 𝒜^{-1} b:  φ b = (1-μ²α²) x
@@ -215,26 +250,32 @@ int cg_grid(int64_t n, int B) { return vec_grid(n, B); }
 
 void cg_init(CgArgs a, cudaStream_t s) {
   WL_LAUNCH("cg_vec");
-  const int g = vec_grid(a.n, a.B);
-  cg_init_kernel<<<g, kThreads, 0, s>>>(a);
+  cg_init_kernel<<<vec_grid(a.n, a.B), kThreads, 0, s>>>(a);
   WL_CUDA(cudaGetLastError());
-  reduce_partials(a.partials, 2 * a.B, g, a.sums, s);
 }
 
 void cg_dot(CgArgs a, cudaStream_t s) {
   WL_LAUNCH("cg_vec");
-  const int g = vec_grid(a.n, a.B);
-  cg_dot_kernel<<<g, kThreads, 0, s>>>(a);
+  cg_dot_kernel<<<vec_grid(a.n, a.B), kThreads, 0, s>>>(a);
   WL_CUDA(cudaGetLastError());
-  reduce_partials(a.partials, a.B, g, a.sums, s);
 }
 
 void cg_update(CgArgs a, cudaStream_t s) {
   WL_LAUNCH("cg_vec");
-  const int g = vec_grid(a.n, a.B);
-  cg_update_kernel<<<g, kThreads, 0, s>>>(a);
+  cg_update_kernel<<<vec_grid(a.n, a.B), kThreads, 0, s>>>(a);
   WL_CUDA(cudaGetLastError());
-  reduce_partials(a.partials, 2 * a.B, g, a.sums, s);
+}
+
+void cg_reduce_scalar(int which, const CgArgs& a, cudaStream_t s) {
+  WL_LAUNCH("cg_scalar");
+  const int nout = (which == 1 ? 1 : 2) * a.B;
+  cg_reduce_scalar_kernel<<<1, 256, 0, s>>>(which, nout, vec_grid(a.n, a.B), a);
+  WL_CUDA(cudaGetLastError());
+}
+
+void cg_reduce(int which, const CgArgs& a, cudaStream_t s) {
+  WL_LAUNCH("cg_scalar");
+  reduce_partials(a.partials, (which == 1 ? 1 : 2) * a.B, vec_grid(a.n, a.B), a.sums, s);
 }
 
 void cg_direction(CgArgs a, cudaStream_t s) {
@@ -246,6 +287,7 @@ void cg_direction(CgArgs a, cudaStream_t s) {
 void cg_scalar(int which, const CgArgs& a, cudaStream_t s) {
   WL_LAUNCH("cg_scalar");
   cg_scalar_kernel<<<1, 32, 0, s>>>(which, a.sums, a.B, a.sc, a.bb, a.cs, a.iters, a.flags);
+
   WL_CUDA(cudaGetLastError());
 }
 

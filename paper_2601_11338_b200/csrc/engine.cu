@@ -172,7 +172,8 @@ struct wl_workspace {
   // conjugate-gradient solver state (cg.cu): per column constants, scalars, |b|², iterations, flags
   DArr<double> cg_cs, cg_sc, cg_bb;
   DArr<int> cg_iters, cg_flags;
-  int* cg_flags_host = nullptr;  // pinned
+  int* cg_flags_host = nullptr;  // pinned: 2 flags + kMaxCols iteration counts
+  int64_t cg_iterations = 0;     // executed CG iterations (max over the columns of each solve), cumulative
   // host-buffer entry point
   DArr<double> hV, hLV;
   // diffusion (outer Lanczos)
@@ -237,8 +238,9 @@ void halo_exchange(const wl_operator* op, wl_workspace* ws, const double* src, i
 
 void do_spmv(const wl_operator* op, wl_workspace* ws, const double* y, const double* x,
              const double* g0, const double* g1, const double* scale, double* out, int B,
-             cudaStream_t s) {
+             cudaStream_t s, const int* active = nullptr) {
   SpmvArgs a{};
+  a.active = active;
   a.rowptr = op->rowptr.p;
   a.col = op->col.p;
   a.n_loc = op->n_loc;
@@ -406,19 +408,23 @@ void cg_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double* V
   a.iters = ws->cg_iters.p;
   a.flags = ws->cg_flags.p;
   WL_CUDA(cudaMemsetAsync(ws->cg_flags.p, 0, 2 * sizeof(int), s));
+  // reductions: one fused reduce+scalar CTA on one GPU; reduce -> NCCL allreduce -> scalar across GPUs
+  auto reduce_scalar = [&](int which) {
+    if (!multi(op)) return cg_reduce_scalar(which, a, s);
+    cg_reduce(which, a, s);
+    allreduce(op, a.sums, (size_t)(which == 1 ? 1 : 2) * B, s);
+    cg_scalar(which, a, s);
+  };
   cg_init(a, s);
-  allreduce(op, a.sums, (size_t)2 * B, s);
-  cg_scalar(0, a, s);
+  reduce_scalar(0);
   bool done = false;
   for (int it = 0; it < op->opts.cg_maxit && !done; ++it) {
     halo_exchange(op, ws, a.p, B, B, s);
-    do_spmv(op, ws, a.p, a.p, g0, g1, scale, a.q, B, s);  // q = 𝒜 p
+    do_spmv(op, ws, a.p, a.p, g0, g1, scale, a.q, B, s, a.flags + 1);  // q = 𝒜 p
     cg_dot(a, s);
-    allreduce(op, a.sums, (size_t)B, s);
-    cg_scalar(1, a, s);
+    reduce_scalar(1);
     cg_update(a, s);
-    allreduce(op, a.sums, (size_t)2 * B, s);
-    cg_scalar(2, a, s);
+    reduce_scalar(2);
     cg_direction(a, s);
     if ((it + 1) % op->opts.cg_check == 0 || it + 1 == op->opts.cg_maxit) {
       WL_CUDA(cudaMemcpyAsync(ws->cg_flags_host, ws->cg_flags.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -429,6 +435,9 @@ void cg_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double* V
   }
   cg_combine(mode, a.x, n, B, ws->cg_cs.p, V, ldv, ws->vcol.p, op->c0, op->tprime.p, op->n_theta, ws->tcol.p, out,
              ldo, perm, s);
+  WL_CUDA(cudaMemcpyAsync(ws->cg_flags_host + 2, ws->cg_iters.p, B * sizeof(int), cudaMemcpyDeviceToHost, s));
+  WL_CUDA(cudaStreamSynchronize(s));
+  ws->cg_iterations += *std::max_element(ws->cg_flags_host + 2, ws->cg_flags_host + 2 + B);
   if (!done) throw Error(WL_ENOCONV, "CG: residual above cg_tol after cg_maxit iterations (best iterate written)");
 }
 
@@ -485,7 +494,7 @@ void workspace_alloc(wl_workspace* ws, const wl_operator* op, int max_b) {
   ws->cg_bb.alloc(kMaxCols);
   ws->cg_iters.alloc(kMaxCols);
   ws->cg_flags.alloc(2);
-  if (!ws->cg_flags_host) WL_CUDA(cudaMallocHost(&ws->cg_flags_host, 2 * sizeof(int)));
+  if (!ws->cg_flags_host) WL_CUDA(cudaMallocHost(&ws->cg_flags_host, (2 + kMaxCols) * sizeof(int)));
   spmv_scratch(op, ws, B);
   WL_CUDA(cudaDeviceSynchronize());
 }
@@ -997,6 +1006,13 @@ void wl_operator_destroy(wl_operator* op) {
   DeviceGuard dg(op->device);
   WL_CUDA(cudaDeviceSynchronize());
   delete op;
+}
+
+wl_status wl_workspace_stats(const wl_workspace* ws, int64_t* cg_iterations) {
+  return guarded([&] {
+    if (!ws) throw Error(WL_EINVAL, "ws is NULL");
+    if (cg_iterations) *cg_iterations = ws->cg_iterations;
+  });
 }
 
 wl_status wl_operator_info(const wl_operator* op, int64_t* n_local, int64_t* nnz_local, int64_t* n_halo,

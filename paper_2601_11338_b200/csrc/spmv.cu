@@ -96,6 +96,7 @@ __device__ inline double group_reduce(double v, int B, int gpw) {
 
 template <int kU, bool HALO>
 __global__ void __launch_bounds__(kThreads) spmv_binned_kernel(SpmvArgs a) {
+  if (a.active && *a.active == 0) return;
   const int B = a.B;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int gpw = 32 / B;
@@ -158,6 +159,7 @@ __global__ void __launch_bounds__(kThreads) spmv_binned_kernel(SpmvArgs a) {
 // flushing rows as their ranges end: ~1 latency per kU gathers instead of ~3 per row.
 template <int kU, bool HALO>
 __global__ void __launch_bounds__(kThreads) spmv_small_batched_kernel(SpmvArgs a) {
+  if (a.active && *a.active == 0) return;
   extern __shared__ __align__(16) int s_small[];
   constexpr int kColCap = 32 * kSmallMax;  // max nonzeros of a 32-row batch
   constexpr int kIntsPerWarp = kColCap + 40;

@@ -51,6 +51,7 @@ struct SpmvArgs {
   double* out; int64_t ldo;
   const double* g0; const double* g1; const double* scale;  // device, B entries (null = 0,0,1)
   int B;
+  const int* active;                 // optional (CG): the launch does nothing when *active == 0
 };
 void spmv(const SpmvArgs& a, cudaStream_t s);
 
@@ -125,7 +126,9 @@ void cg_init(CgArgs a, cudaStream_t s);
 void cg_dot(CgArgs a, cudaStream_t s);
 void cg_update(CgArgs a, cudaStream_t s);
 void cg_direction(CgArgs a, cudaStream_t s);
-void cg_scalar(int which, const CgArgs& a, cudaStream_t s);
+void cg_scalar(int which, const CgArgs& a, cudaStream_t s);         // after reduce (+ allreduce)
+void cg_reduce(int which, const CgArgs& a, cudaStream_t s);         // partials -> sums
+void cg_reduce_scalar(int which, const CgArgs& a, cudaStream_t s);  // single GPU: both in one CTA
 void cg_combine(int mode, const double* x, int64_t n, int B, const double* cs, const double* V, int64_t ldv,
                 const int* vcol, double c0, const double* tprime, int64_t ldt, const int* tcol, double* out,
                 int64_t ldo, const int32_t* perm, cudaStream_t s);

@@ -67,6 +67,7 @@ def load():
         "wl_operator_diag_shift": ([vp, vp, i64, vp], ctypes.c_int),
         "wl_workspace_create": ([vp, i32, pvp], ctypes.c_int),
         "wl_workspace_destroy": ([vp], None),
+        "wl_workspace_stats": ([vp, vp], ctypes.c_int),
         "wl_apply": ([vp, i32, vp, i64, vp, i64, vp, vp], ctypes.c_int),
         "wl_phi_apply": ([vp, i32, vp, i64, vp, i64, vp, vp], ctypes.c_int),
         "wl_apply_host": ([vp, i32, vp, i64, vp, i64, vp, vp], ctypes.c_int),
@@ -188,6 +189,12 @@ class Comm:
 
 
 class Workspace:
+    def cg_iterations(self) -> int:
+        """CG iterations executed by actions on this workspace so far (wl_workspace_stats)."""
+        v = ctypes.c_int64()
+        _check(load().wl_workspace_stats(self.handle, ctypes.byref(v)))
+        return v.value
+
     def __init__(self, op: "Operator", max_b: int):
         self.op = op
         self.max_b = max_b
