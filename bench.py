@@ -362,8 +362,8 @@ def cpu_baseline(g, cfg, beta, args):
 def run_cg(args):
     """--solver cg: the paper's §5.3 workload on a config's graph — one resolvent NBT
     Laplacian action 𝕃_1((1-αx)^{-1}) v for each of 4 α log-spaced in [1e-3, 10^-1/2]/ρ, CG to a
-    relative residual of 1e-9 (Jacobi preconditioner instead of the paper's AMG).  ρ(A) >= ρ(Z_1)
-    scales α (R8).  A step applies all four operators."""
+    relative residual of 1e-9 (Jacobi preconditioner instead of the paper's AMG).  ρ(Z_1) from
+    wl_spectral_radius_z scales α.  A step applies all four operators."""
     import torch
     import torch.distributed as dist
     import paper_2601_11338_b200 as wl
@@ -380,13 +380,13 @@ def run_cg(args):
     ci = g.col_idx[g.row_ptr[rb]:g.row_ptr[re]]
     comm = wl.Comm(rank, world, local) if world > 1 else None
     t0 = time.time()
-    probe = wl.Operator(g.n, rp, ci, thetas=[1.0], f=("series", [0.0, 1.0]), row_range=(rb, re), comm=comm,
+    probe = wl.Operator(g.n, rp, ci, thetas=[0.0], f=("series", [0.0, 1.0]), row_range=(rb, re), comm=comm,
                         krylov_dim=2)
-    rho = probe.spectral_radius(k=args.rho_k)
+    rho = probe.spectral_radius_z(0, k=args.rho_k)  # ρ(Z_1) by Arnoldi on Z (NEXT-4), as §5.3 prescribes
     probe.close()
     alphas = [a / rho for a in np.logspace(-3, -0.5, 4)]
     ops = [wl.Operator(g.n, rp, ci, variant="nbt", f=("resolvent", a), row_range=(rb, re), comm=comm,
-                       solver="cg", cg_tol=1e-9, rho_bound=rho) for a in alphas]
+                       solver="cg", cg_tol=1e-9) for a in alphas]
     torch.cuda.synchronize()
     t_create = time.time() - t0
     b = args.b if args.b else 1
@@ -465,8 +465,8 @@ def run_cg(args):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded graphgen)",
             "config": {"workload": f"{args.config}: {cfg['desc']}; resolvent NBT Laplacian by PCG (Jacobi), "
-                                   f"4 alpha log-spaced in [1e-3, 10^-0.5]/rho(A), rel. tol 1e-9 (paper 5.3)",
-                       "n": g.n, "nnz": g.nnz, "b": b, "alphas": alphas, "rho_A": rho,
+                                   f"4 alpha log-spaced in [1e-3, 10^-0.5]/rho(Z_1), rel. tol 1e-9 (paper 5.3)",
+                       "n": g.n, "nnz": g.nnz, "b": b, "alphas": alphas, "rho_Z1": rho,
                        "actions_per_step": actions, "parallelism": f"row-partition x{world}",
                        "setup_s": {"generate": round(t_gen, 2), "operators_incl_t": round(t_create, 2)}},
             "roofline": roof,

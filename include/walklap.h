@@ -197,6 +197,20 @@ wl_status wl_diffuse(const wl_operator* op, int32_t theta_index, int32_t nt, con
  * Synchronous.  2 <= k <= 128. */
 wl_status wl_spectral_radius(const wl_operator* op, int32_t k, double* rho_out, wl_stream stream);
 
+/* ---- ρ(Z_θ) (Prop. pro:whe-we-converge P:317-322, §5.3 α scaling P:1490)
+ * Spectral radius of the companion operator Z_θ = [[O, I], [μ(μI - D), A]] (eq:Zdef) of θ value
+ * theta_index: k steps of Arnoldi (CGS2) on Z from a positive pseudo-random vector (hash of the
+ * row index; [1; 1] itself is an eigenvector of Z_1), then the largest
+ * modulus among the eigenvalues of the k_eff x k_eff Hessenberg matrix (Francis double-shift QR on
+ * the host).  Ritz values converge to the extremal eigenvalues; for θ = 0 Z is the Ihara-Bass
+ * linearisation of the nonbacktracking matrix, whose spectral radius is a real eigenvalue.
+ * Synchronous.  2 <= k <= 128.  WL_ENOCONV if the small QR iteration fails. */
+wl_status wl_spectral_radius_z(const wl_operator* op, int32_t theta_index, int32_t k, double* rho_out,
+                               wl_stream stream);
+/* The host eigenvalue routine behind it, exported for testing: H (host) n x n row-major upper
+ * Hessenberg (entries below the subdiagonal ignored); wr/wi (host, n) receive real/imaginary parts. */
+wl_status wl_hessenberg_eigvals(int32_t n, const double* H, double* wr, double* wi);
+
 /* ---- live per-kernel timing (benchmarking) ----------------------------------------------------
  * When enabled, every kernel launch scope is bracketed by CUDA events on its stream (small
  * overhead).  wl_profile_collect() synchronizes on the recorded events, aggregates elapsed time

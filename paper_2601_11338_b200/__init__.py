@@ -10,6 +10,7 @@ from .walklap import (  # noqa: F401
     WalkLapError,
     Workspace,
     halo_plan,
+    hessenberg_eigvals,
     launch_count,
     load,
     partition,

@@ -694,8 +694,8 @@ inline int64_t outer_stride(const wl_operator* op) { return std::max<int64_t>(2,
 // caller), Hessenberg ws->oH (layout (m+1) x m), scales ws->os, ||P_0|| in ws->on0.
 // `apply(P̃_j, out)` writes the operator applied to the UNNORMALISED basis vector P̃_j.
 template <class Apply>
-void outer_arnoldi(const wl_operator* op, wl_workspace* ws, int m, Apply&& apply, cudaStream_t s) {
-  const int64_t n = outer_stride(op);
+void outer_arnoldi(const wl_operator* op, wl_workspace* ws, int m, Apply&& apply, cudaStream_t s, int64_t len = 0) {
+  const int64_t n = len ? len : outer_stride(op);
   WL_CUDA(cudaMemsetAsync(ws->oH.p, 0, sizeof(double) * (m + 1) * m, s));
   GramArgs g{};
   g.Q = ws->oQ.p;
@@ -757,8 +757,8 @@ void outer_arnoldi(const wl_operator* op, wl_workspace* ws, int m, Apply&& apply
 }
 
 
-void outer_alloc(const wl_operator* op, wl_workspace* ws, int m, int nt) {
-  const int64_t np = outer_stride(op);
+void outer_alloc(const wl_operator* op, wl_workspace* ws, int m, int nt, int64_t len = 0) {
+  const int64_t np = len ? len : outer_stride(op);
   if (ws->kout_alloc >= m && ws->otau.n >= (size_t)nt) return;
   ws->oQ.alloc((size_t)(m + 1) * np);
   ws->ow.alloc((size_t)np);
@@ -1183,6 +1183,63 @@ wl_status wl_spectral_radius(const wl_operator* op, int32_t k, double* rho_out, 
     for (int i = 0; i < keff; ++i) a[i] = H[(size_t)i * (k + 1) + i];
     for (int i = 0; i + 1 < keff; ++i) b[i] = H[(size_t)i * (k + 1) + i + 1];
     *rho_out = tridiag_max_eig(a, b);
+  });
+}
+
+wl_status wl_spectral_radius_z(const wl_operator* op, int32_t theta_index, int32_t k, double* rho_out,
+                               wl_stream stream) {
+  return guarded([&] {
+    if (!op || !rho_out) throw Error(WL_EINVAL, "NULL argument");
+    if (k < 2 || k > 128) throw Error(WL_EINVAL, "k must be in [2, 128]");
+    if (theta_index < 0 || theta_index >= op->n_theta) throw Error(WL_EINVAL, "theta_index out of range");
+    DeviceGuard dg(op->device);
+    cudaStream_t s = S_(stream);
+    wl_workspace ws;
+    ws.op = op;
+    if (op->n_halo > 0) ws.halo_recv.alloc(op->n_halo);
+    if (op->n_send > 0) ws.halo_send.alloc(op->n_send);
+    const int64_t np = outer_stride(op), len = 2 * np;  // Z vector = [top np ; bottom np], pad rows stay 0
+    outer_alloc(op, &ws, k, 1, len);
+    spmv_scratch(op, &ws, 1);
+    ws.colp.alloc(4 * kMaxCols);
+    ws.vcol.alloc(kMaxCols);
+    ws.tcol.alloc(kMaxCols);
+    double* g0z = ws.colp.p;
+    double* g1z = g0z + kMaxCols;
+    setup_chunk(op->mu_dev.p, theta_index, 1, 1, g0z, g1z, g0z + 2 * kMaxCols, g0z + 3 * kMaxCols, ws.vcol.p,
+                ws.tcol.p, s);
+    // positive pseudo-random start vector (structured ones can be eigenvectors: Z_1 [1; 1] = [1; 1])
+    fill_hash(ws.oQ.p, op->n_loc, 0x5EEDull, 2 * op->row_begin, s);
+    fill_hash(ws.oQ.p + np, op->n_loc, 0x5EEDull, 2 * op->row_begin + op->n_loc, s);
+    outer_arnoldi(op, &ws, k, [&](const double* Pj, double* out) {
+      // Z (x; y) = (y; A y + μ(μ - d) x)   (eq:Zdef)
+      WL_CUDA(cudaMemcpyAsync(out, Pj + np, sizeof(double) * np, cudaMemcpyDeviceToDevice, s));
+      halo_exchange(op, &ws, Pj + np, 1, 1, s);
+      do_spmv(op, &ws, Pj + np, Pj, g0z, g1z, nullptr, out + np, 1, s);
+    }, s, len);
+    std::vector<double> H((size_t)(k + 1) * k);
+    int keff = 0;
+    WL_CUDA(cudaMemcpyAsync(H.data(), ws.oH.p, sizeof(double) * H.size(), cudaMemcpyDeviceToHost, s));
+    WL_CUDA(cudaMemcpyAsync(&keff, ws.okeff.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    WL_CUDA(cudaStreamSynchronize(s));
+    if (keff <= 0) { *rho_out = 0.0; return; }
+    std::vector<double> Hm((size_t)keff * keff, 0.0), wr, wi;
+    for (int j = 0; j < keff; ++j)
+      for (int i = 0; i <= std::min(j + 1, keff - 1); ++i) Hm[(size_t)i * keff + j] = H[(size_t)j * (k + 1) + i];
+    if (!hessenberg_eigvals(Hm, keff, wr, wi)) throw Error(WL_ENOCONV, "Hessenberg QR did not converge");
+    double r = 0.0;
+    for (int i = 0; i < keff; ++i) r = std::max(r, std::hypot(wr[i], wi[i]));
+    *rho_out = r;
+  });
+}
+
+wl_status wl_hessenberg_eigvals(int32_t n, const double* H, double* wr, double* wi) {
+  return guarded([&] {
+    if (n < 1 || !H || !wr || !wi) throw Error(WL_EINVAL, "bad arguments");
+    std::vector<double> a(H, H + (size_t)n * n), r, i;
+    if (!hessenberg_eigvals(a, n, r, i)) throw Error(WL_ENOCONV, "Hessenberg QR did not converge");
+    std::copy(r.begin(), r.end(), wr);
+    std::copy(i.begin(), i.end(), wi);
   });
 }
 

@@ -101,6 +101,17 @@ __global__ void pack_rows_kernel(const double* src, int64_t lds, const int32_t* 
   }
 }
 
+// p[i] = 0.5 + u(seed, i0 + i), u uniform in [0,1) from a counter-based hash (splitmix64)
+__global__ void fill_hash_kernel(double* p, int64_t n, uint64_t seed, int64_t i0) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t z = seed + 0x9E3779B97F4A7C15ull * (uint64_t)(i0 + i + 1);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    p[i] = 0.5 + (double)(z >> 11) * (1.0 / 9007199254740992.0);
+  }
+}
+
 __global__ void fill_kernel(double* p, int64_t n, double v) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = v;
@@ -291,6 +302,13 @@ void pack_rows(const double* src, int64_t lds, const int32_t* idx, int64_t cnt, 
   if (cnt <= 0) return;
   WL_LAUNCH("pack_rows");
   pack_rows_kernel<<<grid_for(cnt * B), 256, 0, s>>>(src, lds, idx, cnt, B, dst);
+  WL_CUDA(cudaGetLastError());
+}
+
+void fill_hash(double* p, int64_t n, uint64_t seed, int64_t i0, cudaStream_t s) {
+  WL_LAUNCH("fill");
+  if (n <= 0) return;
+  fill_hash_kernel<<<grid_for(n), 256, 0, s>>>(p, n, seed, i0);
   WL_CUDA(cudaGetLastError());
 }
 

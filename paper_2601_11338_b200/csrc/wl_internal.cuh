@@ -4,6 +4,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 namespace wl {
 
@@ -175,6 +176,10 @@ void combine(int mode, const VecPtrs& Q, int nvec, int64_t n, int B,
 void pack_rows(const double* src, int64_t lds, const int32_t* idx, int64_t cnt, int B, double* dst,
                cudaStream_t s);
 void fill(double* p, int64_t n, double v, cudaStream_t s);
+void fill_hash(double* p, int64_t n, uint64_t seed, int64_t i0, cudaStream_t s);  // 0.5 + U[0,1)
+
+// eigenvalues of a small real upper Hessenberg matrix (host; eig.cu). H row-major n x n, overwritten.
+bool hessenberg_eigvals(std::vector<double>& H, int n, std::vector<double>& wr, std::vector<double>& wi);
 
 // outer Lanczos helpers (diffusion)
 void lanczos_combine(const double* Q, int64_t stride, int m, int64_t n, const double* Y, int nt,

@@ -74,6 +74,8 @@ def load():
         "wl_diffuse": ([vp, i32, i32, vp, vp, vp, i64, i32, vp, vp], ctypes.c_int),
         "wl_wait": ([vp, vp], ctypes.c_int),
         "wl_spectral_radius": ([vp, i32, ctypes.POINTER(dbl), vp], ctypes.c_int),
+        "wl_spectral_radius_z": ([vp, i32, i32, ctypes.POINTER(dbl), vp], ctypes.c_int),
+        "wl_hessenberg_eigvals": ([i32, vp, vp, vp], ctypes.c_int),
         "wl_profile_enable": ([i32], None),
         "wl_profile_collect": ([], ctypes.c_int),
         "wl_profile_count": ([], i32),
@@ -141,6 +143,15 @@ def halo_plan(n_global: int, bounds: np.ndarray, rank: int, row_ptr_local: np.nd
     _check(load().wl_halo_plan(n_global, len(b) - 1, b.ctypes.data, rank, rp.ctypes.data, ci.ctypes.data,
                                col.ctypes.data, halo.ctypes.data, ctypes.byref(nh), cnt.ctypes.data))
     return col[:nnz], halo[:nh.value], cnt
+
+
+def hessenberg_eigvals(H: np.ndarray) -> np.ndarray:
+    """Eigenvalues of a real upper Hessenberg matrix by the library's host QR (wl_hessenberg_eigvals)."""
+    H = np.ascontiguousarray(H, dtype=np.float64)
+    n = H.shape[0]
+    wr, wi = np.empty(n), np.empty(n)
+    _check(load().wl_hessenberg_eigvals(n, H.ctypes.data, wr.ctypes.data, wi.ctypes.data))
+    return wr + 1j * wi
 
 
 def _stream_handle(stream):
@@ -339,6 +350,12 @@ class Operator:
         rho = ctypes.c_double()
         _check(load().wl_spectral_radius(self.handle, k, ctypes.byref(rho), _stream_handle(stream)))
         return rho.value
+
+    def spectral_radius_z(self, theta_index: int = 0, k: int = 60, stream=None) -> float:
+        """ρ(Z_θ) of the companion operator by k Arnoldi steps on Z (wl_spectral_radius_z)."""
+        r = ctypes.c_double()
+        _check(load().wl_spectral_radius_z(self.handle, theta_index, k, ctypes.byref(r), _stream_handle(stream)))
+        return r.value
 
     def wait(self, stream=None):
         _check(load().wl_wait(self.handle, _stream_handle(stream)))

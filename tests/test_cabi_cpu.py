@@ -71,3 +71,45 @@ def test_no_cpu_fallback_in_product(lib):
             src = open(os.path.join(pkg, fn)).read()
             assert "oracle" not in src.replace("# oracle", ""), fn
             assert "scipy" not in src, fn
+
+
+def _hessenberg(rng, n, kind):
+    H = np.triu(rng.standard_normal((n, n)), -1)
+    if kind == "companion":  # roots of a random polynomial: many complex pairs
+        H = np.zeros((n, n))
+        H[0, :] = rng.standard_normal(n)
+        H[np.arange(1, n), np.arange(n - 1)] = 1.0
+    elif kind == "deflated":  # exact zeros on the subdiagonal
+        H[np.arange(1, n, 3), np.arange(0, n - 1, 3)] = 0.0
+    elif kind == "symmetric":  # tridiagonal symmetric: real spectrum
+        d, e = rng.standard_normal(n), rng.standard_normal(n - 1)
+        H = np.diag(d) + np.diag(e, 1) + np.diag(e, -1)
+    return H
+
+
+@pytest.mark.parametrize("kind", ["random", "companion", "deflated", "symmetric"])
+def test_hessenberg_eigvals_match_lapack(lib, kind):
+    """The host Francis QR behind wl_spectral_radius_z (eig.cu) against LAPACK (numpy.linalg.eigvals),
+    as multisets, for sizes 1..64 — including complex pairs, exact deflations and real spectra."""
+    import paper_2601_11338_b200 as wl
+    rng = np.random.default_rng(7)
+    for n in list(range(1, 13)) + [20, 31, 48, 64]:
+        H = _hessenberg(rng, n, kind)
+        got = wl.hessenberg_eigvals(H)
+        ref = np.linalg.eigvals(H)
+        scale = max(1.0, np.abs(ref).max())
+        # greedy matching (multisets)
+        left = list(ref)
+        for z in got:
+            k = int(np.argmin([abs(z - r) for r in left]))
+            assert abs(z - left[k]) <= 1e-8 * scale, (kind, n, z, left[k])
+            left.pop(k)
+
+
+def test_hessenberg_eigvals_closed_forms(lib):
+    import paper_2601_11338_b200 as wl
+    # rotation generator: ±i; Jordan-like upper triangular: its diagonal; 2x2 real pair
+    assert np.allclose(sorted(wl.hessenberg_eigvals(np.array([[0.0, -1.0], [1.0, 0.0]])), key=lambda z: z.imag), [-1j, 1j])
+    T = np.triu(np.arange(1.0, 26.0).reshape(5, 5))
+    assert np.allclose(np.sort(wl.hessenberg_eigvals(T).real), [1.0, 7.0, 13.0, 19.0, 25.0])
+    assert np.allclose(np.sort(wl.hessenberg_eigvals(np.array([[2.0, 1.0], [1.0, 2.0]])).real), [1.0, 3.0])

@@ -330,3 +330,25 @@ def test_apply_captured_in_cuda_graph(wl):
             assert relerr(got[:, i * b:(i + 1) * b], ref).max() < TOL
     ws.close()
     op.close()
+
+
+def test_spectral_radius_z_vs_dense(wl):
+    """NEXT-4: ρ(Z_θ) by Arnoldi on the companion operator + host Hessenberg QR vs the dense eigenvalues
+    of Z (oracle/dense.rho_Z); the karate NBT value is the one Fig. 4b's α uses (ρ(Z_1) = 5.29278...)."""
+    g = gg.karate()
+    A = D.adjacency(g)
+    thetas = [0.0, 0.5, 1.0]
+    op = wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=thetas, f=("exp", 0.1))
+    for i, th in enumerate(thetas):
+        got = op.spectral_radius_z(i, k=68)
+        assert abs(got - D.rho_Z(A, 1.0 - th)) <= 1e-9 * got, th
+    assert abs(op.spectral_radius_z(0, k=68) - 5.292780644548677) < 1e-9
+    op.close()
+    g = gg.barabasi_albert(400, 3, 11)
+    A = D.adjacency(g)
+    op = wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=thetas, f=("exp", 0.1))
+    for i, th in enumerate(thetas):
+        got = op.spectral_radius_z(i, k=100)
+        ref = D.rho_Z(A, 1.0 - th)
+        assert abs(got - ref) <= 1e-8 * ref, (th, got, ref)
+    op.close()
