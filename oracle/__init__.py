@@ -24,6 +24,8 @@ paper by eye:
                   recurrence" of the north star).
 * ``chebyshev`` — diffusion exp(-t𝕃)x0 at large n by a Chebyshev expansion on
                   the Gershgorin interval of Prop. pro:still-again-an-mmatrix.
+* ``markov``    — the discrete-time chain P = I - D^{-1}𝕃 (eq:let_there_be_markov,
+                  P:506-533) and its evolution p_{k+1} = p_k P.
 
 Readings of silent/garbled passages are listed in DESIGN.md §3; each function
 cites the passage it follows.  Pins (tests/test_oracle_*.py) check the oracle

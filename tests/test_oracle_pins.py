@@ -257,3 +257,43 @@ def test_survey_karate_cross_check(theta):
     phr = D.phi(A, mu, C.resolvent(0.5 / rA))
     assert (phr @ np.ones(34)).sum() == pytest.approx(ref[5], rel=1e-12)
     assert np.linalg.norm(D.walk_laplacian(phr) @ v) == pytest.approx(ref[6], rel=1e-12)
+
+
+# ---------------------------------------------------------------- Markov chain (NEXT-3)
+def test_fig1_markov_chain_stationary_by_eigenvector():
+    """eq:let_there_be_markov: the chain P = I - D^{-1}𝕃 built by oracle/markov.py has the
+    Fig. 1 bars as its stationary distribution, computed as a left eigenvector of P (independent of the
+    t/Σt route of the test above).  Pins transition() and reading R6 (D = diag(t))."""
+    from oracle import markov as M
+    gold = _fig1_panels()
+    A = D.adjacency(gg.trap_graph(5, 8))
+    rA = D.rho_A(A)
+    for key, f in (("res", C.resolvent(1.0 / (2.0 * rA))), ("exp", C.exp(1.0))):
+        ph = D.phi(A, 0.0, f)
+        t = ph @ np.ones(13)
+        P = M.transition(D.walk_laplacian(ph), t)
+        assert np.allclose(P.sum(1), 1.0, atol=1e-14) and P.min() >= -1e-15   # row-stochastic
+        assert np.max(np.abs(M.stationary_eig(P) - gold[key])) < 1e-13, key
+    # standard Laplacian panel: D = diag(L) = degrees, P = D^{-1}A (simple random walk)
+    L = D.standard_laplacian(A)
+    P = M.transition(L, A.sum(1))
+    assert np.allclose(P, A / A.sum(1)[:, None])
+    assert np.max(np.abs(M.stationary_eig(P) - gold["L"])) < 1e-13
+
+
+def test_markov_evolution_invariants():
+    """p_k keeps mass 1 and nonnegativity and converges to π ∝ t on a connected non-bipartite graph
+    (karate) for every θ; one step equals the plain vector-matrix product."""
+    from oracle import markov as M
+    g = gg.karate()
+    A = D.adjacency(g)
+    for mu in (0.0, 0.5, 1.0):
+        ph = D.phi(A, mu, C.exp(1.0 / D.rho_A(A)))
+        t = ph @ np.ones(g.n)
+        P = M.transition(D.walk_laplacian(ph), t)
+        p0 = np.zeros(g.n)
+        p0[0] = 1.0
+        ps = M.evolve(P, p0, 200)
+        assert np.allclose(ps.sum(1), 1.0, atol=1e-12) and ps.min() >= -1e-15
+        assert np.allclose(ps[0], p0 @ (np.diag(1.0 / t) @ ph))
+        assert np.max(np.abs(ps[-1] - t / t.sum())) < 1e-10
