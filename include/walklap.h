@@ -190,6 +190,17 @@ wl_status wl_diffuse(const wl_operator* op, int32_t theta_index, int32_t nt, con
                      const double* x0, double* X, int64_t ldx, int32_t k_out, wl_workspace* ws,
                      wl_stream stream);
 
+/* ---- discrete-time diffusion: Markov chain (eq:let_there_be_markov P:506-533)
+ * P = I - D^{-1} 𝕃_θ with D = diag(t_θ), t_θ = φ_θ 1 (reading R6: "a single evaluation of
+ * the underlying matrix function"; Fig. 1's stationary bars are t/Σt), i.e. P = diag(t)^{-1} φ_θ,
+ * row-stochastic with stationary distribution π = t/Σt (see wl_operator_diag_shift).  Evolves
+ * p_{k+1} = p_k P (row vectors) from p0 for θ value theta_index: each step is one φ_θ action on
+ * p_k / t (φ symmetric).  p0 : device, n_local (user row order, p0 1 = 1 over all ranks);
+ * P : device, n_local x nsteps (ldp >= nsteps), column k receives p_{k+1}.  Requires t > 0
+ * (true for exp and resolvent weights, c_0 = 1).  Asynchronous on `stream`. */
+wl_status wl_markov(const wl_operator* op, int32_t theta_index, int32_t nsteps, const double* p0, double* P,
+                    int64_t ldp, wl_workspace* ws, wl_stream stream);
+
 /* ---- spectral radius (helper for β = 1/ρ(A); convergence checks, Prop. pro:whe-we-converge)
  * ρ(A) of the operator's graph by k steps of Lanczos on A (full reorthogonalisation) started from
  * the all-ones vector (positive overlap with the Perron vector of the nonnegative symmetric A);

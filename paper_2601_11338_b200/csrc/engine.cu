@@ -174,6 +174,7 @@ struct wl_workspace {
   DArr<int> cg_iters, cg_flags;
   int* cg_flags_host = nullptr;  // pinned: 2 flags + kMaxCols iteration counts
   int64_t cg_iterations = 0;     // executed CG iterations (max over the columns of each solve), cumulative
+  DArr<double> mk_p, mk_v;       // Markov chain: current distribution and p / t (internal order)
   // host-buffer entry point
   DArr<double> hV, hLV;
   // diffusion (outer Lanczos)
@@ -1230,6 +1231,31 @@ wl_status wl_spectral_radius_z(const wl_operator* op, int32_t theta_index, int32
     double r = 0.0;
     for (int i = 0; i < keff; ++i) r = std::max(r, std::hypot(wr[i], wi[i]));
     *rho_out = r;
+  });
+}
+
+wl_status wl_markov(const wl_operator* op, int32_t theta_index, int32_t nsteps, const double* p0, double* P,
+                    int64_t ldp, wl_workspace* ws, wl_stream stream) {
+  return guarded([&] {
+    if (!op || !ws || ws->op != op) throw Error(WL_EINVAL, "operator/workspace mismatch");
+    if (theta_index < 0 || theta_index >= op->n_theta) throw Error(WL_EINVAL, "theta_index out of range");
+    if (nsteps < 1) throw Error(WL_EINVAL, "nsteps must be >= 1");
+    if (op->n_loc > 0) {
+      check_block(p0, 1, 1, "p0");
+      check_block(P, ldp, nsteps, "P");
+    }
+    DeviceGuard dg(op->device);
+    cudaStream_t s = S_(stream);
+    const int64_t n = op->n_loc;
+    ws->mk_p.alloc((size_t)std::max<int64_t>(1, n));
+    ws->mk_v.alloc((size_t)std::max<int64_t>(1, n));
+    gather_col(p0, 1, op->perm.p, n, ws->mk_p.p, s);  // user -> internal order
+    for (int k = 0; k < nsteps; ++k) {
+      // p_{k+1}^T = P^T p_k^T = φ (p_k / t)   (P = diag(t)^{-1} φ, φ symmetric)
+      markov_scale(ws->mk_p.p, op->tprime.p, op->n_theta, theta_index, op->c0, n, ws->mk_v.p, s);
+      run_chunk(op, ws, 0, ws->mk_v.p, 1, 1, theta_index, 1, ws->mk_p.p, 1, s, false);
+      scatter_col(ws->mk_p.p, op->perm.p, n, P + k, ldp, s);
+    }
   });
 }
 

@@ -101,6 +101,22 @@ __global__ void pack_rows_kernel(const double* src, int64_t lds, const int32_t* 
   }
 }
 
+// Markov chain helpers (eq:let_there_be_markov): internal-order vectors, perm = internal -> user row
+__global__ void gather_col_kernel(const double* src, int64_t lds, const int32_t* perm, int64_t n, double* dst) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+    dst[r] = src[(perm ? (int64_t)perm[r] : r) * lds];
+}
+__global__ void scatter_col_kernel(const double* src, const int32_t* perm, int64_t n, double* dst, int64_t ldd) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+    dst[(perm ? (int64_t)perm[r] : r) * ldd] = src[r];
+}
+// v = p / t,  t = t' + c0 (D = diag(t), reading R6)
+__global__ void markov_scale_kernel(const double* p, const double* tprime, int64_t ldt, int tcol, double c0,
+                                    int64_t n, double* v) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+    v[r] = p[r] / (tprime[r * ldt + tcol] + c0);
+}
+
 // p[i] = 0.5 + u(seed, i0 + i), u uniform in [0,1) from a counter-based hash (splitmix64)
 __global__ void fill_hash_kernel(double* p, int64_t n, uint64_t seed, int64_t i0) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -302,6 +318,28 @@ void pack_rows(const double* src, int64_t lds, const int32_t* idx, int64_t cnt, 
   if (cnt <= 0) return;
   WL_LAUNCH("pack_rows");
   pack_rows_kernel<<<grid_for(cnt * B), 256, 0, s>>>(src, lds, idx, cnt, B, dst);
+  WL_CUDA(cudaGetLastError());
+}
+
+void gather_col(const double* src, int64_t lds, const int32_t* perm, int64_t n, double* dst, cudaStream_t s) {
+  WL_LAUNCH("markov_vec");
+  if (n <= 0) return;
+  gather_col_kernel<<<grid_for(n), 256, 0, s>>>(src, lds, perm, n, dst);
+  WL_CUDA(cudaGetLastError());
+}
+
+void scatter_col(const double* src, const int32_t* perm, int64_t n, double* dst, int64_t ldd, cudaStream_t s) {
+  WL_LAUNCH("markov_vec");
+  if (n <= 0) return;
+  scatter_col_kernel<<<grid_for(n), 256, 0, s>>>(src, perm, n, dst, ldd);
+  WL_CUDA(cudaGetLastError());
+}
+
+void markov_scale(const double* p, const double* tprime, int64_t ldt, int tcol, double c0, int64_t n, double* v,
+                  cudaStream_t s) {
+  WL_LAUNCH("markov_vec");
+  if (n <= 0) return;
+  markov_scale_kernel<<<grid_for(n), 256, 0, s>>>(p, tprime, ldt, tcol, c0, n, v);
   WL_CUDA(cudaGetLastError());
 }
 

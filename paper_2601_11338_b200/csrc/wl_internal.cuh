@@ -177,6 +177,10 @@ void pack_rows(const double* src, int64_t lds, const int32_t* idx, int64_t cnt, 
                cudaStream_t s);
 void fill(double* p, int64_t n, double v, cudaStream_t s);
 void fill_hash(double* p, int64_t n, uint64_t seed, int64_t i0, cudaStream_t s);  // 0.5 + U[0,1)
+void gather_col(const double* src, int64_t lds, const int32_t* perm, int64_t n, double* dst, cudaStream_t s);
+void scatter_col(const double* src, const int32_t* perm, int64_t n, double* dst, int64_t ldd, cudaStream_t s);
+void markov_scale(const double* p, const double* tprime, int64_t ldt, int tcol, double c0, int64_t n, double* v,
+                  cudaStream_t s);
 
 // eigenvalues of a small real upper Hessenberg matrix (host; eig.cu). H row-major n x n, overwritten.
 bool hessenberg_eigvals(std::vector<double>& H, int n, std::vector<double>& wr, std::vector<double>& wi);

@@ -75,6 +75,7 @@ def load():
         "wl_wait": ([vp, vp], ctypes.c_int),
         "wl_spectral_radius": ([vp, i32, ctypes.POINTER(dbl), vp], ctypes.c_int),
         "wl_spectral_radius_z": ([vp, i32, i32, ctypes.POINTER(dbl), vp], ctypes.c_int),
+        "wl_markov": ([vp, i32, i32, vp, vp, i64, vp, vp], ctypes.c_int),
         "wl_hessenberg_eigvals": ([i32, vp, vp, vp], ctypes.c_int),
         "wl_profile_enable": ([i32], None),
         "wl_profile_collect": ([], ctypes.c_int),
@@ -350,6 +351,20 @@ class Operator:
         rho = ctypes.c_double()
         _check(load().wl_spectral_radius(self.handle, k, ctypes.byref(rho), _stream_handle(stream)))
         return rho.value
+
+    def markov(self, p0, nsteps, theta_index=0, out=None, ws=None, stream=None):
+        """Markov chain P = I - diag(t)^{-1} 𝕃_θ (eq:let_there_be_markov): column k of the result is p_{k+1}."""
+        import torch
+        p0 = p0.reshape(-1)
+        if not (p0.is_cuda and p0.dtype == torch.float64 and p0.is_contiguous()):
+            raise TypeError("p0: expected a contiguous CUDA float64 vector")
+        if out is None:
+            out = torch.empty((self.n_local, nsteps), dtype=torch.float64, device=p0.device)
+        out2, ldp = _block(out, nsteps, "out")
+        ws = ws or self.workspace(1)
+        _check(load().wl_markov(self.handle, theta_index, nsteps, ctypes.c_void_p(p0.data_ptr()),
+                                ctypes.c_void_p(out2.data_ptr()), ldp, ws.handle, _stream_handle(stream)))
+        return out
 
     def spectral_radius_z(self, theta_index: int = 0, k: int = 60, stream=None) -> float:
         """ρ(Z_θ) of the companion operator by k Arnoldi steps on Z (wl_spectral_radius_z)."""

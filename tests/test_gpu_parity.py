@@ -352,3 +352,33 @@ def test_spectral_radius_z_vs_dense(wl):
         ref = D.rho_Z(A, 1.0 - th)
         assert abs(got - ref) <= 1e-8 * ref, (th, got, ref)
     op.close()
+
+
+def test_markov_chain_vs_oracle(wl):
+    """NEXT-3: p_{k+1} = p_k P, P = I - diag(t)^{-1}𝕃_θ (eq:let_there_be_markov, reading R6) vs the dense
+    oracle chain (oracle/markov.py, pinned to Fig. 1); mass conservation; convergence to π = t/Σt."""
+    from oracle import markov as M
+    for g in (gg.karate(), gg.barabasi_albert(300, 3, 13)):
+        A = D.adjacency(g)
+        rA = D.rho_A(A)
+        thetas = [0.0, 0.5, 1.0]
+        op = wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=thetas, f=("exp", 1.0 / rA))
+        p0 = gg.vectors(g.n, 1, 4)[:, 0] ** 2
+        p0 /= p0.sum()
+        for i, th in enumerate(thetas):
+            ph = D.phi(A, 1.0 - th, C.exp(1.0 / rA))
+            t = ph.sum(1)
+            ref = M.evolve(M.transition(D.walk_laplacian(ph), t), p0, 6)
+            got = op.markov(torch.from_numpy(p0).cuda(), 6, theta_index=i).cpu().numpy()
+            assert relerr(got, ref.T).max() < TOL, (g.name, th)
+            assert np.allclose(got.sum(0), 1.0, atol=1e-12)
+        op.close()
+    g = gg.karate()
+    A = D.adjacency(g)
+    op = wl.Operator(g.n, g.row_ptr, g.col_idx, variant="nbt", f=("resolvent", 0.5 / D.rho_A(A)))
+    p0 = np.zeros(g.n)
+    p0[0] = 1.0
+    got = op.markov(torch.from_numpy(p0).cuda(), 300).cpu().numpy()
+    t = op.diag_shift().cpu().numpy()[:, 0]
+    assert np.max(np.abs(got[:, -1] - t / t.sum())) < 1e-9
+    op.close()
