@@ -124,8 +124,8 @@ def load_graph(cfg, world, rank, torch, dist):
     return g, time.time() - t0
 
 
-def algorithmic_bytes(n, nnz, n_halo, G, K, Bmax, b, n_theta):
-    """Bytes each kernel must move per step (DESIGN.md §5), by kernel name."""
+def algorithmic_bytes(n, nnz, n_halo, G, K, Bmax, b, n_theta, reorth=2):
+    """Bytes each kernel must move per step (DESIGN.md §7), by kernel name."""
     out = {}
     def add(k, v):
         out[k] = out.get(k, 0) + v
@@ -138,13 +138,24 @@ def algorithmic_bytes(n, nnz, n_halo, G, K, Bmax, b, n_theta):
         add("spmv_binned", (csr + 2 * blk + 8 * n_halo * B))          # seed 1: gather y + write
         add("spmv_binned", (csr + 3 * blk + 8 * n_halo * B))          # seed 2: + x
         add("spmv_binned", K * (csr + 3 * blk + 8 * n_halo * B))      # Z steps
-        # DCGS2 step j: dots read q_0..q_{j-1}, p_j and the SpMM output (w's top half IS p_j's
-        # bottom half, read once); update reads the same and writes q_j and p_{j+1}
-        for j in range(K):
-            add("dcgs2_dots", (j + 1.5) * vec)   # (w top re-read from L2/HBM: not algorithmic)
-            add("dcgs2_update", (j + 3.5) * vec)
-        add("dcgs2_dots", (K + 1) * vec)                              # final delayed reorth.
-        add("combine", K * blk + blk + 8 * n * b + 8 * n * n_theta)
+        if reorth == 2:
+            # TOAR: n-vector basis U (m = j+2 vectors at step j).  dots: Gram row of the newest U
+            # vector + U^T y + |y|^2; update: u_m, x_{j+1}, z_{j+1} from y and U
+            add("dcgs2_dots", 2 * blk)                                 # seed: (t0, b0)
+            add("toar_update", 3 * blk)                                # seed: u_1
+            for j in range(K):
+                add("dcgs2_dots", (j + 3) * blk)
+                add("toar_update", (j + 6) * blk)
+            add("dcgs2_dots", (K + 2) * blk)                           # final Gram row
+            add("combine", (K + 2) * blk + blk + 8 * n * b + 8 * n * n_theta)
+        else:
+            # DCGS2 step j: dots read q_0..q_{j-1}, p_j and the SpMM output (w's top half IS p_j's
+            # bottom half, read once); update reads the same and writes q_j and p_{j+1}
+            for j in range(K):
+                add("dcgs2_dots", (j + 1.5) * vec)
+                add("dcgs2_update", (j + 3.5) * vec)
+            add("dcgs2_dots", (K + 1) * vec)                          # final delayed reorth.
+            add("combine", K * blk + blk + 8 * n * b + 8 * n * n_theta)
         add("batch_inputs", 8 * n * b + blk)
     return out
 
@@ -270,7 +281,8 @@ def run_walklap(args):
     # ---- roofline of the dominant kernel (rank 0's kernels; live CUDA-event timing) ----
     peak, peak_src = peaks()
     nnz_loc = int(ci.shape[0])
-    ab = algorithmic_bytes(n_loc, nnz_loc, op.n_halo, G, K, ws_bmax(op, b), b, op.n_theta)
+    ab = algorithmic_bytes(n_loc, nnz_loc, op.n_halo, G, K, ws_bmax(op, b), b, op.n_theta,
+                           reorth=int(os.environ.get("WL_FORCE_REORTH", "2")))
     kernels = {}
     for name, (tot_ms, cnt) in prof.items():
         per_step_ms = tot_ms / args.steps

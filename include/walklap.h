@@ -72,9 +72,13 @@ typedef struct {
 /* Options; initialise with wl_opts_default(). */
 typedef struct {
   int32_t krylov_dim;   /* Arnoldi steps k per action (default 30; 1..64) */
-  int32_t reorth;       /* 1 = reorthogonalised classical Gram-Schmidt (DCGS2: the second pass is
-                           delayed and fused with the next step's projection; default);
-                           0 = single classical Gram-Schmidt pass */
+  int32_t reorth;       /* Arnoldi orthogonalisation of the 2n-long Krylov basis of Z:
+                           2 = TOAR (default; two-level orthogonal Arnoldi): the basis is stored as [U g; U f]
+                           over k+2 n-vectors U (the halves of all Krylov vectors of Z share one
+                           n-dimensional space, eq:qrec), one dot pass + one update pass over U per
+                           step, coefficient-space Gram-Schmidt twice;
+                           1 = DCGS2 on the 2n-vectors (second pass delayed and fused with the next
+                           step's projection);  0 = single classical Gram-Schmidt pass */
   int32_t max_cols;     /* columns per internal Krylov batch (default 32; 1..32) */
   double breakdown_tol; /* lucky breakdown when ||w_{j+1}|| <= tol * ||Z q_j|| (default 1e-12) */
   double rho_bound;     /* optional upper bound on ρ(Z_θ) (e.g. ρ(A), which bounds it since
@@ -159,7 +163,8 @@ wl_status wl_operator_diag_shift(const wl_operator* op, double* t_dev, int64_t l
                                  wl_stream stream);
 
 /* Workspace for actions on up to max_b input columns (device memory is allocated here: the
- * Krylov basis takes (k+1) * 2 * n_local * min(32, n_theta*max_b) doubles). */
+ * Krylov basis takes (k+5) * n_local * min(32, n_theta*max_b) doubles with TOAR, (k+2) * 2 * n_local *
+ * min(32, n_theta*max_b) with DCGS2). */
 wl_status wl_workspace_create(const wl_operator* op, int32_t max_b, wl_workspace** out);
 void wl_workspace_destroy(wl_workspace* ws);
 /* Counters of a workspace (host): cg_iterations = CG iterations executed by actions on it so far

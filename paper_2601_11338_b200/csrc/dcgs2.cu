@@ -267,6 +267,93 @@ __global__ void __launch_bounds__(kUpdConsumers + 32, 1) dcgs2_update_ring(Dcgs2
   }
 }
 
+
+// ---- TOAR basis update (engine.cu toar_chunk): out_o = Σ_b cb[b][o] base_b + Σ_i co[o][i] U_i --------
+// Items per tile: the bases (y for the first vector tile; the outputs themselves, identity
+// coefficients, for later tiles of > 32 vectors) then U_0..U_{m-1}.  Same ring as pass B.
+constexpr int kToarMaxOut = 3;
+template <int NOUT>
+__global__ void __launch_bounds__(kUpdConsumers + 32, 1) toar_update_ring(ToarArgs a, int tpb) {
+  extern __shared__ __align__(128) double ring[];
+  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+  __shared__ double coef[NOUT * kMaxVecPerLaunch * kMaxCols];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, t = threadIdx.x;
+  const int B = a.B, m = a.m;
+  const int E = tpb * kUpdPer;
+  const int64_t N = a.len * a.B;
+  const int nb = a.accumulate ? NOUT : 1;
+  for (int i = t; i < NOUT * m * B; i += blockDim.x) {
+    const int o = i / (m * B), r = i - o * m * B;
+    coef[i] = a.coef_u[(int64_t)(o * a.coef_ld) * B + r];
+  }
+  ring_init(full, empty, kUpdConsumers / 32);
+  __syncthreads();
+  if (warp == kUpdConsumers / 32) {
+    if (lane == 0) {  // producer: items [bases..., U_0..U_{m-1}] per tile
+      int s = 0;
+      uint32_t ph = 0;
+      int64_t it = 0;
+      for (int64_t e0 = (int64_t)blockIdx.x * E; e0 < N; e0 += (int64_t)gridDim.x * E) {
+        const int cnt = (int)min((int64_t)E, N - e0);
+        for (int item = 0; item < nb + m; ++item, ++it) {
+          if (it >= kStages) mbar_wait(su32(&empty[s]), ph ^ 1);
+          const uint32_t bar = su32(&full[s]);
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(cnt * 8) : "memory");
+          const double* src = item < nb ? (a.accumulate ? a.out[item] : a.y) : a.U.p[item - nb];
+          bulk_g2s(su32(ring + (int64_t)s * kStageElems), src + e0, cnt * 8, bar);
+          if (++s == kStages) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+    return;
+  }
+  const bool act = t < tpb;
+  const int c = t % B;
+  double cy[NOUT];
+#pragma unroll
+  for (int o = 0; o < NOUT; ++o) cy[o] = a.coef_y[o * B + c];
+  RingCursor cur;
+  for (int64_t e0 = (int64_t)blockIdx.x * E; e0 < N; e0 += (int64_t)gridDim.x * E) {
+    const int cnt = (int)min((int64_t)E, N - e0);
+    double acc[NOUT][kUpdPer];
+#pragma unroll
+    for (int o = 0; o < NOUT; ++o)
+#pragma unroll
+      for (int i = 0; i < kUpdPer; ++i) acc[o][i] = 0.0;
+    for (int b = 0; b < nb; ++b) {
+      const double* st = cur.acquire(ring, full);
+#pragma unroll
+      for (int i = 0; i < kUpdPer; ++i) {
+        const double v = (act && t + i * tpb < cnt) ? st[t + i * tpb] : 0.0;
+#pragma unroll
+        for (int o = 0; o < NOUT; ++o) acc[o][i] += (a.accumulate ? (o == b ? 1.0 : 0.0) : cy[o]) * v;
+      }
+      cur.release(empty, lane);
+    }
+    for (int j = 0; j < m; ++j) {
+      double cj[NOUT];
+#pragma unroll
+      for (int o = 0; o < NOUT; ++o) cj[o] = coef[(o * m + j) * B + c];
+      const double* st = cur.acquire(ring, full);
+#pragma unroll
+      for (int i = 0; i < kUpdPer; ++i) {
+        const double v = (act && t + i * tpb < cnt) ? st[t + i * tpb] : 0.0;
+#pragma unroll
+        for (int o = 0; o < NOUT; ++o) acc[o][i] += cj[o] * v;
+      }
+      cur.release(empty, lane);
+    }
+    if (act) {
+#pragma unroll
+      for (int i = 0; i < kUpdPer; ++i)
+        if (t + i * tpb < cnt) {
+#pragma unroll
+          for (int o = 0; o < NOUT; ++o) a.out[o][e0 + t + i * tpb] = acc[o][i];
+        }
+    }
+  }
+}
+
 size_t ring_smem() { return (size_t)kStages * kStageElems * sizeof(double); }
 
 VecPtrs shifted(const VecPtrs& v, int i0) {
@@ -334,6 +421,36 @@ void dcgs2_update(Dcgs2Args a, cudaStream_t s) {
     dcgs2_update_ring<<<grid, kUpdConsumers + 32, ring_smem(), s>>>(a, tpb);
     WL_CUDA(cudaGetLastError());
   }
+}
+
+// outputs = linear combinations of one base vector and the basis U (TOAR, engine.cu).  Bases of more
+// than 32 vectors are tiled: tiles after the first read the outputs back as their bases.
+void toar_update(ToarArgs a, cudaStream_t s) {
+  if (a.nout < 1 || a.nout > kToarMaxOut) throw Error(1, "toar_update: 1..3 outputs");
+  if (a.m > kMaxVecPerLaunch) {
+    for (int i0 = 0; i0 < a.m; i0 += kMaxVecPerLaunch) {
+      ToarArgs t = a;
+      t.m = std::min(kMaxVecPerLaunch, a.m - i0);
+      t.U = shifted(a.U, i0);
+      t.coef_u = a.coef_u + (int64_t)i0 * a.B;
+      t.accumulate = i0 > 0 ? 1 : a.accumulate;
+      toar_update(t, s);
+    }
+    return;
+  }
+  WL_LAUNCH("toar_update");
+  if ((a.len * a.B) % 2) throw Error(1, "toar_update: vector length must be even (phantom row)");
+  static bool attr[kToarMaxOut + 1] = {};
+  auto kern = a.nout == 1 ? toar_update_ring<1> : a.nout == 2 ? toar_update_ring<2> : toar_update_ring<3>;
+  if (!attr[a.nout]) {
+    WL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ring_smem()));
+    attr[a.nout] = true;
+  }
+  const int tpb = kUpdConsumers / a.B * a.B;
+  const int64_t N = a.len * a.B;
+  const int grid = (int)std::min<int64_t>(148, (N + tpb * kUpdPer - 1) / (tpb * kUpdPer));
+  kern<<<grid, kUpdConsumers + 32, ring_smem(), s>>>(a, tpb);
+  WL_CUDA(cudaGetLastError());
 }
 
 }  // namespace wl

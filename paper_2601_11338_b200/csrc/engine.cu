@@ -175,6 +175,7 @@ struct wl_workspace {
   int* cg_flags_host = nullptr;  // pinned: 2 flags + kMaxCols iteration counts
   int64_t cg_iterations = 0;     // executed CG iterations (max over the columns of each solve), cumulative
   DArr<double> mk_p, mk_v;       // Markov chain: current distribution and p / t (internal order)
+  DArr<double> toar_state, toar_cy, toar_cu, toar_comb;  // TOAR (toar.cu): per-column state, update coefficients
   // host-buffer entry point
   DArr<double> hV, hLV;
   // diffusion (outer Lanczos)
@@ -379,6 +380,122 @@ void krylov_chunk(const wl_operator* op, wl_workspace* ws, int mode, const doubl
 }
 
 
+// TOAR Arnoldi on Z (opts.reorth == 2; toar.cu): the 2n-long basis is q_i = [U g_i; U f_i] over K+2
+// n-vectors U, so each step runs one dot pass and one three-output update pass over U (n-vectors)
+// instead of DCGS2's two passes over 2n-vectors.  Same seeds, SpMM, f(H) and combine as krylov_chunk.
+void toar_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double* V, int64_t ldv, int b, int gstart,
+                int B, double* out, int64_t ldo, cudaStream_t s, bool user_order) {
+  const int32_t* perm = user_order ? op->perm.p : nullptr;
+  const int64_t n = op->n_loc;
+  const int K = ws->K;
+  const int64_t n_pad = n + ((n * B) & 1);  // even element counts for the bulk copies (phantom row)
+  const int64_t vs = n_pad * B;
+  double* g0z = ws->colp.p;
+  double* g1z = g0z + kMaxCols;
+  double* g0s = g1z + kMaxCols;
+  double* g1s = g0s + kMaxCols;
+  setup_chunk(op->mu_dev.p, gstart, b, B, g0z, g1z, g0s, g1s, ws->vcol.p, ws->tcol.p, s);
+  batch_inputs(V, ldv, B, n, ws->Vb.p, ws->vcol.p, perm, s);
+  VecPtrs U{};
+  for (int i = 0; i < K + 2; ++i) U.p[i] = ws->basis.p + (int64_t)i * vs;
+  double* xb = ws->basis.p + (int64_t)(K + 2) * vs;
+  double* zb = xb + vs;
+  double* yb = zb + vs;
+  double* U0 = const_cast<double*>(U.p[0]);
+  // a3 seeds: t0 = A v -> U_0, b0 = A t0 - μ d⊙v -> x   (eq:qrec seeds); q̂_0 = [t0; b0]
+  halo_exchange(op, ws, ws->Vb.p, B, B, s);
+  do_spmv(op, ws, ws->Vb.p, nullptr, nullptr, nullptr, nullptr, U0, B, s);
+  halo_exchange(op, ws, U0, B, B, s);
+  do_spmv(op, ws, U0, ws->Vb.p, g0s, g1s, nullptr, xb, B, s);
+  if (n_pad > n) {
+    fill(U0 + n * B, B, 0.0, s);
+    fill(xb + n * B, B, 0.0, s);
+    fill(yb + n * B, B, 0.0, s);
+  }
+  WL_CUDA(cudaMemsetAsync(ws->H.p, 0, sizeof(double) * B * (K + 1) * K, s));
+  const size_t stride = toar_state_doubles(K);
+  const int ld = K + 3;
+  const double btol = op->opts.breakdown_tol;
+  Dcgs2Args d{};
+  d.len = n_pad;
+  d.B = B;
+  d.split = n_pad;
+  d.partials = ws->partials.p;
+  d.sums_out = ws->sums1.p;
+  d.Q = U;
+  ToarArgs t{};
+  t.U = U;
+  t.len = n_pad;
+  t.B = B;
+  t.coef_y = ws->toar_cy.p;
+  t.coef_u = ws->toar_cu.p;
+  t.coef_ld = ld;
+  auto coeffs = [&](int j, int final_pass) {
+    toar_coeffs(ws->sums1.p, j, final_pass, B, K, btol, ws->H.p, ws->n0.p, ws->keff.p, ws->toar_state.p, stride,
+                ws->toar_cy.p, ws->toar_cu.p, ld, s);
+  };
+  // seed step: Gram of (t0, b0), u_1 = (b0 - proj)/ν
+  d.nq = 0;
+  d.P = U0;
+  d.wa = xb;
+  dcgs2_dots(d, s);
+  allreduce(op, ws->sums1.p, (size_t)3 * B, s);
+  coeffs(-1, 0);
+  t.m = 1;
+  t.y = xb;
+  t.out[0] = const_cast<double*>(U.p[1]);
+  t.nout = 1;
+  toar_update(t, s);
+  const double* xin = xb;  // bottom half of the vector the next SpMM applies Z to
+  const double* zin = U0;  // its top half
+  for (int j = 0; j < K; ++j) {
+    const int m = j + 2;
+    // a4: y = A x + μ(μ - d)⊙z  (bottom half of Z [z; x])
+    halo_exchange(op, ws, xin, B, B, s);
+    do_spmv(op, ws, xin, zin, g0z, g1z, nullptr, yb, B, s);
+    // a5: one dot pass (Gram row of the newest U vector, U^T y, |y|^2) and one update pass
+    d.nq = m - 1;
+    d.P = U.p[m - 1];
+    d.wa = yb;
+    dcgs2_dots(d, s);
+    allreduce(op, ws->sums1.p, (size_t)(2 * (m - 1) + 3) * B, s);
+    coeffs(j, 0);
+    t.m = m;
+    t.y = yb;
+    t.out[0] = const_cast<double*>(U.p[m]);
+    t.out[1] = xb;
+    t.out[2] = zb;
+    t.nout = 3;
+    toar_update(t, s);
+    xin = xb;
+    zin = zb;
+  }
+  d.nq = K + 1;  // Gram row of the last U vector completes H column K-1
+  d.P = U.p[K + 1];
+  d.wa = nullptr;
+  dcgs2_dots(d, s);
+  allreduce(op, ws->sums1.p, (size_t)(2 * (K + 1) + 3) * B, s);
+  coeffs(K, 1);
+  // a6: y = f_1(H_k) e_1 per column; a7: combine top halves U (Σ_i comb_i g_i)
+  SmallFArgs f{};
+  f.H = ws->H.p;
+  f.K = K;
+  f.keff = ws->keff.p;
+  f.kind = op->fkind;
+  f.param = op->fparam;
+  f.coeffs = op->coeffs_dev.p;
+  f.ncoeffs = (int)op->coeffs.size();
+  f.n0 = ws->n0.p;
+  f.s = nullptr;
+  f.comb = ws->comb.p;
+  f.scratch = ws->scratch.p;
+  f.B = B;
+  small_f(f, s);
+  toar_combine_coef(ws->comb.p, B, K, ws->keff.p, ws->toar_state.p, stride, ws->toar_comb.p, s);
+  combine(mode, U, K + 2, n, B, ws->toar_comb.p, V, ldv, ws->vcol.p, op->c0, op->tprime.p, op->n_theta, ws->tcol.p,
+          out, ldo, perm, s);
+}
+
 // Resolvent action by Jacobi-preconditioned CG on the deformed Laplacian (cg.cu; opts.solver ==
 // WL_SOLVER_CG): x = 𝒜_θ(α)^{-1} V per column, then φ V = (1-μ²α²) x.  Vector roles reuse the
 // Krylov basis memory: x, r, p, q.  Synchronizes every opts.cg_check iterations.
@@ -445,6 +562,7 @@ void cg_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double* V
 void run_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double* V, int64_t ldv, int b, int gstart,
                int B, double* out, int64_t ldo, cudaStream_t s, bool user_order = true) {
   if (op->opts.solver == WL_SOLVER_CG) cg_chunk(op, ws, mode, V, ldv, b, gstart, B, out, ldo, s, user_order);
+  else if (op->opts.reorth == 2) toar_chunk(op, ws, mode, V, ldv, b, gstart, B, out, ldo, s, user_order);
   else krylov_chunk(op, ws, mode, V, ldv, b, gstart, B, out, ldo, s, user_order);
 }
 
@@ -465,6 +583,7 @@ void workspace_alloc(wl_workspace* ws, const wl_operator* op, int max_b) {
   const int64_t n = op->n_loc;
   const int B = ws->Bmax, K = ws->K;
   if (op->opts.solver == WL_SOLVER_CG) ws->basis.alloc((size_t)4 * (n + 1) * B);  // x, r, p, q
+  else if (op->opts.reorth == 2) ws->basis.alloc((size_t)(K + 5) * (n + 1) * B);  // TOAR: U (K+2), x, z, y
   else ws->basis.alloc((size_t)(K + 2) * 2 * (n + 1) * B);  // halves padded by <= 1 phantom row
   ws->S.alloc((size_t)(n + 1) * B);
   ws->Vb.alloc((size_t)n * B);
@@ -495,6 +614,12 @@ void workspace_alloc(wl_workspace* ws, const wl_operator* op, int max_b) {
   ws->cg_bb.alloc(kMaxCols);
   ws->cg_iters.alloc(kMaxCols);
   ws->cg_flags.alloc(2);
+  if (op->opts.reorth == 2) {
+    ws->toar_state.alloc(toar_state_doubles(K) * B);
+    ws->toar_cy.alloc((size_t)3 * B);
+    ws->toar_cu.alloc((size_t)3 * (K + 3) * B);
+    ws->toar_comb.alloc((size_t)(K + 2) * B);
+  }
   if (!ws->cg_flags_host) WL_CUDA(cudaMallocHost(&ws->cg_flags_host, (2 + kMaxCols) * sizeof(int)));
   spmv_scratch(op, ws, B);
   WL_CUDA(cudaDeviceSynchronize());
@@ -830,7 +955,7 @@ int64_t wl_launch_count(void) { return g_launches.load(); }
 void wl_opts_default(wl_opts* o) {
   if (!o) return;
   o->krylov_dim = 30;
-  o->reorth = 1;
+  o->reorth = 2;
   o->max_cols = 32;
   o->breakdown_tol = 1e-12;
   o->rho_bound = 0.0;
@@ -944,6 +1069,8 @@ wl_status wl_operator_create(wl_comm* comm, int64_t n_global, int64_t row_begin,
     if (op->opts.max_cols < 1 || op->opts.max_cols > kMaxCols) throw Error(WL_EINVAL, "max_cols must be in [1, 32]");
     if (!(op->opts.breakdown_tol >= 0.0)) throw Error(WL_EINVAL, "breakdown_tol < 0");
     if (op->opts.solver != WL_SOLVER_KRYLOV && op->opts.solver != WL_SOLVER_CG) throw Error(WL_EINVAL, "unknown solver");
+    if (const char* fr = getenv("WL_FORCE_REORTH")) op->opts.reorth = atoi(fr);  // experiment knob (tests)
+    if (op->opts.reorth < 0 || op->opts.reorth > 2) throw Error(WL_EINVAL, "reorth must be 0, 1 or 2");
     if (op->opts.solver == WL_SOLVER_CG) {
       if (f->kind != WL_F_RESOLVENT || !(f->param > 0.0))
         throw Error(WL_EINVAL, "WL_SOLVER_CG needs the resolvent with α > 0");

@@ -309,7 +309,7 @@ void combine(int mode, const VecPtrs& Q, int nvec, int64_t n, int B,
   else if (nvec <= 32)
     combine_kernel<32><<<g, 256, 0, s>>>(mode, Q, nvec, n, B, comb, V, ldv, vcol, c0, tprime, ldt, tcol, out, ldo, perm);
   else
-    combine_kernel<kMaxKrylov + 1><<<g, 256, 0, s>>>(mode, Q, nvec, n, B, comb, V, ldv, vcol, c0, tprime, ldt, tcol, out, ldo, perm);
+    combine_kernel<kMaxKrylov + 2><<<g, 256, 0, s>>>(mode, Q, nvec, n, B, comb, V, ldv, vcol, c0, tprime, ldt, tcol, out, ldo, perm);
   WL_CUDA(cudaGetLastError());
 }
 

@@ -103,6 +103,26 @@ struct Dcgs2Args {
   int grid;
 };
 void reduce_partials(const double* partials, int nout, int G, double* sums_out, cudaStream_t s);
+
+// TOAR basis update (dcgs2.cu): out_o = coef_y[o] y + Σ_i coef_u[o][i] U_i, o < nout <= 3.
+// coef_u layout [(o * coef_ld + i) * B + c].  Outputs must not alias y or U.
+struct ToarArgs {
+  VecPtrs U; int m;
+  int64_t len; int B;
+  const double* y;
+  double* out[3]; int nout;
+  const double* coef_y;
+  const double* coef_u; int coef_ld;
+  int accumulate;
+};
+void toar_update(ToarArgs a, cudaStream_t s);
+// TOAR coefficient bookkeeping (toar.cu), one thread per Krylov column
+size_t toar_state_doubles(int K);
+void toar_coeffs(const double* sums, int j, int final_pass, int B, int K, double btol, double* H, double* n0,
+                 int* keff, double* state, size_t stride, double* coef_y, double* coef_u, int coef_ld,
+                 cudaStream_t s);
+void toar_combine_coef(const double* comb, int B, int K, const int* keff, const double* state, size_t stride,
+                       double* combU, cudaStream_t s);
 void dcgs2_dots(Dcgs2Args a, cudaStream_t s);
 void dcgs2_update(Dcgs2Args a, cudaStream_t s);
 void dcgs2_coeffs(const double* sums, int j, int B, int K, double btol, int final_pass, int reorth, double* H,

@@ -236,7 +236,7 @@ class Operator:
     """
 
     def __init__(self, n_global, row_ptr, col_idx, thetas=(1.0,), f=("exp", 1.0), variant=None,
-                 row_range=None, comm: Comm | None = None, krylov_dim=30, reorth=1, max_cols=32,
+                 row_range=None, comm: Comm | None = None, krylov_dim=30, reorth=2, max_cols=32,
                  breakdown_tol=1e-12, rho_bound=0.0, relabel=1, solver="krylov", cg_tol=1e-9, cg_maxit=1000,
                  cg_check=8, stream=None):
         lib = load()

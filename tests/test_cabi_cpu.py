@@ -36,7 +36,7 @@ def test_opts_default(lib):
     import paper_2601_11338_b200.walklap as w
     o = w._Opts()
     lib.wl_opts_default(ctypes.byref(o))
-    assert (o.krylov_dim, o.reorth, o.max_cols, o.breakdown_tol, o.rho_bound, o.relabel) == (30, 1, 32, 1e-12, 0.0, 1)
+    assert (o.krylov_dim, o.reorth, o.max_cols, o.breakdown_tol, o.rho_bound, o.relabel) == (30, 2, 32, 1e-12, 0.0, 1)
     assert (o.solver, o.cg_tol, o.cg_maxit, o.cg_check) == (0, 1e-9, 1000, 8)
 
 
