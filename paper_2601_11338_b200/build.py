@@ -46,6 +46,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
            "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v" if verbose else "-O3",
            "-I", os.path.join(ROOT, "include"), "-I", inc,
+           *os.environ.get("WL_EXTRA_NVCC", "").split(),  # developer experiments (e.g. -DWL_SPMV_HINTS=1)
            *sources(), "-o", tmp,
            "-L", libdir, "-l:libnccl.so.2", f"-Xlinker", f"-rpath={libdir}"]
     if verbose:

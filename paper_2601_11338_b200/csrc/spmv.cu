@@ -28,6 +28,34 @@ namespace wl {
 namespace {
 
 constexpr int kThreads = 256;
+
+// Compile-time cache-hint experiment (build with WL_EXTRA_NVCC=-DWL_SPMV_HINTS=n): 1 = evict-first
+// ("cache streaming") loads/stores for the col / x / out streams, 2 = also evict-last for gathers of
+// the degree-sorted hot rows.  0 (default) = plain loads.
+#ifndef WL_SPMV_HINTS
+#define WL_SPMV_HINTS 0
+#endif
+__device__ __forceinline__ int ld_col(const int32_t* p) {
+#if WL_SPMV_HINTS >= 1
+  return __ldcs(p);
+#else
+  return __ldg(p);
+#endif
+}
+__device__ __forceinline__ double ld_stream(const double* p) {
+#if WL_SPMV_HINTS >= 1
+  return __ldcs(p);
+#else
+  return *p;
+#endif
+}
+__device__ __forceinline__ void st_stream(double* p, double v) {
+#if WL_SPMV_HINTS >= 1
+  __stcs(p, v);
+#else
+  *p = v;
+#endif
+}
 constexpr int kWarps = kThreads / 32;
 
 // Per-lane gather context.  Offsets are 32-bit (n_loc * ld < 2^31 is checked on the host), the
@@ -41,14 +69,22 @@ struct Ctx {
   const double* yc;   // y + c
   const double* yhc;  // yh + c
   int ldy, ldh;
+  uint64_t pol = 0;  // L2 evict-last policy (WL_SPMV_HINTS >= 2)
   __device__ double gather(int cl) const {
     if (HALO && cl >= a.n_loc) return __ldg(yhc + (cl - a.n_loc) * ldh);
+#if WL_SPMV_HINTS >= 2
+    if (cl < a.small_first) {
+      double v;
+      asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(yc + cl * ldy), "l"(pol));
+      return v;
+    }
+#endif
     return __ldg(yc + cl * ldy);
   }
   __device__ void write(int r, int deg, double sum) const {
     double o = sum;
-    if (a.x) o += (g0 + g1 * (double)deg) * a.x[(int64_t)r * a.ldx + c];
-    a.out[(int64_t)r * a.ldo + c] = sc * o;
+    if (a.x) o += (g0 + g1 * (double)deg) * ld_stream(a.x + (int64_t)r * a.ldx + c);
+    st_stream(a.out + (int64_t)r * a.ldo + c, sc * o);
   }
   // Σ y[col[z]] for z = z0 + first, z0 + first + step, ... < z1 (step = lane groups sharing the row)
   __device__ double strided_sum(int z0, int z1, int first, int step) const {
@@ -58,7 +94,7 @@ struct Ctx {
     for (; z < full; z += kU * step) {
       int cl[kU];
 #pragma unroll
-      for (int u = 0; u < kU; ++u) cl[u] = __ldg(a.col + z + u * step);
+      for (int u = 0; u < kU; ++u) cl[u] = ld_col(a.col + z + u * step);
       double v[kU];
 #pragma unroll
       for (int u = 0; u < kU; ++u) v[u] = gather(cl[u]);
@@ -68,7 +104,7 @@ struct Ctx {
     if (z < z1) {  // predicated tail round
       int cl[kU];
 #pragma unroll
-      for (int u = 0; u < kU; ++u) cl[u] = (z + u * step < z1) ? __ldg(a.col + z + u * step) : -1;
+      for (int u = 0; u < kU; ++u) cl[u] = (z + u * step < z1) ? ld_col(a.col + z + u * step) : -1;
       double v[kU];
 #pragma unroll
       for (int u = 0; u < kU; ++u) v[u] = cl[u] >= 0 ? gather(cl[u]) : 0.0;
@@ -105,6 +141,9 @@ __global__ void __launch_bounds__(kThreads) spmv_binned_kernel(SpmvArgs a) {
   const int cc = lane_ok ? c : 0;
   Ctx<kU, HALO> ctx{a, cc, a.g0 ? a.g0[cc] : 0.0, a.g1 ? a.g1[cc] : 0.0, a.scale ? a.scale[cc] : 1.0,
                     a.y + cc, a.yh + cc, (int)a.ldy, (int)a.ldh};
+#if WL_SPMV_HINTS >= 2
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(ctx.pol));
+#endif
   int blk = blockIdx.x;
   if (blk < a.nblk_small) {  // ---- small rows: one lane group per row
     const int idx = (blk * kWarps + warp) * gpw + gi;
@@ -172,6 +211,9 @@ __global__ void __launch_bounds__(kThreads) spmv_small_batched_kernel(SpmvArgs a
   double* sx = reinterpret_cast<double*>(s_small + kWarps * kIntsPerWarp) + warp * 32 * B;
   Ctx<kU, HALO> ctx{a, cc, a.g0 ? a.g0[cc] : 0.0, a.g1 ? a.g1[cc] : 0.0, a.scale ? a.scale[cc] : 1.0,
                     a.y + cc, a.yh + cc, (int)a.ldy, (int)a.ldh};
+#if WL_SPMV_HINTS >= 2
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(ctx.pol));
+#endif
   const int nb = (a.n_small + 31) / 32;
   for (int bt = blockIdx.x * kWarps + warp; bt < nb; bt += gridDim.x * kWarps) {
     const int r0 = a.small_first + bt * 32;
@@ -183,16 +225,16 @@ __global__ void __launch_bounds__(kThreads) spmv_small_batched_kernel(SpmvArgs a
     if (lane == 0) srow[32] = Z1 - Z0;
     const int T = Z1 - Z0;
 #pragma unroll 4
-    for (int p = lane; p < T; p += 32) scol[p] = __ldg(a.col + Z0 + p);
+    for (int p = lane; p < T; p += 32) scol[p] = ld_col(a.col + Z0 + p);
     if (a.x)
-      for (int e = lane; e < nr * B; e += 32) sx[e] = __ldg(a.x + (int64_t)r0 * B + e);
+      for (int e = lane; e < nr * B; e += 32) sx[e] = ld_stream(a.x + (int64_t)r0 * B + e);
     __syncwarp();
     if (lane_ok) {
       const int ia = gi * nr / gpw, ib = (gi + 1) * nr / gpw;  // this group's rows
       auto flush = [&](int i, double acc) {
         double o = acc;
         if (a.x) o += (ctx.g0 + ctx.g1 * (double)(srow[i + 1] - srow[i])) * sx[i * B + c];
-        a.out[(int64_t)(r0 + i) * a.ldo + c] = ctx.sc * o;
+        st_stream(a.out + (int64_t)(r0 + i) * a.ldo + c, ctx.sc * o);
       };
       int cur = ia, rend = srow[ia + 1];
       const int P1 = srow[ib];
