@@ -44,6 +44,34 @@ __global__ void __launch_bounds__(256) reg_kernel(const double* Y, int ld, const
   }
 }
 
+
+// double2 variant: rows padded to ld (even), W = ld/2 lanes per row, each lane loads 16 bytes
+template <int U>
+__global__ void __launch_bounds__(256) reg2_kernel(const double* Y, int ld, const int* idx, int64_t m, int D, int B, double* out) {
+  const int W = ld / 2;
+  const int lane = threadIdx.x & 31, gpw = 32 / W, gi = lane / W, c = lane - gi * W;
+  const bool ok = gi < gpw;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const int64_t nw = (int64_t)gridDim.x * blockDim.x / 32;
+  for (int64_t r = gw * gpw + gi; r - gi < m; r += nw * gpw) {
+    if (!ok || r >= m) continue;
+    const int* ix = idx + r * D;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int k = 0; k < D; k += U) {
+      int cl[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) cl[u] = k + u < D ? __ldg(ix + k + u) : -1;
+      double2 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = cl[u] >= 0 ? __ldg(reinterpret_cast<const double2*>(Y + (int64_t)cl[u] * ld) + c) : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int u = 0; u < U; ++u) { acc.x += v[u].x; acc.y += v[u].y; }
+    }
+    if (2 * c < B) out[r * B + 2 * c] = acc.x;
+    if (2 * c + 1 < B) out[r * B + 2 * c + 1] = acc.y;
+  }
+}
+
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t ph) {
   asm volatile("{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W_%=;\n}" ::"r"(bar), "r"(ph) : "memory");
@@ -136,6 +164,11 @@ int main() {
     float ms; cudaEventElapsedTime(&ms, a, b); char nm[64]; snprintf(nm, 64, "reg U=%d ld=%d grid=%d", U, ld, G); report(nm, ms / 3); }
   REG(4, 11, Y11, 148 * 8) REG(8, 11, Y11, 148 * 8) REG(10, 11, Y11, 148 * 8) REG(20, 11, Y11, 148 * 8) REG(20, 11, Y11, 148 * 4)
   REG(8, 12, Y12, 148 * 8) REG(20, 12, Y12, 148 * 8)
+#define REG2(U, G) { reg2_kernel<U><<<G, 256>>>(Y12, 12, idx, m, D, B, out); cudaEventRecord(a); \
+    for (int r = 0; r < 3; ++r) reg2_kernel<U><<<G, 256>>>(Y12, 12, idx, m, D, B, out); cudaEventRecord(b); CK(cudaEventSynchronize(b)); \
+    float ms; cudaEventElapsedTime(&ms, a, b); char nm[64]; snprintf(nm, 64, "reg2 (double2) U=%d ld=12 grid=%d", U, G); report(nm, ms / 3); }
+  REG2(4, 148 * 8) REG2(8, 148 * 8) REG2(20, 148 * 8)
+  return 0;
   // TMA gather4
   EncodeFn enc = nullptr;
   cudaDriverEntryPointQueryResult q;
