@@ -297,6 +297,13 @@ def run_walklap(args):
     roof = {"kernel": top, "bound": "hbm", "achieved": kernels[top]["achieved_gbs"], "peak": peak,
             "unit": "GB/s", "frac": kernels[top]["frac"], "peak_source": peak_src,
             "traffic": ncu.get(top), "alg_bytes_per_launch": ab[top] / max(1, kernels[top]["launches_per_step"])}
+    if top == "spmv_binned" and ncu.get(top):
+        # the SpMM's real bound is the rate HBM serves random rows: context for `frac`
+        ms_launch = kernels[top]["ms_per_step"] / max(1, kernels[top]["launches_per_step"])
+        roof["traffic_gbs"] = ncu[top] / (ms_launch / 1e3) / 1e9
+        roof["traffic_frac"] = roof["traffic_gbs"] / peak
+        roof["gathers_per_s"] = nnz_loc / (ms_launch / 1e3)
+        roof["uniform_random_gather_ceiling_per_s"] = 3.3e10  # tools/gather_bench.cu, 88-byte rows, no reuse
     spmv = kernels.get("spmv_binned", {})
 
     cpu = None
