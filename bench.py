@@ -197,7 +197,8 @@ def run_walklap(args):
     beta = 1.0 / rho
     thetas = cfg["thetas"]
     K = args.krylov if args.krylov else cfg["krylov_dim"]
-    op = wl.Operator(g.n, rp, ci, thetas=thetas, f=("exp", beta), row_range=(rb, re), comm=comm, krylov_dim=K)
+    op = wl.Operator(g.n, rp, ci, thetas=thetas, f=("exp", beta), row_range=(rb, re), comm=comm, krylov_dim=K,
+                     max_cols=args.max_cols)
     torch.cuda.synchronize()
     t_create = time.time() - t0
     b = args.b if args.b else cfg["b"]
@@ -540,6 +541,7 @@ def main():
     ap.add_argument("--b", type=int, default=0)
     ap.add_argument("--krylov", type=int, default=0)
     ap.add_argument("--rho-k", type=int, default=60)
+    ap.add_argument("--max-cols", type=int, default=32, help="columns per internal Krylov batch (opts.max_cols)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--graph", action="store_true", help="also time the step captured as one CUDA graph")
