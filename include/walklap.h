@@ -67,6 +67,9 @@ typedef struct {
   double param;         /* β (WL_F_EXP) or α (WL_F_RESOLVENT) */
   const double* coeffs; /* host; WL_F_SERIES only */
   int32_t ncoeffs;      /* 1..64; WL_F_SERIES only */
+  double scale;         /* multiplies 𝕃 (wl_apply, wl_diffuse); 0 means 1.  The paper's eq:katz-based-
+                           walk-laplacian uses (1-α²); Fig. 4b was produced with (1-α), i.e. scale =
+                           1/(1+α) (reading R5).  φ, t and the Markov chain are not scaled. */
 } wl_walkfun;
 
 /* Options; initialise with wl_opts_default(). */

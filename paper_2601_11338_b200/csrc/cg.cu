@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(256) cg_reduce_scalar_kernel(int which, int no
 
 // out (user order) from the solution x = 𝒜^{-1} b:  φ b = (1-μ²α²) x
 //   mode 0: out = φ V;  mode 1: out = (t' + c0) ⊙ V - φ V;  mode 2 (V = 1): t' = φ 1 - c0 (internal order)
-__global__ void cg_combine_kernel(int mode, const double* x, int64_t n, int B, const double* cs, const double* V,
+__global__ void cg_combine_kernel(int mode, double lscale, const double* x, int64_t n, int B, const double* cs, const double* V,
                                   int64_t ldv, const int* vcol, double c0, const double* tprime, int64_t ldt,
                                   const int* tcol, double* out, int64_t ldo, const int32_t* perm) {
   const int64_t N = n * B;
@@ -227,7 +227,7 @@ __global__ void cg_combine_kernel(int mode, const double* x, int64_t n, int B, c
     }
     const int64_t ru = perm ? perm[r] : r;
     const double v = V ? V[ru * ldv + vcol[c]] : 1.0;
-    out[ru * ldo + c] = mode == 0 ? ph : (tprime[r * ldt + tcol[c]] + c0) * v - ph;
+    out[ru * ldo + c] = mode == 0 ? ph : lscale * ((tprime[r * ldt + tcol[c]] + c0) * v - ph);
   }
 }
 
@@ -291,13 +291,13 @@ void cg_scalar(int which, const CgArgs& a, cudaStream_t s) {
   WL_CUDA(cudaGetLastError());
 }
 
-void cg_combine(int mode, const double* x, int64_t n, int B, const double* cs, const double* V, int64_t ldv,
+void cg_combine(int mode, double lscale, const double* x, int64_t n, int B, const double* cs, const double* V, int64_t ldv,
                 const int* vcol, double c0, const double* tprime, int64_t ldt, const int* tcol, double* out,
                 int64_t ldo, const int32_t* perm, cudaStream_t s) {
   WL_LAUNCH("cg_combine");
   const int64_t N = n * B;
   const int g = (int)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, 148 * 8));
-  cg_combine_kernel<<<g, 256, 0, s>>>(mode, x, n, B, cs, V, ldv, vcol, c0, tprime, ldt, tcol, out, ldo, perm);
+  cg_combine_kernel<<<g, 256, 0, s>>>(mode, lscale, x, n, B, cs, V, ldv, vcol, c0, tprime, ldt, tcol, out, ldo, perm);
   WL_CUDA(cudaGetLastError());
 }
 

@@ -146,6 +146,7 @@ struct wl_operator {
   DArr<double> mu_dev;
   int fkind = WL_F_EXP;
   double fparam = 1.0, c0 = 1.0;
+  double lscale = 1.0;  // multiplies 𝕃 (wl_walkfun.scale)
   std::vector<double> coeffs;
   DArr<double> coeffs_dev;
   wl_opts opts{};
@@ -375,7 +376,7 @@ void krylov_chunk(const wl_operator* op, wl_workspace* ws, int mode, const doubl
   f.B = B;
   small_f(f, s);
   // a7: combine (top halves of the basis)
-  combine(mode, slot, K, n, B, ws->comb.p, V, ldv, ws->vcol.p, op->c0,
+  combine(mode, op->lscale, slot, K, n, B, ws->comb.p, V, ldv, ws->vcol.p, op->c0,
           op->tprime.p, op->n_theta, ws->tcol.p, out, ldo, perm, s);
 }
 
@@ -492,7 +493,7 @@ void toar_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double*
   f.B = B;
   small_f(f, s);
   toar_combine_coef(ws->comb.p, B, K, ws->keff.p, ws->toar_state.p, stride, ws->toar_comb.p, s);
-  combine(mode, U, K + 2, n, B, ws->toar_comb.p, V, ldv, ws->vcol.p, op->c0, op->tprime.p, op->n_theta, ws->tcol.p,
+  combine(mode, op->lscale, U, K + 2, n, B, ws->toar_comb.p, V, ldv, ws->vcol.p, op->c0, op->tprime.p, op->n_theta, ws->tcol.p,
           out, ldo, perm, s);
 }
 
@@ -551,7 +552,7 @@ void cg_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double* V
       done = ws->cg_flags_host[1] == 0;
     }
   }
-  cg_combine(mode, a.x, n, B, ws->cg_cs.p, V, ldv, ws->vcol.p, op->c0, op->tprime.p, op->n_theta, ws->tcol.p, out,
+  cg_combine(mode, op->lscale, a.x, n, B, ws->cg_cs.p, V, ldv, ws->vcol.p, op->c0, op->tprime.p, op->n_theta, ws->tcol.p, out,
              ldo, perm, s);
   WL_CUDA(cudaMemcpyAsync(ws->cg_flags_host + 2, ws->cg_iters.p, B * sizeof(int), cudaMemcpyDeviceToHost, s));
   WL_CUDA(cudaStreamSynchronize(s));
@@ -1095,6 +1096,7 @@ wl_status wl_operator_create(wl_comm* comm, int64_t n_global, int64_t row_begin,
     // walk weights
     op->fkind = f->kind;
     op->fparam = f->param;
+    op->lscale = f->scale != 0.0 ? f->scale : 1.0;
     if (f->kind == WL_F_EXP) {
       op->c0 = 1.0;
     } else if (f->kind == WL_F_RESOLVENT) {

@@ -61,7 +61,7 @@ __global__ void finalize_step_kernel(const double* sums1, const double* sums2, c
 // mode 1: out = t' ⊙ V - Σ_i comb_i Q_i        (𝕃 V = diag(t)V - φV, c_0 cancels)
 // mode 2: out = Σ_i comb_i Q_i                 (t' = φ1 - c_0 1 for V = 1)
 template <int NV>
-__global__ void combine_kernel(int mode, const VecPtrs Q, int nvec, int64_t n, int B,
+__global__ void combine_kernel(int mode, double lscale, const VecPtrs Q, int nvec, int64_t n, int B,
                                const double* comb, const double* V, int64_t ldv, const int* vcol,
                                double c0, const double* tprime, int64_t ldt, const int* tcol,
                                double* out, int64_t ldo, const int32_t* perm) {
@@ -84,7 +84,7 @@ __global__ void combine_kernel(int mode, const VecPtrs Q, int nvec, int64_t n, i
       out[r * ldo + c] = o;  // t' stays in internal order
     } else {
       const double v = V ? V[ru * ldv + vcol[c]] : 1.0;
-      o = (mode == 0) ? c0 * v + acc : tprime[r * ldt + tcol[c]] * v - acc;
+      o = (mode == 0) ? c0 * v + acc : lscale * (tprime[r * ldt + tcol[c]] * v - acc);
       out[ru * ldo + c] = o;
     }
   }
@@ -298,18 +298,18 @@ void finalize_step(const double* sums1, const double* sums2, const double* sums3
   WL_CUDA(cudaGetLastError());
 }
 
-void combine(int mode, const VecPtrs& Q, int nvec, int64_t n, int B,
+void combine(int mode, double lscale, const VecPtrs& Q, int nvec, int64_t n, int B,
                  const double* comb, const double* V, int64_t ldv, const int* vcol, double c0,
                  const double* tprime, int64_t ldt, const int* tcol, double* out, int64_t ldo,
                  const int32_t* perm, cudaStream_t s) {
   WL_LAUNCH("combine");
   const int g = grid_for(n * B);
   if (nvec <= 16)
-    combine_kernel<16><<<g, 256, 0, s>>>(mode, Q, nvec, n, B, comb, V, ldv, vcol, c0, tprime, ldt, tcol, out, ldo, perm);
+    combine_kernel<16><<<g, 256, 0, s>>>(mode, lscale, Q, nvec, n, B, comb, V, ldv, vcol, c0, tprime, ldt, tcol, out, ldo, perm);
   else if (nvec <= 32)
-    combine_kernel<32><<<g, 256, 0, s>>>(mode, Q, nvec, n, B, comb, V, ldv, vcol, c0, tprime, ldt, tcol, out, ldo, perm);
+    combine_kernel<32><<<g, 256, 0, s>>>(mode, lscale, Q, nvec, n, B, comb, V, ldv, vcol, c0, tprime, ldt, tcol, out, ldo, perm);
   else
-    combine_kernel<kMaxKrylov + 2><<<g, 256, 0, s>>>(mode, Q, nvec, n, B, comb, V, ldv, vcol, c0, tprime, ldt, tcol, out, ldo, perm);
+    combine_kernel<kMaxKrylov + 2><<<g, 256, 0, s>>>(mode, lscale, Q, nvec, n, B, comb, V, ldv, vcol, c0, tprime, ldt, tcol, out, ldo, perm);
   WL_CUDA(cudaGetLastError());
 }
 

@@ -150,7 +150,7 @@ void cg_direction(CgArgs a, cudaStream_t s);
 void cg_scalar(int which, const CgArgs& a, cudaStream_t s);         // after reduce (+ allreduce)
 void cg_reduce(int which, const CgArgs& a, cudaStream_t s);         // partials -> sums
 void cg_reduce_scalar(int which, const CgArgs& a, cudaStream_t s);  // single GPU: both in one CTA
-void cg_combine(int mode, const double* x, int64_t n, int B, const double* cs, const double* V, int64_t ldv,
+void cg_combine(int mode, double lscale, const double* x, int64_t n, int B, const double* cs, const double* V, int64_t ldv,
                 const int* vcol, double c0, const double* tprime, int64_t ldt, const int* tcol, double* out,
                 int64_t ldo, const int32_t* perm, cudaStream_t s);
 
@@ -185,11 +185,11 @@ void finalize_norm0(const double* sums, int B, double* n0, double* s0, int* keff
 void finalize_step(const double* sums1, const double* sums2, const double* sums3, int j, int B,
                    int K, double btol, int reorth, double* s_all, double* H, int* keff,
                    cudaStream_t s);
-// combine: mode 0 = φV (c0 V + Σ comb_i Q_i,top), 1 = 𝕃V (t'⊙V - Σ comb_i Q_i,top),
+// combine: mode 0 = φV (c0 V + Σ comb_i Q_i,top), 1 = 𝕃V (lscale (t'⊙V - Σ comb_i Q_i,top)),
 //          2 = t' (Σ comb_i Q_i,top) for V = 1
 // V column of batch column c is vcol[c]; t' column is tcol[c]; internal row r is user row
 // perm[r] (modes 0/1 read V and write out in user order; mode 2 writes t' in internal order).
-void combine(int mode, const VecPtrs& Q, int nvec, int64_t n, int B,
+void combine(int mode, double lscale, const VecPtrs& Q, int nvec, int64_t n, int B,
              const double* comb, const double* V, int64_t ldv, const int* vcol, double c0,
              const double* tprime, int64_t ldt, const int* tcol, double* out, int64_t ldo,
              const int32_t* perm, cudaStream_t s);

@@ -29,7 +29,8 @@ class WalkLapError(RuntimeError):
 
 class _WalkFun(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("param", ctypes.c_double),
-                ("coeffs", ctypes.POINTER(ctypes.c_double)), ("ncoeffs", ctypes.c_int32)]
+                ("coeffs", ctypes.POINTER(ctypes.c_double)), ("ncoeffs", ctypes.c_int32),
+                ("scale", ctypes.c_double)]
 
 
 class _Opts(ctypes.Structure):
@@ -233,12 +234,13 @@ class Operator:
     of those rows (global offsets and column ids).  f = ("exp", β) | ("resolvent", α) |
     ("series", [c0, c1, ...]).  solver="cg" (resolvent only) evaluates φ_θ = (1-μ²α²) 𝒜_θ(α)^{-1} by
     Jacobi-preconditioned conjugate gradients on the deformed Laplacian instead of Krylov on Z.
+    lap_scale multiplies 𝕃 (wl_walkfun.scale; 1/(1+α) reproduces Fig. 4b's (1-α) normalisation).
     """
 
     def __init__(self, n_global, row_ptr, col_idx, thetas=(1.0,), f=("exp", 1.0), variant=None,
                  row_range=None, comm: Comm | None = None, krylov_dim=30, reorth=2, max_cols=32,
                  breakdown_tol=1e-12, rho_bound=0.0, relabel=1, solver="krylov", cg_tol=1e-9, cg_maxit=1000,
-                 cg_check=8, stream=None):
+                 cg_check=8, lap_scale=1.0, stream=None):
         lib = load()
         rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
         ci = np.ascontiguousarray(col_idx, dtype=np.int32)
@@ -261,6 +263,7 @@ class Operator:
             wf.kind, wf.param, wf.coeffs, wf.ncoeffs = WL_F_SERIES, 0.0, coeffs, len(param)
         else:
             raise ValueError(kind)
+        wf.scale = float(lap_scale)
         opts = _Opts()
         lib.wl_opts_default(ctypes.byref(opts))
         opts.krylov_dim, opts.reorth, opts.max_cols = krylov_dim, reorth, max_cols

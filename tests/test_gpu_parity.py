@@ -104,7 +104,17 @@ def test_fig4b_through_gpu_operator(wl):
     Lap = op.apply(torch.eye(34, dtype=torch.float64, device="cuda")).cpu().numpy()
     ph = D.return_probability(Lap / (1.0 + alpha), gold[:, 0])
     assert np.max(np.abs(ph - gold[:, 1])) < 1e-9
+    t = op.diag_shift().cpu().numpy()
     op.close()
+    # the same through the C ABI's 𝕃 scale (wl_walkfun.scale = 1/(1+α), reading R5), Krylov and CG solvers;
+    # t = φ1 is not scaled
+    for solver in ("krylov", "cg"):
+        op = wl.Operator(g.n, g.row_ptr, g.col_idx, variant="nbt", f=("resolvent", alpha), krylov_dim=64,
+                         lap_scale=1.0 / (1.0 + alpha), solver=solver, cg_tol=1e-14)
+        Ls = op.apply(torch.eye(34, dtype=torch.float64, device="cuda")).cpu().numpy()
+        assert np.max(np.abs(D.return_probability(Ls, gold[:, 0]) - gold[:, 1])) < 1e-9, solver
+        assert np.allclose(op.diag_shift().cpu().numpy(), t, rtol=1e-10, atol=0)
+        op.close()
 
 
 @pytest.mark.parametrize("theta", [1.0, 0.5, 0.0])
