@@ -41,7 +41,8 @@ typedef enum {
                          self loop or duplicate entry (simple graphs only) */
   WL_EDIVERGE = 3,    /* resolvent with α·ρ ≥ 1: the series of Prop. pro:whe-we-converge diverges
                          (Remark P:390-392); CG solver: 𝒜_θ(α) not positive definite */
-  WL_ENOCONV = 4,     /* CG solver: a column did not reach cg_tol within cg_maxit (best iterate written) */
+  WL_ENOCONV = 4,     /* CG solver: a column did not reach cg_tol within cg_maxit; Krylov: the a-posteriori
+                         estimate exceeded opts.tol (reported by wl_wait).  Best iterate written. */
   WL_ENOMEM = 5,      /* device allocation failed */
   WL_ECUDA = 6,       /* CUDA runtime error (message has the CUDA error string) */
   WL_ENCCL = 7,       /* NCCL error */
@@ -99,6 +100,10 @@ typedef struct {
   double cg_tol;        /* relative residual ||b - 𝒜x|| <= cg_tol ||b|| per column (default 1e-9) */
   int32_t cg_maxit;     /* iteration cap (default 1000) */
   int32_t cg_check;     /* convergence is read back every cg_check iterations (default 8) */
+  double tol;           /* a-posteriori Krylov check (reading R11): when > 0, every action estimates
+                           ||u|| h_{k+1,k} |e_k^T f_1(H_k) e_1| relative to ||u|| ||f_1(H_k) e_1|| per column;
+                           an estimate above tol sets a sticky WL_ENOCONV that wl_wait reports (the
+                           result is still written).  0 = no check (default). */
 } wl_opts;
 
 typedef enum { WL_SOLVER_KRYLOV = 0, WL_SOLVER_CG = 1 } wl_solver;
@@ -240,7 +245,9 @@ wl_status wl_profile_collect(void);
 int32_t wl_profile_count(void);
 wl_status wl_profile_get(int32_t i, const char** name, double* total_ms, int64_t* launches);
 
-/* Synchronizes `stream` and returns the first asynchronous error recorded on `op` (or WL_OK). */
+/* Synchronizes `stream` and returns the first asynchronous error recorded on `op` (or WL_OK): CUDA
+ * errors, and WL_ENOCONV when an action's a-posteriori Krylov estimate exceeded opts.tol (the flag is
+ * cleared by the call). */
 wl_status wl_wait(const wl_operator* op, wl_stream stream);
 
 #ifdef __cplusplus

@@ -147,6 +147,7 @@ struct wl_operator {
   int fkind = WL_F_EXP;
   double fparam = 1.0, c0 = 1.0;
   double lscale = 1.0;  // multiplies 𝕃 (wl_walkfun.scale)
+  mutable DArr<int> kstat;  // sticky a-posteriori Krylov check (opts.tol): [bits, pad, max estimate (2 ints)]
   std::vector<double> coeffs;
   DArr<double> coeffs_dev;
   wl_opts opts{};
@@ -176,6 +177,7 @@ struct wl_workspace {
   int* cg_flags_host = nullptr;  // pinned: 2 flags + kMaxCols iteration counts
   int64_t cg_iterations = 0;     // executed CG iterations (max over the columns of each solve), cumulative
   DArr<double> mk_p, mk_v;       // Markov chain: current distribution and p / t (internal order)
+  DArr<double> kerr;             // a-posteriori Krylov error estimates per column (opts.tol > 0)
   DArr<double> toar_state, toar_cy, toar_cu, toar_comb;  // TOAR (toar.cu): per-column state, update coefficients
   // host-buffer entry point
   DArr<double> hV, hLV;
@@ -374,7 +376,9 @@ void krylov_chunk(const wl_operator* op, wl_workspace* ws, int mode, const doubl
   f.comb = ws->comb.p;
   f.scratch = ws->scratch.p;
   f.B = B;
+  f.err = op->opts.tol > 0.0 ? ws->kerr.p : nullptr;
   small_f(f, s);
+  if (op->opts.tol > 0.0) krylov_check(ws->kerr.p, B, op->opts.tol, op->kstat.p, s);
   // a7: combine (top halves of the basis)
   combine(mode, op->lscale, slot, K, n, B, ws->comb.p, V, ldv, ws->vcol.p, op->c0,
           op->tprime.p, op->n_theta, ws->tcol.p, out, ldo, perm, s);
@@ -491,7 +495,9 @@ void toar_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double*
   f.comb = ws->comb.p;
   f.scratch = ws->scratch.p;
   f.B = B;
+  f.err = op->opts.tol > 0.0 ? ws->kerr.p : nullptr;
   small_f(f, s);
+  if (op->opts.tol > 0.0) krylov_check(ws->kerr.p, B, op->opts.tol, op->kstat.p, s);
   toar_combine_coef(ws->comb.p, B, K, ws->keff.p, ws->toar_state.p, stride, ws->toar_comb.p, s);
   combine(mode, op->lscale, U, K + 2, n, B, ws->toar_comb.p, V, ldv, ws->vcol.p, op->c0, op->tprime.p, op->n_theta, ws->tcol.p,
           out, ldo, perm, s);
@@ -611,6 +617,7 @@ void workspace_alloc(wl_workspace* ws, const wl_operator* op, int max_b) {
   ws->tcol.alloc(kMaxCols);
   ws->colp.alloc(4 * kMaxCols);
   ws->cg_cs.alloc(8 * kMaxCols);
+  ws->kerr.alloc(kMaxCols);
   ws->cg_sc.alloc(4 * kMaxCols);
   ws->cg_bb.alloc(kMaxCols);
   ws->cg_iters.alloc(kMaxCols);
@@ -965,6 +972,7 @@ void wl_opts_default(wl_opts* o) {
   o->cg_tol = 1e-9;
   o->cg_maxit = 1000;
   o->cg_check = 8;
+  o->tol = 0.0;
 }
 
 wl_status wl_nccl_unique_id(void* out128) {
@@ -1072,6 +1080,9 @@ wl_status wl_operator_create(wl_comm* comm, int64_t n_global, int64_t row_begin,
     if (op->opts.solver != WL_SOLVER_KRYLOV && op->opts.solver != WL_SOLVER_CG) throw Error(WL_EINVAL, "unknown solver");
     if (const char* fr = getenv("WL_FORCE_REORTH")) op->opts.reorth = atoi(fr);  // experiment knob (tests)
     if (op->opts.reorth < 0 || op->opts.reorth > 2) throw Error(WL_EINVAL, "reorth must be 0, 1 or 2");
+    if (!(op->opts.tol >= 0.0)) throw Error(WL_EINVAL, "tol must be >= 0");
+    op->kstat.alloc(4);
+    WL_CUDA(cudaMemset(op->kstat.p, 0, 4 * sizeof(int)));
     if (op->opts.solver == WL_SOLVER_CG) {
       if (f->kind != WL_F_RESOLVENT || !(f->param > 0.0))
         throw Error(WL_EINVAL, "WL_SOLVER_CG needs the resolvent with α > 0");
@@ -1126,6 +1137,7 @@ wl_status wl_operator_create(wl_comm* comm, int64_t n_global, int64_t row_begin,
       workspace_alloc(&ws, op.get(), 1);
       run_action(op.get(), &ws, 2, nullptr, 1, 1, op->tprime.p, op->n_theta, s);
       WL_CUDA(cudaStreamSynchronize(s));
+      WL_CUDA(cudaMemset(op->kstat.p, 0, 4 * sizeof(int)));  // opts.tol reports on actions, not on t
     }
     *out = op.release();
   });
@@ -1439,6 +1451,14 @@ wl_status wl_wait(const wl_operator* op, wl_stream stream) {
     DeviceGuard dg(op->device);
     WL_CUDA(cudaStreamSynchronize(S_(stream)));
     WL_CUDA(cudaGetLastError());
+    int st[4] = {0, 0, 0, 0};
+    WL_CUDA(cudaMemcpy(st, op->kstat.p, sizeof(st), cudaMemcpyDeviceToHost));
+    if (st[0] & 1) {
+      WL_CUDA(cudaMemset(op->kstat.p, 0, sizeof(st)));
+      double est;
+      std::memcpy(&est, st + 2, sizeof(est));
+      throw Error(WL_ENOCONV, "a-posteriori Krylov estimate " + std::to_string(est) + " above opts.tol (best iterate written)");
+    }
   });
 }
 

@@ -101,6 +101,14 @@ __global__ void pack_rows_kernel(const double* src, int64_t lds, const int32_t* 
   }
 }
 
+__global__ void krylov_check_kernel(const double* err, int B, double tol, int* flag) {
+  const int c = threadIdx.x;
+  if (c < B && err[c] > tol) {
+    atomicOr(flag, 1);
+    atomicMax(reinterpret_cast<unsigned long long*>(flag + 2), (unsigned long long)__double_as_longlong(err[c]));
+  }
+}
+
 // Markov chain helpers (eq:let_there_be_markov): internal-order vectors, perm = internal -> user row
 __global__ void gather_col_kernel(const double* src, int64_t lds, const int32_t* perm, int64_t n, double* dst) {
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
@@ -318,6 +326,12 @@ void pack_rows(const double* src, int64_t lds, const int32_t* idx, int64_t cnt, 
   if (cnt <= 0) return;
   WL_LAUNCH("pack_rows");
   pack_rows_kernel<<<grid_for(cnt * B), 256, 0, s>>>(src, lds, idx, cnt, B, dst);
+  WL_CUDA(cudaGetLastError());
+}
+
+void krylov_check(const double* err, int B, double tol, int* flag, cudaStream_t s) {
+  WL_LAUNCH("krylov_check");
+  krylov_check_kernel<<<1, 32, 0, s>>>(err, B, tol, flag);
   WL_CUDA(cudaGetLastError());
 }
 

@@ -212,6 +212,17 @@ __global__ void __launch_bounds__(kBS) small_f_kernel(SmallFArgs a) {
   }
   __syncthreads();
   const double n0 = a.n0[c];
+  // a-posteriori estimate (kinds 0-2): ||u|| h_{k+1,k} |e_k^T y| relative to ||u|| ||y||; exact (0) after a
+  // breakdown (m < K: invariant Krylov space)
+  if (a.kind != 3 && a.err && threadIdx.x == 0) {
+    double e = 0.0;
+    if (m == K && m > 0) {
+      double yy = 0.0;
+      for (int i = 0; i < m; ++i) yy += y[i] * y[i];
+      e = yy > 0.0 ? fabs(H[(m - 1) * (K + 1) + m] * y[m - 1]) / sqrt(yy) : 0.0;
+    }
+    a.err[c] = e;
+  }
   for (int i = threadIdx.x; i <= K; i += blockDim.x) {
     const double v = (i < m) ? n0 * y[i] * (a.s ? a.s[i * B + c] : 1.0) : 0.0;
     if (a.kind == 3) a.comb[(int64_t)p * (K + 1) + i] = v;

@@ -170,6 +170,7 @@ struct SmallFArgs {
   int B;             // columns of H/s/n0 (problems for kinds 0-2)
   const double* tau; // kind 3 only: nprob values
   int nprob;         // kind 3 only
+  double* err;       // optional (kinds 0-2): relative a-posteriori error estimate per column
 };
 void small_f(const SmallFArgs& a, cudaStream_t s);
 
@@ -196,6 +197,8 @@ void combine(int mode, double lscale, const VecPtrs& Q, int nvec, int64_t n, int
 void pack_rows(const double* src, int64_t lds, const int32_t* idx, int64_t cnt, int B, double* dst,
                cudaStream_t s);
 void fill(double* p, int64_t n, double v, cudaStream_t s);
+// sticky convergence flag: flag[0] |= 1 and flag[1] = max estimate (as bits) when err[c] > tol
+void krylov_check(const double* err, int B, double tol, int* flag, cudaStream_t s);
 void fill_hash(double* p, int64_t n, uint64_t seed, int64_t i0, cudaStream_t s);  // 0.5 + U[0,1)
 void gather_col(const double* src, int64_t lds, const int32_t* perm, int64_t n, double* dst, cudaStream_t s);
 void scatter_col(const double* src, const int32_t* perm, int64_t n, double* dst, int64_t ldd, cudaStream_t s);

@@ -37,7 +37,7 @@ def test_opts_default(lib):
     o = w._Opts()
     lib.wl_opts_default(ctypes.byref(o))
     assert (o.krylov_dim, o.reorth, o.max_cols, o.breakdown_tol, o.rho_bound, o.relabel) == (30, 2, 32, 1e-12, 0.0, 1)
-    assert (o.solver, o.cg_tol, o.cg_maxit, o.cg_check) == (0, 1e-9, 1000, 8)
+    assert (o.solver, o.cg_tol, o.cg_maxit, o.cg_check, o.tol) == (0, 1e-9, 1000, 8, 0.0)
 
 
 def _partition_def(row_ptr, P):

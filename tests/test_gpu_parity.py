@@ -415,3 +415,29 @@ def test_orthogonalisation_variants_vs_series(wl, reorth, K):
     tol = {1: 1e-1, 2: 1e-2, 7: 1e-8}.get(K, TOL)
     assert worst < tol, (reorth, K, worst)
     op.close()
+
+
+def test_aposteriori_krylov_check(wl):
+    """opts.tol (reading R11): a truncated Krylov space (k = 3) trips the sticky WL_ENOCONV reported by
+    wl_wait, with the best iterate still written; a converged one (k = 30) does not, for both bases."""
+    g = gg.karate()
+    A = D.adjacency(g)
+    beta = 1.0 / D.rho_A(A)
+    V = torch.from_numpy(gg.vectors(g.n, 2, 3)).cuda()
+    for reorth in (1, 2):
+        op = wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=[0.5], f=("exp", beta), krylov_dim=3, krylov_tol=1e-12,
+                         reorth=reorth)
+        op.wait()  # operator creation (t) does not report
+        got = op.apply(V).cpu().numpy()
+        with pytest.raises(wl.WalkLapError) as e:
+            op.wait()
+        assert e.value.code == 4
+        op.wait()  # cleared
+        ref = D.laplacian(A, 0.5, C.exp(beta)) @ V.cpu().numpy()
+        assert 1e-12 < relerr(got, ref).max() < 1e-1  # the truncated iterate is written
+        op.close()
+        op = wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=[0.5], f=("exp", beta), krylov_dim=30, krylov_tol=1e-12,
+                         reorth=reorth)
+        op.apply(V)
+        op.wait()
+        op.close()
