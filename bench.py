@@ -503,6 +503,92 @@ def run_cg(args):
         dist.destroy_process_group()
 
 
+def run_diffusion(args):
+    """--diffusion: step a9 on a config with a τ sweep (C3: NBT diffusion exp(-τ𝕃)x0 for 90 τ in [0,100],
+    k_out = 80, x0 = e_center), one full sweep per step.  Each outer Lanczos step is one inner 𝕃 action
+    (k = 30 Krylov on Z), so the rate is reported as inner Laplacian actions/s and sweeps/s."""
+    import torch
+    import torch.distributed as dist
+    import paper_2601_11338_b200 as wl
+
+    world, rank, local = dist_setup(args.gpus)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = configs.get(args.config if args.config != "c4" else "c3")
+    g, t_gen = load_graph(cfg, world, rank, torch, dist)
+    bounds = wl.partition(g.row_ptr, world)
+    rb, re = int(bounds[rank]), int(bounds[rank + 1])
+    rp = g.row_ptr[rb:re + 1]
+    ci = g.col_idx[g.row_ptr[rb]:g.row_ptr[re]]
+    comm = wl.Comm(rank, world, local) if world > 1 else None
+    t0 = time.time()
+    probe = wl.Operator(g.n, rp, ci, thetas=[1.0], f=("series", [0.0, 1.0]), row_range=(rb, re), comm=comm,
+                        krylov_dim=2)
+    rho = probe.spectral_radius(k=args.rho_k)
+    probe.close()
+    op = wl.Operator(g.n, rp, ci, thetas=cfg["thetas"], f=("exp", 1.0 / rho), row_range=(rb, re), comm=comm,
+                     krylov_dim=cfg["krylov_dim"])
+    torch.cuda.synchronize()
+    t_create = time.time() - t0
+    kind, lo, hi, nt = cfg.get("taus", ("linspace", 0.0, 100.0, 90))
+    taus = np.linspace(lo, hi, nt)
+    k_out = cfg.get("k_out", 80)
+    x0 = np.zeros(re - rb)
+    c = g.n // 2
+    if rb <= c < re:
+        x0[c - rb] = 1.0
+    x0 = torch.from_numpy(x0).cuda()
+    out = torch.empty((op.n_local, nt), dtype=torch.float64, device="cuda")
+    ws = op.workspace(1)
+    for _ in range(args.warmup):
+        op.diffuse(x0, taus, k_out=k_out, out=out, ws=ws)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    stream = torch.cuda.current_stream()
+    l0 = wl.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            op.diffuse(x0, taus, k_out=k_out, out=out, ws=ws)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = wl.launch_count() - l0
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    actions = k_out  # inner 𝕃 applications per sweep
+    wl.profile_enable(True)
+    op.diffuse(x0, taus, k_out=k_out, out=out, ws=ws)
+    torch.cuda.synchronize()
+    wl.profile_enable(False)
+    kernels = {k: {"ms_per_step": v[0], "launches_per_step": v[1], "share": v[0] / ms}
+               for k, v in sorted(wl.profile_collect().items(), key=lambda kv: -kv[1][0])}
+    if rank == 0:
+        peak, peak_src = peaks()
+        line = {
+            "metric": METRIC, "value": actions / (ms / 1e3), "unit": "actions/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded graphgen)",
+            "config": {"workload": f"{cfg['desc']}; diffusion exp(-tau L)x0 (step a9), {nt} tau in [{lo}, {hi}], "
+                                   f"k_out={k_out}, inner k={cfg['krylov_dim']}, theta={cfg['thetas']}",
+                       "n": g.n, "nnz": g.nnz, "sweeps_per_s": 1e3 / ms,
+                       "setup_s": {"generate": round(t_gen, 2), "operator_create_incl_t": round(t_create, 2)}},
+            "roofline": None, "kernels": kernels, "cpu_baseline": None, "e2e": None, "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    op.close()
+    if comm:
+        comm.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def run_reference(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -545,6 +631,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--graph", action="store_true", help="also time the step captured as one CUDA graph")
+    ap.add_argument("--diffusion", action="store_true", help="step a9: a full diffusion sweep (default config c3)")
     ap.add_argument("--solver", default="krylov", choices=["krylov", "cg"],
                     help="cg: the paper's 5.3 resolvent workload by PCG on --config's graph")
     args = ap.parse_args()
@@ -554,6 +641,8 @@ def main():
         run_reference(args)
     elif args.solver == "cg":
         run_cg(args)
+    elif args.diffusion:
+        run_diffusion(args)
     else:
         run_walklap(args)
 

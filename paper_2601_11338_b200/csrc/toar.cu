@@ -59,13 +59,14 @@ size_t toar_state_doubles(int K) {
   return (size_t)M * M + 2 * (size_t)(K + 1) * M + 5 * (size_t)M + 8;
 }
 
-// One warp per column c (lanes over coefficient indices).  j = -1: seed step (U = [t0], y = b0);
-// j = 0..K-1: Arnoldi step j; final = 1: only the Gram row of the last U vector and the correction
-// of H column K-1.
+// One CTA (4 warps) per column c, its state staged in shared memory.  j = -1: seed step (U = [t0],
+// y = b0); j = 0..K-1: Arnoldi step j; final = 1: only the Gram row of the last U vector and the
+// correction of H column K-1.
 // sums: the dcgs2_dots layout for Q = U_0..U_{m-2}, p = U_{m-1}, w = y: [a_i b_i]_{i<m-1} α β γ.
 // Outputs: coef_y[o*B + c], coef_u[(o*coef_ld + i)*B + c] for the TOAR update pass:
 //   j = -1: o = 0 -> u_1;   j >= 0: o = 0 -> u_m, 1 -> x_{j+1} = bottom(q̂_{j+1}), 2 -> z_{j+1} = top.
-constexpr int kCoefWarps = 4;
+// Gram-Schmidt in coefficient space is classical (all projections of a pass at once), done twice.
+constexpr int kCoefThreads = 128;
 constexpr int kV = kMaxKrylov + 4;  // coefficient vector capacity (>= K + 3)
 
 __device__ inline double wsum(double v) {
@@ -74,7 +75,7 @@ __device__ inline double wsum(double v) {
 }
 __device__ inline double diag_or_one(double d) { return d != 0.0 ? d : 1.0; }
 
-// x = L^{-1} v (rows < m), x may not alias v
+// x = L^{-1} v (rows < m) by one warp; x may not alias v
 __device__ void fwd_w(const double* L, int M, int m, const double* v, double* x, int lane) {
   for (int i = 0; i < m; ++i) {
     double p = 0.0;
@@ -84,7 +85,7 @@ __device__ void fwd_w(const double* L, int M, int m, const double* v, double* x,
     __syncwarp();
   }
 }
-// x = L^{-T} v (rows < m); rows never measured (column stopped early) act as identity
+// x = L^{-T} v (rows < m) by one warp; rows never measured (column stopped early) act as identity
 __device__ void bwd_w(const double* L, int M, int m, const double* v, double* x, int lane) {
   for (int i = m - 1; i >= 0; --i) {
     double p = 0.0;
@@ -94,218 +95,258 @@ __device__ void bwd_w(const double* L, int M, int m, const double* v, double* x,
     __syncwarp();
   }
 }
-// <(g1,f1),(g2,f2)> over indices < m
-__device__ inline double dot2(const double* g1, const double* f1, const double* g2, const double* f2, int m,
-                              int lane) {
-  double p = 0.0;
-  for (int k = lane; k < m; k += 32) p += g1[k] * g2[k] + f1[k] * f2[k];
-  return wsum(p);
-}
-__device__ inline void axpy2(double s, const double* g, const double* f, double* yg, double* yf, int m, int lane) {
-  for (int k = lane; k < m; k += 32) {
-    yg[k] += s * g[k];
-    yf[k] += s * f[k];
+
+// classical Gram-Schmidt pass of (wg, wf) (length n) against the nb vectors (TG_i, TF_i) (stride M):
+// d_i = <TQ_i, w> for all i (a warp per i, lanes over k), then w -= Σ d_i TQ_i (a thread per k);
+// acc[i] += d_i
+__device__ void cgs_pass(const double* TG, const double* TF, int M, int nb, double* wg, double* wf, int n,
+                         double* dv, double* acc) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = warp; i < nb; i += kCoefThreads / 32) {
+    double p = 0.0;
+    for (int k = lane; k < n; k += 32) p += TG[i * M + k] * wg[k] + TF[i * M + k] * wf[k];
+    p = wsum(p);
+    if (lane == 0) dv[i] = p;
   }
-  __syncwarp();
+  __syncthreads();
+  for (int k = threadIdx.x; k < n; k += kCoefThreads) {
+    double sg = 0.0, sf = 0.0;
+    for (int i = 0; i < nb; ++i) {
+      sg += dv[i] * TG[i * M + k];
+      sf += dv[i] * TF[i * M + k];
+    }
+    wg[k] -= sg;
+    wf[k] -= sf;
+  }
+  for (int i = threadIdx.x; i < nb; i += kCoefThreads) acc[i] += dv[i];
+  __syncthreads();
+}
+__device__ double block_norm2(const double* g, const double* f, int n, double* red) {
+  double p = 0.0;
+  for (int k = threadIdx.x; k < n; k += kCoefThreads) p += g[k] * g[k] + f[k] * f[k];
+  p = wsum(p);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = p;
+  __syncthreads();
+  double s = 0.0;
+  for (int w = 0; w < kCoefThreads / 32; ++w) s += red[w];
+  __syncthreads();
+  return s;
 }
 
-__global__ void __launch_bounds__(32 * kCoefWarps) toar_coeffs_kernel(const double* sums, int j, int final_pass, int B,
-                                                                      int K, double btol, double* H, double* n0,
-                                                                      int* keff, double* state, size_t stride,
-                                                                      double* coef_y, double* coef_u, int coef_ld) {
-  __shared__ double sh[kCoefWarps][8][kV];
-  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int c = blockIdx.x * kCoefWarps + wid;
-  if (c >= B) return;
-  double* Fh = sh[wid][0];
-  double* av = sh[wid][1];
-  double* wg = sh[wid][2];
-  double* wf = sh[wid][3];
-  double* cu = sh[wid][4];
-  double* tmp = sh[wid][5];
-  double* sv = sh[wid][6];
-  double* hv = sh[wid][7];
+__global__ void __launch_bounds__(kCoefThreads) toar_coeffs_kernel(const double* sums, int j, int final_pass, int B,
+                                                                   int K, double btol, double* H, double* n0,
+                                                                   int* keff, double* state, size_t stride,
+                                                                   double* coef_y, double* coef_u, int coef_ld) {
+  extern __shared__ double smem[];
+  const int c = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int M = K + 3;
   State S(state + (size_t)c * stride, M, K);
   double* Hc = H + (size_t)c * (K + 1) * K;  // (row i, col l) at Hc[l*(K+1) + i]
   const int m = final_pass ? K + 2 : (j < 0 ? 1 : j + 2);  // U vectors with a Gram row after this step
   const int nq = m - 1;
+  const int nt = j < 0 ? 0 : (final_pass ? K : j + 1);      // q vectors used this step (q_0..q_j)
+  // shared layout: L (m x M), TQg/TQf (nt x M), QHg/QHf, ZY, work vectors
+  double* L = smem;
+  double* TG = L + (size_t)m * M;
+  double* TF = TG + (size_t)nt * M;
+  double* QG = TF + (size_t)nt * M;
+  double* QF = QG + kV;
+  double* ZY = QF + kV;
+  double* Fh = ZY + kV;
+  double* av = Fh + kV;
+  double* wg = av + kV;
+  double* wf = wg + kV;
+  double* cu = wf + kV;
+  double* t1 = cu + kV;
+  double* t2 = t1 + kV;
+  double* sv = t2 + kV;
+  double* hv = sv + kV;
+  double* dv = hv + kV;
+  double* red = dv + kV;
+  double* Hs = red + kV;  // H columns 0..j (ld K+1), staged
+  __shared__ int alive_s;
   auto sum = [&](int k) { return sums[(size_t)k * B + c]; };
   const int nout = j < 0 ? 1 : 3;
   auto zero_out = [&]() {
     for (int o = 0; o < nout; ++o) {
-      if (lane == 0) coef_y[o * B + c] = 0.0;
-      for (int i = lane; i < m; i += 32) coef_u[((size_t)o * coef_ld + i) * B + c] = 0.0;
+      if (tid == 0) coef_y[o * B + c] = 0.0;
+      for (int i = tid; i < m; i += kCoefThreads) coef_u[((size_t)o * coef_ld + i) * B + c] = 0.0;
     }
   };
   if (j < 0) {  // fresh column state
-    for (int i = lane; i < M * M; i += 32) S.L[i] = 0.0;
-    for (int i = lane; i < M; i += 32) S.DEAD[i] = 0.0;
-    if (lane == 0) S.SC[kAlive] = 1.0;
-    __syncwarp();
+    for (int i = tid; i < M * M; i += kCoefThreads) S.L[i] = 0.0;
+    for (int i = tid; i < M; i += kCoefThreads) S.DEAD[i] = 0.0;
+    if (tid == 0) S.SC[kAlive] = 1.0;
+    __syncthreads();
   }
   if (S.SC[kAlive] == 0.0) {
     if (!final_pass) zero_out();
     return;
   }
-  // 1. Gram row of the newest U vector u_{m-1}: L row m-1 (forward solve); a zero vector gets the
-  //    identity row and is marked dead
-  {
-    double* Lr = S.L + (size_t)(m - 1) * M;
+  // stage the state
+  for (int i = tid; i < (m - 1) * M; i += kCoefThreads) L[i] = S.L[i];
+  for (int i = tid; i < nt * M; i += kCoefThreads) {
+    TG[i] = i < (nt - (final_pass ? 0 : 1)) * M || final_pass ? S.TQg[i] : 0.0;
+    TF[i] = i < (nt - (final_pass ? 0 : 1)) * M || final_pass ? S.TQf[i] : 0.0;
+  }
+  for (int i = tid; i < kV; i += kCoefThreads) {
+    QG[i] = i < M ? S.QHg[i] : 0.0;
+    QF[i] = i < M ? S.QHf[i] : 0.0;
+  }
+  const int hcols = j < 0 ? 0 : (final_pass ? K : j + 1);
+  for (int i = tid; i < hcols * (K + 1); i += kCoefThreads) Hs[i] = Hc[i];
+  __syncthreads();
+  // 1. Gram row of the newest U vector u_{m-1}: L row m-1 (forward solve, warp 0); a zero vector gets
+  //    the identity row and is marked dead
+  double* Lr = L + (size_t)(m - 1) * M;
+  if (warp == 0) {
     for (int i = lane; i < nq; i += 32) sv[i] = sum(2 * i);
     __syncwarp();
-    fwd_w(S.L, M, nq, sv, tmp, lane);
+    fwd_w(L, M, nq, sv, t1, lane);
     double ll = 0.0;
-    for (int i = lane; i < nq; i += 32) ll += tmp[i] * tmp[i];
+    for (int i = lane; i < nq; i += 32) ll += t1[i] * t1[i];
     ll = wsum(ll);
     const double alpha = sum(2 * nq);
     const double d2 = alpha - ll;
     const bool dead = !(alpha > 0.0) || !(d2 > 1e-24 * alpha);
-    for (int i = lane; i < nq; i += 32) Lr[i] = dead ? 0.0 : tmp[i];
-    if (lane == 0) {
-      Lr[nq] = dead ? 1.0 : sqrt(d2);
-      S.DEAD[nq] = dead ? 1.0 : 0.0;
-    }
-    __syncwarp();
+    for (int i = lane; i < M; i += 32) Lr[i] = i < nq ? (dead ? 0.0 : t1[i]) : (i == nq ? (dead ? 1.0 : sqrt(d2)) : 0.0);
+    if (lane == 0) S.DEAD[nq] = dead ? 1.0 : 0.0;
   }
-  const double* Lm = S.L + (size_t)(m - 1) * M;
+  __syncthreads();
+  for (int i = tid; i < M; i += kCoefThreads) S.L[(size_t)(m - 1) * M + i] = Lr[i];
   // 2. provisional vector to true W coordinates: its component e along the assumed w_{m-1} = u_{m-1}
   //    is e u_{m-1} = e Σ_i L[m-1][i] w_i
   if (j >= 0) {
-    const double eg = S.QHg[m - 1], ef = S.QHf[m - 1];
+    const double eg = QG[m - 1], ef = QF[m - 1];
     const bool dead = S.DEAD[m - 1] != 0.0;
-    __syncwarp();
-    for (int i = lane; i < m; i += 32) {
-      const double l = dead ? 0.0 : Lm[i];
+    __syncthreads();
+    for (int i = tid; i < m; i += kCoefThreads) {
+      const double l = dead ? 0.0 : Lr[i];
       if (i < m - 1) {
-        S.QHg[i] += eg * l;
-        S.QHf[i] += ef * l;
+        QG[i] += eg * l;
+        QF[i] += ef * l;
       } else {
-        S.QHg[i] = eg * l;
-        S.QHf[i] = ef * l;
+        QG[i] = eg * l;
+        QF[i] = ef * l;
       }
     }
-    __syncwarp();
-    for (int i = lane; i < m; i += 32) Fh[i] = S.QHf[i];
-    __syncwarp();
+    __syncthreads();
+    for (int i = tid; i < m; i += kCoefThreads) Fh[i] = QF[i];
   }
   // 3. y in W coordinates: z = L^{-1} s, ν_y² = γ - |z|²;  y = W z + ν_y u_m  (u_m := (y - U c)/ν_y)
   double nuy = 0.0;
   if (!final_pass) {
-    for (int i = lane; i < m; i += 32) sv[i] = i < nq ? sum(2 * i + 1) : sum(2 * nq + 1);
-    __syncwarp();
-    fwd_w(S.L, M, m, sv, S.ZY, lane);
+    if (warp == 0) {
+      for (int i = lane; i < m; i += 32) sv[i] = i < nq ? sum(2 * i + 1) : sum(2 * nq + 1);
+      __syncwarp();
+      fwd_w(L, M, m, sv, ZY, lane);
+    }
+    __syncthreads();
     double zz = 0.0;
-    for (int i = lane; i < m; i += 32) zz += S.ZY[i] * S.ZY[i];
+    for (int i = lane; i < m; i += 32) zz += ZY[i] * ZY[i];
     zz = wsum(zz);
     const double gamma = sum(2 * nq + 2);
     nuy = sqrt(fmax(gamma - zz, 0.0));
     if (!(nuy > 1e-12 * sqrt(gamma))) nuy = 0.0;  // y in span(U): no new direction
   }
   if (j < 0) {  // seed: q̂_0 = [t0; b0] = [L00 w_0; W z + ν_y u_1]
-    for (int i = lane; i < M; i += 32) {
-      S.QHg[i] = i == 0 ? (S.DEAD[0] != 0.0 ? 0.0 : S.L[0]) : 0.0;
-      S.QHf[i] = i == 0 ? S.ZY[0] : (i == 1 ? nuy : 0.0);
+    for (int i = tid; i < M; i += kCoefThreads) {
+      S.QHg[i] = i == 0 ? (S.DEAD[0] != 0.0 ? 0.0 : L[0]) : 0.0;
+      S.QHf[i] = i == 0 ? ZY[0] : (i == 1 ? nuy : 0.0);
     }
-    __syncwarp();
-    bwd_w(S.L, M, m, S.ZY, cu, lane);  // u_1 = (b0 - U c)/ν_y, c = L^{-T} z
+    if (warp == 0) bwd_w(L, M, m, ZY, cu, lane);  // u_1 = (b0 - U c)/ν_y, c = L^{-T} z
+    __syncthreads();
     const double inv = nuy > 0.0 ? 1.0 / nuy : 0.0;
-    if (lane == 0) coef_y[c] = inv;
-    for (int i = lane; i < m; i += 32) coef_u[(size_t)i * B + c] = -cu[i] * inv;
+    if (tid == 0) coef_y[c] = inv;
+    for (int i = tid; i < m; i += kCoefThreads) coef_u[(size_t)i * B + c] = -cu[i] * inv;
     return;
   }
-  // 4. re-orthonormalise q̂_j against q_0..q_{j-1} (twice), completing H column j-1
-  for (int i = lane; i < j; i += 32) av[i] = 0.0;
-  __syncwarp();
-  for (int pass = 0; pass < 2; ++pass)
-    for (int i = 0; i < j; ++i) {
-      const double* tg = S.TQg + (size_t)i * M;
-      const double* tf = S.TQf + (size_t)i * M;
-      const double dd = dot2(tg, tf, S.QHg, S.QHf, m, lane);
-      axpy2(-dd, tg, tf, S.QHg, S.QHf, m, lane);
-      if (lane == 0) av[i] += dd;
+  // 4. re-orthonormalise q̂_j against q_0..q_{j-1} (classical, twice), completing H column j-1
+  for (int i = tid; i < kV; i += kCoefThreads) av[i] = 0.0;
+  __syncthreads();
+  cgs_pass(TG, TF, M, j, QG, QF, m, dv, av);
+  cgs_pass(TG, TF, M, j, QG, QF, m, dv, av);
+  const double nuq = sqrt(block_norm2(QG, QF, m, red));
+  if (j > 0) {  // H column j-1 += hprov a, H(j, j-1) = hprov ν
+    const double hp = S.SC[kHprov];
+    for (int i = tid; i < j; i += kCoefThreads) {
+      const double v = Hs[(j - 1) * (K + 1) + i] + hp * av[i];
+      Hs[(j - 1) * (K + 1) + i] = v;
+      Hc[(j - 1) * (K + 1) + i] = v;
     }
-  __syncwarp();
-  const double nuq = sqrt(dot2(S.QHg, S.QHf, S.QHg, S.QHf, m, lane));
-  if (j == 0) {
-    if (lane == 0) {
+  }
+  if (tid == 0) {
+    if (j == 0) {
       n0[c] = nuq;
       keff[c] = nuq > 0.0 ? K : 0;
       S.SC[kRef] = nuq;
-      if (!(nuq > 0.0)) S.SC[kAlive] = 0.0;
-    }
-  } else if (lane == 0) {
-    const double hp = S.SC[kHprov];
-    for (int i = 0; i < j; ++i) Hc[(j - 1) * (K + 1) + i] += hp * av[i];
-    const double sub = hp * nuq;
-    if (sub > btol * S.SC[kRef] && sub > 0.0) {
-      Hc[(j - 1) * (K + 1) + j] = sub;
+      alive_s = nuq > 0.0;
     } else {
-      Hc[(j - 1) * (K + 1) + j] = 0.0;
-      keff[c] = j;
-      S.SC[kAlive] = 0.0;
+      const double sub = S.SC[kHprov] * nuq;
+      alive_s = sub > btol * S.SC[kRef] && sub > 0.0;
+      Hs[(j - 1) * (K + 1) + j] = alive_s ? sub : 0.0;
+      Hc[(j - 1) * (K + 1) + j] = alive_s ? sub : 0.0;
+      if (!alive_s) keff[c] = j;
     }
+    if (!alive_s) S.SC[kAlive] = 0.0;
   }
-  __syncwarp();
+  __syncthreads();
   if (final_pass) return;
-  if (S.SC[kAlive] == 0.0) {
+  if (!alive_s) {
     zero_out();
     return;
   }
   {  // q_j
-    double* tg = S.TQg + (size_t)j * M;
-    double* tf = S.TQf + (size_t)j * M;
     const double inv = 1.0 / nuq;
-    for (int k = lane; k < M; k += 32) {
-      tg[k] = k < m ? S.QHg[k] * inv : 0.0;
-      tf[k] = k < m ? S.QHf[k] * inv : 0.0;
+    for (int k = tid; k < M; k += kCoefThreads) {
+      const double g = k < m ? QG[k] * inv : 0.0, f = k < m ? QF[k] * inv : 0.0;
+      TG[(size_t)j * M + k] = g;
+      TF[(size_t)j * M + k] = f;
+      S.TQg[(size_t)j * M + k] = g;
+      S.TQf[(size_t)j * M + k] = f;
     }
-    __syncwarp();
   }
   // 5. Z q_j = (Z q̂_j - Σ_{i<j} a_i Z q_i)/ν,  Z q̂_j = [f̂ ; W z + ν_y u_m],  Σ_i a_i Z q_i = Σ_l (H a)_l q_l
   const int m1 = m + 1;
-  for (int k = lane; k < m1; k += 32) {
+  for (int k = tid; k < m1; k += kCoefThreads) {
     wg[k] = k < m ? Fh[k] : 0.0;
-    wf[k] = k < m ? S.ZY[k] : nuy;
+    wf[k] = k < m ? ZY[k] : nuy;
   }
-  for (int l = lane; l <= j; l += 32) {
+  for (int l = tid; l <= j; l += kCoefThreads) {
     double s = 0.0;
-    for (int i = (l > 0 ? l - 1 : 0); i < j; ++i) s += Hc[i * (K + 1) + l] * av[i];
+    for (int i = (l > 0 ? l - 1 : 0); i < j; ++i) s += Hs[i * (K + 1) + l] * av[i];
     hv[l] = s;
   }
-  __syncwarp();
-  for (int l = 0; l <= j; ++l)
-    if (hv[l] != 0.0) axpy2(-hv[l], S.TQg + (size_t)l * M, S.TQf + (size_t)l * M, wg, wf, m, lane);
-  {
-    const double inv = 1.0 / nuq;
-    for (int k = lane; k < m1; k += 32) {
-      wg[k] *= inv;
-      wf[k] *= inv;
+  __syncthreads();
+  for (int k = tid; k < m; k += kCoefThreads) {
+    double sg = 0.0, sf = 0.0;
+    for (int l = 0; l <= j; ++l) {
+      sg += hv[l] * TG[(size_t)l * M + k];
+      sf += hv[l] * TF[(size_t)l * M + k];
     }
-    __syncwarp();
+    wg[k] = (wg[k] - sg) / nuq;
+    wf[k] = (wf[k] - sf) / nuq;
   }
-  const double ref = sqrt(dot2(wg, wf, wg, wf, m1, lane));
-  // 6. Arnoldi: h = Q^T Z q_j (twice), provisional q̂_{j+1}
-  for (int i = lane; i <= j; i += 32) hv[i] = 0.0;
-  __syncwarp();
-  for (int pass = 0; pass < 2; ++pass)
-    for (int i = 0; i <= j; ++i) {
-      const double* tg = S.TQg + (size_t)i * M;
-      const double* tf = S.TQf + (size_t)i * M;
-      const double dd = dot2(tg, tf, wg, wf, m, lane);
-      axpy2(-dd, tg, tf, wg, wf, m, lane);
-      if (lane == 0) hv[i] += dd;
-    }
-  __syncwarp();
-  const double hs = sqrt(dot2(wg, wf, wg, wf, m1, lane));
-  for (int i = lane; i <= j; i += 32) Hc[j * (K + 1) + i] = hv[i];
-  if (lane == 0) {
+  if (tid == 0) {
+    wg[m] /= nuq;
+    wf[m] /= nuq;
+  }
+  __syncthreads();
+  const double ref = sqrt(block_norm2(wg, wf, m1, red));
+  // 6. Arnoldi: h = Q^T Z q_j (classical, twice), provisional q̂_{j+1}
+  for (int i = tid; i < kV; i += kCoefThreads) hv[i] = 0.0;
+  __syncthreads();
+  cgs_pass(TG, TF, M, j + 1, wg, wf, m, dv, hv);
+  cgs_pass(TG, TF, M, j + 1, wg, wf, m, dv, hv);
+  const double hs = sqrt(block_norm2(wg, wf, m1, red));
+  for (int i = tid; i <= j; i += kCoefThreads) Hc[j * (K + 1) + i] = hv[i];
+  if (tid == 0) {
     S.SC[kHprov] = hs;
     S.SC[kRef] = ref;
   }
-  __syncwarp();
   if (!(hs > btol * ref)) {  // invariant Krylov subspace: column j is final, H(j+1, j) = 0
-    if (lane == 0) {
+    if (tid == 0) {
       keff[c] = j + 1;
       S.SC[kAlive] = 0.0;
     }
@@ -314,25 +355,32 @@ __global__ void __launch_bounds__(32 * kCoefWarps) toar_coeffs_kernel(const doub
   }
   {
     const double inv = 1.0 / hs;
-    for (int k = lane; k < M; k += 32) {
-      S.QHg[k] = k < m1 ? wg[k] * inv : 0.0;
-      S.QHf[k] = k < m1 ? wf[k] * inv : 0.0;
+    for (int k = tid; k < M; k += kCoefThreads) {
+      const double g = k < m1 ? wg[k] * inv : 0.0, f = k < m1 ? wf[k] * inv : 0.0;
+      QG[k] = g;
+      QF[k] = f;
+      S.QHg[k] = g;
+      S.QHf[k] = f;
     }
-    __syncwarp();
   }
+  __syncthreads();
   // 7. update-pass coefficients: u_m = (y - U c)/ν_y;  v in W coords over [W_m, u_m]:
-  //    W v = U L^{-T} v[0:m] + v[m] (y - U c)/ν_y
-  bwd_w(S.L, M, m, S.ZY, cu, lane);
+  //    W v = U L^{-T} v[0:m] + v[m] (y - U c)/ν_y      (three back-solves on three warps)
+  if (warp == 0) bwd_w(L, M, m, ZY, cu, lane);
+  else if (warp == 1) bwd_w(L, M, m, QF, t1, lane);
+  else if (warp == 2) bwd_w(L, M, m, QG, t2, lane);
+  __syncthreads();
   const double iy = nuy > 0.0 ? 1.0 / nuy : 0.0;
-  if (lane == 0) coef_y[c] = iy;
-  for (int i = lane; i < m; i += 32) coef_u[(size_t)i * B + c] = -cu[i] * iy;
-  for (int o = 1; o < 3; ++o) {
-    const double* v = o == 1 ? S.QHf : S.QHg;
-    bwd_w(S.L, M, m, v, tmp, lane);
-    const double vm = v[m] * iy;
-    if (lane == 0) coef_y[o * B + c] = vm;
-    for (int i = lane; i < m; i += 32) coef_u[((size_t)o * coef_ld + i) * B + c] = tmp[i] - vm * cu[i];
-    __syncwarp();
+  const double vm1 = QF[m] * iy, vm2 = QG[m] * iy;
+  if (tid == 0) {
+    coef_y[c] = iy;
+    coef_y[B + c] = vm1;
+    coef_y[2 * B + c] = vm2;
+  }
+  for (int i = tid; i < m; i += kCoefThreads) {
+    coef_u[(size_t)i * B + c] = -cu[i] * iy;
+    coef_u[((size_t)coef_ld + i) * B + c] = t1[i] - vm1 * cu[i];
+    coef_u[((size_t)2 * coef_ld + i) * B + c] = t2[i] - vm2 * cu[i];
   }
 }
 
@@ -360,8 +408,19 @@ void toar_coeffs(const double* sums, int j, int final_pass, int B, int K, double
                  int* keff, double* state, size_t stride, double* coef_y, double* coef_u, int coef_ld,
                  cudaStream_t s) {
   WL_LAUNCH("toar_coeffs");
-  toar_coeffs_kernel<<<(B + kCoefWarps - 1) / kCoefWarps, 32 * kCoefWarps, 0, s>>>(
-      sums, j, final_pass, B, K, btol, H, n0, keff, state, stride, coef_y, coef_u, coef_ld);
+  const int M = K + 3;
+  const size_t smem = sizeof(double) * ((size_t)(K + 2) * M + 2 * (size_t)(K + 1) * M + 16 * (size_t)kV +
+                                       (size_t)(K + 1) * K);
+  static bool attr = false;
+  if (!attr) {
+    const size_t smax = sizeof(double) * ((size_t)(kMaxKrylov + 2) * (kMaxKrylov + 3) +
+                                          2 * (size_t)(kMaxKrylov + 1) * (kMaxKrylov + 3) + 16 * (size_t)kV +
+                                          (size_t)(kMaxKrylov + 1) * kMaxKrylov);
+    WL_CUDA(cudaFuncSetAttribute(toar_coeffs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
+    attr = true;
+  }
+  toar_coeffs_kernel<<<B, kCoefThreads, smem, s>>>(sums, j, final_pass, B, K, btol, H, n0, keff, state, stride,
+                                                  coef_y, coef_u, coef_ld);
   WL_CUDA(cudaGetLastError());
 }
 
