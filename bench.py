@@ -589,6 +589,58 @@ def run_diffusion(args):
         dist.destroy_process_group()
 
 
+def run_extra(args):
+    """--markov / --rhoz: measurement lines for NEXT-3 (one step = nsteps Markov steps p_{k+1} = p_k P on the
+    config's graph at θ = 0.5, each one φ action of k = 30) and NEXT-4 (one step = ρ(Z_1) by 60 Arnoldi steps on
+    the 2n companion operator).  1 GPU."""
+    import torch
+    import paper_2601_11338_b200 as wl
+
+    cfg = configs.get(args.config)
+    t0 = time.time()
+    g = cfg["make"]()
+    t_gen = time.time() - t0
+    probe = wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=[1.0], f=("series", [0.0, 1.0]), krylov_dim=2)
+    rho = probe.spectral_radius(k=args.rho_k)
+    probe.close()
+    stream = torch.cuda.current_stream()
+    if args.markov:
+        op = wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=[0.5], f=("exp", 1.0 / rho), krylov_dim=30)
+        p0 = torch.from_numpy(np.abs(gg.vectors(g.n, 1, 7)[:, 0])).cuda()
+        p0 /= p0.sum()
+        nsteps = 4
+        out = torch.empty((g.n, nsteps), dtype=torch.float64, device="cuda")
+        ws = op.workspace(1)
+        fn = lambda: op.markov(p0, nsteps, out=out, ws=ws)  # noqa: E731
+        unit, per_step, what = "markov steps/s", nsteps, f"{nsteps} Markov steps at theta=0.5 (eq:let_there_be_markov)"
+    else:
+        op = wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=[0.0], f=("series", [0.0, 1.0]), krylov_dim=2)
+        fn = lambda: op.spectral_radius_z(0, k=60)  # noqa: E731
+        unit, per_step, what = "estimates/s", 1, "rho(Z_1) by 60 Arnoldi steps on the companion operator"
+    for _ in range(args.warmup):
+        fn()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = wl.launch_count()
+    with ClockSampler(0) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            fn()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    line = {"metric": what, "value": per_step / (ms / 1e3), "unit": unit, "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded graphgen)",
+            "config": {"workload": f"{args.config}: {cfg['desc']}", "n": g.n, "nnz": g.nnz, "rho_A": rho,
+                       "setup_s": {"generate": round(t_gen, 2)}},
+            "gpu_launches": wl.launch_count() - l0, "clocks": clk.summary()}
+    if not args.markov:
+        line["config"]["rho_Z1"] = op.spectral_radius_z(0, k=60)
+    print(json.dumps(line), flush=True)
+    op.close()
+
+
 def run_reference(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -632,6 +684,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--graph", action="store_true", help="also time the step captured as one CUDA graph")
     ap.add_argument("--diffusion", action="store_true", help="step a9: a full diffusion sweep (default config c3)")
+    ap.add_argument("--markov", action="store_true", help="NEXT-3: Markov chain steps")
+    ap.add_argument("--rhoz", action="store_true", help="NEXT-4: rho(Z_1) by Arnoldi on the companion operator")
     ap.add_argument("--solver", default="krylov", choices=["krylov", "cg"],
                     help="cg: the paper's 5.3 resolvent workload by PCG on --config's graph")
     args = ap.parse_args()
@@ -643,6 +697,8 @@ def main():
         run_cg(args)
     elif args.diffusion:
         run_diffusion(args)
+    elif args.markov or args.rhoz:
+        run_extra(args)
     else:
         run_walklap(args)
 
