@@ -135,8 +135,13 @@ def algorithmic_bytes(n, nnz, n_halo, G, K, Bmax, b, n_theta, reorth=2):
         vec = 8 * L * B
         blk = 8 * n * B
         csr = 4 * nnz + 4 * (n + 1)
-        add("spmv_binned", (csr + 2 * blk + 8 * n_halo * B))          # seed 1: gather y + write
-        add("spmv_binned", (csr + 3 * blk + 8 * n_halo * B))          # seed 2: + x
+        if reorth == 2 and b < B and g0 % b == 0 and B % b == 0:
+            bb = 8 * n * b                                              # θ-independent seeds over b columns
+            add("spmv_binned", 2 * (csr + 2 * bb + 8 * n_halo * b))    # A v, A(Av)
+            add("batch_inputs", 3 * bb + 2 * blk)                      # expand to the B columns
+        else:
+            add("spmv_binned", (csr + 2 * blk + 8 * n_halo * B))      # seed 1: gather y + write
+            add("spmv_binned", (csr + 3 * blk + 8 * n_halo * B))      # seed 2: + x
         add("spmv_binned", K * (csr + 3 * blk + 8 * n_halo * B))      # Z steps
         if reorth == 2:
             # TOAR: n-vector basis U (m = j+2 vectors at step j).  dots: Gram row of the newest U

@@ -178,6 +178,8 @@ struct wl_workspace {
   int64_t cg_iterations = 0;     // executed CG iterations (max over the columns of each solve), cumulative
   DArr<double> mk_p, mk_v;       // Markov chain: current distribution and p / t (internal order)
   DArr<double> kerr;             // a-posteriori Krylov error estimates per column (opts.tol > 0)
+  DArr<double> seed;             // TOAR shared seeds: v, A v, A(Av) over the b input columns
+  DArr<int> vid;                 // 0, 1, ..., kMaxCols-1
   DArr<double> toar_state, toar_cy, toar_cu, toar_comb;  // TOAR (toar.cu): per-column state, update coefficients
   // host-buffer entry point
   DArr<double> hV, hLV;
@@ -400,7 +402,6 @@ void toar_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double*
   double* g0s = g1z + kMaxCols;
   double* g1s = g0s + kMaxCols;
   setup_chunk(op->mu_dev.p, gstart, b, B, g0z, g1z, g0s, g1s, ws->vcol.p, ws->tcol.p, s);
-  batch_inputs(V, ldv, B, n, ws->Vb.p, ws->vcol.p, perm, s);
   VecPtrs U{};
   for (int i = 0; i < K + 2; ++i) U.p[i] = ws->basis.p + (int64_t)i * vs;
   double* xb = ws->basis.p + (int64_t)(K + 2) * vs;
@@ -408,10 +409,24 @@ void toar_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double*
   double* yb = zb + vs;
   double* U0 = const_cast<double*>(U.p[0]);
   // a3 seeds: t0 = A v -> U_0, b0 = A t0 - μ d⊙v -> x   (eq:qrec seeds); q̂_0 = [t0; b0]
-  halo_exchange(op, ws, ws->Vb.p, B, B, s);
-  do_spmv(op, ws, ws->Vb.p, nullptr, nullptr, nullptr, nullptr, U0, B, s);
-  halo_exchange(op, ws, U0, B, B, s);
-  do_spmv(op, ws, U0, ws->Vb.p, g0s, g1s, nullptr, xb, B, s);
+  if (b < B && gstart % b == 0 && B % b == 0) {
+    // A v and A(Av) do not depend on θ: two SpMMs over the b input columns, expanded to the B columns
+    double* vs_ = ws->seed.p;
+    double* s1 = vs_ + (n + 1) * b;
+    double* s2 = s1 + (n + 1) * b;
+    batch_inputs(V, ldv, b, n, vs_, ws->vid.p, perm, s);
+    halo_exchange(op, ws, vs_, b, b, s);
+    do_spmv(op, ws, vs_, nullptr, nullptr, nullptr, nullptr, s1, b, s);
+    halo_exchange(op, ws, s1, b, b, s);
+    do_spmv(op, ws, s1, nullptr, nullptr, nullptr, nullptr, s2, b, s);
+    seed_expand(s1, s2, vs_, b, op->rowptr.p, g1s, ws->vcol.p, B, n, U0, xb, s);
+  } else {
+    batch_inputs(V, ldv, B, n, ws->Vb.p, ws->vcol.p, perm, s);
+    halo_exchange(op, ws, ws->Vb.p, B, B, s);
+    do_spmv(op, ws, ws->Vb.p, nullptr, nullptr, nullptr, nullptr, U0, B, s);
+    halo_exchange(op, ws, U0, B, B, s);
+    do_spmv(op, ws, U0, ws->Vb.p, g0s, g1s, nullptr, xb, B, s);
+  }
   if (n_pad > n) {
     fill(U0 + n * B, B, 0.0, s);
     fill(xb + n * B, B, 0.0, s);
@@ -627,6 +642,11 @@ void workspace_alloc(wl_workspace* ws, const wl_operator* op, int max_b) {
     ws->toar_cy.alloc((size_t)3 * B);
     ws->toar_cu.alloc((size_t)3 * (K + 3) * B);
     ws->toar_comb.alloc((size_t)(K + 2) * B);
+    ws->seed.alloc((size_t)3 * (n + 1) * std::max(1, std::min(max_b, kMaxCols)));
+    std::vector<int> id(kMaxCols);
+    std::iota(id.begin(), id.end(), 0);
+    ws->vid.alloc(kMaxCols);
+    WL_CUDA(cudaMemcpy(ws->vid.p, id.data(), sizeof(int) * kMaxCols, cudaMemcpyHostToDevice));
   }
   if (!ws->cg_flags_host) WL_CUDA(cudaMallocHost(&ws->cg_flags_host, (2 + kMaxCols) * sizeof(int)));
   spmv_scratch(op, ws, B);

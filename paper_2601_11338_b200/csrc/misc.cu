@@ -19,6 +19,23 @@ __global__ void batch_inputs_kernel(const double* V, int64_t ldv, int B, int64_t
   }
 }
 
+// Seeds shared by the θ columns of one input column (TOAR path): s1 = A v and s2 = A(Av) are
+// θ-independent, so they are computed once per input column (n x b) and expanded to the B Krylov
+// columns: t0[r][c] = s1[r][vcol c],  b0[r][c] = s2[r][vcol c] - μ_c d_r v[r][vcol c]  (eq:qrec seeds).
+__global__ void seed_expand_kernel(const double* s1, const double* s2, const double* v, int b, const int32_t* rowptr,
+                                   const double* g1s, const int* vcol, int B, int64_t n, double* t0, double* b0) {
+  const int64_t total = n * B;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / B;
+    const int c = (int)(e - r * B);
+    const int64_t src = r * b + vcol[c];
+    const double d = (double)(__ldg(rowptr + r + 1) - __ldg(rowptr + r));
+    t0[e] = s1[src];
+    b0[e] = s2[src] + g1s[c] * d * v[src];  // g1s = -μ
+  }
+}
+
 // n0 = ||u||, s0 = 1/n0 (0 if u == 0: φv = c_0 v exactly), keff = K (0 if u == 0)
 __global__ void finalize_norm0_kernel(const double* sums, int B, double* n0, double* s0, int* keff,
                                       int K) {
@@ -281,6 +298,13 @@ void batch_inputs(const double* V, int64_t ldv, int B, int64_t n, double* Vb, co
                   const int32_t* perm, cudaStream_t s) {
   WL_LAUNCH("batch_inputs");
   batch_inputs_kernel<<<grid_for(n * B), 256, 0, s>>>(V, ldv, B, n, Vb, vcol, perm);
+  WL_CUDA(cudaGetLastError());
+}
+
+void seed_expand(const double* s1, const double* s2, const double* v, int b, const int32_t* rowptr, const double* g1s,
+                 const int* vcol, int B, int64_t n, double* t0, double* b0, cudaStream_t s) {
+  WL_LAUNCH("batch_inputs");
+  seed_expand_kernel<<<grid_for(n * B), 256, 0, s>>>(s1, s2, v, b, rowptr, g1s, vcol, B, n, t0, b0);
   WL_CUDA(cudaGetLastError());
 }
 

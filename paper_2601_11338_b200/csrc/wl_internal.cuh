@@ -178,6 +178,8 @@ void small_f(const SmallFArgs& a, cudaStream_t s);
 // Vb[r*B + j] = V[r*ldv + vcol[j]]   (j < B); V null => ones
 void batch_inputs(const double* V, int64_t ldv, int B, int64_t n, double* Vb, const int* vcol,
                   const int32_t* perm, cudaStream_t s);
+void seed_expand(const double* s1, const double* s2, const double* v, int b, const int32_t* rowptr, const double* g1s,
+                 const int* vcol, int B, int64_t n, double* t0, double* b0, cudaStream_t s);
 void setup_chunk(const double* mu, int gstart, int b, int B, double* g0z, double* g1z, double* g0s,
                  double* g1s, int* vcol, int* tcol, cudaStream_t s);
 // Arnoldi bookkeeping after a reduction: see engine.cu for the exact semantics.
