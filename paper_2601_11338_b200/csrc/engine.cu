@@ -775,7 +775,7 @@ void build_operator(wl_operator* op, const int64_t* rp_in, const int32_t* ci_in,
     for (int64_t r = 0; r < n; ++r) {
       const int32_t d = rp[r + 1] - rp[r];
       if (d <= kSmallMax) sm.push_back((int32_t)r);
-      else if (d <= kHubChunk) md.push_back((int32_t)r);
+      else if (d <= kMediumMax) md.push_back((int32_t)r);
       else {
         const int first = (int)ch.size();
         for (int32_t z = rp[r]; z < rp[r + 1]; z += kHubChunk)

@@ -11,9 +11,9 @@
 //   small rows  (deg <= 32, incl. isolated rows): one lane group (B lanes, lane c = column c of the
 //               row-major n x B blocks) per row, rows in id order so neighbouring groups read
 //               neighbouring col_idx ranges;
-//   medium rows (32 < deg <= 1024): one warp per row, its lane groups split the nonzeros and are
+//   medium rows (32 < deg <= 2048): one warp per row, its lane groups split the nonzeros and are
 //               reduced with shuffles;
-//   hub rows    (deg > 1024): split into 1024-nonzero chunks, one warp per chunk; each chunk writes
+//   hub rows    (deg > 2048): split into 2048-nonzero chunks, one warp per chunk; each chunk writes
 //               a partial and the last chunk to finish (per-row ticket) sums the row's partials in
 //               chunk order — deterministic, no second launch.
 // Every lane issues up to 8 independent gathers before consuming them (ILP), and all control flow
@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(kThreads) spmv_binned_kernel(SpmvArgs a) {
     return;
   }
   blk -= a.nblk_medium;
-  {  // ---- hub rows: one warp per 1024-nonzero chunk, last chunk of the row reduces in order
+  {  // ---- hub rows: one warp per kHubChunk-nonzero chunk, last chunk of the row reduces in order
     const int idx = blk * kWarps + warp;
     if (idx >= a.n_chunks) return;
     const int4 ch = a.chunks[idx];  // (row, z0, z1, first chunk index of the row)

@@ -33,8 +33,18 @@ constexpr int kMaxSmallN = 130; // largest dense matrix of the projected-functio
 // ---------------------------------------------------------------- degree-binned Z-SpMV
 // out[r][c] = scale[c] * ( Σ_{z in row r} y[col[z]][c] + (g0[c] + g1[c] * deg(r)) * x[r][c] )
 // Gathers y rows (ld ldy) for local columns < n_loc, halo rows (ld ldh) for columns >= n_loc.
-constexpr int kSmallMax = 32;    // rows with deg <= 32: one lane group per row
-constexpr int kHubChunk = 1024;  // rows with deg > 1024: split into chunks of 1024 nonzeros
+#ifndef WL_SMALL_MAX
+#define WL_SMALL_MAX 32
+#endif
+#ifndef WL_HUB_CHUNK
+#define WL_HUB_CHUNK 2048
+#endif
+#ifndef WL_MEDIUM_MAX
+#define WL_MEDIUM_MAX WL_HUB_CHUNK
+#endif
+constexpr int kSmallMax = WL_SMALL_MAX;    // rows with deg <= 32: lane group per row (batched, 32 rows a warp)
+constexpr int kMediumMax = WL_MEDIUM_MAX;  // rows with deg <= kMediumMax: one warp per row
+constexpr int kHubChunk = WL_HUB_CHUNK;    // longer rows: split into chunks of kHubChunk nonzeros
 struct SpmvArgs {
   const int32_t* rowptr;  // n_loc + 1, local offsets
   const int32_t* col;     // nnz, local ids (halo ids >= n_loc)

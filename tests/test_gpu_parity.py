@@ -441,3 +441,28 @@ def test_aposteriori_krylov_check(wl):
         op.apply(V)
         op.wait()
         op.close()
+
+
+def test_hub_rows_split_into_chunks(wl):
+    """Rows longer than the hub chunk (2048 nonzeros) are split across warps and reduced in chunk order by
+    the last chunk to finish; several hubs of different lengths plus medium and small rows, vs the series."""
+    rng = np.random.default_rng(5)
+    n = 9000
+    edges = set()
+    for hub, deg in ((0, 5000), (1, 2049), (2, 4097), (3, 2048), (4, 700)):
+        for v in rng.choice(np.arange(5, n), size=deg, replace=False):
+            edges.add((min(hub, int(v)), max(hub, int(v))))
+    for _ in range(20000):
+        a, b = rng.integers(5, n, size=2)
+        if a != b:
+            edges.add((min(a, b), max(a, b)))
+    g = gg.from_edges(n, sorted(edges), "hubs")
+    assert np.diff(g.row_ptr).max() >= 5000
+    rA = S.rho_A(g)
+    f = C.exp(1.0 / rA)
+    V = gg.vectors(g.n, 3, 8)
+    for th in (0.0, 0.6):
+        op = wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=[th], f=("exp", f.param))
+        got = op.apply(torch.from_numpy(V).cuda()).cpu().numpy()
+        assert relerr(got, S.laplacian_apply(g, 1.0 - th, f, V, rA)).max() < TOL
+        op.close()
