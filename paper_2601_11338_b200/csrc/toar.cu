@@ -28,7 +28,7 @@ namespace {
 // per-column state: L (M x M, row-major lower), TQg/TQf ((K+1) x M: W coords of q_i), QHg/QHf (M:
 // the provisional next vector), ZY (M: W coords of y), DEAD (M), SC (8 scalars)
 struct State {
-  double *L, *TQg, *TQf, *QHg, *QHf, *ZY, *DEAD, *SC;
+  double *L, *TQg, *TQf, *QHg, *QHf, *ZY, *DEAD, *SC, *LI;
   __device__ State(double* base, int M, int K) {
     L = base;
     TQg = L + M * M;
@@ -38,6 +38,7 @@ struct State {
     ZY = QHf + M;
     DEAD = ZY + M;
     SC = DEAD + M;
+    LI = SC + 8;  // L^{-1}, maintained row by row (M x M, row-major lower)
   }
 };
 enum { kHprov = 0, kAlive = 1, kNuY = 2, kRef = 3 };
@@ -56,7 +57,7 @@ __device__ void solve_lt(const double* L, int M, int m, const double* v, double*
 
 size_t toar_state_doubles(int K) {
   const int M = K + 3;
-  return (size_t)M * M + 2 * (size_t)(K + 1) * M + 5 * (size_t)M + 8;
+  return 2 * (size_t)M * M + 2 * (size_t)(K + 1) * M + 5 * (size_t)M + 8;
 }
 
 // One CTA (4 warps) per column c, its state staged in shared memory.  j = -1: seed step (U = [t0],
@@ -75,24 +76,20 @@ __device__ inline double wsum(double v) {
 }
 __device__ inline double diag_or_one(double d) { return d != 0.0 ? d : 1.0; }
 
-// x = L^{-1} v (rows < m) by one warp; x may not alias v
-__device__ void fwd_w(const double* L, int M, int m, const double* v, double* x, int lane) {
-  for (int i = 0; i < m; ++i) {
-    double p = 0.0;
-    for (int k = lane; k < i; k += 32) p += L[i * M + k] * x[k];
-    p = wsum(p);
-    if (lane == 0) x[i] = (v[i] - p) / diag_or_one(L[i * M + i]);
-    __syncwarp();
+// x = LI v (LI lower triangular, rows < m), a thread per row; caller syncs
+__device__ void li_mv(const double* LI, int M, int m, const double* v, double* x) {
+  for (int i = threadIdx.x; i < m; i += kCoefThreads) {
+    double s = 0.0;
+    for (int k = 0; k <= i; ++k) s += LI[i * M + k] * v[k];
+    x[i] = s;
   }
 }
-// x = L^{-T} v (rows < m) by one warp; rows never measured (column stopped early) act as identity
-__device__ void bwd_w(const double* L, int M, int m, const double* v, double* x, int lane) {
-  for (int i = m - 1; i >= 0; --i) {
-    double p = 0.0;
-    for (int k = i + 1 + lane; k < m; k += 32) p += L[k * M + i] * x[k];
-    p = wsum(p);
-    if (lane == 0) x[i] = (v[i] - p) / diag_or_one(L[i * M + i]);
-    __syncwarp();
+// x = LI^T v (rows < m), a thread per entry; caller syncs
+__device__ void li_tmv(const double* LI, int M, int m, const double* v, double* x) {
+  for (int k = threadIdx.x; k < m; k += kCoefThreads) {
+    double s = 0.0;
+    for (int i = k; i < m; ++i) s += LI[i * M + k] * v[i];
+    x[k] = s;
   }
 }
 
@@ -165,6 +162,7 @@ __global__ void __launch_bounds__(kCoefThreads) toar_coeffs_kernel(const double*
   double* dv = hv + kV;
   double* red = dv + kV;
   double* Hs = red + kV;  // H columns 0..j (ld K+1), staged
+  double* LIs = Hs + (size_t)(K + 1) * K;  // L^{-1} rows 0..m-1
   __shared__ int alive_s;
   auto sum = [&](int k) { return sums[(size_t)k * B + c]; };
   const int nout = j < 0 ? 1 : 3;
@@ -175,7 +173,10 @@ __global__ void __launch_bounds__(kCoefThreads) toar_coeffs_kernel(const double*
     }
   };
   if (j < 0) {  // fresh column state
-    for (int i = tid; i < M * M; i += kCoefThreads) S.L[i] = 0.0;
+    for (int i = tid; i < M * M; i += kCoefThreads) {
+      S.L[i] = 0.0;
+      S.LI[i] = 0.0;
+    }
     for (int i = tid; i < M; i += kCoefThreads) S.DEAD[i] = 0.0;
     if (tid == 0) S.SC[kAlive] = 1.0;
     __syncthreads();
@@ -185,7 +186,10 @@ __global__ void __launch_bounds__(kCoefThreads) toar_coeffs_kernel(const double*
     return;
   }
   // stage the state
-  for (int i = tid; i < (m - 1) * M; i += kCoefThreads) L[i] = S.L[i];
+  for (int i = tid; i < (m - 1) * M; i += kCoefThreads) {
+    L[i] = S.L[i];
+    LIs[i] = S.LI[i];
+  }
   for (int i = tid; i < nt * M; i += kCoefThreads) {
     TG[i] = i < (nt - (final_pass ? 0 : 1)) * M || final_pass ? S.TQg[i] : 0.0;
     TF[i] = i < (nt - (final_pass ? 0 : 1)) * M || final_pass ? S.TQf[i] : 0.0;
@@ -197,24 +201,41 @@ __global__ void __launch_bounds__(kCoefThreads) toar_coeffs_kernel(const double*
   const int hcols = j < 0 ? 0 : (final_pass ? K : j + 1);
   for (int i = tid; i < hcols * (K + 1); i += kCoefThreads) Hs[i] = Hc[i];
   __syncthreads();
-  // 1. Gram row of the newest U vector u_{m-1}: L row m-1 (forward solve, warp 0); a zero vector gets
-  //    the identity row and is marked dead
+  // 1. Gram row of the newest U vector u_{m-1}: l = L^{-1} a, L row m-1 = (l, sqrt(α - |l|²)), and the
+  //    matching row of L^{-1}, (-l^T L^{-1}, 1)/L[m-1][m-1]; a zero vector gets identity rows (dead)
   double* Lr = L + (size_t)(m - 1) * M;
-  if (warp == 0) {
-    for (int i = lane; i < nq; i += 32) sv[i] = sum(2 * i);
-    __syncwarp();
-    fwd_w(L, M, nq, sv, t1, lane);
-    double ll = 0.0;
-    for (int i = lane; i < nq; i += 32) ll += t1[i] * t1[i];
-    ll = wsum(ll);
-    const double alpha = sum(2 * nq);
-    const double d2 = alpha - ll;
-    const bool dead = !(alpha > 0.0) || !(d2 > 1e-24 * alpha);
-    for (int i = lane; i < M; i += 32) Lr[i] = i < nq ? (dead ? 0.0 : t1[i]) : (i == nq ? (dead ? 1.0 : sqrt(d2)) : 0.0);
-    if (lane == 0) S.DEAD[nq] = dead ? 1.0 : 0.0;
-  }
+  double* LIr = LIs + (size_t)(m - 1) * M;
+  for (int i = tid; i < nq; i += kCoefThreads) sv[i] = sum(2 * i);
   __syncthreads();
-  for (int i = tid; i < M; i += kCoefThreads) S.L[(size_t)(m - 1) * M + i] = Lr[i];
+  li_mv(LIs, M, nq, sv, t1);
+  __syncthreads();
+  double llv = 0.0;
+  {
+    double p = 0.0;
+    for (int i = tid; i < nq; i += kCoefThreads) p += t1[i] * t1[i];
+    p = wsum(p);
+    if (lane == 0) red[warp] = p;
+    __syncthreads();
+    for (int w = 0; w < kCoefThreads / 32; ++w) llv += red[w];
+    __syncthreads();
+  }
+  const double alpha = sum(2 * nq);
+  const double d2 = alpha - llv;
+  const bool dead_new = !(alpha > 0.0) || !(d2 > 1e-24 * alpha);
+  const double lmm = dead_new ? 1.0 : sqrt(d2);
+  for (int k = tid; k < M; k += kCoefThreads) {
+    Lr[k] = k < nq ? (dead_new ? 0.0 : t1[k]) : (k == nq ? lmm : 0.0);
+    double s = 0.0;
+    if (k < nq && !dead_new)
+      for (int i = k; i < nq; ++i) s += t1[i] * LIs[i * M + k];
+    LIr[k] = k < nq ? -s / lmm : (k == nq ? 1.0 / lmm : 0.0);
+  }
+  if (tid == 0) S.DEAD[nq] = dead_new ? 1.0 : 0.0;
+  __syncthreads();
+  for (int i = tid; i < M; i += kCoefThreads) {
+    S.L[(size_t)(m - 1) * M + i] = Lr[i];
+    S.LI[(size_t)(m - 1) * M + i] = LIr[i];
+  }
   // 2. provisional vector to true W coordinates: its component e along the assumed w_{m-1} = u_{m-1}
   //    is e u_{m-1} = e Σ_i L[m-1][i] w_i
   if (j >= 0) {
@@ -237,11 +258,9 @@ __global__ void __launch_bounds__(kCoefThreads) toar_coeffs_kernel(const double*
   // 3. y in W coordinates: z = L^{-1} s, ν_y² = γ - |z|²;  y = W z + ν_y u_m  (u_m := (y - U c)/ν_y)
   double nuy = 0.0;
   if (!final_pass) {
-    if (warp == 0) {
-      for (int i = lane; i < m; i += 32) sv[i] = i < nq ? sum(2 * i + 1) : sum(2 * nq + 1);
-      __syncwarp();
-      fwd_w(L, M, m, sv, ZY, lane);
-    }
+    for (int i = tid; i < m; i += kCoefThreads) sv[i] = i < nq ? sum(2 * i + 1) : sum(2 * nq + 1);
+    __syncthreads();
+    li_mv(LIs, M, m, sv, ZY);
     __syncthreads();
     double zz = 0.0;
     for (int i = lane; i < m; i += 32) zz += ZY[i] * ZY[i];
@@ -255,7 +274,7 @@ __global__ void __launch_bounds__(kCoefThreads) toar_coeffs_kernel(const double*
       S.QHg[i] = i == 0 ? (S.DEAD[0] != 0.0 ? 0.0 : L[0]) : 0.0;
       S.QHf[i] = i == 0 ? ZY[0] : (i == 1 ? nuy : 0.0);
     }
-    if (warp == 0) bwd_w(L, M, m, ZY, cu, lane);  // u_1 = (b0 - U c)/ν_y, c = L^{-T} z
+    li_tmv(LIs, M, m, ZY, cu);  // u_1 = (b0 - U c)/ν_y, c = L^{-T} z
     __syncthreads();
     const double inv = nuy > 0.0 ? 1.0 / nuy : 0.0;
     if (tid == 0) coef_y[c] = inv;
@@ -366,9 +385,9 @@ __global__ void __launch_bounds__(kCoefThreads) toar_coeffs_kernel(const double*
   __syncthreads();
   // 7. update-pass coefficients: u_m = (y - U c)/ν_y;  v in W coords over [W_m, u_m]:
   //    W v = U L^{-T} v[0:m] + v[m] (y - U c)/ν_y      (three back-solves on three warps)
-  if (warp == 0) bwd_w(L, M, m, ZY, cu, lane);
-  else if (warp == 1) bwd_w(L, M, m, QF, t1, lane);
-  else if (warp == 2) bwd_w(L, M, m, QG, t2, lane);
+  li_tmv(LIs, M, m, ZY, cu);
+  li_tmv(LIs, M, m, QF, t1);
+  li_tmv(LIs, M, m, QG, t2);
   __syncthreads();
   const double iy = nuy > 0.0 ? 1.0 / nuy : 0.0;
   const double vm1 = QF[m] * iy, vm2 = QG[m] * iy;
@@ -409,11 +428,11 @@ void toar_coeffs(const double* sums, int j, int final_pass, int B, int K, double
                  cudaStream_t s) {
   WL_LAUNCH("toar_coeffs");
   const int M = K + 3;
-  const size_t smem = sizeof(double) * ((size_t)(K + 2) * M + 2 * (size_t)(K + 1) * M + 16 * (size_t)kV +
+  const size_t smem = sizeof(double) * (2 * (size_t)(K + 2) * M + 2 * (size_t)(K + 1) * M + 16 * (size_t)kV +
                                        (size_t)(K + 1) * K);
   static bool attr = false;
   if (!attr) {
-    const size_t smax = sizeof(double) * ((size_t)(kMaxKrylov + 2) * (kMaxKrylov + 3) +
+    const size_t smax = sizeof(double) * (2 * (size_t)(kMaxKrylov + 2) * (kMaxKrylov + 3) +
                                           2 * (size_t)(kMaxKrylov + 1) * (kMaxKrylov + 3) + 16 * (size_t)kV +
                                           (size_t)(kMaxKrylov + 1) * kMaxKrylov);
     WL_CUDA(cudaFuncSetAttribute(toar_coeffs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
