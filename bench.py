@@ -287,8 +287,7 @@ def run_walklap(args):
     # ---- roofline of the dominant kernel (rank 0's kernels; live CUDA-event timing) ----
     peak, peak_src = peaks()
     nnz_loc = int(ci.shape[0])
-    ab = algorithmic_bytes(n_loc, nnz_loc, op.n_halo, G, K, ws_bmax(op, b), b, op.n_theta,
-                           reorth=int(os.environ.get("WL_FORCE_REORTH", "2")))
+    ab = algorithmic_bytes(n_loc, nnz_loc, op.n_halo, G, K, ws_bmax(op, b), b, op.n_theta, reorth=op.reorth)
     kernels = {}
     for name, (tot_ms, cnt) in prof.items():
         per_step_ms = tot_ms / args.steps

@@ -1098,7 +1098,6 @@ wl_status wl_operator_create(wl_comm* comm, int64_t n_global, int64_t row_begin,
     if (op->opts.max_cols < 1 || op->opts.max_cols > kMaxCols) throw Error(WL_EINVAL, "max_cols must be in [1, 32]");
     if (!(op->opts.breakdown_tol >= 0.0)) throw Error(WL_EINVAL, "breakdown_tol < 0");
     if (op->opts.solver != WL_SOLVER_KRYLOV && op->opts.solver != WL_SOLVER_CG) throw Error(WL_EINVAL, "unknown solver");
-    if (const char* fr = getenv("WL_FORCE_REORTH")) op->opts.reorth = atoi(fr);  // experiment knob (tests)
     if (op->opts.reorth < 0 || op->opts.reorth > 2) throw Error(WL_EINVAL, "reorth must be 0, 1 or 2");
     if (!(op->opts.tol >= 0.0)) throw Error(WL_EINVAL, "tol must be >= 0");
     op->kstat.alloc(4);

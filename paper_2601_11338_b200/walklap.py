@@ -279,6 +279,7 @@ class Operator:
                                       _stream_handle(stream), ctypes.byref(h)))
         self.handle = h
         self.comm = comm
+        self.reorth = reorth
         self.thetas = thetas if variant == WL_BTDW else [1.0 if variant == WL_WALK else 0.0]
         nl, nz, nh, nt = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int32()
         _check(lib.wl_operator_info(h, ctypes.byref(nl), ctypes.byref(nz), ctypes.byref(nh), ctypes.byref(nt)))
