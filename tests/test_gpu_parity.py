@@ -466,3 +466,39 @@ def test_hub_rows_split_into_chunks(wl):
         got = op.apply(torch.from_numpy(V).cuda()).cpu().numpy()
         assert relerr(got, S.laplacian_apply(g, 1.0 - th, f, V, rA)).max() < TOL
         op.close()
+
+
+@pytest.mark.parametrize("reorth", [1, 2])
+def test_fuzz_small_graphs_exact_krylov(wl, reorth):
+    """Randomised small cases (n <= 30, random density incl. isolated vertices, θ, walk function, b) with
+    k = 64 >= 2n, where the Krylov space of Z is exhausted (lucky breakdown / U-level deflation paths): the
+    action must equal the dense oracle to 1e-10 for both basis schemes."""
+    rng = np.random.default_rng(1234 + reorth)
+    for case in range(25):
+        n = int(rng.integers(2, 31))
+        p = float(rng.uniform(0.05, 0.6))
+        e = [(i, j) for i in range(n) for j in range(i + 1, n) if rng.random() < p]
+        if not e:
+            e = [(0, 1)]
+        g = gg.from_edges(n, e, f"fuzz{case}")
+        A = D.adjacency(g)
+        rA = max(D.rho_A(A), 1.0)
+        kind = ("exp", "resolvent", "series")[case % 3]
+        if kind == "exp":
+            f, fo = ("exp", 1.0 / rA), C.exp(1.0 / rA)
+        elif kind == "resolvent":
+            a = float(rng.uniform(0.05, 0.8)) / rA
+            f, fo = ("resolvent", a), C.resolvent(a)
+        else:
+            cs = list(rng.uniform(0.0, 1.0, size=int(rng.integers(2, 7))))
+            f, fo = ("series", cs), C.series(cs)
+        thetas = list(np.round(rng.uniform(0, 1, size=int(rng.integers(1, 4))), 3))
+        b = int(rng.integers(1, 4))
+        V = gg.vectors(n, b, 100 + case)
+        op = wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=thetas, f=f, krylov_dim=64, reorth=reorth)
+        got = op.apply(torch.from_numpy(V).cuda()).cpu().numpy()
+        for i, th in enumerate(thetas):
+            ref = D.walk_laplacian(D.phi(A, 1.0 - th, fo)) @ V
+            err = relerr(got[:, i * b:(i + 1) * b], ref).max()
+            assert err < TOL, (case, n, kind, th, b, err)
+        op.close()
