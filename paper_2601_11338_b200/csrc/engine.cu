@@ -1266,11 +1266,14 @@ wl_status wl_apply_host(const wl_operator* op, int32_t b, const double* Vh, int6
     cudaStream_t s = S_(stream);
     ws->hV.alloc((size_t)std::max<int64_t>(1, n * b));
     ws->hLV.alloc((size_t)std::max<int64_t>(1, n * G));
-    WL_CUDA(cudaMemcpy2DAsync(ws->hV.p, sizeof(double) * b, Vh, sizeof(double) * ldv, sizeof(double) * b, n,
-                              cudaMemcpyHostToDevice, s));
+    // contiguous blocks go as one linear copy (a pitched copy of 1e7 short rows runs at a fraction of the link)
+    if (ldv == b) WL_CUDA(cudaMemcpyAsync(ws->hV.p, Vh, sizeof(double) * n * b, cudaMemcpyHostToDevice, s));
+    else WL_CUDA(cudaMemcpy2DAsync(ws->hV.p, sizeof(double) * b, Vh, sizeof(double) * ldv, sizeof(double) * b, n,
+                                   cudaMemcpyHostToDevice, s));
     run_action(op, ws, 1, ws->hV.p, b, b, ws->hLV.p, G, s);
-    WL_CUDA(cudaMemcpy2DAsync(LVh, sizeof(double) * ldlv, ws->hLV.p, sizeof(double) * G, sizeof(double) * G, n,
-                              cudaMemcpyDeviceToHost, s));
+    if (ldlv == G) WL_CUDA(cudaMemcpyAsync(LVh, ws->hLV.p, sizeof(double) * n * G, cudaMemcpyDeviceToHost, s));
+    else WL_CUDA(cudaMemcpy2DAsync(LVh, sizeof(double) * ldlv, ws->hLV.p, sizeof(double) * G, sizeof(double) * G, n,
+                                   cudaMemcpyDeviceToHost, s));
     WL_CUDA(cudaStreamSynchronize(s));
   });
 }
