@@ -358,7 +358,7 @@ size_t ring_smem() { return (size_t)kStages * kStageElems * sizeof(double); }
 
 VecPtrs shifted(const VecPtrs& v, int i0) {
   VecPtrs r{};
-  for (int k = 0; k + i0 < kMaxKrylov + 2; ++k) r.p[k] = v.p[k + i0];
+  for (int k = 0; k + i0 < kMaxVecSlots; ++k) r.p[k] = v.p[k + i0];
   return r;
 }
 

@@ -2,10 +2,10 @@
 //
 // One "action" on a chunk of B <= 32 columns (column c = (θ index, input column)) is
 // (SURVEY §8(a) a3-a7):
-//   a3  u = [A v ; A(Av) - μ d⊙v]                          two Z-SpMM launches (seeds q_1 v, q_2 v)
-//   a4  for j < k: w = Z q_j  (bottom half only)           spmv (merge-path, fused recurrence)
-//   a5            CGS2 of w against q_0..q_j, ||w''||       gram_proj / gram_update_proj /
-//                                                           gram_update_norm + finalize_step
+//   a3  u = [A v ; A(Av) - μ d⊙v]                          two SpMM launches (θ-independent: over b columns)
+//   a4  for j < k: w = Z q_j  (bottom half only)           spmv (degree-binned, fused recurrence)
+//   a5            orthogonalise against the basis           TOAR (default): dcgs2_dots + toar_coeffs +
+//                                                           toar_update; DCGS2: dcgs2_dots/coeffs/update
 //   a6  y = f_1(H_k) e_1 on the device                     small_f
 //   a7  φv = c_0 v + ||u|| [I O] Q_k y ;  𝕃v = t'⊙v - (φv - c_0 v)    combine
 // with t' = φ1 - c_0 1 cached at operator creation (a8).  Multi-GPU: the SpMM input rows owned
@@ -185,7 +185,7 @@ struct wl_workspace {
   DArr<double> hV, hLV;
   // diffusion (outer Lanczos)
   int kout_alloc = 0;
-  DArr<double> oQ, ow, oH, os, on0, osums1, osums2, osums3, otau, oY, oscratch;
+  DArr<double> oQ, ow, oH, on0, oref, osums1, ocoef_v, ocoef_s, otau, oY, oscratch;
   DArr<int> okeff;
   ~wl_workspace() {
     if (cg_flags_host) cudaFreeHost(cg_flags_host);
@@ -849,82 +849,66 @@ inline int64_t outer_stride(const wl_operator* op) { return std::max<int64_t>(2,
 // `apply(P̃_j, out)` writes the operator applied to the UNNORMALISED basis vector P̃_j.
 template <class Apply>
 void outer_arnoldi(const wl_operator* op, wl_workspace* ws, int m, Apply&& apply, cudaStream_t s, int64_t len = 0) {
+  // Arnoldi with DCGS2 on the bulk-copy ring passes (B = 1): q_i in order at oQ + i*n (normalised),
+  // the pending once-orthogonalised p_j alternates between the two buffers after slot m.
   const int64_t n = len ? len : outer_stride(op);
   WL_CUDA(cudaMemsetAsync(ws->oH.p, 0, sizeof(double) * (m + 1) * m, s));
-  GramArgs g{};
-  g.Q = ws->oQ.p;
-  g.vstride = n;
-  g.len = n;
-  g.B = 1;
-  g.s = ws->os.p;
-  g.partials = ws->partials.p;
-  g.ticket = ws->ticket.p;
-  g.grid = gram_grid(n, 1);
-  g.nvec = 0;
-  g.wa = ws->oQ.p;
-  g.split = n;
-  g.sums_out = ws->osums1.p;
-  gram_proj(g, s);
-  allreduce(op, ws->osums1.p, 1, s);
-  finalize_norm0(ws->osums1.p, 1, ws->on0.p, ws->os.p, ws->okeff.p, m, s);
+  VecPtrs Q{};
+  for (int i = 0; i <= m; ++i) Q.p[i] = ws->oQ.p + (int64_t)i * n;
+  double* P[2] = {ws->oQ.p + (int64_t)(m + 1) * n, ws->oQ.p + (int64_t)(m + 2) * n};
+  WL_CUDA(cudaMemcpyAsync(P[0], ws->oQ.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));  // p_0 = x0
+  Dcgs2Args d{};
+  d.Q = Q;
+  d.len = n;
+  d.B = 1;
+  d.split = n;
+  d.partials = ws->partials.p;
+  d.sums_out = ws->osums1.p;
+  d.coef_v = ws->ocoef_v.p;
+  d.coef_s = ws->ocoef_s.p;
+  const double btol = op->opts.breakdown_tol;
+  int cur = 0;
   for (int j = 0; j < m; ++j) {
-    double* Pj = ws->oQ.p + (int64_t)j * n;
-    double* Pn = ws->oQ.p + (int64_t)(j + 1) * n;
-    apply(Pj, ws->ow.p);
-    GramArgs w = g;
-    w.nvec = j + 1;
-    w.wa = ws->ow.p;
-    w.wscale = ws->os.p + j;  // q_j = s_j P̃_j, so Z q_j = s_j * apply(P̃_j)
-    w.split = n;
-    w.sums_out = ws->osums1.p;
-    gram_proj(w, s);
-    allreduce(op, ws->osums1.p, j + 2, s);
-    GramArgs u = w;
-    u.wout = Pn;
-    u.sums_in = ws->osums1.p;
-    u.sums_out = ws->osums2.p;
-    if (j + 1 <= 32) {
-      gram_update_proj(u, s);
-    } else {
-      u.sums_out = ws->osums3.p;
-      gram_update_norm(u, s);
-      GramArgs p2 = g;
-      p2.nvec = j + 1;
-      p2.wa = Pn;
-      p2.split = n;
-      p2.sums_out = ws->osums2.p;
-      gram_proj(p2, s);
-    }
-    allreduce(op, ws->osums2.p, j + 1, s);
-    GramArgs v = g;
-    v.nvec = j + 1;
-    v.wa = Pn;
-    v.split = n;
-    v.wout = Pn;
-    v.sums_in = ws->osums2.p;
-    v.sums_out = ws->osums3.p;
-    gram_update_norm(v, s);
-    allreduce(op, ws->osums3.p, 1, s);
-    finalize_step(ws->osums1.p, ws->osums2.p, ws->osums3.p, j, 1, m, op->opts.breakdown_tol, 1, ws->os.p,
-                  ws->oH.p, ws->okeff.p, s);
+    apply(P[cur], ws->ow.p);  // w = Op p_j
+    d.nq = j;
+    d.P = P[cur];
+    d.wa = ws->ow.p;
+    d.wb = nullptr;
+    dcgs2_dots(d, s);
+    allreduce(op, ws->osums1.p, (size_t)(2 * j + 3), s);
+    dcgs2_coeffs(ws->osums1.p, j, 1, m, btol, 0, 1, ws->oH.p, ws->oref.p, ws->on0.p, ws->okeff.p, ws->ocoef_v.p,
+                 ws->ocoef_s.p, s);
+    d.Qout = const_cast<double*>(Q.p[j]);
+    d.Pnext = P[cur ^ 1];
+    d.accumulate = 0;
+    dcgs2_update(d, s);
+    cur ^= 1;
   }
+  d.nq = m;  // delayed reorthogonalisation of p_m completes column m-1 of H
+  d.P = P[cur];
+  d.wa = nullptr;
+  d.wb = nullptr;
+  dcgs2_dots(d, s);
+  allreduce(op, ws->osums1.p, (size_t)(2 * m + 3), s);
+  dcgs2_coeffs(ws->osums1.p, m, 1, m, btol, 1, 1, ws->oH.p, ws->oref.p, ws->on0.p, ws->okeff.p, ws->ocoef_v.p,
+               ws->ocoef_s.p, s);
 }
 
 
 void outer_alloc(const wl_operator* op, wl_workspace* ws, int m, int nt, int64_t len = 0) {
   const int64_t np = len ? len : outer_stride(op);
   if (ws->kout_alloc >= m && ws->otau.n >= (size_t)nt) return;
-  ws->oQ.alloc((size_t)(m + 1) * np);
+  ws->oQ.alloc((size_t)(m + 3) * np);  // q_0..q_m, then the two pending-vector buffers
   ws->ow.alloc((size_t)np);
-  WL_CUDA(cudaMemset(ws->oQ.p, 0, sizeof(double) * (m + 1) * np));
+  WL_CUDA(cudaMemset(ws->oQ.p, 0, sizeof(double) * (m + 3) * np));
   WL_CUDA(cudaMemset(ws->ow.p, 0, sizeof(double) * np));
   ws->oH.alloc((size_t)(m + 1) * m);
-  ws->os.alloc(m + 1);
   ws->on0.alloc(1);
   ws->okeff.alloc(1);
-  ws->osums1.alloc(m + 2);
-  ws->osums2.alloc(m + 2);
-  ws->osums3.alloc(m + 2);
+  ws->oref.alloc(1);
+  ws->osums1.alloc((size_t)2 * m + 5);
+  ws->ocoef_v.alloc((size_t)2 * (m + 1));
+  ws->ocoef_s.alloc(3);
   ws->otau.alloc(std::max(1, nt));
   ws->oY.alloc((size_t)std::max(1, nt) * (m + 1));
   ws->oscratch.alloc((size_t)std::max(1, nt) * 9 * kMaxSmallN * kMaxSmallN);
@@ -1309,13 +1293,14 @@ wl_status wl_diffuse(const wl_operator* op, int32_t theta_index, int32_t nt, con
     f.keff = ws->okeff.p;
     f.kind = 3;
     f.n0 = ws->on0.p;
-    f.s = ws->os.p;
+    f.s = nullptr;  // q_i stored normalised
     f.comb = ws->oY.p;
     f.scratch = ws->oscratch.p;
     f.B = 1;
     f.tau = ws->otau.p;
     f.nprob = nt;
     small_f(f, s);
+    // m + 1 = the row stride of Y (small_f kind 3); slot m is never written (zero) and its weight is 0
     lanczos_combine(ws->oQ.p, outer_stride(op), m + 1, n, ws->oY.p, nt, 1.0, X, ldx, op->perm.p, s);
   });
 }

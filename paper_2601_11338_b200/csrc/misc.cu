@@ -1,4 +1,4 @@
-// misc.cu — small kernels of the Krylov engine: batching of inputs, Arnoldi bookkeeping,
+// misc.cu — small kernels of the Krylov engine: batching of inputs, DCGS2 bookkeeping,
 // the combine/Laplacian epilogue (step a7) and halo packing.
 #include "wl_internal.cuh"
 #include <cmath>
@@ -33,44 +33,6 @@ __global__ void seed_expand_kernel(const double* s1, const double* s2, const dou
     const double d = (double)(__ldg(rowptr + r + 1) - __ldg(rowptr + r));
     t0[e] = s1[src];
     b0[e] = s2[src] + g1s[c] * d * v[src];  // g1s = -μ
-  }
-}
-
-// n0 = ||u||, s0 = 1/n0 (0 if u == 0: φv = c_0 v exactly), keff = K (0 if u == 0)
-__global__ void finalize_norm0_kernel(const double* sums, int B, double* n0, double* s0, int* keff,
-                                      int K) {
-  const int c = threadIdx.x;
-  if (c >= B) return;
-  const double nrm = sqrt(sums[c]);
-  n0[c] = nrm;
-  s0[c] = nrm > 0.0 ? 1.0 / nrm : 0.0;
-  keff[c] = nrm > 0.0 ? K : 0;
-}
-
-// Column j of the Arnoldi Hessenberg H (entries (i, j), i <= j+1) and the scale of q_{j+1}.
-//   h_i = s_i (sums1_i + sums2_i)        (CGS2: both passes' coefficients; CGS: sums1 only)
-//   ||w''|| = sqrt(sums3);  breakdown if ||w''|| <= btol ||Z q_j|| (||Z q_j||² = sums1_nvec)
-__global__ void finalize_step_kernel(const double* sums1, const double* sums2, const double* sums3,
-                                     int j, int B, int K, double btol, int reorth, double* s_all,
-                                     double* H, int* keff) {
-  const int c = threadIdx.x;
-  if (c >= B) return;
-  const int nvec = j + 1;
-  double* Hc = H + (int64_t)c * (K + 1) * K + (int64_t)j * (K + 1);
-  const bool alive = s_all[j * B + c] != 0.0;
-  const double nrm = sqrt(sums3[c]);
-  const double wn = sqrt(sums1[nvec * B + c]);
-  for (int i = 0; i <= j; ++i) {
-    const double si = s_all[i * B + c];
-    Hc[i] = alive ? si * (sums1[i * B + c] + (reorth ? sums2[i * B + c] : 0.0)) : 0.0;
-  }
-  if (alive && nrm > btol * wn && nrm > 0.0) {
-    Hc[j + 1] = nrm;
-    s_all[(j + 1) * B + c] = 1.0 / nrm;
-  } else {
-    Hc[j + 1] = 0.0;
-    s_all[(j + 1) * B + c] = 0.0;
-    if (alive && keff[c] == K) keff[c] = j + 1;  // invariant subspace: use H_{j+1}
   }
 }
 
@@ -312,21 +274,6 @@ void setup_chunk(const double* mu, int gstart, int b, int B, double* g0z, double
                  double* g1s, int* vcol, int* tcol, cudaStream_t s) {
   WL_LAUNCH("setup_chunk");
   setup_chunk_kernel<<<1, 32, 0, s>>>(mu, gstart, b, B, g0z, g1z, g0s, g1s, vcol, tcol);
-  WL_CUDA(cudaGetLastError());
-}
-
-void finalize_norm0(const double* sums, int B, double* n0, double* s0, int* keff, int K,
-                    cudaStream_t s) {
-  WL_LAUNCH("finalize_norm0");
-  finalize_norm0_kernel<<<1, 32, 0, s>>>(sums, B, n0, s0, keff, K);
-  WL_CUDA(cudaGetLastError());
-}
-
-void finalize_step(const double* sums1, const double* sums2, const double* sums3, int j, int B,
-                   int K, double btol, int reorth, double* s_all, double* H, int* keff,
-                   cudaStream_t s) {
-  WL_LAUNCH("finalize_step");
-  finalize_step_kernel<<<1, 32, 0, s>>>(sums1, sums2, sums3, j, B, K, btol, reorth, s_all, H, keff);
   WL_CUDA(cudaGetLastError());
 }
 

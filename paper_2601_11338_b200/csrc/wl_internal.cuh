@@ -66,28 +66,8 @@ struct SpmvArgs {
 };
 void spmv(const SpmvArgs& a, cudaStream_t s);
 
-// ---------------------------------------------------------------- Gram-Schmidt kernels
-// Basis: nvec vectors, vector i at Q + i*vstride, element e (column e % B) for e < len*B.
-// w(e) = e < split*B ? wscale[c] * wa[e] : wb[e - split*B]   ("two-source" vector).
-struct GramArgs {
-  const double* Q; int64_t vstride;
-  int nvec;
-  int64_t len;      // rows (L = 2 n_loc for Z vectors)
-  int B;
-  const double* s;  // per-vector column scales s[i*B + c] (basis stores unnormalised vectors)
-  const double* wa; const double* wscale; int64_t split;
-  const double* wb;
-  double* wout;     // written vector (update kernels)
-  const double* sums_in;   // previous reduction results ((nvec)*B): coefficients c_i = s_i^2 * sums_in_i
-  double* partials;        // per-CTA partial sums
-  double* sums_out;        // reduced sums (nvec+1)*B
-  unsigned int* ticket;
-  int grid;
-};
-void gram_proj(GramArgs a, cudaStream_t s);         // sums_out[i] = Σ Q_i w, sums_out[nvec] = Σ w²
-void gram_update_proj(GramArgs a, cudaStream_t s);  // wout = w - Σ c_i Q_i ; sums_out[i] = Σ Q_i wout
-void gram_update_norm(GramArgs a, cudaStream_t s);  // wout = w - Σ c_i Q_i ; sums_out[0] = Σ wout²
-int gram_grid(int64_t elems, int B);
+// ---------------------------------------------------------------- Gram-Schmidt passes
+int gram_grid(int64_t elems, int B);  // upper bound on the CTAs of a dot pass (partial buffer sizing)
 
 // DCGS2: delayed classical Gram-Schmidt (one reduction per Arnoldi step).  Step j holds the
 // finalised orthonormal q_0..q_{j-1} (Q) and p_j (P): once orthogonalised, unnormalised.
@@ -96,8 +76,9 @@ int gram_grid(int64_t elems, int B);
 //   pass B (dcgs2_update): q_j = cq_p p_j + Σ cq_i q_i  (into Qout, which must not alias P),
 //                          p_{j+1} = cp_w w + cp_p p_j + Σ cp_i q_i  (into Pnext)
 // Basis vectors are addressed through a pointer table (slot i -> vector), passed by value.
+constexpr int kMaxVecSlots = 130;  // basis slots a pass can address: k+2 <= 66 inner, k_out+1 <= 129 outer
 struct VecPtrs {
-  const double* p[kMaxKrylov + 2];
+  const double* p[kMaxVecSlots];
 };
 struct Dcgs2Args {
   VecPtrs Q; int nq;                  // q_0 .. q_{nq-1}
@@ -192,12 +173,6 @@ void seed_expand(const double* s1, const double* s2, const double* v, int b, con
                  const int* vcol, int B, int64_t n, double* t0, double* b0, cudaStream_t s);
 void setup_chunk(const double* mu, int gstart, int b, int B, double* g0z, double* g1z, double* g0s,
                  double* g1s, int* vcol, int* tcol, cudaStream_t s);
-// Arnoldi bookkeeping after a reduction: see engine.cu for the exact semantics.
-void finalize_norm0(const double* sums, int B, double* n0, double* s0, int* keff, int K,
-                    cudaStream_t s);
-void finalize_step(const double* sums1, const double* sums2, const double* sums3, int j, int B,
-                   int K, double btol, int reorth, double* s_all, double* H, int* keff,
-                   cudaStream_t s);
 // combine: mode 0 = φV (c0 V + Σ comb_i Q_i,top), 1 = 𝕃V (lscale (t'⊙V - Σ comb_i Q_i,top)),
 //          2 = t' (Σ comb_i Q_i,top) for V = 1
 // V column of batch column c is vcol[c]; t' column is tcol[c]; internal row r is user row
