@@ -185,11 +185,12 @@ __global__ void __launch_bounds__(kDotsConsumers + 32, 1) dcgs2_dots_ring(Dcgs2A
     }
     __syncthreads();
     const int nv = min(kRedBatch, nval - v0);
-    for (int idx = t; idx < nv * B; idx += blockDim.x) {
+    for (int idx = warp; idx < nv * B; idx += blockDim.x / 32) {  // a warp per output, fixed-order tree
       const int vv = idx / B, c = idx - vv * B;
       double sum = 0.0;
-      for (int tt = c; tt < tpb; tt += B) sum += red[vv * kDotsConsumers + tt];
-      a.partials[(int64_t)((v0 + vv) * B + c) * gridDim.x + blockIdx.x] = sum;
+      for (int tt = c + lane * B; tt < tpb; tt += 32 * B) sum += red[vv * kDotsConsumers + tt];
+      for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+      if (lane == 0) a.partials[(int64_t)((v0 + vv) * B + c) * gridDim.x + blockIdx.x] = sum;
     }
     __syncthreads();
   }
@@ -366,8 +367,9 @@ VecPtrs shifted(const VecPtrs& v, int i0) {
 
 // pass A for nq <= 32 per launch; longer bases tile the vectors: tile [i0, i1) writes its a/b
 // pairs at offset 2*i0 and its trailing α/β/γ are overwritten by the next tile.
-void dcgs2_dots(Dcgs2Args a, cudaStream_t s) {
+int dcgs2_dots(Dcgs2Args a, cudaStream_t s) {
   if (a.nq > kMaxVecPerLaunch) {
+    if (!a.sums_out) throw Error(1, "dcgs2_dots: tiled passes (> 32 vectors) need sums_out");
     for (int i0 = 0; i0 < a.nq; i0 += kMaxVecPerLaunch) {
       Dcgs2Args t = a;
       t.nq = std::min(kMaxVecPerLaunch, a.nq - i0);
@@ -375,7 +377,7 @@ void dcgs2_dots(Dcgs2Args a, cudaStream_t s) {
       t.sums_out = a.sums_out + (int64_t)2 * i0 * a.B;
       dcgs2_dots(t, s);
     }
-    return;
+    return 0;
   }
   WL_LAUNCH("dcgs2_dots");
   {
@@ -390,8 +392,11 @@ void dcgs2_dots(Dcgs2Args a, cudaStream_t s) {
     a.grid = (int)std::min<int64_t>(148, (N + tpb * kDotsPer - 1) / (tpb * kDotsPer));
     dcgs2_dots_ring<<<a.grid, kDotsConsumers + 32, ring_smem(), s>>>(a, tpb);
     WL_CUDA(cudaGetLastError());
-    note_launch("gram_reduce");
-    reduce_partials(a.partials, (2 * a.nq + 3) * a.B, a.grid, a.sums_out, s);
+    if (a.sums_out) {  // null: the consumer reduces the partials itself (a.grid of them per output)
+      note_launch("gram_reduce");
+      reduce_partials(a.partials, (2 * a.nq + 3) * a.B, a.grid, a.sums_out, s);
+    }
+    return a.grid;
   }
 }
 

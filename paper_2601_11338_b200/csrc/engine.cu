@@ -450,16 +450,24 @@ void toar_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double*
   t.coef_y = ws->toar_cy.p;
   t.coef_u = ws->toar_cu.p;
   t.coef_ld = ld;
+  // one GPU, <= 32 basis vectors per dot pass: toar_coeffs reduces the dot pass's partials itself;
+  // otherwise the pass reduces them and NCCL allreduces the sums across ranks
+  const bool fuse = !multi(op) && K + 1 <= 32;
+  int G = 0;
+  auto dots = [&](int count) {
+    d.sums_out = fuse ? nullptr : ws->sums1.p;
+    G = dcgs2_dots(d, s);
+    if (!fuse) allreduce(op, ws->sums1.p, (size_t)count, s);
+  };
   auto coeffs = [&](int j, int final_pass) {
-    toar_coeffs(ws->sums1.p, j, final_pass, B, K, btol, ws->H.p, ws->n0.p, ws->keff.p, ws->toar_state.p, stride,
-                ws->toar_cy.p, ws->toar_cu.p, ld, s);
+    toar_coeffs(ws->sums1.p, fuse ? ws->partials.p : nullptr, G, j, final_pass, B, K, btol, ws->H.p, ws->n0.p,
+                ws->keff.p, ws->toar_state.p, stride, ws->toar_cy.p, ws->toar_cu.p, ld, s);
   };
   // seed step: Gram of (t0, b0), u_1 = (b0 - proj)/ν
   d.nq = 0;
   d.P = U0;
   d.wa = xb;
-  dcgs2_dots(d, s);
-  allreduce(op, ws->sums1.p, (size_t)3 * B, s);
+  dots(3 * B);
   coeffs(-1, 0);
   t.m = 1;
   t.y = xb;
@@ -477,8 +485,7 @@ void toar_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double*
     d.nq = m - 1;
     d.P = U.p[m - 1];
     d.wa = yb;
-    dcgs2_dots(d, s);
-    allreduce(op, ws->sums1.p, (size_t)(2 * (m - 1) + 3) * B, s);
+    dots((2 * (m - 1) + 3) * B);
     coeffs(j, 0);
     t.m = m;
     t.y = yb;
@@ -493,8 +500,7 @@ void toar_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double*
   d.nq = K + 1;  // Gram row of the last U vector completes H column K-1
   d.P = U.p[K + 1];
   d.wa = nullptr;
-  dcgs2_dots(d, s);
-  allreduce(op, ws->sums1.p, (size_t)(2 * (K + 1) + 3) * B, s);
+  dots((2 * (K + 1) + 3) * B);
   coeffs(K, 1);
   // a6: y = f_1(H_k) e_1 per column; a7: combine top halves U (Σ_i comb_i g_i)
   SmallFArgs f{};

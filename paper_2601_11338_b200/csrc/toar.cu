@@ -68,6 +68,7 @@ size_t toar_state_doubles(int K) {
 //   j = -1: o = 0 -> u_1;   j >= 0: o = 0 -> u_m, 1 -> x_{j+1} = bottom(q̂_{j+1}), 2 -> z_{j+1} = top.
 // Gram-Schmidt in coefficient space is classical (all projections of a pass at once), done twice.
 constexpr int kCoefThreads = 128;
+constexpr int kMaxVecPerLaunchCoef = kMaxKrylov + 2;  // dot-pass outputs per column: 2(m-1)+3, m <= K+2
 constexpr int kV = kMaxKrylov + 4;  // coefficient vector capacity (>= K + 3)
 
 __device__ inline double wsum(double v) {
@@ -130,7 +131,8 @@ __device__ double block_norm2(const double* g, const double* f, int n, double* r
   return s;
 }
 
-__global__ void __launch_bounds__(kCoefThreads) toar_coeffs_kernel(const double* sums, int j, int final_pass, int B,
+__global__ void __launch_bounds__(kCoefThreads) toar_coeffs_kernel(const double* sums, const double* partials, int G,
+                                                                   int j, int final_pass, int B,
                                                                    int K, double btol, double* H, double* n0,
                                                                    int* keff, double* state, size_t stride,
                                                                    double* coef_y, double* coef_u, int coef_ld) {
@@ -164,7 +166,23 @@ __global__ void __launch_bounds__(kCoefThreads) toar_coeffs_kernel(const double*
   double* Hs = red + kV;  // H columns 0..j (ld K+1), staged
   double* LIs = Hs + (size_t)(K + 1) * K;  // L^{-1} rows 0..m-1
   __shared__ int alive_s;
-  auto sum = [&](int k) { return sums[(size_t)k * B + c]; };
+  __shared__ double ssum[2 * kMaxVecPerLaunchCoef + 3];
+  {  // this column's dot-pass outputs, reduced here from the per-CTA partials when given (fixed order)
+    const int nval = 2 * (m - 1) + 3;
+    if (partials) {
+      for (int k = warp; k < nval; k += kCoefThreads / 32) {
+        const double* p = partials + ((size_t)k * B + c) * G;
+        double v = 0.0;
+        for (int g = lane; g < G; g += 32) v += p[g];
+        v = wsum(v);
+        if (lane == 0) ssum[k] = v;
+      }
+    } else {
+      for (int k = tid; k < nval; k += kCoefThreads) ssum[k] = sums[(size_t)k * B + c];
+    }
+    __syncthreads();
+  }
+  auto sum = [&](int k) { return ssum[k]; };
   const int nout = j < 0 ? 1 : 3;
   auto zero_out = [&]() {
     for (int o = 0; o < nout; ++o) {
@@ -423,9 +441,9 @@ __global__ void toar_combine_coef_kernel(const double* comb, int B, int K, const
   for (int k = 0; k < mU; ++k) combU[(size_t)k * B + c] = ke > 0 ? x[k] : 0.0;
 }
 
-void toar_coeffs(const double* sums, int j, int final_pass, int B, int K, double btol, double* H, double* n0,
-                 int* keff, double* state, size_t stride, double* coef_y, double* coef_u, int coef_ld,
-                 cudaStream_t s) {
+void toar_coeffs(const double* sums, const double* partials, int G, int j, int final_pass, int B, int K, double btol,
+                 double* H, double* n0, int* keff, double* state, size_t stride, double* coef_y, double* coef_u,
+                 int coef_ld, cudaStream_t s) {
   WL_LAUNCH("toar_coeffs");
   const int M = K + 3;
   const size_t smem = sizeof(double) * (2 * (size_t)(K + 2) * M + 2 * (size_t)(K + 1) * M + 16 * (size_t)kV +
@@ -438,8 +456,8 @@ void toar_coeffs(const double* sums, int j, int final_pass, int B, int K, double
     WL_CUDA(cudaFuncSetAttribute(toar_coeffs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
     attr = true;
   }
-  toar_coeffs_kernel<<<B, kCoefThreads, smem, s>>>(sums, j, final_pass, B, K, btol, H, n0, keff, state, stride,
-                                                  coef_y, coef_u, coef_ld);
+  toar_coeffs_kernel<<<B, kCoefThreads, smem, s>>>(sums, partials, G, j, final_pass, B, K, btol, H, n0, keff, state,
+                                                  stride, coef_y, coef_u, coef_ld);
   WL_CUDA(cudaGetLastError());
 }
 

@@ -109,12 +109,16 @@ struct ToarArgs {
 void toar_update(ToarArgs a, cudaStream_t s);
 // TOAR coefficient bookkeeping (toar.cu), one thread per Krylov column
 size_t toar_state_doubles(int K);
-void toar_coeffs(const double* sums, int j, int final_pass, int B, int K, double btol, double* H, double* n0,
-                 int* keff, double* state, size_t stride, double* coef_y, double* coef_u, int coef_ld,
-                 cudaStream_t s);
+// sums: reduced dot-pass outputs ([k*B + c]); or, with partials != null, the unreduced per-CTA partials
+// ([(k*B + c)*G + cta]) that the kernel reduces itself (single GPU: one launch fewer per step)
+void toar_coeffs(const double* sums, const double* partials, int G, int j, int final_pass, int B, int K, double btol,
+                 double* H, double* n0, int* keff, double* state, size_t stride, double* coef_y, double* coef_u,
+                 int coef_ld, cudaStream_t s);
 void toar_combine_coef(const double* comb, int B, int K, const int* keff, const double* state, size_t stride,
                        double* combU, cudaStream_t s);
-void dcgs2_dots(Dcgs2Args a, cudaStream_t s);
+// returns the grid of the (single) launch: with sums_out == null the partials ([output][CTA]) are left
+// for the consumer to reduce (single launch, nq <= 32)
+int dcgs2_dots(Dcgs2Args a, cudaStream_t s);
 void dcgs2_update(Dcgs2Args a, cudaStream_t s);
 void dcgs2_coeffs(const double* sums, int j, int B, int K, double btol, int final_pass, int reorth, double* H,
                   double* ref, double* n0, int* keff, double* coef_v, double* coef_s, cudaStream_t s);
