@@ -301,8 +301,9 @@ def run_walklap(args):
     ncu = ncu_traffic()
     roof = {"kernel": top, "bound": "hbm", "achieved": kernels[top]["achieved_gbs"], "peak": peak,
             "unit": "GB/s", "frac": kernels[top]["frac"], "peak_source": peak_src,
-            "traffic": ncu.get(top), "alg_bytes_per_launch": ab[top] / max(1, kernels[top]["launches_per_step"])}
-    if top == "spmv_binned" and ncu.get(top):
+            "traffic": ncu.get(top) if world == 1 else None,  # the committed ncu capture is single-GPU
+            "alg_bytes_per_launch": ab[top] / max(1, kernels[top]["launches_per_step"])}
+    if top == "spmv_binned" and ncu.get(top) and world == 1:
         # the SpMM's real bound is the rate HBM serves random rows: context for `frac`
         ms_launch = kernels[top]["ms_per_step"] / max(1, kernels[top]["launches_per_step"])
         roof["traffic_gbs"] = ncu[top] / (ms_launch / 1e3) / 1e9
@@ -329,7 +330,8 @@ def run_walklap(args):
                        "setup_s": {"generate": round(t_gen, 2), "operator_create_incl_t": round(t_create, 2)}},
             "roofline": roof,
             "spmv": {"b": G if G <= 32 else 32, "achieved_gbs": spmv.get("achieved_gbs"), "frac": spmv.get("frac"),
-                     "peak": peak, "share": spmv.get("share"), "traffic": ncu.get("spmv_binned"),
+                     "peak": peak, "share": spmv.get("share"),
+                     "traffic": ncu.get("spmv_binned") if world == 1 else None,
                      "b1": (dict(spmv_b1, frac=spmv_b1["achieved_gbs"] / peak) if spmv_b1 else None)},
             "kernels": {k: {kk: (round(vv, 6) if isinstance(vv, float) else vv) for kk, vv in v.items()}
                         for k, v in sorted(kernels.items(), key=lambda kv: -kv[1]["ms_per_step"])},
