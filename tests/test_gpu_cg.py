@@ -145,3 +145,20 @@ def test_cg_diffusion_karate(wl):
     ref = D.diffusion(Lap, x0, taus)
     assert relerr(X, ref).max() < 1e-9
     op.close()
+
+
+@pytest.mark.slow
+def test_full_c3_cg_resolvent_vs_series(wl):
+    """Config C3 at full size (n ~ 2e6, road-like): the §5.3 resolvent NBT Laplacian by PCG at the largest α of the
+    sweep vs the matrix-free series oracle (α ρ(A) = 10^-1/2: ~40 series terms)."""
+    from graphgen import configs
+    g = configs.get("c3")["make"]()
+    rA = S.rho_A(g)
+    alpha = ALPHAS[-1] / rA
+    f = C.resolvent(alpha)
+    V = gg.vectors(g.n, 2, 55)
+    op = wl.Operator(g.n, g.row_ptr, g.col_idx, variant="nbt", f=("resolvent", alpha), solver="cg", cg_tol=1e-13)
+    got = op.apply(torch.from_numpy(V).cuda()).cpu().numpy()
+    op.close()
+    ref = S.laplacian_apply(g, 1.0, f, V, rA)
+    assert relerr(got, ref).max() < TOL

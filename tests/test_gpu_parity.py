@@ -502,3 +502,26 @@ def test_fuzz_small_graphs_exact_krylov(wl, reorth):
             err = relerr(got[:, i * b:(i + 1) * b], ref).max()
             assert err < TOL, (case, n, kind, th, b, err)
         op.close()
+
+
+@pytest.mark.slow
+def test_full_c2_markov_vs_series(wl):
+    """NEXT-3 at config C2 size (Barabási-Albert n = 1e5): three chain steps p_{k+1}^T = φ_θ (p_k / t) vs the series
+    oracle (t and φ applies by the explicit recurrence); mass stays 1."""
+    from graphgen import configs
+    g = configs.get("c2")["make"]()
+    rA = S.rho_A(g)
+    f = C.exp(1.0 / rA)
+    th = 0.5
+    op = wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=[th], f=("exp", f.param))
+    p0 = gg.vectors(g.n, 1, 9)[:, 0] ** 2
+    p0 /= p0.sum()
+    got = op.markov(torch.from_numpy(p0).cuda(), 3).cpu().numpy()
+    op.close()
+    A = S.csr(g)
+    t = S.total_communicability(g, 1.0 - th, f, rA, A=A)
+    p = p0.copy()
+    for k in range(3):
+        p = S.phi_apply(g, 1.0 - th, f, p / t, rA, A=A)
+        assert relerr(got[:, k], p).max() < TOL
+        assert abs(got[:, k].sum() - 1.0) < 1e-12
