@@ -595,6 +595,83 @@ def run_diffusion(args):
         dist.destroy_process_group()
 
 
+def run_trace(args):
+    """--trace: NEXT-2, Alg. 1 XNysTrace-exp with poles at ∞ (reading R16) in the shape of Fig. 7:
+    M = 30 Gaussian probes, 90 t-points, on the config's graph (default C3, NBT θ = 0, f = exp(βx), β = 1/ρ(A)).
+    One step = the whole curve: k block Laplacian actions on M columns + block Gram–Schmidt + the host
+    estimator.  Reported as p̂ curves/s and inner Laplacian column-actions/s."""
+    import torch
+    import torch.distributed as dist
+    import paper_2601_11338_b200 as wl
+
+    world, rank, local = dist_setup(args.gpus)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = configs.get(args.config if args.config != "c4" else "c3")
+    g, t_gen = load_graph(cfg, world, rank, torch, dist)
+    bounds = wl.partition(g.row_ptr, world)
+    rb, re = int(bounds[rank]), int(bounds[rank + 1])
+    rp = g.row_ptr[rb:re + 1]
+    ci = g.col_idx[g.row_ptr[rb]:g.row_ptr[re]]
+    comm = wl.Comm(rank, world, local) if world > 1 else None
+    probe = wl.Operator(g.n, rp, ci, thetas=[1.0], f=("series", [0.0, 1.0]), row_range=(rb, re), comm=comm,
+                        krylov_dim=2)
+    rho = probe.spectral_radius(k=args.rho_k)
+    probe.close()
+    op = wl.Operator(g.n, rp, ci, thetas=cfg["thetas"][:1], f=("exp", 1.0 / rho), row_range=(rb, re), comm=comm,
+                     krylov_dim=cfg["krylov_dim"])
+    M, k = args.trace_m, args.trace_k
+    ts = np.linspace(0.0, 10.0, 90)
+    Om = torch.from_numpy(np.ascontiguousarray(gg.vectors(g.n, M, 2026)[rb:re])).cuda()
+    ws = op.workspace(M)
+    for _ in range(args.warmup):
+        p, e = op.xnystrace_exp(Om, ts, k, ws=ws)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    stream = torch.cuda.current_stream()
+    l0 = wl.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            p, e = op.xnystrace_exp(Om, ts, k, ws=ws)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = wl.launch_count() - l0
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    wl.profile_enable(True)
+    op.xnystrace_exp(Om, ts, k, ws=ws)
+    torch.cuda.synchronize()
+    wl.profile_enable(False)
+    kernels = {kk: {"ms_per_step": v[0], "launches_per_step": v[1], "share": v[0] / ms}
+               for kk, v in sorted(wl.profile_collect().items(), key=lambda kv: -kv[1][0])}
+    if rank == 0:
+        line = {
+            "metric": "XNysTrace-exp return-probability curves/s", "value": 1e3 / ms, "unit": "curves/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded graphgen)",
+            "config": {"workload": f"{cfg['desc']}; Alg. 1 (poles at inf), M={M} probes, k={k} blocks, 90 t in [0,10], "
+                                   f"theta={cfg['thetas'][0]}, inner k={cfg['krylov_dim']}",
+                       "n": g.n, "nnz": g.nnz, "column_actions_per_s": k * M / (ms / 1e3),
+                       "p_hat": [round(float(x), 6) for x in p[::10]], "e_hat": [float(x) for x in e[::10]]},
+            "roofline": None, "kernels": kernels, "cpu_baseline": None, "e2e": None, "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    op.close()
+    if comm:
+        comm.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def run_extra(args):
     """--markov / --rhoz: measurement lines for NEXT-3 (one step = nsteps Markov steps p_{k+1} = p_k P on the
     config's graph at θ = 0.5, each one φ action of k = 30) and NEXT-4 (one step = ρ(Z_1) by 60 Arnoldi steps on
@@ -691,6 +768,9 @@ def main():
     ap.add_argument("--graph", action="store_true", help="also time the step captured as one CUDA graph")
     ap.add_argument("--diffusion", action="store_true", help="step a9: a full diffusion sweep (default config c3)")
     ap.add_argument("--markov", action="store_true", help="NEXT-3: Markov chain steps")
+    ap.add_argument("--trace", action="store_true", help="NEXT-2: XNysTrace-exp return-probability curve")
+    ap.add_argument("--trace-m", type=int, default=30, help="--trace: probes M")
+    ap.add_argument("--trace-k", type=int, default=8, help="--trace: block Krylov steps k")
     ap.add_argument("--rhoz", action="store_true", help="NEXT-4: rho(Z_1) by Arnoldi on the companion operator")
     ap.add_argument("--solver", default="krylov", choices=["krylov", "cg"],
                     help="cg: the paper's 5.3 resolvent workload by PCG on --config's graph")
@@ -701,6 +781,8 @@ def main():
         run_reference(args)
     elif args.solver == "cg":
         run_cg(args)
+    elif args.trace:
+        run_trace(args)
     elif args.diffusion:
         run_diffusion(args)
     elif args.markov or args.rhoz:

@@ -203,6 +203,37 @@ wl_status wl_diffuse(const wl_operator* op, int32_t theta_index, int32_t nt, con
                      const double* x0, double* X, int64_t ldx, int32_t k_out, wl_workspace* ws,
                      wl_stream stream);
 
+/* ---- average return probability (Alg. 1 XNysTrace-exp) -----------
+ * p_out[s] ≈ p̂_0(t_s) = (1/n) tr exp(-t_s 𝕃_{θ_i}) (eq:average_return_probabilities) and
+ * e_out[s] its error estimate, for i = theta_index:
+ *   1. V_1 R_0 = Ω (Cholesky QR, twice); block Arnoldi with every pole at ∞ (reading R16: the
+ *      polynomial block Krylov space span{Ω, 𝕃Ω, …, 𝕃^{k-1}Ω}; each step one batched wl_apply on M
+ *      columns and block classical Gram–Schmidt applied twice, with cuBLAS DGEMMs and an NCCL
+ *      allreduce of the Gram blocks across ranks);
+ *   2. H_k = V_kᵀ 𝕃 V_k (kM x kM) = Q Λ Qᵀ on the host;
+ *   3. for every t: Y(t) = (1/n) V_k exp(-t H_k) V_kᵀ Ω and XNysTrace(Y(t), Ω) (reading R17), both in
+ *      the kM-dimensional coordinates of V_k.
+ * Omega: device, n_local x M (ld ldo >= M), user row order: the iid isotropic probes (e.g. Gaussian)
+ *        ω_1..ω_M; rows of all ranks together form the global probe block.
+ * times: host, nt >= 1 values >= 0.  p_out, e_out: host, nt values (identical on every rank).
+ * 1 <= M <= the workspace's column batch (wl_workspace_create max_b and opts.max_cols);
+ * 1 <= k and k*M <= min(1024, n_global).  Synchronous.  WL_ENOCONV if the block Krylov space is
+ * exhausted (k*M above the dimension it can reach) or an eigen/Cholesky step fails. */
+wl_status wl_xnystrace_exp(const wl_operator* op, int32_t theta_index, int32_t M, const double* Omega,
+                           int64_t ldo, int32_t k, int32_t nt, const double* times, double* p_out,
+                           double* e_out, wl_workspace* ws, wl_stream stream);
+
+/* The host steps behind it, exported for testing (host buffers, synchronous):
+ * wl_symmetric_eig: A (n x n row-major symmetric) is overwritten by its eigenvectors (column i of A =
+ *   eigenvector i), lam (n) receives the eigenvalues; method 0 = Householder tridiagonalisation +
+ *   implicit QL (the one wl_xnystrace_exp uses), 1 = cyclic Jacobi.
+ * wl_xnystrace_curve: XNysTrace (reading R17) of Y(t) = (1/n) Q diag(e^{-t lam}) W for every t, in
+ *   the coordinates of an orthonormal basis: lam (d) the eigenvalues of the projected 𝕃, W (d x M
+ *   row-major) the probes in its eigen-coordinates, n the global dimension (for 1/n and the shift). */
+wl_status wl_symmetric_eig(int32_t n, double* A, double* lam, int32_t method);
+wl_status wl_xnystrace_curve(int32_t d, int32_t M, double n, const double* lam, const double* W, int32_t nt,
+                             const double* times, double* p_out, double* e_out);
+
 /* ---- discrete-time diffusion: Markov chain (eq:let_there_be_markov P:506-533)
  * P = I - D^{-1} 𝕃_θ with D = diag(t_θ), t_θ = φ_θ 1 (reading R6: "a single evaluation of
  * the underlying matrix function"; Fig. 1's stationary bars are t/Σt), i.e. P = diag(t)^{-1} φ_θ,

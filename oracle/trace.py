@@ -7,13 +7,13 @@ leg may import this module.  Plain fp64 NumPy / SciPy, in the order and notation
 1. Ω = [ω_1 … ω_M], iid isotropic probes.  The caller passes Ω in (Gaussian columns
    from ``graphgen.vectors``); E[ω ωᵀ] = I.
 2. Block Krylov basis V_{k+1} and block Hessenberg pencil (𝓗_k, 𝒦_k) with 𝔏 V_{k+1} 𝒦_k =
-   V_{k+1} 𝓗_k.  Reading R14: every pole ξ_j = ∞ — the
+   V_{k+1} 𝓗_k.  Reading R16: every pole ξ_j = ∞ — the
    definition allows "complex numbers or infinity" and then r_k ≡ 1, 𝒬^block_{k+1} is the
    polynomial block Krylov space span{Ω, 𝔏Ω, …, 𝔏^kΩ} (eq:block-rational-Krylov),
    𝒦_k = [I; 0] and the reduced pencil gives Ĥ_k 𝒦̂_k⁻¹ = H_k, the leading kM × kM block of 𝓗_k.
    AAA pole selection and the shifted inner solves are the next step.
 3. Y(t) = (1/n) V_k exp(-t Ĥ_k 𝒦̂_k⁻¹) V_kᵀ Ω for every t.
-4. p̂(t), ê(t) = XNysTrace(Y(t), Ω) ([XTRACE]).  Reading R15: the leave-one-out Nyström
+4. p̂(t), ê(t) = XNysTrace(Y(t), Ω) ([XTRACE]).  Reading R17: the leave-one-out Nyström
    estimator of the cited work, written as its definition —
        Â_(i) = Y_{-i} (Ω_{-i}ᵀ Y_{-i})⁻¹ Y_{-i}ᵀ        (Nyström from the other M-1 probes)
        est_i = tr Â_(i) + ω_iᵀ (y_i − Â_(i) ω_i)       (exact part + Girard–Hutchinson residual)
@@ -32,7 +32,7 @@ import scipy.linalg as sla
 
 
 def xnystrace(Y: np.ndarray, Omega: np.ndarray) -> tuple[float, float]:
-    """Trace estimate of the symmetric PSD A with Y = A Ω, and its error estimate (reading R15)."""
+    """Trace estimate of the symmetric PSD A with Y = A Ω, and its error estimate (reading R17)."""
     n, M = Omega.shape
     nu = 1e-12 * np.linalg.norm(Y) / np.sqrt(M)
     Yn = Y + nu * Omega
@@ -59,7 +59,7 @@ def xnystrace(Y: np.ndarray, Omega: np.ndarray) -> tuple[float, float]:
 
 
 def block_arnoldi(Lap: np.ndarray, Omega: np.ndarray, k: int):
-    """Block Arnoldi with all poles at ∞ (reading R14): V_{k+1} (n × (k+1)M) orthonormal,
+    """Block Arnoldi with all poles at ∞ (reading R16): V_{k+1} (n × (k+1)M) orthonormal,
     𝓗_k ((k+1)M × kM) block upper Hessenberg with Lap V_k = V_{k+1} 𝓗_k, and R_0 with
     Ω = V_1 R_0.  Block Gram–Schmidt, applied twice (the orthogonalisation the paper leaves to
     [MR4082482]; it changes rounding only)."""

@@ -11,6 +11,8 @@ from .walklap import (  # noqa: F401
     Workspace,
     halo_plan,
     hessenberg_eigvals,
+    symmetric_eig,
+    xnystrace_curve,
     launch_count,
     load,
     partition,

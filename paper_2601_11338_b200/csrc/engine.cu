@@ -14,6 +14,7 @@
 #include "walklap.h"
 #include "wl_internal.cuh"
 
+#include <cublas_v2.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -1420,6 +1421,186 @@ wl_status wl_hessenberg_eigvals(int32_t n, const double* H, double* wr, double* 
     if (!hessenberg_eigvals(a, n, r, i)) throw Error(WL_ENOCONV, "Hessenberg QR did not converge");
     std::copy(r.begin(), r.end(), wr);
     std::copy(i.begin(), i.end(), wi);
+  });
+}
+
+namespace wl {
+namespace {
+void cublas_check(cublasStatus_t st, const char* what) {
+  if (st != CUBLAS_STATUS_SUCCESS) throw Error(WL_ECUDA, std::string("cuBLAS: ") + what);
+}
+struct Cublas {
+  cublasHandle_t h = nullptr;
+  explicit Cublas(cudaStream_t s) {
+    cublas_check(cublasCreate(&h), "create");
+    cublas_check(cublasSetStream(h, s), "set stream");
+  }
+  ~Cublas() { if (h) cublasDestroy(h); }
+};
+// Column-major views of the row-major n x cols blocks the engine uses: X (n x cols, ld) is Xᶜ
+// (cols x n, ld).  gram: C (p x q, col-major, ld p) = X[:, :p]ᵀ Y[:, :q].
+void gram(cublasHandle_t h, int p, int q, int64_t n, const double* X, int64_t ldx, const double* Y, int64_t ldy,
+          double* C) {
+  const double one = 1.0, zero = 0.0;
+  cublas_check(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, p, q, (int)n, &one, X, (int)ldx, Y, (int)ldy, &zero, C, p),
+               "gram");
+}
+// Y[:, :q] = beta Y + alpha X[:, :p] C,  C p x q col-major (ld p)
+void axpy_block(cublasHandle_t h, int p, int q, int64_t n, double alpha, const double* X, int64_t ldx,
+                const double* C, double beta, double* Y, int64_t ldy) {
+  cublas_check(cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, q, (int)n, p, &alpha, C, p, X, (int)ldx, &beta, Y, (int)ldy),
+               "update");
+}
+}  // namespace
+}  // namespace wl
+
+// Block Arnoldi with poles at ∞ (reading R16) on 𝔏 = 𝕃_{θ_i}, then XNysTrace in the projected space.
+wl_status wl_xnystrace_exp(const wl_operator* op, int32_t theta_index, int32_t M, const double* Omega,
+                           int64_t ldo, int32_t k, int32_t nt, const double* times, double* p_out, double* e_out,
+                           wl_workspace* ws, wl_stream stream) {
+  return guarded([&] {
+    if (!op || !ws || ws->op != op) throw Error(WL_EINVAL, "operator/workspace mismatch");
+    if (theta_index < 0 || theta_index >= op->n_theta) throw Error(WL_EINVAL, "theta_index out of range");
+    if (M < 1 || M > ws->Bmax) throw Error(WL_EINVAL, "M must be in [1, workspace column batch]");
+    if (k < 1 || (int64_t)k * M > std::min<int64_t>(1024, op->n_global))
+      throw Error(WL_EINVAL, "need 1 <= k and k*M <= min(1024, n)");
+    if (nt < 1 || !times || !p_out || !e_out) throw Error(WL_EINVAL, "bad output arguments");
+    for (int i = 0; i < nt; ++i)
+      if (!(times[i] >= 0.0)) throw Error(WL_EINVAL, "times must be >= 0");
+    if (op->n_loc > 0) check_block(Omega, ldo, M, "Omega");
+    DeviceGuard dg(op->device);
+    cudaStream_t s = S_(stream);
+    const int64_t n = op->n_loc;
+    const int P = (k + 1) * M, d = k * M;
+    DArr<double> V, Wb, W2, Cd, Rd;
+    V.alloc(std::max<int64_t>(1, n) * P);
+    Wb.alloc(std::max<int64_t>(1, n) * M);
+    W2.alloc(std::max<int64_t>(1, n) * M);
+    Cd.alloc((size_t)P * M);
+    Rd.alloc((size_t)M * M);
+    Cublas cb(s);
+    std::vector<double> H((size_t)d * d, 0.0), R0((size_t)M * M), Ch((size_t)P * M), G((size_t)M * M);
+    // Ω in internal row order
+    if (n > 0) {
+      if (op->perm.p) pack_rows(Omega, ldo, op->perm.p, n, M, Wb.p, s);
+      else WL_CUDA(cudaMemcpy2DAsync(Wb.p, sizeof(double) * M, Omega, sizeof(double) * ldo, sizeof(double) * M, n,
+                                     cudaMemcpyDeviceToDevice, s));
+    }
+    // dst (ld P) R = Wb (ld M) by Cholesky QR applied twice; R (M x M upper, col-major) returned
+    auto cholqr = [&](double* dst, std::vector<double>& R) {
+      std::vector<double> Rt((size_t)M * M, 0.0);
+      for (int i = 0; i < M; ++i) Rt[(size_t)i * M + i] = 1.0;
+      for (int pass = 0; pass < 2; ++pass) {
+        const double* src = pass == 0 ? Wb.p : W2.p;
+        gram(cb.h, M, M, n, src, M, src, M, Rd.p);
+        allreduce(op, Rd.p, (size_t)M * M, s);
+        WL_CUDA(cudaMemcpyAsync(G.data(), Rd.p, sizeof(double) * M * M, cudaMemcpyDeviceToHost, s));
+        WL_CUDA(cudaStreamSynchronize(s));
+        // G = Uᵀ U (U upper, col-major): Cholesky
+        std::vector<double> U((size_t)M * M, 0.0), Ui((size_t)M * M, 0.0);
+        for (int j = 0; j < M; ++j) {
+          for (int i = 0; i <= j; ++i) {
+            double v = G[(size_t)j * M + i];
+            for (int q = 0; q < i; ++q) v -= U[(size_t)i * M + q] * U[(size_t)j * M + q];
+            if (i == j) {
+              if (!(v > 1e-28 * std::max(1.0, G[0]))) throw Error(WL_ENOCONV, "block Krylov space exhausted (k*M too large for this graph)");
+              U[(size_t)j * M + j] = std::sqrt(v);
+            } else {
+              U[(size_t)j * M + i] = v / U[(size_t)i * M + i];
+            }
+          }
+        }
+        // U⁻¹ (upper) by back substitution, column by column
+        for (int j = 0; j < M; ++j) {
+          Ui[(size_t)j * M + j] = 1.0 / U[(size_t)j * M + j];
+          for (int i = j - 1; i >= 0; --i) {
+            double v = 0.0;
+            for (int q = i + 1; q <= j; ++q) v += U[(size_t)q * M + i] * Ui[(size_t)j * M + q];
+            Ui[(size_t)j * M + i] = -v / U[(size_t)i * M + i];
+          }
+        }
+        WL_CUDA(cudaMemcpyAsync(Rd.p, Ui.data(), sizeof(double) * M * M, cudaMemcpyHostToDevice, s));
+        // out = src U⁻¹  (Uinv is M x M col-major: exactly the "C" operand of axpy_block)
+        double* out = pass == 0 ? W2.p : dst;
+        const int64_t ldout = pass == 0 ? M : P;
+        axpy_block(cb.h, M, M, n, 1.0, src, M, Rd.p, 0.0, out, ldout);
+        // Rt <- U Rt
+        std::vector<double> T((size_t)M * M, 0.0);
+        for (int c = 0; c < M; ++c)
+          for (int r = 0; r < M; ++r) {
+            double v = 0.0;
+            for (int q = r; q < M; ++q) v += U[(size_t)q * M + r] * Rt[(size_t)c * M + q];
+            T[(size_t)c * M + r] = v;
+          }
+        Rt.swap(T);
+        WL_CUDA(cudaStreamSynchronize(s));  // Ui host buffer reused next pass
+      }
+      R = Rt;
+    };
+    cholqr(V.p, R0);
+    std::vector<double> Rj;
+    for (int j = 0; j < k; ++j) {
+      // W = 𝕃_θ V_j  (one batched Laplacian action on M columns, internal order)
+      run_chunk(op, ws, 1, V.p + (size_t)j * M, P, M, theta_index * M, M, Wb.p, M, s, false);
+      const int pj = (j + 1) * M;
+      for (int pass = 0; pass < 2; ++pass) {  // block classical Gram–Schmidt, twice
+        gram(cb.h, pj, M, n, V.p, P, Wb.p, M, Cd.p);
+        allreduce(op, Cd.p, (size_t)pj * M, s);
+        axpy_block(cb.h, pj, M, n, -1.0, V.p, P, Cd.p, 1.0, Wb.p, M);
+        WL_CUDA(cudaMemcpyAsync(Ch.data(), Cd.p, sizeof(double) * pj * M, cudaMemcpyDeviceToHost, s));
+        WL_CUDA(cudaStreamSynchronize(s));
+        for (int c = 0; c < M; ++c)
+          for (int r = 0; r < pj; ++r)
+            if (r < d) H[(size_t)r * d + j * M + c] += Ch[(size_t)c * pj + r];
+      }
+      if (j + 1 < k) {
+        cholqr(V.p + (size_t)(j + 1) * M, Rj);
+        for (int c = 0; c < M; ++c)
+          for (int r = 0; r < M; ++r) H[(size_t)((j + 1) * M + r) * d + j * M + c] = Rj[(size_t)c * M + r];
+      }
+    }
+    // symmetric 𝕃 ⇒ H_k symmetric up to rounding
+    for (int r = 0; r < d; ++r)
+      for (int c = r + 1; c < d; ++c) {
+        const double v = 0.5 * (H[(size_t)r * d + c] + H[(size_t)c * d + r]);
+        H[(size_t)r * d + c] = H[(size_t)c * d + r] = v;
+      }
+    std::vector<double> lam, Q;
+    if (!sym_eig_tridiag_ql(H, d, lam)) throw Error(WL_ENOCONV, "symmetric QL iteration did not converge");
+    Q.swap(H);  // column a = eigenvector a
+    // W = Qᵀ [R_0; 0]  (d x M row-major)
+    std::vector<double> Wc((size_t)d * M, 0.0);
+    for (int a = 0; a < d; ++a)
+      for (int c = 0; c < M; ++c) {
+        double v = 0.0;
+        for (int r = 0; r <= c; ++r) v += Q[(size_t)r * d + a] * R0[(size_t)c * M + r];
+        Wc[(size_t)a * M + c] = v;
+      }
+    if (!xnystrace_curve(lam, Wc, d, M, (double)op->n_global, times, nt, p_out, e_out))
+      throw Error(WL_ENOCONV, "XNysTrace: leave-one-out Gram matrix not positive definite");
+  });
+}
+
+wl_status wl_symmetric_eig(int32_t n, double* A, double* lam, int32_t method) {
+  return guarded([&] {
+    if (n < 1 || !A || !lam || method < 0 || method > 1) throw Error(WL_EINVAL, "bad arguments");
+    std::vector<double> a(A, A + (size_t)n * n), w, Q;
+    bool ok = method == 0 ? sym_eig_tridiag_ql(a, n, w) : sym_eig_jacobi(a, n, w, Q);
+    if (!ok) throw Error(WL_ENOCONV, "symmetric eigensolver did not converge");
+    if (method == 1) a.swap(Q);
+    std::copy(a.begin(), a.end(), A);
+    std::copy(w.begin(), w.end(), lam);
+  });
+}
+
+wl_status wl_xnystrace_curve(int32_t d, int32_t M, double n, const double* lam, const double* W, int32_t nt,
+                             const double* times, double* p_out, double* e_out) {
+  return guarded([&] {
+    if (d < 1 || M < 1 || !(n > 0) || !lam || !W || nt < 1 || !times || !p_out || !e_out)
+      throw Error(WL_EINVAL, "bad arguments");
+    std::vector<double> l(lam, lam + d), w(W, W + (size_t)d * M);
+    if (!xnystrace_curve(l, w, d, M, n, times, nt, p_out, e_out))
+      throw Error(WL_ENOCONV, "XNysTrace: leave-one-out Gram matrix not positive definite");
   });
 }
 

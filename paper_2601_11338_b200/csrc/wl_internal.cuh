@@ -199,6 +199,12 @@ void markov_scale(const double* p, const double* tprime, int64_t ldt, int tcol, 
 // eigenvalues of a small real upper Hessenberg matrix (host; eig.cu). H row-major n x n, overwritten.
 bool hessenberg_eigvals(std::vector<double>& H, int n, std::vector<double>& wr, std::vector<double>& wi);
 
+// XNysTrace-exp host side (trace.cu)
+bool sym_eig_jacobi(std::vector<double>& A, int d, std::vector<double>& lam, std::vector<double>& Q);
+bool sym_eig_tridiag_ql(std::vector<double>& A, int d, std::vector<double>& lam);
+bool xnystrace_curve(const std::vector<double>& lam, const std::vector<double>& W, int d, int M, double n,
+                     const double* times, int nt, double* p_out, double* e_out);
+
 // outer Lanczos helpers (diffusion)
 void lanczos_combine(const double* Q, int64_t stride, int m, int64_t n, const double* Y, int nt,
                      double scale, double* X, int64_t ldx, const int32_t* perm, cudaStream_t s);

@@ -78,7 +78,10 @@ def load():
         "wl_spectral_radius": ([vp, i32, ctypes.POINTER(dbl), vp], ctypes.c_int),
         "wl_spectral_radius_z": ([vp, i32, i32, ctypes.POINTER(dbl), vp], ctypes.c_int),
         "wl_markov": ([vp, i32, i32, vp, vp, i64, vp, vp], ctypes.c_int),
+        "wl_xnystrace_exp": ([vp, i32, i32, vp, i64, i32, i32, vp, vp, vp, vp, vp], ctypes.c_int),
         "wl_hessenberg_eigvals": ([i32, vp, vp, vp], ctypes.c_int),
+        "wl_symmetric_eig": ([i32, vp, vp, i32], ctypes.c_int),
+        "wl_xnystrace_curve": ([i32, i32, dbl, vp, vp, i32, vp, vp, vp], ctypes.c_int),
         "wl_profile_enable": ([i32], None),
         "wl_profile_collect": ([], ctypes.c_int),
         "wl_profile_count": ([], i32),
@@ -155,6 +158,26 @@ def hessenberg_eigvals(H: np.ndarray) -> np.ndarray:
     wr, wi = np.empty(n), np.empty(n)
     _check(load().wl_hessenberg_eigvals(n, H.ctypes.data, wr.ctypes.data, wi.ctypes.data))
     return wr + 1j * wi
+
+
+def symmetric_eig(A: np.ndarray, method: int = 0):
+    """Eigenvalues and eigenvectors (columns) of a symmetric matrix by the library's host solver
+    (wl_symmetric_eig: 0 = tridiagonal QL, 1 = Jacobi)."""
+    A = np.array(A, dtype=np.float64, order="C", copy=True)
+    lam = np.empty(A.shape[0])
+    _check(load().wl_symmetric_eig(A.shape[0], A.ctypes.data, lam.ctypes.data, method))
+    return lam, A
+
+
+def xnystrace_curve(lam, W, n: float, times):
+    """The library's host XNysTrace (wl_xnystrace_curve) on eigen-coordinates lam (d), W (d x M)."""
+    lam = np.ascontiguousarray(lam, dtype=np.float64)
+    W = np.ascontiguousarray(W, dtype=np.float64)
+    times = np.ascontiguousarray(np.atleast_1d(times), dtype=np.float64)
+    p, e = np.empty(len(times)), np.empty(len(times))
+    _check(load().wl_xnystrace_curve(W.shape[0], W.shape[1], float(n), lam.ctypes.data, W.ctypes.data,
+                                     len(times), times.ctypes.data, p.ctypes.data, e.ctypes.data))
+    return p, e
 
 
 def _stream_handle(stream):
@@ -371,6 +394,20 @@ class Operator:
         _check(load().wl_markov(self.handle, theta_index, nsteps, ctypes.c_void_p(p0.data_ptr()),
                                 ctypes.c_void_p(out2.data_ptr()), ldp, ws.handle, _stream_handle(stream)))
         return out
+
+    def xnystrace_exp(self, omega, times, k, theta_index=0, ws=None, stream=None):
+        """Average return probability p̂_0(t) ≈ (1/n) tr exp(-t 𝕃_θ) and its error estimate for every t
+        (Alg. 1 XNysTrace-exp with poles at ∞; wl_xnystrace_exp).  omega: (n_local, M) CUDA float64 probes."""
+        times = np.ascontiguousarray(np.atleast_1d(times), dtype=np.float64)
+        M = omega.shape[1] if omega.dim() == 2 else 1
+        om, ldo = _block(omega, M, "omega")
+        p = np.empty(len(times))
+        e = np.empty(len(times))
+        ws = ws or self.workspace(M)
+        _check(load().wl_xnystrace_exp(self.handle, theta_index, M, ctypes.c_void_p(om.data_ptr()), ldo, k,
+                                       len(times), times.ctypes.data, p.ctypes.data, e.ctypes.data, ws.handle,
+                                       _stream_handle(stream)))
+        return p, e
 
     def spectral_radius_z(self, theta_index: int = 0, k: int = 60, stream=None) -> float:
         """ρ(Z_θ) of the companion operator by k Arnoldi steps on Z (wl_spectral_radius_z)."""

@@ -113,3 +113,38 @@ def test_hessenberg_eigvals_closed_forms(lib):
     T = np.triu(np.arange(1.0, 26.0).reshape(5, 5))
     assert np.allclose(np.sort(wl.hessenberg_eigvals(T).real), [1.0, 7.0, 13.0, 19.0, 25.0])
     assert np.allclose(np.sort(wl.hessenberg_eigvals(np.array([[2.0, 1.0], [1.0, 2.0]])).real), [1.0, 3.0])
+
+
+@pytest.mark.parametrize("method", [0, 1])
+def test_symmetric_eig_matches_lapack(lib, method):
+    """The host eigensolvers behind wl_xnystrace_exp (trace.cu) against LAPACK (numpy.linalg.eigh):
+    eigenvalues, residual ‖A z − λ z‖ and orthonormality, including repeated eigenvalues."""
+    import paper_2601_11338_b200 as wl
+    rng = np.random.default_rng(3)
+    for n in [1, 2, 3, 7, 24, 61, 130]:
+        G = rng.standard_normal((n, n))
+        Qr = np.linalg.qr(rng.standard_normal((n, n)))[0]
+        for A in (G + G.T, (Qr * np.resize([1.0, 1.0, 2.0, 2.0], n)) @ Qr.T):
+            lam, Z = wl.symmetric_eig(A, method)
+            assert np.allclose(np.sort(lam), np.linalg.eigvalsh(A), atol=1e-12 * max(1, np.abs(A).max()))
+            assert np.abs(A @ Z - Z * lam).max() <= 1e-12 * max(1, np.abs(A).max()) * n
+            assert np.abs(Z.T @ Z - np.eye(n)).max() <= 1e-12 * n
+
+
+def test_xnystrace_curve_matches_oracle(lib):
+    """The host estimator behind wl_xnystrace_exp against oracle/trace.xnystrace, with exact Y(t):
+    the projected space is the whole space (d = n) and lam, Q come from LAPACK."""
+    import paper_2601_11338_b200 as wl
+    import scipy.linalg as sla
+    import graphgen as gg
+    from oracle import dense as D
+    from oracle import trace as T
+    L = D.standard_laplacian(D.adjacency(gg.karate()))
+    lam, Q = np.linalg.eigh(L)
+    ts = np.linspace(0.0, 10.0, 30)
+    for M in (1, 2, 5, 12):
+        Om = gg.vectors(34, M, 40 + M)
+        p, e = wl.xnystrace_curve(lam, Q.T @ Om, 34, ts)
+        ref = np.array([T.xnystrace(sla.expm(-t * L) @ Om / 34, Om) for t in ts])
+        assert np.max(np.abs(p - ref[:, 0]) / np.abs(ref[:, 0])) < 1e-9, M
+        assert np.max(np.abs(e - ref[:, 1])) <= 1e-9 * np.max(ref[:, 0]) + 1e-7 * np.max(ref[:, 1]), M

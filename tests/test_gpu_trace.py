@@ -1,0 +1,83 @@
+"""GPU parity of XNysTrace-exp (Alg. 1 with poles at ∞) vs oracle/trace.py.
+
+Both sides take the same seeded Gaussian probes Ω (graphgen.vectors) and the same k; the oracle
+runs block Arnoldi and the estimator on the dense 𝕃 from oracle/dense.py, the GPU path runs k
+batched Laplacian actions through the C ABI (wl_xnystrace_exp).  Rounding differs (Gram–Schmidt
+order, Jacobi vs scaling-and-squaring expm), so the estimates agree to 1e-8 relative — the
+estimator's leave-one-out Gram matrices have condition numbers up to ~1/ν ≈ 1e12 at large t —
+far below its own statistical error (ê, 1e-3..1e-1 here).
+"""
+import numpy as np
+import pytest
+
+import graphgen as gg
+from oracle import coeffs as C
+from oracle import dense as D
+from oracle import trace as T
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def wl():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2601_11338_b200 as wl
+    from paper_2601_11338_b200 import build
+    build.build()
+    wl.load()
+    return wl
+
+
+def _case(wl, g, thetas, f, ti, M, k, ts, seed, **kw):
+    A = D.adjacency(g)
+    fo = {"exp": C.exp, "resolvent": C.resolvent}[f[0]](f[1])
+    Lap = D.laplacian(A, 1.0 - thetas[ti], fo)
+    Om = gg.vectors(g.n, M, seed)
+    op = wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=thetas, f=f, **kw)
+    p, e = op.xnystrace_exp(torch.from_numpy(Om).cuda(), ts, k, theta_index=ti)
+    op.close()
+    po, eo = T.xnystrace_exp(Lap, Om, k, ts)
+    return p, e, po, eo
+
+
+# karate's 𝕃 has a 4-fold eigenvalue, so its block Krylov spaces stop growing before kM = 34: kM ≤ 24
+@pytest.mark.parametrize("M,k", [(1, 6), (4, 6), (8, 3)])
+def test_karate_exp_vs_oracle(wl, M, k):
+    g = gg.karate()
+    rA = D.rho_A(D.adjacency(g))
+    ts = np.linspace(0.0, 10.0, 30)
+    p, e, po, eo = _case(wl, g, [0.0, 0.5, 1.0], ("exp", 1.0 / rA), 1, M, k, ts, 7 + M)
+    assert np.max(np.abs(p - po) / np.abs(po)) < 1e-8
+    assert np.max(np.abs(e - eo)) < 1e-8 * np.max(np.abs(po)) + 1e-6 * np.max(eo)
+
+
+def test_fig4b_shape_nbt_resolvent(wl):
+    """Fig. 4(b) workload: 𝕃_1((1-αx)^{-1}) on karate, α = 1/(1+ρ(Z)), M = 3 (caption P:1260)."""
+    g = gg.karate()
+    alpha = 1.0 / (1.0 + D.rho_Z(D.adjacency(g), 1.0))
+    ts = np.linspace(0.0, 10.0, 30)
+    p, e, po, eo = _case(wl, g, [0.0], ("resolvent", alpha), 0, 3, 10, ts, 99, krylov_dim=64)  # θ = 0: NBT
+    assert np.max(np.abs(p - po) / np.abs(po)) < 1e-8
+
+
+def test_multi_tile_graph(wl):
+    """A Barabási–Albert graph spanning many SpMM tiles and a ragged tail (n = 1201)."""
+    g = gg.barabasi_albert(1201, 3, 5)
+    rA = D.rho_A(D.adjacency(g))
+    ts = np.linspace(0.0, 4.0, 9)
+    p, e, po, eo = _case(wl, g, [0.7], ("exp", 1.0 / rA), 0, 6, 6, ts, 3)
+    assert np.max(np.abs(p - po) / np.abs(po)) < 1e-8
+    assert p[0] > 0 and np.all(e >= 0)
+
+
+def test_argument_errors(wl):
+    g = gg.karate()
+    op = wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=[1.0], f=("exp", 0.1))
+    Om = torch.from_numpy(gg.vectors(34, 4, 1)).cuda()
+    with pytest.raises(Exception):
+        op.xnystrace_exp(Om, [0.0, 1.0], 9)          # k*M = 36 > n = 34
+    with pytest.raises(Exception):
+        op.xnystrace_exp(Om, [-1.0], 2)              # negative time
+    op.close()

@@ -1,4 +1,4 @@
-"""Pins for oracle/trace.py (Alg. 1, XNysTrace-exp; readings R14/R15 in DESIGN.md §3).
+"""Pins for oracle/trace.py (Alg. 1, XNysTrace-exp; readings R16/R17 in DESIGN.md §3).
 
 Each pin fixes the oracle against something other than itself:
 * low-rank exactness of the Nyström estimator (rank(A) < M-1 ⇒ Â_(i) = A, every est_i = tr A);
