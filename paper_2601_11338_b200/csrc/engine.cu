@@ -188,8 +188,12 @@ struct wl_workspace {
   int kout_alloc = 0;
   DArr<double> oQ, ow, oH, on0, oref, osums1, ocoef_v, ocoef_s, otau, oY, oscratch;
   DArr<int> okeff;
+  // XNysTrace-exp (wl_xnystrace_exp): block basis, block, temp block, Gram blocks; cuBLAS handle
+  DArr<double> trV, trW, trW2, trC, trR;
+  cublasHandle_t cublas = nullptr;
   ~wl_workspace() {
     if (cg_flags_host) cudaFreeHost(cg_flags_host);
+    if (cublas) cublasDestroy(cublas);
   }
 };
 
@@ -1429,14 +1433,6 @@ namespace {
 void cublas_check(cublasStatus_t st, const char* what) {
   if (st != CUBLAS_STATUS_SUCCESS) throw Error(WL_ECUDA, std::string("cuBLAS: ") + what);
 }
-struct Cublas {
-  cublasHandle_t h = nullptr;
-  explicit Cublas(cudaStream_t s) {
-    cublas_check(cublasCreate(&h), "create");
-    cublas_check(cublasSetStream(h, s), "set stream");
-  }
-  ~Cublas() { if (h) cublasDestroy(h); }
-};
 // Column-major views of the row-major n x cols blocks the engine uses: X (n x cols, ld) is Xᶜ
 // (cols x n, ld).  gram: C (p x q, col-major, ld p) = X[:, :p]ᵀ Y[:, :q].
 void gram(cublasHandle_t h, int p, int q, int64_t n, const double* X, int64_t ldx, const double* Y, int64_t ldy,
@@ -1472,13 +1468,16 @@ wl_status wl_xnystrace_exp(const wl_operator* op, int32_t theta_index, int32_t M
     cudaStream_t s = S_(stream);
     const int64_t n = op->n_loc;
     const int P = (k + 1) * M, d = k * M;
-    DArr<double> V, Wb, W2, Cd, Rd;
+    // buffers and the cuBLAS handle live in the workspace (grown on demand, reused across calls)
+    DArr<double>&V = ws->trV, &Wb = ws->trW, &W2 = ws->trW2, &Cd = ws->trC, &Rd = ws->trR;
     V.alloc(std::max<int64_t>(1, n) * P);
     Wb.alloc(std::max<int64_t>(1, n) * M);
     W2.alloc(std::max<int64_t>(1, n) * M);
     Cd.alloc((size_t)P * M);
     Rd.alloc((size_t)M * M);
-    Cublas cb(s);
+    if (!ws->cublas) cublas_check(cublasCreate(&ws->cublas), "create");
+    cublas_check(cublasSetStream(ws->cublas, s), "set stream");
+    struct { cublasHandle_t h; } cb{ws->cublas};
     std::vector<double> H((size_t)d * d, 0.0), R0((size_t)M * M), Ch((size_t)P * M), G((size_t)M * M);
     // Ω in internal row order
     if (n > 0) {
