@@ -48,7 +48,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
            "-I", os.path.join(ROOT, "include"), "-I", inc,
            *os.environ.get("WL_EXTRA_NVCC", "").split(),  # developer experiments (e.g. -DWL_SPMV_HINTS=1)
            *sources(), "-o", tmp,
-           "-L", libdir, "-l:libnccl.so.2", f"-Xlinker", f"-rpath={libdir}", "-lcublas"]
+           "-L", libdir, "-l:libnccl.so.2", f"-Xlinker", f"-rpath={libdir}", "-L/usr/local/cuda/lib64", "-lcublas", "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
