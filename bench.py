@@ -203,6 +203,7 @@ def run_walklap(args):
     thetas = cfg["thetas"]
     K = args.krylov if args.krylov else cfg["krylov_dim"]
     op = wl.Operator(g.n, rp, ci, thetas=thetas, f=("exp", beta), row_range=(rb, re), comm=comm, krylov_dim=K,
+                     relabel=args.relabel,
                      max_cols=args.max_cols)
     torch.cuda.synchronize()
     t_create = time.time() - t0
@@ -411,7 +412,7 @@ def run_cg(args):
     rho = probe.spectral_radius_z(0, k=args.rho_k)  # ρ(Z_1) by Arnoldi on Z (NEXT-4), as §5.3 prescribes
     probe.close()
     alphas = [a / rho for a in np.logspace(-3, -0.5, 4)]
-    ops = [wl.Operator(g.n, rp, ci, variant="nbt", f=("resolvent", a), row_range=(rb, re), comm=comm,
+    ops = [wl.Operator(g.n, rp, ci, variant="nbt", f=("resolvent", a), row_range=(rb, re), comm=comm, relabel=args.relabel,
                        solver="cg", cg_tol=1e-9) for a in alphas]
     torch.cuda.synchronize()
     t_create = time.time() - t0
@@ -534,6 +535,7 @@ def run_diffusion(args):
     rho = probe.spectral_radius(k=args.rho_k)
     probe.close()
     op = wl.Operator(g.n, rp, ci, thetas=cfg["thetas"], f=("exp", 1.0 / rho), row_range=(rb, re), comm=comm,
+                     relabel=args.relabel,
                      krylov_dim=cfg["krylov_dim"])
     torch.cuda.synchronize()
     t_create = time.time() - t0
@@ -620,6 +622,7 @@ def run_trace(args):
     rho = probe.spectral_radius(k=args.rho_k)
     probe.close()
     op = wl.Operator(g.n, rp, ci, thetas=cfg["thetas"][:1], f=("exp", 1.0 / rho), row_range=(rb, re), comm=comm,
+                     relabel=args.relabel,
                      krylov_dim=cfg["krylov_dim"])
     M, k = args.trace_m, args.trace_k
     ts = np.linspace(0.0, 10.0, 90)
@@ -768,6 +771,8 @@ def main():
     ap.add_argument("--graph", action="store_true", help="also time the step captured as one CUDA graph")
     ap.add_argument("--diffusion", action="store_true", help="step a9: a full diffusion sweep (default config c3)")
     ap.add_argument("--markov", action="store_true", help="NEXT-3: Markov chain steps")
+    ap.add_argument("--relabel", type=int, default=1, choices=[0, 1],
+                    help="degree-sorted row relabelling inside the operator (opts.relabel)")
     ap.add_argument("--trace", action="store_true", help="NEXT-2: XNysTrace-exp return-probability curve")
     ap.add_argument("--trace-m", type=int, default=30, help="--trace: probes M")
     ap.add_argument("--trace-k", type=int, default=8, help="--trace: block Krylov steps k")

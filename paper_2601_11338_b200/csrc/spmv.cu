@@ -275,6 +275,22 @@ __global__ void __launch_bounds__(kThreads) spmv_small_batched_kernel(SpmvArgs a
   }
 }
 
+// ---- small rows, one column (B = 1: diffusion, CG, Markov): one thread per row ----
+// At B = 1 a 32-row batch is one row per lane, so the batched kernel's staging buys nothing and its
+// per-batch chain (rowptr -> col -> smem -> gather) plus warp syncs dominates.  A thread per row
+// keeps the same three dependent loads with ~8x the rows in flight per SM.
+template <bool HALO>
+__global__ void __launch_bounds__(kThreads) spmv_small_row1_kernel(SpmvArgs a) {
+  if (a.active && *a.active == 0) return;
+  const int i = blockIdx.x * kThreads + threadIdx.x;
+  if (i >= a.n_small) return;
+  Ctx<4, HALO> ctx{a, 0, a.g0 ? a.g0[0] : 0.0, a.g1 ? a.g1[0] : 0.0, a.scale ? a.scale[0] : 1.0,
+                   a.y, a.yh, (int)a.ldy, (int)a.ldh};
+  const int r = a.small_first + i;
+  const int z0 = __ldg(a.rowptr + r), z1 = __ldg(a.rowptr + r + 1);
+  ctx.write(r, z1 - z0, ctx.strided_sum(z0, z1, 0, 1));
+}
+
 size_t small_batched_smem(int B) {
   return (size_t)kWarps * ((32 * kSmallMax + 40) * sizeof(int) + 32 * B * sizeof(double));
 }
@@ -308,7 +324,15 @@ void spmv(const SpmvArgs& a0, cudaStream_t s) {
   // small rows with contiguous ids (x rows contiguous too): the batched kernel takes them
   static const bool batched_on = [] { const char* v = getenv("WL_SPMV_BATCHED"); return v ? atoi(v) != 0 : true; }();
   const bool batched = batched_on && a.small_first >= 0 && a.n_small > 0 && (a.x == nullptr || a.ldx == a.B);
+  static const bool row1_on = [] { const char* v = getenv("WL_SPMV_ROW1"); return v ? atoi(v) != 0 : true; }();
   auto go_small = [&]() {
+    if (a.B == 1 && row1_on) {
+      const int g = (a.n_small + kThreads - 1) / kThreads;
+      if (halo) spmv_small_row1_kernel<true><<<g, kThreads, 0, s>>>(a);
+      else spmv_small_row1_kernel<false><<<g, kThreads, 0, s>>>(a);
+      WL_CUDA(cudaGetLastError());
+      return;
+    }
     auto kern = halo ? spmv_small_batched_kernel<8, true> : spmv_small_batched_kernel<8, false>;
     const size_t smem = small_batched_smem(a.B);
     static bool attr[2] = {false, false};
