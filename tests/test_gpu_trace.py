@@ -81,3 +81,26 @@ def test_argument_errors(wl):
     with pytest.raises(Exception):
         op.xnystrace_exp(Om, [-1.0], 2)              # negative time
     op.close()
+
+
+def test_full_c3_fig7_shape(wl):
+    """Full C3 (n ≈ 2e6 road-like grid, NBT θ = 0) in the Fig. 7 shape (M = 30, 90 t-points), as
+    bench.py --trace runs it.  At t = 0, Y(0) = Ω/n exactly (exp(0) = I), so p̂(0), ê(0) depend only on Ω
+    and the oracle's XNysTrace computes them at full size; the curve must decrease like (1/n)tr e^{-t𝕃}
+    (every eigenvalue of 𝕃 is ≥ 0) within its error estimate, and stay above 1/n."""
+    from graphgen import configs
+    cfg = configs.get("c3")
+    g = cfg["make"]()
+    probe = wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=[1.0], f=("series", [0.0, 1.0]), krylov_dim=2)
+    rho = probe.spectral_radius(k=60)
+    probe.close()
+    op = wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=[0.0], f=("exp", 1.0 / rho), krylov_dim=30)
+    Om = gg.vectors(g.n, 30, 2026)
+    ts = np.linspace(0.0, 10.0, 90)
+    p, e = op.xnystrace_exp(torch.from_numpy(Om).cuda(), ts, 8)
+    op.close()
+    p0, e0 = T.xnystrace(Om / g.n, Om)
+    assert abs(p[0] - p0) <= 1e-9 * abs(p0)
+    assert abs(e[0] - e0) <= 1e-6 * e0
+    assert np.all(np.diff(p) <= 3 * (e[1:] + e[:-1]))
+    assert np.all(p > 1.0 / g.n)
