@@ -67,7 +67,10 @@ size_t toar_state_doubles(int K) {
 // Outputs: coef_y[o*B + c], coef_u[(o*coef_ld + i)*B + c] for the TOAR update pass:
 //   j = -1: o = 0 -> u_1;   j >= 0: o = 0 -> u_m, 1 -> x_{j+1} = bottom(q̂_{j+1}), 2 -> z_{j+1} = top.
 // Gram-Schmidt in coefficient space is classical (all projections of a pass at once), done twice.
-constexpr int kCoefThreads = 128;
+#ifndef WL_COEF_THREADS
+#define WL_COEF_THREADS 1024  // C3 diffusion sweep: 128 -> 1024 threads, toar_coeffs 119 -> 111 ms
+#endif
+constexpr int kCoefThreads = WL_COEF_THREADS;
 constexpr int kMaxVecPerLaunchCoef = kMaxKrylov + 2;  // dot-pass outputs per column: 2(m-1)+3, m <= K+2
 constexpr int kV = kMaxKrylov + 4;  // coefficient vector capacity (>= K + 3)
 
@@ -77,21 +80,30 @@ __device__ inline double wsum(double v) {
 }
 __device__ inline double diag_or_one(double d) { return d != 0.0 ? d : 1.0; }
 
-// x = LI v (LI lower triangular, rows < m), a thread per row; caller syncs
-__device__ void li_mv(const double* LI, int M, int m, const double* v, double* x) {
-  for (int i = threadIdx.x; i < m; i += kCoefThreads) {
+constexpr int kCoefWarps = kCoefThreads / 32;
+
+// out(r, Σ_{k in [lo(r), hi(r))} term(r, k)) for r < nrows: a warp per output, lanes over k (the
+// mat-vecs here have <= K+3 terms, so one or two lane rounds and one shuffle reduction); caller syncs
+template <class Lo, class Hi, class T, class O>
+__device__ inline void warp_rows(int nrows, Lo lo, Hi hi, T term, O out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int r = warp; r < nrows; r += kCoefWarps) {
     double s = 0.0;
-    for (int k = 0; k <= i; ++k) s += LI[i * M + k] * v[k];
-    x[i] = s;
+    for (int k = lo(r) + lane; k < hi(r); k += 32) s += term(r, k);
+    s = wsum(s);
+    if (lane == 0) out(r, s);
   }
 }
-// x = LI^T v (rows < m), a thread per entry; caller syncs
+
+// x = LI v (LI lower triangular, rows < m); caller syncs
+__device__ void li_mv(const double* LI, int M, int m, const double* v, double* x) {
+  warp_rows(m, [](int) { return 0; }, [](int i) { return i + 1; },
+            [&](int i, int k) { return LI[i * M + k] * v[k]; }, [&](int i, double s) { x[i] = s; });
+}
+// x = LI^T v (rows < m); caller syncs
 __device__ void li_tmv(const double* LI, int M, int m, const double* v, double* x) {
-  for (int k = threadIdx.x; k < m; k += kCoefThreads) {
-    double s = 0.0;
-    for (int i = k; i < m; ++i) s += LI[i * M + k] * v[i];
-    x[k] = s;
-  }
+  warp_rows(m, [](int k) { return k; }, [&](int) { return m; },
+            [&](int k, int i) { return LI[i * M + k] * v[i]; }, [&](int k, double s) { x[k] = s; });
 }
 
 // classical Gram-Schmidt pass of (wg, wf) (length n) against the nb vectors (TG_i, TF_i) (stride M):
@@ -100,22 +112,20 @@ __device__ void li_tmv(const double* LI, int M, int m, const double* v, double* 
 __device__ void cgs_pass(const double* TG, const double* TF, int M, int nb, double* wg, double* wf, int n,
                          double* dv, double* acc) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int i = warp; i < nb; i += kCoefThreads / 32) {
+  for (int i = warp; i < nb; i += kCoefWarps) {
     double p = 0.0;
     for (int k = lane; k < n; k += 32) p += TG[i * M + k] * wg[k] + TF[i * M + k] * wf[k];
     p = wsum(p);
     if (lane == 0) dv[i] = p;
   }
   __syncthreads();
-  for (int k = threadIdx.x; k < n; k += kCoefThreads) {
-    double sg = 0.0, sf = 0.0;
-    for (int i = 0; i < nb; ++i) {
-      sg += dv[i] * TG[i * M + k];
-      sf += dv[i] * TF[i * M + k];
-    }
-    wg[k] -= sg;
-    wf[k] -= sf;
-  }
+  // w -= Σ_i d_i TQ_i: a warp per entry (g half in rows [0, n), f half in [n, 2n))
+  warp_rows(2 * n, [](int) { return 0; }, [&](int) { return nb; },
+            [&](int r, int i) { return dv[i] * (r < n ? TG[i * M + r] : TF[i * M + r - n]); },
+            [&](int r, double s) {
+              if (r < n) wg[r] -= s;
+              else wf[r - n] -= s;
+            });
   for (int i = threadIdx.x; i < nb; i += kCoefThreads) acc[i] += dv[i];
   __syncthreads();
 }
@@ -170,7 +180,7 @@ __global__ void __launch_bounds__(kCoefThreads) toar_coeffs_kernel(const double*
   {  // this column's dot-pass outputs, reduced here from the per-CTA partials when given (fixed order)
     const int nval = 2 * (m - 1) + 3;
     if (partials) {
-      for (int k = warp; k < nval; k += kCoefThreads / 32) {
+      for (int k = warp; k < nval; k += kCoefWarps) {
         const double* p = partials + ((size_t)k * B + c) * G;
         double v = 0.0;
         for (int g = lane; g < G; g += 32) v += p[g];
@@ -243,11 +253,11 @@ __global__ void __launch_bounds__(kCoefThreads) toar_coeffs_kernel(const double*
   const double lmm = dead_new ? 1.0 : sqrt(d2);
   for (int k = tid; k < M; k += kCoefThreads) {
     Lr[k] = k < nq ? (dead_new ? 0.0 : t1[k]) : (k == nq ? lmm : 0.0);
-    double s = 0.0;
-    if (k < nq && !dead_new)
-      for (int i = k; i < nq; ++i) s += t1[i] * LIs[i * M + k];
-    LIr[k] = k < nq ? -s / lmm : (k == nq ? 1.0 / lmm : 0.0);
+    if (k >= nq || dead_new) LIr[k] = k == nq ? 1.0 / lmm : 0.0;
   }
+  if (!dead_new)
+    warp_rows(nq, [](int k) { return k; }, [&](int) { return nq; },
+              [&](int k, int i) { return t1[i] * LIs[i * M + k]; }, [&](int k, double s) { LIr[k] = -s / lmm; });
   if (tid == 0) S.DEAD[nq] = dead_new ? 1.0 : 0.0;
   __syncthreads();
   for (int i = tid; i < M; i += kCoefThreads) {
@@ -350,21 +360,15 @@ __global__ void __launch_bounds__(kCoefThreads) toar_coeffs_kernel(const double*
     wg[k] = k < m ? Fh[k] : 0.0;
     wf[k] = k < m ? ZY[k] : nuy;
   }
-  for (int l = tid; l <= j; l += kCoefThreads) {
-    double s = 0.0;
-    for (int i = (l > 0 ? l - 1 : 0); i < j; ++i) s += Hs[i * (K + 1) + l] * av[i];
-    hv[l] = s;
-  }
+  warp_rows(j + 1, [](int l) { return l > 0 ? l - 1 : 0; }, [&](int) { return j; },
+            [&](int l, int i) { return Hs[i * (K + 1) + l] * av[i]; }, [&](int l, double s) { hv[l] = s; });
   __syncthreads();
-  for (int k = tid; k < m; k += kCoefThreads) {
-    double sg = 0.0, sf = 0.0;
-    for (int l = 0; l <= j; ++l) {
-      sg += hv[l] * TG[(size_t)l * M + k];
-      sf += hv[l] * TF[(size_t)l * M + k];
-    }
-    wg[k] = (wg[k] - sg) / nuq;
-    wf[k] = (wf[k] - sf) / nuq;
-  }
+  warp_rows(2 * m, [](int) { return 0; }, [&](int) { return j + 1; },
+            [&](int r, int l) { return hv[l] * (r < m ? TG[(size_t)l * M + r] : TF[(size_t)l * M + r - m]); },
+            [&](int r, double s) {
+              if (r < m) wg[r] = (wg[r] - s) / nuq;
+              else wf[r - m] = (wf[r - m] - s) / nuq;
+            });
   if (tid == 0) {
     wg[m] /= nuq;
     wf[m] /= nuq;
