@@ -87,8 +87,10 @@ constexpr int kCoefWarps = kCoefThreads / 32;
 template <class Lo, class Hi, class T, class O>
 __device__ inline void warp_rows(int nrows, Lo lo, Hi hi, T term, O out) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  #pragma unroll 1
   for (int r = warp; r < nrows; r += kCoefWarps) {
     double s = 0.0;
+    #pragma unroll 1
     for (int k = lo(r) + lane; k < hi(r); k += 32) s += term(r, k);
     s = wsum(s);
     if (lane == 0) out(r, s);
@@ -96,12 +98,12 @@ __device__ inline void warp_rows(int nrows, Lo lo, Hi hi, T term, O out) {
 }
 
 // x = LI v (LI lower triangular, rows < m); caller syncs
-__device__ void li_mv(const double* LI, int M, int m, const double* v, double* x) {
+__device__ __noinline__ void li_mv(const double* LI, int M, int m, const double* v, double* x) {
   warp_rows(m, [](int) { return 0; }, [](int i) { return i + 1; },
             [&](int i, int k) { return LI[i * M + k] * v[k]; }, [&](int i, double s) { x[i] = s; });
 }
 // x = LI^T v (rows < m); caller syncs
-__device__ void li_tmv(const double* LI, int M, int m, const double* v, double* x) {
+__device__ __noinline__ void li_tmv(const double* LI, int M, int m, const double* v, double* x) {
   warp_rows(m, [](int k) { return k; }, [&](int) { return m; },
             [&](int k, int i) { return LI[i * M + k] * v[i]; }, [&](int k, double s) { x[k] = s; });
 }
@@ -109,11 +111,13 @@ __device__ void li_tmv(const double* LI, int M, int m, const double* v, double* 
 // classical Gram-Schmidt pass of (wg, wf) (length n) against the nb vectors (TG_i, TF_i) (stride M):
 // d_i = <TQ_i, w> for all i (a warp per i, lanes over k), then w -= Σ d_i TQ_i (a thread per k);
 // acc[i] += d_i
-__device__ void cgs_pass(const double* TG, const double* TF, int M, int nb, double* wg, double* wf, int n,
+__device__ __noinline__ void cgs_pass(const double* TG, const double* TF, int M, int nb, double* wg, double* wf, int n,
                          double* dv, double* acc) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  #pragma unroll 1
   for (int i = warp; i < nb; i += kCoefWarps) {
     double p = 0.0;
+    #pragma unroll 1
     for (int k = lane; k < n; k += 32) p += TG[i * M + k] * wg[k] + TF[i * M + k] * wf[k];
     p = wsum(p);
     if (lane == 0) dv[i] = p;
@@ -126,16 +130,19 @@ __device__ void cgs_pass(const double* TG, const double* TF, int M, int nb, doub
               if (r < n) wg[r] -= s;
               else wf[r - n] -= s;
             });
+  #pragma unroll 1
   for (int i = threadIdx.x; i < nb; i += kCoefThreads) acc[i] += dv[i];
   __syncthreads();
 }
-__device__ double block_norm2(const double* g, const double* f, int n, double* red) {
+__device__ __noinline__ double block_norm2(const double* g, const double* f, int n, double* red) {
   double p = 0.0;
+  #pragma unroll 1
   for (int k = threadIdx.x; k < n; k += kCoefThreads) p += g[k] * g[k] + f[k] * f[k];
   p = wsum(p);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = p;
   __syncthreads();
   double s = 0.0;
+  #pragma unroll 1
   for (int w = 0; w < kCoefThreads / 32; ++w) s += red[w];
   __syncthreads();
   return s;
@@ -180,14 +187,17 @@ __global__ void __launch_bounds__(kCoefThreads) toar_coeffs_kernel(const double*
   {  // this column's dot-pass outputs, reduced here from the per-CTA partials when given (fixed order)
     const int nval = 2 * (m - 1) + 3;
     if (partials) {
+      #pragma unroll 1
       for (int k = warp; k < nval; k += kCoefWarps) {
         const double* p = partials + ((size_t)k * B + c) * G;
         double v = 0.0;
+        #pragma unroll 1
         for (int g = lane; g < G; g += 32) v += p[g];
         v = wsum(v);
         if (lane == 0) ssum[k] = v;
       }
     } else {
+      #pragma unroll 1
       for (int k = tid; k < nval; k += kCoefThreads) ssum[k] = sums[(size_t)k * B + c];
     }
     __syncthreads();
@@ -195,16 +205,20 @@ __global__ void __launch_bounds__(kCoefThreads) toar_coeffs_kernel(const double*
   auto sum = [&](int k) { return ssum[k]; };
   const int nout = j < 0 ? 1 : 3;
   auto zero_out = [&]() {
+    #pragma unroll 1
     for (int o = 0; o < nout; ++o) {
       if (tid == 0) coef_y[o * B + c] = 0.0;
+      #pragma unroll 1
       for (int i = tid; i < m; i += kCoefThreads) coef_u[((size_t)o * coef_ld + i) * B + c] = 0.0;
     }
   };
   if (j < 0) {  // fresh column state
+    #pragma unroll 1
     for (int i = tid; i < M * M; i += kCoefThreads) {
       S.L[i] = 0.0;
       S.LI[i] = 0.0;
     }
+    #pragma unroll 1
     for (int i = tid; i < M; i += kCoefThreads) S.DEAD[i] = 0.0;
     if (tid == 0) S.SC[kAlive] = 1.0;
     __syncthreads();
@@ -214,25 +228,30 @@ __global__ void __launch_bounds__(kCoefThreads) toar_coeffs_kernel(const double*
     return;
   }
   // stage the state
+  #pragma unroll 1
   for (int i = tid; i < (m - 1) * M; i += kCoefThreads) {
     L[i] = S.L[i];
     LIs[i] = S.LI[i];
   }
+  #pragma unroll 1
   for (int i = tid; i < nt * M; i += kCoefThreads) {
     TG[i] = i < (nt - (final_pass ? 0 : 1)) * M || final_pass ? S.TQg[i] : 0.0;
     TF[i] = i < (nt - (final_pass ? 0 : 1)) * M || final_pass ? S.TQf[i] : 0.0;
   }
+  #pragma unroll 1
   for (int i = tid; i < kV; i += kCoefThreads) {
     QG[i] = i < M ? S.QHg[i] : 0.0;
     QF[i] = i < M ? S.QHf[i] : 0.0;
   }
   const int hcols = j < 0 ? 0 : (final_pass ? K : j + 1);
+  #pragma unroll 1
   for (int i = tid; i < hcols * (K + 1); i += kCoefThreads) Hs[i] = Hc[i];
   __syncthreads();
   // 1. Gram row of the newest U vector u_{m-1}: l = L^{-1} a, L row m-1 = (l, sqrt(α - |l|²)), and the
   //    matching row of L^{-1}, (-l^T L^{-1}, 1)/L[m-1][m-1]; a zero vector gets identity rows (dead)
   double* Lr = L + (size_t)(m - 1) * M;
   double* LIr = LIs + (size_t)(m - 1) * M;
+  #pragma unroll 1
   for (int i = tid; i < nq; i += kCoefThreads) sv[i] = sum(2 * i);
   __syncthreads();
   li_mv(LIs, M, nq, sv, t1);
@@ -240,10 +259,12 @@ __global__ void __launch_bounds__(kCoefThreads) toar_coeffs_kernel(const double*
   double llv = 0.0;
   {
     double p = 0.0;
+    #pragma unroll 1
     for (int i = tid; i < nq; i += kCoefThreads) p += t1[i] * t1[i];
     p = wsum(p);
     if (lane == 0) red[warp] = p;
     __syncthreads();
+    #pragma unroll 1
     for (int w = 0; w < kCoefThreads / 32; ++w) llv += red[w];
     __syncthreads();
   }
@@ -251,6 +272,7 @@ __global__ void __launch_bounds__(kCoefThreads) toar_coeffs_kernel(const double*
   const double d2 = alpha - llv;
   const bool dead_new = !(alpha > 0.0) || !(d2 > 1e-24 * alpha);
   const double lmm = dead_new ? 1.0 : sqrt(d2);
+  #pragma unroll 1
   for (int k = tid; k < M; k += kCoefThreads) {
     Lr[k] = k < nq ? (dead_new ? 0.0 : t1[k]) : (k == nq ? lmm : 0.0);
     if (k >= nq || dead_new) LIr[k] = k == nq ? 1.0 / lmm : 0.0;
@@ -260,6 +282,7 @@ __global__ void __launch_bounds__(kCoefThreads) toar_coeffs_kernel(const double*
               [&](int k, int i) { return t1[i] * LIs[i * M + k]; }, [&](int k, double s) { LIr[k] = -s / lmm; });
   if (tid == 0) S.DEAD[nq] = dead_new ? 1.0 : 0.0;
   __syncthreads();
+  #pragma unroll 1
   for (int i = tid; i < M; i += kCoefThreads) {
     S.L[(size_t)(m - 1) * M + i] = Lr[i];
     S.LI[(size_t)(m - 1) * M + i] = LIr[i];
@@ -270,6 +293,7 @@ __global__ void __launch_bounds__(kCoefThreads) toar_coeffs_kernel(const double*
     const double eg = QG[m - 1], ef = QF[m - 1];
     const bool dead = S.DEAD[m - 1] != 0.0;
     __syncthreads();
+    #pragma unroll 1
     for (int i = tid; i < m; i += kCoefThreads) {
       const double l = dead ? 0.0 : Lr[i];
       if (i < m - 1) {
@@ -281,16 +305,19 @@ __global__ void __launch_bounds__(kCoefThreads) toar_coeffs_kernel(const double*
       }
     }
     __syncthreads();
+    #pragma unroll 1
     for (int i = tid; i < m; i += kCoefThreads) Fh[i] = QF[i];
   }
   // 3. y in W coordinates: z = L^{-1} s, ν_y² = γ - |z|²;  y = W z + ν_y u_m  (u_m := (y - U c)/ν_y)
   double nuy = 0.0;
   if (!final_pass) {
+    #pragma unroll 1
     for (int i = tid; i < m; i += kCoefThreads) sv[i] = i < nq ? sum(2 * i + 1) : sum(2 * nq + 1);
     __syncthreads();
     li_mv(LIs, M, m, sv, ZY);
     __syncthreads();
     double zz = 0.0;
+    #pragma unroll 1
     for (int i = lane; i < m; i += 32) zz += ZY[i] * ZY[i];
     zz = wsum(zz);
     const double gamma = sum(2 * nq + 2);
@@ -298,6 +325,7 @@ __global__ void __launch_bounds__(kCoefThreads) toar_coeffs_kernel(const double*
     if (!(nuy > 1e-12 * sqrt(gamma))) nuy = 0.0;  // y in span(U): no new direction
   }
   if (j < 0) {  // seed: q̂_0 = [t0; b0] = [L00 w_0; W z + ν_y u_1]
+    #pragma unroll 1
     for (int i = tid; i < M; i += kCoefThreads) {
       S.QHg[i] = i == 0 ? (S.DEAD[0] != 0.0 ? 0.0 : L[0]) : 0.0;
       S.QHf[i] = i == 0 ? ZY[0] : (i == 1 ? nuy : 0.0);
@@ -306,10 +334,12 @@ __global__ void __launch_bounds__(kCoefThreads) toar_coeffs_kernel(const double*
     __syncthreads();
     const double inv = nuy > 0.0 ? 1.0 / nuy : 0.0;
     if (tid == 0) coef_y[c] = inv;
+    #pragma unroll 1
     for (int i = tid; i < m; i += kCoefThreads) coef_u[(size_t)i * B + c] = -cu[i] * inv;
     return;
   }
   // 4. re-orthonormalise q̂_j against q_0..q_{j-1} (classical, twice), completing H column j-1
+  #pragma unroll 1
   for (int i = tid; i < kV; i += kCoefThreads) av[i] = 0.0;
   __syncthreads();
   cgs_pass(TG, TF, M, j, QG, QF, m, dv, av);
@@ -317,6 +347,7 @@ __global__ void __launch_bounds__(kCoefThreads) toar_coeffs_kernel(const double*
   const double nuq = sqrt(block_norm2(QG, QF, m, red));
   if (j > 0) {  // H column j-1 += hprov a, H(j, j-1) = hprov ν
     const double hp = S.SC[kHprov];
+    #pragma unroll 1
     for (int i = tid; i < j; i += kCoefThreads) {
       const double v = Hs[(j - 1) * (K + 1) + i] + hp * av[i];
       Hs[(j - 1) * (K + 1) + i] = v;
@@ -346,6 +377,7 @@ __global__ void __launch_bounds__(kCoefThreads) toar_coeffs_kernel(const double*
   }
   {  // q_j
     const double inv = 1.0 / nuq;
+    #pragma unroll 1
     for (int k = tid; k < M; k += kCoefThreads) {
       const double g = k < m ? QG[k] * inv : 0.0, f = k < m ? QF[k] * inv : 0.0;
       TG[(size_t)j * M + k] = g;
@@ -356,6 +388,7 @@ __global__ void __launch_bounds__(kCoefThreads) toar_coeffs_kernel(const double*
   }
   // 5. Z q_j = (Z q̂_j - Σ_{i<j} a_i Z q_i)/ν,  Z q̂_j = [f̂ ; W z + ν_y u_m],  Σ_i a_i Z q_i = Σ_l (H a)_l q_l
   const int m1 = m + 1;
+  #pragma unroll 1
   for (int k = tid; k < m1; k += kCoefThreads) {
     wg[k] = k < m ? Fh[k] : 0.0;
     wf[k] = k < m ? ZY[k] : nuy;
@@ -376,11 +409,13 @@ __global__ void __launch_bounds__(kCoefThreads) toar_coeffs_kernel(const double*
   __syncthreads();
   const double ref = sqrt(block_norm2(wg, wf, m1, red));
   // 6. Arnoldi: h = Q^T Z q_j (classical, twice), provisional q̂_{j+1}
+  #pragma unroll 1
   for (int i = tid; i < kV; i += kCoefThreads) hv[i] = 0.0;
   __syncthreads();
   cgs_pass(TG, TF, M, j + 1, wg, wf, m, dv, hv);
   cgs_pass(TG, TF, M, j + 1, wg, wf, m, dv, hv);
   const double hs = sqrt(block_norm2(wg, wf, m1, red));
+  #pragma unroll 1
   for (int i = tid; i <= j; i += kCoefThreads) Hc[j * (K + 1) + i] = hv[i];
   if (tid == 0) {
     S.SC[kHprov] = hs;
@@ -396,6 +431,7 @@ __global__ void __launch_bounds__(kCoefThreads) toar_coeffs_kernel(const double*
   }
   {
     const double inv = 1.0 / hs;
+    #pragma unroll 1
     for (int k = tid; k < M; k += kCoefThreads) {
       const double g = k < m1 ? wg[k] * inv : 0.0, f = k < m1 ? wf[k] * inv : 0.0;
       QG[k] = g;
@@ -418,6 +454,7 @@ __global__ void __launch_bounds__(kCoefThreads) toar_coeffs_kernel(const double*
     coef_y[B + c] = vm1;
     coef_y[2 * B + c] = vm2;
   }
+  #pragma unroll 1
   for (int i = tid; i < m; i += kCoefThreads) {
     coef_u[(size_t)i * B + c] = -cu[i] * iy;
     coef_u[((size_t)coef_ld + i) * B + c] = t1[i] - vm1 * cu[i];
