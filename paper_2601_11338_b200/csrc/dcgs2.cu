@@ -34,6 +34,7 @@ constexpr int kMaxVecPerLaunch = 32;  // longer bases are tiled by the launchers
 // pass A keeps 2 x 32 dot accumulators per thread, so it runs 128 consumers x 16 elements (5 warps: 255 registers per thread);
 // pass B 512 consumers x 4 elements.
 constexpr int kDotsConsumers = 128, kDotsPer = 16;
+static_assert(kDotsConsumers * kDotsPer <= 2048, "dots: unpredicated basis loads stay inside one ring stage");
 constexpr int kUpdConsumers = 512, kUpdPer = 4;
 constexpr int kStages = 12;
 constexpr int kStageElems = 2048;  // 16 KB
@@ -122,6 +123,11 @@ __global__ void __launch_bounds__(kDotsConsumers + 32, 1) dcgs2_dots_ring(Dcgs2A
   const int64_t N = a.len * a.B, h = a.split * a.B;
   const bool has_w = a.wa != nullptr;
   ring_init(full, empty, kDotsConsumers / 32);
+  // zero the ring once, so that the basis loads below need no bounds predicate: entries past a
+  // ragged tile's end (or a lane past tpb) hold zeros or values of an earlier piece, always finite,
+  // and meet p = w = 0 there (fewer instructions in the 32x-unrolled loop: less icache pressure)
+  for (int i = t; i < kStages * kStageElems; i += blockDim.x) ring[i] = 0.0;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
   double acc[2 * kMaxVecPerLaunch], alpha = 0.0, beta = 0.0, gamma = 0.0;
 #pragma unroll
@@ -161,7 +167,7 @@ __global__ void __launch_bounds__(kDotsConsumers + 32, 1) dcgs2_dots_ring(Dcgs2A
           const double* st = cur.acquire(ring, full);
 #pragma unroll
           for (int i = 0; i < kDotsPer; ++i) {
-            const double q = (act && t + i * tpb < cnt) ? st[t + i * tpb] : 0.0;
+            const double q = st[t + i * tpb];  // t + 15 tpb < kStageElems for every B
             acc[2 * j] += q * pv[i];
             acc[2 * j + 1] += q * wv[i];
           }
