@@ -141,9 +141,7 @@ __device__ __noinline__ double block_norm2(const double* g, const double* f, int
   p = wsum(p);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = p;
   __syncthreads();
-  double s = 0.0;
-  #pragma unroll 1
-  for (int w = 0; w < kCoefThreads / 32; ++w) s += red[w];
+  const double s = wsum((threadIdx.x & 31) < kCoefWarps ? red[threadIdx.x & 31] : 0.0);
   __syncthreads();
   return s;
 }
@@ -191,7 +189,7 @@ __global__ void __launch_bounds__(kCoefThreads) toar_coeffs_kernel(const double*
       for (int k = warp; k < nval; k += kCoefWarps) {
         const double* p = partials + ((size_t)k * B + c) * G;
         double v = 0.0;
-        #pragma unroll 1
+        #pragma unroll 8  // independent loads in flight: G partials are L2 round trips
         for (int g = lane; g < G; g += 32) v += p[g];
         v = wsum(v);
         if (lane == 0) ssum[k] = v;
@@ -264,8 +262,7 @@ __global__ void __launch_bounds__(kCoefThreads) toar_coeffs_kernel(const double*
     p = wsum(p);
     if (lane == 0) red[warp] = p;
     __syncthreads();
-    #pragma unroll 1
-    for (int w = 0; w < kCoefThreads / 32; ++w) llv += red[w];
+    llv = wsum(lane < kCoefWarps ? red[lane] : 0.0);
     __syncthreads();
   }
   const double alpha = sum(2 * nq);
