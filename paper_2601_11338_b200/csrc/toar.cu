@@ -112,7 +112,7 @@ __device__ __noinline__ void li_tmv(const double* LI, int M, int m, const double
 // d_i = <TQ_i, w> for all i (a warp per i, lanes over k), then w -= Σ d_i TQ_i (a thread per k);
 // acc[i] += d_i
 __device__ __noinline__ void cgs_pass(const double* TG, const double* TF, int M, int nb, double* wg, double* wf, int n,
-                         double* dv, double* acc) {
+                         double* dv, double* acc, bool first) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   #pragma unroll 1
   for (int i = warp; i < nb; i += kCoefWarps) {
@@ -131,7 +131,7 @@ __device__ __noinline__ void cgs_pass(const double* TG, const double* TF, int M,
               else wf[r - n] -= s;
             });
   #pragma unroll 1
-  for (int i = threadIdx.x; i < nb; i += kCoefThreads) acc[i] += dv[i];
+  for (int i = threadIdx.x; i < nb; i += kCoefThreads) acc[i] = first ? dv[i] : acc[i] + dv[i];
   __syncthreads();
 }
 __device__ __noinline__ double block_norm2(const double* g, const double* f, int n, double* red) {
@@ -336,11 +336,8 @@ __global__ void __launch_bounds__(kCoefThreads) toar_coeffs_kernel(const double*
     return;
   }
   // 4. re-orthonormalise q̂_j against q_0..q_{j-1} (classical, twice), completing H column j-1
-  #pragma unroll 1
-  for (int i = tid; i < kV; i += kCoefThreads) av[i] = 0.0;
-  __syncthreads();
-  cgs_pass(TG, TF, M, j, QG, QF, m, dv, av);
-  cgs_pass(TG, TF, M, j, QG, QF, m, dv, av);
+  cgs_pass(TG, TF, M, j, QG, QF, m, dv, av, true);  // av[i < j] = the two passes' coefficients
+  cgs_pass(TG, TF, M, j, QG, QF, m, dv, av, false);
   const double nuq = sqrt(block_norm2(QG, QF, m, red));
   if (j > 0) {  // H column j-1 += hprov a, H(j, j-1) = hprov ν
     const double hp = S.SC[kHprov];
@@ -406,11 +403,8 @@ __global__ void __launch_bounds__(kCoefThreads) toar_coeffs_kernel(const double*
   __syncthreads();
   const double ref = sqrt(block_norm2(wg, wf, m1, red));
   // 6. Arnoldi: h = Q^T Z q_j (classical, twice), provisional q̂_{j+1}
-  #pragma unroll 1
-  for (int i = tid; i < kV; i += kCoefThreads) hv[i] = 0.0;
-  __syncthreads();
-  cgs_pass(TG, TF, M, j + 1, wg, wf, m, dv, hv);
-  cgs_pass(TG, TF, M, j + 1, wg, wf, m, dv, hv);
+  cgs_pass(TG, TF, M, j + 1, wg, wf, m, dv, hv, true);  // hv[i <= j] = h
+  cgs_pass(TG, TF, M, j + 1, wg, wf, m, dv, hv, false);
   const double hs = sqrt(block_norm2(wg, wf, m1, red));
   #pragma unroll 1
   for (int i = tid; i <= j; i += kCoefThreads) Hc[j * (K + 1) + i] = hv[i];
