@@ -123,10 +123,16 @@ __global__ void __launch_bounds__(kDotsConsumers + 32, 1) dcgs2_dots_ring(Dcgs2A
   const int64_t N = a.len * a.B, h = a.split * a.B;
   const bool has_w = a.wa != nullptr;
   ring_init(full, empty, kDotsConsumers / 32);
-  // zero the ring once, so that the basis loads below need no bounds predicate: entries past a
-  // ragged tile's end (or a lane past tpb) hold zeros or values of an earlier piece, always finite,
-  // and meet p = w = 0 there (fewer instructions in the 32x-unrolled loop: less icache pressure)
-  for (int i = t; i < kStages * kStageElems; i += blockDim.x) ring[i] = 0.0;
+  // the basis loads below carry no bounds predicate (fewer instructions in the 32x-unrolled loop:
+  // less icache pressure).  Entries they read past a ragged tile's end, or past E for a lane beyond
+  // tpb, meet p = w = 0 and must be finite: zero [E, stage end) of every stage, and the whole ring in
+  // the one CTA that owns the ragged last tile (elsewhere the ring only ever holds basis values)
+  {
+    const int64_t last = (N - 1) / E;
+    const bool ragged = N % E != 0 && last % gridDim.x == blockIdx.x;
+    for (int st = 0; st < kStages; ++st)
+      for (int i = (ragged ? 0 : E) + t; i < kStageElems; i += blockDim.x) ring[(int64_t)st * kStageElems + i] = 0.0;
+  }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
   double acc[2 * kMaxVecPerLaunch], alpha = 0.0, beta = 0.0, gamma = 0.0;
