@@ -225,25 +225,54 @@ __global__ void __launch_bounds__(kCoefThreads) toar_coeffs_kernel(const double*
     if (!final_pass) zero_out();
     return;
   }
-  // stage the state
-  #pragma unroll 1
-  for (int i = tid; i < (m - 1) * M; i += kCoefThreads) {
-    L[i] = S.L[i];
-    LIs[i] = S.LI[i];
-  }
-  #pragma unroll 1
-  for (int i = tid; i < nt * M; i += kCoefThreads) {
-    TG[i] = i < (nt - (final_pass ? 0 : 1)) * M || final_pass ? S.TQg[i] : 0.0;
-    TF[i] = i < (nt - (final_pass ? 0 : 1)) * M || final_pass ? S.TQf[i] : 0.0;
-  }
-  #pragma unroll 1
-  for (int i = tid; i < kV; i += kCoefThreads) {
-    QG[i] = i < M ? S.QHg[i] : 0.0;
-    QF[i] = i < M ? S.QHf[i] : 0.0;
-  }
+  // stage the state: one flat index space over (L, L^{-1}), (TQg, TQf), (QHg, QHf), H; each thread
+  // issues the global loads of 4 pairs before it stores any of them (one L2 round trip per 4 pairs
+  // instead of one per array)
   const int hcols = j < 0 ? 0 : (final_pass ? K : j + 1);
-  #pragma unroll 1
-  for (int i = tid; i < hcols * (K + 1); i += kCoefThreads) Hs[i] = Hc[i];
+  {
+    const int nL = (m - 1) * M, nT = nt * M, nH = hcols * (K + 1);
+    const int tkeep = final_pass ? nT : (nt - 1) * M;  // q_j is recomputed this step
+    const int total = nL + nT + kV + nH;
+    auto load = [&](int i, double& x, double& y) {
+      if (i < nL) {
+        x = S.L[i];
+        y = S.LI[i];
+      } else if ((i -= nL) < nT) {
+        x = i < tkeep ? S.TQg[i] : 0.0;
+        y = i < tkeep ? S.TQf[i] : 0.0;
+      } else if ((i -= nT) < kV) {
+        x = i < M ? S.QHg[i] : 0.0;
+        y = i < M ? S.QHf[i] : 0.0;
+      } else {
+        x = Hc[i - kV];
+        y = 0.0;
+      }
+    };
+    auto store = [&](int i, double x, double y) {
+      if (i < nL) {
+        L[i] = x;
+        LIs[i] = y;
+      } else if ((i -= nL) < nT) {
+        TG[i] = x;
+        TF[i] = y;
+      } else if ((i -= nT) < kV) {
+        QG[i] = x;
+        QF[i] = y;
+      } else {
+        Hs[i - kV] = x;
+      }
+    };
+    #pragma unroll 1
+    for (int base = tid; base < total; base += 4 * kCoefThreads) {
+      double x[4], y[4];
+      #pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (base + u * kCoefThreads < total) load(base + u * kCoefThreads, x[u], y[u]);
+      #pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (base + u * kCoefThreads < total) store(base + u * kCoefThreads, x[u], y[u]);
+    }
+  }
   __syncthreads();
   // 1. Gram row of the newest U vector u_{m-1}: l = L^{-1} a, L row m-1 = (l, sqrt(α - |l|²)), and the
   //    matching row of L^{-1}, (-l^T L^{-1}, 1)/L[m-1][m-1]; a zero vector gets identity rows (dead)
