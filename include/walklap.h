@@ -104,6 +104,10 @@ typedef struct {
                            ||u|| h_{k+1,k} |e_k^T f_1(H_k) e_1| relative to ||u|| ||f_1(H_k) e_1|| per column;
                            an estimate above tol sets a sticky WL_ENOCONV that wl_wait reports (the
                            result is still written).  0 = no check (default). */
+  int32_t halo_overlap; /* multi-rank only: 1 (default) splits the local CSR into A_loc (local columns)
+                           and A_halo (halo columns) so A_loc's SpMM runs while the halo exchange is
+                           in flight on a second stream; 0 exchanges first, then runs
+                           one SpMM over the full local CSR */
 } wl_opts;
 
 typedef enum { WL_SOLVER_KRYLOV = 0, WL_SOLVER_CG = 1 } wl_solver;
@@ -126,6 +130,20 @@ wl_status wl_nccl_unique_id(void* out128);
 wl_status wl_comm_create(int32_t nranks, int32_t rank, const void* id128, int32_t device,
                          wl_comm** out);
 void wl_comm_destroy(wl_comm* comm);
+
+/* Loopback transport (testing the row-partitioned path on ONE device; SURVEY §4 "simulated
+ * exchange"): a group of nranks ranks living in one process, each driven by its own host thread and
+ * its own stream.  Every rank calls wl_comm_create_loopback(group, rank, device) and then uses the
+ * comm exactly like an NCCL one; halo exchanges become device-to-device copies between the ranks'
+ * buffers and allreduces a fixed-order device sum, both stream-ordered like NCCL.  Collective calls
+ * block the calling host thread until every rank has joined (a rendezvous, up to the group timeout,
+ * default 600 s, after which the group is broken and every collective returns WL_ENCCL).
+ * The group must outlive its comms.  1 <= nranks <= 64. */
+typedef struct wl_loopback wl_loopback;
+wl_status wl_loopback_create(int32_t nranks, wl_loopback** out);
+wl_status wl_loopback_set_timeout(wl_loopback* group, double seconds);
+void wl_loopback_destroy(wl_loopback* group);
+wl_status wl_comm_create_loopback(wl_loopback* group, int32_t rank, int32_t device, wl_comm** out);
 
 /* nnz-balanced contiguous row partition (host, bit-exact integer arithmetic):
  * bounds[0] = 0, bounds[nranks] = n, bounds[p] = smallest r with row_ptr[r] >= ceil(p*nnz/nranks)

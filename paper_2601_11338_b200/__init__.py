@@ -6,6 +6,7 @@ There is no CPU fallback: if the CUDA library is missing, importing `walklap` ra
 """
 from .walklap import (  # noqa: F401
     Comm,
+    LoopbackGroup,
     Operator,
     WalkLapError,
     Workspace,
@@ -16,6 +17,7 @@ from .walklap import (  # noqa: F401
     launch_count,
     load,
     partition,
+    run_loopback,
     profile_collect,
     profile_enable,
     version,

@@ -37,22 +37,45 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every csrc/*.cu to an object in parallel (nvcc -c, sm_100a), then link the shared library."""
     if not force and not needs_build():
         return LIB
+    from concurrent.futures import ThreadPoolExecutor
     os.makedirs(LIB_DIR, exist_ok=True)
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     inc, libdir = nccl_paths()
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-           "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v" if verbose else "-O3",
-           "-I", os.path.join(ROOT, "include"), "-I", inc,
-           *os.environ.get("WL_EXTRA_NVCC", "").split(),  # developer experiments (e.g. -DWL_SPMV_HINTS=1)
-           *sources(), "-o", tmp,
-           "-L", libdir, "-l:libnccl.so.2", f"-Xlinker", f"-rpath={libdir}", "-L/usr/local/cuda/lib64", "-lcublas", "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
-    if verbose:
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
+    tag = f"tmp{os.getpid()}"
+    flags = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+             "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
+             "-I", os.path.join(ROOT, "include"), "-I", inc,
+             *os.environ.get("WL_EXTRA_NVCC", "").split()]  # developer experiments (e.g. -DWL_SPMV_HINTS=1)
+    objs = [os.path.join(LIB_DIR, os.path.basename(src)[:-3] + f".{tag}.o") for src in sources()]
+
+    def compile_one(job):
+        src, obj = job
+        cmd = [nvcc, *flags, "-c", src, "-o", obj]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0 or verbose:
+            sys.stderr.write(r.stdout + r.stderr)
+        return r.returncode
+
+    try:
+        with ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 4)) as ex:
+            rcs = list(ex.map(compile_one, zip(sources(), objs)))
+        if any(rcs):
+            raise subprocess.CalledProcessError(max(rcs), "nvcc -c")
+        tmp = LIB + f".{tag}"
+        cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", *objs, "-o", tmp,
+               "-L", libdir, "-l:libnccl.so.2", "-Xlinker", f"-rpath={libdir}", "-L/usr/local/cuda/lib64",
+               "-lcublas", "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
+        subprocess.check_call(cmd)
+        os.replace(tmp, LIB)
+    finally:
+        for o in objs:
+            if os.path.exists(o):
+                os.remove(o)
     return LIB
 
 

@@ -234,7 +234,7 @@ __global__ void cg_combine_kernel(int mode, double lscale, const double* x, int6
 int vec_grid(int64_t n, int B) {
   const int tpb = kThreads / B * B;
   const int64_t need = (n * B + tpb - 1) / tpb;
-  return (int)std::max<int64_t>(1, std::min<int64_t>(need, 148 * 6));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)num_sms() * 6));
 }
 
 }  // namespace
@@ -296,7 +296,7 @@ void cg_combine(int mode, double lscale, const double* x, int64_t n, int B, cons
                 int64_t ldo, const int32_t* perm, cudaStream_t s) {
   WL_LAUNCH("cg_combine");
   const int64_t N = n * B;
-  const int g = (int)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, 148 * 8));
+  const int g = (int)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, (int64_t)num_sms() * 8));
   cg_combine_kernel<<<g, 256, 0, s>>>(mode, lscale, x, n, B, cs, V, ldv, vcol, c0, tprime, ldt, tcol, out, ldo, perm);
   WL_CUDA(cudaGetLastError());
 }

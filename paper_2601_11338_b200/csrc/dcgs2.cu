@@ -401,7 +401,8 @@ int dcgs2_dots(Dcgs2Args a, cudaStream_t s) {
     }
     const int tpb = kDotsConsumers / a.B * a.B;
     const int64_t N = a.len * a.B;
-    a.grid = (int)std::min<int64_t>(148, (N + tpb * kDotsPer - 1) / (tpb * kDotsPer));
+    // one persistent CTA per SM; an empty rank (N = 0) still launches one CTA so its partials are zeros
+    a.grid = (int)std::max<int64_t>(1, std::min<int64_t>(num_sms(), (N + tpb * kDotsPer - 1) / (tpb * kDotsPer)));
     dcgs2_dots_ring<<<a.grid, kDotsConsumers + 32, ring_smem(), s>>>(a, tpb);
     WL_CUDA(cudaGetLastError());
     if (a.sums_out) {  // null: the consumer reduces the partials itself (a.grid of them per output)
@@ -434,7 +435,8 @@ void dcgs2_update(Dcgs2Args a, cudaStream_t s) {
     }
     const int tpb = kUpdConsumers / a.B * a.B;
     const int64_t N = a.len * a.B;
-    const int grid = (int)std::min<int64_t>(148, (N + tpb * kUpdPer - 1) / (tpb * kUpdPer));
+    const int grid = (int)std::min<int64_t>(num_sms(), (N + tpb * kUpdPer - 1) / (tpb * kUpdPer));
+    if (grid == 0) return;  // empty rank
     dcgs2_update_ring<<<grid, kUpdConsumers + 32, ring_smem(), s>>>(a, tpb);
     WL_CUDA(cudaGetLastError());
   }
@@ -465,7 +467,8 @@ void toar_update(ToarArgs a, cudaStream_t s) {
   }
   const int tpb = kUpdConsumers / a.B * a.B;
   const int64_t N = a.len * a.B;
-  const int grid = (int)std::min<int64_t>(148, (N + tpb * kUpdPer - 1) / (tpb * kUpdPer));
+  const int grid = (int)std::min<int64_t>(num_sms(), (N + tpb * kUpdPer - 1) / (tpb * kUpdPer));
+  if (grid == 0) return;  // empty rank
   kern<<<grid, kUpdConsumers + 32, ring_smem(), s>>>(a, tpb);
   WL_CUDA(cudaGetLastError());
 }

@@ -15,7 +15,6 @@
 #include "wl_internal.cuh"
 
 #include <cublas_v2.h>
-#include <nccl.h>
 
 #include <algorithm>
 #include <atomic>
@@ -71,6 +70,27 @@ LaunchScope::~LaunchScope() {
   cudaEventRecord(g_prof[slot].b, s);
 }
 
+thread_local std::string g_last_error;
+
+wl_status set_last_error(int code, const std::string& m) {
+  g_last_error = m;
+  return (wl_status)code;
+}
+
+int num_sms() {
+  static std::mutex mtx;
+  static std::map<int, int> cache;
+  int dev = 0;
+  WL_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mtx);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  int sms = 0;
+  WL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  cache[dev] = sms;
+  return sms;
+}
+
 void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
   if (e == cudaSuccess) return;
   const std::string msg = std::string(what) + ": " + cudaGetErrorString(e) + " (" + file + ":" +
@@ -78,12 +98,6 @@ void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
   if (e == cudaErrorMemoryAllocation) throw Error(WL_ENOMEM, msg);
   throw Error(WL_ECUDA, msg);
 }
-
-#define WL_NCCL(x)                                                                        \
-  do {                                                                                    \
-    ncclResult_t r_ = (x);                                                                \
-    if (r_ != ncclSuccess) throw ::wl::Error(WL_ENCCL, std::string(#x) + ": " + ncclGetErrorString(r_)); \
-  } while (0)
 
 template <class T>
 struct DArr {
@@ -120,15 +134,58 @@ struct DeviceGuard {
   }
 };
 
+// One CSR operand of the SpMM with its degree bins (spmv.cu): small rows (deg <= kSmallMax),
+// medium rows (deg <= kMediumMax) and hub-row chunks; out_row maps row i of this CSR to the output
+// row it updates (null = identity).
+struct CsrPart {
+  DArr<int32_t> rowptr, col, small_rows, medium_rows, out_row;
+  DArr<int4> chunks;
+  int32_t n_rows = 0;
+  int64_t nnz = 0;
+  int n_small = 0, n_medium = 0, n_chunks = 0;
+  int small_first = -1;  // small rows form the contiguous id range [small_first, +n_small), or -1
+
+  void upload(const std::vector<int32_t>& rp, const std::vector<int32_t>& col_h, const std::vector<int32_t>* rows) {
+    n_rows = (int32_t)rp.size() - 1;
+    nnz = rp.back();
+    std::vector<int32_t> sm, md;
+    std::vector<int4> ch;
+    for (int64_t r = 0; r < n_rows; ++r) {
+      const int32_t d = rp[r + 1] - rp[r];
+      if (d <= kSmallMax) sm.push_back((int32_t)r);
+      else if (d <= kMediumMax) md.push_back((int32_t)r);
+      else {
+        const int first = (int)ch.size();
+        for (int32_t z = rp[r]; z < rp[r + 1]; z += kHubChunk)
+          ch.push_back(make_int4((int)r, z, std::min(z + kHubChunk, rp[r + 1]), first));
+      }
+    }
+    n_small = (int)sm.size();
+    n_medium = (int)md.size();
+    // the batched small-row kernel needs contiguous ids and writes rows in place (no out_row)
+    small_first = (!rows && !sm.empty() && sm.back() - sm.front() + 1 == (int32_t)sm.size()) ? sm.front() : -1;
+    n_chunks = (int)ch.size();
+    small_rows.alloc(std::max<size_t>(1, sm.size()));
+    medium_rows.alloc(std::max<size_t>(1, md.size()));
+    chunks.alloc(std::max<size_t>(1, ch.size()));
+    if (!sm.empty()) WL_CUDA(cudaMemcpy(small_rows.p, sm.data(), 4 * sm.size(), cudaMemcpyHostToDevice));
+    if (!md.empty()) WL_CUDA(cudaMemcpy(medium_rows.p, md.data(), 4 * md.size(), cudaMemcpyHostToDevice));
+    if (!ch.empty()) WL_CUDA(cudaMemcpy(chunks.p, ch.data(), sizeof(int4) * ch.size(), cudaMemcpyHostToDevice));
+    rowptr.alloc(n_rows + 1);
+    col.alloc(std::max<int64_t>(nnz, 1));
+    WL_CUDA(cudaMemcpy(rowptr.p, rp.data(), sizeof(int32_t) * (n_rows + 1), cudaMemcpyHostToDevice));
+    if (nnz) WL_CUDA(cudaMemcpy(col.p, col_h.data(), sizeof(int32_t) * nnz, cudaMemcpyHostToDevice));
+    if (rows) {
+      out_row.alloc(std::max<size_t>(1, rows->size()));
+      if (!rows->empty()) WL_CUDA(cudaMemcpy(out_row.p, rows->data(), 4 * rows->size(), cudaMemcpyHostToDevice));
+    }
+  }
+};
+
 }  // namespace wl
 
 using wl::DArr;
 using wl::Error;
-
-struct wl_comm {
-  ncclComm_t nccl = nullptr;
-  int nranks = 1, rank = 0, device = 0;
-};
 
 struct wl_operator {
   int device = 0;
@@ -136,7 +193,13 @@ struct wl_operator {
   int nranks = 1, rank = 0;
   int64_t n_global = 0, row_begin = 0, row_end = 0;
   int32_t n_loc = 0, nnz_loc = 0;
-  DArr<int32_t> rowptr, col;
+  // SpMM operand: A (all local rows; with split, only their local columns) and, with split, Ah (the
+  // rows that reference halo columns, only those columns) — the A_loc / A_halo split of SURVEY §8(e):
+  // A's SpMM runs while the halo is in flight, Ah's adds the halo terms after it arrived.
+  wl::CsrPart A, Ah;
+  bool split = false;
+  DArr<int32_t> rowptr_full;  // split only: row pointer of the full local rows (degrees d_i)
+  const int32_t* degrp() const { return split ? rowptr_full.p : A.rowptr.p; }
   // halo plan (rows exchanged per SpMM; counts in rows)
   int64_t n_halo = 0, n_send = 0;
   std::vector<int64_t> send_cnt, send_displ, recv_cnt, recv_displ;
@@ -154,11 +217,6 @@ struct wl_operator {
   wl_opts opts{};
   DArr<double> tprime;  // n_loc x n_theta, internal row order: t - c_0 (φ1 minus its identity term)
   DArr<int32_t> perm;   // internal row -> user row (degree-sorted relabelling); empty = identity
-  // degree bins of the SpMM (spmv.cu)
-  DArr<int32_t> small_rows, medium_rows;
-  DArr<int4> chunks;
-  int n_small = 0, n_medium = 0, n_chunks = 0;
-  int small_first = -1;  // small rows form the contiguous id range [small_first, +n_small) (relabelled)
 };
 
 struct wl_workspace {
@@ -172,6 +230,9 @@ struct wl_workspace {
   DArr<double> colp;  // g0z, g1z, g0s, g1s (kMaxCols each)
   DArr<double> chunk_part;
   DArr<unsigned int> row_ticket;
+  // multi-rank: the halo exchange runs on its own stream, overlapping the local SpMM
+  cudaStream_t cstream = nullptr;
+  cudaEvent_t ev_pack = nullptr, ev_halo = nullptr;
   // conjugate-gradient solver state (cg.cu): per column constants, scalars, |b|², iterations, flags
   DArr<double> cg_cs, cg_sc, cg_bb;
   DArr<int> cg_iters, cg_flags;
@@ -192,6 +253,9 @@ struct wl_workspace {
   DArr<double> trV, trW, trW2, trC, trR;
   cublasHandle_t cublas = nullptr;
   ~wl_workspace() {
+    if (cstream) cudaStreamDestroy(cstream);
+    if (ev_pack) cudaEventDestroy(ev_pack);
+    if (ev_halo) cudaEventDestroy(ev_halo);
     if (cg_flags_host) cudaFreeHost(cg_flags_host);
     if (cublas) cublasDestroy(cublas);
   }
@@ -200,93 +264,125 @@ struct wl_workspace {
 namespace wl {
 namespace {
 
-thread_local std::string g_last_error;
-
-wl_status fail(int code, const std::string& m) {
-  g_last_error = m;
-  return (wl_status)code;
-}
-
-template <class F>
-wl_status guarded(F&& f) {
-  try {
-    f();
-    return WL_OK;
-  } catch (const Error& e) {
-    return fail(e.code, e.what());
-  } catch (const std::bad_alloc&) {
-    return fail(WL_ENOMEM, "host allocation failed");
-  } catch (const std::exception& e) {
-    return fail(WL_EINVAL, e.what());
-  }
-}
-
 inline cudaStream_t S_(wl_stream s) { return reinterpret_cast<cudaStream_t>(s); }
 inline bool multi(const wl_operator* op) { return op->comm && op->comm->nranks > 1; }
 
 void allreduce(const wl_operator* op, double* buf, size_t count, cudaStream_t s) {
   if (!multi(op)) return;
-  WL_NCCL(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, op->comm->nccl, s));
+  comm_allreduce(op->comm, buf, count, s);
 }
 
 // Rows of `src` (n_loc x B, ld lds) that other ranks reference are packed and exchanged into
-// ws->halo_recv (n_halo x B), ordered by owner rank then global id.
+// ws->halo_recv (n_halo x B), ordered by owner rank then global id (comm.cu: grouped NCCL
+// send/recv, or device copies in a loopback group).
 void halo_exchange(const wl_operator* op, wl_workspace* ws, const double* src, int64_t lds, int B,
                    cudaStream_t s) {
   if (!multi(op)) return;
   pack_rows(src, lds, op->send_idx.p, op->n_send, B, ws->halo_send.p, s);
-  WL_NCCL(ncclGroupStart());
+  std::vector<Xfer> sends, recvs;
   for (int p = 0; p < op->nranks; ++p) {
     if (p == op->rank) continue;
     if (op->send_cnt[p] > 0)
-      WL_NCCL(ncclSend(ws->halo_send.p + op->send_displ[p] * B, (size_t)(op->send_cnt[p] * B), ncclDouble,
-                       p, op->comm->nccl, s));
+      sends.push_back({ws->halo_send.p + op->send_displ[p] * B, sizeof(double) * op->send_cnt[p] * B, p});
     if (op->recv_cnt[p] > 0)
-      WL_NCCL(ncclRecv(ws->halo_recv.p + op->recv_displ[p] * B, (size_t)(op->recv_cnt[p] * B), ncclDouble,
-                       p, op->comm->nccl, s));
+      recvs.push_back({ws->halo_recv.p + op->recv_displ[p] * B, sizeof(double) * op->recv_cnt[p] * B, p});
   }
-  WL_NCCL(ncclGroupEnd());
+  comm_sendrecv(op->comm, sends, recvs, s);
 }
 
-void do_spmv(const wl_operator* op, wl_workspace* ws, const double* y, const double* x,
-             const double* g0, const double* g1, const double* scale, double* out, int B,
-             cudaStream_t s, const int* active = nullptr) {
+// One SpMM launch over CSR part `part` of the operator (see wl_operator::A / Ah).
+void spmv_part(const wl_operator* op, wl_workspace* ws, const CsrPart& part, bool halo_part, const double* y,
+               const double* x, const double* g0, const double* g1, const double* scale, double* out, int B,
+               cudaStream_t s, const int* active) {
   SpmvArgs a{};
   a.active = active;
-  a.rowptr = op->rowptr.p;
-  a.col = op->col.p;
+  a.rowptr = part.rowptr.p;
+  a.col = part.col.p;
   a.n_loc = op->n_loc;
-  a.small_rows = op->small_rows.p;
-  a.n_small = op->n_small;
-  a.small_first = op->small_first;
-  a.medium_rows = op->medium_rows.p;
-  a.n_medium = op->n_medium;
-  a.chunks = op->chunks.p;
-  a.n_chunks = op->n_chunks;
+  a.small_rows = part.small_rows.p;
+  a.n_small = part.n_small;
+  a.small_first = part.small_first;
+  a.medium_rows = part.medium_rows.p;
+  a.n_medium = part.n_medium;
+  a.chunks = part.chunks.p;
+  a.n_chunks = part.n_chunks;
   a.chunk_part = ws->chunk_part.p;
   a.row_ticket = ws->row_ticket.p;
+  a.out_row = part.out_row.p;
   a.y = y;
   a.ldy = B;
-  a.yh = ws->halo_recv.p;
+  // halo rows: the full CSR without split, or the Ah part with it
+  const bool with_halo = multi(op) && op->n_halo > 0 && (halo_part || !op->split);
+  a.yh = with_halo ? ws->halo_recv.p : nullptr;
   a.ldh = B;
-  a.x = x;
+  a.n_halo = op->n_halo;
   a.ldx = B;
   a.out = out;
   a.ldo = B;
-  a.g0 = g0;
-  a.g1 = g1;
-  a.scale = scale;
   a.B = B;
+  if (halo_part) {  // out += scale * Σ_halo y: no diagonal term
+    a.accumulate = 1;
+    a.scale = scale;
+  } else {
+    a.x = x;
+    a.g0 = g0;
+    a.g1 = g1;
+    a.scale = scale;
+    a.degptr = op->split ? op->rowptr_full.p : nullptr;  // γ = μ(μ - d) needs the full degree
+  }
   spmv(a, s);
+}
+
+// Z-SpMM out = scale ⊙ (A y + (g0 + g1 d) ⊙ x) with y in this rank's rows (n_loc x B, ld B).
+// Multi-rank: the rows of y that peers reference are exchanged first; with the A_loc / A_halo split
+// (opts.halo_overlap) the exchange runs on the workspace's comm stream while A_loc's SpMM runs, and
+// A_halo's SpMM adds the halo terms once it has arrived.
+void do_spmv(const wl_operator* op, wl_workspace* ws, const double* y, const double* x,
+             const double* g0, const double* g1, const double* scale, double* out, int B,
+             cudaStream_t s, const int* active = nullptr) {
+  if (!multi(op) || !op->split) {
+    halo_exchange(op, ws, y, B, B, s);
+    spmv_part(op, ws, op->A, false, y, x, g0, g1, scale, out, B, s, active);
+    return;
+  }
+  pack_rows(y, B, op->send_idx.p, op->n_send, B, ws->halo_send.p, s);
+  WL_CUDA(cudaEventRecord(ws->ev_pack, s));
+  WL_CUDA(cudaStreamWaitEvent(ws->cstream, ws->ev_pack, 0));
+  std::vector<Xfer> sends, recvs;
+  for (int p = 0; p < op->nranks; ++p) {
+    if (p == op->rank) continue;
+    if (op->send_cnt[p] > 0)
+      sends.push_back({ws->halo_send.p + op->send_displ[p] * B, sizeof(double) * op->send_cnt[p] * B, p});
+    if (op->recv_cnt[p] > 0)
+      recvs.push_back({ws->halo_recv.p + op->recv_displ[p] * B, sizeof(double) * op->recv_cnt[p] * B, p});
+  }
+  comm_sendrecv(op->comm, sends, recvs, ws->cstream);
+  WL_CUDA(cudaEventRecord(ws->ev_halo, ws->cstream));
+  spmv_part(op, ws, op->A, false, y, x, g0, g1, scale, out, B, s, active);
+  WL_CUDA(cudaStreamWaitEvent(s, ws->ev_halo, 0));
+  spmv_part(op, ws, op->Ah, true, y, x, g0, g1, scale, out, B, s, active);
+}
+
+// halo buffers, comm stream and events of a workspace (multi-rank)
+void ws_comm_init(const wl_operator* op, wl_workspace* ws, int B) {
+  if (op->n_halo > 0 && ws->halo_recv.n < (size_t)op->n_halo * B) ws->halo_recv.alloc((size_t)op->n_halo * B);
+  if (op->n_send > 0 && ws->halo_send.n < (size_t)op->n_send * B) ws->halo_send.alloc((size_t)op->n_send * B);
+  if (op->split && !ws->cstream) {
+    WL_CUDA(cudaStreamCreateWithFlags(&ws->cstream, cudaStreamNonBlocking));
+    WL_CUDA(cudaEventCreateWithFlags(&ws->ev_pack, cudaEventDisableTiming));
+    WL_CUDA(cudaEventCreateWithFlags(&ws->ev_halo, cudaEventDisableTiming));
+  }
 }
 
 // Scratch of the hub-row chunks (partials + tickets) for B columns.
 void spmv_scratch(const wl_operator* op, wl_workspace* ws, int B) {
-  if (op->n_chunks == 0) return;
-  if (ws->chunk_part.n < (size_t)op->n_chunks * B) ws->chunk_part.alloc((size_t)op->n_chunks * B);
-  if (ws->row_ticket.n < (size_t)op->n_chunks) {
-    ws->row_ticket.alloc(op->n_chunks);
-    WL_CUDA(cudaMemset(ws->row_ticket.p, 0, sizeof(unsigned int) * op->n_chunks));
+  ws_comm_init(op, ws, B);
+  const int nch = std::max(op->A.n_chunks, op->Ah.n_chunks);  // the two parts run one after the other
+  if (nch == 0) return;
+  if (ws->chunk_part.n < (size_t)nch * B) ws->chunk_part.alloc((size_t)nch * B);
+  if (ws->row_ticket.n < (size_t)nch) {
+    ws->row_ticket.alloc(nch);
+    WL_CUDA(cudaMemset(ws->row_ticket.p, 0, sizeof(unsigned int) * nch));
   }
 }
 
@@ -312,9 +408,7 @@ void krylov_chunk(const wl_operator* op, wl_workspace* ws, int mode, const doubl
   batch_inputs(V, ldv, B, n, ws->Vb.p, ws->vcol.p, perm, s);
   double* Q0 = ws->basis.p;
   // a3: seeds q_1 v = A v (top) and q_2 v = A(Av) - μ d⊙v (bottom)   (eq:qrec seeds)
-  halo_exchange(op, ws, ws->Vb.p, B, B, s);
   do_spmv(op, ws, ws->Vb.p, nullptr, nullptr, nullptr, nullptr, Q0, B, s);
-  halo_exchange(op, ws, Q0, B, B, s);
   do_spmv(op, ws, Q0, ws->Vb.p, g0s, g1s, nullptr, Q0 + n_pad * B, B, s);
   if (n_pad > n) {  // phantom rows of the seed vector and of S stay zero; the passes keep them so
     fill(Q0 + n * B, B, 0.0, s);
@@ -339,7 +433,6 @@ void krylov_chunk(const wl_operator* op, wl_workspace* ws, int mode, const doubl
   for (int j = 0; j < K; ++j) {
     double* Pj = const_cast<double*>(slot.p[j]);
     // a4: S = A Pj_bot + μ(μ - d) Pj_top — bottom half of Z p_j; its top half is Pj_bot
-    halo_exchange(op, ws, Pj + n_pad * B, B, B, s);
     do_spmv(op, ws, Pj + n_pad * B, Pj, g0z, g1z, nullptr, ws->S.p, B, s);
     d.Q = slot;
     d.nq = j;
@@ -420,16 +513,12 @@ void toar_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double*
     double* s1 = vs_ + (n + 1) * b;
     double* s2 = s1 + (n + 1) * b;
     batch_inputs(V, ldv, b, n, vs_, ws->vid.p, perm, s);
-    halo_exchange(op, ws, vs_, b, b, s);
     do_spmv(op, ws, vs_, nullptr, nullptr, nullptr, nullptr, s1, b, s);
-    halo_exchange(op, ws, s1, b, b, s);
     do_spmv(op, ws, s1, nullptr, nullptr, nullptr, nullptr, s2, b, s);
-    seed_expand(s1, s2, vs_, b, op->rowptr.p, g1s, ws->vcol.p, B, n, U0, xb, s);
+    seed_expand(s1, s2, vs_, b, op->degrp(), g1s, ws->vcol.p, B, n, U0, xb, s);
   } else {
     batch_inputs(V, ldv, B, n, ws->Vb.p, ws->vcol.p, perm, s);
-    halo_exchange(op, ws, ws->Vb.p, B, B, s);
     do_spmv(op, ws, ws->Vb.p, nullptr, nullptr, nullptr, nullptr, U0, B, s);
-    halo_exchange(op, ws, U0, B, B, s);
     do_spmv(op, ws, U0, ws->Vb.p, g0s, g1s, nullptr, xb, B, s);
   }
   if (n_pad > n) {
@@ -484,7 +573,6 @@ void toar_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double*
   for (int j = 0; j < K; ++j) {
     const int m = j + 2;
     // a4: y = A x + μ(μ - d)⊙z  (bottom half of Z [z; x])
-    halo_exchange(op, ws, xin, B, B, s);
     do_spmv(op, ws, xin, zin, g0z, g1z, nullptr, yb, B, s);
     // a5: one dot pass (Gram row of the newest U vector, U^T y, |y|^2) and one update pass
     d.nq = m - 1;
@@ -545,7 +633,7 @@ void cg_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double* V
   CgArgs a{};
   a.n = n;
   a.B = B;
-  a.rowptr = op->rowptr.p;
+  a.rowptr = op->degrp();
   a.cs = ws->cg_cs.p;
   a.b = ws->Vb.p;
   a.x = ws->basis.p;
@@ -570,7 +658,6 @@ void cg_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double* V
   reduce_scalar(0);
   bool done = false;
   for (int it = 0; it < op->opts.cg_maxit && !done; ++it) {
-    halo_exchange(op, ws, a.p, B, B, s);
     do_spmv(op, ws, a.p, a.p, g0, g1, scale, a.q, B, s, a.flags + 1);  // q = 𝒜 p
     cg_dot(a, s);
     reduce_scalar(1);
@@ -664,25 +751,6 @@ void workspace_alloc(wl_workspace* ws, const wl_operator* op, int max_b) {
   WL_CUDA(cudaDeviceSynchronize());
 }
 
-// Collective exchange of small host int64 vectors through NCCL (device staging).
-void nccl_alltoall_counts(wl_comm* c, const std::vector<int64_t>& send, std::vector<int64_t>& recv,
-                          cudaStream_t s) {
-  const int P = c->nranks;
-  DArr<int64_t> ds, dr;
-  ds.alloc(P);
-  dr.alloc(P);
-  WL_CUDA(cudaMemcpy(ds.p, send.data(), sizeof(int64_t) * P, cudaMemcpyHostToDevice));
-  WL_NCCL(ncclGroupStart());
-  for (int p = 0; p < P; ++p) {
-    WL_NCCL(ncclSend(ds.p + p, 1, ncclInt64, p, c->nccl, s));
-    WL_NCCL(ncclRecv(dr.p + p, 1, ncclInt64, p, c->nccl, s));
-  }
-  WL_NCCL(ncclGroupEnd());
-  WL_CUDA(cudaStreamSynchronize(s));
-  recv.resize(P);
-  WL_CUDA(cudaMemcpy(recv.data(), dr.p, sizeof(int64_t) * P, cudaMemcpyDeviceToHost));
-}
-
 // Column renumbering of a row block [row_begin, row_end): owned column g -> g - row_begin, other
 // columns -> n + (index of g in the sorted, deduplicated halo list).  Validates the CSR
 // (in-range, no self loops, strictly increasing columns per row: simple graphs).
@@ -729,18 +797,12 @@ void build_operator(wl_operator* op, const int64_t* rp_in, const int32_t* ci_in,
   // gather all ranks' row ranges
   std::vector<int64_t> bounds(op->nranks + 1, 0);
   if (multi(op)) {
-    DArr<int64_t> d;
-    d.alloc(2 * op->nranks);
-    int64_t mine[2] = {op->row_begin, op->row_end};
-    WL_CUDA(cudaMemcpy(d.p + 2 * op->rank, mine, sizeof(mine), cudaMemcpyHostToDevice));
-    WL_NCCL(ncclAllGather(d.p + 2 * op->rank, d.p, 2, ncclInt64, op->comm->nccl, s));
-    WL_CUDA(cudaStreamSynchronize(s));
-    std::vector<int64_t> h(2 * op->nranks);
-    WL_CUDA(cudaMemcpy(h.data(), d.p, sizeof(int64_t) * h.size(), cudaMemcpyDeviceToHost));
+    std::vector<std::vector<int64_t>> all;
+    comm_allgather_host(op->comm, {op->row_begin, op->row_end}, all, s);
     for (int p = 0; p < op->nranks; ++p) {
-      if (h[2 * p] != (p == 0 ? 0 : h[2 * p - 1])) throw Error(WL_EINVAL, "row ranges not contiguous by rank");
-      bounds[p] = h[2 * p];
-      bounds[p + 1] = h[2 * p + 1];
+      if (all[p][0] != (p == 0 ? 0 : all[p - 1][1])) throw Error(WL_EINVAL, "row ranges not contiguous by rank");
+      bounds[p] = all[p][0];
+      bounds[p + 1] = all[p][1];
     }
     if (bounds[op->nranks] != op->n_global) throw Error(WL_EINVAL, "row ranges do not cover n_global");
   } else {
@@ -752,18 +814,26 @@ void build_operator(wl_operator* op, const int64_t* rp_in, const int32_t* ci_in,
   std::vector<int64_t> remote;
   halo_plan_host(op->n_global, op->row_begin, op->row_end, rp_in, ci_in, col, remote);
   op->n_halo = (int64_t)remote.size();
+  // A_loc / A_halo split: only with peers to exchange with
+  op->split = multi(op) && op->opts.halo_overlap && op->n_halo > 0;
   // Degree-sorted relabelling of the local rows: internal row r' holds user row perm[r'], rows
   // in decreasing degree (ties by id).  The hot gather set (high-degree rows, i.e. the columns
   // most nonzeros point to) becomes a dense, L2-resident prefix of every gathered block instead
   // of being scattered across random ids.  Halo ids (>= n) are unchanged; inputs are gathered and
-  // outputs scattered through perm at the boundary (batch_inputs / combine).
+  // outputs scattered through perm at the boundary (batch_inputs / combine).  With the split the
+  // key is the LOCAL degree: the number of local nonzeros that gather the row, and the row length
+  // the local SpMM's bins see.
+  std::vector<int32_t> key((size_t)n);
+  for (int64_t r = 0; r < n; ++r) {
+    key[r] = rp[r + 1] - rp[r];
+    if (op->split)
+      for (int32_t z = rp[r]; z < rp[r + 1]; ++z) key[r] -= col[z] >= n;
+  }
   std::vector<int32_t> newid;
   if (op->opts.relabel) {
     std::vector<int32_t> perm((size_t)n);
     std::iota(perm.begin(), perm.end(), 0);
-    std::stable_sort(perm.begin(), perm.end(), [&](int32_t x, int32_t y) {
-      return (rp[x + 1] - rp[x]) > (rp[y + 1] - rp[y]);
-    });
+    std::stable_sort(perm.begin(), perm.end(), [&](int32_t x, int32_t y) { return key[x] > key[y]; });
     newid.assign((size_t)n, 0);
     for (int64_t k = 0; k < n; ++k) newid[perm[k]] = (int32_t)k;
     std::vector<int32_t> rp2((size_t)n + 1, 0), col2((size_t)nnz);
@@ -780,34 +850,29 @@ void build_operator(wl_operator* op, const int64_t* rp_in, const int32_t* ci_in,
     op->perm.alloc(std::max<int64_t>(1, n));
     if (n) WL_CUDA(cudaMemcpy(op->perm.p, perm.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
   }
-  {  // degree bins (spmv.cu): small rows, medium rows, hub-row chunks
-    std::vector<int32_t> sm, md;
-    std::vector<int4> ch;
+  if (!op->split) {
+    op->A.upload(rp, col, nullptr);
+  } else {
+    // A_loc: every row, its local columns; A_halo: the rows with halo columns, those columns
+    std::vector<int32_t> rpl((size_t)n + 1, 0), cl, rph(1, 0), ch, hrows;
+    cl.reserve((size_t)nnz);
     for (int64_t r = 0; r < n; ++r) {
-      const int32_t d = rp[r + 1] - rp[r];
-      if (d <= kSmallMax) sm.push_back((int32_t)r);
-      else if (d <= kMediumMax) md.push_back((int32_t)r);
-      else {
-        const int first = (int)ch.size();
-        for (int32_t z = rp[r]; z < rp[r + 1]; z += kHubChunk)
-          ch.push_back(make_int4((int)r, z, std::min(z + kHubChunk, rp[r + 1]), first));
+      int32_t nh = 0;
+      for (int32_t z = rp[r]; z < rp[r + 1]; ++z) {
+        if (col[z] < n) cl.push_back(col[z]);
+        else { ch.push_back(col[z]); ++nh; }
+      }
+      rpl[r + 1] = (int32_t)cl.size();
+      if (nh) {
+        hrows.push_back((int32_t)r);
+        rph.push_back((int32_t)ch.size());
       }
     }
-    op->n_small = (int)sm.size();
-    op->n_medium = (int)md.size();
-    op->small_first = (!sm.empty() && sm.back() - sm.front() + 1 == (int32_t)sm.size()) ? sm.front() : -1;
-    op->n_chunks = (int)ch.size();
-    op->small_rows.alloc(std::max<size_t>(1, sm.size()));
-    op->medium_rows.alloc(std::max<size_t>(1, md.size()));
-    op->chunks.alloc(std::max<size_t>(1, ch.size()));
-    if (!sm.empty()) WL_CUDA(cudaMemcpy(op->small_rows.p, sm.data(), 4 * sm.size(), cudaMemcpyHostToDevice));
-    if (!md.empty()) WL_CUDA(cudaMemcpy(op->medium_rows.p, md.data(), 4 * md.size(), cudaMemcpyHostToDevice));
-    if (!ch.empty()) WL_CUDA(cudaMemcpy(op->chunks.p, ch.data(), sizeof(int4) * ch.size(), cudaMemcpyHostToDevice));
+    op->A.upload(rpl, cl, nullptr);
+    op->Ah.upload(rph, ch, &hrows);
+    op->rowptr_full.alloc(n + 1);
+    WL_CUDA(cudaMemcpy(op->rowptr_full.p, rp.data(), sizeof(int32_t) * (n + 1), cudaMemcpyHostToDevice));
   }
-  op->rowptr.alloc(n + 1);
-  op->col.alloc(std::max<int64_t>(nnz, 1));
-  WL_CUDA(cudaMemcpy(op->rowptr.p, rp.data(), sizeof(int32_t) * (n + 1), cudaMemcpyHostToDevice));
-  if (nnz) WL_CUDA(cudaMemcpy(op->col.p, col.data(), sizeof(int32_t) * nnz, cudaMemcpyHostToDevice));
   // halo plan: how many rows I need from each owner, then the ids (owners pack them)
   const int P = op->nranks;
   op->recv_cnt.assign(P, 0);
@@ -815,34 +880,27 @@ void build_operator(wl_operator* op, const int64_t* rp_in, const int32_t* ci_in,
   op->send_cnt.assign(P, 0);
   op->send_displ.assign(P, 0);
   if (multi(op)) {
+    // requests grouped by owner (remote is sorted and partitions are contiguous)
+    std::vector<std::vector<int64_t>> need(P), give;
     for (int64_t id : remote) {
       const int owner = (int)(std::upper_bound(bounds.begin(), bounds.end(), id) - bounds.begin()) - 1;
-      op->recv_cnt[owner]++;
+      need[owner].push_back(id);
     }
+    for (int p = 0; p < P; ++p) op->recv_cnt[p] = (int64_t)need[p].size();
     for (int p = 1; p < P; ++p) op->recv_displ[p] = op->recv_displ[p - 1] + op->recv_cnt[p - 1];
-    nccl_alltoall_counts(op->comm, op->recv_cnt, op->send_cnt, s);
+    comm_alltoallv_host(op->comm, need, give, s);
+    for (int p = 0; p < P; ++p) op->send_cnt[p] = (int64_t)give[p].size();
     for (int p = 1; p < P; ++p) op->send_displ[p] = op->send_displ[p - 1] + op->send_cnt[p - 1];
     op->n_send = op->send_displ[P - 1] + op->send_cnt[P - 1];
-    DArr<int64_t> need, give;
-    need.alloc(std::max<int64_t>(1, op->n_halo));
-    give.alloc(std::max<int64_t>(1, op->n_send));
-    if (op->n_halo)
-      WL_CUDA(cudaMemcpy(need.p, remote.data(), sizeof(int64_t) * op->n_halo, cudaMemcpyHostToDevice));
-    WL_NCCL(ncclGroupStart());
-    for (int p = 0; p < P; ++p) {
-      if (op->recv_cnt[p]) WL_NCCL(ncclSend(need.p + op->recv_displ[p], op->recv_cnt[p], ncclInt64, p, op->comm->nccl, s));
-      if (op->send_cnt[p]) WL_NCCL(ncclRecv(give.p + op->send_displ[p], op->send_cnt[p], ncclInt64, p, op->comm->nccl, s));
-    }
-    WL_NCCL(ncclGroupEnd());
-    WL_CUDA(cudaStreamSynchronize(s));
-    std::vector<int64_t> g((size_t)op->n_send);
-    if (op->n_send) WL_CUDA(cudaMemcpy(g.data(), give.p, sizeof(int64_t) * op->n_send, cudaMemcpyDeviceToHost));
+    // owners pack the requested rows in request order; ids -> internal (relabelled) local rows
     std::vector<int32_t> idx((size_t)op->n_send);
-    for (int64_t k = 0; k < op->n_send; ++k) {
-      if (g[k] < op->row_begin || g[k] >= op->row_end) throw Error(WL_EGRAPH, "halo request for a row not owned");
-      idx[k] = (int32_t)(g[k] - op->row_begin);
-      if (!newid.empty()) idx[k] = newid[idx[k]];
-    }
+    for (int p = 0, k = 0; p < P; ++p)
+      for (int64_t g : give[p]) {
+        if (g < op->row_begin || g >= op->row_end) throw Error(WL_EGRAPH, "halo request for a row not owned");
+        idx[k] = (int32_t)(g - op->row_begin);
+        if (!newid.empty()) idx[k] = newid[idx[k]];
+        ++k;
+      }
     op->send_idx.alloc(std::max<int64_t>(1, op->n_send));
     if (op->n_send) WL_CUDA(cudaMemcpy(op->send_idx.p, idx.data(), sizeof(int32_t) * op->n_send, cudaMemcpyHostToDevice));
   } else if (op->n_halo) {
@@ -988,37 +1046,7 @@ void wl_opts_default(wl_opts* o) {
   o->cg_maxit = 1000;
   o->cg_check = 8;
   o->tol = 0.0;
-}
-
-wl_status wl_nccl_unique_id(void* out128) {
-  return guarded([&] {
-    if (!out128) throw Error(WL_EINVAL, "out128 is NULL");
-    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
-    ncclUniqueId id;
-    WL_NCCL(ncclGetUniqueId(&id));
-    std::memcpy(out128, &id, 128);
-  });
-}
-
-wl_status wl_comm_create(int32_t nranks, int32_t rank, const void* id128, int32_t device, wl_comm** out) {
-  return guarded([&] {
-    if (!out || !id128 || nranks < 1 || rank < 0 || rank >= nranks) throw Error(WL_EINVAL, "bad comm args");
-    WL_CUDA(cudaSetDevice(device));
-    auto c = std::make_unique<wl_comm>();
-    c->nranks = nranks;
-    c->rank = rank;
-    c->device = device;
-    ncclUniqueId id;
-    std::memcpy(&id, id128, 128);
-    WL_NCCL(ncclCommInitRank(&c->nccl, nranks, id, rank));
-    *out = c.release();
-  });
-}
-
-void wl_comm_destroy(wl_comm* c) {
-  if (!c) return;
-  if (c->nccl) ncclCommDestroy(c->nccl);
-  delete c;
+  o->halo_overlap = 1;
 }
 
 wl_status wl_partition(int64_t n, const int64_t* row_ptr, int32_t nranks, int64_t* bounds) {
@@ -1086,6 +1114,7 @@ wl_status wl_operator_create(wl_comm* comm, int64_t n_global, int64_t row_begin,
     op->n_global = n_global;
     op->row_begin = row_begin;
     op->row_end = row_end;
+    if (row_end - row_begin >= INT32_MAX) throw Error(WL_EUNSUPPORTED, "local rows >= 2^31");
     op->n_loc = (int32_t)(row_end - row_begin);
     if (opts) op->opts = *opts;
     else wl_opts_default(&op->opts);
@@ -1324,13 +1353,10 @@ wl_status wl_spectral_radius(const wl_operator* op, int32_t k, double* rho_out, 
     cudaStream_t s = S_(stream);
     wl_workspace ws;
     ws.op = op;
-    if (op->n_halo > 0) ws.halo_recv.alloc(op->n_halo);
-    if (op->n_send > 0) ws.halo_send.alloc(op->n_send);
     outer_alloc(op, &ws, k, 1);
     spmv_scratch(op, &ws, 1);
     fill(ws.oQ.p, op->n_loc, 1.0, s);
     outer_arnoldi(op, &ws, k, [&](const double* Pj, double* out) {
-      halo_exchange(op, &ws, Pj, 1, 1, s);
       do_spmv(op, &ws, Pj, nullptr, nullptr, nullptr, nullptr, out, 1, s);  // A P̃_j
     }, s);
     std::vector<double> H((size_t)(k + 1) * k);
@@ -1356,8 +1382,6 @@ wl_status wl_spectral_radius_z(const wl_operator* op, int32_t theta_index, int32
     cudaStream_t s = S_(stream);
     wl_workspace ws;
     ws.op = op;
-    if (op->n_halo > 0) ws.halo_recv.alloc(op->n_halo);
-    if (op->n_send > 0) ws.halo_send.alloc(op->n_send);
     const int64_t np = outer_stride(op), len = 2 * np;  // Z vector = [top np ; bottom np], pad rows stay 0
     outer_alloc(op, &ws, k, 1, len);
     spmv_scratch(op, &ws, 1);
@@ -1374,7 +1398,6 @@ wl_status wl_spectral_radius_z(const wl_operator* op, int32_t theta_index, int32
     outer_arnoldi(op, &ws, k, [&](const double* Pj, double* out) {
       // Z (x; y) = (y; A y + μ(μ - d) x)   (eq:Zdef)
       WL_CUDA(cudaMemcpyAsync(out, Pj + np, sizeof(double) * np, cudaMemcpyDeviceToDevice, s));
-      halo_exchange(op, &ws, Pj + np, 1, 1, s);
       do_spmv(op, &ws, Pj + np, Pj, g0z, g1z, nullptr, out + np, 1, s);
     }, s, len);
     std::vector<double> H((size_t)(k + 1) * k);

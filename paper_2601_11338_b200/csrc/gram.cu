@@ -34,7 +34,7 @@ __global__ void reduce_partials_kernel(const double* partials, int nout, int G, 
 int gram_grid(int64_t elems, int B) {
   (void)elems;
   (void)B;
-  return 148 * 6;  // upper bound on the CTAs of a dot pass: partial buffers are sized for it
+  return num_sms() * 6;  // upper bound on the CTAs of a dot pass: partial buffers are sized for it
 }
 
 void reduce_partials(const double* partials, int nout, int G, double* sums_out, cudaStream_t s) {

@@ -251,7 +251,16 @@ __global__ void dcgs2_coeffs_kernel(const double* sums, int j, int B, int K, dou
 
 inline int grid_for(int64_t total, int bs = 256) {
   int64_t g = (total + bs - 1) / bs;
-  return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 8));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(g, (int64_t)num_sms() * 8));
+}
+
+// loopback allreduce: dst = Σ_r src_r in rank order (bitwise identical on every rank)
+__global__ void sum_ranks_kernel(const SumSrc src, int P, int64_t count, double* dst) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    double v = src.p[0][i];
+    for (int r = 1; r < P; ++r) v += src.p[r][i];
+    dst[i] = v;
+  }
 }
 
 }  // namespace
@@ -289,6 +298,13 @@ void combine(int mode, double lscale, const VecPtrs& Q, int nvec, int64_t n, int
     combine_kernel<32><<<g, 256, 0, s>>>(mode, lscale, Q, nvec, n, B, comb, V, ldv, vcol, c0, tprime, ldt, tcol, out, ldo, perm);
   else
     combine_kernel<kMaxKrylov + 2><<<g, 256, 0, s>>>(mode, lscale, Q, nvec, n, B, comb, V, ldv, vcol, c0, tprime, ldt, tcol, out, ldo, perm);
+  WL_CUDA(cudaGetLastError());
+}
+
+void sum_ranks(const SumSrc& src, int P, int64_t count, double* dst, cudaStream_t s) {
+  if (count <= 0) return;
+  WL_LAUNCH("allreduce_sum");
+  sum_ranks_kernel<<<grid_for(count), 256, 0, s>>>(src, P, count, dst);
   WL_CUDA(cudaGetLastError());
 }
 

@@ -81,10 +81,17 @@ struct Ctx {
 #endif
     return __ldg(yc + cl * ldy);
   }
+  // row r of this CSR -> output row a.out_row[r]; the γ term uses d_r from a.degptr when given
+  // (the A_loc part of a split operator); the A_halo part accumulates into out
   __device__ void write(int r, int deg, double sum) const {
+    const int ro = a.out_row ? __ldg(a.out_row + r) : r;
     double o = sum;
-    if (a.x) o += (g0 + g1 * (double)deg) * ld_stream(a.x + (int64_t)r * a.ldx + c);
-    st_stream(a.out + (int64_t)r * a.ldo + c, sc * o);
+    if (a.x) {
+      if (a.degptr) deg = __ldg(a.degptr + ro + 1) - __ldg(a.degptr + ro);
+      o += (g0 + g1 * (double)deg) * ld_stream(a.x + (int64_t)ro * a.ldx + c);
+    }
+    double* dst = a.out + (int64_t)ro * a.ldo + c;
+    st_stream(dst, a.accumulate ? *dst + sc * o : sc * o);
   }
   // Σ y[col[z]] for z = z0 + first, z0 + first + step, ... < z1 (step = lane groups sharing the row)
   __device__ double strided_sum(int z0, int z1, int first, int step) const {
@@ -235,7 +242,10 @@ __global__ void __launch_bounds__(kThreads) spmv_small_batched_kernel(SpmvArgs a
       const int ia = gi * nr / gpw, ib = (gi + 1) * nr / gpw;  // this group's rows
       auto flush = [&](int i, double acc) {
         double o = acc;
-        if (a.x) o += (ctx.g0 + ctx.g1 * (double)(srow[i + 1] - srow[i])) * sx[i * B + c];
+        if (a.x) {
+          const int d = a.degptr ? __ldg(a.degptr + r0 + i + 1) - __ldg(a.degptr + r0 + i) : srow[i + 1] - srow[i];
+          o += (ctx.g0 + ctx.g1 * (double)d) * sx[i * B + c];
+        }
         st_stream(a.out + (int64_t)(r0 + i) * a.ldo + c, ctx.sc * o);
       };
       int cur = ia, rend = srow[ia + 1];
@@ -308,8 +318,9 @@ void spmv(const SpmvArgs& a0, cudaStream_t s) {
   if (grid <= 0) return;
   static const int U = [] { const char* v = getenv("WL_SPMV_U"); return v ? atoi(v) : 8; }();
   static const bool split = getenv("WL_SPMV_SPLIT") != nullptr;  // per-class timing experiment
-  if ((int64_t)(a.n_loc + 1) * a.ldy >= INT32_MAX || a.yh && (int64_t)a.ldh * a.n_loc >= INT32_MAX)
-    throw Error(8, "spmv: n_loc * ld must be < 2^31 (32-bit gather offsets)");
+  // gather offsets are 32-bit: local rows (col < n_loc) at col * ldy, halo rows at (col - n_loc) * ldh
+  if ((int64_t)(a.n_loc + 1) * a.ldy >= INT32_MAX || (a.yh && (int64_t)(a.n_halo + 1) * a.ldh >= INT32_MAX))
+    throw Error(8, "spmv: n_loc * ld and n_halo * ldh must be < 2^31 (32-bit gather offsets)");
   const bool halo = a.yh != nullptr;
   auto go = [&](const SpmvArgs& aa, int g) {
     if (halo) {
@@ -342,12 +353,7 @@ void spmv(const SpmvArgs& a0, cudaStream_t s) {
     }
     int occ = 0;
     WL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem));
-    static int sms = 0;
-    if (!sms) {
-      int dev = 0;
-      WL_CUDA(cudaGetDevice(&dev));
-      WL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    }
+    const int sms = num_sms();
     const int nb = (a.n_small + 31) / 32;
     const int g = std::max(1, std::min((nb + kWarps - 1) / kWarps, sms * std::max(occ, 1)));
     kern<<<g, kThreads, smem, s>>>(a);

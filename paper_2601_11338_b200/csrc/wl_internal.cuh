@@ -1,6 +1,7 @@
 // wl_internal.cuh — shared declarations of the walklap CUDA library (not part of the C ABI).
 #pragma once
 #include <cuda_runtime.h>
+#include "walklap.h"
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -25,6 +26,26 @@ struct LaunchScope {
   ~LaunchScope();
 };
 #define WL_LAUNCH(name) ::wl::LaunchScope wl_launch_scope_(name, s)
+
+// ---------------------------------------------------------------- C ABI error plumbing
+// Every extern "C" entry point runs its body through guarded(): a thrown Error becomes its
+// wl_status and the thread-local message returned by wl_last_error().
+wl_status set_last_error(int code, const std::string& m);
+template <class F>
+wl_status guarded(F&& f) {
+  try {
+    f();
+    return WL_OK;
+  } catch (const Error& e) {
+    return set_last_error(e.code, e.what());
+  } catch (const std::bad_alloc&) {
+    return set_last_error(WL_ENOMEM, "host allocation failed");
+  } catch (const std::exception& e) {
+    return set_last_error(WL_EINVAL, e.what());
+  }
+}
+
+int num_sms();  // SMs of the current device (cached per device)
 
 constexpr int kMaxCols = 32;    // columns per Krylov batch (B)
 constexpr int kMaxKrylov = 64;  // Arnoldi steps per action
@@ -57,10 +78,14 @@ struct SpmvArgs {
   unsigned int* row_ticket;          // n_chunks, zero between launches
   int nblk_small, nblk_medium;       // filled by spmv()
   const double* y; int64_t ldy;
-  const double* yh; int64_t ldh;
+  const double* yh; int64_t ldh;   // halo rows (multi-rank), n_halo of them
+  int64_t n_halo;
   const double* x; int64_t ldx;   // may be null (no diagonal term)
   double* out; int64_t ldo;
   const double* g0; const double* g1; const double* scale;  // device, B entries (null = 0,0,1)
+  const int32_t* degptr;             // row pointer giving d_i for the γ term (null: this CSR's rowptr)
+  const int32_t* out_row;            // output row of CSR row i (null: i); not with the batched small rows
+  int accumulate;                    // out += scale * Σ (no diagonal term): the A_halo part
   int B;
   const int* active;                 // optional (CG): the launch does nothing when *active == 0
 };
@@ -209,4 +234,35 @@ bool xnystrace_curve(const std::vector<double>& lam, const std::vector<double>& 
 void lanczos_combine(const double* Q, int64_t stride, int m, int64_t n, const double* Y, int nt,
                      double scale, double* X, int64_t ldx, const int32_t* perm, cudaStream_t s);
 
+// ---------------------------------------------------------------- collectives (comm.cu)
+constexpr int kMaxRanks = 64;
+struct SumSrc {
+  const double* p[kMaxRanks];
+};
+// dst[i] = Σ_{r < P} src.p[r][i], summed in rank order (the loopback allreduce)
+void sum_ranks(const SumSrc& src, int P, int64_t count, double* dst, cudaStream_t s);
+struct Xfer {
+  void* ptr;     // device
+  size_t bytes;
+  int peer;
+};
+void comm_allreduce(wl_comm* c, double* buf, size_t count, cudaStream_t s);
+void comm_sendrecv(wl_comm* c, const std::vector<Xfer>& sends, const std::vector<Xfer>& recvs, cudaStream_t s);
+void comm_alltoallv_host(wl_comm* c, const std::vector<std::vector<int64_t>>& send,
+                         std::vector<std::vector<int64_t>>& recv, cudaStream_t s);
+void comm_allgather_host(wl_comm* c, const std::vector<int64_t>& mine, std::vector<std::vector<int64_t>>& all,
+                         cudaStream_t s);
+void comm_barrier_host(wl_comm* c);
+
 }  // namespace wl
+
+// Communicator: NCCL (one process per GPU) or a loopback group (P ranks in one process on one device).
+struct wl_loopback;
+struct wl_comm {
+  void* nccl = nullptr;        // ncclComm_t
+  wl_loopback* lb = nullptr;   // loopback transport when set
+  int nranks = 1, rank = 0, device = 0;
+  cudaEvent_t ev_ready = nullptr, ev_done = nullptr;  // loopback rendezvous events
+  double* scratch = nullptr;                           // loopback allreduce sums
+  size_t scratch_n = 0;
+};

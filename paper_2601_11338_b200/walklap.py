@@ -38,7 +38,7 @@ class _Opts(ctypes.Structure):
                 ("max_cols", ctypes.c_int32), ("breakdown_tol", ctypes.c_double),
                 ("rho_bound", ctypes.c_double), ("relabel", ctypes.c_int32), ("solver", ctypes.c_int32),
                 ("cg_tol", ctypes.c_double), ("cg_maxit", ctypes.c_int32), ("cg_check", ctypes.c_int32),
-                ("tol", ctypes.c_double)]
+                ("tol", ctypes.c_double), ("halo_overlap", ctypes.c_int32)]
 
 
 def load():
@@ -60,6 +60,10 @@ def load():
         "wl_nccl_unique_id": ([vp], ctypes.c_int),
         "wl_comm_create": ([i32, i32, vp, i32, pvp], ctypes.c_int),
         "wl_comm_destroy": ([vp], None),
+        "wl_loopback_create": ([i32, pvp], ctypes.c_int),
+        "wl_loopback_set_timeout": ([vp, dbl], ctypes.c_int),
+        "wl_loopback_destroy": ([vp], None),
+        "wl_comm_create_loopback": ([vp, i32, i32, pvp], ctypes.c_int),
         "wl_partition": ([i64, vp, i32, vp], ctypes.c_int),
         "wl_halo_plan": ([i64, i32, vp, i32, vp, vp, vp, vp, vp, vp], ctypes.c_int),
         "wl_operator_create": ([vp, i64, i64, i64, vp, vp, i32, i32, vp, ctypes.POINTER(_WalkFun),
@@ -198,7 +202,18 @@ def _block(t, cols, what):
 
 
 class Comm:
-    """NCCL communicator over the current torch.distributed group (one process per GPU)."""
+    """NCCL communicator over the current torch.distributed group (one process per GPU), or a rank of
+    a LoopbackGroup (Comm.loopback)."""
+
+    @classmethod
+    def loopback(cls, group: "LoopbackGroup", rank: int, device: int = 0) -> "Comm":
+        """Rank `rank` of a single-process loopback group (wl_comm_create_loopback)."""
+        self = cls.__new__(cls)
+        h = ctypes.c_void_p()
+        _check(load().wl_comm_create_loopback(group.handle, rank, device, ctypes.byref(h)))
+        self.handle, self.rank, self.world, self.device = h, rank, group.nranks, device
+        self._group = group  # the group must outlive its comms
+        return self
 
     def __init__(self, rank: int, world: int, device: int, group=None):
         import torch.distributed as dist
@@ -223,6 +238,65 @@ class Comm:
             self.close()
         except Exception:
             pass
+
+
+class LoopbackGroup:
+    """P ranks of the row-partitioned path in ONE process on one device (wl_loopback_create): each rank
+    is driven by its own host thread and stream; halo exchanges are device copies and allreduces a
+    fixed-order device sum.  Collective calls rendezvous across the ranks' threads (timeout seconds)."""
+
+    def __init__(self, nranks: int, timeout: float = 600.0):
+        h = ctypes.c_void_p()
+        _check(load().wl_loopback_create(nranks, ctypes.byref(h)))
+        self.handle, self.nranks = h, nranks
+        _check(load().wl_loopback_set_timeout(h, float(timeout)))
+
+    def close(self):
+        if getattr(self, "handle", None):
+            load().wl_loopback_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def run_loopback(nranks: int, fn, device: int = 0, timeout: float = 600.0):
+    """Run fn(rank, comm, stream) for every rank of a loopback group, one host thread and one CUDA
+    stream per rank on `device`; returns the per-rank results (the first exception is re-raised)."""
+    import threading
+
+    import torch
+    group = LoopbackGroup(nranks, timeout)
+    out, errs = [None] * nranks, [None] * nranks
+
+    def body(r):
+        comm = None
+        try:
+            torch.cuda.set_device(device)
+            stream = torch.cuda.Stream(device)
+            comm = Comm.loopback(group, r, device)
+            with torch.cuda.stream(stream):
+                out[r] = fn(r, comm, stream)
+            stream.synchronize()
+        except BaseException as e:  # noqa: BLE001 (re-raised in the caller's thread)
+            errs[r] = e
+        finally:
+            if comm is not None:
+                comm.close()
+
+    threads = [threading.Thread(target=body, args=(r,)) for r in range(nranks)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    group.close()
+    for e in errs:
+        if e is not None:
+            raise e
+    return out
 
 
 class Workspace:
@@ -264,7 +338,7 @@ class Operator:
     def __init__(self, n_global, row_ptr, col_idx, thetas=(1.0,), f=("exp", 1.0), variant=None,
                  row_range=None, comm: Comm | None = None, krylov_dim=30, reorth=2, max_cols=32,
                  breakdown_tol=1e-12, rho_bound=0.0, relabel=1, solver="krylov", cg_tol=1e-9, cg_maxit=1000,
-                 cg_check=8, lap_scale=1.0, krylov_tol=0.0, stream=None):
+                 cg_check=8, lap_scale=1.0, krylov_tol=0.0, halo_overlap=1, stream=None):
         lib = load()
         rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
         ci = np.ascontiguousarray(col_idx, dtype=np.int32)
@@ -295,6 +369,7 @@ class Operator:
         opts.solver = {"krylov": 0, "cg": 1}[solver]
         opts.cg_tol, opts.cg_maxit, opts.cg_check = cg_tol, cg_maxit, cg_check
         opts.tol = krylov_tol
+        opts.halo_overlap = halo_overlap
         h = ctypes.c_void_p()
         _check(lib.wl_operator_create(comm.handle if comm else None, n_global, rb, re, rp.ctypes.data,
                                       ci.ctypes.data, variant, len(thetas) if variant == WL_BTDW else 1,
