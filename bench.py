@@ -198,6 +198,10 @@ def run_walklap(args):
         by1 = 4 * nz + 4 * (nl + 1) + 8 * nl + 8 * probe.n_halo + 8 * nl  # col, rowptr, y (once), halo, out
         spmv_b1 = {"alg_bytes_per_launch": by1, "ms_per_launch": ms1 / cnt1, "launches": cnt1,
                    "achieved_gbs": by1 / (ms1 / cnt1 / 1e3) / 1e9}
+        # per degree class when the library splits the launch scopes (WL_SPMV_SPLIT, profiling only)
+        cls = {k: v[0] / cnt1 for k, v in prof_rho.items() if k.startswith("spmv_") and k != "spmv_binned"}
+        if cls:
+            spmv_b1["class_ms_per_launch"] = cls
     probe.close()
     beta = 1.0 / rho
     thetas = cfg["thetas"]

@@ -357,11 +357,17 @@ __global__ void __launch_bounds__(kUpdConsumers + 32, 1) toar_update_ring(ToarAr
       cur.release(empty, lane);
     }
     if (act) {
+      // element e = e0 + t + i*tpb is (row e / B, column c); tpb and E are multiples of B, so the row is
+      // e0/B + t/B + i*(tpb/B) — outputs with a padded row stride (out_ld) are addressed from it
+      const int64_t r0 = e0 / B + t / B;
 #pragma unroll
       for (int i = 0; i < kUpdPer; ++i)
         if (t + i * tpb < cnt) {
 #pragma unroll
-          for (int o = 0; o < NOUT; ++o) a.out[o][e0 + t + i * tpb] = acc[o][i];
+          for (int o = 0; o < NOUT; ++o) {
+            if (a.out_ld[o] > B) a.out[o][(r0 + (int64_t)i * (tpb / B)) * a.out_ld[o] + c] = acc[o][i];
+            else a.out[o][e0 + t + i * tpb] = acc[o][i];
+          }
         }
     }
   }
@@ -447,6 +453,8 @@ void dcgs2_update(Dcgs2Args a, cudaStream_t s) {
 void toar_update(ToarArgs a, cudaStream_t s) {
   if (a.nout < 1 || a.nout > kToarMaxOut) throw Error(1, "toar_update: 1..3 outputs");
   if (a.m > kMaxVecPerLaunch) {
+    for (int o = 0; o < a.nout; ++o)
+      if (a.out_ld[o] > a.B) throw Error(1, "toar_update: padded outputs need m <= 32 (tiles read outputs back)");
     for (int i0 = 0; i0 < a.m; i0 += kMaxVecPerLaunch) {
       ToarArgs t = a;
       t.m = std::min(kMaxVecPerLaunch, a.m - i0);

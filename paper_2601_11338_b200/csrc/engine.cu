@@ -55,6 +55,7 @@ static cudaEvent_t prof_event() {
 }
 
 LaunchScope::LaunchScope(const char* name, cudaStream_t st) : s(st) {
+  if (!name) return;  // disabled scope
   note_launch(name);
   if (!g_prof_on) return;
   std::lock_guard<std::mutex> lk(g_prof_mtx);
@@ -243,6 +244,7 @@ struct wl_workspace {
   DArr<double> seed;             // TOAR shared seeds: v, A v, A(Av) over the b input columns
   DArr<int> vid;                 // 0, 1, ..., kMaxCols-1
   DArr<double> toar_state, toar_cy, toar_cu, toar_comb;  // TOAR (toar.cu): per-column state, update coefficients
+  DArr<double> xg;               // TOAR: the SpMM's gathered block with rows padded to pad_cols(B) (zero phantoms)
   // host-buffer entry point
   DArr<double> hV, hLV;
   // diffusion (outer Lanczos)
@@ -292,8 +294,8 @@ void halo_exchange(const wl_operator* op, wl_workspace* ws, const double* src, i
 
 // One SpMM launch over CSR part `part` of the operator (see wl_operator::A / Ah).
 void spmv_part(const wl_operator* op, wl_workspace* ws, const CsrPart& part, bool halo_part, const double* y,
-               const double* x, const double* g0, const double* g1, const double* scale, double* out, int B,
-               cudaStream_t s, const int* active) {
+               int64_t ldy, const double* x, const double* g0, const double* g1, const double* scale, double* out,
+               int B, cudaStream_t s, const int* active) {
   SpmvArgs a{};
   a.active = active;
   a.rowptr = part.rowptr.p;
@@ -310,11 +312,11 @@ void spmv_part(const wl_operator* op, wl_workspace* ws, const CsrPart& part, boo
   a.row_ticket = ws->row_ticket.p;
   a.out_row = part.out_row.p;
   a.y = y;
-  a.ldy = B;
+  a.ldy = ldy;
   // halo rows: the full CSR without split, or the Ah part with it
   const bool with_halo = multi(op) && op->n_halo > 0 && (halo_part || !op->split);
   a.yh = with_halo ? ws->halo_recv.p : nullptr;
-  a.ldh = B;
+  a.ldh = ldy;  // halo rows are packed with the gathered block's row width
   a.n_halo = op->n_halo;
   a.ldx = B;
   a.out = out;
@@ -333,34 +335,36 @@ void spmv_part(const wl_operator* op, wl_workspace* ws, const CsrPart& part, boo
   spmv(a, s);
 }
 
-// Z-SpMM out = scale ⊙ (A y + (g0 + g1 d) ⊙ x) with y in this rank's rows (n_loc x B, ld B).
-// Multi-rank: the rows of y that peers reference are exchanged first; with the A_loc / A_halo split
-// (opts.halo_overlap) the exchange runs on the workspace's comm stream while A_loc's SpMM runs, and
-// A_halo's SpMM adds the halo terms once it has arrived.
-void do_spmv(const wl_operator* op, wl_workspace* ws, const double* y, const double* x,
+// Z-SpMM out = scale ⊙ (A y + (g0 + g1 d) ⊙ x) with y in this rank's rows (n_loc x B, ld ldy >= B: the
+// gathered block may be padded to a row width the wide-lane gathers can load, spmv.cu).
+// Multi-rank: the rows of y that peers reference are exchanged first (whole padded rows); with the
+// A_loc / A_halo split (opts.halo_overlap) the exchange runs on the workspace's comm stream while
+// A_loc's SpMM runs, and A_halo's SpMM adds the halo terms once it has arrived.
+void do_spmv(const wl_operator* op, wl_workspace* ws, const double* y, int64_t ldy, const double* x,
              const double* g0, const double* g1, const double* scale, double* out, int B,
              cudaStream_t s, const int* active = nullptr) {
   if (!multi(op) || !op->split) {
-    halo_exchange(op, ws, y, B, B, s);
-    spmv_part(op, ws, op->A, false, y, x, g0, g1, scale, out, B, s, active);
+    halo_exchange(op, ws, y, ldy, (int)ldy, s);
+    spmv_part(op, ws, op->A, false, y, ldy, x, g0, g1, scale, out, B, s, active);
     return;
   }
-  pack_rows(y, B, op->send_idx.p, op->n_send, B, ws->halo_send.p, s);
+  const int w = (int)ldy;
+  pack_rows(y, ldy, op->send_idx.p, op->n_send, w, ws->halo_send.p, s);
   WL_CUDA(cudaEventRecord(ws->ev_pack, s));
   WL_CUDA(cudaStreamWaitEvent(ws->cstream, ws->ev_pack, 0));
   std::vector<Xfer> sends, recvs;
   for (int p = 0; p < op->nranks; ++p) {
     if (p == op->rank) continue;
     if (op->send_cnt[p] > 0)
-      sends.push_back({ws->halo_send.p + op->send_displ[p] * B, sizeof(double) * op->send_cnt[p] * B, p});
+      sends.push_back({ws->halo_send.p + op->send_displ[p] * w, sizeof(double) * op->send_cnt[p] * w, p});
     if (op->recv_cnt[p] > 0)
-      recvs.push_back({ws->halo_recv.p + op->recv_displ[p] * B, sizeof(double) * op->recv_cnt[p] * B, p});
+      recvs.push_back({ws->halo_recv.p + op->recv_displ[p] * w, sizeof(double) * op->recv_cnt[p] * w, p});
   }
   comm_sendrecv(op->comm, sends, recvs, ws->cstream);
   WL_CUDA(cudaEventRecord(ws->ev_halo, ws->cstream));
-  spmv_part(op, ws, op->A, false, y, x, g0, g1, scale, out, B, s, active);
+  spmv_part(op, ws, op->A, false, y, ldy, x, g0, g1, scale, out, B, s, active);
   WL_CUDA(cudaStreamWaitEvent(s, ws->ev_halo, 0));
-  spmv_part(op, ws, op->Ah, true, y, x, g0, g1, scale, out, B, s, active);
+  spmv_part(op, ws, op->Ah, true, y, ldy, x, g0, g1, scale, out, B, s, active);
 }
 
 // halo buffers, comm stream and events of a workspace (multi-rank)
@@ -379,7 +383,7 @@ void spmv_scratch(const wl_operator* op, wl_workspace* ws, int B) {
   ws_comm_init(op, ws, B);
   const int nch = std::max(op->A.n_chunks, op->Ah.n_chunks);  // the two parts run one after the other
   if (nch == 0) return;
-  if (ws->chunk_part.n < (size_t)nch * B) ws->chunk_part.alloc((size_t)nch * B);
+  if (ws->chunk_part.n < (size_t)nch * pad_cols(B)) ws->chunk_part.alloc((size_t)nch * pad_cols(B));
   if (ws->row_ticket.n < (size_t)nch) {
     ws->row_ticket.alloc(nch);
     WL_CUDA(cudaMemset(ws->row_ticket.p, 0, sizeof(unsigned int) * nch));
@@ -408,8 +412,8 @@ void krylov_chunk(const wl_operator* op, wl_workspace* ws, int mode, const doubl
   batch_inputs(V, ldv, B, n, ws->Vb.p, ws->vcol.p, perm, s);
   double* Q0 = ws->basis.p;
   // a3: seeds q_1 v = A v (top) and q_2 v = A(Av) - μ d⊙v (bottom)   (eq:qrec seeds)
-  do_spmv(op, ws, ws->Vb.p, nullptr, nullptr, nullptr, nullptr, Q0, B, s);
-  do_spmv(op, ws, Q0, ws->Vb.p, g0s, g1s, nullptr, Q0 + n_pad * B, B, s);
+  do_spmv(op, ws, ws->Vb.p, B, nullptr, nullptr, nullptr, nullptr, Q0, B, s);
+  do_spmv(op, ws, Q0, B, ws->Vb.p, g0s, g1s, nullptr, Q0 + n_pad * B, B, s);
   if (n_pad > n) {  // phantom rows of the seed vector and of S stay zero; the passes keep them so
     fill(Q0 + n * B, B, 0.0, s);
     fill(Q0 + (n_pad + n) * B, B, 0.0, s);
@@ -433,7 +437,7 @@ void krylov_chunk(const wl_operator* op, wl_workspace* ws, int mode, const doubl
   for (int j = 0; j < K; ++j) {
     double* Pj = const_cast<double*>(slot.p[j]);
     // a4: S = A Pj_bot + μ(μ - d) Pj_top — bottom half of Z p_j; its top half is Pj_bot
-    do_spmv(op, ws, Pj + n_pad * B, Pj, g0z, g1z, nullptr, ws->S.p, B, s);
+    do_spmv(op, ws, Pj + n_pad * B, B, Pj, g0z, g1z, nullptr, ws->S.p, B, s);
     d.Q = slot;
     d.nq = j;
     d.P = Pj;
@@ -513,13 +517,13 @@ void toar_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double*
     double* s1 = vs_ + (n + 1) * b;
     double* s2 = s1 + (n + 1) * b;
     batch_inputs(V, ldv, b, n, vs_, ws->vid.p, perm, s);
-    do_spmv(op, ws, vs_, nullptr, nullptr, nullptr, nullptr, s1, b, s);
-    do_spmv(op, ws, s1, nullptr, nullptr, nullptr, nullptr, s2, b, s);
+    do_spmv(op, ws, vs_, b, nullptr, nullptr, nullptr, nullptr, s1, b, s);
+    do_spmv(op, ws, s1, b, nullptr, nullptr, nullptr, nullptr, s2, b, s);
     seed_expand(s1, s2, vs_, b, op->degrp(), g1s, ws->vcol.p, B, n, U0, xb, s);
   } else {
     batch_inputs(V, ldv, B, n, ws->Vb.p, ws->vcol.p, perm, s);
-    do_spmv(op, ws, ws->Vb.p, nullptr, nullptr, nullptr, nullptr, U0, B, s);
-    do_spmv(op, ws, U0, ws->Vb.p, g0s, g1s, nullptr, xb, B, s);
+    do_spmv(op, ws, ws->Vb.p, B, nullptr, nullptr, nullptr, nullptr, U0, B, s);
+    do_spmv(op, ws, U0, B, ws->Vb.p, g0s, g1s, nullptr, xb, B, s);
   }
   if (n_pad > n) {
     fill(U0 + n * B, B, 0.0, s);
@@ -568,12 +572,21 @@ void toar_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double*
   t.out[0] = const_cast<double*>(U.p[1]);
   t.nout = 1;
   toar_update(t, s);
-  const double* xin = xb;  // bottom half of the vector the next SpMM applies Z to
+  // The SpMM gathers rows of x.  With B not a multiple of 4 they are kept in a second block xg whose
+  // rows are padded to ldg = 4 ceil(B/4) doubles (zero phantom columns), so every gathered row is
+  // whole 32-byte pieces for the 256-bit lane loads (spmv.cu): the update pass writes x there
+  // directly; the seed's x is repacked once.  (Tiled update passes, K + 1 > 32, keep ld B.)
+  const int64_t ldg = ws->xg.p ? pad_cols(B) : B;
+  const bool padx = ldg != B && K + 1 <= 32;
+  double* xg = padx ? ws->xg.p : xb;
+  if (padx) repack_rows(xb, B, n, B, xg, ldg, s);
+  const double* xin = xg;  // bottom half of the vector the next SpMM applies Z to
+  const int64_t ldx_in = padx ? ldg : B;
   const double* zin = U0;  // its top half
   for (int j = 0; j < K; ++j) {
     const int m = j + 2;
     // a4: y = A x + μ(μ - d)⊙z  (bottom half of Z [z; x])
-    do_spmv(op, ws, xin, zin, g0z, g1z, nullptr, yb, B, s);
+    do_spmv(op, ws, xin, ldx_in, zin, g0z, g1z, nullptr, yb, B, s);
     // a5: one dot pass (Gram row of the newest U vector, U^T y, |y|^2) and one update pass
     d.nq = m - 1;
     d.P = U.p[m - 1];
@@ -583,11 +596,13 @@ void toar_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double*
     t.m = m;
     t.y = yb;
     t.out[0] = const_cast<double*>(U.p[m]);
-    t.out[1] = xb;
+    t.out[1] = xg;
+    t.out_ld[1] = ldx_in;
     t.out[2] = zb;
     t.nout = 3;
     toar_update(t, s);
-    xin = xb;
+    t.out_ld[1] = 0;
+    xin = xg;
     zin = zb;
   }
   d.nq = K + 1;  // Gram row of the last U vector completes H column K-1
@@ -658,7 +673,7 @@ void cg_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double* V
   reduce_scalar(0);
   bool done = false;
   for (int it = 0; it < op->opts.cg_maxit && !done; ++it) {
-    do_spmv(op, ws, a.p, a.p, g0, g1, scale, a.q, B, s, a.flags + 1);  // q = 𝒜 p
+    do_spmv(op, ws, a.p, B, a.p, g0, g1, scale, a.q, B, s, a.flags + 1);  // q = 𝒜 p
     cg_dot(a, s);
     reduce_scalar(1);
     cg_update(a, s);
@@ -707,8 +722,8 @@ void workspace_alloc(wl_workspace* ws, const wl_operator* op, int max_b) {
   else ws->basis.alloc((size_t)(K + 2) * 2 * (n + 1) * B);  // halves padded by <= 1 phantom row
   ws->S.alloc((size_t)(n + 1) * B);
   ws->Vb.alloc((size_t)n * B);
-  if (op->n_halo > 0) ws->halo_recv.alloc((size_t)op->n_halo * B);
-  if (op->n_send > 0) ws->halo_send.alloc((size_t)op->n_send * B);
+  if (op->n_halo > 0) ws->halo_recv.alloc((size_t)op->n_halo * pad_cols(B));  // padded gathered rows
+  if (op->n_send > 0) ws->halo_send.alloc((size_t)op->n_send * pad_cols(B));
   const int grid = gram_grid(2 * n * B, B);
   ws->partials.alloc((size_t)grid * (2 * K + 5) * B);
   ws->ref.alloc(B);
@@ -740,6 +755,10 @@ void workspace_alloc(wl_workspace* ws, const wl_operator* op, int max_b) {
     ws->toar_cy.alloc((size_t)3 * B);
     ws->toar_cu.alloc((size_t)3 * (K + 3) * B);
     ws->toar_comb.alloc((size_t)(K + 2) * B);
+    if (pad_cols(B) != B) {  // phantom columns stay zero: only columns < B are ever written
+      ws->xg.alloc((size_t)(n + 1) * pad_cols(B));
+      WL_CUDA(cudaMemset(ws->xg.p, 0, sizeof(double) * (n + 1) * pad_cols(B)));
+    }
     ws->seed.alloc((size_t)3 * (n + 1) * std::max(1, std::min(max_b, kMaxCols)));
     std::vector<int> id(kMaxCols);
     std::iota(id.begin(), id.end(), 0);
@@ -1357,7 +1376,7 @@ wl_status wl_spectral_radius(const wl_operator* op, int32_t k, double* rho_out, 
     spmv_scratch(op, &ws, 1);
     fill(ws.oQ.p, op->n_loc, 1.0, s);
     outer_arnoldi(op, &ws, k, [&](const double* Pj, double* out) {
-      do_spmv(op, &ws, Pj, nullptr, nullptr, nullptr, nullptr, out, 1, s);  // A P̃_j
+      do_spmv(op, &ws, Pj, 1, nullptr, nullptr, nullptr, nullptr, out, 1, s);  // A P̃_j
     }, s);
     std::vector<double> H((size_t)(k + 1) * k);
     int keff = 0;
@@ -1398,7 +1417,7 @@ wl_status wl_spectral_radius_z(const wl_operator* op, int32_t theta_index, int32
     outer_arnoldi(op, &ws, k, [&](const double* Pj, double* out) {
       // Z (x; y) = (y; A y + μ(μ - d) x)   (eq:Zdef)
       WL_CUDA(cudaMemcpyAsync(out, Pj + np, sizeof(double) * np, cudaMemcpyDeviceToDevice, s));
-      do_spmv(op, &ws, Pj + np, Pj, g0z, g1z, nullptr, out + np, 1, s);
+      do_spmv(op, &ws, Pj + np, 1, Pj, g0z, g1z, nullptr, out + np, 1, s);
     }, s, len);
     std::vector<double> H((size_t)(k + 1) * k);
     int keff = 0;

@@ -301,6 +301,23 @@ void combine(int mode, double lscale, const VecPtrs& Q, int nvec, int64_t n, int
   WL_CUDA(cudaGetLastError());
 }
 
+namespace {
+__global__ void repack_rows_kernel(const double* src, int64_t lds, int64_t n, int B, double* dst, int64_t ldd) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n * B; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / B;
+    const int c = (int)(e - r * B);
+    dst[r * ldd + c] = src[r * lds + c];
+  }
+}
+}  // namespace
+
+void repack_rows(const double* src, int64_t lds, int64_t n, int B, double* dst, int64_t ldd, cudaStream_t s) {
+  if (n <= 0) return;
+  WL_LAUNCH("repack_rows");
+  repack_rows_kernel<<<grid_for(n * B), 256, 0, s>>>(src, lds, n, B, dst, ldd);
+  WL_CUDA(cudaGetLastError());
+}
+
 void sum_ranks(const SumSrc& src, int P, int64_t count, double* dst, cudaStream_t s) {
   if (count <= 0) return;
   WL_LAUNCH("allreduce_sum");

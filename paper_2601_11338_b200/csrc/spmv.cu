@@ -8,149 +8,219 @@
 // values, so the kernel only adds gathered rows — no value array is read.
 //
 // Power-law load balance by degree binning (built once per operator, B-independent):
-//   small rows  (deg <= 32, incl. isolated rows): one lane group (B lanes, lane c = column c of the
-//               row-major n x B blocks) per row, rows in id order so neighbouring groups read
-//               neighbouring col_idx ranges;
+//   small rows  (deg <= 32, incl. isolated rows): one lane group per row; rows with contiguous ids
+//               (the degree-sorted layout) go to the batched kernel (a warp per 32 rows);
 //   medium rows (32 < deg <= 2048): one warp per row, its lane groups split the nonzeros and are
 //               reduced with shuffles;
 //   hub rows    (deg > 2048): split into 2048-nonzero chunks, one warp per chunk; each chunk writes
 //               a partial and the last chunk to finish (per-row ticket) sums the row's partials in
 //               chunk order — deterministic, no second launch.
-// Every lane issues up to 8 independent gathers before consuming them (ILP), and all control flow
-// is uniform within a lane group.
+//
+// Lane groups and gather width.  A gathered row of the row-major block y holds B doubles.  A lane
+// loads VW consecutive doubles (VW = 1: 8 B; VW = 2: 16 B; VW = 4: 32 B, the sm_100 256-bit load
+// LDG.E.ENL2.256), so a row takes W = ceil(B / VW) lanes and one warp instruction gathers
+// gpw = 32 / W rows.  On this B200 the rate of random row gathers from L2 depends on it far more
+// than on bytes (tools/gather_ceiling.cu, C4 degree distribution, 4e8 rows of 11 columns):
+// 8-byte lanes (W = 11, 2 rows per instruction) 8.16 ms; 16-byte lanes 3.34 ms; 32-byte lanes
+// (W = 3, 10 rows per instruction) 3.02 ms.  VW > 1 needs ld y (and the halo's ld) a multiple of
+// VW and VW-aligned rows: the engine keeps the gathered operand of the TOAR steps in a block padded
+// to ld = 4 * ceil(B / 4) (zero phantom columns).  B = 1 uses VW = 1 with a thread per small row.
 #include "wl_internal.cuh"
 
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
 
+// compile-time tuning knobs (tools/build_variants.sh): wide-lane unroll, min CTAs per SM of the rows kernel
+#ifndef WL_SPMV_UW
+#define WL_SPMV_UW 4
+#endif
+#ifndef WL_SPMV_MINB
+#define WL_SPMV_MINB 6
+#endif
+#ifndef WL_SPMV_MINB_S
+#define WL_SPMV_MINB_S 3
+#endif
+
 namespace wl {
 namespace {
 
 constexpr int kThreads = 256;
-
-// Compile-time cache-hint experiment (build with WL_EXTRA_NVCC=-DWL_SPMV_HINTS=n): 1 = evict-first
-// ("cache streaming") loads/stores for the col / x / out streams, 2 = also evict-last for gathers of
-// the degree-sorted hot rows.  0 (default) = plain loads.
-#ifndef WL_SPMV_HINTS
-#define WL_SPMV_HINTS 0
-#endif
-__device__ __forceinline__ int ld_col(const int32_t* p) {
-#if WL_SPMV_HINTS >= 1
-  return __ldcs(p);
-#else
-  return __ldg(p);
-#endif
-}
-__device__ __forceinline__ double ld_stream(const double* p) {
-#if WL_SPMV_HINTS >= 1
-  return __ldcs(p);
-#else
-  return *p;
-#endif
-}
-__device__ __forceinline__ void st_stream(double* p, double v) {
-#if WL_SPMV_HINTS >= 1
-  __stcs(p, v);
-#else
-  *p = v;
-#endif
-}
 constexpr int kWarps = kThreads / 32;
 
-// Per-lane gather context.  Offsets are 32-bit (n_loc * ld < 2^31 is checked on the host), the
-// halo select exists only in the HALO instantiation, and only the last round of a range is
-// predicated (ncu r3: 18 warp instructions per nonzero before, mostly address/predicate work).
-template <int kU, bool HALO>
+template <int VW>
+struct Vec {
+  double v[VW];
+};
+
+template <int VW>
+__device__ __forceinline__ Vec<VW> vzero() {
+  Vec<VW> r;
+#pragma unroll
+  for (int k = 0; k < VW; ++k) r.v[k] = 0.0;
+  return r;
+}
+template <int VW>
+__device__ __forceinline__ void vadd(Vec<VW>& a, const Vec<VW>& b) {
+#pragma unroll
+  for (int k = 0; k < VW; ++k) a.v[k] += b.v[k];
+}
+// read-only (non-coherent) load of VW consecutive doubles, VW-aligned
+template <int VW>
+__device__ __forceinline__ Vec<VW> vload(const double* p) {
+  Vec<VW> r;
+  if constexpr (VW == 1) {
+    r.v[0] = __ldg(p);
+  } else if constexpr (VW == 2) {
+    const double2 t = __ldg(reinterpret_cast<const double2*>(p));
+    r.v[0] = t.x;
+    r.v[1] = t.y;
+  } else {
+    static_assert(VW == 4, "VW in {1, 2, 4}");
+    asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+        : "=d"(r.v[0]), "=d"(r.v[1]), "=d"(r.v[2]), "=d"(r.v[3])
+        : "l"(p));
+  }
+  return r;
+}
+
+// The same with an L2 eviction-priority policy (createpolicy): the hot prefix of the degree-sorted
+// gathered block is loaded evict_last, everything streamed once (column ids, cold rows) evict_first.
+template <int VW>
+__device__ __forceinline__ Vec<VW> vload_hint(const double* p, uint64_t pol) {
+  Vec<VW> r;
+  if constexpr (VW == 1) {
+    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r.v[0]) : "l"(p), "l"(pol));
+  } else if constexpr (VW == 2) {
+    asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(r.v[0]), "=d"(r.v[1]) : "l"(p), "l"(pol));
+  } else {
+    asm("ld.global.nc.L2::cache_hint.v4.f64 {%0, %1, %2, %3}, [%4], %5;"
+        : "=d"(r.v[0]), "=d"(r.v[1]), "=d"(r.v[2]), "=d"(r.v[3])
+        : "l"(p), "l"(pol));
+  }
+  return r;
+}
+__device__ __forceinline__ int ld_col_hint(const int32_t* p, uint64_t pol) {
+  int v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
+// Per-lane gather context.  Lane group gi of W lanes handles one row at a time; lane (gi, w) owns
+// columns c0 = w*VW .. c0+VW-1 (those < B are real).  Offsets are 32-bit (n_loc * ld < 2^31 is
+// checked on the host); the halo select exists only in the HALO instantiation, and only the last
+// round of a range is predicated.
+template <int kU, bool HALO, int VW, bool HINT = false>
 struct Ctx {
   const SpmvArgs& a;
-  int c;
-  double g0, g1, sc;
-  const double* yc;   // y + c
-  const double* yhc;  // yh + c
+  uint64_t pol_last = 0, pol_first = 0;  // HINT: L2 policies
+  int c0;             // first column of this lane
+  int nc;             // real columns of this lane (0..VW)
+  const double* yc;   // y + c0
+  const double* yhc;  // yh + c0
   int ldy, ldh;
-  uint64_t pol = 0;  // L2 evict-last policy (WL_SPMV_HINTS >= 2)
-  __device__ double gather(int cl) const {
-    if (HALO && cl >= a.n_loc) return __ldg(yhc + (cl - a.n_loc) * ldh);
-#if WL_SPMV_HINTS >= 2
-    if (cl < a.small_first) {
-      double v;
-      asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(yc + cl * ldy), "l"(pol));
-      return v;
+  __device__ Ctx(const SpmvArgs& args, int col0) : a(args), c0(col0) {
+    nc = max(0, min(VW, a.B - c0));
+    yc = a.y + c0;
+    yhc = a.yh + c0;
+    ldy = (int)a.ldy;
+    ldh = (int)a.ldh;
+    if (HINT) {
+      asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_last));
+      asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
     }
-#endif
-    return __ldg(yc + cl * ldy);
+  }
+  __device__ Vec<VW> gather(int cl) const {
+    if (HALO && cl >= a.n_loc) {
+      if (HINT) return vload_hint<VW>(yhc + (cl - a.n_loc) * ldh, pol_first);
+      return vload<VW>(yhc + (cl - a.n_loc) * ldh);
+    }
+    if (HINT) return vload_hint<VW>(yc + cl * ldy, cl < a.hot_rows ? pol_last : pol_first);
+    return vload<VW>(yc + cl * ldy);
+  }
+  __device__ int col(int z) const {
+    if (HINT) return ld_col_hint(a.col + z, pol_first);
+    return __ldg(a.col + z);
   }
   // row r of this CSR -> output row a.out_row[r]; the γ term uses d_r from a.degptr when given
-  // (the A_loc part of a split operator); the A_halo part accumulates into out
-  __device__ void write(int r, int deg, double sum) const {
+  // (the A_loc part of a split operator); the A_halo part accumulates into out.  `x` (the diagonal
+  // operand, ld ldx) and out (ld ldo) are unpadded: per-column scalar accesses.
+  __device__ void write(int r, int deg, const Vec<VW>& sum, const double* xrow = nullptr) const {
     const int ro = a.out_row ? __ldg(a.out_row + r) : r;
-    double o = sum;
-    if (a.x) {
-      if (a.degptr) deg = __ldg(a.degptr + ro + 1) - __ldg(a.degptr + ro);
-      o += (g0 + g1 * (double)deg) * ld_stream(a.x + (int64_t)ro * a.ldx + c);
+    if (a.x && a.degptr) deg = __ldg(a.degptr + ro + 1) - __ldg(a.degptr + ro);
+    double* dst = a.out + (int64_t)ro * a.ldo + c0;
+    const double* xs = xrow ? xrow : a.x + (int64_t)ro * a.ldx + c0;
+    // per-column constants are read here (L1-resident, B values) rather than held in registers
+#pragma unroll
+    for (int k = 0; k < VW; ++k) {
+      if (k < nc) {
+        const int c = c0 + k;
+        double o = sum.v[k];
+        if (a.x) o += ((a.g0 ? __ldg(a.g0 + c) : 0.0) + (a.g1 ? __ldg(a.g1 + c) : 0.0) * (double)deg) * xs[k];
+        const double sc = a.scale ? __ldg(a.scale + c) : 1.0;
+        dst[k] = a.accumulate ? dst[k] + sc * o : sc * o;
+      }
     }
-    double* dst = a.out + (int64_t)ro * a.ldo + c;
-    st_stream(dst, a.accumulate ? *dst + sc * o : sc * o);
   }
   // Σ y[col[z]] for z = z0 + first, z0 + first + step, ... < z1 (step = lane groups sharing the row)
-  __device__ double strided_sum(int z0, int z1, int first, int step) const {
-    double acc = 0.0;
+  __device__ Vec<VW> strided_sum(int z0, int z1, int first, int step) const {
+    Vec<VW> acc = vzero<VW>();
     int z = z0 + first;
     const int full = z1 - (kU - 1) * step;  // rounds with all kU nonzeros present
     for (; z < full; z += kU * step) {
       int cl[kU];
 #pragma unroll
-      for (int u = 0; u < kU; ++u) cl[u] = ld_col(a.col + z + u * step);
-      double v[kU];
+      for (int u = 0; u < kU; ++u) cl[u] = col(z + u * step);
+      Vec<VW> v[kU];
 #pragma unroll
       for (int u = 0; u < kU; ++u) v[u] = gather(cl[u]);
 #pragma unroll
-      for (int u = 0; u < kU; ++u) acc += v[u];
+      for (int u = 0; u < kU; ++u) vadd(acc, v[u]);
     }
     if (z < z1) {  // predicated tail round
       int cl[kU];
 #pragma unroll
-      for (int u = 0; u < kU; ++u) cl[u] = (z + u * step < z1) ? ld_col(a.col + z + u * step) : -1;
-      double v[kU];
+      for (int u = 0; u < kU; ++u) cl[u] = (z + u * step < z1) ? col(z + u * step) : -1;
+      Vec<VW> v[kU];
 #pragma unroll
-      for (int u = 0; u < kU; ++u) v[u] = cl[u] >= 0 ? gather(cl[u]) : 0.0;
+      for (int u = 0; u < kU; ++u) v[u] = cl[u] >= 0 ? gather(cl[u]) : vzero<VW>();
 #pragma unroll
-      for (int u = 0; u < kU; ++u) acc += v[u];
+      for (int u = 0; u < kU; ++u) vadd(acc, v[u]);
     }
     return acc;
   }
 };
 
-// sum of `v` over the lane groups of a warp, result valid in group 0 (lanes 0..B-1)
-__device__ inline double group_reduce(double v, int B, int gpw) {
-  if ((B & (B - 1)) == 0) {
-    for (int off = 16; off >= B; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+// sum of `v` over the lane groups (W lanes each) of a warp, result valid in group 0 (lanes 0..W-1)
+template <int VW>
+__device__ inline Vec<VW> group_reduce(Vec<VW> v, int W, int gpw) {
+  if ((W & (W - 1)) == 0) {
+#pragma unroll
+    for (int k = 0; k < VW; ++k)
+      for (int off = 16; off >= W; off >>= 1) v.v[k] += __shfl_down_sync(0xffffffffu, v.v[k], off);
     return v;
   }
   const int lane = threadIdx.x & 31;
-  double s = v;
+  Vec<VW> s = v;
   for (int g = 1; g < gpw; ++g) {
-    const double o = __shfl_sync(0xffffffffu, v, (lane + g * B) & 31);
-    s += o;
+#pragma unroll
+    for (int k = 0; k < VW; ++k) s.v[k] += __shfl_sync(0xffffffffu, v.v[k], (lane + g * W) & 31);
   }
   return s;
 }
 
-template <int kU, bool HALO>
-__global__ void __launch_bounds__(kThreads) spmv_binned_kernel(SpmvArgs a) {
+template <int VW>
+__device__ __forceinline__ int lanes_per_row(int B) { return (B + VW - 1) / VW; }
+
+template <int kU, bool HALO, int VW, bool HINT>
+__global__ void __launch_bounds__(kThreads, VW == 1 ? 1 : WL_SPMV_MINB) spmv_binned_kernel(SpmvArgs a) {
   if (a.active && *a.active == 0) return;
-  const int B = a.B;
+  const int W = lanes_per_row<VW>(a.B);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int gpw = 32 / B;
-  const int gi = lane / B, c = lane - gi * B;
+  const int gpw = 32 / W;
+  const int gi = lane / W, w = lane - gi * W;
   const bool lane_ok = gi < gpw;
-  const int cc = lane_ok ? c : 0;
-  Ctx<kU, HALO> ctx{a, cc, a.g0 ? a.g0[cc] : 0.0, a.g1 ? a.g1[cc] : 0.0, a.scale ? a.scale[cc] : 1.0,
-                    a.y + cc, a.yh + cc, (int)a.ldy, (int)a.ldh};
-#if WL_SPMV_HINTS >= 2
-  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(ctx.pol));
-#endif
+  const Ctx<kU, HALO, VW, HINT> ctx(a, lane_ok ? w * VW : 0);
   int blk = blockIdx.x;
   if (blk < a.nblk_small) {  // ---- small rows: one lane group per row
     const int idx = (blk * kWarps + warp) * gpw + gi;
@@ -166,8 +236,8 @@ __global__ void __launch_bounds__(kThreads) spmv_binned_kernel(SpmvArgs a) {
     if (idx >= a.n_medium) return;
     const int r = a.medium_rows[idx];
     const int z0 = __ldg(a.rowptr + r), z1 = __ldg(a.rowptr + r + 1);
-    const double part = lane_ok ? ctx.strided_sum(z0, z1, gi, gpw) : 0.0;
-    const double sum = group_reduce(part, B, gpw);
+    const Vec<VW> part = lane_ok ? ctx.strided_sum(z0, z1, gi, gpw) : vzero<VW>();
+    const Vec<VW> sum = group_reduce<VW>(part, W, gpw);
     if (gi == 0) ctx.write(r, z1 - z0, sum);
     return;
   }
@@ -176,9 +246,13 @@ __global__ void __launch_bounds__(kThreads) spmv_binned_kernel(SpmvArgs a) {
     const int idx = blk * kWarps + warp;
     if (idx >= a.n_chunks) return;
     const int4 ch = a.chunks[idx];  // (row, z0, z1, first chunk index of the row)
-    const double part = lane_ok ? ctx.strided_sum(ch.y, ch.z, gi, gpw) : 0.0;
-    const double sum = group_reduce(part, B, gpw);
-    if (gi == 0) a.chunk_part[(int64_t)idx * B + c] = sum;
+    const Vec<VW> part = lane_ok ? ctx.strided_sum(ch.y, ch.z, gi, gpw) : vzero<VW>();
+    const Vec<VW> sum = group_reduce<VW>(part, W, gpw);
+    const int ldp = W * VW;  // partial row: every column slot of the lane group
+    if (gi == 0) {
+#pragma unroll
+      for (int k = 0; k < VW; ++k) a.chunk_part[(int64_t)idx * ldp + w * VW + k] = sum.v[k];
+    }
     __threadfence();
     __syncwarp();
     unsigned ticket = 0;
@@ -189,8 +263,10 @@ __global__ void __launch_bounds__(kThreads) spmv_binned_kernel(SpmvArgs a) {
     if (ticket != (unsigned)(nch - 1)) return;
     __threadfence();
     if (gi == 0) {
-      double tot = 0.0;
-      for (int k = 0; k < nch; ++k) tot += __ldcg(a.chunk_part + (int64_t)(ch.w + k) * B + c);
+      Vec<VW> tot = vzero<VW>();
+      for (int k = 0; k < nch; ++k)
+#pragma unroll
+        for (int q = 0; q < VW; ++q) tot.v[q] += __ldcg(a.chunk_part + (int64_t)(ch.w + k) * ldp + w * VW + q);
       ctx.write(ch.x, z1r - z0r, tot);
     }
     if (lane == 0) a.row_ticket[ch.w] = 0u;
@@ -204,25 +280,21 @@ __global__ void __launch_bounds__(kThreads) spmv_binned_kernel(SpmvArgs a) {
 // each lane group then walks its share of the batch's nonzeros in rounds of kU gathers,
 // flushing rows as their ranges end: ~1 latency per kU gathers instead of ~3 per row.  The rounds
 // are software-pipelined (round r+1's gathers issue before round r is summed): 39.7 -> 32.0 ms/step
-// on C4.  (The same pipelining in the medium/hub path costs registers and occupancy: +38 ms.)
-template <int kU, bool HALO>
-__global__ void __launch_bounds__(kThreads) spmv_small_batched_kernel(SpmvArgs a) {
+// on C4 at VW = 1.
+template <int kU, bool HALO, int VW, bool HINT>
+__global__ void __launch_bounds__(kThreads, WL_SPMV_MINB_S) spmv_small_batched_kernel(SpmvArgs a) {
   if (a.active && *a.active == 0) return;
   extern __shared__ __align__(16) int s_small[];
   constexpr int kColCap = 32 * kSmallMax;  // max nonzeros of a 32-row batch
   constexpr int kIntsPerWarp = kColCap + 40;
   const int B = a.B, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int gpw = 32 / B, gi = lane / B, c = lane - gi * B;
+  const int W = lanes_per_row<VW>(B);
+  const int gpw = 32 / W, gi = lane / W, w = lane - gi * W;
   const bool lane_ok = gi < gpw;
-  const int cc = lane_ok ? c : 0;
   int* scol = s_small + warp * kIntsPerWarp;
   int* srow = scol + kColCap;
   double* sx = reinterpret_cast<double*>(s_small + kWarps * kIntsPerWarp) + warp * 32 * B;
-  Ctx<kU, HALO> ctx{a, cc, a.g0 ? a.g0[cc] : 0.0, a.g1 ? a.g1[cc] : 0.0, a.scale ? a.scale[cc] : 1.0,
-                    a.y + cc, a.yh + cc, (int)a.ldy, (int)a.ldh};
-#if WL_SPMV_HINTS >= 2
-  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(ctx.pol));
-#endif
+  const Ctx<kU, HALO, VW, HINT> ctx(a, lane_ok ? w * VW : 0);
   const int nb = (a.n_small + 31) / 32;
   for (int bt = blockIdx.x * kWarps + warp; bt < nb; bt += gridDim.x * kWarps) {
     const int r0 = a.small_first + bt * 32;
@@ -234,43 +306,39 @@ __global__ void __launch_bounds__(kThreads) spmv_small_batched_kernel(SpmvArgs a
     if (lane == 0) srow[32] = Z1 - Z0;
     const int T = Z1 - Z0;
 #pragma unroll 4
-    for (int p = lane; p < T; p += 32) scol[p] = ld_col(a.col + Z0 + p);
+    for (int p = lane; p < T; p += 32) scol[p] = ctx.col(Z0 + p);
     if (a.x)
-      for (int e = lane; e < nr * B; e += 32) sx[e] = ld_stream(a.x + (int64_t)r0 * B + e);
+      for (int e = lane; e < nr * B; e += 32) sx[e] = a.x[(int64_t)r0 * B + e];
     __syncwarp();
     if (lane_ok) {
       const int ia = gi * nr / gpw, ib = (gi + 1) * nr / gpw;  // this group's rows
-      auto flush = [&](int i, double acc) {
-        double o = acc;
-        if (a.x) {
-          const int d = a.degptr ? __ldg(a.degptr + r0 + i + 1) - __ldg(a.degptr + r0 + i) : srow[i + 1] - srow[i];
-          o += (ctx.g0 + ctx.g1 * (double)d) * sx[i * B + c];
-        }
-        st_stream(a.out + (int64_t)(r0 + i) * a.ldo + c, ctx.sc * o);
+      auto flush = [&](int i, const Vec<VW>& acc) {
+        const int d = a.degptr ? 0 : srow[i + 1] - srow[i];  // (degptr: write() reads d_r itself)
+        ctx.write(r0 + i, d, acc, sx + i * B + ctx.c0);
       };
       int cur = ia, rend = srow[ia + 1];
       const int P1 = srow[ib];
-      double acc = 0.0;
+      Vec<VW> acc = vzero<VW>();
       // software pipeline: round r+1's gathers are issued before round r is consumed
-      double v[kU];
+      Vec<VW> v[kU];
       {
         const int p = srow[ia];
 #pragma unroll
-        for (int u = 0; u < kU; ++u) v[u] = p + u < P1 ? ctx.gather(scol[p + u]) : 0.0;
+        for (int u = 0; u < kU; ++u) v[u] = p + u < P1 ? ctx.gather(scol[p + u]) : vzero<VW>();
       }
       for (int p = srow[ia]; p < P1; p += kU) {
-        double vn[kU];
+        Vec<VW> vn[kU];
 #pragma unroll
-        for (int u = 0; u < kU; ++u) vn[u] = p + kU + u < P1 ? ctx.gather(scol[p + kU + u]) : 0.0;
+        for (int u = 0; u < kU; ++u) vn[u] = p + kU + u < P1 ? ctx.gather(scol[p + kU + u]) : vzero<VW>();
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
           if (p + u < P1) {
             while (p + u >= rend) {
               flush(cur, acc);
-              acc = 0.0;
+              acc = vzero<VW>();
               rend = srow[++cur + 1];
             }
-            acc += v[u];
+            vadd(acc, v[u]);
           }
         }
 #pragma unroll
@@ -278,7 +346,7 @@ __global__ void __launch_bounds__(kThreads) spmv_small_batched_kernel(SpmvArgs a
       }
       for (; cur < ib; ++cur) {  // the last row with nonzeros and any empty rows after it
         flush(cur, acc);
-        acc = 0.0;
+        acc = vzero<VW>();
       }
     }
     __syncwarp();
@@ -289,13 +357,12 @@ __global__ void __launch_bounds__(kThreads) spmv_small_batched_kernel(SpmvArgs a
 // At B = 1 a 32-row batch is one row per lane, so the batched kernel's staging buys nothing and its
 // per-batch chain (rowptr -> col -> smem -> gather) plus warp syncs dominates.  A thread per row
 // keeps the same three dependent loads with ~8x the rows in flight per SM.
-template <bool HALO>
+template <bool HALO, bool HINT>
 __global__ void __launch_bounds__(kThreads) spmv_small_row1_kernel(SpmvArgs a) {
   if (a.active && *a.active == 0) return;
   const int i = blockIdx.x * kThreads + threadIdx.x;
   if (i >= a.n_small) return;
-  Ctx<4, HALO> ctx{a, 0, a.g0 ? a.g0[0] : 0.0, a.g1 ? a.g1[0] : 0.0, a.scale ? a.scale[0] : 1.0,
-                   a.y, a.yh, (int)a.ldy, (int)a.ldh};
+  const Ctx<4, HALO, 1, HINT> ctx(a, 0);
   const int r = a.small_first + i;
   const int z0 = __ldg(a.rowptr + r), z1 = __ldg(a.rowptr + r + 1);
   ctx.write(r, z1 - z0, ctx.strided_sum(z0, z1, 0, 1));
@@ -305,46 +372,20 @@ size_t small_batched_smem(int B) {
   return (size_t)kWarps * ((32 * kSmallMax + 40) * sizeof(int) + 32 * B * sizeof(double));
 }
 
-}  // namespace
+template <int VW>
+constexpr int unroll_for() { return VW == 1 ? 8 : WL_SPMV_UW; }  // wide lanes: 4 rounds in flight
+template <int VW>
+constexpr int unroll_batched() { return VW == 1 ? 8 : VW == 2 ? 4 : 2; }  // pipelined: 2 rounds live
 
-void spmv(const SpmvArgs& a0, cudaStream_t s) {
-  if (a0.B < 1 || a0.B > kMaxCols) throw Error(1, "spmv: B out of range");
-  SpmvArgs a = a0;
-  const int gpw = 32 / a.B;
-  a.nblk_small = (a.n_small + kWarps * gpw - 1) / (kWarps * gpw);
-  a.nblk_medium = (a.n_medium + kWarps - 1) / kWarps;
-  const int nblk_hub = (a.n_chunks + kWarps - 1) / kWarps;
-  const int grid = a.nblk_small + a.nblk_medium + nblk_hub;
-  if (grid <= 0) return;
-  static const int U = [] { const char* v = getenv("WL_SPMV_U"); return v ? atoi(v) : 8; }();
-  static const bool split = getenv("WL_SPMV_SPLIT") != nullptr;  // per-class timing experiment
-  // gather offsets are 32-bit: local rows (col < n_loc) at col * ldy, halo rows at (col - n_loc) * ldh
-  if ((int64_t)(a.n_loc + 1) * a.ldy >= INT32_MAX || (a.yh && (int64_t)(a.n_halo + 1) * a.ldh >= INT32_MAX))
-    throw Error(8, "spmv: n_loc * ld and n_halo * ldh must be < 2^31 (32-bit gather offsets)");
-  const bool halo = a.yh != nullptr;
-  auto go = [&](const SpmvArgs& aa, int g) {
-    if (halo) {
-      if (U >= 16) spmv_binned_kernel<16, true><<<g, kThreads, 0, s>>>(aa);
-      else spmv_binned_kernel<8, true><<<g, kThreads, 0, s>>>(aa);
-    } else {
-      if (U >= 16) spmv_binned_kernel<16, false><<<g, kThreads, 0, s>>>(aa);
-      else spmv_binned_kernel<8, false><<<g, kThreads, 0, s>>>(aa);
-    }
-    WL_CUDA(cudaGetLastError());
-  };
-  // small rows with contiguous ids (x rows contiguous too): the batched kernel takes them
-  static const bool batched_on = [] { const char* v = getenv("WL_SPMV_BATCHED"); return v ? atoi(v) != 0 : true; }();
-  const bool batched = batched_on && a.small_first >= 0 && a.n_small > 0 && (a.x == nullptr || a.ldx == a.B);
-  static const bool row1_on = [] { const char* v = getenv("WL_SPMV_ROW1"); return v ? atoi(v) != 0 : true; }();
-  auto go_small = [&]() {
-    if (a.B == 1 && row1_on) {
-      const int g = (a.n_small + kThreads - 1) / kThreads;
-      if (halo) spmv_small_row1_kernel<true><<<g, kThreads, 0, s>>>(a);
-      else spmv_small_row1_kernel<false><<<g, kThreads, 0, s>>>(a);
-      WL_CUDA(cudaGetLastError());
-      return;
-    }
-    auto kern = halo ? spmv_small_batched_kernel<8, true> : spmv_small_batched_kernel<8, false>;
+// launch the batched small rows (if any) and the binned kernel (small rows by id list, medium, hub)
+template <int VW, bool HINT>
+void launch_vw(const SpmvArgs& a, bool halo, bool batched, int grid_rest, cudaStream_t s) {
+  constexpr int kU = unroll_for<VW>(), kUb = unroll_batched<VW>();
+  static const bool split = getenv("WL_SPMV_SPLIT") != nullptr;  // per-class timing (profiling only)
+  SpmvArgs t = a;
+  if (batched) {
+    LaunchScope ls(split ? "spmv_small_batched" : nullptr, s);
+    auto kern = halo ? spmv_small_batched_kernel<kUb, true, VW, HINT> : spmv_small_batched_kernel<kUb, false, VW, HINT>;
     const size_t smem = small_batched_smem(a.B);
     static bool attr[2] = {false, false};
     if (!attr[halo]) {
@@ -353,63 +394,92 @@ void spmv(const SpmvArgs& a0, cudaStream_t s) {
     }
     int occ = 0;
     WL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem));
-    const int sms = num_sms();
     const int nb = (a.n_small + 31) / 32;
-    const int g = std::max(1, std::min((nb + kWarps - 1) / kWarps, sms * std::max(occ, 1)));
+    const int g = std::max(1, std::min((nb + kWarps - 1) / kWarps, num_sms() * std::max(occ, 1)));
     kern<<<g, kThreads, smem, s>>>(a);
     WL_CUDA(cudaGetLastError());
-  };
-  if (batched) {
-    SpmvArgs t = a;
     t.n_small = 0;
     t.nblk_small = 0;
-    if (!split) {
-      WL_LAUNCH("spmv_binned");
-      go_small();
-      if (grid - a.nblk_small > 0) go(t, grid - a.nblk_small);
-      return;
-    }
-    {
-      WL_LAUNCH("spmv_small");
-      go_small();
-    }
-    {
-      WL_LAUNCH("spmv_medium");
-      SpmvArgs m = t;
-      m.n_chunks = 0;
-      if (m.nblk_medium) go(m, m.nblk_medium);
-    }
-    {
-      WL_LAUNCH("spmv_hub");
-      SpmvArgs h = t;
-      h.n_medium = 0; h.nblk_medium = 0;
-      if (nblk_hub) go(h, nblk_hub);
+  }
+  if (grid_rest <= 0) return;
+  LaunchScope ls(split ? "spmv_rows" : nullptr, s);
+  if (halo) spmv_binned_kernel<kU, true, VW, HINT><<<grid_rest, kThreads, 0, s>>>(t);
+  else spmv_binned_kernel<kU, false, VW, HINT><<<grid_rest, kThreads, 0, s>>>(t);
+  WL_CUDA(cudaGetLastError());
+}
+
+template <int VW>
+void launch_vw(const SpmvArgs& a, bool halo, bool batched, int grid_rest, cudaStream_t s) {
+  if (a.hot_rows > 0) launch_vw<VW, true>(a, halo, batched, grid_rest, s);
+  else launch_vw<VW, false>(a, halo, batched, grid_rest, s);
+}
+
+inline bool aligned(const void* p, int bytes) { return (reinterpret_cast<uintptr_t>(p) % bytes) == 0; }
+
+}  // namespace
+
+// widest lane load the gathered operand allows (see the file comment)
+int spmv_vector_width(const SpmvArgs& a) {
+  if (a.B == 1) return 1;
+  const bool halo = a.yh != nullptr;
+  for (int vw : {4, 2}) {
+    if (a.ldy % vw == 0 && aligned(a.y, 8 * vw) && (!halo || (a.ldh % vw == 0 && aligned(a.yh, 8 * vw)))) return vw;
+  }
+  return 1;
+}
+
+void spmv(const SpmvArgs& a0, cudaStream_t s) {
+  if (a0.B < 1 || a0.B > kMaxCols) throw Error(1, "spmv: B out of range");
+  SpmvArgs a = a0;
+  // L2 eviction hints: rows [0, hot_rows) of the degree-sorted gathered block (the most gathered
+  // rows) stay, column ids and cold rows go first.  Budget WL_SPMV_HOT_MB of L2 (0 = no hints).
+  static const double hot_mb = [] { const char* v = getenv("WL_SPMV_HOT_MB"); return v ? atof(v) : 0.0; }();
+  if (hot_mb > 0.0 && a.hot_rows == 0)
+    a.hot_rows = (int)std::min<int64_t>(a.n_loc, (int64_t)(hot_mb * 1e6 / (8.0 * a.ldy)));
+  static const int vw_cap = [] { const char* v = getenv("WL_SPMV_VW"); return v ? atoi(v) : 4; }();
+  int VW = spmv_vector_width(a);
+  while (VW > vw_cap) VW /= 2;
+  const int W = (a.B + VW - 1) / VW;
+  const int gpw = 32 / W;
+  a.nblk_small = (a.n_small + kWarps * gpw - 1) / (kWarps * gpw);
+  a.nblk_medium = (a.n_medium + kWarps - 1) / kWarps;
+  const int nblk_hub = (a.n_chunks + kWarps - 1) / kWarps;
+  const int grid = a.nblk_small + a.nblk_medium + nblk_hub;
+  if (grid <= 0) return;
+  // gather offsets are 32-bit: local rows (col < n_loc) at col * ldy, halo rows at (col - n_loc) * ldh
+  if ((int64_t)(a.n_loc + 1) * a.ldy >= INT32_MAX || (a.yh && (int64_t)(a.n_halo + 1) * a.ldh >= INT32_MAX))
+    throw Error(8, "spmv: n_loc * ld and n_halo * ldh must be < 2^31 (32-bit gather offsets)");
+  if (a.out_row && a.small_first >= 0) throw Error(1, "spmv: batched small rows cannot remap output rows");
+  const bool halo = a.yh != nullptr;
+  WL_LAUNCH("spmv_binned");
+  if (a.B == 1) {
+    if (a.small_first >= 0 && a.n_small > 0) {  // thread per small row
+      static const bool split = getenv("WL_SPMV_SPLIT") != nullptr;
+      LaunchScope ls(split ? "spmv_small_row1" : nullptr, s);
+      const int g = (a.n_small + kThreads - 1) / kThreads;
+      if (a.hot_rows > 0) {
+        if (halo) spmv_small_row1_kernel<true, true><<<g, kThreads, 0, s>>>(a);
+        else spmv_small_row1_kernel<false, true><<<g, kThreads, 0, s>>>(a);
+      } else {
+        if (halo) spmv_small_row1_kernel<true, false><<<g, kThreads, 0, s>>>(a);
+        else spmv_small_row1_kernel<false, false><<<g, kThreads, 0, s>>>(a);
+      }
+      WL_CUDA(cudaGetLastError());
+      SpmvArgs t = a;
+      t.n_small = 0;
+      t.nblk_small = 0;
+      launch_vw<1>(t, halo, false, grid - a.nblk_small, s);
+    } else {
+      launch_vw<1>(a, halo, false, grid, s);
     }
     return;
   }
-  if (!split) {
-    WL_LAUNCH("spmv_binned");
-    go(a, grid);
-    return;
-  }
-  {
-    WL_LAUNCH("spmv_small");
-    SpmvArgs t = a;
-    t.n_medium = 0; t.nblk_medium = 0; t.n_chunks = 0;
-    if (t.nblk_small) go(t, t.nblk_small);
-  }
-  {
-    WL_LAUNCH("spmv_medium");
-    SpmvArgs t = a;
-    t.n_small = 0; t.nblk_small = 0; t.n_chunks = 0;
-    if (t.nblk_medium) go(t, t.nblk_medium);
-  }
-  {
-    WL_LAUNCH("spmv_hub");
-    SpmvArgs t = a;
-    t.n_small = 0; t.nblk_small = 0; t.n_medium = 0; t.nblk_medium = 0;
-    if (nblk_hub) go(t, nblk_hub);
-  }
+  // small rows with contiguous ids (x rows contiguous too): the batched kernel takes them
+  const bool batched = a.small_first >= 0 && a.n_small > 0 && (a.x == nullptr || a.ldx == a.B);
+  const int rest = batched ? grid - a.nblk_small : grid;
+  if (VW == 4) launch_vw<4>(a, halo, batched, rest, s);
+  else if (VW == 2) launch_vw<2>(a, halo, batched, rest, s);
+  else launch_vw<1>(a, halo, batched, rest, s);
 }
 
 }  // namespace wl

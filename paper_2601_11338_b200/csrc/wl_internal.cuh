@@ -46,6 +46,8 @@ wl_status guarded(F&& f) {
 }
 
 int num_sms();  // SMs of the current device (cached per device)
+// row width of a gathered block of B columns: whole 32-byte pieces for B > 1 (spmv.cu 256-bit lanes)
+inline int pad_cols(int B) { return B <= 1 ? B : (B + 3) / 4 * 4; }
 
 constexpr int kMaxCols = 32;    // columns per Krylov batch (B)
 constexpr int kMaxKrylov = 64;  // Arnoldi steps per action
@@ -86,6 +88,7 @@ struct SpmvArgs {
   const int32_t* degptr;             // row pointer giving d_i for the γ term (null: this CSR's rowptr)
   const int32_t* out_row;            // output row of CSR row i (null: i); not with the batched small rows
   int accumulate;                    // out += scale * Σ (no diagonal term): the A_halo part
+  int hot_rows;                      // > 0: L2 evict_last hints for gathered rows < hot_rows (degree-sorted)
   int B;
   const int* active;                 // optional (CG): the launch does nothing when *active == 0
 };
@@ -127,6 +130,7 @@ struct ToarArgs {
   int64_t len; int B;
   const double* y;
   double* out[3]; int nout;
+  int64_t out_ld[3];                  // row stride of output o (0 = B); > B only without tiling (m <= 32)
   const double* coef_y;
   const double* coef_u; int coef_ld;
   int accumulate;
@@ -212,6 +216,8 @@ void combine(int mode, double lscale, const VecPtrs& Q, int nvec, int64_t n, int
              const int32_t* perm, cudaStream_t s);
 void pack_rows(const double* src, int64_t lds, const int32_t* idx, int64_t cnt, int B, double* dst,
                cudaStream_t s);
+// dst[r * ldd + c] = src[r * lds + c] for c < B (other columns of dst untouched), r < n
+void repack_rows(const double* src, int64_t lds, int64_t n, int B, double* dst, int64_t ldd, cudaStream_t s);
 void fill(double* p, int64_t n, double v, cudaStream_t s);
 // sticky convergence flag: flag[0] |= 1 and flag[1] = max estimate (as bits) when err[c] > tol
 void krylov_check(const double* err, int B, double tol, int* flag, cudaStream_t s);
