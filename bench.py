@@ -99,10 +99,43 @@ def dist_setup(ngpus):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != ngpus:
-        if world == 1 and ngpus > 1:
-            raise SystemExit("--gpus N>1 must be launched with torchrun (one process per GPU)")
+    if world != ngpus and "WORLD_SIZE" in os.environ:
+        raise SystemExit(f"--gpus {ngpus} but WORLD_SIZE={world}")
     return world, rank, local
+
+
+def host_info() -> dict:
+    """The host the CPU baseline ran on: CPU model, logical cores, BLAS threads."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    blas = None
+    try:
+        from threadpoolctl import threadpool_info
+        blas = [{"api": d.get("internal_api"), "threads": d.get("num_threads")} for d in threadpool_info()]
+    except Exception:
+        pass
+    return {"cpu_model": model, "os_cpu_count": os.cpu_count(), "blas": blas}
+
+
+def self_spawn(ngpus: int) -> int:
+    """`bench.py --gpus N` without a launcher: start N ranks (one process per GPU) through
+    torch.distributed.run on 127.0.0.1 with this same command line; rank 0 prints the JSON line."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={ngpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    log("self-spawn:", " ".join(cmd))
+    return subprocess.call(cmd)
 
 
 def load_graph(cfg, world, rank, torch, dist):
@@ -387,7 +420,7 @@ def cpu_baseline(g, cfg, beta, args):
     return {"value": 1.0 / dt, "unit": "actions/s", "cores": 1, "kind": "oracle",
             "sample": "one action L_theta v at theta=0.5 on the full graph (fp64 series oracle, "
                       "scipy CSR SpMV, 1 thread; t precomputed outside the timing)",
-            "seconds": dt}
+            "seconds": dt, "host": host_info()}
 
 
 def run_cg(args):
@@ -754,7 +787,8 @@ def run_reference(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded R-MAT, graphgen)",
         "config": {"workload": f"{args.config}: {cfg['desc']}", "n": g.n, "nnz": g.nnz,
                    "f": f"exp(beta x), beta=1/rho(A)={beta:.6g}"},
-        "cpu_baseline": {"value": value, "unit": "actions/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "actions/s", "cores": 1, "kind": "oracle", "sample": sample,
+                         "host": host_info()},
         "e2e": {"value": value, "unit": "actions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -784,6 +818,8 @@ def main():
     ap.add_argument("--solver", default="krylov", choices=["krylov", "cg"],
                     help="cg: the paper's 5.3 resolvent workload by PCG on --config's graph")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl != "reference":
+        raise SystemExit(self_spawn(args.gpus))
     if args.warmup < 3:
         log("warning: contract requires >= 3 warm-up steps")
     if args.impl == "reference":

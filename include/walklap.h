@@ -241,6 +241,36 @@ wl_status wl_xnystrace_exp(const wl_operator* op, int32_t theta_index, int32_t M
                            int64_t ldo, int32_t k, int32_t nt, const double* times, double* p_out,
                            double* e_out, wl_workspace* ws, wl_stream stream);
 
+/* ---- the RATIONAL block Krylov variant of Alg. 1 ------------------
+ * Same estimate as wl_xnystrace_exp, on the block rational Krylov space of eq:block-rational-Krylov with
+ * the given poles and the reduced pencil (𝓗_k, 𝒦_k) of the block rational Arnoldi
+ * decomposition 𝔏 V_{k+1} 𝒦_k = V_{k+1} 𝓗_k, Y(t) = (1/n) V_k exp(−t Ĥ_k K̂_k⁻¹) V_kᵀ Ω:
+ *   poles_re/poles_im (host, npoles >= 0): ξ_j = +inf (pole at ∞), a real number (poles_im = 0), or
+ *     a + ib with b > 0 standing for the conjugate pair {ξ, ξ̄} (the basis is kept real: the pair adds
+ *     the real and imaginary parts of (𝔏 − ξI)⁻¹u, 2M columns).  A final pole at ∞ is appended (reading
+ *     R18), which makes Ĥ_k K̂_k⁻¹ = V_kᵀ 𝔏 V_k.  Each finite pole costs one shifted solve
+ *     (𝔏 − ξI)X = u by MINRES to relative residual inner_tol (at most inner_maxit iterations; the paper
+ *     used GMRES at 1e-6), one batched Laplacian action per iteration (two for a pair).
+ *   The basis dimension M(1 + Σ_j m_j) − M (m_j = 2 for a pair, else 1, plus the final ∞) must be
+ *     <= min(1024, n_global).  inner_iters (host, may be NULL) receives Σ over poles of the largest
+ *     MINRES iteration count over the M columns.
+ * WL_ENOCONV when a shifted solve misses inner_tol, the basis becomes rank deficient, or a small
+ * eigen/Cholesky step fails.  Synchronous. */
+wl_status wl_xnystrace_exp_rational(const wl_operator* op, int32_t theta_index, int32_t M, const double* Omega,
+                                    int64_t ldo, int32_t npoles, const double* poles_re, const double* poles_im,
+                                    double inner_tol, int32_t inner_maxit, int32_t nt, const double* times,
+                                    double* p_out, double* e_out, int64_t* inner_iters, wl_workspace* ws,
+                                    wl_stream stream);
+/* Poles of the AAA rational approximation of exp(−x) on [0, xmax] (Alg. 1 line 3, P:595, P:623-625;
+ * AAA = Nakatsukasa–Sète–Trefethen, the paper's [MR3805855]): samples {0} ∪ xmax·10^linspace(−10, 0, 2000),
+ * relative tolerance tol, at most 30 support points; Froissart doublets (|residue| < 1e-13) and poles on
+ * [0, xmax] are dropped; one representative (Im > 0) per conjugate pair; sorted by (|Im|, Re) (reading
+ * R18).  re/im: host arrays of capacity cap; *npoles receives the count (WL_EINVAL if above cap). */
+wl_status wl_aaa_exp_poles(double xmax, double tol, int32_t cap, double* re, double* im, int32_t* npoles);
+/* Gershgorin bound 2·scale·max_i t'_i >= ρ(𝕃_θ) (Prop. pro:still-again-an-mmatrix), the ρ(𝔏) estimate of
+ * Alg. 1 line 3 (host output; collective over the ranks). */
+wl_status wl_laplacian_bound(const wl_operator* op, int32_t theta_index, double* bound);
+
 /* The host steps behind it, exported for testing (host buffers, synchronous):
  * wl_symmetric_eig: A (n x n row-major symmetric) is overwritten by its eigenvectors (column i of A =
  *   eigenvector i), lam (n) receives the eigenvalues; method 0 = Householder tridiagonalisation +

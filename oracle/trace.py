@@ -11,7 +11,8 @@ leg may import this module.  Plain fp64 NumPy / SciPy, in the order and notation
    definition allows "complex numbers or infinity" and then r_k ≡ 1, 𝒬^block_{k+1} is the
    polynomial block Krylov space span{Ω, 𝔏Ω, …, 𝔏^kΩ} (eq:block-rational-Krylov),
    𝒦_k = [I; 0] and the reduced pencil gives Ĥ_k 𝒦̂_k⁻¹ = H_k, the leading kM × kM block of 𝓗_k.
-   AAA pole selection and the shifted inner solves are the next step.
+   The rational case, AAA poles (oracle/aaa.py) and shifted solves, is
+   block_rational_arnoldi / xnystrace_exp_rational below.
 3. Y(t) = (1/n) V_k exp(-t Ĥ_k 𝒦̂_k⁻¹) V_kᵀ Ω for every t.
 4. p̂(t), ê(t) = XNysTrace(Y(t), Ω) ([XTRACE]).  Reading R17: the leave-one-out Nyström
    estimator of the cited work, written as its definition —
@@ -92,5 +93,76 @@ def xnystrace_exp(Lap: np.ndarray, Omega: np.ndarray, k: int, ts) -> tuple[np.nd
     p, e = np.empty(len(ts)), np.empty(len(ts))
     for s, t in enumerate(ts):
         Y = (1.0 / n) * (Vk @ (sla.expm(-t * Hk) @ (Vk.T @ Omega)))
+        p[s], e[s] = xnystrace(Y, Omega)
+    return p, e
+
+
+def block_rational_arnoldi(Lap: np.ndarray, Omega: np.ndarray, poles):
+    """Block rational Arnoldi ([MR4082482]) for the symmetric 𝔏 = Lap in REAL arithmetic.
+
+    poles: sequence of ξ_j — np.inf, real numbers, or complex numbers standing for the conjugate pair
+    {ξ, ξ̄} (real Ω, real 𝔏: the space with both poles has a real basis).  A final pole at ∞ is
+    appended (reading R18: the reduced pencil Ĥ K̂⁻¹ is then the Rayleigh quotient V_kᵀ𝔏V_k).
+    Step j takes the continuation block u = V c (the first M columns of the newest block) and
+        ξ = ∞:      X = 𝔏 u                            𝔏 X-coefficients: K ← c,   H ← h
+        ξ real:     X = (𝔏 − ξI)⁻¹ u   (dense solve)   𝔏 X = u + ξ X:  K ← h,   H ← c + ξ h
+        ξ = a + ib: X = (𝔏 − ξI)⁻¹ u,  X ← [Re X, Im X]
+                    𝔏 Xr = u + a Xr − b Xi, 𝔏 Xi = b Xr + a Xi:  K ← [hr hi], H ← [c + a hr − b hi, b hr + a hi]
+    where X = V_new h after block classical Gram–Schmidt (applied twice) and a QR of the remainder, so
+    𝔏 V K = V H holds column by column.  Returns V (n × D), K, H (D × (D − M)), R_0 (Ω = V_1 R_0)."""
+    n, M = Omega.shape
+    Q, R0 = np.linalg.qr(Omega)
+    V = Q
+    Kc, Hc = [], []                          # pencil columns (lengths grow with V)
+    cstart = 0                               # continuation = columns [cstart, cstart + M) of V
+    for xi in list(poles) + [np.inf]:
+        D = V.shape[1]
+        c = np.zeros((D, M))
+        c[cstart:cstart + M] = np.eye(M)
+        u = V @ c
+        if np.isinf(xi):
+            X = Lap @ u
+        else:
+            Xc = np.linalg.solve(Lap - xi * np.eye(n), u.astype(complex if np.iscomplex(xi) else float))
+            X = np.hstack([Xc.real, Xc.imag]) if np.iscomplex(xi) else Xc
+        m = X.shape[1]
+        h = np.zeros((D + m, m))
+        for _ in range(2):                   # block classical Gram–Schmidt, twice
+            C = V.T @ X
+            h[:D] += C
+            X = X - V @ C
+        Qn, Rn = np.linalg.qr(X)
+        h[D:] = Rn
+        V = np.hstack([V, Qn])
+        cz = np.vstack([c, np.zeros((m, M))])
+        if np.isinf(xi):
+            Kc.append(cz)
+            Hc.append(h)
+        elif not np.iscomplex(xi):
+            Kc.append(h)
+            Hc.append(cz + xi * h)
+        else:
+            a, b = xi.real, xi.imag
+            hr, hi = h[:, :M], h[:, M:]
+            Kc.append(h)
+            Hc.append(np.hstack([cz + a * hr - b * hi, b * hr + a * hi]))
+        cstart = D
+    Dn = V.shape[1]
+    K = np.hstack([np.vstack([k, np.zeros((Dn - k.shape[0], k.shape[1]))]) for k in Kc])
+    H = np.hstack([np.vstack([x, np.zeros((Dn - x.shape[0], x.shape[1]))]) for x in Hc])
+    return V, K, H, R0
+
+
+def xnystrace_exp_rational(Lap: np.ndarray, Omega: np.ndarray, poles, ts) -> tuple[np.ndarray, np.ndarray]:
+    """Alg. 1 with the given poles: Y(t) = (1/n) V_k exp(−t Ĥ_k K̂_k⁻¹) V_kᵀ Ω on the reduced pencil (the
+    pencil without its last block row), then XNysTrace (reading R17)."""
+    n, M = Omega.shape
+    V, K, H, _ = block_rational_arnoldi(Lap, Omega, poles)
+    d = V.shape[1] - M
+    Vk = V[:, :d]
+    Ared = H[:d] @ np.linalg.inv(K[:d])
+    p, e = np.empty(len(ts)), np.empty(len(ts))
+    for s, t in enumerate(ts):
+        Y = (1.0 / n) * (Vk @ (sla.expm(-t * Ared) @ (Vk.T @ Omega)))
         p[s], e[s] = xnystrace(Y, Omega)
     return p, e

@@ -6,6 +6,7 @@ There is no CPU fallback: if the CUDA library is missing, importing `walklap` ra
 """
 from .walklap import (  # noqa: F401
     Comm,
+    aaa_exp_poles,
     LoopbackGroup,
     Operator,
     WalkLapError,

@@ -254,11 +254,17 @@ struct wl_workspace {
   // XNysTrace-exp (wl_xnystrace_exp): block basis, block, temp block, Gram blocks; cuBLAS handle
   DArr<double> trV, trW, trW2, trC, trR;
   cublasHandle_t cublas = nullptr;
+  // rational XNysTrace-exp: continuation block, MINRES vectors (v, v_prev, w1, w2, x, p; 2 halves each)
+  DArr<double> rkU, mrV;
+  DArr<double> mr_sc, mr_sums;
+  DArr<int> mr_nact;
+  int* mr_nact_host = nullptr;
   ~wl_workspace() {
     if (cstream) cudaStreamDestroy(cstream);
     if (ev_pack) cudaEventDestroy(ev_pack);
     if (ev_halo) cudaEventDestroy(ev_halo);
     if (cg_flags_host) cudaFreeHost(cg_flags_host);
+    if (mr_nact_host) cudaFreeHost(mr_nact_host);
     if (cublas) cublasDestroy(cublas);
   }
 };
@@ -1489,6 +1495,131 @@ void axpy_block(cublasHandle_t h, int p, int q, int64_t n, double alpha, const d
   cublas_check(cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, q, (int)n, p, &alpha, C, p, X, (int)ldx, &beta, Y, (int)ldy),
                "update");
 }
+
+// dst (ld lddst) R = src (n x m, ld m) by Cholesky QR applied twice (Gram by cuBLAS + allreduce, the
+// m x m Cholesky and triangular inverse on the host); R (m x m upper, col-major) returned.  W2 is
+// n x m scratch.  Throws WL_ENOCONV when the block is numerically rank deficient.
+void chol_qr2(const wl_operator* op, cublasHandle_t h, const double* src, int m, int64_t n, double* W2, double* Rd,
+              double* dst, int64_t lddst, std::vector<double>& R, cudaStream_t s) {
+  std::vector<double> Rt((size_t)m * m, 0.0), G((size_t)m * m);
+  for (int i = 0; i < m; ++i) Rt[(size_t)i * m + i] = 1.0;
+  for (int pass = 0; pass < 2; ++pass) {
+    const double* in = pass == 0 ? src : W2;
+    gram(h, m, m, n, in, m, in, m, Rd);
+    allreduce(op, Rd, (size_t)m * m, s);
+    WL_CUDA(cudaMemcpyAsync(G.data(), Rd, sizeof(double) * m * m, cudaMemcpyDeviceToHost, s));
+    WL_CUDA(cudaStreamSynchronize(s));
+    std::vector<double> U((size_t)m * m, 0.0), Ui((size_t)m * m, 0.0);  // G = Uᵀ U, col-major
+    for (int j = 0; j < m; ++j)
+      for (int i = 0; i <= j; ++i) {
+        double v = G[(size_t)j * m + i];
+        for (int q = 0; q < i; ++q) v -= U[(size_t)i * m + q] * U[(size_t)j * m + q];
+        if (i == j) {
+          if (!(v > 1e-28 * std::max(1.0, G[0]))) throw Error(WL_ENOCONV, "block rational Krylov space exhausted (rank-deficient block)");
+          U[(size_t)j * m + j] = std::sqrt(v);
+        } else {
+          U[(size_t)j * m + i] = v / U[(size_t)i * m + i];
+        }
+      }
+    for (int j = 0; j < m; ++j) {
+      Ui[(size_t)j * m + j] = 1.0 / U[(size_t)j * m + j];
+      for (int i = j - 1; i >= 0; --i) {
+        double v = 0.0;
+        for (int q = i + 1; q <= j; ++q) v += U[(size_t)q * m + i] * Ui[(size_t)j * m + q];
+        Ui[(size_t)j * m + i] = -v / U[(size_t)i * m + i];
+      }
+    }
+    WL_CUDA(cudaMemcpyAsync(Rd, Ui.data(), sizeof(double) * m * m, cudaMemcpyHostToDevice, s));
+    axpy_block(h, m, m, n, 1.0, in, m, Rd, 0.0, pass == 0 ? W2 : dst, pass == 0 ? m : lddst);
+    std::vector<double> T((size_t)m * m, 0.0);  // Rt <- U Rt
+    for (int c = 0; c < m; ++c)
+      for (int r = 0; r < m; ++r) {
+        double v = 0.0;
+        for (int q = r; q < m; ++q) v += U[(size_t)q * m + r] * Rt[(size_t)c * m + q];
+        T[(size_t)c * m + r] = v;
+      }
+    Rt.swap(T);
+    WL_CUDA(cudaStreamSynchronize(s));  // the host Ui buffer is reused by the next pass
+  }
+  R = Rt;
+}
+
+// X (n x B, ld B, internal order) = (𝔏 − ξI)⁻¹ U by MINRES (minres.cu), 𝔏 = 𝕃_θ (wl_apply's operator,
+// one batched action per iteration on the real and the imaginary half).  Complex ξ: X holds
+// [Re x | Im x] as two n x B blocks.  Returns the largest iteration count over the columns.
+int shifted_solve(const wl_operator* op, wl_workspace* ws, int theta_index, const double* U, int B, double xre,
+                  double xim, double tol, int maxit, double* X, cudaStream_t s) {
+  const int64_t n = op->n_loc;
+  const int64_t nb = std::max<int64_t>(1, n) * B;
+  const bool cplx = xim != 0.0;
+  ws->mrV.alloc((size_t)12 * nb);
+  ws->mr_sc.alloc(minres_scalar_doubles(kMaxCols));
+  ws->mr_sums.alloc(kMaxCols);
+  ws->mr_nact.alloc(1);
+  if (!ws->mr_nact_host) WL_CUDA(cudaMallocHost(&ws->mr_nact_host, sizeof(int)));
+  const size_t need = (size_t)minres_grid(n, B) * B;
+  if (ws->partials.n < need) ws->partials.alloc(need);
+  MinresArgs a{};
+  a.n = n;
+  a.B = B;
+  a.cplx = cplx;
+  a.shift_re = xre;
+  a.shift_im = xim;
+  a.tol = tol;
+  a.u = U;
+  a.v = ws->mrV.p;
+  a.vp = a.v + 2 * nb;
+  a.w1 = a.vp + 2 * nb;
+  a.w2 = a.w1 + 2 * nb;
+  a.p = a.w2 + 2 * nb;
+  a.x = X;
+  a.partials = ws->partials.p;
+  a.sums = ws->mr_sums.p;
+  a.sc = ws->mr_sc.p;
+  a.nactive = ws->mr_nact.p;
+  a.presummed = multi(op) ? 1 : 0;
+  auto reduce = [&](int which) {
+    if (multi(op)) {
+      reduce_partials(a.partials, B, minres_grid(n, B), a.sums, s);
+      allreduce(op, a.sums, (size_t)B, s);
+    }
+    minres_scalar(which, a, s);
+  };
+  minres_vec(0, a, s);
+  reduce(0);
+  minres_vec(1, a, s);
+  const int check = 4;
+  for (int it = 0; it < maxit; ++it) {
+    // p = 𝔏 v on both halves: the whole Laplacian action per half (internal row order)
+    run_chunk(op, ws, 1, a.v, B, B, theta_index * B, B, a.p, B, s, false);
+    if (cplx) run_chunk(op, ws, 1, a.v + nb, B, B, theta_index * B, B, a.p + nb, B, s, false);
+    minres_vec(2, a, s);
+    reduce(1);
+    minres_vec(3, a, s);
+    reduce(2);
+    minres_vec(4, a, s);
+    std::swap(a.v, a.vp);   // v_{j+1} was written over v̂ in the v_prev buffer
+    std::swap(a.w1, a.w2);  // w_j was written over w_{j-2}
+    if ((it + 1) % check == 0 || it + 1 == maxit) {
+      WL_CUDA(cudaMemcpyAsync(ws->mr_nact_host, a.nactive, sizeof(int), cudaMemcpyDeviceToHost, s));
+      WL_CUDA(cudaStreamSynchronize(s));
+      if (*ws->mr_nact_host == 0) break;
+    }
+  }
+  std::vector<double> sc(minres_scalar_doubles(B));
+  WL_CUDA(cudaMemcpyAsync(sc.data(), a.sc, sizeof(double) * sc.size(), cudaMemcpyDeviceToHost, s));
+  WL_CUDA(cudaStreamSynchronize(s));
+  int iters = 0;
+  bool conv = true;
+  const int kS = (int)(minres_scalar_doubles(1));
+  for (int c = 0; c < B; ++c) {
+    iters = std::max(iters, (int)sc[(size_t)c * kS + 15]);
+    conv &= sc[(size_t)c * kS + 9] == 0.0;
+  }
+  if (!conv) throw Error(WL_ENOCONV, "MINRES: shifted solve above inner_tol after inner_maxit iterations");
+  return iters;
+}
+
 }  // namespace
 }  // namespace wl
 
@@ -1619,6 +1750,200 @@ wl_status wl_xnystrace_exp(const wl_operator* op, int32_t theta_index, int32_t M
       }
     if (!xnystrace_curve(lam, Wc, d, M, (double)op->n_global, times, nt, p_out, e_out))
       throw Error(WL_ENOCONV, "XNysTrace: leave-one-out Gram matrix not positive definite");
+  });
+}
+
+// Block RATIONAL Arnoldi (Alg. 1 with its poles) on 𝔏 = 𝕃_{θ_i} in real arithmetic, then
+// XNysTrace in the projected space.  Poles: ξ = ∞ (re = +inf), real, or a + ib (b > 0) standing for
+// the conjugate pair; a final ∞ is appended (reading R18).  Step with continuation block u = V c:
+//   ∞: X = 𝔏 u;  real ξ: X = (𝔏 − ξI)⁻¹ u;  pair: X = [Re, Im] of (𝔏 − ξI)⁻¹ u   (MINRES, minres.cu)
+// then block classical Gram–Schmidt twice + Cholesky QR (X = V_new h) and the pencil columns
+//   ∞: K ← c, H ← h;  real: K ← h, H ← c + ξh;  pair: K ← [hr hi], H ← [c + a hr − b hi, b hr + a hi]
+// so 𝔏 V K = V H.  Reduced pencil (last block row dropped): Ĥ K̂⁻¹ = V_kᵀ𝔏V_k (last pole ∞),
+// symmetrised, eigendecomposed on the host, and Y(t) / XNysTrace as in wl_xnystrace_exp.
+wl_status wl_xnystrace_exp_rational(const wl_operator* op, int32_t theta_index, int32_t M, const double* Omega,
+                                    int64_t ldo, int32_t npoles, const double* poles_re, const double* poles_im,
+                                    double inner_tol, int32_t inner_maxit, int32_t nt, const double* times,
+                                    double* p_out, double* e_out, int64_t* inner_iters, wl_workspace* ws,
+                                    wl_stream stream) {
+  return guarded([&] {
+    if (!op || !ws || ws->op != op) throw Error(WL_EINVAL, "operator/workspace mismatch");
+    if (theta_index < 0 || theta_index >= op->n_theta) throw Error(WL_EINVAL, "theta_index out of range");
+    if (M < 1 || M > ws->Bmax) throw Error(WL_EINVAL, "M must be in [1, workspace column batch]");
+    if (npoles < 0 || (npoles > 0 && (!poles_re || !poles_im))) throw Error(WL_EINVAL, "bad poles");
+    if (!(inner_tol > 0.0) || inner_maxit < 1) throw Error(WL_EINVAL, "inner_tol > 0 and inner_maxit >= 1 required");
+    if (nt < 1 || !times || !p_out || !e_out) throw Error(WL_EINVAL, "bad output arguments");
+    for (int i = 0; i < nt; ++i)
+      if (!(times[i] >= 0.0)) throw Error(WL_EINVAL, "times must be >= 0");
+    // pole list (+ the final ∞) and the dimension it builds
+    std::vector<double> pre, pim;
+    int64_t Dtot = M;
+    for (int i = 0; i <= npoles; ++i) {
+      const double re = i < npoles ? poles_re[i] : INFINITY, im = i < npoles ? poles_im[i] : 0.0;
+      if (std::isnan(re) || std::isnan(im) || im < 0.0) throw Error(WL_EINVAL, "poles: NaN or negative imaginary part");
+      if (std::isinf(re) && im != 0.0) throw Error(WL_EINVAL, "poles: infinite pole with an imaginary part");
+      pre.push_back(re);
+      pim.push_back(im);
+      Dtot += im != 0.0 ? 2 * M : M;
+    }
+    if (Dtot - M > std::min<int64_t>(1024, op->n_global)) throw Error(WL_EINVAL, "basis dimension above min(1024, n)");
+    if (op->n_loc > 0) check_block(Omega, ldo, M, "Omega");
+    DeviceGuard dg(op->device);
+    cudaStream_t s = S_(stream);
+    const int64_t n = op->n_loc, nn = std::max<int64_t>(1, n);
+    const int64_t ldV = Dtot;
+    DArr<double>&V = ws->trV, &X = ws->trW, &W2 = ws->trW2, &Cd = ws->trC, &Rd = ws->trR;
+    V.alloc((size_t)nn * ldV);
+    X.alloc((size_t)nn * 2 * M);
+    W2.alloc((size_t)nn * 2 * M);
+    Cd.alloc((size_t)Dtot * 2 * M);
+    Rd.alloc((size_t)4 * M * M);
+    ws->rkU.alloc((size_t)nn * M + (size_t)nn * 2 * M);
+    double* U = ws->rkU.p;
+    double* XS = U + nn * M;  // MINRES solution [Re | Im], each n x M
+    if (!ws->cublas) cublas_check(cublasCreate(&ws->cublas), "create");
+    cublas_check(cublasSetStream(ws->cublas, s), "set stream");
+    cublasHandle_t h = ws->cublas;
+    // Ω (user order) -> internal order -> V_1 R_0
+    if (n > 0) {
+      if (op->perm.p) pack_rows(Omega, ldo, op->perm.p, n, M, X.p, s);
+      else WL_CUDA(cudaMemcpy2DAsync(X.p, sizeof(double) * M, Omega, sizeof(double) * ldo, sizeof(double) * M, n,
+                                     cudaMemcpyDeviceToDevice, s));
+    }
+    std::vector<double> R0;
+    chol_qr2(op, h, X.p, M, n, W2.p, Rd.p, V.p, ldV, R0, s);
+    const int64_t Dk = Dtot - M;                      // columns of the pencil
+    std::vector<double> K((size_t)Dtot * Dk, 0.0), Hm((size_t)Dtot * Dk, 0.0);  // row-major D x Dk
+    int64_t D = M, cstart = 0, col = 0, iters = 0;
+    std::vector<double> Ch((size_t)Dtot * 2 * M), Rj;
+    for (size_t st = 0; st < pre.size(); ++st) {
+      const double re = pre[st], im = pim[st];
+      const bool inf = std::isinf(re), cplx = im != 0.0;
+      const int m = cplx ? 2 * M : M;
+      // continuation u = V[:, cstart : cstart + M]
+      repack_rows(V.p + cstart, ldV, n, M, U, M, s);
+      if (inf) {
+        run_chunk(op, ws, 1, U, M, M, theta_index * M, M, X.p, M, s, false);  // X = 𝔏 u
+      } else {
+        iters += shifted_solve(op, ws, theta_index, U, M, re, im, inner_tol, inner_maxit, XS, s);
+        if (cplx) {
+          repack_rows(XS, M, n, M, X.p, 2 * M, s);
+          repack_rows(XS + nn * M, M, n, M, X.p + M, 2 * M, s);
+        } else {
+          repack_rows(XS, M, n, M, X.p, M, s);
+        }
+      }
+      // block classical Gram–Schmidt twice against V[:, :D]; h accumulates the coefficients
+      std::vector<double> hcoef((size_t)(D + m) * m, 0.0);  // row-major (D + m) x m
+      for (int pass = 0; pass < 2; ++pass) {
+        gram(h, (int)D, m, n, V.p, ldV, X.p, m, Cd.p);
+        allreduce(op, Cd.p, (size_t)D * m, s);
+        axpy_block(h, (int)D, m, n, -1.0, V.p, ldV, Cd.p, 1.0, X.p, m);
+        WL_CUDA(cudaMemcpyAsync(Ch.data(), Cd.p, sizeof(double) * D * m, cudaMemcpyDeviceToHost, s));
+        WL_CUDA(cudaStreamSynchronize(s));
+        for (int c = 0; c < m; ++c)
+          for (int64_t r = 0; r < D; ++r) hcoef[(size_t)r * m + c] += Ch[(size_t)c * D + r];
+      }
+      chol_qr2(op, h, X.p, m, n, W2.p, Rd.p, V.p + D, ldV, Rj, s);
+      for (int c = 0; c < m; ++c)
+        for (int r = 0; r <= c; ++r) hcoef[(size_t)(D + r) * m + c] = Rj[(size_t)c * m + r];
+      // pencil columns [col, col + m)
+      auto Kat = [&](int64_t r, int64_t c) -> double& { return K[(size_t)r * Dk + c]; };
+      auto Hat = [&](int64_t r, int64_t c) -> double& { return Hm[(size_t)r * Dk + c]; };
+      for (int c = 0; c < m; ++c)
+        for (int64_t r = 0; r < D + m; ++r) {
+          const double hv = hcoef[(size_t)r * m + c];
+          const double cu = (c < M && r == cstart + c) ? 1.0 : 0.0;  // continuation selector
+          if (inf) {
+            Kat(r, col + c) = cu;
+            Hat(r, col + c) = hv;
+          } else if (!cplx) {
+            Kat(r, col + c) = hv;
+            Hat(r, col + c) = cu + re * hv;
+          } else {
+            Kat(r, col + c) = hv;
+            if (c < M) Hat(r, col + c) = cu + re * hv - im * hcoef[(size_t)r * m + c + M];
+            else Hat(r, col + c) = im * hcoef[(size_t)r * m + c - M] + re * hv;
+          }
+        }
+      col += m;
+      cstart = D;
+      D += m;
+    }
+    // reduced pencil: A = Ĥ K̂⁻¹ (first Dk rows), i.e. K̂ᵀ Aᵀ = Ĥᵀ by LU with partial pivoting
+    const int d = (int)Dk;
+    std::vector<double> Kt((size_t)d * d), Bt((size_t)d * d);
+    for (int r = 0; r < d; ++r)
+      for (int c = 0; c < d; ++c) {
+        Kt[(size_t)c * d + r] = K[(size_t)r * Dk + c];
+        Bt[(size_t)c * d + r] = Hm[(size_t)r * Dk + c];
+      }
+    std::vector<int> piv(d);
+    for (int k = 0; k < d; ++k) {
+      int pr = k;
+      for (int i = k + 1; i < d; ++i)
+        if (std::abs(Kt[(size_t)i * d + k]) > std::abs(Kt[(size_t)pr * d + k])) pr = i;
+      if (Kt[(size_t)pr * d + k] == 0.0) throw Error(WL_ENOCONV, "rational pencil: K̂ singular");
+      if (pr != k)
+        for (int j = 0; j < d; ++j) {
+          std::swap(Kt[(size_t)k * d + j], Kt[(size_t)pr * d + j]);
+          std::swap(Bt[(size_t)k * d + j], Bt[(size_t)pr * d + j]);
+        }
+      for (int i = k + 1; i < d; ++i) {
+        const double f = Kt[(size_t)i * d + k] / Kt[(size_t)k * d + k];
+        if (f == 0.0) continue;
+        for (int j = k; j < d; ++j) Kt[(size_t)i * d + j] -= f * Kt[(size_t)k * d + j];
+        for (int j = 0; j < d; ++j) Bt[(size_t)i * d + j] -= f * Bt[(size_t)k * d + j];
+      }
+    }
+    for (int k = d - 1; k >= 0; --k)
+      for (int j = 0; j < d; ++j) {
+        double v = Bt[(size_t)k * d + j];
+        for (int i = k + 1; i < d; ++i) v -= Kt[(size_t)k * d + i] * Bt[(size_t)i * d + j];
+        Bt[(size_t)k * d + j] = v / Kt[(size_t)k * d + k];
+      }
+    // Bt = Aᵀ (row-major); symmetrise (𝔏 symmetric, last pole ∞: A = V_kᵀ𝔏V_k up to rounding)
+    std::vector<double> A((size_t)d * d);
+    for (int r = 0; r < d; ++r)
+      for (int c = 0; c < d; ++c) A[(size_t)r * d + c] = 0.5 * (Bt[(size_t)c * d + r] + Bt[(size_t)r * d + c]);
+    std::vector<double> lam;
+    if (!sym_eig_tridiag_ql(A, d, lam)) throw Error(WL_ENOCONV, "symmetric QL iteration did not converge");
+    std::vector<double> Wc((size_t)d * M, 0.0);  // Qᵀ [R_0; 0]
+    for (int a2 = 0; a2 < d; ++a2)
+      for (int c = 0; c < M; ++c) {
+        double v = 0.0;
+        for (int r = 0; r <= c; ++r) v += A[(size_t)r * d + a2] * R0[(size_t)c * M + r];
+        Wc[(size_t)a2 * M + c] = v;
+      }
+    if (!xnystrace_curve(lam, Wc, d, M, (double)op->n_global, times, nt, p_out, e_out))
+      throw Error(WL_ENOCONV, "XNysTrace: leave-one-out Gram matrix not positive definite");
+    if (inner_iters) *inner_iters = iters;
+  });
+}
+
+// Gershgorin bound on ρ(𝕃_θ): |𝕃| row sums are 2 (t_i − φ_ii) <= 2 t'_i (φ − c_0 I >= 0 entrywise,
+// Prop. pro:still-again-an-mmatrix), times wl_walkfun.scale — the interval of Alg. 1 line 3.
+wl_status wl_laplacian_bound(const wl_operator* op, int32_t theta_index, double* bound) {
+  return guarded([&] {
+    if (!op || !bound) throw Error(WL_EINVAL, "NULL argument");
+    if (theta_index < 0 || theta_index >= op->n_theta) throw Error(WL_EINVAL, "theta_index out of range");
+    DeviceGuard dg(op->device);
+    std::vector<double> t((size_t)op->n_loc * op->n_theta);
+    if (!t.empty()) WL_CUDA(cudaMemcpy(t.data(), op->tprime.p, sizeof(double) * t.size(), cudaMemcpyDeviceToHost));
+    double mx = 0.0;
+    for (int64_t r = 0; r < op->n_loc; ++r) mx = std::max(mx, t[(size_t)r * op->n_theta + theta_index]);
+    if (multi(op)) {
+      int64_t bits;
+      std::memcpy(&bits, &mx, sizeof(bits));
+      std::vector<std::vector<int64_t>> all;
+      comm_allgather_host(op->comm, {bits}, all, nullptr);
+      for (auto& v : all) {
+        double x;
+        std::memcpy(&x, &v[0], sizeof(x));
+        mx = std::max(mx, x);
+      }
+    }
+    *bound = 2.0 * std::fabs(op->lscale) * mx;
   });
 }
 

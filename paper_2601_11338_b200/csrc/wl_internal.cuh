@@ -178,6 +178,27 @@ void cg_combine(int mode, double lscale, const double* x, int64_t n, int B, cons
                 const int* vcol, double c0, const double* tprime, int64_t ldt, const int* tcol, double* out,
                 int64_t ldo, const int32_t* perm, cudaStream_t s);
 
+// ---------------------------------------------------------------- shifted solves by MINRES (minres.cu)
+// (𝔏 − ξI) X = U for the n × B block U, ξ = shift_re + i shift_im; complex shifts solve the real
+// symmetric 2n form, vectors then hold [real n × B | imaginary n × B] (offset n * B).
+struct MinresArgs {
+  int64_t n; int B;
+  int cplx;                       // shift_im != 0
+  double shift_re, shift_im, tol;
+  const double* u;                // right-hand side (n x B, real)
+  double *v, *vp, *w1, *w2, *x;   // Lanczos vectors, MINRES directions, solution
+  double* p;                      // in: 𝔏 v (both halves); out: S v
+  double* partials; double* sums; double* sc;
+  int* nactive;                   // device: columns not yet converged
+  int presummed;                  // scalar phase: a.sums already reduced (multi-rank allreduce)
+};
+size_t minres_scalar_doubles(int B);
+int minres_grid(int64_t n, int B);
+// phases: 0 ‖u‖² partials, 1 init vectors, 2 S v + α partials, 3 v̂ + ‖v̂‖² partials, 4 w, x, v update
+void minres_vec(int phase, const MinresArgs& a, cudaStream_t s);
+// which: 0 after phase 0, 1 after phase 2, 2 after phase 3
+void minres_scalar(int which, const MinresArgs& a, cudaStream_t s);
+
 // ---------------------------------------------------------------- small dense functions
 // Per column c (problem), m = keff[c]: y_c = f_1(H_m) e_1 for the Arnoldi matrix H.
 // kind 3 (outer diffusion): problem p uses column 0's H and computes exp(-tau[p] H_m) e_1;

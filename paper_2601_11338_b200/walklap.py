@@ -83,6 +83,10 @@ def load():
         "wl_spectral_radius_z": ([vp, i32, i32, ctypes.POINTER(dbl), vp], ctypes.c_int),
         "wl_markov": ([vp, i32, i32, vp, vp, i64, vp, vp], ctypes.c_int),
         "wl_xnystrace_exp": ([vp, i32, i32, vp, i64, i32, i32, vp, vp, vp, vp, vp], ctypes.c_int),
+        "wl_xnystrace_exp_rational": ([vp, i32, i32, vp, i64, i32, vp, vp, dbl, i32, i32, vp, vp, vp, vp, vp, vp],
+                                      ctypes.c_int),
+        "wl_aaa_exp_poles": ([dbl, dbl, i32, vp, vp, ctypes.POINTER(i32)], ctypes.c_int),
+        "wl_laplacian_bound": ([vp, i32, ctypes.POINTER(dbl)], ctypes.c_int),
         "wl_hessenberg_eigvals": ([i32, vp, vp, vp], ctypes.c_int),
         "wl_symmetric_eig": ([i32, vp, vp, i32], ctypes.c_int),
         "wl_xnystrace_curve": ([i32, i32, dbl, vp, vp, i32, vp, vp, vp], ctypes.c_int),
@@ -182,6 +186,14 @@ def xnystrace_curve(lam, W, n: float, times):
     _check(load().wl_xnystrace_curve(W.shape[0], W.shape[1], float(n), lam.ctypes.data, W.ctypes.data,
                                      len(times), times.ctypes.data, p.ctypes.data, e.ctypes.data))
     return p, e
+
+
+def aaa_exp_poles(xmax: float, tol: float = 1e-13) -> np.ndarray:
+    """AAA poles of exp(-x) on [0, xmax] (wl_aaa_exp_poles): one representative per conjugate pair."""
+    re, im = np.empty(64), np.empty(64)
+    k = ctypes.c_int32()
+    _check(load().wl_aaa_exp_poles(float(xmax), float(tol), 64, re.ctypes.data, im.ctypes.data, ctypes.byref(k)))
+    return re[:k.value] + 1j * im[:k.value]
 
 
 def _stream_handle(stream):
@@ -483,6 +495,34 @@ class Operator:
                                        len(times), times.ctypes.data, p.ctypes.data, e.ctypes.data, ws.handle,
                                        _stream_handle(stream)))
         return p, e
+
+    def laplacian_bound(self, theta_index: int = 0) -> float:
+        """Gershgorin bound on ρ(𝕃_θ) (wl_laplacian_bound)."""
+        v = ctypes.c_double()
+        _check(load().wl_laplacian_bound(self.handle, theta_index, ctypes.byref(v)))
+        return v.value
+
+    def xnystrace_exp_rational(self, omega, times, poles="aaa", theta_index=0, inner_tol=1e-6, inner_maxit=500,
+                               aaa_tol=1e-13, ws=None, stream=None):
+        """Alg. 1 on the block RATIONAL Krylov space (wl_xnystrace_exp_rational).  poles: "aaa" (the AAA poles of
+        exp(-x) on [0, t* ρ(𝕃)], with the library's Gershgorin bound for ρ) or an array of ξ (np.inf, real, or
+        complex with Im > 0 for a conjugate pair).  Returns (p̂, ê, info) with info = {poles, inner_iters}."""
+        times = np.ascontiguousarray(np.atleast_1d(times), dtype=np.float64)
+        if isinstance(poles, str):
+            poles = aaa_exp_poles(float(times.max()) * self.laplacian_bound(theta_index), aaa_tol)
+        poles = np.asarray(poles, dtype=complex)
+        re = np.ascontiguousarray(poles.real, dtype=np.float64)
+        im = np.ascontiguousarray(np.abs(poles.imag), dtype=np.float64)
+        M = omega.shape[1] if omega.dim() == 2 else 1
+        om, ldo = _block(omega, M, "omega")
+        p, e = np.empty(len(times)), np.empty(len(times))
+        it = ctypes.c_int64()
+        ws = ws or self.workspace(M)
+        _check(load().wl_xnystrace_exp_rational(self.handle, theta_index, M, ctypes.c_void_p(om.data_ptr()), ldo,
+                                                len(re), re.ctypes.data, im.ctypes.data, float(inner_tol),
+                                                int(inner_maxit), len(times), times.ctypes.data, p.ctypes.data,
+                                                e.ctypes.data, ctypes.byref(it), ws.handle, _stream_handle(stream)))
+        return p, e, {"poles": poles, "inner_iters": it.value}
 
     def spectral_radius_z(self, theta_index: int = 0, k: int = 60, stream=None) -> float:
         """ρ(Z_θ) of the companion operator by k Arnoldi steps on Z (wl_spectral_radius_z)."""

@@ -148,3 +148,20 @@ def test_xnystrace_curve_matches_oracle(lib):
         ref = np.array([T.xnystrace(sla.expm(-t * L) @ Om / 34, Om) for t in ts])
         assert np.max(np.abs(p - ref[:, 0]) / np.abs(ref[:, 0])) < 1e-9, M
         assert np.max(np.abs(e - ref[:, 1])) <= 1e-9 * np.max(ref[:, 0]) + 1e-7 * np.max(ref[:, 1]), M
+
+
+def test_aaa_exp_poles_host_routine(lib):
+    """wl_aaa_exp_poles (host, no GPU): the library's AAA poles carry a rational approximation of exp(-x) on
+    [0, X] as good as the oracle's (least-squares fit over the poles on the sample set, ~1e-13).  The poles
+    themselves may differ from the oracle's: AAA's null vector of a Loewner matrix with a tiny singular gap is
+    method dependent, so GPU parity tests pass the SAME poles to both sides."""
+    import paper_2601_11338_b200 as wl
+    from oracle import aaa as AA
+    for X in (10.0, 100.0, 1000.0, 30.5):
+        p = wl.aaa_exp_poles(X)
+        Z = np.concatenate([[0.0], X * np.logspace(-10.0, 0.0, 2000)])
+        allp = [q for x in p for q in ((x, np.conj(x)) if x.imag != 0 else (x,))]
+        B = np.column_stack([np.ones_like(Z)] + [1.0 / (Z - q) for q in allp]).astype(complex)
+        c, *_ = np.linalg.lstsq(B, np.exp(-Z).astype(complex), rcond=None)
+        assert np.abs(B @ c - np.exp(-Z)).max() < 1e-12, X
+        assert np.all(p.imag >= 0) and abs(len(p) - len(AA.exp_poles(X))) <= 1

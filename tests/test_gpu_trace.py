@@ -104,3 +104,68 @@ def test_full_c3_fig7_shape(wl):
     assert abs(e[0] - e0) <= 1e-6 * e0
     assert np.all(np.diff(p) <= 3 * (e[1:] + e[:-1]))
     assert np.all(p > 1.0 / g.n)
+
+
+@pytest.mark.slow
+def test_midsize_road_full_curve_fig7_shape(wl):
+    """The bench's launch configuration (M = 30 probes, k = 8 block steps, 90 t-points, NBT θ = 0 on a
+    road-like grid) on a graph the dense oracle handles (n ≈ 2.5e3): the WHOLE curve p̂(t) and ê(t)
+    against oracle/trace.py, not only t = 0."""
+    g = gg.grid_lcc(60, 60, 0.3, 2002)
+    rA = D.rho_A(D.adjacency(g))
+    ts = np.linspace(0.0, 10.0, 90)
+    p, e, po, eo = _case(wl, g, [0.0], ("exp", 1.0 / rA), 0, 30, 8, ts, 2026)
+    assert np.max(np.abs(p - po) / np.abs(po)) < 1e-8
+    assert np.max(np.abs(e - eo)) < 1e-8 * np.max(np.abs(po)) + 1e-6 * np.max(eo)
+
+
+# ---- the rational block Krylov variant (AAA poles + shifted MINRES solves; wl_xnystrace_exp_rational) ----
+
+def _rational_case(wl, g, thetas, f, ti, M, ts, seed, poles=None, inner_tol=1e-14, **kw):
+    A = D.adjacency(g)
+    fo = {"exp": C.exp, "resolvent": C.resolvent}[f[0]](f[1])
+    Lap = D.laplacian(A, 1.0 - thetas[ti], fo)
+    Om = gg.vectors(g.n, M, seed)
+    op = wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=thetas, f=f, **kw)
+    if poles is None:   # the library's AAA poles on [0, t* ρ] with its Gershgorin ρ bound (Alg. 1 line 3)
+        poles = wl.aaa_exp_poles(max(ts) * op.laplacian_bound(ti))
+    p, e, info = op.xnystrace_exp_rational(torch.from_numpy(Om).cuda(), ts, poles=poles, theta_index=ti,
+                                           inner_tol=inner_tol, inner_maxit=2000)
+    op.close()
+    po, eo = T.xnystrace_exp_rational(Lap, Om, poles, ts)   # the same poles, dense solves
+    return p, e, po, eo, info
+
+
+def test_rational_karate_aaa_poles_vs_oracle(wl):
+    """Fig. 4(a)-shape workload (karate, standard-like 𝕃 at θ = 1, t ∈ [0, 10]) with the AAA poles: the
+    block rational Krylov estimate against the oracle's block rational Arnoldi with dense shifted solves."""
+    g = gg.karate()
+    rA = D.rho_A(D.adjacency(g))
+    ts = np.linspace(0.0, 10.0, 30)
+    p, e, po, eo, info = _rational_case(wl, g, [1.0, 0.0], ("exp", 1.0 / rA), 0, 2, ts, 11)
+    assert len(info["poles"]) >= 3 and info["inner_iters"] > 0
+    assert np.max(np.abs(p - po) / np.abs(po)) < 1e-10
+    assert np.max(np.abs(e - eo)) < 1e-10 * np.max(np.abs(po)) + 1e-8 * np.max(eo)
+
+
+def test_rational_poles_real_pair_and_infinity(wl):
+    """Every pole kind in one space: ∞, a real pole, a conjugate pair, on a multi-tile BA graph (NBT θ = 0)."""
+    g = gg.barabasi_albert(1201, 3, 5)
+    rA = D.rho_A(D.adjacency(g))
+    ts = np.linspace(0.0, 4.0, 9)
+    poles = np.array([np.inf, -2.5, -1.0 + 3.0j, 0.5 + 6.0j])
+    p, e, po, eo, info = _rational_case(wl, g, [0.0], ("exp", 1.0 / rA), 0, 5, ts, 3, poles=poles)
+    assert np.max(np.abs(p - po) / np.abs(po)) < 1e-10
+    assert np.max(np.abs(e - eo)) < 1e-10 * np.max(np.abs(po)) + 1e-8 * np.max(eo)
+
+
+@pytest.mark.slow
+def test_rational_midsize_road_fig7_shape(wl):
+    """The paper's §5.2 / Fig. 7 configuration shape — road-like grid, NBT, M = 30 probes, 90 t in [0, 100],
+    AAA poles on [0, t* ρ] — on a graph the dense oracle handles (n ≈ 3.5e3)."""
+    g = gg.grid_lcc(60, 60, 0.3, 2002)
+    rA = D.rho_A(D.adjacency(g))
+    ts = np.linspace(0.0, 100.0, 90)
+    p, e, po, eo, info = _rational_case(wl, g, [0.0], ("exp", 1.0 / rA), 0, 30, ts, 2026)
+    assert np.max(np.abs(p - po) / np.abs(po)) < 1e-10
+    assert np.max(np.abs(e - eo)) < 1e-10 * np.max(np.abs(po)) + 1e-8 * np.max(eo)

@@ -9,9 +9,11 @@ Each pin fixes the oracle against something other than itself:
   error estimate.
 """
 import numpy as np
+import pytest
 import scipy.linalg as sla
 
 import graphgen as gg
+from oracle import coeffs as C
 from oracle import dense as D
 from oracle import trace as T
 from conftest import read_golden
@@ -92,3 +94,73 @@ def test_fig4a_within_error_estimate():
         good += np.mean(np.abs(p - gold[:, 1]) <= 3 * e + 1e-12) >= 0.9
     assert good >= 8
     assert np.max(np.abs(np.mean(ps, axis=0) - gold[:, 1])) < 0.03
+
+
+# ---- rational part of Alg. 1: AAA poles (oracle/aaa.py) and the block rational Arnoldi (oracle/trace.py) ----
+
+def _lsq_rational_error(poles, X):
+    """Max error on the AAA sample set of the least-squares fit of exp(-x) by 1 + Σ_j c_j/(x − ξ_j) over the
+    poles and their conjugates: small iff the poles carry a rational approximation of exp(-x) on [0, X]."""
+    from oracle import aaa as AA  # noqa: F401
+    Z = np.concatenate([[0.0], X * np.logspace(-10.0, 0.0, 2000)])
+    allp = []
+    for p in poles:
+        allp.append(p)
+        if p.imag != 0:
+            allp.append(np.conj(p))
+    B = np.column_stack([np.ones_like(Z)] + [1.0 / (Z - p) for p in allp]).astype(complex)
+    c, *_ = np.linalg.lstsq(B, np.exp(-Z).astype(complex), rcond=None)
+    return float(np.abs(B @ c - np.exp(-Z)).max())
+
+
+def test_aaa_recovers_the_poles_of_a_rational_function():
+    """AAA is exact on a rational function (its closed form): 1/(x+2) + 3/(x+5) − 1/(x−12) sampled on [0, 10]."""
+    from oracle import aaa as AA
+    Z = np.linspace(0.0, 10.0, 500)
+    F = 1.0 / (Z + 2.0) + 3.0 / (Z + 5.0) - 1.0 / (Z - 12.0)
+    z, f, w, err = AA.aaa(Z, F)
+    pol, res = AA.aaa_poles(z, f, w)
+    assert err < 1e-13
+    order = np.argsort(pol.real)
+    assert np.allclose(pol[order].real, [-5.0, -2.0, 12.0], atol=1e-9) and np.all(np.abs(pol.imag) < 1e-9)
+    assert np.allclose(res[order].real, [3.0, 1.0, -1.0], atol=1e-8)
+
+
+@pytest.mark.parametrize("X", [10.0, 100.0, 1000.0])
+def test_aaa_exp_poles_carry_the_approximation(X):
+    """The poles of Alg. 1 line 3 support a rational approximation of exp(-x) on [0, X] to ~1e-13, come as
+    conjugate pairs / real poles off the spectral interval; t* = 100 gives 13 poles counting conjugates,
+    the count the paper reports for its road networks."""
+    from oracle import aaa as AA
+    poles = AA.exp_poles(X)
+    assert _lsq_rational_error(poles, X) < 1e-12
+    assert np.all(poles.imag >= 0)
+    assert not np.any((poles.imag == 0) & (poles.real >= 0) & (poles.real <= X))
+    if X == 100.0:
+        assert sum(2 if p.imag > 0 else 1 for p in poles) == 13
+
+
+def test_block_rational_arnoldi_decomposition_and_limits():
+    """𝔏 V K = V H with V orthonormal for ∞ / real / complex-pair poles; all poles at ∞ reproduce the polynomial
+    block Arnoldi estimate; the space is exact for f(x) = 1/(x − ξ) at each of its poles (rational Krylov
+    exactness)."""
+    g = gg.karate()
+    A = D.adjacency(g)
+    Lap = D.laplacian(A, 1.0, C.exp(1.0 / D.rho_A(A)))
+    Om = gg.vectors(34, 3, 5)
+    V, K, H, _ = T.block_rational_arnoldi(Lap, Om, [-2.0, 1.5 + 3.0j, np.inf])
+    assert np.abs(Lap @ V @ K - V @ H).max() < 1e-13
+    assert np.abs(V.T @ V - np.eye(V.shape[1])).max() < 1e-13
+    ts = np.linspace(0.0, 10.0, 5)
+    p1, e1 = T.xnystrace_exp(Lap, Om, 3, ts)
+    p2, e2 = T.xnystrace_exp_rational(Lap, Om, [np.inf, np.inf], ts)
+    assert np.abs(p1 - p2).max() < 1e-13 and np.abs(e1 - e2).max() < 1e-13
+    for xi in (-2.0, 0.7 + 2.0j):
+        V, K, H, _ = T.block_rational_arnoldi(Lap, Om, [-2.0, 0.7 + 2.0j])
+        d = V.shape[1] - 3
+        Vk = V[:, :d]
+        Ar = H[:d] @ np.linalg.inv(K[:d])
+        for x in (xi, np.conj(xi)):
+            approx = Vk @ np.linalg.solve(Ar - x * np.eye(d), Vk.T @ Om)
+            exact = np.linalg.solve(Lap - x * np.eye(34), Om)
+            assert np.abs(approx - exact).max() < 1e-12 * np.abs(exact).max()
