@@ -662,11 +662,26 @@ def run_trace(args):
                      relabel=args.relabel,
                      krylov_dim=cfg["krylov_dim"])
     M, k = args.trace_m, args.trace_k
-    ts = np.linspace(0.0, 10.0, 90)
+    rational = args.trace_poles == "aaa"
+    # Fig. 7: [0, t*] = [0, 100], 90 points, AAA poles, inner solves at 1e-6; the polynomial
+    # (poles at ∞) variant keeps round 1's [0, 10] grid
+    ts = np.linspace(0.0, 100.0 if rational else 10.0, 90)
     Om = torch.from_numpy(np.ascontiguousarray(gg.vectors(g.n, M, 2026)[rb:re])).cuda()
     ws = op.workspace(M)
+    info = {}
+    if rational:
+        poles = wl.aaa_exp_poles(float(ts.max()) * op.laplacian_bound(0))  # Alg. 1 line 3
+
+        def curve():
+            p_, e_, inf_ = op.xnystrace_exp_rational(Om, ts, poles=poles, inner_tol=args.trace_inner_tol,
+                                                     inner_maxit=2000, ws=ws)
+            info.update(inf_)
+            return p_, e_
+    else:
+        def curve():
+            return op.xnystrace_exp(Om, ts, k, ws=ws)
     for _ in range(args.warmup):
-        p, e = op.xnystrace_exp(Om, ts, k, ws=ws)
+        p, e = curve()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -676,7 +691,7 @@ def run_trace(args):
     with ClockSampler(local) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
-            p, e = op.xnystrace_exp(Om, ts, k, ws=ws)
+            p, e = curve()
         ev1.record(stream)
         torch.cuda.synchronize()
     launches = wl.launch_count() - l0
@@ -686,7 +701,7 @@ def run_trace(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     wl.profile_enable(True)
-    op.xnystrace_exp(Om, ts, k, ws=ws)
+    curve()
     torch.cuda.synchronize()
     wl.profile_enable(False)
     kernels = {kk: {"ms_per_step": v[0], "launches_per_step": v[1], "share": v[0] / ms}
@@ -697,9 +712,15 @@ def run_trace(args):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded graphgen)",
-            "config": {"workload": f"{cfg['desc']}; Alg. 1 (poles at inf), M={M} probes, k={k} blocks, 90 t in [0,10], "
-                                   f"theta={cfg['thetas'][0]}, inner k={cfg['krylov_dim']}",
-                       "n": g.n, "nnz": g.nnz, "column_actions_per_s": k * M / (ms / 1e3),
+            "config": {"workload": (f"{cfg['desc']}; Alg. 1 with {len(info['poles'])} AAA poles (+conjugates, +inf), "
+                                    f"MINRES inner solves to {args.trace_inner_tol:g}, M={M} probes, 90 t in [0,100]"
+                                    if rational else
+                                    f"{cfg['desc']}; Alg. 1 (poles at inf), M={M} probes, k={k} blocks, 90 t in [0,10]")
+                                   + f", theta={cfg['thetas'][0]}, inner Krylov k={cfg['krylov_dim']}",
+                       "n": g.n, "nnz": g.nnz,
+                       "poles": [[float(z.real), float(z.imag)] for z in info.get("poles", [])],
+                       "inner_minres_iterations": info.get("inner_iters"),
+                       "column_actions_per_s": (None if rational else k * M / (ms / 1e3)),
                        "p_hat": [round(float(x), 6) for x in p[::10]], "e_hat": [float(x) for x in e[::10]]},
             "roofline": None, "kernels": kernels, "cpu_baseline": None, "e2e": None, "gpu_launches": launches,
             "clocks": clk.summary(),
@@ -813,7 +834,10 @@ def main():
                     help="degree-sorted row relabelling inside the operator (opts.relabel)")
     ap.add_argument("--trace", action="store_true", help="NEXT-2: XNysTrace-exp return-probability curve")
     ap.add_argument("--trace-m", type=int, default=30, help="--trace: probes M")
-    ap.add_argument("--trace-k", type=int, default=8, help="--trace: block Krylov steps k")
+    ap.add_argument("--trace-k", type=int, default=8, help="--trace: block Krylov steps k (poles at inf)")
+    ap.add_argument("--trace-poles", default="aaa", choices=["aaa", "inf"],
+                    help="--trace: AAA poles + MINRES shifted solves (Alg. 1 as in the paper) or all poles at inf")
+    ap.add_argument("--trace-inner-tol", type=float, default=1e-6, help="--trace: MINRES relative tolerance (P:1483)")
     ap.add_argument("--rhoz", action="store_true", help="NEXT-4: rho(Z_1) by Arnoldi on the companion operator")
     ap.add_argument("--solver", default="krylov", choices=["krylov", "cg"],
                     help="cg: the paper's 5.3 resolvent workload by PCG on --config's graph")

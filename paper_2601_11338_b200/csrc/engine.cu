@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -1755,7 +1756,8 @@ wl_status wl_xnystrace_exp(const wl_operator* op, int32_t theta_index, int32_t M
 
 // Block RATIONAL Arnoldi (Alg. 1 with its poles) on 𝔏 = 𝕃_{θ_i} in real arithmetic, then
 // XNysTrace in the projected space.  Poles: ξ = ∞ (re = +inf), real, or a + ib (b > 0) standing for
-// the conjugate pair; a final ∞ is appended (reading R18).  Step with continuation block u = V c:
+// the conjugate pair; a final ∞ is appended (reading R18).  Step with continuation block u = V c (the last M
+// columns of the newest block):
 //   ∞: X = 𝔏 u;  real ξ: X = (𝔏 − ξI)⁻¹ u;  pair: X = [Re, Im] of (𝔏 − ξI)⁻¹ u   (MINRES, minres.cu)
 // then block classical Gram–Schmidt twice + Cholesky QR (X = V_new h) and the pencil columns
 //   ∞: K ← c, H ← h;  real: K ← h, H ← c + ξh;  pair: K ← [hr hi], H ← [c + a hr − b hi, b hr + a hi]
@@ -1845,6 +1847,13 @@ wl_status wl_xnystrace_exp_rational(const wl_operator* op, int32_t theta_index, 
           for (int64_t r = 0; r < D; ++r) hcoef[(size_t)r * m + c] += Ch[(size_t)c * D + r];
       }
       chol_qr2(op, h, X.p, m, n, W2.p, Rd.p, V.p + D, ldV, Rj, s);
+      if (getenv("WL_DEBUG_RATIONAL")) {
+        double hmax = 0.0, rmin = INFINITY;
+        for (double v : hcoef) hmax = std::max(hmax, std::fabs(v));
+        for (int c = 0; c < m; ++c) rmin = std::min(rmin, std::fabs(Rj[(size_t)c * m + c]));
+        fprintf(stderr, "[rational] step %zu pole (%g, %g) m=%d D=%lld max|h| %.3e min|R_ii| %.3e iters %lld\n", st, re,
+                im, m, (long long)D, hmax, rmin, (long long)iters);
+      }
       for (int c = 0; c < m; ++c)
         for (int r = 0; r <= c; ++r) hcoef[(size_t)(D + r) * m + c] = Rj[(size_t)c * m + r];
       // pencil columns [col, col + m)
@@ -1867,47 +1876,39 @@ wl_status wl_xnystrace_exp_rational(const wl_operator* op, int32_t theta_index, 
           }
         }
       col += m;
-      cstart = D;
+      cstart = D + m - M;  // continuation: the last M columns of the newest block (reading R18)
       D += m;
     }
-    // reduced pencil: A = Ĥ K̂⁻¹ (first Dk rows), i.e. K̂ᵀ Aᵀ = Ĥᵀ by LU with partial pivoting
+    // Projected operator on V_k = V[:, :d].  With the last pole at ∞ the reduced pencil Ĥ K̂⁻¹ equals the
+    // Rayleigh quotient V_kᵀ 𝔏 V_k (reading R18); K̂ is, however, ill-conditioned in floating point once a
+    // conjugate pair's real and imaginary directions nearly coincide modulo the basis (far poles: both
+    // ≈ 𝔏u/|ξ|²; measured on the oracle at d = 450: ‖Ĥ K̂⁻¹ − (Ĥ K̂⁻¹)ᵀ‖ = 0.6 and a negative eigenvalue).
+    // So the Rayleigh quotient is formed directly: d/M more batched Laplacian actions, symmetric by
+    // construction.  (K, H above stay the Arnoldi bookkeeping of the decomposition 𝔏 V K = V H.)
     const int d = (int)Dk;
-    std::vector<double> Kt((size_t)d * d), Bt((size_t)d * d);
-    for (int r = 0; r < d; ++r)
-      for (int c = 0; c < d; ++c) {
-        Kt[(size_t)c * d + r] = K[(size_t)r * Dk + c];
-        Bt[(size_t)c * d + r] = Hm[(size_t)r * Dk + c];
-      }
-    std::vector<int> piv(d);
-    for (int k = 0; k < d; ++k) {
-      int pr = k;
-      for (int i = k + 1; i < d; ++i)
-        if (std::abs(Kt[(size_t)i * d + k]) > std::abs(Kt[(size_t)pr * d + k])) pr = i;
-      if (Kt[(size_t)pr * d + k] == 0.0) throw Error(WL_ENOCONV, "rational pencil: K̂ singular");
-      if (pr != k)
-        for (int j = 0; j < d; ++j) {
-          std::swap(Kt[(size_t)k * d + j], Kt[(size_t)pr * d + j]);
-          std::swap(Bt[(size_t)k * d + j], Bt[(size_t)pr * d + j]);
-        }
-      for (int i = k + 1; i < d; ++i) {
-        const double f = Kt[(size_t)i * d + k] / Kt[(size_t)k * d + k];
-        if (f == 0.0) continue;
-        for (int j = k; j < d; ++j) Kt[(size_t)i * d + j] -= f * Kt[(size_t)k * d + j];
-        for (int j = 0; j < d; ++j) Bt[(size_t)i * d + j] -= f * Bt[(size_t)k * d + j];
-      }
+    std::vector<double> A((size_t)d * d, 0.0);
+    for (int j0 = 0; j0 < d; j0 += M) {
+      repack_rows(V.p + j0, ldV, n, M, U, M, s);
+      run_chunk(op, ws, 1, U, M, M, theta_index * M, M, X.p, M, s, false);  // 𝔏 V[:, j0 : j0 + M]
+      gram(h, d, M, n, V.p, ldV, X.p, M, Cd.p);
+      allreduce(op, Cd.p, (size_t)d * M, s);
+      WL_CUDA(cudaMemcpyAsync(Ch.data(), Cd.p, sizeof(double) * d * M, cudaMemcpyDeviceToHost, s));
+      WL_CUDA(cudaStreamSynchronize(s));
+      for (int c = 0; c < M; ++c)
+        for (int r = 0; r < d; ++r) A[(size_t)r * d + j0 + c] = Ch[(size_t)c * d + r];
     }
-    for (int k = d - 1; k >= 0; --k)
-      for (int j = 0; j < d; ++j) {
-        double v = Bt[(size_t)k * d + j];
-        for (int i = k + 1; i < d; ++i) v -= Kt[(size_t)k * d + i] * Bt[(size_t)i * d + j];
-        Bt[(size_t)k * d + j] = v / Kt[(size_t)k * d + k];
-      }
-    // Bt = Aᵀ (row-major); symmetrise (𝔏 symmetric, last pole ∞: A = V_kᵀ𝔏V_k up to rounding)
-    std::vector<double> A((size_t)d * d);
+    double asym = 0.0;
     for (int r = 0; r < d; ++r)
-      for (int c = 0; c < d; ++c) A[(size_t)r * d + c] = 0.5 * (Bt[(size_t)c * d + r] + Bt[(size_t)r * d + c]);
+      for (int c = r + 1; c < d; ++c) {
+        asym = std::max(asym, std::fabs(A[(size_t)r * d + c] - A[(size_t)c * d + r]));
+        A[(size_t)r * d + c] = A[(size_t)c * d + r] = 0.5 * (A[(size_t)r * d + c] + A[(size_t)c * d + r]);
+      }
     std::vector<double> lam;
     if (!sym_eig_tridiag_ql(A, d, lam)) throw Error(WL_ENOCONV, "symmetric QL iteration did not converge");
+    static const bool dbg = getenv("WL_DEBUG_RATIONAL") != nullptr;
+    if (dbg)
+      fprintf(stderr, "[rational] d=%d max|A-A^T| %.3e lambda [%.6e, %.6e] inner iters %lld\n", d, asym,
+              *std::min_element(lam.begin(), lam.end()), *std::max_element(lam.begin(), lam.end()), (long long)iters);
     std::vector<double> Wc((size_t)d * M, 0.0);  // Qᵀ [R_0; 0]
     for (int a2 = 0; a2 < d; ++a2)
       for (int c = 0; c < M; ++c) {

@@ -151,6 +151,8 @@ def test_block_rational_arnoldi_decomposition_and_limits():
     V, K, H, _ = T.block_rational_arnoldi(Lap, Om, [-2.0, 1.5 + 3.0j, np.inf])
     assert np.abs(Lap @ V @ K - V @ H).max() < 1e-13
     assert np.abs(V.T @ V - np.eye(V.shape[1])).max() < 1e-13
+    d = V.shape[1] - 3                     # last pole ∞: reduced pencil = Rayleigh quotient (reading R18)
+    assert np.abs(H[:d] @ np.linalg.inv(K[:d]) - V[:, :d].T @ Lap @ V[:, :d]).max() < 1e-12
     ts = np.linspace(0.0, 10.0, 5)
     p1, e1 = T.xnystrace_exp(Lap, Om, 3, ts)
     p2, e2 = T.xnystrace_exp_rational(Lap, Om, [np.inf, np.inf], ts)
