@@ -108,6 +108,10 @@ typedef struct {
                            and A_halo (halo columns) so A_loc's SpMM runs while the halo exchange is
                            in flight on a second stream; 0 exchanges first, then runs
                            one SpMM over the full local CSR */
+  int32_t lanczos;      /* 1 (default, with reorth = 2): Krylov batches whose columns are all θ = 1 (μ = 0, the
+                           all-walk operator, where q_k = A^k) run the symmetric three-term Lanczos
+                           recurrence on A from A v ("Lanczos (for A = Aᵀ)") instead of TOAR on Z:
+                           three n-block passes per step instead of two passes over the whole basis */
 } wl_opts;
 
 typedef enum { WL_SOLVER_KRYLOV = 0, WL_SOLVER_CG = 1 } wl_solver;

@@ -92,8 +92,31 @@ std::vector<double> min_right_singular(std::vector<double> L, int r, int m) {
   return w;
 }
 
-// eigenvalues of a general real m x m matrix (row-major): Householder Hessenberg + Francis QR
+// eigenvalues of a general real m x m matrix (row-major): balancing (Parlett & Reinsch: a diagonal
+// similarity by powers of 2 equalising row and column norms — the diagonal-plus-rank-one matrix below has
+// rows of very different scale), Householder Hessenberg reduction, then the Francis QR of eig.cu
 bool eigvals_general(std::vector<double> A, int m, std::vector<cd>& ev) {
+  for (bool done = false; !done;) {
+    done = true;
+    for (int i = 0; i < m; ++i) {
+      double c = 0.0, r = 0.0;
+      for (int j = 0; j < m; ++j)
+        if (j != i) {
+          c += std::fabs(A[(size_t)j * m + i]);
+          r += std::fabs(A[(size_t)i * m + j]);
+        }
+      if (c == 0.0 || r == 0.0) continue;
+      double f = 1.0;
+      const double sum = c + r;
+      while (c < r / 2.0) { c *= 2.0; r /= 2.0; f *= 2.0; }
+      while (c >= r * 2.0) { c /= 2.0; r *= 2.0; f /= 2.0; }
+      if ((c + r) < 0.95 * sum) {
+        done = false;
+        for (int j = 0; j < m; ++j) A[(size_t)i * m + j] /= f;
+        for (int j = 0; j < m; ++j) A[(size_t)j * m + i] *= f;
+      }
+    }
+  }
   for (int k = 0; k + 2 < m; ++k) {
     double nrm = 0.0;
     for (int i = k + 1; i < m; ++i) nrm += A[(size_t)i * m + k] * A[(size_t)i * m + k];
@@ -179,15 +202,21 @@ bool aaa_exp_poles(double xmax, double tol, std::vector<cd>& poles) {
   poles.clear();
   if (m < 2) return true;
   // roots of D(λ) = Σ w_j/(λ − z_j): eigenvalues of diag(y) − u 1ᵀ (y = z − σ), minus the one at y = 0
-  const double sigma = -1.0;
   double W = 0.0;
   for (double x : w) W += x;
   if (W == 0.0) return false;
-  std::vector<double> G((size_t)m * m);
-  for (int i = 0; i < m; ++i)
-    for (int k = 0; k < m; ++k) G[(size_t)i * m + k] = (i == k ? z[i] - sigma : 0.0) - w[i] * (z[i] - sigma) / W;
+  // Σ w tiny makes the matrix badly scaled and the QR may stall: retry with other shifts σ (< 0 <= z_j)
   std::vector<cd> ev;
-  if (!eigvals_general(G, m, ev)) return false;
+  double sigma = 0.0;
+  bool ok = false;
+  for (double sg : {-1.0, -2.71828, -0.367879, -7.38906, -0.135335, -20.0855}) {
+    sigma = sg;
+    std::vector<double> G((size_t)m * m);
+    for (int i = 0; i < m; ++i)
+      for (int k = 0; k < m; ++k) G[(size_t)i * m + k] = (i == k ? z[i] - sigma : 0.0) - w[i] * (z[i] - sigma) / W;
+    if ((ok = eigvals_general(G, m, ev))) break;
+  }
+  if (!ok) return false;
   int spurious = 0;
   for (int i = 1; i < m; ++i)
     if (std::abs(ev[i]) < std::abs(ev[spurious])) spurious = i;

@@ -35,7 +35,7 @@ void eig2(double a, double b, double c, double d, double& r1, double& i1, double
 }  // namespace
 
 // H: n x n row-major upper Hessenberg (entries below the subdiagonal are ignored), overwritten.
-// Returns false if some eigenvalue failed to converge in 30 sweeps (wr/wi then partial).
+// Returns false if some eigenvalue failed to converge in 60 sweeps (wr/wi then partial).
 bool hessenberg_eigvals(std::vector<double>& H, int n, std::vector<double>& wr, std::vector<double>& wi) {
   auto A = [&](int i, int j) -> double& { return H[(size_t)i * n + j]; };
   wr.assign(n, 0.0);
@@ -50,7 +50,9 @@ bool hessenberg_eigvals(std::vector<double>& H, int n, std::vector<double>& wr, 
     while (lo > 0) {
       double s = std::fabs(A(lo - 1, lo - 1)) + std::fabs(A(lo, lo));
       if (s == 0.0) s = norm;
-      if (std::fabs(A(lo, lo - 1)) <= 1e-16 * s) {
+      // local test (unit roundoff relative to the neighbouring diagonal); after 20 stagnant sweeps also the
+      // global one (relative to ‖H‖), which trades relative accuracy of tiny eigenvalues for convergence
+      if (std::fabs(A(lo, lo - 1)) <= 2.220446049250313e-16 * (its >= 20 ? std::max(s, norm) : s)) {
         A(lo, lo - 1) = 0.0;
         break;
       }
@@ -68,10 +70,10 @@ bool hessenberg_eigvals(std::vector<double>& H, int n, std::vector<double>& wr, 
       its = 0;
       continue;
     }
-    if (its >= 30) return false;
+    if (its >= 60) return false;
     // shifts: eigenvalues of the trailing 2x2 (via trace s and determinant t), exceptional every 10
     double s, t;
-    if (its == 10 || its == 20) {
+    if (its == 10 || its == 20 || its == 40) {
       const double w = std::fabs(A(hi, hi - 1)) + std::fabs(A(hi - 1, hi - 2));
       s = 1.5 * w;
       t = w * w;

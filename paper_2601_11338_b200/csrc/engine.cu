@@ -639,6 +639,71 @@ void toar_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double*
           out, ldo, perm, s);
 }
 
+// μ = 0 (θ = 1) chunks: symmetric Lanczos on A from u = A v (lanczos.cu; "Lanczos (for A = Aᵀ)"):
+// φ v = c_0 v + ‖u‖ Q_k f_1(T_k) e_1 with the same f_1, small_f and combine as the companion path.
+void lanczos_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double* V, int64_t ldv, int b,
+                   int gstart, int B, double* out, int64_t ldo, cudaStream_t s, bool user_order) {
+  const int32_t* perm = user_order ? op->perm.p : nullptr;
+  const int64_t n = op->n_loc;
+  const int K = ws->K;
+  const int64_t vs = (n + 1) * B;
+  double* g0z = ws->colp.p;
+  double* g1z = g0z + kMaxCols;
+  double* g0s = g1z + kMaxCols;
+  double* g1s = g0s + kMaxCols;
+  setup_chunk(op->mu_dev.p, gstart, b, B, g0z, g1z, g0s, g1s, ws->vcol.p, ws->tcol.p, s);
+  VecPtrs Q{};
+  for (int i = 0; i <= K; ++i) Q.p[i] = ws->basis.p + (int64_t)i * vs;
+  batch_inputs(V, ldv, B, n, ws->Vb.p, ws->vcol.p, perm, s);
+  const int G = lanczos_grid(n, B);
+  const size_t need = (size_t)G * B;
+  if (ws->partials.n < need) ws->partials.alloc(need);
+  double* sc = ws->cg_sc.p;  // 4 slots per column: [β_j, α_j, scale, active]
+  const double btol = op->opts.breakdown_tol;
+  const int pres = multi(op) ? 1 : 0;
+  auto scalar = [&](int which, int j) {
+    if (pres) {
+      reduce_partials(ws->partials.p, B, G, ws->sums1.p, s);
+      allreduce(op, ws->sums1.p, (size_t)B, s);
+    }
+    lanczos_scalar(which, j, n, pres, ws->partials.p, ws->sums1.p, B, K, btol, sc, ws->H.p, ws->n0.p, ws->keff.p, s);
+  };
+  WL_CUDA(cudaMemsetAsync(ws->H.p, 0, sizeof(double) * B * (K + 1) * K, s));
+  double* q0 = const_cast<double*>(Q.p[0]);
+  do_spmv(op, ws, ws->Vb.p, B, nullptr, nullptr, nullptr, nullptr, q0, B, s);  // u = A v  (a3 seed, μ = 0)
+  lanczos_vec(0, q0, nullptr, nullptr, n, B, sc, ws->partials.p, s);
+  scalar(0, 0);
+  lanczos_vec(3, q0, nullptr, nullptr, n, B, sc, ws->partials.p, s);            // q_0 = u / ‖u‖
+  for (int j = 0; j < K; ++j) {
+    double* qj = const_cast<double*>(Q.p[j]);
+    double* w = const_cast<double*>(Q.p[j + 1]);
+    do_spmv(op, ws, qj, B, nullptr, nullptr, nullptr, nullptr, w, B, s);       // a4 at μ = 0: w' = A q_j
+    lanczos_vec(1, qj, w, nullptr, n, B, sc, ws->partials.p, s);
+    scalar(1, j);                                                                 // α_j
+    lanczos_vec(2, w, qj, j > 0 ? Q.p[j - 1] : nullptr, n, B, sc, ws->partials.p, s);
+    scalar(2, j);                                                                 // β_{j+1}
+    lanczos_vec(3, w, nullptr, nullptr, n, B, sc, ws->partials.p, s);            // q_{j+1}
+  }
+  SmallFArgs f{};
+  f.H = ws->H.p;
+  f.K = K;
+  f.keff = ws->keff.p;
+  f.kind = op->fkind;
+  f.param = op->fparam;
+  f.coeffs = op->coeffs_dev.p;
+  f.ncoeffs = (int)op->coeffs.size();
+  f.n0 = ws->n0.p;
+  f.s = nullptr;
+  f.comb = ws->comb.p;
+  f.scratch = ws->scratch.p;
+  f.B = B;
+  f.err = op->opts.tol > 0.0 ? ws->kerr.p : nullptr;
+  small_f(f, s);
+  if (op->opts.tol > 0.0) krylov_check(ws->kerr.p, B, op->opts.tol, op->kstat.p, s);
+  combine(mode, op->lscale, Q, K, n, B, ws->comb.p, V, ldv, ws->vcol.p, op->c0, op->tprime.p, op->n_theta, ws->tcol.p,
+          out, ldo, perm, s);
+}
+
 // Resolvent action by Jacobi-preconditioned CG on the deformed Laplacian (cg.cu; opts.solver ==
 // WL_SOLVER_CG): x = 𝒜_θ(α)^{-1} V per column, then φ V = (1-μ²α²) x.  Vector roles reuse the
 // Krylov basis memory: x, r, p, q.  Synchronizes every opts.cg_check iterations.
@@ -703,7 +768,10 @@ void cg_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double* V
 
 void run_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double* V, int64_t ldv, int b, int gstart,
                int B, double* out, int64_t ldo, cudaStream_t s, bool user_order = true) {
+  bool walk = op->opts.reorth == 2 && op->opts.lanczos;  // every column θ = 1 (μ = 0): Lanczos on A
+  for (int c = 0; c < B && walk; ++c) walk = op->mu[(gstart + c) / b] == 0.0;
   if (op->opts.solver == WL_SOLVER_CG) cg_chunk(op, ws, mode, V, ldv, b, gstart, B, out, ldo, s, user_order);
+  else if (walk) lanczos_chunk(op, ws, mode, V, ldv, b, gstart, B, out, ldo, s, user_order);
   else if (op->opts.reorth == 2) toar_chunk(op, ws, mode, V, ldv, b, gstart, B, out, ldo, s, user_order);
   else krylov_chunk(op, ws, mode, V, ldv, b, gstart, B, out, ldo, s, user_order);
 }
@@ -1073,6 +1141,7 @@ void wl_opts_default(wl_opts* o) {
   o->cg_check = 8;
   o->tol = 0.0;
   o->halo_overlap = 1;
+  o->lanczos = 1;
 }
 
 wl_status wl_partition(int64_t n, const int64_t* row_ptr, int32_t nranks, int64_t* bounds) {

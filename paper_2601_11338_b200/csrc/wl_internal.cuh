@@ -199,6 +199,15 @@ void minres_vec(int phase, const MinresArgs& a, cudaStream_t s);
 // which: 0 after phase 0, 1 after phase 2, 2 after phase 3
 void minres_scalar(int which, const MinresArgs& a, cudaStream_t s);
 
+// ---------------------------------------------------------------- μ = 0 Lanczos (lanczos.cu)
+int lanczos_grid(int64_t n, int B);
+// phase 0: partials of Σ x²; 1: Σ x·y; 2: x = x − α y − β qm with partials of ‖x‖²; 3: x *= scale
+void lanczos_vec(int phase, double* x, const double* y, const double* qm, int64_t n, int B, const double* sc,
+                 double* partials, cudaStream_t s);
+// which 0: β_0 = ‖u‖ (n0, scale); 1: α_j; 2: β_{j+1} (H, scale, breakdown -> keff)
+void lanczos_scalar(int which, int j, int64_t n, int presummed, const double* partials, double* sums, int B, int K,
+                    double btol, double* sc, double* H, double* n0, int* keff, cudaStream_t s);
+
 // ---------------------------------------------------------------- small dense functions
 // Per column c (problem), m = keff[c]: y_c = f_1(H_m) e_1 for the Arnoldi matrix H.
 // kind 3 (outer diffusion): problem p uses column 0's H and computes exp(-tau[p] H_m) e_1;

@@ -38,7 +38,8 @@ class _Opts(ctypes.Structure):
                 ("max_cols", ctypes.c_int32), ("breakdown_tol", ctypes.c_double),
                 ("rho_bound", ctypes.c_double), ("relabel", ctypes.c_int32), ("solver", ctypes.c_int32),
                 ("cg_tol", ctypes.c_double), ("cg_maxit", ctypes.c_int32), ("cg_check", ctypes.c_int32),
-                ("tol", ctypes.c_double), ("halo_overlap", ctypes.c_int32)]
+                ("tol", ctypes.c_double), ("halo_overlap", ctypes.c_int32),
+                ("lanczos", ctypes.c_int32)]
 
 
 def load():
@@ -350,7 +351,7 @@ class Operator:
     def __init__(self, n_global, row_ptr, col_idx, thetas=(1.0,), f=("exp", 1.0), variant=None,
                  row_range=None, comm: Comm | None = None, krylov_dim=30, reorth=2, max_cols=32,
                  breakdown_tol=1e-12, rho_bound=0.0, relabel=1, solver="krylov", cg_tol=1e-9, cg_maxit=1000,
-                 cg_check=8, lap_scale=1.0, krylov_tol=0.0, halo_overlap=1, stream=None):
+                 cg_check=8, lap_scale=1.0, krylov_tol=0.0, halo_overlap=1, lanczos=1, stream=None):
         lib = load()
         rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
         ci = np.ascontiguousarray(col_idx, dtype=np.int32)
@@ -382,6 +383,7 @@ class Operator:
         opts.cg_tol, opts.cg_maxit, opts.cg_check = cg_tol, cg_maxit, cg_check
         opts.tol = krylov_tol
         opts.halo_overlap = halo_overlap
+        opts.lanczos = lanczos
         h = ctypes.c_void_p()
         _check(lib.wl_operator_create(comm.handle if comm else None, n_global, rb, re, rp.ctypes.data,
                                       ci.ctypes.data, variant, len(thetas) if variant == WL_BTDW else 1,

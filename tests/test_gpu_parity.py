@@ -526,3 +526,54 @@ def test_full_c2_markov_vs_series(wl):
         p = S.phi_apply(g, 1.0 - th, f, p / t, rA, A=A)
         assert relerr(got[:, k], p).max() < TOL
         assert abs(got[:, k].sum() - 1.0) < 1e-12
+
+
+def test_bitwise_reproducible_race_probe(wl):
+    """compute-sanitizer is closed on this GPU pool (profiles/r02_compute_sanitizer_closed.log), so races are
+    probed by determinism: every reduction on the path is fixed-order by design (per-CTA partials summed in CTA
+    order, the hub-row chunks summed in chunk order by the last arriver, the mbarrier rings consumed in stage
+    order), so repeated actions must agree BIT FOR BIT.  A hub with 3000 neighbours (two 2048-nonzero chunks and
+    a ticket), 11 θ columns (32-byte lane gathers over the padded block), TOAR and DCGS2 rings, CG, diffusion."""
+    r = gg.rmat(10, 900, 4000, seed=3, perm_seed=4)
+    edges = [(int(i), int(j)) for i in range(r.n) for j in r.col_idx[r.row_ptr[i]:r.row_ptr[i + 1]] if i < j]
+    n = r.n + 3001
+    edges += [(r.n, r.n + 1 + k) for k in range(3000)] + [(0, r.n)]
+    g = gg.from_edges(n, edges)
+    rA = S.rho_A(g)
+    V = torch.from_numpy(gg.vectors(n, 1, 5)).cuda()
+    x0 = torch.zeros(n, dtype=torch.float64, device="cuda")
+    x0[0] = 1.0
+    for kw in (dict(reorth=2), dict(reorth=1), dict(solver="cg", f=("resolvent", 0.5 / rA))):
+        kw.setdefault("f", ("exp", 1.0 / rA))
+        op = wl.Operator(n, g.row_ptr, g.col_idx, thetas=[round(0.1 * i, 1) for i in range(11)], krylov_dim=16, **kw)
+        outs = [op.apply(V).cpu().numpy() for _ in range(4)]
+        if kw.get("solver") != "cg":
+            outs += [op.diffuse(x0, [0.5, 2.0], k_out=12, theta_index=4).cpu().numpy() for _ in range(2)]
+        op.close()
+        for a, b in zip(outs[0:3], outs[1:4]):
+            assert np.array_equal(a, b), kw
+        if len(outs) > 4:
+            assert np.array_equal(outs[4], outs[5]), kw
+
+
+@pytest.mark.parametrize("f", [("exp", None), ("resolvent", None), ("series", [1.0, 0.5, 0.25, 0.125, 1.0 / 16])])
+def test_lanczos_walk_path_vs_series(wl, f):
+    """θ = 1 (all walks, μ = 0): batches whose columns are all θ = 1 take the symmetric Lanczos path
+    (opts.lanczos); against the series oracle and against TOAR on Z (lanczos = 0), on power-law, BA
+    and road-like graphs spanning many tiles, b = 3, plus t = φ1 at creation."""
+    graphs = [gg.rmat(14, 12000, 150000, seed=21, perm_seed=22), gg.barabasi_albert(20000, 5, 31),
+              gg.grid_lcc(150, 149, 0.3, 41)]
+    for g in graphs:
+        rA = S.rho_A(g)
+        fo = C.exp(1.0 / rA) if f[0] == "exp" else C.resolvent(0.5 / rA) if f[0] == "resolvent" else C.series(f[1])
+        fa = (f[0], fo.param if f[0] != "series" else f[1])
+        V = gg.vectors(g.n, 3, 77)
+        outs = []
+        for lz in (1, 0):
+            op = wl.Operator(g.n, g.row_ptr, g.col_idx, variant="walk", f=fa, lanczos=lz)
+            outs.append((op.apply(torch.from_numpy(V).cuda()).cpu().numpy(), op.diag_shift().cpu().numpy()[:, 0]))
+            op.close()
+        ref = S.laplacian_apply(g, 0.0, fo, V, rA)
+        assert relerr(outs[0][0], ref).max() < TOL, (g.name, f[0])
+        assert relerr(outs[0][1], S.total_communicability(g, 0.0, fo, rA)).max() < TOL
+        assert relerr(outs[0][0], outs[1][0]).max() < 1e-12
