@@ -240,8 +240,9 @@ def run_walklap(args):
     thetas = cfg["thetas"]
     K = args.krylov if args.krylov else cfg["krylov_dim"]
     op = wl.Operator(g.n, rp, ci, thetas=thetas, f=("exp", beta), row_range=(rb, re), comm=comm, krylov_dim=K,
-                     relabel=args.relabel,
-                     max_cols=args.max_cols)
+                     relabel=args.relabel, max_cols=args.max_cols,
+                     krylov_tol=args.adaptive if args.adaptive > 0 else 0.0,
+                     krylov_adaptive=1 if args.adaptive > 0 else 0)
     torch.cuda.synchronize()
     t_create = time.time() - t0
     b = args.b if args.b else cfg["b"]
@@ -260,6 +261,7 @@ def run_walklap(args):
         dist.barrier()
     torch.cuda.synchronize()
     l0 = wl.launch_count()
+    _, ks0, kb0 = ws.stats()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         ev0.record(stream)
@@ -268,6 +270,8 @@ def run_walklap(args):
         ev1.record(stream)
         torch.cuda.synchronize()
     launches = wl.launch_count() - l0
+    _, ks1, kb1 = ws.stats()
+    k_mean = (ks1 - ks0) / max(1, kb1 - kb0)
     ms = ev0.elapsed_time(ev1) / args.steps
     # per-kernel table: the same K steps again with per-launch-scope CUDA events (kept out of the timed region)
     torch.cuda.synchronize()
@@ -325,7 +329,8 @@ def run_walklap(args):
     # ---- roofline of the dominant kernel (rank 0's kernels; live CUDA-event timing) ----
     peak, peak_src = peaks()
     nnz_loc = int(ci.shape[0])
-    ab = algorithmic_bytes(n_loc, nnz_loc, op.n_halo, G, K, ws_bmax(op, b), b, op.n_theta, reorth=op.reorth)
+    Kab = int(round(k_mean)) if args.adaptive > 0 else K  # the steps actually taken
+    ab = algorithmic_bytes(n_loc, nnz_loc, op.n_halo, G, Kab, ws_bmax(op, b), b, op.n_theta, reorth=op.reorth)
     kernels = {}
     for name, (tot_ms, cnt) in prof.items():
         per_step_ms = tot_ms / args.steps
@@ -362,6 +367,7 @@ def run_walklap(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded R-MAT, graphgen)",
             "config": {"workload": f"{args.config}: {cfg['desc']}", "n": g.n, "nnz": g.nnz,
                        "thetas": thetas, "b": b, "actions_per_step": actions, "krylov_dim": K,
+                       "krylov_adaptive": ({"tol": args.adaptive, "mean_steps": k_mean} if args.adaptive > 0 else None),
                        "f": f"exp(beta x), beta=1/rho(A)={beta:.6g}", "global_batch": actions,
                        "parallelism": f"row-partition x{world} (NCCL halo + allreduce)",
                        "l2": "inputs larger than L2 (col_idx 1.6 GB, basis tens of GB): no flush",
@@ -825,6 +831,8 @@ def main():
     ap.add_argument("--krylov", type=int, default=0)
     ap.add_argument("--rho-k", type=int, default=60)
     ap.add_argument("--max-cols", type=int, default=32, help="columns per internal Krylov batch (opts.max_cols)")
+    ap.add_argument("--adaptive", type=float, default=0.0,
+                    help="> 0: stop each Arnoldi process once the a-posteriori estimate is below this (opts.krylov_adaptive)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--graph", action="store_true", help="also time the step captured as one CUDA graph")

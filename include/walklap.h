@@ -112,6 +112,11 @@ typedef struct {
                            all-walk operator, where q_k = A^k) run the symmetric three-term Lanczos
                            recurrence on A from A v ("Lanczos (for A = Aᵀ)") instead of TOAR on Z:
                            three n-block passes per step instead of two passes over the whole basis */
+  int32_t krylov_adaptive; /* 1 (requires tol > 0; TOAR path): stop the Arnoldi process early, after the
+                           first step k' >= 10 (checked every 2 steps) at which the a-posteriori estimate of
+                           `tol` is below tol for every column of the batch (reading R11); krylov_dim is
+                           then the cap.  Each check synchronizes the stream (not CUDA-graph capturable).
+                           0 (default): always krylov_dim steps */
 } wl_opts;
 
 typedef enum { WL_SOLVER_KRYLOV = 0, WL_SOLVER_CG = 1 } wl_solver;
@@ -198,8 +203,11 @@ wl_status wl_operator_diag_shift(const wl_operator* op, double* t_dev, int64_t l
 wl_status wl_workspace_create(const wl_operator* op, int32_t max_b, wl_workspace** out);
 void wl_workspace_destroy(wl_workspace* ws);
 /* Counters of a workspace (host): cg_iterations = CG iterations executed by actions on it so far
- * (per solve, the largest count over its columns; WL_SOLVER_CG only).  Any pointer may be NULL. */
-wl_status wl_workspace_stats(const wl_workspace* ws, int64_t* cg_iterations);
+ * (per solve, the largest count over its columns; WL_SOLVER_CG only); krylov_steps / krylov_batches =
+ * Arnoldi steps taken and Krylov batches run by the TOAR path (their ratio is the mean k' under
+ * opts.krylov_adaptive).  Any pointer may be NULL. */
+wl_status wl_workspace_stats(const wl_workspace* ws, int64_t* cg_iterations, int64_t* krylov_steps,
+                             int64_t* krylov_batches);
 
 /* ---- actions (step a3-a7) -------------------------------------------------------------------
  * V  : device, n_local x b, leading dimension ldv >= b

@@ -240,6 +240,10 @@ struct wl_workspace {
   DArr<int> cg_iters, cg_flags;
   int* cg_flags_host = nullptr;  // pinned: 2 flags + kMaxCols iteration counts
   int64_t cg_iterations = 0;     // executed CG iterations (max over the columns of each solve), cumulative
+  int64_t krylov_steps = 0, krylov_batches = 0;  // Arnoldi steps taken / Krylov batches run (adaptive stop)
+  DArr<int> kprobe;              // adaptive stop: probe dimensions per column + flag (4 ints)
+  DArr<double> kcomb;            // adaptive stop: the probe's f_1(H_m)e_1 (discarded)
+  int* kflag_host = nullptr;
   DArr<double> mk_p, mk_v;       // Markov chain: current distribution and p / t (internal order)
   DArr<double> kerr;             // a-posteriori Krylov error estimates per column (opts.tol > 0)
   DArr<double> seed;             // TOAR shared seeds: v, A v, A(Av) over the b input columns
@@ -266,6 +270,7 @@ struct wl_workspace {
     if (ev_halo) cudaEventDestroy(ev_halo);
     if (cg_flags_host) cudaFreeHost(cg_flags_host);
     if (mr_nact_host) cudaFreeHost(mr_nact_host);
+    if (kflag_host) cudaFreeHost(kflag_host);
     if (cublas) cublasDestroy(cublas);
   }
 };
@@ -590,6 +595,16 @@ void toar_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double*
   const double* xin = xg;  // bottom half of the vector the next SpMM applies Z to
   const int64_t ldx_in = padx ? ldg : B;
   const double* zin = U0;  // its top half
+  // opts.krylov_adaptive: after step j (j + 1 >= 10, every 2 steps) the a-posteriori estimate of smallf.cu is
+  // evaluated on the final H columns 0..j-1 (m = j); once every column is below opts.tol the basis stops
+  // at k' = j + 1 steps (the final pass completes column j).  One host synchronisation per probe.
+  const bool adaptive = op->opts.krylov_adaptive && op->opts.tol > 0.0;
+  int kstop = K;
+  if (adaptive) {
+    ws->kprobe.alloc(kMaxCols + 4);
+    ws->kcomb.alloc((size_t)(K + 1) * B);
+    if (!ws->kflag_host) WL_CUDA(cudaMallocHost(&ws->kflag_host, 4 * sizeof(int)));
+  }
   for (int j = 0; j < K; ++j) {
     const int m = j + 2;
     // a4: y = A x + μ(μ - d)⊙z  (bottom half of Z [z; x])
@@ -611,12 +626,40 @@ void toar_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double*
     t.out_ld[1] = 0;
     xin = xg;
     zin = zb;
+    if (adaptive && j + 1 < K && j + 1 >= 10 && (j + 1) % 2 == 0) {
+      int* kp = ws->kprobe.p;
+      int* flag = kp + kMaxCols;
+      clamp_keff(ws->keff.p, j, B, kp, flag, s);
+      SmallFArgs f{};
+      f.H = ws->H.p;
+      f.K = K;
+      f.keff = kp;
+      f.kind = op->fkind;
+      f.param = op->fparam;
+      f.coeffs = op->coeffs_dev.p;
+      f.ncoeffs = (int)op->coeffs.size();
+      f.n0 = ws->n0.p;
+      f.comb = ws->kcomb.p;
+      f.scratch = ws->scratch.p;
+      f.B = B;
+      f.err = ws->kerr.p;
+      small_f(f, s);
+      krylov_check(ws->kerr.p, B, op->opts.tol, flag, s);
+      WL_CUDA(cudaMemcpyAsync(ws->kflag_host, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+      WL_CUDA(cudaStreamSynchronize(s));
+      if ((ws->kflag_host[0] & 1) == 0) {
+        kstop = j + 1;
+        break;
+      }
+    }
   }
-  d.nq = K + 1;  // Gram row of the last U vector completes H column K-1
-  d.P = U.p[K + 1];
+  ws->krylov_steps += kstop;
+  ws->krylov_batches += 1;
+  d.nq = kstop + 1;  // Gram row of the last U vector completes H column kstop-1
+  d.P = U.p[kstop + 1];
   d.wa = nullptr;
-  dots((2 * (K + 1) + 3) * B);
-  coeffs(K, 1);
+  dots((2 * (kstop + 1) + 3) * B);
+  coeffs(kstop, 1);
   // a6: y = f_1(H_k) e_1 per column; a7: combine top halves U (Σ_i comb_i g_i)
   SmallFArgs f{};
   f.H = ws->H.p;
@@ -635,8 +678,8 @@ void toar_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double*
   small_f(f, s);
   if (op->opts.tol > 0.0) krylov_check(ws->kerr.p, B, op->opts.tol, op->kstat.p, s);
   toar_combine_coef(ws->comb.p, B, K, ws->keff.p, ws->toar_state.p, stride, ws->toar_comb.p, s);
-  combine(mode, op->lscale, U, K + 2, n, B, ws->toar_comb.p, V, ldv, ws->vcol.p, op->c0, op->tprime.p, op->n_theta, ws->tcol.p,
-          out, ldo, perm, s);
+  combine(mode, op->lscale, U, kstop + 2, n, B, ws->toar_comb.p, V, ldv, ws->vcol.p, op->c0, op->tprime.p, op->n_theta,
+          ws->tcol.p, out, ldo, perm, s);
 }
 
 // μ = 0 (θ = 1) chunks: symmetric Lanczos on A from u = A v (lanczos.cu; "Lanczos (for A = Aᵀ)"):
@@ -1142,6 +1185,7 @@ void wl_opts_default(wl_opts* o) {
   o->tol = 0.0;
   o->halo_overlap = 1;
   o->lanczos = 1;
+  o->krylov_adaptive = 0;
 }
 
 wl_status wl_partition(int64_t n, const int64_t* row_ptr, int32_t nranks, int64_t* bounds) {
@@ -1288,10 +1332,13 @@ void wl_operator_destroy(wl_operator* op) {
   delete op;
 }
 
-wl_status wl_workspace_stats(const wl_workspace* ws, int64_t* cg_iterations) {
+wl_status wl_workspace_stats(const wl_workspace* ws, int64_t* cg_iterations, int64_t* krylov_steps,
+                             int64_t* krylov_batches) {
   return guarded([&] {
     if (!ws) throw Error(WL_EINVAL, "ws is NULL");
     if (cg_iterations) *cg_iterations = ws->cg_iterations;
+    if (krylov_steps) *krylov_steps = ws->krylov_steps;
+    if (krylov_batches) *krylov_batches = ws->krylov_batches;
   });
 }
 

@@ -333,6 +333,20 @@ void pack_rows(const double* src, int64_t lds, const int32_t* idx, int64_t cnt, 
   WL_CUDA(cudaGetLastError());
 }
 
+namespace {
+__global__ void clamp_keff_kernel(const int* keff, int m, int B, int* out, int* flag) {
+  const int c = threadIdx.x;
+  if (c < B) out[c] = min(keff[c], m);
+  if (c == 0) flag[0] = 0;
+}
+}  // namespace
+
+void clamp_keff(const int* keff, int m, int B, int* out, int* flag, cudaStream_t s) {
+  WL_LAUNCH("krylov_check");
+  clamp_keff_kernel<<<1, 32, 0, s>>>(keff, m, B, out, flag);
+  WL_CUDA(cudaGetLastError());
+}
+
 void krylov_check(const double* err, int B, double tol, int* flag, cudaStream_t s) {
   WL_LAUNCH("krylov_check");
   krylov_check_kernel<<<1, 32, 0, s>>>(err, B, tol, flag);

@@ -212,11 +212,11 @@ __global__ void __launch_bounds__(kBS) small_f_kernel(SmallFArgs a) {
   }
   __syncthreads();
   const double n0 = a.n0[c];
-  // a-posteriori estimate (kinds 0-2): ||u|| h_{k+1,k} |e_k^T y| relative to ||u|| ||y||; exact (0) after a
-  // breakdown (m < K: invariant Krylov space)
+  // a-posteriori estimate (kinds 0-2): ||u|| h_{m+1,m} |e_m^T y| relative to ||u|| ||y||; exact (0) after a
+  // breakdown (h_{m+1,m} = 0: invariant Krylov space).  m < K is also the probe of the adaptive stop.
   if (a.kind != 3 && a.err && threadIdx.x == 0) {
     double e = 0.0;
-    if (m == K && m > 0) {
+    if (m > 0) {
       double yy = 0.0;
       for (int i = 0; i < m; ++i) yy += y[i] * y[i];
       e = yy > 0.0 ? fabs(H[(m - 1) * (K + 1) + m] * y[m - 1]) / sqrt(yy) : 0.0;

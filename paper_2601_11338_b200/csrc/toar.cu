@@ -157,9 +157,10 @@ __global__ void __launch_bounds__(kCoefThreads) toar_coeffs_kernel(const double*
   const int M = K + 3;
   State S(state + (size_t)c * stride, M, K);
   double* Hc = H + (size_t)c * (K + 1) * K;  // (row i, col l) at Hc[l*(K+1) + i]
-  const int m = final_pass ? K + 2 : (j < 0 ? 1 : j + 2);  // U vectors with a Gram row after this step
+  // the final pass after k' <= K steps (k' = K, or earlier with opts.krylov_adaptive) is called with j = k'
+  const int m = final_pass ? j + 2 : (j < 0 ? 1 : j + 2);  // U vectors with a Gram row after this step
   const int nq = m - 1;
-  const int nt = j < 0 ? 0 : (final_pass ? K : j + 1);      // q vectors used this step (q_0..q_j)
+  const int nt = j < 0 ? 0 : (final_pass ? j : j + 1);      // q vectors used this step (q_0..q_j)
   // shared layout: L (m x M), TQg/TQf (nt x M), QHg/QHf, ZY, work vectors
   double* L = smem;
   double* TG = L + (size_t)m * M;
@@ -228,7 +229,7 @@ __global__ void __launch_bounds__(kCoefThreads) toar_coeffs_kernel(const double*
   // stage the state: one flat index space over (L, L^{-1}), (TQg, TQf), (QHg, QHf), H; each thread
   // issues the global loads of 4 pairs before it stores any of them (one L2 round trip per 4 pairs
   // instead of one per array)
-  const int hcols = j < 0 ? 0 : (final_pass ? K : j + 1);
+  const int hcols = j < 0 ? 0 : (final_pass ? j : j + 1);
   {
     const int nL = (m - 1) * M, nT = nt * M, nH = hcols * (K + 1);
     const int tkeep = final_pass ? nT : (nt - 1) * M;  // q_j is recomputed this step
@@ -391,6 +392,7 @@ __global__ void __launch_bounds__(kCoefThreads) toar_coeffs_kernel(const double*
       if (!alive_s) keff[c] = j;
     }
     if (!alive_s) S.SC[kAlive] = 0.0;
+    if (final_pass && keff[c] > j) keff[c] = j;  // stopped after j < K steps
   }
   __syncthreads();
   if (final_pass) return;

@@ -251,6 +251,8 @@ void repack_rows(const double* src, int64_t lds, int64_t n, int B, double* dst, 
 void fill(double* p, int64_t n, double v, cudaStream_t s);
 // sticky convergence flag: flag[0] |= 1 and flag[1] = max estimate (as bits) when err[c] > tol
 void krylov_check(const double* err, int B, double tol, int* flag, cudaStream_t s);
+// out[c] = min(keff[c], m) (c < B) and flag[0] = 0: the probe of the adaptive Krylov stop
+void clamp_keff(const int* keff, int m, int B, int* out, int* flag, cudaStream_t s);
 void fill_hash(double* p, int64_t n, uint64_t seed, int64_t i0, cudaStream_t s);  // 0.5 + U[0,1)
 void gather_col(const double* src, int64_t lds, const int32_t* perm, int64_t n, double* dst, cudaStream_t s);
 void scatter_col(const double* src, const int32_t* perm, int64_t n, double* dst, int64_t ldd, cudaStream_t s);

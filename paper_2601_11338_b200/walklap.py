@@ -39,7 +39,7 @@ class _Opts(ctypes.Structure):
                 ("rho_bound", ctypes.c_double), ("relabel", ctypes.c_int32), ("solver", ctypes.c_int32),
                 ("cg_tol", ctypes.c_double), ("cg_maxit", ctypes.c_int32), ("cg_check", ctypes.c_int32),
                 ("tol", ctypes.c_double), ("halo_overlap", ctypes.c_int32),
-                ("lanczos", ctypes.c_int32)]
+                ("lanczos", ctypes.c_int32), ("krylov_adaptive", ctypes.c_int32)]
 
 
 def load():
@@ -74,7 +74,7 @@ def load():
         "wl_operator_diag_shift": ([vp, vp, i64, vp], ctypes.c_int),
         "wl_workspace_create": ([vp, i32, pvp], ctypes.c_int),
         "wl_workspace_destroy": ([vp], None),
-        "wl_workspace_stats": ([vp, vp], ctypes.c_int),
+        "wl_workspace_stats": ([vp, vp, vp, vp], ctypes.c_int),
         "wl_apply": ([vp, i32, vp, i64, vp, i64, vp, vp], ctypes.c_int),
         "wl_phi_apply": ([vp, i32, vp, i64, vp, i64, vp, vp], ctypes.c_int),
         "wl_apply_host": ([vp, i32, vp, i64, vp, i64, vp, vp], ctypes.c_int),
@@ -315,9 +315,13 @@ def run_loopback(nranks: int, fn, device: int = 0, timeout: float = 600.0):
 class Workspace:
     def cg_iterations(self) -> int:
         """CG iterations executed by actions on this workspace so far (wl_workspace_stats)."""
-        v = ctypes.c_int64()
-        _check(load().wl_workspace_stats(self.handle, ctypes.byref(v)))
-        return v.value
+        return self.stats()[0]
+
+    def stats(self):
+        """(cg_iterations, krylov_steps, krylov_batches) so far (wl_workspace_stats)."""
+        v, k, b = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _check(load().wl_workspace_stats(self.handle, ctypes.byref(v), ctypes.byref(k), ctypes.byref(b)))
+        return v.value, k.value, b.value
 
     def __init__(self, op: "Operator", max_b: int):
         self.op = op
@@ -351,7 +355,8 @@ class Operator:
     def __init__(self, n_global, row_ptr, col_idx, thetas=(1.0,), f=("exp", 1.0), variant=None,
                  row_range=None, comm: Comm | None = None, krylov_dim=30, reorth=2, max_cols=32,
                  breakdown_tol=1e-12, rho_bound=0.0, relabel=1, solver="krylov", cg_tol=1e-9, cg_maxit=1000,
-                 cg_check=8, lap_scale=1.0, krylov_tol=0.0, halo_overlap=1, lanczos=1, stream=None):
+                 cg_check=8, lap_scale=1.0, krylov_tol=0.0, halo_overlap=1, lanczos=1, krylov_adaptive=0,
+                 stream=None):
         lib = load()
         rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
         ci = np.ascontiguousarray(col_idx, dtype=np.int32)
@@ -384,6 +389,7 @@ class Operator:
         opts.tol = krylov_tol
         opts.halo_overlap = halo_overlap
         opts.lanczos = lanczos
+        opts.krylov_adaptive = krylov_adaptive
         h = ctypes.c_void_p()
         _check(lib.wl_operator_create(comm.handle if comm else None, n_global, rb, re, rp.ctypes.data,
                                       ci.ctypes.data, variant, len(thetas) if variant == WL_BTDW else 1,

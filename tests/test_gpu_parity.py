@@ -276,6 +276,14 @@ def test_full_c4_theta_sweep_vs_series(wl):
     got = op.apply(torch.from_numpy(V).cuda()).cpu().numpy()
     t_gpu = op.diag_shift().cpu().numpy()
     op.close()
+    # the adaptive-k bench line (bench.py --adaptive 1e-13): same workload, Arnoldi stopped by the estimate
+    opa = wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=cfg["thetas"], f=("exp", beta), krylov_dim=30,
+                      krylov_tol=1e-13, krylov_adaptive=1)
+    ws = opa.workspace(1)
+    got_a = opa.apply(torch.from_numpy(V).cuda(), ws=ws).cpu().numpy()
+    _, ksteps, kbatches = ws.stats()
+    opa.close()
+    assert ksteps / kbatches < 30
     f = C.exp(beta)
     ones_v = np.stack([np.ones(g.n), V[:, 0]], axis=1)
     for th in (0.0, 0.5, 1.0):
@@ -285,6 +293,7 @@ def test_full_c4_theta_sweep_vs_series(wl):
         ref = t * V[:, 0] - phi[:, 1]
         assert relerr(t_gpu[:, i], t).max() < TOL, th
         assert relerr(got[:, i], ref).max() < TOL, th
+        assert relerr(got_a[:, i], ref).max() < TOL, ("adaptive", th)
     # Σ_i (𝕃v)_i = tᵀv - 1ᵀφv = 0 for every θ column (φ symmetric, 1ᵀφ = tᵀ)
     for j in range(len(cfg["thetas"])):
         assert abs(got[:, j].sum()) < 1e-10 * np.abs(got[:, j]).sum()
@@ -577,3 +586,25 @@ def test_lanczos_walk_path_vs_series(wl, f):
         assert relerr(outs[0][0], ref).max() < TOL, (g.name, f[0])
         assert relerr(outs[0][1], S.total_communicability(g, 0.0, fo, rA)).max() < TOL
         assert relerr(outs[0][0], outs[1][0]).max() < 1e-12
+
+
+def test_adaptive_krylov_stop(wl):
+    """opts.krylov_adaptive: the Arnoldi process stops at the first k' >= 10 where the a-posteriori estimate
+    (reading R11) is below opts.tol for every column; the result still matches the series oracle (1e-10),
+    and k' < krylov_dim on these graphs (k = 15 reaches 1.9e-16 on C2)."""
+    graphs = [gg.rmat(14, 12000, 150000, seed=21, perm_seed=22), gg.grid_lcc(150, 149, 0.3, 41)]
+    thetas = [0.0, 0.5, 0.8]
+    for g in graphs:
+        rA = S.rho_A(g)
+        f = C.exp(1.0 / rA)
+        V = gg.vectors(g.n, 2, 7)
+        op = wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=thetas, f=("exp", f.param), krylov_dim=40,
+                         krylov_tol=1e-13, krylov_adaptive=1)
+        ws = op.workspace(2)
+        LV = op.apply(torch.from_numpy(V).cuda(), ws=ws).cpu().numpy()
+        op.wait()
+        _, steps, batches = ws.stats()
+        op.close()
+        assert steps / batches < 40, (g.name, steps, batches)
+        for i, th in enumerate(thetas):
+            assert relerr(LV[:, 2 * i:2 * i + 2], S.laplacian_apply(g, 1.0 - th, f, V, rA)).max() < TOL, (g.name, th)
