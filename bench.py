@@ -578,8 +578,9 @@ def run_diffusion(args):
     rho = probe.spectral_radius(k=args.rho_k)
     probe.close()
     op = wl.Operator(g.n, rp, ci, thetas=cfg["thetas"], f=("exp", 1.0 / rho), row_range=(rb, re), comm=comm,
-                     relabel=args.relabel,
-                     krylov_dim=cfg["krylov_dim"])
+                     relabel=args.relabel, krylov_dim=cfg["krylov_dim"],
+                     krylov_tol=args.adaptive if args.adaptive > 0 else 0.0,
+                     krylov_adaptive=1 if args.adaptive > 0 else 0)
     torch.cuda.synchronize()
     t_create = time.time() - t0
     kind, lo, hi, nt = cfg.get("taus", ("linspace", 0.0, 100.0, 90))
@@ -599,6 +600,7 @@ def run_diffusion(args):
         dist.barrier()
     stream = torch.cuda.current_stream()
     l0 = wl.launch_count()
+    _, ks0, kb0 = ws.stats()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         ev0.record(stream)
@@ -607,6 +609,8 @@ def run_diffusion(args):
         ev1.record(stream)
         torch.cuda.synchronize()
     launches = wl.launch_count() - l0
+    _, ks1, kb1 = ws.stats()
+    k_mean = (ks1 - ks0) / max(1, kb1 - kb0)  # inner Arnoldi steps per action
     ms = ev0.elapsed_time(ev1) / args.steps
     if world > 1:
         tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
@@ -619,8 +623,30 @@ def run_diffusion(args):
     wl.profile_enable(False)
     kernels = {k: {"ms_per_step": v[0], "launches_per_step": v[1], "share": v[0] / ms}
                for k, v in sorted(wl.profile_collect().items(), key=lambda kv: -kv[1][0])}
+    # algorithmic bytes per sweep: k_out inner B = 1 actions of k' steps + the outer Arnoldi
+    # (DCGS2 ring passes on n-vectors: dots read q_0..q_{j-1}, p_j, w; update also writes q_j, p_{j+1})
+    # + the τ combine
+    n_l = op.n_local
+    ab = {}
+    inner = algorithmic_bytes(n_l, int(ci.shape[0]), op.n_halo, 1, int(round(k_mean)), 1, 1, 1, reorth=op.reorth)
+    for kk, v in inner.items():
+        ab[kk] = ab.get(kk, 0) + k_out * v
+    for j in range(k_out):
+        ab["dcgs2_dots"] = ab.get("dcgs2_dots", 0) + (j + 2) * 8 * n_l
+        ab["dcgs2_update"] = ab.get("dcgs2_update", 0) + (j + 4) * 8 * n_l
+    ab["dcgs2_dots"] += (k_out + 1) * 8 * n_l
+    ab["lanczos_combine"] = 8 * n_l * (k_out + nt)
+    peak, peak_src = peaks()
+    for kk, v in kernels.items():
+        if ab.get(kk):
+            v["alg_bytes_per_step"] = ab[kk]
+            v["achieved_gbs"] = ab[kk] / (v["ms_per_step"] / 1e3) / 1e9
+            v["frac"] = v["achieved_gbs"] / peak
+    top = max((kk for kk in kernels if "alg_bytes_per_step" in kernels[kk]), key=lambda kk: kernels[kk]["ms_per_step"])
+    roof = {"kernel": top, "bound": "hbm", "achieved": kernels[top]["achieved_gbs"], "peak": peak, "unit": "GB/s",
+            "frac": kernels[top]["frac"], "peak_source": peak_src, "traffic": None,
+            "alg_bytes_per_launch": ab[top] / max(1, kernels[top]["launches_per_step"])}
     if rank == 0:
-        peak, peak_src = peaks()
         line = {
             "metric": METRIC, "value": actions / (ms / 1e3), "unit": "actions/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -628,8 +654,9 @@ def run_diffusion(args):
             "config": {"workload": f"{cfg['desc']}; diffusion exp(-tau L)x0 (step a9), {nt} tau in [{lo}, {hi}], "
                                    f"k_out={k_out}, inner k={cfg['krylov_dim']}, theta={cfg['thetas']}",
                        "n": g.n, "nnz": g.nnz, "sweeps_per_s": 1e3 / ms,
+                       "krylov_adaptive": ({"tol": args.adaptive, "mean_steps": k_mean} if args.adaptive > 0 else None),
                        "setup_s": {"generate": round(t_gen, 2), "operator_create_incl_t": round(t_create, 2)}},
-            "roofline": None, "kernels": kernels, "cpu_baseline": None, "e2e": None, "gpu_launches": launches,
+            "roofline": roof, "kernels": kernels, "cpu_baseline": None, "e2e": None, "gpu_launches": launches,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

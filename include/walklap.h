@@ -113,7 +113,7 @@ typedef struct {
                            recurrence on A from A v ("Lanczos (for A = Aᵀ)") instead of TOAR on Z:
                            three n-block passes per step instead of two passes over the whole basis */
   int32_t krylov_adaptive; /* 1 (requires tol > 0; TOAR path): stop the Arnoldi process early, after the
-                           first step k' >= 10 (checked every 2 steps) at which the a-posteriori estimate of
+                           first step k' >= 6 (checked every 2 steps) at which the a-posteriori estimate of
                            `tol` is below tol for every column of the batch (reading R11); krylov_dim is
                            then the cap.  Each check synchronizes the stream (not CUDA-graph capturable).
                            0 (default): always krylov_dim steps */

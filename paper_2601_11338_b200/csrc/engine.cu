@@ -595,7 +595,7 @@ void toar_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double*
   const double* xin = xg;  // bottom half of the vector the next SpMM applies Z to
   const int64_t ldx_in = padx ? ldg : B;
   const double* zin = U0;  // its top half
-  // opts.krylov_adaptive: after step j (j + 1 >= 10, every 2 steps) the a-posteriori estimate of smallf.cu is
+  // opts.krylov_adaptive: after step j (j + 1 >= 6, every 2 steps) the a-posteriori estimate of smallf.cu is
   // evaluated on the final H columns 0..j-1 (m = j); once every column is below opts.tol the basis stops
   // at k' = j + 1 steps (the final pass completes column j).  One host synchronisation per probe.
   const bool adaptive = op->opts.krylov_adaptive && op->opts.tol > 0.0;
@@ -626,7 +626,7 @@ void toar_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double*
     t.out_ld[1] = 0;
     xin = xg;
     zin = zb;
-    if (adaptive && j + 1 < K && j + 1 >= 10 && (j + 1) % 2 == 0) {
+    if (adaptive && j + 1 < K && j + 1 >= 6 && (j + 1) % 2 == 0) {
       int* kp = ws->kprobe.p;
       int* flag = kp + kMaxCols;
       clamp_keff(ws->keff.p, j, B, kp, flag, s);

@@ -315,9 +315,15 @@ def test_full_c3_road_diffusion(wl):
     op = wl.Operator(g.n, g.row_ptr, g.col_idx, variant="nbt", f=("exp", f.param))
     X = op.diffuse(torch.from_numpy(x0).cuda(), taus, k_out=80).cpu().numpy()
     op.close()
+    # the adaptive inner-k line (bench.py --diffusion --adaptive 1e-13)
+    opa = wl.Operator(g.n, g.row_ptr, g.col_idx, variant="nbt", f=("exp", f.param), krylov_tol=1e-13,
+                      krylov_adaptive=1)
+    Xa = opa.diffuse(torch.from_numpy(x0).cuda(), taus, k_out=80).cpu().numpy()
+    opa.close()
     assert np.max(np.abs(X.sum(axis=0) - 1.0)) < 1e-10          # mass 1ᵀx(τ) = 1ᵀx0
     ref = chebyshev.diffusion(g, 1.0, f, x0, taus, rA)
     assert relerr(X, ref).max() < TOL
+    assert relerr(Xa, ref).max() < TOL
 
 
 def test_apply_captured_in_cuda_graph(wl):
@@ -589,7 +595,7 @@ def test_lanczos_walk_path_vs_series(wl, f):
 
 
 def test_adaptive_krylov_stop(wl):
-    """opts.krylov_adaptive: the Arnoldi process stops at the first k' >= 10 where the a-posteriori estimate
+    """opts.krylov_adaptive: the Arnoldi process stops at the first k' >= 6 where the a-posteriori estimate
     (reading R11) is below opts.tol for every column; the result still matches the series oracle (1e-10),
     and k' < krylov_dim on these graphs (k = 15 reaches 1.9e-16 on C2)."""
     graphs = [gg.rmat(14, 12000, 150000, seed=21, perm_seed=22), gg.grid_lcc(150, 149, 0.3, 41)]
