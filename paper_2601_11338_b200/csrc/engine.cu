@@ -15,6 +15,7 @@
 #include "wl_internal.cuh"
 
 #include <cublas_v2.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <atomic>
@@ -92,6 +93,9 @@ int num_sms() {
   cache[dev] = sms;
   return sms;
 }
+
+NvtxRange::NvtxRange(const char* name) { nvtxRangePushA(name); }
+NvtxRange::~NvtxRange() { nvtxRangePop(); }
 
 void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
   if (e == cudaSuccess) return;
@@ -292,6 +296,7 @@ void allreduce(const wl_operator* op, double* buf, size_t count, cudaStream_t s)
 void halo_exchange(const wl_operator* op, wl_workspace* ws, const double* src, int64_t lds, int B,
                    cudaStream_t s) {
   if (!multi(op)) return;
+  WL_NVTX("halo_exchange");
   pack_rows(src, lds, op->send_idx.p, op->n_send, B, ws->halo_send.p, s);
   std::vector<Xfer> sends, recvs;
   for (int p = 0; p < op->nranks; ++p) {
@@ -408,6 +413,7 @@ void spmv_scratch(const wl_operator* op, wl_workspace* ws, int B) {
 // false for the internal-order vectors of the outer diffusion Lanczos.
 void krylov_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double* V, int64_t ldv, int b,
                   int gstart, int B, double* out, int64_t ldo, cudaStream_t s, bool user_order) {
+  WL_NVTX("krylov_batch_dcgs2");
   const int32_t* perm = user_order ? op->perm.p : nullptr;
   const int64_t n = op->n_loc;
   const int K = ws->K;
@@ -506,6 +512,7 @@ void krylov_chunk(const wl_operator* op, wl_workspace* ws, int mode, const doubl
 // instead of DCGS2's two passes over 2n-vectors.  Same seeds, SpMM, f(H) and combine as krylov_chunk.
 void toar_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double* V, int64_t ldv, int b, int gstart,
                 int B, double* out, int64_t ldo, cudaStream_t s, bool user_order) {
+  WL_NVTX("krylov_batch_toar");
   const int32_t* perm = user_order ? op->perm.p : nullptr;
   const int64_t n = op->n_loc;
   const int K = ws->K;
@@ -606,6 +613,7 @@ void toar_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double*
     if (!ws->kflag_host) WL_CUDA(cudaMallocHost(&ws->kflag_host, 4 * sizeof(int)));
   }
   for (int j = 0; j < K; ++j) {
+    WL_NVTX("arnoldi_step");
     const int m = j + 2;
     // a4: y = A x + μ(μ - d)⊙z  (bottom half of Z [z; x])
     do_spmv(op, ws, xin, ldx_in, zin, g0z, g1z, nullptr, yb, B, s);
@@ -660,6 +668,7 @@ void toar_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double*
   d.wa = nullptr;
   dots((2 * (kstop + 1) + 3) * B);
   coeffs(kstop, 1);
+  WL_NVTX("f_of_H_and_combine");
   // a6: y = f_1(H_k) e_1 per column; a7: combine top halves U (Σ_i comb_i g_i)
   SmallFArgs f{};
   f.H = ws->H.p;
@@ -686,6 +695,7 @@ void toar_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double*
 // φ v = c_0 v + ‖u‖ Q_k f_1(T_k) e_1 with the same f_1, small_f and combine as the companion path.
 void lanczos_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double* V, int64_t ldv, int b,
                    int gstart, int B, double* out, int64_t ldo, cudaStream_t s, bool user_order) {
+  WL_NVTX("krylov_batch_lanczos");
   const int32_t* perm = user_order ? op->perm.p : nullptr;
   const int64_t n = op->n_loc;
   const int K = ws->K;
@@ -752,6 +762,7 @@ void lanczos_chunk(const wl_operator* op, wl_workspace* ws, int mode, const doub
 // Krylov basis memory: x, r, p, q.  Synchronizes every opts.cg_check iterations.
 void cg_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double* V, int64_t ldv, int b, int gstart,
               int B, double* out, int64_t ldo, cudaStream_t s, bool user_order) {
+  WL_NVTX("cg_solve");
   const int32_t* perm = user_order ? op->perm.p : nullptr;
   const int64_t n = op->n_loc;
   double* g0 = ws->colp.p;
@@ -1666,6 +1677,7 @@ void chol_qr2(const wl_operator* op, cublasHandle_t h, const double* src, int m,
 // [Re x | Im x] as two n x B blocks.  Returns the largest iteration count over the columns.
 int shifted_solve(const wl_operator* op, wl_workspace* ws, int theta_index, const double* U, int B, double xre,
                   double xim, double tol, int maxit, double* X, cudaStream_t s) {
+  WL_NVTX("minres_shifted_solve");
   const int64_t n = op->n_loc;
   const int64_t nb = std::max<int64_t>(1, n) * B;
   const bool cplx = xim != 0.0;

@@ -27,6 +27,16 @@ struct LaunchScope {
 };
 #define WL_LAUNCH(name) ::wl::LaunchScope wl_launch_scope_(name, s)
 
+// NVTX range over a host scope (Krylov phases: seeds, Arnoldi step, f(H) + combine, shifted solve, ...);
+// header-only NVTX3, a no-op unless a profiler is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name);
+  ~NvtxRange();
+};
+#define WL_NVTX_CAT2(a, b) a##b
+#define WL_NVTX_CAT(a, b) WL_NVTX_CAT2(a, b)
+#define WL_NVTX(name) ::wl::NvtxRange WL_NVTX_CAT(wl_nvtx_, __LINE__)(name)
+
 // ---------------------------------------------------------------- C ABI error plumbing
 // Every extern "C" entry point runs its body through guarded(): a thrown Error becomes its
 // wl_status and the thread-local message returned by wl_last_error().
