@@ -162,22 +162,24 @@ struct Ctx {
       }
     }
   }
-  // Σ y[col[z]] for z = z0 + first, z0 + first + step, ... < z1 (step = lane groups sharing the row)
+  // Σ y[col[z]] for z = z0 + first, z0 + first + step, ... < z1 (step = lane groups sharing the row,
+  // 0 <= first < step).  Rounds cover [base, base + kU step); the full-round test depends only on the
+  // shared base, so lane groups sharing a row never diverge: all full rounds, then one predicated round.
   __device__ Vec<VW> strided_sum(int z0, int z1, int first, int step) const {
     Vec<VW> acc = vzero<VW>();
-    int z = z0 + first;
-    const int full = z1 - (kU - 1) * step;  // rounds with all kU nonzeros present
-    for (; z < full; z += kU * step) {
+    int base = z0;
+    for (; base + kU * step <= z1; base += kU * step) {
       int cl[kU];
 #pragma unroll
-      for (int u = 0; u < kU; ++u) cl[u] = col(z + u * step);
+      for (int u = 0; u < kU; ++u) cl[u] = col(base + first + u * step);
       Vec<VW> v[kU];
 #pragma unroll
       for (int u = 0; u < kU; ++u) v[u] = gather(cl[u]);
 #pragma unroll
       for (int u = 0; u < kU; ++u) vadd(acc, v[u]);
     }
-    if (z < z1) {  // predicated tail round
+    const int z = base + first;
+    if (base < z1) {  // predicated tail round
       int cl[kU];
 #pragma unroll
       for (int u = 0; u < kU; ++u) cl[u] = (z + u * step < z1) ? col(z + u * step) : -1;
