@@ -150,6 +150,7 @@ struct CsrPart {
   int64_t nnz = 0;
   int n_small = 0, n_medium = 0, n_chunks = 0;
   int small_first = -1;  // small rows form the contiguous id range [small_first, +n_small), or -1
+  int n_iso = 0;          // the last n_iso rows of that range have no nonzeros
 
   void upload(const std::vector<int32_t>& rp, const std::vector<int32_t>& col_h, const std::vector<int32_t>* rows) {
     n_rows = (int32_t)rp.size() - 1;
@@ -170,6 +171,10 @@ struct CsrPart {
     n_medium = (int)md.size();
     // the batched small-row kernel needs contiguous ids and writes rows in place (no out_row)
     small_first = (!rows && !sm.empty() && sm.back() - sm.front() + 1 == (int32_t)sm.size()) ? sm.front() : -1;
+    // trailing rows of that range without nonzeros (isolated vertices sort last): a plain stream kernel
+    n_iso = 0;
+    if (small_first >= 0)
+      for (int64_t r = small_first + n_small - 1; r >= small_first && rp[r + 1] == rp[r]; --r) ++n_iso;
     n_chunks = (int)ch.size();
     small_rows.alloc(std::max<size_t>(1, sm.size()));
     medium_rows.alloc(std::max<size_t>(1, md.size()));
@@ -321,6 +326,7 @@ void spmv_part(const wl_operator* op, wl_workspace* ws, const CsrPart& part, boo
   a.small_rows = part.small_rows.p;
   a.n_small = part.n_small;
   a.small_first = part.small_first;
+  a.n_iso = part.n_iso;
   a.medium_rows = part.medium_rows.p;
   a.n_medium = part.n_medium;
   a.chunks = part.chunks.p;

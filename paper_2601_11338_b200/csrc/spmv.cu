@@ -370,6 +370,26 @@ __global__ void __launch_bounds__(kThreads) spmv_small_row1_kernel(SpmvArgs a) {
   ctx.write(r, z1 - z0, ctx.strided_sum(z0, z1, 0, 1));
 }
 
+// ---- rows without nonzeros at the end of the contiguous small range (isolated vertices: 40% of C4's ids):
+// out = scale ⊙ (g0 + g1 d) ⊙ x, a stream over the n_iso x B block (d = 0 unless degptr gives the full degree
+// of a split operator's local part)
+__global__ void __launch_bounds__(kThreads) spmv_iso_kernel(SpmvArgs a, int r0) {
+  if (a.active && *a.active == 0) return;
+  const int B = a.B;
+  const int64_t total = (int64_t)a.n_iso * B;
+  for (int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x; e < total; e += (int64_t)gridDim.x * kThreads) {
+    const int64_t i = e / B;
+    const int c = (int)(e - i * B);
+    const int64_t r = r0 + i;
+    double o = 0.0;
+    if (a.x) {
+      const double d = a.degptr ? (double)(__ldg(a.degptr + r + 1) - __ldg(a.degptr + r)) : 0.0;
+      o = ((a.g0 ? __ldg(a.g0 + c) : 0.0) + (a.g1 ? __ldg(a.g1 + c) : 0.0) * d) * __ldg(a.x + r * a.ldx + c);
+    }
+    a.out[r * a.ldo + c] = (a.scale ? __ldg(a.scale + c) : 1.0) * o;
+  }
+}
+
 size_t small_batched_smem(int B) {
   return (size_t)kWarps * ((32 * kSmallMax + 40) * sizeof(int) + 32 * B * sizeof(double));
 }
@@ -433,6 +453,17 @@ int spmv_vector_width(const SpmvArgs& a) {
 void spmv(const SpmvArgs& a0, cudaStream_t s) {
   if (a0.B < 1 || a0.B > kMaxCols) throw Error(1, "spmv: B out of range");
   SpmvArgs a = a0;
+  WL_LAUNCH("spmv_binned");
+  if (a.small_first >= 0 && a.n_iso > 0 && !a.accumulate) {  // isolated rows: a stream, off the row kernels
+    const int r0 = a.small_first + a.n_small - a.n_iso;
+    const int g = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)a.n_iso * a.B + kThreads - 1) / kThreads,
+                                                            (int64_t)num_sms() * 8));
+    spmv_iso_kernel<<<g, kThreads, 0, s>>>(a, r0);
+    WL_CUDA(cudaGetLastError());
+    a.n_small -= a.n_iso;
+    a.n_iso = 0;
+    if (a.n_small == 0) a.small_first = -1;
+  }
   // L2 eviction hints: rows [0, hot_rows) of the degree-sorted gathered block (the most gathered
   // rows) stay, column ids and cold rows go first.  Budget WL_SPMV_HOT_MB of L2 (0 = no hints).
   static const double hot_mb = [] { const char* v = getenv("WL_SPMV_HOT_MB"); return v ? atof(v) : 0.0; }();
@@ -453,7 +484,6 @@ void spmv(const SpmvArgs& a0, cudaStream_t s) {
     throw Error(8, "spmv: n_loc * ld and n_halo * ldh must be < 2^31 (32-bit gather offsets)");
   if (a.out_row && a.small_first >= 0) throw Error(1, "spmv: batched small rows cannot remap output rows");
   const bool halo = a.yh != nullptr;
-  WL_LAUNCH("spmv_binned");
   if (a.B == 1) {
     if (a.small_first >= 0 && a.n_small > 0) {  // thread per small row
       static const bool split = getenv("WL_SPMV_SPLIT") != nullptr;
