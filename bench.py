@@ -739,6 +739,12 @@ def run_trace(args):
     wl.profile_enable(False)
     kernels = {kk: {"ms_per_step": v[0], "launches_per_step": v[1], "share": v[0] / ms}
                for kk, v in sorted(wl.profile_collect().items(), key=lambda kv: -kv[1][0])}
+    # every batched Laplacian action of the curve ends in one combine launch: bytes = actions x one M-column action
+    nact = kernels.get("combine", {}).get("launches_per_step", 0)
+    ab = {kk: nact * v for kk, v in algorithmic_bytes(op.n_local, int(ci.shape[0]), op.n_halo, M, cfg["krylov_dim"],
+                                                       M, M, 1, reorth=op.reorth).items()}
+    peak, peak_src = peaks()
+    roof = roofline_of(kernels, ab, peak, peak_src)
     if rank == 0:
         line = {
             "metric": "XNysTrace-exp return-probability curves/s", "value": 1e3 / ms, "unit": "curves/s",
@@ -755,7 +761,7 @@ def run_trace(args):
                        "inner_minres_iterations": info.get("inner_iters"),
                        "column_actions_per_s": (None if rational else k * M / (ms / 1e3)),
                        "p_hat": [round(float(x), 6) for x in p[::10]], "e_hat": [float(x) for x in e[::10]]},
-            "roofline": None, "kernels": kernels, "cpu_baseline": None, "e2e": None, "gpu_launches": launches,
+            "roofline": roof, "kernels": kernels, "cpu_baseline": None, "e2e": None, "gpu_launches": launches,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -764,6 +770,23 @@ def run_trace(args):
         comm.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def roofline_of(kernels, ab, peak, peak_src):
+    """Attach algorithmic bytes / GB/s / fraction to the kernels with a byte count; the roofline object of the
+    dominant one (HBM bound)."""
+    for k, v in kernels.items():
+        if ab.get(k):
+            v["alg_bytes_per_step"] = ab[k]
+            v["achieved_gbs"] = ab[k] / (v["ms_per_step"] / 1e3) / 1e9
+            v["frac"] = v["achieved_gbs"] / peak
+    tops = [k for k in kernels if "alg_bytes_per_step" in kernels[k]]
+    if not tops:
+        return None
+    top = max(tops, key=lambda k: kernels[k]["ms_per_step"])
+    return {"kernel": top, "bound": "hbm", "achieved": kernels[top]["achieved_gbs"], "peak": peak, "unit": "GB/s",
+            "frac": kernels[top]["frac"], "peak_source": peak_src, "traffic": None,
+            "alg_bytes_per_launch": ab[top] / max(1, kernels[top]["launches_per_step"])}
 
 
 def run_extra(args):
@@ -806,12 +829,34 @@ def run_extra(args):
         ev1.record(stream)
         torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1) / args.steps
+    launches = wl.launch_count() - l0
+    wl.profile_enable(True)
+    fn()
+    torch.cuda.synchronize()
+    wl.profile_enable(False)
+    kernels = {k: {"ms_per_step": v[0], "launches_per_step": v[1], "share": v[0] / ms}
+               for k, v in sorted(wl.profile_collect().items(), key=lambda kv: -kv[1][0])}
+    # algorithmic bytes per step: Markov = nsteps B = 1 actions (k = 30 TOAR) + the chain's vector
+    # passes; ρ(Z) = 60 DCGS2 Arnoldi steps on 2n-vectors with one b = 1 SpMM each
+    n, nnz = g.n, g.nnz
+    if args.markov:
+        ab = {k: nsteps * v for k, v in algorithmic_bytes(n, nnz, 0, 1, 30, 1, 1, 1, reorth=2).items()}
+        ab["markov_vec"] = nsteps * (24 * n + 16 * n) + 16 * n
+    else:
+        L, ks = 2 * n, 60
+        ab = {"spmv_binned": ks * (4 * nnz + 4 * (n + 1) + 3 * 8 * n), "dcgs2_dots": 0, "dcgs2_update": 0}
+        for j in range(ks):
+            ab["dcgs2_dots"] += (j + 2) * 8 * L
+            ab["dcgs2_update"] += (j + 4) * 8 * L
+        ab["dcgs2_dots"] += (ks + 1) * 8 * L
+    peak, peak_src = peaks()
+    roof = roofline_of(kernels, ab, peak, peak_src)
     line = {"metric": what, "value": per_step / (ms / 1e3), "unit": unit, "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded graphgen)",
             "config": {"workload": f"{args.config}: {cfg['desc']}", "n": g.n, "nnz": g.nnz, "rho_A": rho,
                        "setup_s": {"generate": round(t_gen, 2)}},
-            "gpu_launches": wl.launch_count() - l0, "clocks": clk.summary()}
+            "roofline": roof, "kernels": kernels, "gpu_launches": launches, "clocks": clk.summary()}
     if not args.markov:
         line["config"]["rho_Z1"] = op.spectral_radius_z(0, k=60)
     print(json.dumps(line), flush=True)

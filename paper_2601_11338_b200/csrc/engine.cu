@@ -250,6 +250,7 @@ struct wl_workspace {
   int* cg_flags_host = nullptr;  // pinned: 2 flags + kMaxCols iteration counts
   int64_t cg_iterations = 0;     // executed CG iterations (max over the columns of each solve), cumulative
   int64_t krylov_steps = 0, krylov_batches = 0;  // Arnoldi steps taken / Krylov batches run (adaptive stop)
+  int k_last = 0;                                 // steps of the previous batch (first adaptive probe)
   DArr<int> kprobe;              // adaptive stop: probe dimensions per column + flag (4 ints)
   DArr<double> kcomb;            // adaptive stop: the probe's f_1(H_m)e_1 (discarded)
   int* kflag_host = nullptr;
@@ -640,7 +641,10 @@ void toar_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double*
     t.out_ld[1] = 0;
     xin = xg;
     zin = zb;
-    if (adaptive && j + 1 < K && j + 1 >= 6 && (j + 1) % 2 == 0) {
+    // first probe: 2 steps before the previous batch's stop (repeated actions — a diffusion sweep, CG-free
+    // trace steps — converge alike), never before k' = 6; then every 2 steps
+    const int kfirst = std::max(6, ws->k_last - 2);
+    if (adaptive && j + 1 < K && j + 1 >= kfirst && (j + 1 - kfirst) % 2 == 0) {
       int* kp = ws->kprobe.p;
       int* flag = kp + kMaxCols;
       clamp_keff(ws->keff.p, j, B, kp, flag, s);
@@ -659,8 +663,15 @@ void toar_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double*
       f.err = ws->kerr.p;
       small_f(f, s);
       krylov_check(ws->kerr.p, B, op->opts.tol, flag, s);
-      WL_CUDA(cudaMemcpyAsync(ws->kflag_host, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+      WL_CUDA(cudaMemcpyAsync(ws->kflag_host, flag, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
       WL_CUDA(cudaStreamSynchronize(s));
+      static const bool dbg = getenv("WL_DEBUG_ADAPTIVE") != nullptr;
+      if (dbg) {
+        double est;
+        std::memcpy(&est, ws->kflag_host + 2, sizeof(est));
+        fprintf(stderr, "[adaptive] step %d probe m=%d flag=%d max_est=%.3e (k_last %d)\n", j + 1, j, ws->kflag_host[0], est,
+                ws->k_last);
+      }
       if ((ws->kflag_host[0] & 1) == 0) {
         kstop = j + 1;
         break;
@@ -669,6 +680,7 @@ void toar_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double*
   }
   ws->krylov_steps += kstop;
   ws->krylov_batches += 1;
+  ws->k_last = kstop;
   d.nq = kstop + 1;  // Gram row of the last U vector completes H column kstop-1
   d.P = U.p[kstop + 1];
   d.wa = nullptr;

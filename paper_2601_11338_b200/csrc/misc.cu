@@ -337,7 +337,7 @@ namespace {
 __global__ void clamp_keff_kernel(const int* keff, int m, int B, int* out, int* flag) {
   const int c = threadIdx.x;
   if (c < B) out[c] = min(keff[c], m);
-  if (c == 0) flag[0] = 0;
+  if (c < 4) flag[c] = 0;
 }
 }  // namespace
 
