@@ -233,7 +233,21 @@ __global__ void __launch_bounds__(kThreads, VW == 1 ? 1 : WL_SPMV_MINB) spmv_bin
     return;
   }
   blk -= a.nblk_small;
-  if (blk < a.nblk_medium) {  // ---- medium rows: one warp per row
+  if (blk < a.nblk_medium) {  // ---- medium rows: one warp per row (one row per 8 lanes when a row is one lane wide)
+    if (W == 1 && a.med_sub) {
+      // 32/L rows per warp, L = med_sub lanes each: more rows (independent latency chains) in flight per warp,
+      // and the tail round of a ~100-300-nonzero row wastes L lanes instead of 32
+      const int L = a.med_sub;
+      const int idx = (blk * kWarps + warp) * (32 / L) + lane / L, lg = lane % L;
+      const int r = idx < a.n_medium ? a.medium_rows[idx] : 0;
+      const int z0 = idx < a.n_medium ? __ldg(a.rowptr + r) : 0, z1 = idx < a.n_medium ? __ldg(a.rowptr + r + 1) : 0;
+      Vec<VW> part = ctx.strided_sum(z0, z1, lg, L);
+#pragma unroll
+      for (int k = 0; k < VW; ++k)
+        for (int off = L / 2; off > 0; off >>= 1) part.v[k] += __shfl_xor_sync(0xffffffffu, part.v[k], off);
+      if (lg == 0 && idx < a.n_medium) ctx.write(r, z1 - z0, part);
+      return;
+    }
     const int idx = blk * kWarps + warp;
     if (idx >= a.n_medium) return;
     const int r = a.medium_rows[idx];
@@ -475,7 +489,11 @@ void spmv(const SpmvArgs& a0, cudaStream_t s) {
   const int W = (a.B + VW - 1) / VW;
   const int gpw = 32 / W;
   a.nblk_small = (a.n_small + kWarps * gpw - 1) / (kWarps * gpw);
-  a.nblk_medium = (a.n_medium + kWarps - 1) / kWarps;
+  // lanes per medium row when a row is one lane wide (b = 1): 0 = a warp per row
+  static const int med_sub = [] { const char* v = getenv("WL_SPMV_MEDSUB"); return v ? atoi(v) : 4; }();
+  a.med_sub = (W == 1 && (med_sub == 4 || med_sub == 8 || med_sub == 16)) ? med_sub : 0;
+  const int rows_per_warp = a.med_sub ? 32 / a.med_sub : 1;
+  a.nblk_medium = (a.n_medium + kWarps * rows_per_warp - 1) / (kWarps * rows_per_warp);
   const int nblk_hub = (a.n_chunks + kWarps - 1) / kWarps;
   const int grid = a.nblk_small + a.nblk_medium + nblk_hub;
   if (grid <= 0) return;

@@ -100,6 +100,7 @@ struct SpmvArgs {
   const int32_t* out_row;            // output row of CSR row i (null: i); not with the batched small rows
   int accumulate;                    // out += scale * Σ (no diagonal term): the A_halo part
   int hot_rows;                      // > 0: L2 evict_last hints for gathered rows < hot_rows (degree-sorted)
+  int med_sub;                       // filled by spmv(): lanes per medium row when a row is one lane wide (0: a warp)
   int B;
   const int* active;                 // optional (CG): the launch does nothing when *active == 0
 };
