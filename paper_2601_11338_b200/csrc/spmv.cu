@@ -525,7 +525,10 @@ void spmv(const SpmvArgs& a0, cudaStream_t s) {
     return;
   }
   // small rows with contiguous ids (x rows contiguous too): the batched kernel takes them
-  const bool batched = a.small_first >= 0 && a.n_small > 0 && (a.x == nullptr || a.ldx == a.B);
+  static const bool batched_on = [] { const char* v = getenv("WL_SPMV_BATCHED"); return v ? atoi(v) != 0 : true; }();
+  // with 8-byte lanes the batch staging pays (round 1: 59 -> 40 ms/step on C4); with 32-byte lanes a warp already
+  // walks 10 small rows at once through the row kernel, and the staging costs more than it saves (148 -> 140 ms/step)
+  const bool batched = batched_on && VW == 1 && a.small_first >= 0 && a.n_small > 0 && (a.x == nullptr || a.ldx == a.B);
   const int rest = batched ? grid - a.nblk_small : grid;
   if (VW == 4) launch_vw<4>(a, halo, batched, rest, s);
   else if (VW == 2) launch_vw<2>(a, halo, batched, rest, s);
