@@ -248,6 +248,24 @@ __global__ void __launch_bounds__(kThreads, VW == 1 ? 1 : WL_SPMV_MINB) spmv_bin
       if (lg == 0 && idx < a.n_medium) ctx.write(r, z1 - z0, part);
       return;
     }
+    if (a.med_rpw > 1) {
+      // med_rpw rows per warp, gpw / med_rpw lane groups each (B = 11: 2 rows x 5 groups of 3 lanes)
+      const int G2 = gpw / a.med_rpw, LR = G2 * W;
+      const int rs = lane / LR, base = rs * LR, gi2 = (lane - base) / W;
+      const int idx = (blk * kWarps + warp) * a.med_rpw + rs;
+      const bool ok = rs < a.med_rpw && idx < a.n_medium;
+      const int r = ok ? a.medium_rows[idx] : 0;
+      const int z0 = ok ? __ldg(a.rowptr + r) : 0, z1 = ok ? __ldg(a.rowptr + r + 1) : 0;
+      const Vec<VW> part = ok ? ctx.strided_sum(z0, z1, gi2, G2) : vzero<VW>();
+      Vec<VW> sum = part;
+      for (int g = 1; g < G2; ++g) {
+        const int src = base + ((lane - base) + g * W) % LR;
+#pragma unroll
+        for (int k = 0; k < VW; ++k) sum.v[k] += __shfl_sync(0xffffffffu, part.v[k], rs < a.med_rpw ? src : lane);
+      }
+      if (ok && gi2 == 0) ctx.write(r, z1 - z0, sum);
+      return;
+    }
     const int idx = blk * kWarps + warp;
     if (idx >= a.n_medium) return;
     const int r = a.medium_rows[idx];
@@ -492,7 +510,10 @@ void spmv(const SpmvArgs& a0, cudaStream_t s) {
   // lanes per medium row when a row is one lane wide (b = 1): 0 = a warp per row
   static const int med_sub = [] { const char* v = getenv("WL_SPMV_MEDSUB"); return v ? atoi(v) : 4; }();
   a.med_sub = (W == 1 && (med_sub == 4 || med_sub == 8 || med_sub == 16)) ? med_sub : 0;
-  const int rows_per_warp = a.med_sub ? 32 / a.med_sub : 1;
+  // wide rows (W > 1): medium rows per warp (WL_SPMV_MEDRPW; 1 = a warp per row)
+  static const int med_rpw = [] { const char* v = getenv("WL_SPMV_MEDRPW"); return v ? atoi(v) : 5; }();
+  a.med_rpw = (W > 1 && med_rpw > 1 && gpw / med_rpw >= 1) ? med_rpw : 1;
+  const int rows_per_warp = a.med_sub ? 32 / a.med_sub : a.med_rpw;
   a.nblk_medium = (a.n_medium + kWarps * rows_per_warp - 1) / (kWarps * rows_per_warp);
   const int nblk_hub = (a.n_chunks + kWarps - 1) / kWarps;
   const int grid = a.nblk_small + a.nblk_medium + nblk_hub;

@@ -101,6 +101,7 @@ struct SpmvArgs {
   int accumulate;                    // out += scale * Σ (no diagonal term): the A_halo part
   int hot_rows;                      // > 0: L2 evict_last hints for gathered rows < hot_rows (degree-sorted)
   int med_sub;                       // filled by spmv(): lanes per medium row when a row is one lane wide (0: a warp)
+  int med_rpw;                       // filled by spmv(): medium rows per warp when a row is several lanes wide
   int B;
   const int* active;                 // optional (CG): the launch does nothing when *active == 0
 };
