@@ -70,7 +70,7 @@ constexpr int kMaxSmallN = 130; // largest dense matrix of the projected-functio
 #define WL_SMALL_MAX 32
 #endif
 #ifndef WL_HUB_CHUNK
-#define WL_HUB_CHUNK 2048
+#define WL_HUB_CHUNK 4096
 #endif
 #ifndef WL_MEDIUM_MAX
 #define WL_MEDIUM_MAX WL_HUB_CHUNK

@@ -460,12 +460,13 @@ def test_aposteriori_krylov_check(wl):
 
 
 def test_hub_rows_split_into_chunks(wl):
-    """Rows longer than the hub chunk (2048 nonzeros) are split across warps and reduced in chunk order by
-    the last chunk to finish; several hubs of different lengths plus medium and small rows, vs the series."""
+    """Rows longer than the hub chunk (4096 nonzeros) are split across warps and reduced in chunk order by
+    the last chunk to finish; several hubs of different lengths (1 to 3 chunks, and the boundary lengths) plus
+    medium and small rows, vs the series."""
     rng = np.random.default_rng(5)
-    n = 9000
+    n = 20000
     edges = set()
-    for hub, deg in ((0, 5000), (1, 2049), (2, 4097), (3, 2048), (4, 700)):
+    for hub, deg in ((0, 10000), (1, 4097), (2, 8193), (3, 4096), (4, 700), (5, 2049), (6, 12289)):
         for v in rng.choice(np.arange(5, n), size=deg, replace=False):
             edges.add((min(hub, int(v)), max(hub, int(v))))
     for _ in range(20000):
@@ -473,7 +474,7 @@ def test_hub_rows_split_into_chunks(wl):
         if a != b:
             edges.add((min(a, b), max(a, b)))
     g = gg.from_edges(n, sorted(edges), "hubs")
-    assert np.diff(g.row_ptr).max() >= 5000
+    assert np.diff(g.row_ptr).max() >= 12289
     rA = S.rho_A(g)
     f = C.exp(1.0 / rA)
     V = gg.vectors(g.n, 3, 8)
@@ -547,12 +548,12 @@ def test_bitwise_reproducible_race_probe(wl):
     """compute-sanitizer is closed on this GPU pool (profiles/r02_compute_sanitizer_closed.log), so races are
     probed by determinism: every reduction on the path is fixed-order by design (per-CTA partials summed in CTA
     order, the hub-row chunks summed in chunk order by the last arriver, the mbarrier rings consumed in stage
-    order), so repeated actions must agree BIT FOR BIT.  A hub with 3000 neighbours (two 2048-nonzero chunks and
+    order), so repeated actions must agree BIT FOR BIT.  A hub with 9000 neighbours (three 4096-nonzero chunks and
     a ticket), 11 θ columns (32-byte lane gathers over the padded block), TOAR and DCGS2 rings, CG, diffusion."""
     r = gg.rmat(10, 900, 4000, seed=3, perm_seed=4)
     edges = [(int(i), int(j)) for i in range(r.n) for j in r.col_idx[r.row_ptr[i]:r.row_ptr[i + 1]] if i < j]
-    n = r.n + 3001
-    edges += [(r.n, r.n + 1 + k) for k in range(3000)] + [(0, r.n)]
+    n = r.n + 9001
+    edges += [(r.n, r.n + 1 + k) for k in range(9000)] + [(0, r.n)]
     g = gg.from_edges(n, edges)
     rA = S.rho_A(g)
     V = torch.from_numpy(gg.vectors(n, 1, 5)).cuda()

@@ -1,6 +1,6 @@
 """Small run through every kernel family for compute-sanitizer (racecheck / synccheck / memcheck):
 the bulk-copy ring passes (TOAR dots/update, DCGS2 dots/update), the hub-row chunk tickets of the SpMM
-(a star with a 3000-neighbour hub: two 2048-nonzero chunks), the batched small rows, the 32-byte lane
+(a 9000-neighbour hub: three 4096-nonzero chunks), the batched small rows, the 32-byte lane
 gathers (B = 11 over a padded block), CG, the outer diffusion Arnoldi, and the loopback halo exchange.
 Checks the results against the oracle so a silent corruption also fails.
     compute-sanitizer --tool racecheck python tools/sanitize_case.py"""
@@ -27,8 +27,8 @@ def main():
     # a hub of 3000 leaves (2 chunks of 2048 nonzeros) attached to a small R-MAT
     r = gg.rmat(10, 900, 4000, seed=3, perm_seed=4)
     edges = [(int(i), int(j)) for i in range(r.n) for j in r.col_idx[r.row_ptr[i]:r.row_ptr[i + 1]] if i < j]
-    n = r.n + 3001
-    edges += [(r.n, r.n + 1 + k) for k in range(3000)] + [(0, r.n)]
+    n = r.n + 9001
+    edges += [(r.n, r.n + 1 + k) for k in range(9000)] + [(0, r.n)]
     g = gg.from_edges(n, edges)
     rA = S.rho_A(g)
     f = C.exp(1.0 / rA)
