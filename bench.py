@@ -692,8 +692,9 @@ def run_trace(args):
     rho = probe.spectral_radius(k=args.rho_k)
     probe.close()
     op = wl.Operator(g.n, rp, ci, thetas=cfg["thetas"][:1], f=("exp", 1.0 / rho), row_range=(rb, re), comm=comm,
-                     relabel=args.relabel,
-                     krylov_dim=cfg["krylov_dim"])
+                     relabel=args.relabel, krylov_dim=cfg["krylov_dim"],
+                     krylov_tol=args.adaptive if args.adaptive > 0 else 0.0,
+                     krylov_adaptive=1 if args.adaptive > 0 else 0)
     M, k = args.trace_m, args.trace_k
     rational = args.trace_poles == "aaa"
     # Fig. 7: [0, t*] = [0, 100], 90 points, AAA poles, inner solves at 1e-6; the polynomial
@@ -740,8 +741,11 @@ def run_trace(args):
     kernels = {kk: {"ms_per_step": v[0], "launches_per_step": v[1], "share": v[0] / ms}
                for kk, v in sorted(wl.profile_collect().items(), key=lambda kv: -kv[1][0])}
     # every batched Laplacian action of the curve ends in one combine launch: bytes = actions x one M-column action
+    # of the Arnoldi steps actually taken (k' under --adaptive)
     nact = kernels.get("combine", {}).get("launches_per_step", 0)
-    ab = {kk: nact * v for kk, v in algorithmic_bytes(op.n_local, int(ci.shape[0]), op.n_halo, M, cfg["krylov_dim"],
+    _, ks, kb = ws.stats()
+    k_act = int(round(ks / kb)) if (args.adaptive > 0 and kb) else cfg["krylov_dim"]
+    ab = {kk: nact * v for kk, v in algorithmic_bytes(op.n_local, int(ci.shape[0]), op.n_halo, M, k_act,
                                                        M, M, 1, reorth=op.reorth).items()}
     peak, peak_src = peaks()
     roof = roofline_of(kernels, ab, peak, peak_src)
@@ -755,10 +759,12 @@ def run_trace(args):
                                     f"MINRES inner solves to {args.trace_inner_tol:g}, M={M} probes, 90 t in [0,100]"
                                     if rational else
                                     f"{cfg['desc']}; Alg. 1 (poles at inf), M={M} probes, k={k} blocks, 90 t in [0,10]")
-                                   + f", theta={cfg['thetas'][0]}, inner Krylov k={cfg['krylov_dim']}",
+                                   + f", theta={cfg['thetas'][0]}, inner Krylov k={cfg['krylov_dim']}"
+                                   + (f" (adaptive, tol {args.adaptive:g})" if args.adaptive > 0 else ""),
                        "n": g.n, "nnz": g.nnz,
                        "poles": [[float(z.real), float(z.imag)] for z in info.get("poles", [])],
                        "inner_minres_iterations": info.get("inner_iters"),
+                       "inner_krylov_steps": k_act,
                        "column_actions_per_s": (None if rational else k * M / (ms / 1e3)),
                        "p_hat": [round(float(x), 6) for x in p[::10]], "e_hat": [float(x) for x in e[::10]]},
             "roofline": roof, "kernels": kernels, "cpu_baseline": None, "e2e": None, "gpu_launches": launches,
