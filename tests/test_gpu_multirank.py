@@ -209,3 +209,52 @@ def test_loopback_empty_rank(wl):
     X1 = op1.diffuse(torch.from_numpy(np.ascontiguousarray(V[:, 0])).cuda(), ts, k_out=40).cpu().numpy()
     op1.close()
     assert relerr(X, X1).max() < 1e-12
+
+
+def test_loopback_lanczos_adaptive_and_rational_trace(wl):
+    """The round-2 paths across ranks: the μ = 0 Lanczos batches (per-column scalars allreduced), the adaptive
+    Krylov stop (every rank takes the same decision from the replicated H), and the rational XNysTrace-exp (MINRES
+    scalars allreduced, the Cholesky-QR and Rayleigh-quotient Gram blocks allreduced) — each against P = 1."""
+    g = gg.barabasi_albert(3000, 4, 2)
+    rA = S.rho_A(g)
+    f = C.exp(1.0 / rA)
+    V = gg.vectors(g.n, 2, 4)
+    Om = gg.vectors(g.n, 4, 9)
+    ts = np.linspace(0.0, 5.0, 7)
+    poles = np.array([np.inf, -2.5, -1.0 + 3.0j])
+    kw_walk = dict(variant="walk", f=("exp", f.param))
+    kw_ad = dict(thetas=[0.0, 0.5], f=("exp", f.param), krylov_tol=1e-13, krylov_adaptive=1)
+
+    def one_rank():
+        o = wl.Operator(g.n, g.row_ptr, g.col_idx, **kw_walk)
+        a = o.apply(torch.from_numpy(V).cuda()).cpu().numpy()
+        o.close()
+        o = wl.Operator(g.n, g.row_ptr, g.col_idx, **kw_ad)
+        b = o.apply(torch.from_numpy(V).cuda()).cpu().numpy()
+        p, e, _ = o.xnystrace_exp_rational(torch.from_numpy(Om).cuda(), ts, poles=poles, inner_tol=1e-13)
+        o.close()
+        return a, b, p
+
+    a1, b1, p1 = one_rank()
+    bounds = wl.partition(g.row_ptr, 3)
+
+    def rank_fn(r, comm, stream):
+        rb, re = int(bounds[r]), int(bounds[r + 1])
+        rp = g.row_ptr[rb:re + 1]
+        ci = g.col_idx[rp[0]:rp[-1]]
+        o = wl.Operator(g.n, rp, ci, row_range=(rb, re), comm=comm, stream=stream, **kw_walk)
+        a = o.apply(torch.from_numpy(V[rb:re].copy()).cuda(), stream=stream).cpu().numpy()
+        o.close()
+        o = wl.Operator(g.n, rp, ci, row_range=(rb, re), comm=comm, stream=stream, **kw_ad)
+        b = o.apply(torch.from_numpy(V[rb:re].copy()).cuda(), stream=stream).cpu().numpy()
+        p, e, _ = o.xnystrace_exp_rational(torch.from_numpy(Om[rb:re].copy()).cuda(), ts, poles=poles,
+                                           inner_tol=1e-13, stream=stream)
+        o.close()
+        return a, b, p
+
+    res = wl.run_loopback(3, rank_fn, timeout=300.0)
+    assert relerr(np.vstack([r[0] for r in res]), a1).max() < TOL_P1
+    assert relerr(np.vstack([r[1] for r in res]), b1).max() < TOL_P1
+    for r in res:
+        assert np.max(np.abs(r[2] - p1) / np.abs(p1)) < 1e-11
+    assert relerr(a1, S.laplacian_apply(g, 0.0, f, V, rA)).max() < TOL
