@@ -237,15 +237,17 @@ def run_walklap(args):
             spmv_b1["class_ms_per_launch"] = cls
     probe.close()
     beta = 1.0 / rho
-    thetas = cfg["thetas"]
+    # --walk: the all-walk operator (θ = 1) on b = 11 input columns, the same B = 11 batch as the θ sweep:
+    # Lanczos on A (opts.lanczos, default) against TOAR on Z (--lanczos 0) — the Gram bytes μ = 0 saves
+    thetas = [1.0] if args.walk else cfg["thetas"]
     K = args.krylov if args.krylov else cfg["krylov_dim"]
     op = wl.Operator(g.n, rp, ci, thetas=thetas, f=("exp", beta), row_range=(rb, re), comm=comm, krylov_dim=K,
                      relabel=args.relabel, max_cols=args.max_cols,
                      krylov_tol=args.adaptive if args.adaptive > 0 else 0.0,
-                     krylov_adaptive=1 if args.adaptive > 0 else 0)
+                     krylov_adaptive=1 if args.adaptive > 0 else 0, lanczos=args.lanczos)
     torch.cuda.synchronize()
     t_create = time.time() - t0
-    b = args.b if args.b else cfg["b"]
+    b = args.b if args.b else (11 if args.walk else cfg["b"])
     n_loc = op.n_local
     Vfull = gg.vectors(g.n, b, cfg["vec_seed"] or 103)
     V = torch.from_numpy(np.ascontiguousarray(Vfull[rb:re])).cuda()
@@ -331,6 +333,11 @@ def run_walklap(args):
     nnz_loc = int(ci.shape[0])
     Kab = int(round(k_mean)) if args.adaptive > 0 else K  # the steps actually taken
     ab = algorithmic_bytes(n_loc, nnz_loc, op.n_halo, G, Kab, ws_bmax(op, b), b, op.n_theta, reorth=op.reorth)
+    if args.walk and args.lanczos:  # Lanczos batches (R19): K + 1 SpMMs (no diagonal term), 8 n-blocks per step
+        blk = 8 * n_loc * G
+        csr = 4 * nnz_loc + 4 * (n_loc + 1)
+        ab = {"spmv_binned": (Kab + 1) * (csr + 2 * blk + 8 * op.n_halo * G), "lanczos_vec": Kab * 8 * blk + 3 * blk,
+              "combine": Kab * blk + blk + 8 * n_loc * b + 8 * n_loc, "batch_inputs": 8 * n_loc * b + blk}
     kernels = {}
     for name, (tot_ms, cnt) in prof.items():
         per_step_ms = tot_ms / args.steps
@@ -909,6 +916,8 @@ def main():
     ap.add_argument("--krylov", type=int, default=0)
     ap.add_argument("--rho-k", type=int, default=60)
     ap.add_argument("--max-cols", type=int, default=32, help="columns per internal Krylov batch (opts.max_cols)")
+    ap.add_argument("--walk", action="store_true", help="theta = 1 only, b = 11 columns (the mu = 0 Lanczos path)")
+    ap.add_argument("--lanczos", type=int, default=1, choices=[0, 1], help="opts.lanczos (theta = 1 batches)")
     ap.add_argument("--adaptive", type=float, default=0.0,
                     help="> 0: stop each Arnoldi process once the a-posteriori estimate is below this (opts.krylov_adaptive)")
     ap.add_argument("--no-e2e", action="store_true")

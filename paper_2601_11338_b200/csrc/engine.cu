@@ -741,19 +741,22 @@ void lanczos_chunk(const wl_operator* op, wl_workspace* ws, int mode, const doub
   };
   WL_CUDA(cudaMemsetAsync(ws->H.p, 0, sizeof(double) * B * (K + 1) * K, s));
   double* q0 = const_cast<double*>(Q.p[0]);
+  // the SpMM gathers q_j from a row-padded copy (32-byte lanes, §7) written by the scaling pass
+  double* xg = ws->xg.p && pad_cols(B) != B ? ws->xg.p : nullptr;
+  const int64_t ldg = xg ? pad_cols(B) : B;
   do_spmv(op, ws, ws->Vb.p, B, nullptr, nullptr, nullptr, nullptr, q0, B, s);  // u = A v  (a3 seed, μ = 0)
   lanczos_vec(0, q0, nullptr, nullptr, n, B, sc, ws->partials.p, s);
   scalar(0, 0);
-  lanczos_vec(3, q0, nullptr, nullptr, n, B, sc, ws->partials.p, s);            // q_0 = u / ‖u‖
+  lanczos_vec(3, q0, nullptr, nullptr, n, B, sc, ws->partials.p, s, xg, ldg);   // q_0 = u / ‖u‖
   for (int j = 0; j < K; ++j) {
     double* qj = const_cast<double*>(Q.p[j]);
     double* w = const_cast<double*>(Q.p[j + 1]);
-    do_spmv(op, ws, qj, B, nullptr, nullptr, nullptr, nullptr, w, B, s);       // a4 at μ = 0: w' = A q_j
+    do_spmv(op, ws, xg ? xg : qj, ldg, nullptr, nullptr, nullptr, nullptr, w, B, s);  // a4 at μ = 0: w' = A q_j
     lanczos_vec(1, qj, w, nullptr, n, B, sc, ws->partials.p, s);
     scalar(1, j);                                                                 // α_j
     lanczos_vec(2, w, qj, j > 0 ? Q.p[j - 1] : nullptr, n, B, sc, ws->partials.p, s);
     scalar(2, j);                                                                 // β_{j+1}
-    lanczos_vec(3, w, nullptr, nullptr, n, B, sc, ws->partials.p, s);            // q_{j+1}
+    lanczos_vec(3, w, nullptr, nullptr, n, B, sc, ws->partials.p, s, xg, ldg);   // q_{j+1}
   }
   SmallFArgs f{};
   f.H = ws->H.p;

@@ -71,12 +71,19 @@ __global__ void __launch_bounds__(kThreads) lz_update_kernel(double* w, const do
   lz_partials(v, B, L.tpb, partials);
 }
 
-// x *= 1/β per column (sc slot 2)
-__global__ void __launch_bounds__(kThreads) lz_scale_kernel(double* x, int64_t n, int B, const double* sc) {
+// x *= 1/β per column (sc slot 2); with xp, also the row-padded copy the SpMM gathers (ld ldp, 32-byte rows)
+__global__ void __launch_bounds__(kThreads) lz_scale_kernel(double* x, int64_t n, int B, const double* sc, double* xp,
+                                                            int64_t ldp) {
   const LzLane L(B);
   if (!L.act) return;
   const double s = sc[L.c * 4 + 2];
-  for (int64_t e = L.e0; e < n * B; e += L.stride) x[e] *= s;
+  const int64_t dr = L.stride / B;  // the stride is a multiple of B: rows advance without a division
+  int64_t r = L.e0 / B;
+  for (int64_t e = L.e0; e < n * B; e += L.stride, r += dr) {
+    const double v = x[e] * s;
+    x[e] = v;
+    if (xp) xp[r * ldp + L.c] = v;
+  }
 }
 
 // One CTA: reduce the per-CTA partial rows (unless presummed), then per column
@@ -150,12 +157,12 @@ int lz_grid(int64_t n, int B) {
 int lanczos_grid(int64_t n, int B) { return lz_grid(n, B); }
 
 void lanczos_vec(int phase, double* x, const double* y, const double* qm, int64_t n, int B, const double* sc,
-                 double* partials, cudaStream_t s) {
+                 double* partials, cudaStream_t s, double* xp, int64_t ldp) {
   WL_LAUNCH("lanczos_vec");
   const int G = lz_grid(n, B);
   if (phase <= 1) lz_dot_kernel<<<G, kThreads, 0, s>>>(phase, x, y, n, B, partials);
   else if (phase == 2) lz_update_kernel<<<G, kThreads, 0, s>>>(x, y, qm, n, B, sc, partials);
-  else lz_scale_kernel<<<G, kThreads, 0, s>>>(x, n, B, sc);
+  else lz_scale_kernel<<<G, kThreads, 0, s>>>(x, n, B, sc, xp, ldp);
   WL_CUDA(cudaGetLastError());
 }
 
