@@ -359,7 +359,11 @@ def run_walklap(args):
         roof["traffic_gbs"] = ncu[top] / (ms_launch / 1e3) / 1e9
         roof["traffic_frac"] = roof["traffic_gbs"] / peak
         roof["gathers_per_s"] = nnz_loc / (ms_launch / 1e3)
-        roof["uniform_random_gather_ceiling_per_s"] = 3.3e10  # tools/gather_bench.cu, 88-byte rows, no reuse
+        if args.config == "c4" and G == 11:
+            # tools/gather_ceiling.cu: 4e8 gathers of 11-column rows (32-byte lanes, ld 12) drawn from the C4
+            # degree distribution take 3.02 ms on this B200 — the gather-only ceiling of this SpMM
+            roof["gather_ceiling_ms"] = 3.02
+            roof["frac_of_gather_ceiling"] = 3.02 / ms_launch
     spmv = kernels.get("spmv_binned", {})
 
     cpu = None
