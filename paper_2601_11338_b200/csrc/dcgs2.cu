@@ -365,8 +365,15 @@ __global__ void __launch_bounds__(kUpdConsumers + 32, 1) toar_update_ring(ToarAr
         if (t + i * tpb < cnt) {
 #pragma unroll
           for (int o = 0; o < NOUT; ++o) {
-            if (a.out_ld[o] > B) a.out[o][(r0 + (int64_t)i * (tpb / B)) * a.out_ld[o] + c] = acc[o][i];
-            else a.out[o][e0 + t + i * tpb] = acc[o][i];
+            if (a.out_ld[o] > B) {
+              double* row = a.out[o] + (r0 + (int64_t)i * (tpb / B)) * a.out_ld[o];
+              row[c] = acc[o][i];
+              // the phantom columns too: whole 32-byte sectors reach L2, so DRAM sees no partial-sector writes
+              if (c == B - 1)
+                for (int cc = B; cc < a.out_ld[o]; ++cc) row[cc] = 0.0;
+            } else {
+              a.out[o][e0 + t + i * tpb] = acc[o][i];
+            }
           }
         }
     }

@@ -82,7 +82,11 @@ __global__ void __launch_bounds__(kThreads) lz_scale_kernel(double* x, int64_t n
   for (int64_t e = L.e0; e < n * B; e += L.stride, r += dr) {
     const double v = x[e] * s;
     x[e] = v;
-    if (xp) xp[r * ldp + L.c] = v;
+    if (xp) {
+      xp[r * ldp + L.c] = v;
+      if (L.c == B - 1)  // phantom columns: whole 32-byte sectors (no partial-sector writes in DRAM)
+        for (int cc = B; cc < ldp; ++cc) xp[r * ldp + cc] = 0.0;
+    }
   }
 }
 
