@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(kUpdConsumers + 32, 1) toar_update_ring(ToarAr
               row[c] = acc[o][i];
               // the phantom columns too: whole 32-byte sectors reach L2, so DRAM sees no partial-sector writes
               if (c == B - 1)
-                for (int cc = B; cc < a.out_ld[o]; ++cc) row[cc] = 0.0;
+                for (int cc = B; cc < pad_vec(B); ++cc) row[cc] = 0.0;
             } else {
               a.out[o][e0 + t + i * tpb] = acc[o][i];
             }

@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(kThreads) lz_scale_kernel(double* x, int64_t n
     if (xp) {
       xp[r * ldp + L.c] = v;
       if (L.c == B - 1)  // phantom columns: whole 32-byte sectors (no partial-sector writes in DRAM)
-        for (int cc = B; cc < ldp; ++cc) xp[r * ldp + cc] = 0.0;
+        for (int cc = B; cc < pad_vec(B); ++cc) xp[r * ldp + cc] = 0.0;
     }
   }
 }

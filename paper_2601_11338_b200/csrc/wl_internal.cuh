@@ -56,8 +56,17 @@ wl_status guarded(F&& f) {
 }
 
 int num_sms();  // SMs of the current device (cached per device)
-// row width of a gathered block of B columns: whole 32-byte pieces for B > 1 (spmv.cu 256-bit lanes)
-inline int pad_cols(int B) { return B <= 1 ? B : (B + 3) / 4 * 4; }
+// Gathered blocks of B > 1 columns (spmv.cu 256-bit lanes): a lane loads 32 bytes, so the loaded part of a row is
+// pad_vec(B) = 4⌈B/4⌉ doubles; the row STRIDE pad_cols(B) is the next power of two (4, 8, 16, 32 doubles), so no
+// row straddles a 128-byte line (B = 11: 3 sectors at a 128-byte stride — one L1 wavefront per gathered row
+// instead of 1.5 at a 96-byte stride).  Columns in [B, pad_vec(B)) are zero; beyond are never read.
+__host__ __device__ inline int pad_vec(int B) { return B <= 1 ? B : (B + 3) / 4 * 4; }
+__host__ __device__ inline int pad_cols(int B) {
+  if (B <= 1) return B;
+  int p = 4;
+  while (p < B) p *= 2;
+  return p;
+}
 
 constexpr int kMaxCols = 32;    // columns per Krylov batch (B)
 constexpr int kMaxKrylov = 64;  // Arnoldi steps per action
