@@ -157,8 +157,9 @@ def load_graph(cfg, world, rank, torch, dist):
     return g, time.time() - t0
 
 
-def algorithmic_bytes(n, nnz, n_halo, G, K, Bmax, b, n_theta, reorth=2):
-    """Bytes each kernel must move per step, by kernel name."""
+def algorithmic_bytes(n, nnz, n_halo, G, K, Bmax, b, n_theta, reorth=2, esz=8):
+    """Bytes each kernel must move per step, by kernel name.  esz: bytes per stored element of
+    the TOAR batch's n-vectors (8; 4 in the fp32 mode, where the seeds, inputs and outputs stay double)."""
     out = {}
     def add(k, v):
         out[k] = out.get(k, 0) + v
@@ -166,16 +167,17 @@ def algorithmic_bytes(n, nnz, n_halo, G, K, Bmax, b, n_theta, reorth=2):
         B = min(Bmax, G - g0)
         L = 2 * n
         vec = 8 * L * B
-        blk = 8 * n * B
+        blk8 = 8 * n * B                 # a double n x B block (inputs, outputs, seeds)
+        blk = esz * n * B                # a stored n x B block of the batch
         csr = 4 * nnz + 4 * (n + 1)
         if reorth == 2 and b < B and g0 % b == 0 and B % b == 0:
             bb = 8 * n * b                                              # θ-independent seeds over b columns
             add("spmv_binned", 2 * (csr + 2 * bb + 8 * n_halo * b))    # A v, A(Av)
             add("batch_inputs", 3 * bb + 2 * blk)                      # expand to the B columns
         else:
-            add("spmv_binned", (csr + 2 * blk + 8 * n_halo * B))      # seed 1: gather y + write
-            add("spmv_binned", (csr + 3 * blk + 8 * n_halo * B))      # seed 2: + x
-        add("spmv_binned", K * (csr + 3 * blk + 8 * n_halo * B))      # Z steps
+            add("spmv_binned", (csr + 2 * blk8 + 8 * n_halo * B))     # seed 1: gather y + write
+            add("spmv_binned", (csr + 3 * blk8 + 8 * n_halo * B))     # seed 2: + x
+        add("spmv_binned", K * (csr + 3 * blk + esz * n_halo * B))    # Z steps
         if reorth == 2:
             # TOAR: n-vector basis U (m = j+2 vectors at step j).  dots: Gram row of the newest U
             # vector + U^T y + |y|^2; update: u_m, x_{j+1}, z_{j+1} from y and U
@@ -185,7 +187,7 @@ def algorithmic_bytes(n, nnz, n_halo, G, K, Bmax, b, n_theta, reorth=2):
                 add("dcgs2_dots", (j + 3) * blk)
                 add("toar_update", (j + 6) * blk)
             add("dcgs2_dots", (K + 2) * blk)                           # final Gram row
-            add("combine", (K + 2) * blk + blk + 8 * n * b + 8 * n * n_theta)
+            add("combine", (K + 2) * blk + blk8 + 8 * n * b + 8 * n * n_theta)
         else:
             # DCGS2 step j: dots read q_0..q_{j-1}, p_j and the SpMM output (w's top half IS p_j's
             # bottom half, read once); update reads the same and writes q_j and p_{j+1}
@@ -194,7 +196,7 @@ def algorithmic_bytes(n, nnz, n_halo, G, K, Bmax, b, n_theta, reorth=2):
                 add("dcgs2_update", (j + 3.5) * vec)
             add("dcgs2_dots", (K + 1) * vec)                          # final delayed reorth.
             add("combine", K * blk + blk + 8 * n * b + 8 * n * n_theta)
-        add("batch_inputs", 8 * n * b + blk)
+        add("batch_inputs", 8 * n * b + blk8)
     return out
 
 
@@ -244,7 +246,7 @@ def run_walklap(args):
     op = wl.Operator(g.n, rp, ci, thetas=thetas, f=("exp", beta), row_range=(rb, re), comm=comm, krylov_dim=K,
                      relabel=args.relabel, max_cols=args.max_cols,
                      krylov_tol=args.adaptive if args.adaptive > 0 else 0.0,
-                     krylov_adaptive=1 if args.adaptive > 0 else 0, lanczos=args.lanczos)
+                     krylov_adaptive=1 if args.adaptive > 0 else 0, lanczos=args.lanczos, fp32=args.fp32)
     torch.cuda.synchronize()
     t_create = time.time() - t0
     b = args.b if args.b else (11 if args.walk else cfg["b"])
@@ -332,7 +334,8 @@ def run_walklap(args):
     peak, peak_src = peaks()
     nnz_loc = int(ci.shape[0])
     Kab = int(round(k_mean)) if args.adaptive > 0 else K  # the steps actually taken
-    ab = algorithmic_bytes(n_loc, nnz_loc, op.n_halo, G, Kab, ws_bmax(op, b), b, op.n_theta, reorth=op.reorth)
+    ab = algorithmic_bytes(n_loc, nnz_loc, op.n_halo, G, Kab, ws_bmax(op, b), b, op.n_theta, reorth=op.reorth,
+                           esz=4 if args.fp32 else 8)
     if args.walk and args.lanczos:  # Lanczos batches (R19): K + 1 SpMMs (no diagonal term), 8 n-blocks per step
         blk = 8 * n_loc * G
         csr = 4 * nnz_loc + 4 * (n_loc + 1)
@@ -359,7 +362,7 @@ def run_walklap(args):
         roof["traffic_gbs"] = ncu[top] / (ms_launch / 1e3) / 1e9
         roof["traffic_frac"] = roof["traffic_gbs"] / peak
         roof["gathers_per_s"] = nnz_loc / (ms_launch / 1e3)
-        if args.config == "c4" and G == 11:
+        if args.config == "c4" and G == 11 and not args.fp32:
             # tools/gather_ceiling.cu: 4e8 gathers of 11-column rows (32-byte lanes, ld 12) drawn from the C4
             # degree distribution take 3.02 ms on this B200 — the gather-only ceiling of this SpMM
             roof["gather_ceiling_ms"] = 3.02
@@ -375,7 +378,8 @@ def run_walklap(args):
         line = {
             "metric": METRIC, "value": value, "unit": "actions/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded R-MAT, graphgen)",
+            "vs_baseline": None, "dtype": "f32-storage/f64-accumulate" if args.fp32 else "f64",
+            "data": "synthetic (seeded R-MAT, graphgen)",
             "config": {"workload": f"{args.config}: {cfg['desc']}", "n": g.n, "nnz": g.nnz,
                        "thetas": thetas, "b": b, "actions_per_step": actions, "krylov_dim": K,
                        "krylov_adaptive": ({"tol": args.adaptive, "mean_steps": k_mean} if args.adaptive > 0 else None),
@@ -924,6 +928,8 @@ def main():
     ap.add_argument("--lanczos", type=int, default=1, choices=[0, 1], help="opts.lanczos (theta = 1 batches)")
     ap.add_argument("--adaptive", type=float, default=0.0,
                     help="> 0: stop each Arnoldi process once the a-posteriori estimate is below this (opts.krylov_adaptive)")
+    ap.add_argument("--fp32", type=int, default=0, choices=[0, 1],
+                    help="opts.fp32: float storage of the Krylov batches, double sums (parity 1e-4)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--graph", action="store_true", help="also time the step captured as one CUDA graph")

@@ -117,6 +117,12 @@ typedef struct {
                            `tol` is below tol for every column of the batch (reading R11); krylov_dim is
                            then the cap.  Each check synchronizes the stream (not CUDA-graph capturable).
                            0 (default): always krylov_dim steps */
+  int32_t fp32;         /* 1 (reorth = 2, Krylov solver): the fp32 mode of the north star (parity 1e-4): the
+                           n-vectors of each TOAR batch — the basis U, the SpMM operand and output — are
+                           stored in float, halving the bytes of the Gram passes and of the SpMM gathers;
+                           every sum (SpMM rows, dot products, basis updates, combine) and all projected
+                           work stay double, inputs and results are double, and t (create) is computed
+                           in double.  θ = 1 batches then run TOAR (no Lanczos).  0 (default): double */
 } wl_opts;
 
 typedef enum { WL_SOLVER_KRYLOV = 0, WL_SOLVER_CG = 1 } wl_solver;

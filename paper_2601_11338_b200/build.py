@@ -68,8 +68,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             raise subprocess.CalledProcessError(max(rcs), "nvcc -c")
         tmp = LIB + f".{tag}"
         cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", *objs, "-o", tmp,
-               "-L", libdir, "-l:libnccl.so.2", "-Xlinker", f"-rpath={libdir}", "-L/usr/local/cuda/lib64",
-               "-lcublas", "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
+               "-L", libdir, "-l:libnccl.so.2", "-Xlinker", f"-rpath={libdir}"]
         subprocess.check_call(cmd)
         os.replace(tmp, LIB)
     finally:

@@ -25,6 +25,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 namespace wl {
 namespace {
@@ -35,9 +36,46 @@ constexpr int kMaxVecPerLaunch = 32;  // longer bases are tiled by the launchers
 // pass B 512 consumers x 4 elements.
 constexpr int kDotsConsumers = 128, kDotsPer = 16;
 static_assert(kDotsConsumers * kDotsPer <= 2048, "dots: unpredicated basis loads stay inside one ring stage");
+constexpr int kStageElems = 2048;  // double stages (the DCGS2 2n-vector passes)
 constexpr int kUpdConsumers = 512, kUpdPer = 4;
+// A stage is 16 KB: 2048 doubles, or 4096 floats (opts.fp32 storage), whose consumers own twice the elements per
+// thread (PER<T>) — same copies, barriers and bytes in flight (192 KB per SM) per byte for either type.
 constexpr int kStages = 12;
-constexpr int kStageElems = 2048;  // 16 KB
+constexpr int kRingBytes = kStages * 16384;  // 192 KB per SM
+constexpr int kMaxStages = 24;
+// a ring of SE-element stages of T: as many as fit kRingBytes (the dots pass keeps 2048-element stages, so float
+// storage runs 24 stages of 8 KB; the float update 12 of 16 KB)
+template <class T, int SE>
+__host__ __device__ constexpr int ring_stages() { return kRingBytes / (SE * (int)sizeof(T)); }
+template <class T>
+__host__ __device__ constexpr int stage_elems() { return 16384 / (int)sizeof(T); }
+// float storage tunables (tools/build_variants.sh): elements per dots thread; update consumers and elements
+#ifndef WL_DOTS_F_PER
+#define WL_DOTS_F_PER 16
+#endif
+#ifndef WL_UPD_F_CONSUMERS
+#define WL_UPD_F_CONSUMERS 480
+#endif
+#ifndef WL_UPD_F_PER
+#define WL_UPD_F_PER 8
+#endif
+#ifndef WL_UPD_F_SE
+#define WL_UPD_F_SE 4096
+#endif
+// 1: the float update accumulates in float (coefficients rounded to float: one FFMA per element and output);
+// 0: in double (one float -> double conversion per element on the XU pipe, NOUT DFMA)
+#ifndef WL_UPD_F_ACC32
+#define WL_UPD_F_ACC32 1
+#endif
+template <class T>
+__host__ __device__ constexpr int dots_per() { return sizeof(T) == 8 ? kDotsPer : WL_DOTS_F_PER; }
+// toar_update with float storage: 480 consumers x 8 elements (15 KB tiles; 16 warps, so up to 128 registers
+// hold the 3 x 8 double accumulators without spilling), double: 512 x 4
+template <class T>
+__host__ __device__ constexpr int upd_consumers() { return sizeof(T) == 8 ? kUpdConsumers : WL_UPD_F_CONSUMERS; }
+template <class T>
+__host__ __device__ constexpr int upd_per() { return sizeof(T) == 8 ? kUpdPer : WL_UPD_F_PER; }
+static_assert(WL_UPD_F_CONSUMERS * WL_UPD_F_PER <= WL_UPD_F_SE && 128 * WL_DOTS_F_PER <= 2048, "float tiles fit a stage");
 constexpr int kRedBatch = 24;                       // dots epilogue: values per smem round
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -47,15 +85,18 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t ph) {
       "r"(ph)
       : "memory");
 }
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const double* src, int bytes, uint32_t bar) {
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, int bytes, uint32_t bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                "l"(src), "r"(bytes), "r"(bar)
                : "memory");
 }
 
 // Producer: item sequence per tile = [X0, X1, q_0 .. q_{nq-1}]; X1 may be two-source (wa | wb).
-__device__ __forceinline__ void ring_produce(const Dcgs2Args& a, const double* X0, const double* X1a, const double* X1b,
-                             int64_t h, int E, double* ring, uint64_t* full, uint64_t* empty) {
+template <class T, int SE>
+__device__ __forceinline__ void ring_produce(const Dcgs2Args& a, const T* X0, const T* X1a, const T* X1b,
+                             int64_t h, int E, T* ring, uint64_t* full, uint64_t* empty) {
+  constexpr int kStages = ring_stages<T, SE>();
+  constexpr int sz = (int)sizeof(T);
   const int64_t N = a.len * a.B;
   int s = 0;
   uint32_t ph = 0;
@@ -66,35 +107,37 @@ __device__ __forceinline__ void ring_produce(const Dcgs2Args& a, const double* X
     for (int item = 0; item < nitems; ++item, ++it) {
       if (it >= kStages) mbar_wait(su32(&empty[s]), ph ^ 1);
       const uint32_t bar = su32(&full[s]);
-      const uint32_t dst = su32(ring + (int64_t)s * kStageElems);
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(cnt * 8) : "memory");
+      const uint32_t dst = su32(ring + (int64_t)s * SE);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(cnt * sz) : "memory");
       const int qi = item - (X0 ? 1 : 0) - (X1a ? 1 : 0);
       if (X0 && item == 0) {
-        bulk_g2s(dst, X0 + e0, cnt * 8, bar);
+        bulk_g2s(dst, X0 + e0, cnt * sz, bar);
       } else if (qi < 0) {  // X1, possibly straddling the two sources at h
         if (X1b == nullptr || e0 + cnt <= h) {
-          bulk_g2s(dst, X1a + e0, cnt * 8, bar);
+          bulk_g2s(dst, X1a + e0, cnt * sz, bar);
         } else if (e0 >= h) {
-          bulk_g2s(dst, X1b + (e0 - h), cnt * 8, bar);
+          bulk_g2s(dst, X1b + (e0 - h), cnt * sz, bar);
         } else {
           const int c1 = (int)(h - e0);
-          bulk_g2s(dst, X1a + e0, c1 * 8, bar);
-          bulk_g2s(dst + c1 * 8, X1b, (cnt - c1) * 8, bar);
+          bulk_g2s(dst, X1a + e0, c1 * sz, bar);
+          bulk_g2s(dst + c1 * sz, X1b, (cnt - c1) * sz, bar);
         }
       } else {
-        bulk_g2s(dst, a.Q.p[qi] + e0, cnt * 8, bar);
+        bulk_g2s(dst, reinterpret_cast<const T*>(a.Q.p[qi]) + e0, cnt * sz, bar);
       }
       if (++s == kStages) { s = 0; ph ^= 1; }
     }
   }
 }
 
+template <class T, int SE>
 struct RingCursor {
+  static constexpr int kStages = ring_stages<T, SE>();
   int s = 0;
   uint32_t ph = 0;
-  __device__ const double* acquire(double* ring, uint64_t* full) {
+  __device__ const T* acquire(T* ring, uint64_t* full) {
     mbar_wait(su32(&full[s]), ph);
-    return ring + (int64_t)s * kStageElems;
+    return ring + (int64_t)s * SE;
   }
   __device__ void release(uint64_t* empty, int lane) {
     __syncwarp();
@@ -103,9 +146,9 @@ struct RingCursor {
   }
 };
 
-__device__ __forceinline__ void ring_init(uint64_t* full, uint64_t* empty, int consumer_warps) {
+__device__ __forceinline__ void ring_init(uint64_t* full, uint64_t* empty, int consumer_warps, int nstages) {
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < nstages; ++s) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&full[s])));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&empty[s])), "r"(consumer_warps));
     }
@@ -113,16 +156,22 @@ __device__ __forceinline__ void ring_init(uint64_t* full, uint64_t* empty, int c
   }
 }
 
-// pass A: items [P, w?, q_0..q_{nq-1}]
+// pass A: items [P, w?, q_0..q_{nq-1}]; T = the storage type (values are converted and summed in double)
+template <class T>
 __global__ void __launch_bounds__(kDotsConsumers + 32, 1) dcgs2_dots_ring(Dcgs2Args a, int tpb) {
-  extern __shared__ __align__(128) double ring[];
-  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+  constexpr int SE = 2048;
+  constexpr int kStages = ring_stages<T, SE>();
+  extern __shared__ __align__(128) double ring_raw[];
+  T* ring = reinterpret_cast<T*>(ring_raw);
+  __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, t = threadIdx.x;
   const int B = a.B, nq = a.nq;
-  const int E = tpb * kDotsPer;
+  constexpr int PER = dots_per<T>();
+  constexpr bool kF32 = sizeof(T) == 4;
+  const int E = tpb * PER;
   const int64_t N = a.len * a.B, h = a.split * a.B;
   const bool has_w = a.wa != nullptr;
-  ring_init(full, empty, kDotsConsumers / 32);
+  ring_init(full, empty, kDotsConsumers / 32, kStages);
   // the basis loads below carry no bounds predicate (fewer instructions in the 32x-unrolled loop:
   // less icache pressure).  Entries they read past a ragged tile's end, or past E for a lane beyond
   // tpb, meet p = w = 0 and must be finite: zero [E, stage end) of every stage, and the whole ring in
@@ -131,7 +180,7 @@ __global__ void __launch_bounds__(kDotsConsumers + 32, 1) dcgs2_dots_ring(Dcgs2A
     const int64_t last = (N - 1) / E;
     const bool ragged = N % E != 0 && last % gridDim.x == blockIdx.x;
     for (int st = 0; st < kStages; ++st)
-      for (int i = (ragged ? 0 : E) + t; i < kStageElems; i += blockDim.x) ring[(int64_t)st * kStageElems + i] = 0.0;
+      for (int i = (ragged ? 0 : E) + t; i < SE; i += blockDim.x) ring[(int64_t)st * SE + i] = T(0);
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
@@ -139,44 +188,58 @@ __global__ void __launch_bounds__(kDotsConsumers + 32, 1) dcgs2_dots_ring(Dcgs2A
 #pragma unroll
   for (int v = 0; v < 2 * kMaxVecPerLaunch; ++v) acc[v] = 0.0;
   if (warp == kDotsConsumers / 32) {
-    if (lane == 0) ring_produce(a, a.P, has_w ? a.wa : nullptr, a.wb, h, E, ring, full, empty);
+    if (lane == 0)
+      ring_produce<T, SE>(a, reinterpret_cast<const T*>(a.P), has_w ? reinterpret_cast<const T*>(a.wa) : nullptr,
+                      reinterpret_cast<const T*>(a.wb), h, E, ring, full, empty);
   } else {
-    RingCursor cur;
+    RingCursor<T, SE> cur;
     const bool act = t < tpb;
     for (int64_t e0 = (int64_t)blockIdx.x * E; e0 < N; e0 += (int64_t)gridDim.x * E) {
       const int cnt = (int)min((int64_t)E, N - e0);
-      double pv[kDotsPer], wv[kDotsPer];
+      // the tile's values; with float storage the products of one tile (PER = 32 per thread) are summed in
+      // float and each tile partial is added to the double accumulators (one conversion per tile and vector)
+      T pv[PER], wv[PER];
       {
-        const double* st = cur.acquire(ring, full);
+        const T* st = cur.acquire(ring, full);
 #pragma unroll
-        for (int i = 0; i < kDotsPer; ++i) pv[i] = (act && t + i * tpb < cnt) ? st[t + i * tpb] : 0.0;
+        for (int i = 0; i < PER; ++i) pv[i] = (act && t + i * tpb < cnt) ? st[t + i * tpb] : T(0);
         cur.release(empty, lane);
       }
       if (has_w) {
-        const double* st = cur.acquire(ring, full);
+        const T* st = cur.acquire(ring, full);
 #pragma unroll
-        for (int i = 0; i < kDotsPer; ++i) wv[i] = (act && t + i * tpb < cnt) ? st[t + i * tpb] : 0.0;
+        for (int i = 0; i < PER; ++i) wv[i] = (act && t + i * tpb < cnt) ? st[t + i * tpb] : T(0);
         cur.release(empty, lane);
       } else {
 #pragma unroll
-        for (int i = 0; i < kDotsPer; ++i) wv[i] = 0.0;
+        for (int i = 0; i < PER; ++i) wv[i] = T(0);
       }
+      {
+        T al = kF32 ? T(0) : T(alpha), be = kF32 ? T(0) : T(beta), ga = kF32 ? T(0) : T(gamma);
 #pragma unroll
-      for (int i = 0; i < kDotsPer; ++i) {
-        alpha += pv[i] * pv[i];
-        beta += pv[i] * wv[i];
-        gamma += wv[i] * wv[i];
+        for (int i = 0; i < PER; ++i) {
+          al += pv[i] * pv[i];
+          be += pv[i] * wv[i];
+          ga += wv[i] * wv[i];
+        }
+        alpha = kF32 ? alpha + (double)al : (double)al;
+        beta = kF32 ? beta + (double)be : (double)be;
+        gamma = kF32 ? gamma + (double)ga : (double)ga;
       }
 #pragma unroll 32
       for (int j = 0; j < kMaxVecPerLaunch; ++j) {
         if (j < nq) {
-          const double* st = cur.acquire(ring, full);
+          const T* st = cur.acquire(ring, full);
+          // double: straight into the running sums (the fp64 path's order); float: a per-tile partial
+          T sa = kF32 ? T(0) : T(acc[2 * j]), sb = kF32 ? T(0) : T(acc[2 * j + 1]);
 #pragma unroll
-          for (int i = 0; i < kDotsPer; ++i) {
-            const double q = st[t + i * tpb];  // t + 15 tpb < kStageElems for every B
-            acc[2 * j] += q * pv[i];
-            acc[2 * j + 1] += q * wv[i];
+          for (int i = 0; i < PER; ++i) {
+            const T q = st[t + i * tpb];  // t + (PER - 1) tpb < SE for every B
+            sa += q * pv[i];
+            sb += q * wv[i];
           }
+          acc[2 * j] = kF32 ? acc[2 * j] + (double)sa : (double)sa;
+          acc[2 * j + 1] = kF32 ? acc[2 * j + 1] + (double)sb : (double)sb;
           cur.release(empty, lane);
         }
       }
@@ -185,7 +248,7 @@ __global__ void __launch_bounds__(kDotsConsumers + 32, 1) dcgs2_dots_ring(Dcgs2A
   __syncthreads();  // every copy has landed and been consumed: the ring is free
   // epilogue: per (value, column) sum over the consumer threads of that column, fixed order
   const int nval = 2 * nq + 3;
-  double* red = ring;  // [kRedBatch][kDotsConsumers]
+  double* red = ring_raw;  // [kRedBatch][kDotsConsumers]
   for (int v0 = 0; v0 < nval; v0 += kRedBatch) {
     if (t < kDotsConsumers) {
 #pragma unroll
@@ -211,21 +274,21 @@ __global__ void __launch_bounds__(kDotsConsumers + 32, 1) dcgs2_dots_ring(Dcgs2A
 // pass B: items [X0, X1, q_0..q_{nq-1}];  q_j = a0 X0 + Σ cq_i q_i,  p_{j+1} = a1 X0 + a2 X1 + Σ cp_i q_i
 // (X0, X1) = (p_j, w) with (a0, a1, a2) = (cq_p, cp_p, cp_w), or (Qout, Pnext) with (1, 0, 1)
 // for the vector tiles after the first (accumulate).
-__global__ void __launch_bounds__(kUpdConsumers + 32, 1) dcgs2_update_ring(Dcgs2Args a, int tpb) {
+__global__ void __launch_bounds__(kUpdConsumers + 32, 1) dcgs2_update_ring(Dcgs2Args a, int tpb) {  // double storage
   extern __shared__ __align__(128) double ring[];
-  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+  __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
   __shared__ double coef[2 * kMaxVecPerLaunch * kMaxCols];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, t = threadIdx.x;
   const int B = a.B, nq = a.nq;
   const int E = tpb * kUpdPer;
   const int64_t N = a.len * a.B, h = a.split * a.B;
   for (int i = t; i < 2 * nq * B; i += blockDim.x) coef[i] = a.coef_v[i];
-  ring_init(full, empty, kUpdConsumers / 32);
+  ring_init(full, empty, kUpdConsumers / 32, ring_stages<double, kStageElems>());
   __syncthreads();
   if (warp == kUpdConsumers / 32) {
     if (lane == 0) {
-      if (a.accumulate) ring_produce(a, a.Qout, a.Pnext, nullptr, h, E, ring, full, empty);
-      else ring_produce(a, a.P, a.wa, a.wb, h, E, ring, full, empty);
+      if (a.accumulate) ring_produce<double, kStageElems>(a, a.Qout, a.Pnext, nullptr, h, E, ring, full, empty);
+      else ring_produce<double, kStageElems>(a, a.P, a.wa, a.wb, h, E, ring, full, empty);
     }
     return;
   }
@@ -238,7 +301,7 @@ __global__ void __launch_bounds__(kUpdConsumers + 32, 1) dcgs2_update_ring(Dcgs2
     a0 = a.coef_s[c]; a1 = a.coef_s[B + c]; a2 = a.coef_s[2 * B + c];
     dead = a0 == 0.0;
   }
-  RingCursor cur;
+  RingCursor<double, kStageElems> cur;
   for (int64_t e0 = (int64_t)blockIdx.x * E; e0 < N; e0 += (int64_t)gridDim.x * E) {
     const int cnt = (int)min((int64_t)E, N - e0);
     double sq[kUpdPer], sp[kUpdPer];
@@ -285,23 +348,27 @@ __global__ void __launch_bounds__(kUpdConsumers + 32, 1) dcgs2_update_ring(Dcgs2
 // Items per tile: the bases (y for the first vector tile; the outputs themselves, identity
 // coefficients, for later tiles of > 32 vectors) then U_0..U_{m-1}.  Same ring as pass B.
 constexpr int kToarMaxOut = 3;
-template <int NOUT>
-__global__ void __launch_bounds__(kUpdConsumers + 32, 1) toar_update_ring(ToarArgs a, int tpb) {
-  extern __shared__ __align__(128) double ring[];
-  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+template <int NOUT, class T>
+__global__ void __launch_bounds__(upd_consumers<T>() + 32, 1) toar_update_ring(ToarArgs a, int tpb) {
+  constexpr int SE = sizeof(T) == 8 ? stage_elems<T>() : WL_UPD_F_SE;
+  constexpr int kStages = ring_stages<T, SE>();
+  constexpr int PER = upd_per<T>();
+  extern __shared__ __align__(128) double ring_raw[];
+  T* ring = reinterpret_cast<T*>(ring_raw);
+  __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
   __shared__ double coef[NOUT * kMaxVecPerLaunch * kMaxCols];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, t = threadIdx.x;
   const int B = a.B, m = a.m;
-  const int E = tpb * kUpdPer;
+  const int E = tpb * PER;
   const int64_t N = a.len * a.B;
   const int nb = a.accumulate ? NOUT : 1;
   for (int i = t; i < NOUT * m * B; i += blockDim.x) {
     const int o = i / (m * B), r = i - o * m * B;
     coef[i] = a.coef_u[(int64_t)(o * a.coef_ld) * B + r];
   }
-  ring_init(full, empty, kUpdConsumers / 32);
+  ring_init(full, empty, upd_consumers<T>() / 32, kStages);
   __syncthreads();
-  if (warp == kUpdConsumers / 32) {
+  if (warp == upd_consumers<T>() / 32) {
     if (lane == 0) {  // producer: items [bases..., U_0..U_{m-1}] per tile
       int s = 0;
       uint32_t ph = 0;
@@ -311,9 +378,10 @@ __global__ void __launch_bounds__(kUpdConsumers + 32, 1) toar_update_ring(ToarAr
         for (int item = 0; item < nb + m; ++item, ++it) {
           if (it >= kStages) mbar_wait(su32(&empty[s]), ph ^ 1);
           const uint32_t bar = su32(&full[s]);
-          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(cnt * 8) : "memory");
-          const double* src = item < nb ? (a.accumulate ? a.out[item] : a.y) : a.U.p[item - nb];
-          bulk_g2s(su32(ring + (int64_t)s * kStageElems), src + e0, cnt * 8, bar);
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(cnt * (int)sizeof(T))
+                       : "memory");
+          const T* src = reinterpret_cast<const T*>(item < nb ? (a.accumulate ? a.out[item] : a.y) : a.U.p[item - nb]);
+          bulk_g2s(su32(ring + (int64_t)s * SE), src + e0, cnt * (int)sizeof(T), bar);
           if (++s == kStages) { s = 0; ph ^= 1; }
         }
       }
@@ -322,35 +390,38 @@ __global__ void __launch_bounds__(kUpdConsumers + 32, 1) toar_update_ring(ToarAr
   }
   const bool act = t < tpb;
   const int c = t % B;
-  double cy[NOUT];
+  // accumulator type: double, or float for float storage with WL_UPD_F_ACC32 (the outputs are rounded to float
+  // anyway; the m + 1 <= 33 terms add ~sqrt(m) roundings of the size of the stored inputs' own)
+  using Acc = typename std::conditional<sizeof(T) == 4 && WL_UPD_F_ACC32, float, double>::type;
+  Acc cy[NOUT];
 #pragma unroll
-  for (int o = 0; o < NOUT; ++o) cy[o] = a.coef_y[o * B + c];
-  RingCursor cur;
+  for (int o = 0; o < NOUT; ++o) cy[o] = (Acc)a.coef_y[o * B + c];
+  RingCursor<T, SE> cur;
   for (int64_t e0 = (int64_t)blockIdx.x * E; e0 < N; e0 += (int64_t)gridDim.x * E) {
     const int cnt = (int)min((int64_t)E, N - e0);
-    double acc[NOUT][kUpdPer];
+    Acc acc[NOUT][PER];
 #pragma unroll
     for (int o = 0; o < NOUT; ++o)
 #pragma unroll
-      for (int i = 0; i < kUpdPer; ++i) acc[o][i] = 0.0;
+      for (int i = 0; i < PER; ++i) acc[o][i] = Acc(0);
     for (int b = 0; b < nb; ++b) {
-      const double* st = cur.acquire(ring, full);
+      const T* st = cur.acquire(ring, full);
 #pragma unroll
-      for (int i = 0; i < kUpdPer; ++i) {
-        const double v = (act && t + i * tpb < cnt) ? st[t + i * tpb] : 0.0;
+      for (int i = 0; i < PER; ++i) {
+        const Acc v = (act && t + i * tpb < cnt) ? (Acc)st[t + i * tpb] : Acc(0);
 #pragma unroll
-        for (int o = 0; o < NOUT; ++o) acc[o][i] += (a.accumulate ? (o == b ? 1.0 : 0.0) : cy[o]) * v;
+        for (int o = 0; o < NOUT; ++o) acc[o][i] += (a.accumulate ? (o == b ? Acc(1) : Acc(0)) : cy[o]) * v;
       }
       cur.release(empty, lane);
     }
     for (int j = 0; j < m; ++j) {
-      double cj[NOUT];
+      Acc cj[NOUT];
 #pragma unroll
-      for (int o = 0; o < NOUT; ++o) cj[o] = coef[(o * m + j) * B + c];
-      const double* st = cur.acquire(ring, full);
+      for (int o = 0; o < NOUT; ++o) cj[o] = (Acc)coef[(o * m + j) * B + c];
+      const T* st = cur.acquire(ring, full);
 #pragma unroll
-      for (int i = 0; i < kUpdPer; ++i) {
-        const double v = (act && t + i * tpb < cnt) ? st[t + i * tpb] : 0.0;
+      for (int i = 0; i < PER; ++i) {
+        const Acc v = (act && t + i * tpb < cnt) ? (Acc)st[t + i * tpb] : Acc(0);
 #pragma unroll
         for (int o = 0; o < NOUT; ++o) acc[o][i] += cj[o] * v;
       }
@@ -361,18 +432,19 @@ __global__ void __launch_bounds__(kUpdConsumers + 32, 1) toar_update_ring(ToarAr
       // e0/B + t/B + i*(tpb/B) — outputs with a padded row stride (out_ld) are addressed from it
       const int64_t r0 = e0 / B + t / B;
 #pragma unroll
-      for (int i = 0; i < kUpdPer; ++i)
+      for (int i = 0; i < PER; ++i)
         if (t + i * tpb < cnt) {
 #pragma unroll
           for (int o = 0; o < NOUT; ++o) {
+            T* out = reinterpret_cast<T*>(a.out[o]);
             if (a.out_ld[o] > B) {
-              double* row = a.out[o] + (r0 + (int64_t)i * (tpb / B)) * a.out_ld[o];
-              row[c] = acc[o][i];
+              T* row = out + (r0 + (int64_t)i * (tpb / B)) * a.out_ld[o];
+              row[c] = (T)acc[o][i];
               // the phantom columns too: whole 32-byte sectors reach L2, so DRAM sees no partial-sector writes
               if (c == B - 1)
-                for (int cc = B; cc < pad_vec(B); ++cc) row[cc] = 0.0;
+                for (int cc = B; cc < pad_vec_t<T>(B); ++cc) row[cc] = T(0);
             } else {
-              a.out[o][e0 + t + i * tpb] = acc[o][i];
+              out[e0 + t + i * tpb] = (T)acc[o][i];
             }
           }
         }
@@ -380,7 +452,7 @@ __global__ void __launch_bounds__(kUpdConsumers + 32, 1) toar_update_ring(ToarAr
   }
 }
 
-size_t ring_smem() { return (size_t)kStages * kStageElems * sizeof(double); }
+size_t ring_smem() { return (size_t)kRingBytes; }  // every ring
 
 VecPtrs shifted(const VecPtrs& v, int i0) {
   VecPtrs r{};
@@ -407,16 +479,19 @@ int dcgs2_dots(Dcgs2Args a, cudaStream_t s) {
   WL_LAUNCH("dcgs2_dots");
   {
     if ((a.split * a.B) % 2) throw Error(1, "dcgs2: half length must be even (phantom row)");
-    static bool attr = false;
-    if (!attr) {
-      WL_CUDA(cudaFuncSetAttribute(dcgs2_dots_ring, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ring_smem()));
-      attr = true;
+    if (a.f32 && (a.split * a.B) % 4) throw Error(1, "dcgs2: fp32 half length must be a multiple of 4 elements");
+    auto kern = a.f32 ? dcgs2_dots_ring<float> : dcgs2_dots_ring<double>;
+    static bool attr[2] = {false, false};
+    if (!attr[a.f32 ? 1 : 0]) {
+      WL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ring_smem()));
+      attr[a.f32 ? 1 : 0] = true;
     }
     const int tpb = kDotsConsumers / a.B * a.B;
     const int64_t N = a.len * a.B;
     // one persistent CTA per SM; an empty rank (N = 0) still launches one CTA so its partials are zeros
-    a.grid = (int)std::max<int64_t>(1, std::min<int64_t>(num_sms(), (N + tpb * kDotsPer - 1) / (tpb * kDotsPer)));
-    dcgs2_dots_ring<<<a.grid, kDotsConsumers + 32, ring_smem(), s>>>(a, tpb);
+    const int E = tpb * (a.f32 ? dots_per<float>() : dots_per<double>());
+    a.grid = (int)std::max<int64_t>(1, std::min<int64_t>(num_sms(), (N + E - 1) / E));
+    kern<<<a.grid, kDotsConsumers + 32, ring_smem(), s>>>(a, tpb);
     WL_CUDA(cudaGetLastError());
     if (a.sums_out) {  // null: the consumer reduces the partials itself (a.grid of them per output)
       note_launch("gram_reduce");
@@ -427,6 +502,7 @@ int dcgs2_dots(Dcgs2Args a, cudaStream_t s) {
 }
 
 void dcgs2_update(Dcgs2Args a, cudaStream_t s) {
+  if (a.f32) throw Error(1, "dcgs2_update: double storage only (the fp32 mode runs TOAR)");
   if (a.nq > kMaxVecPerLaunch) {
     for (int i0 = 0; i0 < a.nq; i0 += kMaxVecPerLaunch) {
       Dcgs2Args t = a;
@@ -473,18 +549,23 @@ void toar_update(ToarArgs a, cudaStream_t s) {
     return;
   }
   WL_LAUNCH("toar_update");
-  if ((a.len * a.B) % 2) throw Error(1, "toar_update: vector length must be even (phantom row)");
-  static bool attr[kToarMaxOut + 1] = {};
-  auto kern = a.nout == 1 ? toar_update_ring<1> : a.nout == 2 ? toar_update_ring<2> : toar_update_ring<3>;
-  if (!attr[a.nout]) {
+  if ((a.len * a.B) % (a.f32 ? 4 : 2)) throw Error(1, "toar_update: vector length must be a multiple of 16 bytes (phantom rows)");
+  static bool attr[2][kToarMaxOut + 1] = {};
+  auto kern = a.f32 ? (a.nout == 1 ? toar_update_ring<1, float> : a.nout == 2 ? toar_update_ring<2, float>
+                                                                              : toar_update_ring<3, float>)
+                    : (a.nout == 1 ? toar_update_ring<1, double> : a.nout == 2 ? toar_update_ring<2, double>
+                                                                                : toar_update_ring<3, double>);
+  if (!attr[a.f32 ? 1 : 0][a.nout]) {
     WL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ring_smem()));
-    attr[a.nout] = true;
+    attr[a.f32 ? 1 : 0][a.nout] = true;
   }
-  const int tpb = kUpdConsumers / a.B * a.B;
+  const int nc = a.f32 ? upd_consumers<float>() : upd_consumers<double>();
+  const int tpb = nc / a.B * a.B;
   const int64_t N = a.len * a.B;
-  const int grid = (int)std::min<int64_t>(num_sms(), (N + tpb * kUpdPer - 1) / (tpb * kUpdPer));
+  const int E = tpb * (a.f32 ? upd_per<float>() : upd_per<double>());
+  const int grid = (int)std::min<int64_t>(num_sms(), (N + E - 1) / E);
   if (grid == 0) return;  // empty rank
-  kern<<<grid, kUpdConsumers + 32, ring_smem(), s>>>(a, tpb);
+  kern<<<grid, nc + 32, ring_smem(), s>>>(a, tpb);
   WL_CUDA(cudaGetLastError());
 }
 

@@ -14,7 +14,6 @@
 #include "walklap.h"
 #include "wl_internal.cuh"
 
-#include <cublas_v2.h>
 #include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
@@ -260,15 +259,15 @@ struct wl_workspace {
   DArr<int> vid;                 // 0, 1, ..., kMaxCols-1
   DArr<double> toar_state, toar_cy, toar_cu, toar_comb;  // TOAR (toar.cu): per-column state, update coefficients
   DArr<double> xg;               // TOAR: the SpMM's gathered block with rows padded to pad_cols(B) (zero phantoms)
+  DArr<double> seed32;           // TOAR, opts.fp32: A v and A(Av) - μ d v in double before rounding (2 n x B)
   // host-buffer entry point
   DArr<double> hV, hLV;
   // diffusion (outer Lanczos)
   int kout_alloc = 0;
   DArr<double> oQ, ow, oH, on0, oref, osums1, ocoef_v, ocoef_s, otau, oY, oscratch;
   DArr<int> okeff;
-  // XNysTrace-exp (wl_xnystrace_exp): block basis, block, temp block, Gram blocks; cuBLAS handle
-  DArr<double> trV, trW, trW2, trC, trR;
-  cublasHandle_t cublas = nullptr;
+  // XNysTrace-exp (wl_xnystrace_exp): block basis, block, temp block, Gram blocks, Gram partials (block.cu)
+  DArr<double> trV, trW, trW2, trC, trR, trPart;
   // rational XNysTrace-exp: continuation block, MINRES vectors (v, v_prev, w1, w2, x, p; 2 halves each)
   DArr<double> rkU, mrV;
   DArr<double> mr_sc, mr_sums;
@@ -281,7 +280,6 @@ struct wl_workspace {
     if (cg_flags_host) cudaFreeHost(cg_flags_host);
     if (mr_nact_host) cudaFreeHost(mr_nact_host);
     if (kflag_host) cudaFreeHost(kflag_host);
-    if (cublas) cublasDestroy(cublas);
   }
 };
 
@@ -299,28 +297,41 @@ void allreduce(const wl_operator* op, double* buf, size_t count, cudaStream_t s)
 // Rows of `src` (n_loc x B, ld lds) that other ranks reference are packed and exchanged into
 // ws->halo_recv (n_halo x B), ordered by owner rank then global id (comm.cu: grouped NCCL
 // send/recv, or device copies in a loopback group).
-void halo_exchange(const wl_operator* op, wl_workspace* ws, const double* src, int64_t lds, int B,
-                   cudaStream_t s) {
-  if (!multi(op)) return;
-  WL_NVTX("halo_exchange");
-  pack_rows(src, lds, op->send_idx.p, op->n_send, B, ws->halo_send.p, s);
+// f32: src and the halo buffers hold float (opts.fp32 TOAR batches).
+void halo_post(const wl_operator* op, wl_workspace* ws, const double* src, int64_t lds, int w, bool f32,
+               cudaStream_t pack_stream, cudaStream_t xfer_stream, cudaEvent_t ev) {
+  if (f32) pack_rows_f32(reinterpret_cast<const float*>(src), lds, op->send_idx.p, op->n_send, w,
+                         reinterpret_cast<float*>(ws->halo_send.p), pack_stream);
+  else pack_rows(src, lds, op->send_idx.p, op->n_send, w, ws->halo_send.p, pack_stream);
+  if (ev) {
+    WL_CUDA(cudaEventRecord(ev, pack_stream));
+    WL_CUDA(cudaStreamWaitEvent(xfer_stream, ev, 0));
+  }
+  const size_t esz = f32 ? sizeof(float) : sizeof(double);
+  char* sb = reinterpret_cast<char*>(ws->halo_send.p);
+  char* rb = reinterpret_cast<char*>(ws->halo_recv.p);
   std::vector<Xfer> sends, recvs;
   for (int p = 0; p < op->nranks; ++p) {
     if (p == op->rank) continue;
-    if (op->send_cnt[p] > 0)
-      sends.push_back({ws->halo_send.p + op->send_displ[p] * B, sizeof(double) * op->send_cnt[p] * B, p});
-    if (op->recv_cnt[p] > 0)
-      recvs.push_back({ws->halo_recv.p + op->recv_displ[p] * B, sizeof(double) * op->recv_cnt[p] * B, p});
+    if (op->send_cnt[p] > 0) sends.push_back({sb + esz * op->send_displ[p] * w, esz * op->send_cnt[p] * w, p});
+    if (op->recv_cnt[p] > 0) recvs.push_back({rb + esz * op->recv_displ[p] * w, esz * op->recv_cnt[p] * w, p});
   }
-  comm_sendrecv(op->comm, sends, recvs, s);
+  comm_sendrecv(op->comm, sends, recvs, xfer_stream);
+}
+void halo_exchange(const wl_operator* op, wl_workspace* ws, const double* src, int64_t lds, int B,
+                   cudaStream_t s, bool f32 = false) {
+  if (!multi(op)) return;
+  WL_NVTX("halo_exchange");
+  halo_post(op, ws, src, lds, B, f32, s, s, nullptr);
 }
 
 // One SpMM launch over CSR part `part` of the operator (see wl_operator::A / Ah).
 void spmv_part(const wl_operator* op, wl_workspace* ws, const CsrPart& part, bool halo_part, const double* y,
                int64_t ldy, const double* x, const double* g0, const double* g1, const double* scale, double* out,
-               int B, cudaStream_t s, const int* active) {
+               int B, cudaStream_t s, const int* active, bool f32) {
   SpmvArgs a{};
   a.active = active;
+  a.f32 = f32 ? 1 : 0;
   a.rowptr = part.rowptr.p;
   a.col = part.col.p;
   a.n_loc = op->n_loc;
@@ -364,31 +375,20 @@ void spmv_part(const wl_operator* op, wl_workspace* ws, const CsrPart& part, boo
 // Multi-rank: the rows of y that peers reference are exchanged first (whole padded rows); with the
 // A_loc / A_halo split (opts.halo_overlap) the exchange runs on the workspace's comm stream while
 // A_loc's SpMM runs, and A_halo's SpMM adds the halo terms once it has arrived.
+// f32: y, x and out hold float (opts.fp32 TOAR batches; element strides).
 void do_spmv(const wl_operator* op, wl_workspace* ws, const double* y, int64_t ldy, const double* x,
              const double* g0, const double* g1, const double* scale, double* out, int B,
-             cudaStream_t s, const int* active = nullptr) {
+             cudaStream_t s, const int* active = nullptr, bool f32 = false) {
   if (!multi(op) || !op->split) {
-    halo_exchange(op, ws, y, ldy, (int)ldy, s);
-    spmv_part(op, ws, op->A, false, y, ldy, x, g0, g1, scale, out, B, s, active);
+    halo_exchange(op, ws, y, ldy, (int)ldy, s, f32);
+    spmv_part(op, ws, op->A, false, y, ldy, x, g0, g1, scale, out, B, s, active, f32);
     return;
   }
-  const int w = (int)ldy;
-  pack_rows(y, ldy, op->send_idx.p, op->n_send, w, ws->halo_send.p, s);
-  WL_CUDA(cudaEventRecord(ws->ev_pack, s));
-  WL_CUDA(cudaStreamWaitEvent(ws->cstream, ws->ev_pack, 0));
-  std::vector<Xfer> sends, recvs;
-  for (int p = 0; p < op->nranks; ++p) {
-    if (p == op->rank) continue;
-    if (op->send_cnt[p] > 0)
-      sends.push_back({ws->halo_send.p + op->send_displ[p] * w, sizeof(double) * op->send_cnt[p] * w, p});
-    if (op->recv_cnt[p] > 0)
-      recvs.push_back({ws->halo_recv.p + op->recv_displ[p] * w, sizeof(double) * op->recv_cnt[p] * w, p});
-  }
-  comm_sendrecv(op->comm, sends, recvs, ws->cstream);
+  halo_post(op, ws, y, ldy, (int)ldy, f32, s, ws->cstream, ws->ev_pack);
   WL_CUDA(cudaEventRecord(ws->ev_halo, ws->cstream));
-  spmv_part(op, ws, op->A, false, y, ldy, x, g0, g1, scale, out, B, s, active);
+  spmv_part(op, ws, op->A, false, y, ldy, x, g0, g1, scale, out, B, s, active, f32);
   WL_CUDA(cudaStreamWaitEvent(s, ws->ev_halo, 0));
-  spmv_part(op, ws, op->Ah, true, y, ldy, x, g0, g1, scale, out, B, s, active);
+  spmv_part(op, ws, op->Ah, true, y, ldy, x, g0, g1, scale, out, B, s, active, f32);
 }
 
 // halo buffers, comm stream and events of a workspace (multi-rank)
@@ -407,7 +407,8 @@ void spmv_scratch(const wl_operator* op, wl_workspace* ws, int B) {
   ws_comm_init(op, ws, B);
   const int nch = std::max(op->A.n_chunks, op->Ah.n_chunks);  // the two parts run one after the other
   if (nch == 0) return;
-  if (ws->chunk_part.n < (size_t)nch * pad_cols(B)) ws->chunk_part.alloc((size_t)nch * pad_cols(B));
+  // a chunk's partial row holds W * VW <= 32 values (every lane slot of its group, either storage type)
+  if (ws->chunk_part.n < (size_t)nch * kMaxCols) ws->chunk_part.alloc((size_t)nch * kMaxCols);
   if (ws->row_ticket.n < (size_t)nch) {
     ws->row_ticket.alloc(nch);
     WL_CUDA(cudaMemset(ws->row_ticket.p, 0, sizeof(unsigned int) * nch));
@@ -523,18 +524,31 @@ void toar_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double*
   const int32_t* perm = user_order ? op->perm.p : nullptr;
   const int64_t n = op->n_loc;
   const int K = ws->K;
-  const int64_t n_pad = n + ((n * B) & 1);  // even element counts for the bulk copies (phantom row)
+  // opts.fp32: the n-vectors of the batch (U, x, z, y and the gathered block) hold float; the seeds, every sum and
+  // the coefficient work stay double.  t' (mode 2, at create) is always computed in double.
+  const bool f32 = op->opts.fp32 && mode != 2;
+  const size_t esz = f32 ? sizeof(float) : sizeof(double);
+  // bulk copies move whole 16-byte pieces: the element count of a vector is padded with zero phantom rows
+  int64_t n_pad = n;
+  while ((n_pad * B * (int64_t)esz) % 16) ++n_pad;
   const int64_t vs = n_pad * B;
+  auto vec = [&](int64_t i) -> double* {  // vector slot i of the basis allocation, in the storage type
+    return f32 ? reinterpret_cast<double*>(reinterpret_cast<float*>(ws->basis.p) + i * vs) : ws->basis.p + i * vs;
+  };
+  auto zero_rows = [&](double* v, int64_t r0, int64_t r1) {  // rows [r0, r1) of an n_pad x B vector
+    if (r1 > r0)
+      WL_CUDA(cudaMemsetAsync(reinterpret_cast<char*>(v) + (size_t)r0 * B * esz, 0, (size_t)(r1 - r0) * B * esz, s));
+  };
   double* g0z = ws->colp.p;
   double* g1z = g0z + kMaxCols;
   double* g0s = g1z + kMaxCols;
   double* g1s = g0s + kMaxCols;
   setup_chunk(op->mu_dev.p, gstart, b, B, g0z, g1z, g0s, g1s, ws->vcol.p, ws->tcol.p, s);
   VecPtrs U{};
-  for (int i = 0; i < K + 2; ++i) U.p[i] = ws->basis.p + (int64_t)i * vs;
-  double* xb = ws->basis.p + (int64_t)(K + 2) * vs;
-  double* zb = xb + vs;
-  double* yb = zb + vs;
+  for (int i = 0; i < K + 2; ++i) U.p[i] = vec(i);
+  double* xb = vec(K + 2);
+  double* zb = vec(K + 3);
+  double* yb = vec(K + 4);
   double* U0 = const_cast<double*>(U.p[0]);
   // a3 seeds: t0 = A v -> U_0, b0 = A t0 - μ d⊙v -> x   (eq:qrec seeds); q̂_0 = [t0; b0]
   if (b < B && gstart % b == 0 && B % b == 0) {
@@ -545,17 +559,23 @@ void toar_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double*
     batch_inputs(V, ldv, b, n, vs_, ws->vid.p, perm, s);
     do_spmv(op, ws, vs_, b, nullptr, nullptr, nullptr, nullptr, s1, b, s);
     do_spmv(op, ws, s1, b, nullptr, nullptr, nullptr, nullptr, s2, b, s);
-    seed_expand(s1, s2, vs_, b, op->degrp(), g1s, ws->vcol.p, B, n, U0, xb, s);
-  } else {
+    seed_expand(s1, s2, vs_, b, op->degrp(), g1s, ws->vcol.p, B, n, U0, xb, s, f32);
+  } else if (!f32) {
     batch_inputs(V, ldv, B, n, ws->Vb.p, ws->vcol.p, perm, s);
     do_spmv(op, ws, ws->Vb.p, B, nullptr, nullptr, nullptr, nullptr, U0, B, s);
     do_spmv(op, ws, U0, B, ws->Vb.p, g0s, g1s, nullptr, xb, B, s);
+  } else {  // fp32: the seeds in double, then rounded once
+    double* t1 = ws->seed32.p;
+    double* t2 = t1 + (n + 1) * B;
+    batch_inputs(V, ldv, B, n, ws->Vb.p, ws->vcol.p, perm, s);
+    do_spmv(op, ws, ws->Vb.p, B, nullptr, nullptr, nullptr, nullptr, t1, B, s);
+    do_spmv(op, ws, t1, B, ws->Vb.p, g0s, g1s, nullptr, t2, B, s);
+    repack_rows_t(t1, false, B, n, B, U0, true, B, 0, s);
+    repack_rows_t(t2, false, B, n, B, xb, true, B, 0, s);
   }
-  if (n_pad > n) {
-    fill(U0 + n * B, B, 0.0, s);
-    fill(xb + n * B, B, 0.0, s);
-    fill(yb + n * B, B, 0.0, s);
-  }
+  zero_rows(U0, n, n_pad);
+  zero_rows(xb, n, n_pad);
+  zero_rows(yb, n, n_pad);
   WL_CUDA(cudaMemsetAsync(ws->H.p, 0, sizeof(double) * B * (K + 1) * K, s));
   const size_t stride = toar_state_doubles(K);
   const int ld = K + 3;
@@ -567,10 +587,12 @@ void toar_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double*
   d.partials = ws->partials.p;
   d.sums_out = ws->sums1.p;
   d.Q = U;
+  d.f32 = f32 ? 1 : 0;
   ToarArgs t{};
   t.U = U;
   t.len = n_pad;
   t.B = B;
+  t.f32 = f32 ? 1 : 0;
   t.coef_y = ws->toar_cy.p;
   t.coef_u = ws->toar_cu.p;
   t.coef_ld = ld;
@@ -602,10 +624,10 @@ void toar_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double*
   // rows are padded to ldg = 4 ceil(B/4) doubles (zero phantom columns), so every gathered row is
   // whole 32-byte pieces for the 256-bit lane loads (spmv.cu): the update pass writes x there
   // directly; the seed's x is repacked once.  (Tiled update passes, K + 1 > 32, keep ld B.)
-  const int64_t ldg = ws->xg.p ? pad_cols(B) : B;
+  const int64_t ldg = ws->xg.p ? (f32 ? pad_cols_t<float>(B) : pad_cols(B)) : B;
   const bool padx = ldg != B && K + 1 <= 32;
   double* xg = padx ? ws->xg.p : xb;
-  if (padx) repack_rows(xb, B, n, B, xg, ldg, s);
+  if (padx) repack_rows_t(xb, f32, B, n, B, xg, f32, ldg, f32 ? pad_vec_t<float>(B) : pad_vec(B), s);
   const double* xin = xg;  // bottom half of the vector the next SpMM applies Z to
   const int64_t ldx_in = padx ? ldg : B;
   const double* zin = U0;  // its top half
@@ -623,7 +645,7 @@ void toar_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double*
     WL_NVTX("arnoldi_step");
     const int m = j + 2;
     // a4: y = A x + μ(μ - d)⊙z  (bottom half of Z [z; x])
-    do_spmv(op, ws, xin, ldx_in, zin, g0z, g1z, nullptr, yb, B, s);
+    do_spmv(op, ws, xin, ldx_in, zin, g0z, g1z, nullptr, yb, B, s, nullptr, f32);
     // a5: one dot pass (Gram row of the newest U vector, U^T y, |y|^2) and one update pass
     d.nq = m - 1;
     d.P = U.p[m - 1];
@@ -706,7 +728,7 @@ void toar_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double*
   if (op->opts.tol > 0.0) krylov_check(ws->kerr.p, B, op->opts.tol, op->kstat.p, s);
   toar_combine_coef(ws->comb.p, B, K, ws->keff.p, ws->toar_state.p, stride, ws->toar_comb.p, s);
   combine(mode, op->lscale, U, kstop + 2, n, B, ws->toar_comb.p, V, ldv, ws->vcol.p, op->c0, op->tprime.p, op->n_theta,
-          ws->tcol.p, out, ldo, perm, s);
+          ws->tcol.p, out, ldo, perm, s, f32);
 }
 
 // μ = 0 (θ = 1) chunks: symmetric Lanczos on A from u = A v (lanczos.cu; "Lanczos (for A = Aᵀ)"):
@@ -843,7 +865,8 @@ void cg_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double* V
 
 void run_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double* V, int64_t ldv, int b, int gstart,
                int B, double* out, int64_t ldo, cudaStream_t s, bool user_order = true) {
-  bool walk = op->opts.reorth == 2 && op->opts.lanczos;  // every column θ = 1 (μ = 0): Lanczos on A
+  // every column θ = 1 (μ = 0): Lanczos on A (double storage; the fp32 mode runs TOAR)
+  bool walk = op->opts.reorth == 2 && op->opts.lanczos && !op->opts.fp32;
   for (int c = 0; c < B && walk; ++c) walk = op->mu[(gstart + c) / b] == 0.0;
   if (op->opts.solver == WL_SOLVER_CG) cg_chunk(op, ws, mode, V, ldv, b, gstart, B, out, ldo, s, user_order);
   else if (walk) lanczos_chunk(op, ws, mode, V, ldv, b, gstart, B, out, ldo, s, user_order);
@@ -905,10 +928,13 @@ void workspace_alloc(wl_workspace* ws, const wl_operator* op, int max_b) {
     ws->toar_cy.alloc((size_t)3 * B);
     ws->toar_cu.alloc((size_t)3 * (K + 3) * B);
     ws->toar_comb.alloc((size_t)(K + 2) * B);
-    if (pad_cols(B) != B) {  // phantom columns stay zero: only columns < B are ever written
-      ws->xg.alloc((size_t)(n + 1) * pad_cols(B));
-      WL_CUDA(cudaMemset(ws->xg.p, 0, sizeof(double) * (n + 1) * pad_cols(B)));
+    if (pad_cols(B) != B || (op->opts.fp32 && pad_cols_t<float>(B) != B)) {  // phantom columns stay zero
+      // rows: n plus the phantom rows of either storage (<= 3); float rows take half the bytes of a double row
+      const size_t dbl = (size_t)(n + 4) * std::max(pad_cols(B), (pad_cols_t<float>(B) + 1) / 2);
+      ws->xg.alloc(dbl);
+      WL_CUDA(cudaMemset(ws->xg.p, 0, sizeof(double) * dbl));
     }
+    if (op->opts.fp32) ws->seed32.alloc((size_t)2 * (n + 1) * B);  // fp64 seeds before rounding to float
     ws->seed.alloc((size_t)3 * (n + 1) * std::max(1, std::min(max_b, kMaxCols)));
     std::vector<int> id(kMaxCols);
     std::iota(id.begin(), id.end(), 0);
@@ -1218,6 +1244,7 @@ void wl_opts_default(wl_opts* o) {
   o->halo_overlap = 1;
   o->lanczos = 1;
   o->krylov_adaptive = 0;
+  o->fp32 = 0;
 }
 
 wl_status wl_partition(int64_t n, const int64_t* row_ptr, int32_t nranks, int64_t* bounds) {
@@ -1295,6 +1322,8 @@ wl_status wl_operator_create(wl_comm* comm, int64_t n_global, int64_t row_begin,
     if (op->opts.solver != WL_SOLVER_KRYLOV && op->opts.solver != WL_SOLVER_CG) throw Error(WL_EINVAL, "unknown solver");
     if (op->opts.reorth < 0 || op->opts.reorth > 2) throw Error(WL_EINVAL, "reorth must be 0, 1 or 2");
     if (!(op->opts.tol >= 0.0)) throw Error(WL_EINVAL, "tol must be >= 0");
+    if (op->opts.fp32 && (op->opts.reorth != 2 || op->opts.solver != WL_SOLVER_KRYLOV))
+      throw Error(WL_EINVAL, "fp32 needs reorth = 2 (TOAR) and the Krylov solver");
     op->kstat.alloc(4);
     WL_CUDA(cudaMemset(op->kstat.p, 0, 4 * sizeof(int)));
     if (op->opts.solver == WL_SOLVER_CG) {
@@ -1627,34 +1656,28 @@ wl_status wl_hessenberg_eigvals(int32_t n, const double* H, double* wr, double* 
 
 namespace wl {
 namespace {
-void cublas_check(cublasStatus_t st, const char* what) {
-  if (st != CUBLAS_STATUS_SUCCESS) throw Error(WL_ECUDA, std::string("cuBLAS: ") + what);
+// Column-major views of the row-major n x cols blocks the engine uses (block.cu): gram: C (p x q, col-major,
+// ld p) = X[:, :p]ᵀ Y[:, :q];  axpy_block: Y[:, :q] = beta Y + alpha X[:, :p] C, C p x q col-major (ld p).
+void gram(wl_workspace* ws, int p, int q, int64_t n, const double* X, int64_t ldx, const double* Y, int64_t ldy,
+          double* C, cudaStream_t s) {
+  ws->trPart.alloc(block_gram_partials(n, p));
+  block_gram(p, q, n, X, ldx, Y, ldy, C, ws->trPart.p, s);
 }
-// Column-major views of the row-major n x cols blocks the engine uses: X (n x cols, ld) is Xᶜ
-// (cols x n, ld).  gram: C (p x q, col-major, ld p) = X[:, :p]ᵀ Y[:, :q].
-void gram(cublasHandle_t h, int p, int q, int64_t n, const double* X, int64_t ldx, const double* Y, int64_t ldy,
-          double* C) {
-  const double one = 1.0, zero = 0.0;
-  cublas_check(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, p, q, (int)n, &one, X, (int)ldx, Y, (int)ldy, &zero, C, p),
-               "gram");
-}
-// Y[:, :q] = beta Y + alpha X[:, :p] C,  C p x q col-major (ld p)
-void axpy_block(cublasHandle_t h, int p, int q, int64_t n, double alpha, const double* X, int64_t ldx,
-                const double* C, double beta, double* Y, int64_t ldy) {
-  cublas_check(cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, q, (int)n, p, &alpha, C, p, X, (int)ldx, &beta, Y, (int)ldy),
-               "update");
+void axpy_block(int p, int q, int64_t n, double alpha, const double* X, int64_t ldx, const double* C, double beta,
+                double* Y, int64_t ldy, cudaStream_t s) {
+  block_axpy(p, q, n, alpha, X, ldx, C, beta, Y, ldy, s);
 }
 
-// dst (ld lddst) R = src (n x m, ld m) by Cholesky QR applied twice (Gram by cuBLAS + allreduce, the
+// dst (ld lddst) R = src (n x m, ld m) by Cholesky QR applied twice (Gram by block.cu + allreduce, the
 // m x m Cholesky and triangular inverse on the host); R (m x m upper, col-major) returned.  W2 is
 // n x m scratch.  Throws WL_ENOCONV when the block is numerically rank deficient.
-void chol_qr2(const wl_operator* op, cublasHandle_t h, const double* src, int m, int64_t n, double* W2, double* Rd,
+void chol_qr2(const wl_operator* op, wl_workspace* ws, const double* src, int m, int64_t n, double* W2, double* Rd,
               double* dst, int64_t lddst, std::vector<double>& R, cudaStream_t s) {
   std::vector<double> Rt((size_t)m * m, 0.0), G((size_t)m * m);
   for (int i = 0; i < m; ++i) Rt[(size_t)i * m + i] = 1.0;
   for (int pass = 0; pass < 2; ++pass) {
     const double* in = pass == 0 ? src : W2;
-    gram(h, m, m, n, in, m, in, m, Rd);
+    gram(ws, m, m, n, in, m, in, m, Rd, s);
     allreduce(op, Rd, (size_t)m * m, s);
     WL_CUDA(cudaMemcpyAsync(G.data(), Rd, sizeof(double) * m * m, cudaMemcpyDeviceToHost, s));
     WL_CUDA(cudaStreamSynchronize(s));
@@ -1679,7 +1702,7 @@ void chol_qr2(const wl_operator* op, cublasHandle_t h, const double* src, int m,
       }
     }
     WL_CUDA(cudaMemcpyAsync(Rd, Ui.data(), sizeof(double) * m * m, cudaMemcpyHostToDevice, s));
-    axpy_block(h, m, m, n, 1.0, in, m, Rd, 0.0, pass == 0 ? W2 : dst, pass == 0 ? m : lddst);
+    axpy_block(m, m, n, 1.0, in, m, Rd, 0.0, pass == 0 ? W2 : dst, pass == 0 ? m : lddst, s);
     std::vector<double> T((size_t)m * m, 0.0);  // Rt <- U Rt
     for (int c = 0; c < m; ++c)
       for (int r = 0; r < m; ++r) {
@@ -1791,16 +1814,13 @@ wl_status wl_xnystrace_exp(const wl_operator* op, int32_t theta_index, int32_t M
     cudaStream_t s = S_(stream);
     const int64_t n = op->n_loc;
     const int P = (k + 1) * M, d = k * M;
-    // buffers and the cuBLAS handle live in the workspace (grown on demand, reused across calls)
+    // buffers live in the workspace (grown on demand, reused across calls)
     DArr<double>&V = ws->trV, &Wb = ws->trW, &W2 = ws->trW2, &Cd = ws->trC, &Rd = ws->trR;
     V.alloc(std::max<int64_t>(1, n) * P);
     Wb.alloc(std::max<int64_t>(1, n) * M);
     W2.alloc(std::max<int64_t>(1, n) * M);
     Cd.alloc((size_t)P * M);
     Rd.alloc((size_t)M * M);
-    if (!ws->cublas) cublas_check(cublasCreate(&ws->cublas), "create");
-    cublas_check(cublasSetStream(ws->cublas, s), "set stream");
-    struct { cublasHandle_t h; } cb{ws->cublas};
     std::vector<double> H((size_t)d * d, 0.0), R0((size_t)M * M), Ch((size_t)P * M), G((size_t)M * M);
     // Ω in internal row order
     if (n > 0) {
@@ -1814,7 +1834,7 @@ wl_status wl_xnystrace_exp(const wl_operator* op, int32_t theta_index, int32_t M
       for (int i = 0; i < M; ++i) Rt[(size_t)i * M + i] = 1.0;
       for (int pass = 0; pass < 2; ++pass) {
         const double* src = pass == 0 ? Wb.p : W2.p;
-        gram(cb.h, M, M, n, src, M, src, M, Rd.p);
+        gram(ws, M, M, n, src, M, src, M, Rd.p, s);
         allreduce(op, Rd.p, (size_t)M * M, s);
         WL_CUDA(cudaMemcpyAsync(G.data(), Rd.p, sizeof(double) * M * M, cudaMemcpyDeviceToHost, s));
         WL_CUDA(cudaStreamSynchronize(s));
@@ -1845,7 +1865,7 @@ wl_status wl_xnystrace_exp(const wl_operator* op, int32_t theta_index, int32_t M
         // out = src U⁻¹  (Uinv is M x M col-major: exactly the "C" operand of axpy_block)
         double* out = pass == 0 ? W2.p : dst;
         const int64_t ldout = pass == 0 ? M : P;
-        axpy_block(cb.h, M, M, n, 1.0, src, M, Rd.p, 0.0, out, ldout);
+        axpy_block(M, M, n, 1.0, src, M, Rd.p, 0.0, out, ldout, s);
         // Rt <- U Rt
         std::vector<double> T((size_t)M * M, 0.0);
         for (int c = 0; c < M; ++c)
@@ -1866,9 +1886,9 @@ wl_status wl_xnystrace_exp(const wl_operator* op, int32_t theta_index, int32_t M
       run_chunk(op, ws, 1, V.p + (size_t)j * M, P, M, theta_index * M, M, Wb.p, M, s, false);
       const int pj = (j + 1) * M;
       for (int pass = 0; pass < 2; ++pass) {  // block classical Gram–Schmidt, twice
-        gram(cb.h, pj, M, n, V.p, P, Wb.p, M, Cd.p);
+        gram(ws, pj, M, n, V.p, P, Wb.p, M, Cd.p, s);
         allreduce(op, Cd.p, (size_t)pj * M, s);
-        axpy_block(cb.h, pj, M, n, -1.0, V.p, P, Cd.p, 1.0, Wb.p, M);
+        axpy_block(pj, M, n, -1.0, V.p, P, Cd.p, 1.0, Wb.p, M, s);
         WL_CUDA(cudaMemcpyAsync(Ch.data(), Cd.p, sizeof(double) * pj * M, cudaMemcpyDeviceToHost, s));
         WL_CUDA(cudaStreamSynchronize(s));
         for (int c = 0; c < M; ++c)
@@ -1952,9 +1972,6 @@ wl_status wl_xnystrace_exp_rational(const wl_operator* op, int32_t theta_index, 
     ws->rkU.alloc((size_t)nn * M + (size_t)nn * 2 * M);
     double* U = ws->rkU.p;
     double* XS = U + nn * M;  // MINRES solution [Re | Im], each n x M
-    if (!ws->cublas) cublas_check(cublasCreate(&ws->cublas), "create");
-    cublas_check(cublasSetStream(ws->cublas, s), "set stream");
-    cublasHandle_t h = ws->cublas;
     // Ω (user order) -> internal order -> V_1 R_0
     if (n > 0) {
       if (op->perm.p) pack_rows(Omega, ldo, op->perm.p, n, M, X.p, s);
@@ -1962,7 +1979,7 @@ wl_status wl_xnystrace_exp_rational(const wl_operator* op, int32_t theta_index, 
                                      cudaMemcpyDeviceToDevice, s));
     }
     std::vector<double> R0;
-    chol_qr2(op, h, X.p, M, n, W2.p, Rd.p, V.p, ldV, R0, s);
+    chol_qr2(op, ws, X.p, M, n, W2.p, Rd.p, V.p, ldV, R0, s);
     const int64_t Dk = Dtot - M;                      // columns of the pencil
     std::vector<double> K((size_t)Dtot * Dk, 0.0), Hm((size_t)Dtot * Dk, 0.0);  // row-major D x Dk
     int64_t D = M, cstart = 0, col = 0, iters = 0;
@@ -1987,15 +2004,15 @@ wl_status wl_xnystrace_exp_rational(const wl_operator* op, int32_t theta_index, 
       // block classical Gram–Schmidt twice against V[:, :D]; h accumulates the coefficients
       std::vector<double> hcoef((size_t)(D + m) * m, 0.0);  // row-major (D + m) x m
       for (int pass = 0; pass < 2; ++pass) {
-        gram(h, (int)D, m, n, V.p, ldV, X.p, m, Cd.p);
+        gram(ws, (int)D, m, n, V.p, ldV, X.p, m, Cd.p, s);
         allreduce(op, Cd.p, (size_t)D * m, s);
-        axpy_block(h, (int)D, m, n, -1.0, V.p, ldV, Cd.p, 1.0, X.p, m);
+        axpy_block((int)D, m, n, -1.0, V.p, ldV, Cd.p, 1.0, X.p, m, s);
         WL_CUDA(cudaMemcpyAsync(Ch.data(), Cd.p, sizeof(double) * D * m, cudaMemcpyDeviceToHost, s));
         WL_CUDA(cudaStreamSynchronize(s));
         for (int c = 0; c < m; ++c)
           for (int64_t r = 0; r < D; ++r) hcoef[(size_t)r * m + c] += Ch[(size_t)c * D + r];
       }
-      chol_qr2(op, h, X.p, m, n, W2.p, Rd.p, V.p + D, ldV, Rj, s);
+      chol_qr2(op, ws, X.p, m, n, W2.p, Rd.p, V.p + D, ldV, Rj, s);
       if (getenv("WL_DEBUG_RATIONAL")) {
         double hmax = 0.0, rmin = INFINITY;
         for (double v : hcoef) hmax = std::max(hmax, std::fabs(v));
@@ -2039,7 +2056,7 @@ wl_status wl_xnystrace_exp_rational(const wl_operator* op, int32_t theta_index, 
     for (int j0 = 0; j0 < d; j0 += M) {
       repack_rows(V.p + j0, ldV, n, M, U, M, s);
       run_chunk(op, ws, 1, U, M, M, theta_index * M, M, X.p, M, s, false);  // 𝔏 V[:, j0 : j0 + M]
-      gram(h, d, M, n, V.p, ldV, X.p, M, Cd.p);
+      gram(ws, d, M, n, V.p, ldV, X.p, M, Cd.p, s);
       allreduce(op, Cd.p, (size_t)d * M, s);
       WL_CUDA(cudaMemcpyAsync(Ch.data(), Cd.p, sizeof(double) * d * M, cudaMemcpyDeviceToHost, s));
       WL_CUDA(cudaStreamSynchronize(s));

@@ -22,8 +22,9 @@ __global__ void batch_inputs_kernel(const double* V, int64_t ldv, int B, int64_t
 // Seeds shared by the θ columns of one input column (TOAR path): s1 = A v and s2 = A(Av) are
 // θ-independent, so they are computed once per input column (n x b) and expanded to the B Krylov
 // columns: t0[r][c] = s1[r][vcol c],  b0[r][c] = s2[r][vcol c] - μ_c d_r v[r][vcol c]  (eq:qrec seeds).
+template <class T>
 __global__ void seed_expand_kernel(const double* s1, const double* s2, const double* v, int b, const int32_t* rowptr,
-                                   const double* g1s, const int* vcol, int B, int64_t n, double* t0, double* b0) {
+                                   const double* g1s, const int* vcol, int B, int64_t n, T* t0, T* b0) {
   const int64_t total = n * B;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -31,15 +32,15 @@ __global__ void seed_expand_kernel(const double* s1, const double* s2, const dou
     const int c = (int)(e - r * B);
     const int64_t src = r * b + vcol[c];
     const double d = (double)(__ldg(rowptr + r + 1) - __ldg(rowptr + r));
-    t0[e] = s1[src];
-    b0[e] = s2[src] + g1s[c] * d * v[src];  // g1s = -μ
+    t0[e] = (T)s1[src];
+    b0[e] = (T)(s2[src] + g1s[c] * d * v[src]);  // g1s = -μ
   }
 }
 
 // mode 0: out = c0 V + Σ_i comb_i Q_i          (φ V, top half of the Z basis)
 // mode 1: out = t' ⊙ V - Σ_i comb_i Q_i        (𝕃 V = diag(t)V - φV, c_0 cancels)
 // mode 2: out = Σ_i comb_i Q_i                 (t' = φ1 - c_0 1 for V = 1)
-template <int NV>
+template <int NV, class T>
 __global__ void combine_kernel(int mode, double lscale, const VecPtrs Q, int nvec, int64_t n, int B,
                                const double* comb, const double* V, int64_t ldv, const int* vcol,
                                double c0, const double* tprime, int64_t ldt, const int* tcol,
@@ -55,7 +56,7 @@ __global__ void combine_kernel(int mode, double lscale, const VecPtrs Q, int nve
     double acc = 0.0;
 #pragma unroll 8
     for (int i = 0; i < NV; ++i)
-      if (i < nvec) acc += s_comb[i * B + c] * __ldg(Q.p[i] + e);
+      if (i < nvec) acc += s_comb[i * B + c] * (double)__ldg(reinterpret_cast<const T*>(Q.p[i]) + e);
     double o;
     const int64_t ru = perm ? perm[r] : r;  // user row of internal row r
     if (mode == 2) {
@@ -69,8 +70,8 @@ __global__ void combine_kernel(int mode, double lscale, const VecPtrs Q, int nve
   }
 }
 
-__global__ void pack_rows_kernel(const double* src, int64_t lds, const int32_t* idx, int64_t cnt, int B,
-                                 double* dst) {
+template <class T>
+__global__ void pack_rows_kernel(const T* src, int64_t lds, const int32_t* idx, int64_t cnt, int B, T* dst) {
   const int64_t total = cnt * B;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -273,9 +274,13 @@ void batch_inputs(const double* V, int64_t ldv, int B, int64_t n, double* Vb, co
 }
 
 void seed_expand(const double* s1, const double* s2, const double* v, int b, const int32_t* rowptr, const double* g1s,
-                 const int* vcol, int B, int64_t n, double* t0, double* b0, cudaStream_t s) {
+                 const int* vcol, int B, int64_t n, double* t0, double* b0, cudaStream_t s, bool f32) {
   WL_LAUNCH("batch_inputs");
-  seed_expand_kernel<<<grid_for(n * B), 256, 0, s>>>(s1, s2, v, b, rowptr, g1s, vcol, B, n, t0, b0);
+  if (f32)
+    seed_expand_kernel<float><<<grid_for(n * B), 256, 0, s>>>(s1, s2, v, b, rowptr, g1s, vcol, B, n,
+                                                              reinterpret_cast<float*>(t0), reinterpret_cast<float*>(b0));
+  else
+    seed_expand_kernel<double><<<grid_for(n * B), 256, 0, s>>>(s1, s2, v, b, rowptr, g1s, vcol, B, n, t0, b0);
   WL_CUDA(cudaGetLastError());
 }
 
@@ -289,24 +294,33 @@ void setup_chunk(const double* mu, int gstart, int b, int B, double* g0z, double
 void combine(int mode, double lscale, const VecPtrs& Q, int nvec, int64_t n, int B,
                  const double* comb, const double* V, int64_t ldv, const int* vcol, double c0,
                  const double* tprime, int64_t ldt, const int* tcol, double* out, int64_t ldo,
-                 const int32_t* perm, cudaStream_t s) {
+                 const int32_t* perm, cudaStream_t s, bool f32) {
   WL_LAUNCH("combine");
   const int g = grid_for(n * B);
-  if (nvec <= 16)
-    combine_kernel<16><<<g, 256, 0, s>>>(mode, lscale, Q, nvec, n, B, comb, V, ldv, vcol, c0, tprime, ldt, tcol, out, ldo, perm);
-  else if (nvec <= 32)
-    combine_kernel<32><<<g, 256, 0, s>>>(mode, lscale, Q, nvec, n, B, comb, V, ldv, vcol, c0, tprime, ldt, tcol, out, ldo, perm);
-  else
-    combine_kernel<kMaxKrylov + 2><<<g, 256, 0, s>>>(mode, lscale, Q, nvec, n, B, comb, V, ldv, vcol, c0, tprime, ldt, tcol, out, ldo, perm);
+#define WL_COMBINE(NV, T) \
+  combine_kernel<NV, T><<<g, 256, 0, s>>>(mode, lscale, Q, nvec, n, B, comb, V, ldv, vcol, c0, tprime, ldt, tcol, out, ldo, perm)
+  if (f32) {
+    if (nvec <= 16) WL_COMBINE(16, float);
+    else if (nvec <= 32) WL_COMBINE(32, float);
+    else WL_COMBINE(kMaxKrylov + 2, float);
+  } else {
+    if (nvec <= 16) WL_COMBINE(16, double);
+    else if (nvec <= 32) WL_COMBINE(32, double);
+    else WL_COMBINE(kMaxKrylov + 2, double);
+  }
+#undef WL_COMBINE
   WL_CUDA(cudaGetLastError());
 }
 
 namespace {
-__global__ void repack_rows_kernel(const double* src, int64_t lds, int64_t n, int B, double* dst, int64_t ldd) {
+template <class Ti, class To>
+__global__ void repack_rows_kernel(const Ti* src, int64_t lds, int64_t n, int B, To* dst, int64_t ldd, int zpad) {
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n * B; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = e / B;
     const int c = (int)(e - r * B);
-    dst[r * ldd + c] = src[r * lds + c];
+    dst[r * ldd + c] = (To)src[r * lds + c];
+    if (c == B - 1)
+      for (int cc = B; cc < zpad; ++cc) dst[r * ldd + cc] = To(0);
   }
 }
 }  // namespace
@@ -314,7 +328,23 @@ __global__ void repack_rows_kernel(const double* src, int64_t lds, int64_t n, in
 void repack_rows(const double* src, int64_t lds, int64_t n, int B, double* dst, int64_t ldd, cudaStream_t s) {
   if (n <= 0) return;
   WL_LAUNCH("repack_rows");
-  repack_rows_kernel<<<grid_for(n * B), 256, 0, s>>>(src, lds, n, B, dst, ldd);
+  repack_rows_kernel<double, double><<<grid_for(n * B), 256, 0, s>>>(src, lds, n, B, dst, ldd, 0);
+  WL_CUDA(cudaGetLastError());
+}
+
+void repack_rows_t(const void* src, bool src_f32, int64_t lds, int64_t n, int B, void* dst, bool dst_f32, int64_t ldd,
+                   int zpad, cudaStream_t s) {
+  if (n <= 0) return;
+  WL_LAUNCH("repack_rows");
+  const int g = grid_for(n * B);
+  if (src_f32 && dst_f32)
+    repack_rows_kernel<float, float><<<g, 256, 0, s>>>((const float*)src, lds, n, B, (float*)dst, ldd, zpad);
+  else if (!src_f32 && dst_f32)
+    repack_rows_kernel<double, float><<<g, 256, 0, s>>>((const double*)src, lds, n, B, (float*)dst, ldd, zpad);
+  else if (!src_f32 && !dst_f32)
+    repack_rows_kernel<double, double><<<g, 256, 0, s>>>((const double*)src, lds, n, B, (double*)dst, ldd, zpad);
+  else
+    throw Error(1, "repack_rows_t: float -> double not used");
   WL_CUDA(cudaGetLastError());
 }
 
@@ -329,7 +359,14 @@ void pack_rows(const double* src, int64_t lds, const int32_t* idx, int64_t cnt, 
                cudaStream_t s) {
   if (cnt <= 0) return;
   WL_LAUNCH("pack_rows");
-  pack_rows_kernel<<<grid_for(cnt * B), 256, 0, s>>>(src, lds, idx, cnt, B, dst);
+  pack_rows_kernel<double><<<grid_for(cnt * B), 256, 0, s>>>(src, lds, idx, cnt, B, dst);
+  WL_CUDA(cudaGetLastError());
+}
+
+void pack_rows_f32(const float* src, int64_t lds, const int32_t* idx, int64_t cnt, int B, float* dst, cudaStream_t s) {
+  if (cnt <= 0) return;
+  WL_LAUNCH("pack_rows");
+  pack_rows_kernel<float><<<grid_for(cnt * B), 256, 0, s>>>(src, lds, idx, cnt, B, dst);
   WL_CUDA(cudaGetLastError());
 }
 

@@ -30,6 +30,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
+#include <type_traits>
 
 // compile-time tuning knobs (tools/build_variants.sh): wide-lane unroll, min CTAs per SM of the rows kernel
 #ifndef WL_SPMV_UW
@@ -41,6 +42,13 @@
 #ifndef WL_SPMV_MINB_S
 #define WL_SPMV_MINB_S 3
 #endif
+// fp32 storage (8-float lanes): unroll and min CTAs per SM of the row kernel
+#ifndef WL_SPMV_UW_F
+#define WL_SPMV_UW_F 4
+#endif
+#ifndef WL_SPMV_MINB_F
+#define WL_SPMV_MINB_F 4
+#endif
 
 namespace wl {
 namespace {
@@ -48,37 +56,51 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 
-template <int VW>
+// VW values of the storage type T (double; float in the fp32 mode) — sums are always accumulated in double
+template <int VW, class T = double>
 struct Vec {
-  double v[VW];
+  T v[VW];
 };
 
-template <int VW>
-__device__ __forceinline__ Vec<VW> vzero() {
-  Vec<VW> r;
+template <int VW, class T = double>
+__device__ __forceinline__ Vec<VW, T> vzero() {
+  Vec<VW, T> r;
 #pragma unroll
-  for (int k = 0; k < VW; ++k) r.v[k] = 0.0;
+  for (int k = 0; k < VW; ++k) r.v[k] = T(0);
   return r;
 }
+template <int VW, class T>
+__device__ __forceinline__ void vadd(Vec<VW>& a, const Vec<VW, T>& b) {
+#pragma unroll
+  for (int k = 0; k < VW; ++k) a.v[k] += (double)b.v[k];
+}
 template <int VW>
-__device__ __forceinline__ void vadd(Vec<VW>& a, const Vec<VW>& b) {
+__device__ __forceinline__ void vaddf(Vec<VW, float>& a, const Vec<VW, float>& b) {
 #pragma unroll
   for (int k = 0; k < VW; ++k) a.v[k] += b.v[k];
 }
-// read-only (non-coherent) load of VW consecutive doubles, VW-aligned
-template <int VW>
-__device__ __forceinline__ Vec<VW> vload(const double* p) {
-  Vec<VW> r;
+// read-only (non-coherent) load of VW consecutive values, VW-aligned (32 bytes at most: the 256-bit LDG)
+template <int VW, class T>
+__device__ __forceinline__ Vec<VW, T> vload(const T* p) {
+  Vec<VW, T> r;
   if constexpr (VW == 1) {
     r.v[0] = __ldg(p);
-  } else if constexpr (VW == 2) {
-    const double2 t = __ldg(reinterpret_cast<const double2*>(p));
-    r.v[0] = t.x;
-    r.v[1] = t.y;
+  } else if constexpr (std::is_same<T, double>::value) {
+    if constexpr (VW == 2) {
+      const double2 t = __ldg(reinterpret_cast<const double2*>(p));
+      r.v[0] = t.x;
+      r.v[1] = t.y;
+    } else {
+      static_assert(VW == 4, "double: VW in {1, 2, 4}");
+      asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+          : "=d"(r.v[0]), "=d"(r.v[1]), "=d"(r.v[2]), "=d"(r.v[3])
+          : "l"(p));
+    }
   } else {
-    static_assert(VW == 4, "VW in {1, 2, 4}");
-    asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
-        : "=d"(r.v[0]), "=d"(r.v[1]), "=d"(r.v[2]), "=d"(r.v[3])
+    static_assert(VW == 8, "float: VW in {1, 8}");
+    asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]), "=f"(r.v[5]), "=f"(r.v[6]),
+          "=f"(r.v[7])
         : "l"(p));
   }
   return r;
@@ -110,19 +132,20 @@ __device__ __forceinline__ int ld_col_hint(const int32_t* p, uint64_t pol) {
 // columns c0 = w*VW .. c0+VW-1 (those < B are real).  Offsets are 32-bit (n_loc * ld < 2^31 is
 // checked on the host); the halo select exists only in the HALO instantiation, and only the last
 // round of a range is predicated.
-template <int kU, bool HALO, int VW, bool HINT = false>
+template <int kU, bool HALO, int VW, bool HINT = false, class T = double>
 struct Ctx {
+  static_assert(!HINT || std::is_same<T, double>::value, "L2 hints: double storage only");
   const SpmvArgs& a;
   uint64_t pol_last = 0, pol_first = 0;  // HINT: L2 policies
   int c0;             // first column of this lane
   int nc;             // real columns of this lane (0..VW)
-  const double* yc;   // y + c0
-  const double* yhc;  // yh + c0
+  const T* yc;        // y + c0
+  const T* yhc;       // yh + c0
   int ldy, ldh;
   __device__ Ctx(const SpmvArgs& args, int col0) : a(args), c0(col0) {
     nc = max(0, min(VW, a.B - c0));
-    yc = a.y + c0;
-    yhc = a.yh + c0;
+    yc = reinterpret_cast<const T*>(a.y) + c0;
+    yhc = reinterpret_cast<const T*>(a.yh) + c0;
     ldy = (int)a.ldy;
     ldh = (int)a.ldh;
     if (HINT) {
@@ -130,13 +153,14 @@ struct Ctx {
       asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
     }
   }
-  __device__ Vec<VW> gather(int cl) const {
-    if (HALO && cl >= a.n_loc) {
-      if (HINT) return vload_hint<VW>(yhc + (cl - a.n_loc) * ldh, pol_first);
-      return vload<VW>(yhc + (cl - a.n_loc) * ldh);
+  __device__ Vec<VW, T> gather(int cl) const {
+    if constexpr (HINT) {
+      if (HALO && cl >= a.n_loc) return vload_hint<VW>(yhc + (cl - a.n_loc) * ldh, pol_first);
+      return vload_hint<VW>(yc + cl * ldy, cl < a.hot_rows ? pol_last : pol_first);
+    } else {
+      if (HALO && cl >= a.n_loc) return vload<VW>(yhc + (cl - a.n_loc) * ldh);
+      return vload<VW>(yc + cl * ldy);
     }
-    if (HINT) return vload_hint<VW>(yc + cl * ldy, cl < a.hot_rows ? pol_last : pol_first);
-    return vload<VW>(yc + cl * ldy);
   }
   __device__ int col(int z) const {
     if (HINT) return ld_col_hint(a.col + z, pol_first);
@@ -148,17 +172,17 @@ struct Ctx {
   __device__ void write(int r, int deg, const Vec<VW>& sum, const double* xrow = nullptr) const {
     const int ro = a.out_row ? __ldg(a.out_row + r) : r;
     if (a.x && a.degptr) deg = __ldg(a.degptr + ro + 1) - __ldg(a.degptr + ro);
-    double* dst = a.out + (int64_t)ro * a.ldo + c0;
-    const double* xs = xrow ? xrow : a.x + (int64_t)ro * a.ldx + c0;
+    T* dst = reinterpret_cast<T*>(a.out) + (int64_t)ro * a.ldo + c0;
+    const T* xs = xrow ? reinterpret_cast<const T*>(xrow) : reinterpret_cast<const T*>(a.x) + (int64_t)ro * a.ldx + c0;
     // per-column constants are read here (L1-resident, B values) rather than held in registers
 #pragma unroll
     for (int k = 0; k < VW; ++k) {
       if (k < nc) {
         const int c = c0 + k;
         double o = sum.v[k];
-        if (a.x) o += ((a.g0 ? __ldg(a.g0 + c) : 0.0) + (a.g1 ? __ldg(a.g1 + c) : 0.0) * (double)deg) * xs[k];
+        if (a.x) o += ((a.g0 ? __ldg(a.g0 + c) : 0.0) + (a.g1 ? __ldg(a.g1 + c) : 0.0) * (double)deg) * (double)xs[k];
         const double sc = a.scale ? __ldg(a.scale + c) : 1.0;
-        dst[k] = a.accumulate ? dst[k] + sc * o : sc * o;
+        dst[k] = (T)(a.accumulate ? (double)dst[k] + sc * o : sc * o);
       }
     }
   }
@@ -172,24 +196,35 @@ struct Ctx {
       int cl[kU];
 #pragma unroll
       for (int u = 0; u < kU; ++u) cl[u] = col(base + first + u * step);
-      Vec<VW> v[kU];
+      Vec<VW, T> v[kU];
 #pragma unroll
       for (int u = 0; u < kU; ++u) v[u] = gather(cl[u]);
-#pragma unroll
-      for (int u = 0; u < kU; ++u) vadd(acc, v[u]);
+      add_round(acc, v);
     }
     const int z = base + first;
     if (base < z1) {  // predicated tail round
       int cl[kU];
 #pragma unroll
       for (int u = 0; u < kU; ++u) cl[u] = (z + u * step < z1) ? col(z + u * step) : -1;
-      Vec<VW> v[kU];
+      Vec<VW, T> v[kU];
 #pragma unroll
-      for (int u = 0; u < kU; ++u) v[u] = cl[u] >= 0 ? gather(cl[u]) : vzero<VW>();
-#pragma unroll
-      for (int u = 0; u < kU; ++u) vadd(acc, v[u]);
+      for (int u = 0; u < kU; ++u) v[u] = cl[u] >= 0 ? gather(cl[u]) : vzero<VW, T>();
+      add_round(acc, v);
     }
     return acc;
+  }
+  // one round of kU gathered rows into the double accumulator; fp32 storage sums the round in float first
+  // (one conversion per round instead of per row: its rounding is that of the stored values)
+  __device__ static void add_round(Vec<VW>& acc, const Vec<VW, T> (&v)[kU]) {
+    if constexpr (std::is_same<T, double>::value) {
+#pragma unroll
+      for (int u = 0; u < kU; ++u) vadd(acc, v[u]);
+    } else {
+      Vec<VW, T> r = v[0];
+#pragma unroll
+      for (int u = 1; u < kU; ++u) vaddf(r, v[u]);
+      vadd(acc, r);
+    }
   }
 };
 
@@ -214,15 +249,16 @@ __device__ inline Vec<VW> group_reduce(Vec<VW> v, int W, int gpw) {
 template <int VW>
 __device__ __forceinline__ int lanes_per_row(int B) { return (B + VW - 1) / VW; }
 
-template <int kU, bool HALO, int VW, bool HINT>
-__global__ void __launch_bounds__(kThreads, VW == 1 ? 1 : WL_SPMV_MINB) spmv_binned_kernel(SpmvArgs a) {
+template <int kU, bool HALO, int VW, bool HINT, class T>
+__global__ void __launch_bounds__(kThreads, VW == 1 ? 1 : (sizeof(T) == 4 ? WL_SPMV_MINB_F : WL_SPMV_MINB))
+    spmv_binned_kernel(SpmvArgs a) {
   if (a.active && *a.active == 0) return;
   const int W = lanes_per_row<VW>(a.B);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int gpw = 32 / W;
   const int gi = lane / W, w = lane - gi * W;
   const bool lane_ok = gi < gpw;
-  const Ctx<kU, HALO, VW, HINT> ctx(a, lane_ok ? w * VW : 0);
+  const Ctx<kU, HALO, VW, HINT, T> ctx(a, lane_ok ? w * VW : 0);
   int blk = blockIdx.x;
   if (blk < a.nblk_small) {  // ---- small rows: one lane group per row
     const int idx = (blk * kWarps + warp) * gpw + gi;
@@ -316,7 +352,7 @@ __global__ void __launch_bounds__(kThreads, VW == 1 ? 1 : WL_SPMV_MINB) spmv_bin
 // are software-pipelined (round r+1's gathers issue before round r is summed): 39.7 -> 32.0 ms/step
 // on C4 at VW = 1.
 template <int kU, bool HALO, int VW, bool HINT>
-__global__ void __launch_bounds__(kThreads, WL_SPMV_MINB_S) spmv_small_batched_kernel(SpmvArgs a) {
+__global__ void __launch_bounds__(kThreads, WL_SPMV_MINB_S) spmv_small_batched_kernel(SpmvArgs a) {  // double storage
   if (a.active && *a.active == 0) return;
   extern __shared__ __align__(16) int s_small[];
   constexpr int kColCap = 32 * kSmallMax;  // max nonzeros of a 32-row batch
@@ -391,12 +427,12 @@ __global__ void __launch_bounds__(kThreads, WL_SPMV_MINB_S) spmv_small_batched_k
 // At B = 1 a 32-row batch is one row per lane, so the batched kernel's staging buys nothing and its
 // per-batch chain (rowptr -> col -> smem -> gather) plus warp syncs dominates.  A thread per row
 // keeps the same three dependent loads with ~8x the rows in flight per SM.
-template <bool HALO, bool HINT>
+template <bool HALO, bool HINT, class T>
 __global__ void __launch_bounds__(kThreads) spmv_small_row1_kernel(SpmvArgs a) {
   if (a.active && *a.active == 0) return;
   const int i = blockIdx.x * kThreads + threadIdx.x;
   if (i >= a.n_small) return;
-  const Ctx<4, HALO, 1, HINT> ctx(a, 0);
+  const Ctx<4, HALO, 1, HINT, T> ctx(a, 0);
   const int r = a.small_first + i;
   const int z0 = __ldg(a.rowptr + r), z1 = __ldg(a.rowptr + r + 1);
   ctx.write(r, z1 - z0, ctx.strided_sum(z0, z1, 0, 1));
@@ -405,6 +441,7 @@ __global__ void __launch_bounds__(kThreads) spmv_small_row1_kernel(SpmvArgs a) {
 // ---- rows without nonzeros at the end of the contiguous small range (isolated vertices: 40% of C4's ids):
 // out = scale ⊙ (g0 + g1 d) ⊙ x, a stream over the n_iso x B block (d = 0 unless degptr gives the full degree
 // of a split operator's local part)
+template <class T>
 __global__ void __launch_bounds__(kThreads) spmv_iso_kernel(SpmvArgs a, int r0) {
   if (a.active && *a.active == 0) return;
   const int B = a.B;
@@ -416,9 +453,10 @@ __global__ void __launch_bounds__(kThreads) spmv_iso_kernel(SpmvArgs a, int r0) 
     double o = 0.0;
     if (a.x) {
       const double d = a.degptr ? (double)(__ldg(a.degptr + r + 1) - __ldg(a.degptr + r)) : 0.0;
-      o = ((a.g0 ? __ldg(a.g0 + c) : 0.0) + (a.g1 ? __ldg(a.g1 + c) : 0.0) * d) * __ldg(a.x + r * a.ldx + c);
+      o = ((a.g0 ? __ldg(a.g0 + c) : 0.0) + (a.g1 ? __ldg(a.g1 + c) : 0.0) * d) *
+          (double)__ldg(reinterpret_cast<const T*>(a.x) + r * a.ldx + c);
     }
-    a.out[r * a.ldo + c] = (a.scale ? __ldg(a.scale + c) : 1.0) * o;
+    reinterpret_cast<T*>(a.out)[r * a.ldo + c] = (T)((a.scale ? __ldg(a.scale + c) : 1.0) * o);
   }
 }
 
@@ -427,16 +465,17 @@ size_t small_batched_smem(int B) {
 }
 
 template <int VW>
-constexpr int unroll_for() { return VW == 1 ? 8 : WL_SPMV_UW; }  // wide lanes: 4 rounds in flight
+constexpr int unroll_for() { return VW == 1 ? 8 : VW == 8 ? WL_SPMV_UW_F : WL_SPMV_UW; }  // wide lanes: 4 rounds in flight
 template <int VW>
 constexpr int unroll_batched() { return VW == 1 ? 8 : VW == 2 ? 4 : 2; }  // pipelined: 2 rounds live
 
 // launch the batched small rows (if any) and the binned kernel (small rows by id list, medium, hub)
-template <int VW, bool HINT>
+template <int VW, bool HINT, class T>
 void launch_vw(const SpmvArgs& a, bool halo, bool batched, int grid_rest, cudaStream_t s) {
   constexpr int kU = unroll_for<VW>(), kUb = unroll_batched<VW>();
   static const bool split = getenv("WL_SPMV_SPLIT") != nullptr;  // per-class timing (profiling only)
   SpmvArgs t = a;
+  if constexpr (std::is_same<T, double>::value) {  // the batched staging is double only
   if (batched) {
     LaunchScope ls(split ? "spmv_small_batched" : nullptr, s);
     auto kern = halo ? spmv_small_batched_kernel<kUb, true, VW, HINT> : spmv_small_batched_kernel<kUb, false, VW, HINT>;
@@ -455,17 +494,23 @@ void launch_vw(const SpmvArgs& a, bool halo, bool batched, int grid_rest, cudaSt
     t.n_small = 0;
     t.nblk_small = 0;
   }
+  }
   if (grid_rest <= 0) return;
   LaunchScope ls(split ? "spmv_rows" : nullptr, s);
-  if (halo) spmv_binned_kernel<kU, true, VW, HINT><<<grid_rest, kThreads, 0, s>>>(t);
-  else spmv_binned_kernel<kU, false, VW, HINT><<<grid_rest, kThreads, 0, s>>>(t);
+  if (halo) spmv_binned_kernel<kU, true, VW, HINT, T><<<grid_rest, kThreads, 0, s>>>(t);
+  else spmv_binned_kernel<kU, false, VW, HINT, T><<<grid_rest, kThreads, 0, s>>>(t);
   WL_CUDA(cudaGetLastError());
 }
 
-template <int VW>
+template <int VW, class T = double>
 void launch_vw(const SpmvArgs& a, bool halo, bool batched, int grid_rest, cudaStream_t s) {
-  if (a.hot_rows > 0) launch_vw<VW, true>(a, halo, batched, grid_rest, s);
-  else launch_vw<VW, false>(a, halo, batched, grid_rest, s);
+  if constexpr (std::is_same<T, double>::value) {
+    if (a.hot_rows > 0) {
+      launch_vw<VW, true, T>(a, halo, batched, grid_rest, s);
+      return;
+    }
+  }
+  launch_vw<VW, false, T>(a, halo, batched, grid_rest, s);
 }
 
 inline bool aligned(const void* p, int bytes) { return (reinterpret_cast<uintptr_t>(p) % bytes) == 0; }
@@ -476,6 +521,10 @@ inline bool aligned(const void* p, int bytes) { return (reinterpret_cast<uintptr
 int spmv_vector_width(const SpmvArgs& a) {
   if (a.B == 1) return 1;
   const bool halo = a.yh != nullptr;
+  if (a.f32) {  // fp32 storage: 32-byte lanes of 8 floats or scalar lanes
+    const int vw = 8;
+    return (a.ldy % vw == 0 && aligned(a.y, 4 * vw) && (!halo || (a.ldh % vw == 0 && aligned(a.yh, 4 * vw)))) ? vw : 1;
+  }
   for (int vw : {4, 2}) {
     if (a.ldy % vw == 0 && aligned(a.y, 8 * vw) && (!halo || (a.ldh % vw == 0 && aligned(a.yh, 8 * vw)))) return vw;
   }
@@ -490,7 +539,8 @@ void spmv(const SpmvArgs& a0, cudaStream_t s) {
     const int r0 = a.small_first + a.n_small - a.n_iso;
     const int g = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)a.n_iso * a.B + kThreads - 1) / kThreads,
                                                             (int64_t)num_sms() * 8));
-    spmv_iso_kernel<<<g, kThreads, 0, s>>>(a, r0);
+    if (a.f32) spmv_iso_kernel<float><<<g, kThreads, 0, s>>>(a, r0);
+    else spmv_iso_kernel<double><<<g, kThreads, 0, s>>>(a, r0);
     WL_CUDA(cudaGetLastError());
     a.n_small -= a.n_iso;
     a.n_iso = 0;
@@ -499,11 +549,12 @@ void spmv(const SpmvArgs& a0, cudaStream_t s) {
   // L2 eviction hints: rows [0, hot_rows) of the degree-sorted gathered block (the most gathered
   // rows) stay, column ids and cold rows go first.  Budget WL_SPMV_HOT_MB of L2 (0 = no hints).
   static const double hot_mb = [] { const char* v = getenv("WL_SPMV_HOT_MB"); return v ? atof(v) : 0.0; }();
-  if (hot_mb > 0.0 && a.hot_rows == 0)
+  if (a.f32) a.hot_rows = 0;
+  else if (hot_mb > 0.0 && a.hot_rows == 0)
     a.hot_rows = (int)std::min<int64_t>(a.n_loc, (int64_t)(hot_mb * 1e6 / (8.0 * a.ldy)));
   static const int vw_cap = [] { const char* v = getenv("WL_SPMV_VW"); return v ? atoi(v) : 4; }();
   int VW = spmv_vector_width(a);
-  while (VW > vw_cap) VW /= 2;
+  if (a.f32 ? (VW > 2 * vw_cap) : (VW > vw_cap)) VW = a.f32 ? 1 : vw_cap;  // fp32: 8 or 1
   const int W = (a.B + VW - 1) / VW;
   const int gpw = 32 / W;
   a.nblk_small = (a.n_small + kWarps * gpw - 1) / (kWarps * gpw);
@@ -511,7 +562,9 @@ void spmv(const SpmvArgs& a0, cudaStream_t s) {
   static const int med_sub = [] { const char* v = getenv("WL_SPMV_MEDSUB"); return v ? atoi(v) : 4; }();
   a.med_sub = (W == 1 && (med_sub == 4 || med_sub == 8 || med_sub == 16)) ? med_sub : 0;
   // wide rows (W > 1): medium rows per warp (WL_SPMV_MEDRPW; 1 = a warp per row)
-  static const int med_rpw = [] { const char* v = getenv("WL_SPMV_MEDRPW"); return v ? atoi(v) : 5; }();
+  // (defaults measured on C4: 5 with double rows of 3 lanes, 8 with float rows of 2 lanes)
+  static const int med_rpw_env = [] { const char* v = getenv("WL_SPMV_MEDRPW"); return v ? atoi(v) : 0; }();
+  const int med_rpw = med_rpw_env ? med_rpw_env : (a.f32 ? 8 : 5);
   a.med_rpw = (W > 1 && med_rpw > 1 && gpw / med_rpw >= 1) ? med_rpw : 1;
   const int rows_per_warp = a.med_sub ? 32 / a.med_sub : a.med_rpw;
   a.nblk_medium = (a.n_medium + kWarps * rows_per_warp - 1) / (kWarps * rows_per_warp);
@@ -528,20 +581,25 @@ void spmv(const SpmvArgs& a0, cudaStream_t s) {
       static const bool split = getenv("WL_SPMV_SPLIT") != nullptr;
       LaunchScope ls(split ? "spmv_small_row1" : nullptr, s);
       const int g = (a.n_small + kThreads - 1) / kThreads;
-      if (a.hot_rows > 0) {
-        if (halo) spmv_small_row1_kernel<true, true><<<g, kThreads, 0, s>>>(a);
-        else spmv_small_row1_kernel<false, true><<<g, kThreads, 0, s>>>(a);
+      if (a.f32) {
+        if (halo) spmv_small_row1_kernel<true, false, float><<<g, kThreads, 0, s>>>(a);
+        else spmv_small_row1_kernel<false, false, float><<<g, kThreads, 0, s>>>(a);
+      } else if (a.hot_rows > 0) {
+        if (halo) spmv_small_row1_kernel<true, true, double><<<g, kThreads, 0, s>>>(a);
+        else spmv_small_row1_kernel<false, true, double><<<g, kThreads, 0, s>>>(a);
       } else {
-        if (halo) spmv_small_row1_kernel<true, false><<<g, kThreads, 0, s>>>(a);
-        else spmv_small_row1_kernel<false, false><<<g, kThreads, 0, s>>>(a);
+        if (halo) spmv_small_row1_kernel<true, false, double><<<g, kThreads, 0, s>>>(a);
+        else spmv_small_row1_kernel<false, false, double><<<g, kThreads, 0, s>>>(a);
       }
       WL_CUDA(cudaGetLastError());
       SpmvArgs t = a;
       t.n_small = 0;
       t.nblk_small = 0;
-      launch_vw<1>(t, halo, false, grid - a.nblk_small, s);
+      if (a.f32) launch_vw<1, float>(t, halo, false, grid - a.nblk_small, s);
+      else launch_vw<1>(t, halo, false, grid - a.nblk_small, s);
     } else {
-      launch_vw<1>(a, halo, false, grid, s);
+      if (a.f32) launch_vw<1, float>(a, halo, false, grid, s);
+      else launch_vw<1>(a, halo, false, grid, s);
     }
     return;
   }
@@ -549,8 +607,13 @@ void spmv(const SpmvArgs& a0, cudaStream_t s) {
   static const bool batched_on = [] { const char* v = getenv("WL_SPMV_BATCHED"); return v ? atoi(v) != 0 : true; }();
   // with 8-byte lanes the batch staging pays (round 1: 59 -> 40 ms/step on C4); with 32-byte lanes a warp already
   // walks 10 small rows at once through the row kernel, and the staging costs more than it saves (148 -> 140 ms/step)
-  const bool batched = batched_on && VW == 1 && a.small_first >= 0 && a.n_small > 0 && (a.x == nullptr || a.ldx == a.B);
+  const bool batched = batched_on && !a.f32 && VW == 1 && a.small_first >= 0 && a.n_small > 0 && (a.x == nullptr || a.ldx == a.B);
   const int rest = batched ? grid - a.nblk_small : grid;
+  if (a.f32) {
+    if (VW == 8) launch_vw<8, float>(a, halo, false, rest, s);
+    else launch_vw<1, float>(a, halo, false, rest, s);
+    return;
+  }
   if (VW == 4) launch_vw<4>(a, halo, batched, rest, s);
   else if (VW == 2) launch_vw<2>(a, halo, batched, rest, s);
   else launch_vw<1>(a, halo, batched, rest, s);

@@ -67,6 +67,20 @@ __host__ __device__ inline int pad_cols(int B) {
   while (p < B) p *= 2;
   return p;
 }
+// the same for a storage type T (opts.fp32: a 32-byte lane is 8 floats, rows padded to 8 ⌈B/8⌉ loaded floats at
+// a power-of-two stride >= 8; B = 11: 2 sectors at a 64-byte stride)
+template <class T>
+__host__ __device__ inline int pad_vec_t(int B) {
+  constexpr int L = 32 / (int)sizeof(T);
+  return B <= 1 ? B : (B + L - 1) / L * L;
+}
+template <class T>
+__host__ __device__ inline int pad_cols_t(int B) {
+  if (B <= 1) return B;
+  int p = 32 / (int)sizeof(T);
+  while (p < B) p *= 2;
+  return p;
+}
 
 constexpr int kMaxCols = 32;    // columns per Krylov batch (B)
 constexpr int kMaxKrylov = 64;  // Arnoldi steps per action
@@ -113,6 +127,7 @@ struct SpmvArgs {
   int med_rpw;                       // filled by spmv(): medium rows per warp when a row is several lanes wide
   int B;
   const int* active;                 // optional (CG): the launch does nothing when *active == 0
+  int f32;                           // 1: y, yh, x and out hold float (opts.fp32 TOAR batches); sums stay double
 };
 void spmv(const SpmvArgs& a, cudaStream_t s);
 
@@ -142,6 +157,7 @@ struct Dcgs2Args {
   int accumulate;                     // pass B vector tiles after the first: add to Qout / Pnext
   double* partials; double* sums_out;
   int grid;
+  int f32;                            // 1: P, w and Q hold float (opts.fp32; pass A only), sums in double
 };
 void reduce_partials(const double* partials, int nout, int G, double* sums_out, cudaStream_t s);
 
@@ -156,6 +172,7 @@ struct ToarArgs {
   const double* coef_y;
   const double* coef_u; int coef_ld;
   int accumulate;
+  int f32;                            // 1: y, U and the outputs hold float (opts.fp32), combinations in double
 };
 void toar_update(ToarArgs a, cudaStream_t s);
 // TOAR coefficient bookkeeping (toar.cu), one thread per Krylov column
@@ -256,7 +273,7 @@ void small_f(const SmallFArgs& a, cudaStream_t s);
 void batch_inputs(const double* V, int64_t ldv, int B, int64_t n, double* Vb, const int* vcol,
                   const int32_t* perm, cudaStream_t s);
 void seed_expand(const double* s1, const double* s2, const double* v, int b, const int32_t* rowptr, const double* g1s,
-                 const int* vcol, int B, int64_t n, double* t0, double* b0, cudaStream_t s);
+                 const int* vcol, int B, int64_t n, double* t0, double* b0, cudaStream_t s, bool f32 = false);
 void setup_chunk(const double* mu, int gstart, int b, int B, double* g0z, double* g1z, double* g0s,
                  double* g1s, int* vcol, int* tcol, cudaStream_t s);
 // combine: mode 0 = φV (c0 V + Σ comb_i Q_i,top), 1 = 𝕃V (lscale (t'⊙V - Σ comb_i Q_i,top)),
@@ -266,11 +283,15 @@ void setup_chunk(const double* mu, int gstart, int b, int B, double* g0z, double
 void combine(int mode, double lscale, const VecPtrs& Q, int nvec, int64_t n, int B,
              const double* comb, const double* V, int64_t ldv, const int* vcol, double c0,
              const double* tprime, int64_t ldt, const int* tcol, double* out, int64_t ldo,
-             const int32_t* perm, cudaStream_t s);
+             const int32_t* perm, cudaStream_t s, bool f32 = false);  // f32: Q holds float
 void pack_rows(const double* src, int64_t lds, const int32_t* idx, int64_t cnt, int B, double* dst,
                cudaStream_t s);
 // dst[r * ldd + c] = src[r * lds + c] for c < B (other columns of dst untouched), r < n
 void repack_rows(const double* src, int64_t lds, int64_t n, int B, double* dst, int64_t ldd, cudaStream_t s);
+// the same between storage types (double -> float, float -> float); columns [B, zpad) of dst rows are zeroed
+void repack_rows_t(const void* src, bool src_f32, int64_t lds, int64_t n, int B, void* dst, bool dst_f32, int64_t ldd,
+                   int zpad, cudaStream_t s);
+void pack_rows_f32(const float* src, int64_t lds, const int32_t* idx, int64_t cnt, int B, float* dst, cudaStream_t s);
 void fill(double* p, int64_t n, double v, cudaStream_t s);
 // sticky convergence flag: flag[0] |= 1 and flag[1] = max estimate (as bits) when err[c] > tol
 void krylov_check(const double* err, int B, double tol, int* flag, cudaStream_t s);
@@ -294,6 +315,16 @@ bool xnystrace_curve(const std::vector<double>& lam, const std::vector<double>& 
 // outer Lanczos helpers (diffusion)
 void lanczos_combine(const double* Q, int64_t stride, int m, int64_t n, const double* Y, int nt,
                      double scale, double* X, int64_t ldx, const int32_t* perm, cudaStream_t s);
+
+// ---------------------------------------------------------------- block products (block.cu)
+// C (p x q col-major, ld p) = X[:, :p]ᵀ Y[:, :q] over n rows (row-major X ld ldx, Y ld ldy), q <= 64;
+// partials: block_gram_partials(n, p) doubles of scratch.  Deterministic (fixed row split, CTA order).
+size_t block_gram_partials(int64_t n, int p);
+void block_gram(int p, int q, int64_t n, const double* X, int64_t ldx, const double* Y, int64_t ldy, double* C,
+                double* partials, cudaStream_t s);
+// Y[:, :q] = beta Y + alpha X[:, :p] C  (C p x q col-major, ld p; Y not read when beta == 0), q <= 64
+void block_axpy(int p, int q, int64_t n, double alpha, const double* X, int64_t ldx, const double* C, double beta,
+                double* Y, int64_t ldy, cudaStream_t s);
 
 // ---------------------------------------------------------------- collectives (comm.cu)
 constexpr int kMaxRanks = 64;

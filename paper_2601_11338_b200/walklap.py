@@ -39,7 +39,8 @@ class _Opts(ctypes.Structure):
                 ("rho_bound", ctypes.c_double), ("relabel", ctypes.c_int32), ("solver", ctypes.c_int32),
                 ("cg_tol", ctypes.c_double), ("cg_maxit", ctypes.c_int32), ("cg_check", ctypes.c_int32),
                 ("tol", ctypes.c_double), ("halo_overlap", ctypes.c_int32),
-                ("lanczos", ctypes.c_int32), ("krylov_adaptive", ctypes.c_int32)]
+                ("lanczos", ctypes.c_int32), ("krylov_adaptive", ctypes.c_int32),
+                ("fp32", ctypes.c_int32)]
 
 
 def load():
@@ -350,13 +351,14 @@ class Operator:
     ("series", [c0, c1, ...]).  solver="cg" (resolvent only) evaluates φ_θ = (1-μ²α²) 𝒜_θ(α)^{-1} by
     Jacobi-preconditioned conjugate gradients on the deformed Laplacian instead of Krylov on Z.
     lap_scale multiplies 𝕃 (wl_walkfun.scale; 1/(1+α) reproduces Fig. 4b's (1-α) normalisation).
+    fp32=1: float storage of the Krylov batches' n-vectors, double sums (wl_opts.fp32; parity 1e-4).
     """
 
     def __init__(self, n_global, row_ptr, col_idx, thetas=(1.0,), f=("exp", 1.0), variant=None,
                  row_range=None, comm: Comm | None = None, krylov_dim=30, reorth=2, max_cols=32,
                  breakdown_tol=1e-12, rho_bound=0.0, relabel=1, solver="krylov", cg_tol=1e-9, cg_maxit=1000,
                  cg_check=8, lap_scale=1.0, krylov_tol=0.0, halo_overlap=1, lanczos=1, krylov_adaptive=0,
-                 stream=None):
+                 fp32=0, stream=None):
         lib = load()
         rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
         ci = np.ascontiguousarray(col_idx, dtype=np.int32)
@@ -390,6 +392,7 @@ class Operator:
         opts.halo_overlap = halo_overlap
         opts.lanczos = lanczos
         opts.krylov_adaptive = krylov_adaptive
+        opts.fp32 = int(fp32)
         h = ctypes.c_void_p()
         _check(lib.wl_operator_create(comm.handle if comm else None, n_global, rb, re, rp.ctypes.data,
                                       ci.ctypes.data, variant, len(thetas) if variant == WL_BTDW else 1,

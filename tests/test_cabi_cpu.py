@@ -38,6 +38,7 @@ def test_opts_default(lib):
     lib.wl_opts_default(ctypes.byref(o))
     assert (o.krylov_dim, o.reorth, o.max_cols, o.breakdown_tol, o.rho_bound, o.relabel) == (30, 2, 32, 1e-12, 0.0, 1)
     assert (o.solver, o.cg_tol, o.cg_maxit, o.cg_check, o.tol) == (0, 1e-9, 1000, 8, 0.0)
+    assert (o.halo_overlap, o.lanczos, o.krylov_adaptive, o.fp32) == (1, 1, 0, 0)
 
 
 def _partition_def(row_ptr, P):
