@@ -53,6 +53,9 @@ __host__ __device__ constexpr int stage_elems() { return 16384 / (int)sizeof(T);
 #ifndef WL_DOTS_F_PER
 #define WL_DOTS_F_PER 16
 #endif
+#ifndef WL_DOTS_F_SPLIT
+#define WL_DOTS_F_SPLIT 2
+#endif
 #ifndef WL_UPD_F_CONSUMERS
 #define WL_UPD_F_CONSUMERS 480
 #endif
@@ -230,16 +233,28 @@ __global__ void __launch_bounds__(kDotsConsumers + 32, 1) dcgs2_dots_ring(Dcgs2A
       for (int j = 0; j < kMaxVecPerLaunch; ++j) {
         if (j < nq) {
           const T* st = cur.acquire(ring, full);
-          // double: straight into the running sums (the fp64 path's order); float: a per-tile partial
-          T sa = kF32 ? T(0) : T(acc[2 * j]), sb = kF32 ? T(0) : T(acc[2 * j + 1]);
+          // double: straight into the running sums (the fp64 path's order); float: per-tile partials in NS
+          // independent chains (shorter FFMA dependency chains)
+          constexpr int NS = kF32 ? WL_DOTS_F_SPLIT : 1;
+          T sa[NS], sb[NS];
+#pragma unroll
+          for (int u = 0; u < NS; ++u) {
+            sa[u] = (kF32 || u) ? T(0) : T(acc[2 * j]);
+            sb[u] = (kF32 || u) ? T(0) : T(acc[2 * j + 1]);
+          }
 #pragma unroll
           for (int i = 0; i < PER; ++i) {
             const T q = st[t + i * tpb];  // t + (PER - 1) tpb < SE for every B
-            sa += q * pv[i];
-            sb += q * wv[i];
+            sa[i % NS] += q * pv[i];
+            sb[i % NS] += q * wv[i];
           }
-          acc[2 * j] = kF32 ? acc[2 * j] + (double)sa : (double)sa;
-          acc[2 * j + 1] = kF32 ? acc[2 * j + 1] + (double)sb : (double)sb;
+#pragma unroll
+          for (int u = 1; u < NS; ++u) {
+            sa[0] += sa[u];
+            sb[0] += sb[u];
+          }
+          acc[2 * j] = kF32 ? acc[2 * j] + (double)sa[0] : (double)sa[0];
+          acc[2 * j + 1] = kF32 ? acc[2 * j + 1] + (double)sb[0] : (double)sb[0];
           cur.release(empty, lane);
         }
       }
@@ -441,8 +456,8 @@ __global__ void __launch_bounds__(upd_consumers<T>() + 32, 1) toar_update_ring(T
               T* row = out + (r0 + (int64_t)i * (tpb / B)) * a.out_ld[o];
               row[c] = (T)acc[o][i];
               // the phantom columns too: whole 32-byte sectors reach L2, so DRAM sees no partial-sector writes
-              if (c == B - 1)
-                for (int cc = B; cc < pad_vec_t<T>(B); ++cc) row[cc] = T(0);
+              // (spread over the row's threads: column c writes phantoms B + c, B + c + B, ...)
+              for (int cc = B + c; cc < pad_vec_t<T>(B); cc += B) row[cc] = T(0);
             } else {
               out[e0 + t + i * tpb] = (T)acc[o][i];
             }

@@ -10,3 +10,5 @@ timeout 900 python bench.py --solver cg --config c3 --steps 5 --warmup 3 > gpuru
 timeout 900 python bench.py --markov --steps 3 --warmup 3 > gpurun_out/r02_bench_markov_c4.json 2>gpurun_out/f6.err; tail -2 gpurun_out/f6.err
 timeout 900 python bench.py --rhoz --steps 3 --warmup 3 > gpurun_out/r02_bench_rhoz_c4.json 2>gpurun_out/f7.err; tail -2 gpurun_out/f7.err
 timeout 900 python bench.py --b 8 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/r02_bench_c4_b8.json 2>gpurun_out/f9.err; tail -2 gpurun_out/f9.err
+timeout 900 python bench.py --steps 20 --warmup 5 --fp32 1 > gpurun_out/r02_bench_c4_fp32.json 2>gpurun_out/f10.err; tail -2 gpurun_out/f10.err
+timeout 900 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --walk > gpurun_out/r02_bench_c4_walk_lanczos1.json 2>gpurun_out/f11.err; tail -2 gpurun_out/f11.err
