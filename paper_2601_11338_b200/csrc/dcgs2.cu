@@ -54,7 +54,7 @@ __host__ __device__ constexpr int stage_elems() { return 16384 / (int)sizeof(T);
 #define WL_DOTS_F_PER 16
 #endif
 #ifndef WL_DOTS_F_SPLIT
-#define WL_DOTS_F_SPLIT 2
+#define WL_DOTS_F_SPLIT 1  // measured: 2 and 4 chains are slower (registers)
 #endif
 #ifndef WL_UPD_F_CONSUMERS
 #define WL_UPD_F_CONSUMERS 480
