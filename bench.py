@@ -351,7 +351,8 @@ def run_walklap(args):
             gbs = bytes_ / (per_step_ms / 1e3) / 1e9
             kernels[name].update({"alg_bytes_per_step": bytes_, "achieved_gbs": gbs, "frac": gbs / peak})
     top = max((k for k in kernels if "alg_bytes_per_step" in kernels[k]), key=lambda k: kernels[k]["ms_per_step"])
-    ncu = ncu_traffic()
+    headline = args.config == "c4" and not args.walk and not args.b and not args.krylov  # the captured workload
+    ncu = ncu_traffic("f32" if args.fp32 else "f64") if headline else {}
     roof = {"kernel": top, "bound": "hbm", "achieved": kernels[top]["achieved_gbs"], "peak": peak,
             "unit": "GB/s", "frac": kernels[top]["frac"], "peak_source": peak_src,
             "traffic": ncu.get(top) if world == 1 else None,  # the committed ncu capture is single-GPU
@@ -410,11 +411,13 @@ def ws_bmax(op, b):
     return max(1, min(32, op.n_theta * b))
 
 
-def ncu_traffic():
-    """dram bytes per launch from the committed ncu --set full summary (profiles/), if present."""
+def ncu_traffic(mode="f64"):
+    """DRAM bytes per launch of the C4 bench kernels from the committed ncu launch list (profiles/ncu_traffic.json,
+    one table per storage mode: "f64" and "f32"), if present."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
-        return {k: v["dram_bytes_per_launch"] for k, v in json.load(open(p)).items() if isinstance(v, dict)}
+        tab = json.load(open(p)).get(mode, {})
+        return {k: v["dram_bytes_per_launch"] for k, v in tab.items() if isinstance(v, dict)}
     except Exception:
         return {}
 

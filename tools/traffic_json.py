@@ -1,0 +1,52 @@
+"""profiles/ncu_traffic.json from the ncu launch lists of the C4 bench (tools/r2_ncu_final.sh): mean DRAM
+read+write bytes per launch of the Z-step SpMM scope (row kernel + isolated-row stream), the dot pass and the
+3-output update pass, per storage mode.
+usage: python tools/traffic_json.py f64.csv f32.csv git_hash"""
+import collections
+import csv
+import json
+import sys
+
+
+def per_kernel(path, last=1300):
+    rows = list(csv.reader(open(path)))
+    hdr, data = None, collections.OrderedDict()
+    for r in rows:
+        if r and r[0] == "ID":
+            hdr = r
+            continue
+        if hdr is None or len(r) < len(hdr):
+            continue
+        d = dict(zip(hdr, r))
+        data.setdefault((int(d["ID"]), d["Kernel Name"]), {})[d["Metric Name"]] = (float(d["Metric Value"].replace(",", "")), d["Metric Unit"])
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    agg = collections.defaultdict(list)
+    for (_, name), m in list(data.items())[-last:]:
+        b = sum(m[k][0] * scale[m[k][1]] for k in ("dram__bytes_read.sum", "dram__bytes_write.sum") if k in m)
+        agg[name.split("(")[0]].append(b)
+    return {k: sum(v) / len(v) for k, v in agg.items()}
+
+
+def pick(tab, *subs):
+    for k, v in tab.items():
+        if all(s in k for s in subs):
+            return v
+    return None
+
+
+out = {"_source": "mean DRAM read+write per launch over the last 1300 launches of the C4 bench (B=11, k=30, TOAR), "
+                  "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none "
+                  "(tools/r2_ncu_final.sh; profiles/r02_launches_bench_c4*.csv); spmv_binned = the Z-step row kernel + "
+                  "spmv_iso_kernel of one launch scope",
+       "git": sys.argv[3]}
+for mode, path, rowk in (("f64", sys.argv[1], "ILi4ELb0ELi4ELb0Ed"), ("f32", sys.argv[2], "ILi4ELb0ELi8ELb0Ef")):
+    tab = per_kernel(path)
+    row = pick(tab, "spmv_binned_kernel", rowk) or pick(tab, "spmv_binned_kernel<4, 0, " + ("4" if mode == "f64" else "8"))
+    iso = pick(tab, "spmv_iso_kernel") or 0.0
+    dots = pick(tab, "dcgs2_dots_ring")
+    upd = pick(tab, "toar_update_ring<3") or pick(tab, "toar_update_ringILi3E")
+    out[mode] = {"spmv_binned": {"dram_bytes_per_launch": (row or 0.0) + iso},
+                 "dcgs2_dots": {"dram_bytes_per_launch": dots},
+                 "toar_update": {"dram_bytes_per_launch": upd}}
+json.dump(out, open("profiles/ncu_traffic.json", "w"), indent=1)
+print(json.dumps(out, indent=1))
