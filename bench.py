@@ -598,7 +598,7 @@ def run_diffusion(args):
     op = wl.Operator(g.n, rp, ci, thetas=cfg["thetas"], f=("exp", 1.0 / rho), row_range=(rb, re), comm=comm,
                      relabel=args.relabel, krylov_dim=cfg["krylov_dim"],
                      krylov_tol=args.adaptive if args.adaptive > 0 else 0.0,
-                     krylov_adaptive=1 if args.adaptive > 0 else 0)
+                     krylov_adaptive=1 if args.adaptive > 0 else 0, fp32=args.fp32)
     torch.cuda.synchronize()
     t_create = time.time() - t0
     kind, lo, hi, nt = cfg.get("taus", ("linspace", 0.0, 100.0, 90))
@@ -646,7 +646,8 @@ def run_diffusion(args):
     # + the τ combine
     n_l = op.n_local
     ab = {}
-    inner = algorithmic_bytes(n_l, int(ci.shape[0]), op.n_halo, 1, int(round(k_mean)), 1, 1, 1, reorth=op.reorth)
+    inner = algorithmic_bytes(n_l, int(ci.shape[0]), op.n_halo, 1, int(round(k_mean)), 1, 1, 1, reorth=op.reorth,
+                              esz=4 if args.fp32 else 8)
     for kk, v in inner.items():
         ab[kk] = ab.get(kk, 0) + k_out * v
     for j in range(k_out):
@@ -668,7 +669,8 @@ def run_diffusion(args):
         line = {
             "metric": METRIC, "value": actions / (ms / 1e3), "unit": "actions/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded graphgen)",
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32-storage/f64-accumulate (inner actions)" if args.fp32 else "f64", "data": "synthetic (seeded graphgen)",
             "config": {"workload": f"{cfg['desc']}; diffusion exp(-tau L)x0 (step a9), {nt} tau in [{lo}, {hi}], "
                                    f"k_out={k_out}, inner k={cfg['krylov_dim']}, theta={cfg['thetas']}",
                        "n": g.n, "nnz": g.nnz, "sweeps_per_s": 1e3 / ms,
@@ -712,7 +714,7 @@ def run_trace(args):
     op = wl.Operator(g.n, rp, ci, thetas=cfg["thetas"][:1], f=("exp", 1.0 / rho), row_range=(rb, re), comm=comm,
                      relabel=args.relabel, krylov_dim=cfg["krylov_dim"],
                      krylov_tol=args.adaptive if args.adaptive > 0 else 0.0,
-                     krylov_adaptive=1 if args.adaptive > 0 else 0)
+                     krylov_adaptive=1 if args.adaptive > 0 else 0, fp32=args.fp32)
     M, k = args.trace_m, args.trace_k
     rational = args.trace_poles == "aaa"
     # Fig. 7: [0, t*] = [0, 100], 90 points, AAA poles, inner solves at 1e-6; the polynomial
@@ -764,14 +766,15 @@ def run_trace(args):
     _, ks, kb = ws.stats()
     k_act = int(round(ks / kb)) if (args.adaptive > 0 and kb) else cfg["krylov_dim"]
     ab = {kk: nact * v for kk, v in algorithmic_bytes(op.n_local, int(ci.shape[0]), op.n_halo, M, k_act,
-                                                       M, M, 1, reorth=op.reorth).items()}
+                                                       M, M, 1, reorth=op.reorth, esz=4 if args.fp32 else 8).items()}
     peak, peak_src = peaks()
     roof = roofline_of(kernels, ab, peak, peak_src)
     if rank == 0:
         line = {
             "metric": "XNysTrace-exp return-probability curves/s", "value": 1e3 / ms, "unit": "curves/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32-storage/f64-accumulate (inner actions)" if args.fp32 else "f64",
             "data": "synthetic (seeded graphgen)",
             "config": {"workload": (f"{cfg['desc']}; Alg. 1 with {len(info['poles'])} AAA poles (+conjugates, +inf), "
                                     f"MINRES inner solves to {args.trace_inner_tol:g}, M={M} probes, 90 t in [0,100]"

@@ -201,3 +201,37 @@ def test_fp32_full_c4_theta_sweep_vs_series(wl):
         ref = phi[:, 0] * V[:, 0] - phi[:, 1]
         assert relerr(t_gpu[:, i], phi[:, 0]).max() < TOL64, th
         assert relerr(got[:, i], ref).max() < TOL32, th
+
+
+def _rational_fp32(wl, g, theta, M, ts, seed, poles=None, inner_tol=1e-7):
+    from oracle import trace as T
+    A = D.adjacency(g)
+    rA = D.rho_A(A)
+    Lap = D.laplacian(A, 1.0 - theta, C.exp(1.0 / rA))
+    Om = gg.vectors(g.n, M, seed)
+    op = wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=[theta], f=("exp", 1.0 / rA), fp32=1)
+    if poles is None:
+        poles = wl.aaa_exp_poles(max(ts) * op.laplacian_bound(0))
+    p, e, info = op.xnystrace_exp_rational(torch.from_numpy(Om).cuda(), ts, poles=poles, inner_tol=inner_tol,
+                                           inner_maxit=2000)
+    op.close()
+    po, eo = T.xnystrace_exp_rational(Lap, Om, poles, ts)
+    return p, e, po, eo
+
+
+def test_fp32_rational_trace_every_pole_kind(wl):
+    """NEXT-2 (Alg. 1, rational) with fp32 inner actions (MINRES shifted solves to 1e-7 on float-stored Krylov
+    batches): ∞, a real pole and a conjugate pair on a BA graph, vs the oracle's dense solves, p̂ at the 1e-4 bar."""
+    g = gg.barabasi_albert(1201, 3, 5)
+    ts = np.linspace(0.0, 4.0, 9)
+    p, e, po, eo = _rational_fp32(wl, g, 0.0, 5, ts, 3, poles=np.array([np.inf, -2.5, -1.0 + 3.0j, 0.5 + 6.0j]))
+    assert np.max(np.abs(p - po) / np.abs(po)) < TOL32
+
+
+@pytest.mark.slow
+def test_fp32_rational_midsize_road_fig7_shape(wl):
+    """The Fig. 7 shape (road-like grid, NBT, M = 30, 90 t in [0, 100], the library's AAA poles) with fp32 inner
+    actions and MINRES to 1e-6 (the paper's inner tolerance), vs the oracle: p̂ at the 1e-4 bar."""
+    g = gg.grid_lcc(60, 60, 0.3, 2002)
+    p, e, po, eo = _rational_fp32(wl, g, 0.0, 30, np.linspace(0.0, 100.0, 90), 2026, inner_tol=1e-6)
+    assert np.max(np.abs(p - po) / np.abs(po)) < TOL32

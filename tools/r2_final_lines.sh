@@ -12,3 +12,5 @@ timeout 900 python bench.py --rhoz --steps 3 --warmup 3 > gpurun_out/r02_bench_r
 timeout 900 python bench.py --b 8 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/r02_bench_c4_b8.json 2>gpurun_out/f9.err; tail -2 gpurun_out/f9.err
 timeout 900 python bench.py --steps 20 --warmup 5 --fp32 1 > gpurun_out/r02_bench_c4_fp32.json 2>gpurun_out/f10.err; tail -2 gpurun_out/f10.err
 timeout 900 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --walk > gpurun_out/r02_bench_c4_walk_lanczos1.json 2>gpurun_out/f11.err; tail -2 gpurun_out/f11.err
+timeout 900 python bench.py --diffusion --steps 3 --warmup 3 --no-cpu-baseline --fp32 1 > gpurun_out/r02_bench_diffusion_c3_fp32.json 2>gpurun_out/f12.err; tail -2 gpurun_out/f12.err
+timeout 1200 python bench.py --trace --adaptive 1e-13 --steps 2 --warmup 1 --fp32 1 > gpurun_out/r02_bench_trace_rational_c3_adaptive_fp32.json 2>gpurun_out/f13.err; tail -2 gpurun_out/f13.err
