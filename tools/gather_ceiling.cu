@@ -203,6 +203,53 @@ __global__ void __launch_bounds__(256) gB_v4(const double* Y, const int* idx, in
   if (acc == 1.2345) out[0] = acc;
 }
 
+// 32-byte lanes over rows at stride LD doubles (LD = 16: the power-of-two stride of the round-2 layout)
+template <int U, int LD>
+__global__ void __launch_bounds__(256) gB_v4ld(const double* Y, const int* idx, int64_t nnz, double* out) {
+  const int lane = threadIdx.x & 31, gi = lane / 3, c = lane - gi * 3;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5, W = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  if (gi >= 10) return;
+  double acc = 0.0;
+  for (int64_t z = w * 10 + gi; z < nnz; z += W * 10 * U) {
+    int cl[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) cl[u] = z + u * W * 10 < nnz ? __ldg(idx + z + u * W * 10) : 0;
+    double v[U][4];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v[u][0]), "=d"(v[u][1]), "=d"(v[u][2]), "=d"(v[u][3])
+                   : "l"(Y + (int64_t)cl[u] * LD + 4 * c));
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc += (v[u][0] + v[u][1]) + (v[u][2] + v[u][3]);
+  }
+  if (acc == 1.2345) out[0] = acc;
+}
+
+// fp32 storage: 11 floats per row at a 16-float (64-byte) stride, 2 lanes of 8 floats per row, 16 rows per LDG
+template <int U>
+__global__ void __launch_bounds__(256) gF_v8(const float* Y, const int* idx, int64_t nnz, double* out) {
+  const int lane = threadIdx.x & 31, gi = lane / 2, c = lane - gi * 2;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5, W = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  float acc = 0.0f;
+  for (int64_t z = w * 16 + gi; z < nnz; z += W * 16 * U) {
+    int cl[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) cl[u] = z + u * W * 16 < nnz ? __ldg(idx + z + u * W * 16) : 0;
+    float v[U][8];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=f"(v[u][0]), "=f"(v[u][1]), "=f"(v[u][2]), "=f"(v[u][3]), "=f"(v[u][4]), "=f"(v[u][5]),
+                     "=f"(v[u][6]), "=f"(v[u][7])
+                   : "l"(Y + (int64_t)cl[u] * 16 + 8 * c));
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc += v[u][k];
+  }
+  if (acc == 1.2345f) out[0] = acc;
+}
+
 // L2 -> SM streaming bandwidth: every CTA re-reads an L2-resident buffer with coalesced 32-byte lanes
 __global__ void __launch_bounds__(256) l2_stream(const double* Y, int64_t n, int reps, double* out) {
   double acc = 0.0;
@@ -221,10 +268,10 @@ int main() {
   const int64_t nmax = 10000000;
   double *Y, *out;
   int* idx;
-  CK(cudaMalloc(&Y, sizeof(double) * nmax * 12));
+  CK(cudaMalloc(&Y, sizeof(double) * nmax * 16));
   CK(cudaMalloc(&idx, sizeof(int) * nnz));
   CK(cudaMalloc(&out, sizeof(double) * nnz / 16 + 64));
-  init_y<<<4096, 256>>>(Y, nmax * 12);
+  init_y<<<4096, 256>>>(Y, nmax * 16);
   CK(cudaDeviceSynchronize());
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -320,6 +367,10 @@ int main() {
     float a7 = timeit([&] { gB_v4<8><<<sms * 8, 256>>>(Y, idx, nnz, out); });
     printf("  B=11 group ld11 %.3f ms (%.0f Grows/s)  group ld12 %.3f  double2 ld12 U8 %.3f ms (%.0f Grows/s)  U4 %.3f  v4(32B) ld12 U4 %.3f U8 %.3f\n",
            a1, nnz / a1 / 1e6, a2, a4, nnz / a4 / 1e6, a5, a6, a7);
+    float b1 = timeit([&] { gB_v4ld<4, 16><<<sms * 8, 256>>>(Y, idx, nnz, out); });
+    float b2 = timeit([&] { gF_v8<4><<<sms * 8, 256>>>(reinterpret_cast<const float*>(Y), idx, nnz, out); });
+    float b3 = timeit([&] { gF_v8<8><<<sms * 8, 256>>>(reinterpret_cast<const float*>(Y), idx, nnz, out); });
+    printf("  B=11 v4(32B) ld16 U4 %.3f ms;  fp32 rows (11 floats, ld 16, 2 x 32B lanes) U4 %.3f ms  U8 %.3f ms\n", b1, b2, b3);
   }
   return 0;
 }
