@@ -39,12 +39,12 @@ out = {"_source": "mean DRAM read+write per launch over the last 1300 launches o
                   "(tools/r2_ncu_final.sh; profiles/r02_launches_bench_c4*.csv); spmv_binned = the Z-step row kernel + "
                   "spmv_iso_kernel of one launch scope",
        "git": sys.argv[3]}
-for mode, path, rowk in (("f64", sys.argv[1], "ILi4ELb0ELi4ELb0Ed"), ("f32", sys.argv[2], "ILi4ELb0ELi8ELb0Ef")):
-    tab = per_kernel(path)
-    row = pick(tab, "spmv_binned_kernel", rowk) or pick(tab, "spmv_binned_kernel<4, 0, " + ("4" if mode == "f64" else "8"))
-    iso = pick(tab, "spmv_iso_kernel") or 0.0
-    dots = pick(tab, "dcgs2_dots_ring")
-    upd = pick(tab, "toar_update_ring<3") or pick(tab, "toar_update_ringILi3E")
+for mode, path, ty, vw in (("f64", sys.argv[1], "double", "4"), ("f32", sys.argv[2], "float", "8")):
+    tab = per_kernel(path)   # (the fp32 list also holds create-time double kernels: t' is computed in double)
+    row = pick(tab, f"spmv_binned_kernel<4, 0, {vw}, 0, {ty}>")
+    iso = pick(tab, f"spmv_iso_kernel<{ty}>") or 0.0
+    dots = pick(tab, f"dcgs2_dots_ring<{ty}>")
+    upd = pick(tab, f"toar_update_ring<3, {ty}>")
     out[mode] = {"spmv_binned": {"dram_bytes_per_launch": (row or 0.0) + iso},
                  "dcgs2_dots": {"dram_bytes_per_launch": dots},
                  "toar_update": {"dram_bytes_per_launch": upd}}
