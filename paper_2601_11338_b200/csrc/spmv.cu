@@ -47,7 +47,12 @@
 #define WL_SPMV_UW_F 4
 #endif
 #ifndef WL_SPMV_MINB_F
-#define WL_SPMV_MINB_F 4
+#define WL_SPMV_MINB_F 5  // with float sums: 48 registers (4 CTAs/SM with double sums: 85 -> 78.5 ms/step on C4)
+#endif
+// fp32 storage: 1 = row sums accumulated in float (half the accumulator registers; the rows are <= 4096-nonzero
+// pieces, the output is rounded to float anyway: C4-shaped errors unchanged at 1e-9), 0 = in double
+#ifndef WL_SPMV_F_ACC32
+#define WL_SPMV_F_ACC32 1
 #endif
 
 namespace wl {
@@ -69,10 +74,10 @@ __device__ __forceinline__ Vec<VW, T> vzero() {
   for (int k = 0; k < VW; ++k) r.v[k] = T(0);
   return r;
 }
-template <int VW, class T>
-__device__ __forceinline__ void vadd(Vec<VW>& a, const Vec<VW, T>& b) {
+template <int VW, class A, class T>
+__device__ __forceinline__ void vadd(Vec<VW, A>& a, const Vec<VW, T>& b) {
 #pragma unroll
-  for (int k = 0; k < VW; ++k) a.v[k] += (double)b.v[k];
+  for (int k = 0; k < VW; ++k) a.v[k] += (A)b.v[k];
 }
 template <int VW>
 __device__ __forceinline__ void vaddf(Vec<VW, float>& a, const Vec<VW, float>& b) {
@@ -135,6 +140,7 @@ __device__ __forceinline__ int ld_col_hint(const int32_t* p, uint64_t pol) {
 template <int kU, bool HALO, int VW, bool HINT = false, class T = double>
 struct Ctx {
   static_assert(!HINT || std::is_same<T, double>::value, "L2 hints: double storage only");
+  using Acc = typename std::conditional<std::is_same<T, float>::value && WL_SPMV_F_ACC32, float, double>::type;
   const SpmvArgs& a;
   uint64_t pol_last = 0, pol_first = 0;  // HINT: L2 policies
   int c0;             // first column of this lane
@@ -169,7 +175,7 @@ struct Ctx {
   // row r of this CSR -> output row a.out_row[r]; the γ term uses d_r from a.degptr when given
   // (the A_loc part of a split operator); the A_halo part accumulates into out.  `x` (the diagonal
   // operand, ld ldx) and out (ld ldo) are unpadded: per-column scalar accesses.
-  __device__ void write(int r, int deg, const Vec<VW>& sum, const double* xrow = nullptr) const {
+  __device__ void write(int r, int deg, const Vec<VW, Acc>& sum, const double* xrow = nullptr) const {
     const int ro = a.out_row ? __ldg(a.out_row + r) : r;
     if (a.x && a.degptr) deg = __ldg(a.degptr + ro + 1) - __ldg(a.degptr + ro);
     T* dst = reinterpret_cast<T*>(a.out) + (int64_t)ro * a.ldo + c0;
@@ -179,7 +185,7 @@ struct Ctx {
     for (int k = 0; k < VW; ++k) {
       if (k < nc) {
         const int c = c0 + k;
-        double o = sum.v[k];
+        double o = (double)sum.v[k];
         if (a.x) o += ((a.g0 ? __ldg(a.g0 + c) : 0.0) + (a.g1 ? __ldg(a.g1 + c) : 0.0) * (double)deg) * (double)xs[k];
         const double sc = a.scale ? __ldg(a.scale + c) : 1.0;
         dst[k] = (T)(a.accumulate ? (double)dst[k] + sc * o : sc * o);
@@ -189,8 +195,8 @@ struct Ctx {
   // Σ y[col[z]] for z = z0 + first, z0 + first + step, ... < z1 (step = lane groups sharing the row,
   // 0 <= first < step).  Rounds cover [base, base + kU step); the full-round test depends only on the
   // shared base, so lane groups sharing a row never diverge: all full rounds, then one predicated round.
-  __device__ Vec<VW> strided_sum(int z0, int z1, int first, int step) const {
-    Vec<VW> acc = vzero<VW>();
+  __device__ Vec<VW, Acc> strided_sum(int z0, int z1, int first, int step) const {
+    Vec<VW, Acc> acc = vzero<VW, Acc>();
     int base = z0;
     for (; base + kU * step <= z1; base += kU * step) {
       int cl[kU];
@@ -215,7 +221,7 @@ struct Ctx {
   }
   // one round of kU gathered rows into the double accumulator; fp32 storage sums the round in float first
   // (one conversion per round instead of per row: its rounding is that of the stored values)
-  __device__ static void add_round(Vec<VW>& acc, const Vec<VW, T> (&v)[kU]) {
+  __device__ static void add_round(Vec<VW, Acc>& acc, const Vec<VW, T> (&v)[kU]) {
     if constexpr (std::is_same<T, double>::value) {
 #pragma unroll
       for (int u = 0; u < kU; ++u) vadd(acc, v[u]);
@@ -229,8 +235,8 @@ struct Ctx {
 };
 
 // sum of `v` over the lane groups (W lanes each) of a warp, result valid in group 0 (lanes 0..W-1)
-template <int VW>
-__device__ inline Vec<VW> group_reduce(Vec<VW> v, int W, int gpw) {
+template <int VW, class A>
+__device__ inline Vec<VW, A> group_reduce(Vec<VW, A> v, int W, int gpw) {
   if ((W & (W - 1)) == 0) {
 #pragma unroll
     for (int k = 0; k < VW; ++k)
@@ -238,7 +244,7 @@ __device__ inline Vec<VW> group_reduce(Vec<VW> v, int W, int gpw) {
     return v;
   }
   const int lane = threadIdx.x & 31;
-  Vec<VW> s = v;
+  Vec<VW, A> s = v;
   for (int g = 1; g < gpw; ++g) {
 #pragma unroll
     for (int k = 0; k < VW; ++k) s.v[k] += __shfl_sync(0xffffffffu, v.v[k], (lane + g * W) & 31);
@@ -259,6 +265,7 @@ __global__ void __launch_bounds__(kThreads, VW == 1 ? 1 : (sizeof(T) == 4 ? WL_S
   const int gi = lane / W, w = lane - gi * W;
   const bool lane_ok = gi < gpw;
   const Ctx<kU, HALO, VW, HINT, T> ctx(a, lane_ok ? w * VW : 0);
+  using Acc = typename Ctx<kU, HALO, VW, HINT, T>::Acc;
   int blk = blockIdx.x;
   if (blk < a.nblk_small) {  // ---- small rows: one lane group per row
     const int idx = (blk * kWarps + warp) * gpw + gi;
@@ -277,7 +284,7 @@ __global__ void __launch_bounds__(kThreads, VW == 1 ? 1 : (sizeof(T) == 4 ? WL_S
       const int idx = (blk * kWarps + warp) * (32 / L) + lane / L, lg = lane % L;
       const int r = idx < a.n_medium ? a.medium_rows[idx] : 0;
       const int z0 = idx < a.n_medium ? __ldg(a.rowptr + r) : 0, z1 = idx < a.n_medium ? __ldg(a.rowptr + r + 1) : 0;
-      Vec<VW> part = ctx.strided_sum(z0, z1, lg, L);
+      Vec<VW, Acc> part = ctx.strided_sum(z0, z1, lg, L);
 #pragma unroll
       for (int k = 0; k < VW; ++k)
         for (int off = L / 2; off > 0; off >>= 1) part.v[k] += __shfl_xor_sync(0xffffffffu, part.v[k], off);
@@ -292,8 +299,8 @@ __global__ void __launch_bounds__(kThreads, VW == 1 ? 1 : (sizeof(T) == 4 ? WL_S
       const bool ok = rs < a.med_rpw && idx < a.n_medium;
       const int r = ok ? a.medium_rows[idx] : 0;
       const int z0 = ok ? __ldg(a.rowptr + r) : 0, z1 = ok ? __ldg(a.rowptr + r + 1) : 0;
-      const Vec<VW> part = ok ? ctx.strided_sum(z0, z1, gi2, G2) : vzero<VW>();
-      Vec<VW> sum = part;
+      const Vec<VW, Acc> part = ok ? ctx.strided_sum(z0, z1, gi2, G2) : vzero<VW, Acc>();
+      Vec<VW, Acc> sum = part;
       for (int g = 1; g < G2; ++g) {
         const int src = base + ((lane - base) + g * W) % LR;
 #pragma unroll
@@ -306,8 +313,8 @@ __global__ void __launch_bounds__(kThreads, VW == 1 ? 1 : (sizeof(T) == 4 ? WL_S
     if (idx >= a.n_medium) return;
     const int r = a.medium_rows[idx];
     const int z0 = __ldg(a.rowptr + r), z1 = __ldg(a.rowptr + r + 1);
-    const Vec<VW> part = lane_ok ? ctx.strided_sum(z0, z1, gi, gpw) : vzero<VW>();
-    const Vec<VW> sum = group_reduce<VW>(part, W, gpw);
+    const Vec<VW, Acc> part = lane_ok ? ctx.strided_sum(z0, z1, gi, gpw) : vzero<VW, Acc>();
+    const Vec<VW, Acc> sum = group_reduce<VW>(part, W, gpw);
     if (gi == 0) ctx.write(r, z1 - z0, sum);
     return;
   }
@@ -316,12 +323,12 @@ __global__ void __launch_bounds__(kThreads, VW == 1 ? 1 : (sizeof(T) == 4 ? WL_S
     const int idx = blk * kWarps + warp;
     if (idx >= a.n_chunks) return;
     const int4 ch = a.chunks[idx];  // (row, z0, z1, first chunk index of the row)
-    const Vec<VW> part = lane_ok ? ctx.strided_sum(ch.y, ch.z, gi, gpw) : vzero<VW>();
-    const Vec<VW> sum = group_reduce<VW>(part, W, gpw);
+    const Vec<VW, Acc> part = lane_ok ? ctx.strided_sum(ch.y, ch.z, gi, gpw) : vzero<VW, Acc>();
+    const Vec<VW, Acc> sum = group_reduce<VW>(part, W, gpw);
     const int ldp = W * VW;  // partial row: every column slot of the lane group
     if (gi == 0) {
 #pragma unroll
-      for (int k = 0; k < VW; ++k) a.chunk_part[(int64_t)idx * ldp + w * VW + k] = sum.v[k];
+      for (int k = 0; k < VW; ++k) a.chunk_part[(int64_t)idx * ldp + w * VW + k] = (double)sum.v[k];
     }
     __threadfence();
     __syncwarp();
@@ -333,10 +340,10 @@ __global__ void __launch_bounds__(kThreads, VW == 1 ? 1 : (sizeof(T) == 4 ? WL_S
     if (ticket != (unsigned)(nch - 1)) return;
     __threadfence();
     if (gi == 0) {
-      Vec<VW> tot = vzero<VW>();
+      Vec<VW, Acc> tot = vzero<VW, Acc>();
       for (int k = 0; k < nch; ++k)
 #pragma unroll
-        for (int q = 0; q < VW; ++q) tot.v[q] += __ldcg(a.chunk_part + (int64_t)(ch.w + k) * ldp + w * VW + q);
+        for (int q = 0; q < VW; ++q) tot.v[q] += (Acc)__ldcg(a.chunk_part + (int64_t)(ch.w + k) * ldp + w * VW + q);
       ctx.write(ch.x, z1r - z0r, tot);
     }
     if (lane == 0) a.row_ticket[ch.w] = 0u;
