@@ -363,11 +363,13 @@ def run_walklap(args):
         roof["traffic_gbs"] = ncu[top] / (ms_launch / 1e3) / 1e9
         roof["traffic_frac"] = roof["traffic_gbs"] / peak
         roof["gathers_per_s"] = nnz_loc / (ms_launch / 1e3)
-        if args.config == "c4" and G == 11 and not args.fp32:
-            # tools/gather_ceiling.cu: 4e8 gathers of 11-column rows (32-byte lanes, ld 12) drawn from the C4
-            # degree distribution take 3.02 ms on this B200 — the gather-only ceiling of this SpMM
-            roof["gather_ceiling_ms"] = 3.02
-            roof["frac_of_gather_ceiling"] = 3.02 / ms_launch
+        if args.config == "c4" and G == 11:
+            # tools/gather_ceiling.cu (profiles/r02_gather_ceiling.txt): 4e8 gathers of 11-column rows drawn from the
+            # C4 degree distribution — 32-byte lanes at the 128-byte row stride: 2.81 ms; fp32 rows (2 lanes of 8
+            # floats, 64-byte stride): 1.83 ms — the gather-only ceilings of this SpMM
+            ceil_ms = 1.83 if args.fp32 else 2.81
+            roof["gather_ceiling_ms"] = ceil_ms
+            roof["frac_of_gather_ceiling"] = ceil_ms / ms_launch
     spmv = kernels.get("spmv_binned", {})
 
     cpu = None
