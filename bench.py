@@ -157,9 +157,14 @@ def load_graph(cfg, world, rank, torch, dist):
     return g, time.time() - t0
 
 
-def algorithmic_bytes(n, nnz, n_halo, G, K, Bmax, b, n_theta, reorth=2, esz=8):
+def algorithmic_bytes(n, nnz, n_halo, G, K, Bmax, b, n_theta, reorth=2, esz=8, n_act=None):
     """Bytes each kernel must move per step, by kernel name.  esz: bytes per stored element of
-    the TOAR batch's n-vectors (8; 4 in the fp32 mode, where the seeds, inputs and outputs stay double)."""
+    the TOAR batch's n-vectors (8; 4 in the fp32 mode, where the seeds, inputs and outputs stay double).
+    n_act: the rows the Krylov vectors live on (wl_operator_active_rows: the isolated tail carries none); the
+    inputs V, the outputs and t' cover all n rows."""
+    n_out = n
+    if n_act is not None and reorth == 2:
+        n = n_act
     out = {}
     def add(k, v):
         out[k] = out.get(k, 0) + v
@@ -187,7 +192,7 @@ def algorithmic_bytes(n, nnz, n_halo, G, K, Bmax, b, n_theta, reorth=2, esz=8):
                 add("dcgs2_dots", (j + 3) * blk)
                 add("toar_update", (j + 6) * blk)
             add("dcgs2_dots", (K + 2) * blk)                           # final Gram row
-            add("combine", (K + 2) * blk + blk8 + 8 * n * b + 8 * n * n_theta)
+            add("combine", (K + 2) * blk + 8 * n_out * B + 8 * n_out * b + 8 * n_out * n_theta)
         else:
             # DCGS2 step j: dots read q_0..q_{j-1}, p_j and the SpMM output (w's top half IS p_j's
             # bottom half, read once); update reads the same and writes q_j and p_{j+1}
@@ -335,12 +340,13 @@ def run_walklap(args):
     nnz_loc = int(ci.shape[0])
     Kab = int(round(k_mean)) if args.adaptive > 0 else K  # the steps actually taken
     ab = algorithmic_bytes(n_loc, nnz_loc, op.n_halo, G, Kab, ws_bmax(op, b), b, op.n_theta, reorth=op.reorth,
-                           esz=4 if args.fp32 else 8)
+                           esz=4 if args.fp32 else 8, n_act=op.n_active)
     if args.walk and args.lanczos:  # Lanczos batches (R19): K + 1 SpMMs (no diagonal term), 8 n-blocks per step
-        blk = 8 * n_loc * G
-        csr = 4 * nnz_loc + 4 * (n_loc + 1)
+        na = op.n_active            # the Krylov vectors' rows (the isolated tail carries none)
+        blk = 8 * na * G
+        csr = 4 * nnz_loc + 4 * (na + 1)
         ab = {"spmv_binned": (Kab + 1) * (csr + 2 * blk + 8 * op.n_halo * G), "lanczos_vec": Kab * 8 * blk + 3 * blk,
-              "combine": Kab * blk + blk + 8 * n_loc * b + 8 * n_loc, "batch_inputs": 8 * n_loc * b + blk}
+              "combine": Kab * blk + 8 * n_loc * G + 8 * n_loc * b + 8 * n_loc, "batch_inputs": 8 * na * b + blk}
     kernels = {}
     for name, (tot_ms, cnt) in prof.items():
         per_step_ms = tot_ms / args.steps
@@ -649,7 +655,7 @@ def run_diffusion(args):
     n_l = op.n_local
     ab = {}
     inner = algorithmic_bytes(n_l, int(ci.shape[0]), op.n_halo, 1, int(round(k_mean)), 1, 1, 1, reorth=op.reorth,
-                              esz=4 if args.fp32 else 8)
+                              esz=4 if args.fp32 else 8, n_act=op.n_active)
     for kk, v in inner.items():
         ab[kk] = ab.get(kk, 0) + k_out * v
     for j in range(k_out):
@@ -768,7 +774,8 @@ def run_trace(args):
     _, ks, kb = ws.stats()
     k_act = int(round(ks / kb)) if (args.adaptive > 0 and kb) else cfg["krylov_dim"]
     ab = {kk: nact * v for kk, v in algorithmic_bytes(op.n_local, int(ci.shape[0]), op.n_halo, M, k_act,
-                                                       M, M, 1, reorth=op.reorth, esz=4 if args.fp32 else 8).items()}
+                                                       M, M, 1, reorth=op.reorth, esz=4 if args.fp32 else 8,
+                                                       n_act=op.n_active).items()}
     peak, peak_src = peaks()
     roof = roofline_of(kernels, ab, peak, peak_src)
     if rank == 0:

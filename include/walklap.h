@@ -199,6 +199,12 @@ void wl_operator_destroy(wl_operator* op);
 /* Local sizes: n_local rows, nnz_local, halo rows, number of θ values. Any pointer may be NULL. */
 wl_status wl_operator_info(const wl_operator* op, int64_t* n_local, int64_t* nnz_local,
                            int64_t* n_halo, int32_t* n_theta);
+/* Rows of this rank's internal (relabelled) order that carry Krylov data: the rows after them are isolated (no
+ * nonzeros, referenced by no row of any rank), and every Krylov vector built from A v vanishes there (q_k(A) v = 0
+ * for k >= 1; P:76-88 simple graphs), so the Krylov batches store and stream only the first *n_active rows;
+ * their outputs on the isolated rows are c_0 v (φ) and 0 (𝕃; t = c_0 there).  *n_active = n_local without
+ * relabelling (opts.relabel = 0) or when an empty row is referenced (non-symmetric input).  WL_EINVAL on NULL. */
+wl_status wl_operator_active_rows(const wl_operator* op, int64_t* n_active);
 /* Copies t_θ = φ_θ 1 (device, n_local x n_theta, ld ldt >= n_theta) — the "diagonal shift". */
 wl_status wl_operator_diag_shift(const wl_operator* op, double* t_dev, int64_t ldt,
                                  wl_stream stream);

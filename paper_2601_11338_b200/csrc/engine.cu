@@ -203,6 +203,10 @@ struct wl_operator {
   int nranks = 1, rank = 0;
   int64_t n_global = 0, row_begin = 0, row_end = 0;
   int32_t n_loc = 0, nnz_loc = 0;
+  // rows [n_act, n_loc) of the internal order are isolated (no nonzeros, referenced by no row of any rank): every
+  // Krylov vector built from A v vanishes there (q_k(A) v = 0 for k >= 1, R13), so the Krylov batches store and
+  // stream only the first n_act rows; their outputs there are c_0 v (φ) and t' v = 0 (𝕃)
+  int64_t n_act = 0;
   // SpMM operand: A (all local rows; with split, only their local columns) and, with split, Ah (the
   // rows that reference halo columns, only those columns) — the A_loc / A_halo split of SURVEY §8(e):
   // A's SpMM runs while the halo is in flight, Ah's adds the halo terms after it arrived.
@@ -328,10 +332,11 @@ void halo_exchange(const wl_operator* op, wl_workspace* ws, const double* src, i
 // One SpMM launch over CSR part `part` of the operator (see wl_operator::A / Ah).
 void spmv_part(const wl_operator* op, wl_workspace* ws, const CsrPart& part, bool halo_part, const double* y,
                int64_t ldy, const double* x, const double* g0, const double* g1, const double* scale, double* out,
-               int B, cudaStream_t s, const int* active, bool f32) {
+               int B, cudaStream_t s, const int* active, bool f32, int64_t rows) {
   SpmvArgs a{};
   a.active = active;
   a.f32 = f32 ? 1 : 0;
+  a.row_limit = rows;
   a.rowptr = part.rowptr.p;
   a.col = part.col.p;
   a.n_loc = op->n_loc;
@@ -375,20 +380,21 @@ void spmv_part(const wl_operator* op, wl_workspace* ws, const CsrPart& part, boo
 // Multi-rank: the rows of y that peers reference are exchanged first (whole padded rows); with the
 // A_loc / A_halo split (opts.halo_overlap) the exchange runs on the workspace's comm stream while
 // A_loc's SpMM runs, and A_halo's SpMM adds the halo terms once it has arrived.
-// f32: y, x and out hold float (opts.fp32 TOAR batches; element strides).
+// f32: y, x and out hold float (opts.fp32 TOAR batches; element strides).  rows > 0: only output rows < rows are
+// written (the Krylov batches' active rows; the isolated rows beyond are never gathered)
 void do_spmv(const wl_operator* op, wl_workspace* ws, const double* y, int64_t ldy, const double* x,
              const double* g0, const double* g1, const double* scale, double* out, int B,
-             cudaStream_t s, const int* active = nullptr, bool f32 = false) {
+             cudaStream_t s, const int* active = nullptr, bool f32 = false, int64_t rows = 0) {
   if (!multi(op) || !op->split) {
     halo_exchange(op, ws, y, ldy, (int)ldy, s, f32);
-    spmv_part(op, ws, op->A, false, y, ldy, x, g0, g1, scale, out, B, s, active, f32);
+    spmv_part(op, ws, op->A, false, y, ldy, x, g0, g1, scale, out, B, s, active, f32, rows);
     return;
   }
   halo_post(op, ws, y, ldy, (int)ldy, f32, s, ws->cstream, ws->ev_pack);
   WL_CUDA(cudaEventRecord(ws->ev_halo, ws->cstream));
-  spmv_part(op, ws, op->A, false, y, ldy, x, g0, g1, scale, out, B, s, active, f32);
+  spmv_part(op, ws, op->A, false, y, ldy, x, g0, g1, scale, out, B, s, active, f32, rows);
   WL_CUDA(cudaStreamWaitEvent(s, ws->ev_halo, 0));
-  spmv_part(op, ws, op->Ah, true, y, ldy, x, g0, g1, scale, out, B, s, active, f32);
+  spmv_part(op, ws, op->Ah, true, y, ldy, x, g0, g1, scale, out, B, s, active, f32, rows);
 }
 
 // halo buffers, comm stream and events of a workspace (multi-rank)
@@ -522,7 +528,7 @@ void toar_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double*
                 int B, double* out, int64_t ldo, cudaStream_t s, bool user_order) {
   WL_NVTX("krylov_batch_toar");
   const int32_t* perm = user_order ? op->perm.p : nullptr;
-  const int64_t n = op->n_loc;
+  const int64_t n = op->n_act;  // the rows the Krylov vectors live on (isolated rows beyond: §6)
   const int K = ws->K;
   // opts.fp32: the n-vectors of the batch (U, x, z, y and the gathered block) hold float; the seeds, every sum and
   // the coefficient work stay double.  t' (mode 2, at create) is always computed in double.
@@ -557,19 +563,19 @@ void toar_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double*
     double* s1 = vs_ + (n + 1) * b;
     double* s2 = s1 + (n + 1) * b;
     batch_inputs(V, ldv, b, n, vs_, ws->vid.p, perm, s);
-    do_spmv(op, ws, vs_, b, nullptr, nullptr, nullptr, nullptr, s1, b, s);
-    do_spmv(op, ws, s1, b, nullptr, nullptr, nullptr, nullptr, s2, b, s);
+    do_spmv(op, ws, vs_, b, nullptr, nullptr, nullptr, nullptr, s1, b, s, nullptr, false, n);
+    do_spmv(op, ws, s1, b, nullptr, nullptr, nullptr, nullptr, s2, b, s, nullptr, false, n);
     seed_expand(s1, s2, vs_, b, op->degrp(), g1s, ws->vcol.p, B, n, U0, xb, s, f32);
   } else if (!f32) {
     batch_inputs(V, ldv, B, n, ws->Vb.p, ws->vcol.p, perm, s);
-    do_spmv(op, ws, ws->Vb.p, B, nullptr, nullptr, nullptr, nullptr, U0, B, s);
-    do_spmv(op, ws, U0, B, ws->Vb.p, g0s, g1s, nullptr, xb, B, s);
+    do_spmv(op, ws, ws->Vb.p, B, nullptr, nullptr, nullptr, nullptr, U0, B, s, nullptr, false, n);
+    do_spmv(op, ws, U0, B, ws->Vb.p, g0s, g1s, nullptr, xb, B, s, nullptr, false, n);
   } else {  // fp32: the seeds in double, then rounded once
     double* t1 = ws->seed32.p;
     double* t2 = t1 + (n + 1) * B;
     batch_inputs(V, ldv, B, n, ws->Vb.p, ws->vcol.p, perm, s);
-    do_spmv(op, ws, ws->Vb.p, B, nullptr, nullptr, nullptr, nullptr, t1, B, s);
-    do_spmv(op, ws, t1, B, ws->Vb.p, g0s, g1s, nullptr, t2, B, s);
+    do_spmv(op, ws, ws->Vb.p, B, nullptr, nullptr, nullptr, nullptr, t1, B, s, nullptr, false, n);
+    do_spmv(op, ws, t1, B, ws->Vb.p, g0s, g1s, nullptr, t2, B, s, nullptr, false, n);
     repack_rows_t(t1, false, B, n, B, U0, true, B, 0, s);
     repack_rows_t(t2, false, B, n, B, xb, true, B, 0, s);
   }
@@ -645,7 +651,7 @@ void toar_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double*
     WL_NVTX("arnoldi_step");
     const int m = j + 2;
     // a4: y = A x + μ(μ - d)⊙z  (bottom half of Z [z; x])
-    do_spmv(op, ws, xin, ldx_in, zin, g0z, g1z, nullptr, yb, B, s, nullptr, f32);
+    do_spmv(op, ws, xin, ldx_in, zin, g0z, g1z, nullptr, yb, B, s, nullptr, f32, n);
     // a5: one dot pass (Gram row of the newest U vector, U^T y, |y|^2) and one update pass
     d.nq = m - 1;
     d.P = U.p[m - 1];
@@ -727,8 +733,8 @@ void toar_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double*
   small_f(f, s);
   if (op->opts.tol > 0.0) krylov_check(ws->kerr.p, B, op->opts.tol, op->kstat.p, s);
   toar_combine_coef(ws->comb.p, B, K, ws->keff.p, ws->toar_state.p, stride, ws->toar_comb.p, s);
-  combine(mode, op->lscale, U, kstop + 2, n, B, ws->toar_comb.p, V, ldv, ws->vcol.p, op->c0, op->tprime.p, op->n_theta,
-          ws->tcol.p, out, ldo, perm, s, f32);
+  combine(mode, op->lscale, U, kstop + 2, op->n_loc, B, ws->toar_comb.p, V, ldv, ws->vcol.p, op->c0, op->tprime.p,
+          op->n_theta, ws->tcol.p, out, ldo, perm, s, f32, n);
 }
 
 // μ = 0 (θ = 1) chunks: symmetric Lanczos on A from u = A v (lanczos.cu; "Lanczos (for A = Aᵀ)"):
@@ -737,7 +743,7 @@ void lanczos_chunk(const wl_operator* op, wl_workspace* ws, int mode, const doub
                    int gstart, int B, double* out, int64_t ldo, cudaStream_t s, bool user_order) {
   WL_NVTX("krylov_batch_lanczos");
   const int32_t* perm = user_order ? op->perm.p : nullptr;
-  const int64_t n = op->n_loc;
+  const int64_t n = op->n_act;  // the rows the Krylov vectors live on (isolated rows beyond: §6)
   const int K = ws->K;
   const int64_t vs = (n + 1) * B;
   double* g0z = ws->colp.p;
@@ -766,14 +772,14 @@ void lanczos_chunk(const wl_operator* op, wl_workspace* ws, int mode, const doub
   // the SpMM gathers q_j from a row-padded copy (32-byte lanes, §7) written by the scaling pass
   double* xg = ws->xg.p && pad_cols(B) != B ? ws->xg.p : nullptr;
   const int64_t ldg = xg ? pad_cols(B) : B;
-  do_spmv(op, ws, ws->Vb.p, B, nullptr, nullptr, nullptr, nullptr, q0, B, s);  // u = A v  (a3 seed, μ = 0)
+  do_spmv(op, ws, ws->Vb.p, B, nullptr, nullptr, nullptr, nullptr, q0, B, s, nullptr, false, n);  // u = A v (a3, μ = 0)
   lanczos_vec(0, q0, nullptr, nullptr, n, B, sc, ws->partials.p, s);
   scalar(0, 0);
   lanczos_vec(3, q0, nullptr, nullptr, n, B, sc, ws->partials.p, s, xg, ldg);   // q_0 = u / ‖u‖
   for (int j = 0; j < K; ++j) {
     double* qj = const_cast<double*>(Q.p[j]);
     double* w = const_cast<double*>(Q.p[j + 1]);
-    do_spmv(op, ws, xg ? xg : qj, ldg, nullptr, nullptr, nullptr, nullptr, w, B, s);  // a4 at μ = 0: w' = A q_j
+    do_spmv(op, ws, xg ? xg : qj, ldg, nullptr, nullptr, nullptr, nullptr, w, B, s, nullptr, false, n);  // w' = A q_j
     lanczos_vec(1, qj, w, nullptr, n, B, sc, ws->partials.p, s);
     scalar(1, j);                                                                 // α_j
     lanczos_vec(2, w, qj, j > 0 ? Q.p[j - 1] : nullptr, n, B, sc, ws->partials.p, s);
@@ -796,8 +802,8 @@ void lanczos_chunk(const wl_operator* op, wl_workspace* ws, int mode, const doub
   f.err = op->opts.tol > 0.0 ? ws->kerr.p : nullptr;
   small_f(f, s);
   if (op->opts.tol > 0.0) krylov_check(ws->kerr.p, B, op->opts.tol, op->kstat.p, s);
-  combine(mode, op->lscale, Q, K, n, B, ws->comb.p, V, ldv, ws->vcol.p, op->c0, op->tprime.p, op->n_theta, ws->tcol.p,
-          out, ldo, perm, s);
+  combine(mode, op->lscale, Q, K, op->n_loc, B, ws->comb.p, V, ldv, ws->vcol.p, op->c0, op->tprime.p, op->n_theta,
+          ws->tcol.p, out, ldo, perm, s, false, n);
 }
 
 // Resolvent action by Jacobi-preconditioned CG on the deformed Laplacian (cg.cu; opts.solver ==
@@ -1018,11 +1024,14 @@ void build_operator(wl_operator* op, const int64_t* rp_in, const int32_t* ci_in,
   // outputs scattered through perm at the boundary (batch_inputs / combine).  With the split the
   // key is the LOCAL degree: the number of local nonzeros that gather the row, and the row length
   // the local SpMM's bins see.
+  // Rows without nonzeros sort last (key -1 with the split, whose local degree is 0 for halo-only rows too).
   std::vector<int32_t> key((size_t)n);
   for (int64_t r = 0; r < n; ++r) {
     key[r] = rp[r + 1] - rp[r];
-    if (op->split)
+    if (op->split) {
       for (int32_t z = rp[r]; z < rp[r + 1]; ++z) key[r] -= col[z] >= n;
+      if (rp[r + 1] == rp[r]) key[r] = -1;
+    }
   }
   std::vector<int32_t> newid;
   if (op->opts.relabel) {
@@ -1044,6 +1053,16 @@ void build_operator(wl_operator* op, const int64_t* rp_in, const int32_t* ci_in,
     col.swap(col2);
     op->perm.alloc(std::max<int64_t>(1, n));
     if (n) WL_CUDA(cudaMemcpy(op->perm.p, perm.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+  }
+  // isolated tail: with the relabelling the empty rows are the last ones; they are isolated when no local row
+  // references them (a symmetric graph never does; checked) and no peer requests them (checked below)
+  op->n_act = n;
+  if (op->opts.relabel) {
+    int64_t na = n;
+    while (na > 0 && rp[na] == rp[na - 1]) --na;
+    bool referenced = false;
+    for (int64_t z = 0; z < nnz && !referenced; ++z) referenced = col[z] >= na && col[z] < n;
+    if (!referenced) op->n_act = na;
   }
   if (!op->split) {
     op->A.upload(rp, col, nullptr);
@@ -1094,6 +1113,7 @@ void build_operator(wl_operator* op, const int64_t* rp_in, const int32_t* ci_in,
         if (g < op->row_begin || g >= op->row_end) throw Error(WL_EGRAPH, "halo request for a row not owned");
         idx[k] = (int32_t)(g - op->row_begin);
         if (!newid.empty()) idx[k] = newid[idx[k]];
+        if (idx[k] >= op->n_act) op->n_act = n;  // an "isolated" row a peer references: not isolated
         ++k;
       }
     op->send_idx.alloc(std::max<int64_t>(1, op->n_send));
@@ -1411,6 +1431,13 @@ wl_status wl_operator_info(const wl_operator* op, int64_t* n_local, int64_t* nnz
     if (nnz_local) *nnz_local = op->nnz_loc;
     if (n_halo) *n_halo = op->n_halo;
     if (n_theta) *n_theta = op->n_theta;
+  });
+}
+
+wl_status wl_operator_active_rows(const wl_operator* op, int64_t* n_active) {
+  return guarded([&] {
+    if (!op || !n_active) throw Error(WL_EINVAL, "NULL argument");
+    *n_active = op->n_act;
   });
 }
 

@@ -44,7 +44,7 @@ template <int NV, class T>
 __global__ void combine_kernel(int mode, double lscale, const VecPtrs Q, int nvec, int64_t n, int B,
                                const double* comb, const double* V, int64_t ldv, const int* vcol,
                                double c0, const double* tprime, int64_t ldt, const int* tcol,
-                               double* out, int64_t ldo, const int32_t* perm) {
+                               double* out, int64_t ldo, const int32_t* perm, int64_t nq) {
   __shared__ double s_comb[NV * kMaxCols];
   for (int idx = threadIdx.x; idx < nvec * B; idx += blockDim.x) s_comb[idx] = comb[idx];
   __syncthreads();
@@ -54,9 +54,11 @@ __global__ void combine_kernel(int mode, double lscale, const VecPtrs Q, int nve
     const int64_t r = e / B;
     const int c = (int)(e - r * B);
     double acc = 0.0;
+    if (r < nq) {
 #pragma unroll 8
-    for (int i = 0; i < NV; ++i)
-      if (i < nvec) acc += s_comb[i * B + c] * (double)__ldg(reinterpret_cast<const T*>(Q.p[i]) + e);
+      for (int i = 0; i < NV; ++i)
+        if (i < nvec) acc += s_comb[i * B + c] * (double)__ldg(reinterpret_cast<const T*>(Q.p[i]) + e);
+    }
     double o;
     const int64_t ru = perm ? perm[r] : r;  // user row of internal row r
     if (mode == 2) {
@@ -294,11 +296,12 @@ void setup_chunk(const double* mu, int gstart, int b, int B, double* g0z, double
 void combine(int mode, double lscale, const VecPtrs& Q, int nvec, int64_t n, int B,
                  const double* comb, const double* V, int64_t ldv, const int* vcol, double c0,
                  const double* tprime, int64_t ldt, const int* tcol, double* out, int64_t ldo,
-                 const int32_t* perm, cudaStream_t s, bool f32) {
+                 const int32_t* perm, cudaStream_t s, bool f32, int64_t nq) {
   WL_LAUNCH("combine");
+  if (nq < 0) nq = n;
   const int g = grid_for(n * B);
 #define WL_COMBINE(NV, T) \
-  combine_kernel<NV, T><<<g, 256, 0, s>>>(mode, lscale, Q, nvec, n, B, comb, V, ldv, vcol, c0, tprime, ldt, tcol, out, ldo, perm)
+  combine_kernel<NV, T><<<g, 256, 0, s>>>(mode, lscale, Q, nvec, n, B, comb, V, ldv, vcol, c0, tprime, ldt, tcol, out, ldo, perm, nq)
   if (f32) {
     if (nvec <= 16) WL_COMBINE(16, float);
     else if (nvec <= 32) WL_COMBINE(32, float);

@@ -544,11 +544,15 @@ void spmv(const SpmvArgs& a0, cudaStream_t s) {
   WL_LAUNCH("spmv_binned");
   if (a.small_first >= 0 && a.n_iso > 0 && !a.accumulate) {  // isolated rows: a stream, off the row kernels
     const int r0 = a.small_first + a.n_small - a.n_iso;
-    const int g = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)a.n_iso * a.B + kThreads - 1) / kThreads,
+    SpmvArgs ai = a;  // rows >= row_limit (the Krylov batches' isolated tail) are not written at all
+    if (a.row_limit > 0) ai.n_iso = (int)std::max<int64_t>(0, std::min<int64_t>(a.n_iso, a.row_limit - r0));
+    const int g = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)ai.n_iso * a.B + kThreads - 1) / kThreads,
                                                             (int64_t)num_sms() * 8));
-    if (a.f32) spmv_iso_kernel<float><<<g, kThreads, 0, s>>>(a, r0);
-    else spmv_iso_kernel<double><<<g, kThreads, 0, s>>>(a, r0);
-    WL_CUDA(cudaGetLastError());
+    if (ai.n_iso > 0) {
+      if (a.f32) spmv_iso_kernel<float><<<g, kThreads, 0, s>>>(ai, r0);
+      else spmv_iso_kernel<double><<<g, kThreads, 0, s>>>(ai, r0);
+      WL_CUDA(cudaGetLastError());
+    }
     a.n_small -= a.n_iso;
     a.n_iso = 0;
     if (a.n_small == 0) a.small_first = -1;

@@ -127,7 +127,9 @@ struct SpmvArgs {
   int med_rpw;                       // filled by spmv(): medium rows per warp when a row is several lanes wide
   int B;
   const int* active;                 // optional (CG): the launch does nothing when *active == 0
-  int f32;                           // 1: y, yh, x and out hold float (opts.fp32 TOAR batches); sums stay double
+  int f32;                           // 1: y, yh, x and out hold float (opts.fp32 TOAR batches)
+  int64_t row_limit;                 // > 0: rows >= row_limit (isolated, the tail of the contiguous small range) are
+                                     // not written
 };
 void spmv(const SpmvArgs& a, cudaStream_t s);
 
@@ -283,7 +285,8 @@ void setup_chunk(const double* mu, int gstart, int b, int B, double* g0z, double
 void combine(int mode, double lscale, const VecPtrs& Q, int nvec, int64_t n, int B,
              const double* comb, const double* V, int64_t ldv, const int* vcol, double c0,
              const double* tprime, int64_t ldt, const int* tcol, double* out, int64_t ldo,
-             const int32_t* perm, cudaStream_t s, bool f32 = false);  // f32: Q holds float
+             const int32_t* perm, cudaStream_t s, bool f32 = false,  // f32: Q holds float
+             int64_t nq = -1);  // rows >= nq (>= 0) have no basis entries (isolated rows): the sum is 0 there
 void pack_rows(const double* src, int64_t lds, const int32_t* idx, int64_t cnt, int B, double* dst,
                cudaStream_t s);
 // dst[r * ldd + c] = src[r * lds + c] for c < B (other columns of dst untouched), r < n

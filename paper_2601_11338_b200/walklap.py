@@ -72,6 +72,7 @@ def load():
                                 ctypes.POINTER(_Opts), vp, pvp], ctypes.c_int),
         "wl_operator_destroy": ([vp], None),
         "wl_operator_info": ([vp, vp, vp, vp, vp], ctypes.c_int),
+        "wl_operator_active_rows": ([vp, vp], ctypes.c_int),
         "wl_operator_diag_shift": ([vp, vp, i64, vp], ctypes.c_int),
         "wl_workspace_create": ([vp, i32, pvp], ctypes.c_int),
         "wl_workspace_destroy": ([vp], None),
@@ -405,6 +406,9 @@ class Operator:
         nl, nz, nh, nt = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int32()
         _check(lib.wl_operator_info(h, ctypes.byref(nl), ctypes.byref(nz), ctypes.byref(nh), ctypes.byref(nt)))
         self.n_local, self.nnz_local, self.n_halo, self.n_theta = nl.value, nz.value, nh.value, nt.value
+        na = ctypes.c_int64()
+        _check(lib.wl_operator_active_rows(h, ctypes.byref(na)))
+        self.n_active = na.value  # rows carrying Krylov data (the isolated tail beyond: wl_operator_active_rows)
         self._ws = {}
 
     def workspace(self, max_b: int) -> Workspace:

@@ -615,3 +615,30 @@ def test_adaptive_krylov_stop(wl):
         assert steps / batches < 40, (g.name, steps, batches)
         for i, th in enumerate(thetas):
             assert relerr(LV[:, 2 * i:2 * i + 2], S.laplacian_apply(g, 1.0 - th, f, V, rA)).max() < TOL, (g.name, th)
+
+
+def test_isolated_tail_carries_no_krylov_data(wl):
+    """wl_operator_active_rows: the relabelled isolated rows are left out of every Krylov vector (they vanish there,
+    R13); φV = c_0 V and 𝕃V = 0 on them, the rest unchanged — against the oracle and against relabel = 0 (which
+    keeps every row), for the TOAR and Lanczos batches and the fp32 mode."""
+    g = gg.rmat(14, 12000, 150000, seed=21, perm_seed=22)
+    deg = np.diff(g.row_ptr)
+    rA = S.rho_A(g)
+    f = C.exp(1.0 / rA)
+    V = gg.vectors(g.n, 2, 5)
+    thetas = [0.0, 0.5, 1.0]
+    res = {}
+    for rel in (1, 0):
+        op = wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=thetas, f=("exp", f.param), relabel=rel)
+        assert op.n_active == (int((deg > 0).sum()) if rel else g.n)
+        res[rel] = (op.apply(torch.from_numpy(V).cuda()).cpu().numpy(), op.phi_apply(torch.from_numpy(V).cuda()).cpu().numpy())
+        op.close()
+    assert (deg == 0).sum() > 1000
+    for a, b in zip(res[0], res[1]):
+        assert relerr(a, b).max() < 1e-12
+    LV, PV = res[1]
+    iso = deg == 0
+    assert np.all(LV[iso] == 0.0)
+    assert np.array_equal(PV[iso], np.tile(V[iso], 3) * f.c(0))   # c_0 v exactly
+    for i, th in enumerate(thetas):
+        assert relerr(LV[:, 2 * i:2 * i + 2], S.laplacian_apply(g, 1.0 - th, f, V, rA)).max() < TOL, th
