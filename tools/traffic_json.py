@@ -8,7 +8,7 @@ import json
 import sys
 
 
-def per_kernel(path, last=1300):
+def per_kernel(path, last=600):
     rows = list(csv.reader(open(path)))
     hdr, data = None, collections.OrderedDict()
     for r in rows:
@@ -34,7 +34,7 @@ def pick(tab, *subs):
     return None
 
 
-out = {"_source": "mean DRAM read+write per launch over the last 1300 launches of the C4 bench (B=11, k=30, TOAR), "
+out = {"_source": "mean DRAM read+write per launch over the last 600 launches (the timed and warm-up steps) of the C4 bench (B=11, k=30, TOAR), "
                   "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none "
                   "(tools/r2_ncu_final.sh; profiles/r02_launches_bench_c4*.csv); spmv_binned = the Z-step row kernel + "
                   "spmv_iso_kernel of one launch scope",
