@@ -215,18 +215,19 @@ __global__ void __launch_bounds__(256) cg_reduce_scalar_kernel(int which, int no
 //   mode 0: out = φ V;  mode 1: out = (t' + c0) ⊙ V - φ V;  mode 2 (V = 1): t' = φ 1 - c0 (internal order)
 __global__ void cg_combine_kernel(int mode, double lscale, const double* x, int64_t n, int B, const double* cs, const double* V,
                                   int64_t ldv, const int* vcol, double c0, const double* tprime, int64_t ldt,
-                                  const int* tcol, double* out, int64_t ldo, const int32_t* perm) {
+                                  const int* tcol, double* out, int64_t ldo, const int32_t* perm, int64_t nx) {
   const int64_t N = n * B;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < N; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = e / B;
     const int c = (int)(e - r * B);
-    const double ph = cs[c * 8 + 0] * x[e];
+    const int64_t ru = perm ? perm[r] : r;
+    const double v = V ? V[ru * ldv + vcol[c]] : 1.0;
+    // rows >= nx (isolated: 𝒜 = (1 - μ²α²) I there) were not solved: φ v = (1 - μ²α²) v / (1 - μ²α²) = v
+    const double ph = r < nx ? cs[c * 8 + 0] * x[e] : v;
     if (mode == 2) {
       out[r * ldo + c] = ph - c0;
       continue;
     }
-    const int64_t ru = perm ? perm[r] : r;
-    const double v = V ? V[ru * ldv + vcol[c]] : 1.0;
     out[ru * ldo + c] = mode == 0 ? ph : lscale * ((tprime[r * ldt + tcol[c]] + c0) * v - ph);
   }
 }
@@ -293,11 +294,12 @@ void cg_scalar(int which, const CgArgs& a, cudaStream_t s) {
 
 void cg_combine(int mode, double lscale, const double* x, int64_t n, int B, const double* cs, const double* V, int64_t ldv,
                 const int* vcol, double c0, const double* tprime, int64_t ldt, const int* tcol, double* out,
-                int64_t ldo, const int32_t* perm, cudaStream_t s) {
+                int64_t ldo, const int32_t* perm, cudaStream_t s, int64_t nx) {
+  if (nx < 0) nx = n;
   WL_LAUNCH("cg_combine");
   const int64_t N = n * B;
   const int g = (int)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, (int64_t)num_sms() * 8));
-  cg_combine_kernel<<<g, 256, 0, s>>>(mode, lscale, x, n, B, cs, V, ldv, vcol, c0, tprime, ldt, tcol, out, ldo, perm);
+  cg_combine_kernel<<<g, 256, 0, s>>>(mode, lscale, x, n, B, cs, V, ldv, vcol, c0, tprime, ldt, tcol, out, ldo, perm, nx);
   WL_CUDA(cudaGetLastError());
 }
 

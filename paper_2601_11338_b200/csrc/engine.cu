@@ -813,7 +813,8 @@ void cg_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double* V
               int B, double* out, int64_t ldo, cudaStream_t s, bool user_order) {
   WL_NVTX("cg_solve");
   const int32_t* perm = user_order ? op->perm.p : nullptr;
-  const int64_t n = op->n_loc;
+  // the isolated tail (R13) decouples: 𝒜 = (1 - μ²α²) I there, solved in closed form by cg_combine
+  const int64_t n = op->n_act;
   double* g0 = ws->colp.p;
   double* g1 = g0 + kMaxCols;
   double* scale = g1 + kMaxCols;
@@ -848,7 +849,7 @@ void cg_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double* V
   reduce_scalar(0);
   bool done = false;
   for (int it = 0; it < op->opts.cg_maxit && !done; ++it) {
-    do_spmv(op, ws, a.p, B, a.p, g0, g1, scale, a.q, B, s, a.flags + 1);  // q = 𝒜 p
+    do_spmv(op, ws, a.p, B, a.p, g0, g1, scale, a.q, B, s, a.flags + 1, false, n);  // q = 𝒜 p
     cg_dot(a, s);
     reduce_scalar(1);
     cg_update(a, s);
@@ -861,8 +862,8 @@ void cg_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double* V
       done = ws->cg_flags_host[1] == 0;
     }
   }
-  cg_combine(mode, op->lscale, a.x, n, B, ws->cg_cs.p, V, ldv, ws->vcol.p, op->c0, op->tprime.p, op->n_theta, ws->tcol.p, out,
-             ldo, perm, s);
+  cg_combine(mode, op->lscale, a.x, op->n_loc, B, ws->cg_cs.p, V, ldv, ws->vcol.p, op->c0, op->tprime.p, op->n_theta,
+             ws->tcol.p, out, ldo, perm, s, n);
   WL_CUDA(cudaMemcpyAsync(ws->cg_flags_host + 2, ws->cg_iters.p, B * sizeof(int), cudaMemcpyDeviceToHost, s));
   WL_CUDA(cudaStreamSynchronize(s));
   ws->cg_iterations += *std::max_element(ws->cg_flags_host + 2, ws->cg_flags_host + 2 + B);

@@ -217,7 +217,8 @@ void cg_reduce(int which, const CgArgs& a, cudaStream_t s);         // partials 
 void cg_reduce_scalar(int which, const CgArgs& a, cudaStream_t s);  // single GPU: both in one CTA
 void cg_combine(int mode, double lscale, const double* x, int64_t n, int B, const double* cs, const double* V, int64_t ldv,
                 const int* vcol, double c0, const double* tprime, int64_t ldt, const int* tcol, double* out,
-                int64_t ldo, const int32_t* perm, cudaStream_t s);
+                int64_t ldo, const int32_t* perm, cudaStream_t s,
+                int64_t nx = -1);  // rows >= nx (>= 0): not solved (isolated rows), φ v = v there
 
 // ---------------------------------------------------------------- shifted solves by MINRES (minres.cu)
 // (𝔏 − ξI) X = U for the n × B block U, ξ = shift_re + i shift_im; complex shifts solve the real
