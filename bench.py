@@ -58,10 +58,14 @@ class ClockSampler:
         self.p = None
 
     def __enter__(self):
+        self.first = ""
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
                                        "-lms", "200", "-i", str(self.dev)], stdout=subprocess.PIPE,
                                       stderr=subprocess.DEVNULL, text=True)
+            # wait for the first sample: nvidia-smi's NVML start-up (driver calls, ~0.1-0.3 s) stays out of the
+            # timed region (it delayed the host synchronisations of short steps, e.g. --rhoz: 201 -> 418 ms)
+            self.first = self.p.stdout.readline()
         except Exception:
             self.p = None
         return self
@@ -74,7 +78,7 @@ class ClockSampler:
                 out, _ = self.p.communicate(timeout=5)
             except Exception:
                 out = ""
-            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+            self.lines = [ln for ln in (self.first + (out or "")).splitlines() if ln.strip()]
 
     def summary(self):
         sm, smax, reasons = [], None, set()
