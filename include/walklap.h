@@ -122,7 +122,7 @@ typedef struct {
                            stored in float, halving the bytes of the Gram passes and of the SpMM gathers;
                            every sum (SpMM rows, dot products, basis updates, combine) and all projected
                            work stay double, inputs and results are double, and t (create) is computed
-                           in double.  θ = 1 batches then run TOAR (no Lanczos).  0 (default): double */
+                           in double.  θ = 1 batches run Lanczos on float vectors likewise.  0 (default): double */
 } wl_opts;
 
 typedef enum { WL_SOLVER_KRYLOV = 0, WL_SOLVER_CG = 1 } wl_solver;

@@ -745,14 +745,17 @@ void lanczos_chunk(const wl_operator* op, wl_workspace* ws, int mode, const doub
   const int32_t* perm = user_order ? op->perm.p : nullptr;
   const int64_t n = op->n_act;  // the rows the Krylov vectors live on (isolated rows beyond: §6)
   const int K = ws->K;
-  const int64_t vs = (n + 1) * B;
+  const bool f32 = op->opts.fp32 && mode != 2;  // float storage of the Lanczos vectors (R21); t' stays double
+  const int64_t vs = (n + 1) * B;  // elements per vector (floats fill half of a double slot)
   double* g0z = ws->colp.p;
   double* g1z = g0z + kMaxCols;
   double* g0s = g1z + kMaxCols;
   double* g1s = g0s + kMaxCols;
   setup_chunk(op->mu_dev.p, gstart, b, B, g0z, g1z, g0s, g1s, ws->vcol.p, ws->tcol.p, s);
   VecPtrs Q{};
-  for (int i = 0; i <= K; ++i) Q.p[i] = ws->basis.p + (int64_t)i * vs;
+  for (int i = 0; i <= K; ++i)
+    Q.p[i] = f32 ? reinterpret_cast<const double*>(reinterpret_cast<float*>(ws->basis.p) + (int64_t)i * vs)
+                 : ws->basis.p + (int64_t)i * vs;
   batch_inputs(V, ldv, B, n, ws->Vb.p, ws->vcol.p, perm, s);
   const int G = lanczos_grid(n, B);
   const size_t need = (size_t)G * B;
@@ -770,21 +773,27 @@ void lanczos_chunk(const wl_operator* op, wl_workspace* ws, int mode, const doub
   WL_CUDA(cudaMemsetAsync(ws->H.p, 0, sizeof(double) * B * (K + 1) * K, s));
   double* q0 = const_cast<double*>(Q.p[0]);
   // the SpMM gathers q_j from a row-padded copy (32-byte lanes, §7) written by the scaling pass
-  double* xg = ws->xg.p && pad_cols(B) != B ? ws->xg.p : nullptr;
-  const int64_t ldg = xg ? pad_cols(B) : B;
-  do_spmv(op, ws, ws->Vb.p, B, nullptr, nullptr, nullptr, nullptr, q0, B, s, nullptr, false, n);  // u = A v (a3, μ = 0)
-  lanczos_vec(0, q0, nullptr, nullptr, n, B, sc, ws->partials.p, s);
+  const int pc = f32 ? pad_cols_t<float>(B) : pad_cols(B);
+  double* xg = ws->xg.p && pc != B ? ws->xg.p : nullptr;
+  const int64_t ldg = xg ? pc : B;
+  if (!f32) {
+    do_spmv(op, ws, ws->Vb.p, B, nullptr, nullptr, nullptr, nullptr, q0, B, s, nullptr, false, n);  // u = A v (a3, μ = 0)
+  } else {  // u = A v in double (v is double), rounded once
+    do_spmv(op, ws, ws->Vb.p, B, nullptr, nullptr, nullptr, nullptr, ws->seed32.p, B, s, nullptr, false, n);
+    repack_rows_t(ws->seed32.p, false, B, n, B, q0, true, B, 0, s);
+  }
+  lanczos_vec(0, q0, nullptr, nullptr, n, B, sc, ws->partials.p, s, nullptr, 0, f32);
   scalar(0, 0);
-  lanczos_vec(3, q0, nullptr, nullptr, n, B, sc, ws->partials.p, s, xg, ldg);   // q_0 = u / ‖u‖
+  lanczos_vec(3, q0, nullptr, nullptr, n, B, sc, ws->partials.p, s, xg, ldg, f32);   // q_0 = u / ‖u‖
   for (int j = 0; j < K; ++j) {
     double* qj = const_cast<double*>(Q.p[j]);
     double* w = const_cast<double*>(Q.p[j + 1]);
-    do_spmv(op, ws, xg ? xg : qj, ldg, nullptr, nullptr, nullptr, nullptr, w, B, s, nullptr, false, n);  // w' = A q_j
-    lanczos_vec(1, qj, w, nullptr, n, B, sc, ws->partials.p, s);
+    do_spmv(op, ws, xg ? xg : qj, ldg, nullptr, nullptr, nullptr, nullptr, w, B, s, nullptr, f32, n);  // w' = A q_j
+    lanczos_vec(1, qj, w, nullptr, n, B, sc, ws->partials.p, s, nullptr, 0, f32);
     scalar(1, j);                                                                 // α_j
-    lanczos_vec(2, w, qj, j > 0 ? Q.p[j - 1] : nullptr, n, B, sc, ws->partials.p, s);
+    lanczos_vec(2, w, qj, j > 0 ? Q.p[j - 1] : nullptr, n, B, sc, ws->partials.p, s, nullptr, 0, f32);
     scalar(2, j);                                                                 // β_{j+1}
-    lanczos_vec(3, w, nullptr, nullptr, n, B, sc, ws->partials.p, s, xg, ldg);   // q_{j+1}
+    lanczos_vec(3, w, nullptr, nullptr, n, B, sc, ws->partials.p, s, xg, ldg, f32);   // q_{j+1}
   }
   SmallFArgs f{};
   f.H = ws->H.p;
@@ -803,7 +812,7 @@ void lanczos_chunk(const wl_operator* op, wl_workspace* ws, int mode, const doub
   small_f(f, s);
   if (op->opts.tol > 0.0) krylov_check(ws->kerr.p, B, op->opts.tol, op->kstat.p, s);
   combine(mode, op->lscale, Q, K, op->n_loc, B, ws->comb.p, V, ldv, ws->vcol.p, op->c0, op->tprime.p, op->n_theta,
-          ws->tcol.p, out, ldo, perm, s, false, n);
+          ws->tcol.p, out, ldo, perm, s, f32, n);
 }
 
 // Resolvent action by Jacobi-preconditioned CG on the deformed Laplacian (cg.cu; opts.solver ==
@@ -872,8 +881,8 @@ void cg_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double* V
 
 void run_chunk(const wl_operator* op, wl_workspace* ws, int mode, const double* V, int64_t ldv, int b, int gstart,
                int B, double* out, int64_t ldo, cudaStream_t s, bool user_order = true) {
-  // every column θ = 1 (μ = 0): Lanczos on A (double storage; the fp32 mode runs TOAR)
-  bool walk = op->opts.reorth == 2 && op->opts.lanczos && !op->opts.fp32;
+  // every column θ = 1 (μ = 0): Lanczos on A
+  bool walk = op->opts.reorth == 2 && op->opts.lanczos;
   for (int c = 0; c < B && walk; ++c) walk = op->mu[(gstart + c) / b] == 0.0;
   if (op->opts.solver == WL_SOLVER_CG) cg_chunk(op, ws, mode, V, ldv, b, gstart, B, out, ldo, s, user_order);
   else if (walk) lanczos_chunk(op, ws, mode, V, ldv, b, gstart, B, out, ldo, s, user_order);

@@ -45,34 +45,38 @@ __device__ void lz_partials(double v, int B, int tpb, double* partials) {
   }
 }
 
+// T: the storage type of the Lanczos vectors (double; float in the fp32 mode, R21) — sums are double.
 // phase 0: Σ x² (x = the block at `a`);  phase 1: Σ q·w (a = q_j, b = w')
-__global__ void __launch_bounds__(kThreads) lz_dot_kernel(int phase, const double* x, const double* y, int64_t n, int B,
+template <class T>
+__global__ void __launch_bounds__(kThreads) lz_dot_kernel(int phase, const T* x, const T* y, int64_t n, int B,
                                                           double* partials) {
   const LzLane L(B);
   double v = 0.0;
   if (L.act)
-    for (int64_t e = L.e0; e < n * B; e += L.stride) v += x[e] * (phase == 0 ? x[e] : y[e]);
+    for (int64_t e = L.e0; e < n * B; e += L.stride) v += (double)x[e] * (double)(phase == 0 ? x[e] : y[e]);
   lz_partials(v, B, L.tpb, partials);
 }
 
-// w = w' − α q_j − β_j q_{j−1} (in place over w'); partials of ‖w‖²
-__global__ void __launch_bounds__(kThreads) lz_update_kernel(double* w, const double* q, const double* qm, int64_t n,
-                                                             int B, const double* sc, double* partials) {
+// w = w' − α q_j − β_j q_{j−1} (in place over w'); partials of ‖w‖² (of the stored values)
+template <class T>
+__global__ void __launch_bounds__(kThreads) lz_update_kernel(T* w, const T* q, const T* qm, int64_t n, int B,
+                                                             const double* sc, double* partials) {
   const LzLane L(B);
   double v = 0.0;
   if (L.act) {
     const double al = sc[L.c * 4 + 1], be = sc[L.c * 4 + 0];
     for (int64_t e = L.e0; e < n * B; e += L.stride) {
-      const double x = w[e] - al * q[e] - (qm ? be * qm[e] : 0.0);
+      const T x = (T)((double)w[e] - al * (double)q[e] - (qm ? be * (double)qm[e] : 0.0));
       w[e] = x;
-      v += x * x;
+      v += (double)x * (double)x;
     }
   }
   lz_partials(v, B, L.tpb, partials);
 }
 
 // x *= 1/β per column (sc slot 2); with xp, also the row-padded copy the SpMM gathers (ld ldp, 32-byte rows)
-__global__ void __launch_bounds__(kThreads) lz_scale_kernel(double* x, int64_t n, int B, const double* sc, double* xp,
+template <class T>
+__global__ void __launch_bounds__(kThreads) lz_scale_kernel(T* x, int64_t n, int B, const double* sc, T* xp,
                                                             int64_t ldp) {
   const LzLane L(B);
   if (!L.act) return;
@@ -80,12 +84,12 @@ __global__ void __launch_bounds__(kThreads) lz_scale_kernel(double* x, int64_t n
   const int64_t dr = L.stride / B;  // the stride is a multiple of B: rows advance without a division
   int64_t r = L.e0 / B;
   for (int64_t e = L.e0; e < n * B; e += L.stride, r += dr) {
-    const double v = x[e] * s;
+    const T v = (T)((double)x[e] * s);
     x[e] = v;
     if (xp) {
       xp[r * ldp + L.c] = v;
-      if (L.c == B - 1)  // phantom columns: whole 32-byte sectors (no partial-sector writes in DRAM)
-        for (int cc = B; cc < pad_vec(B); ++cc) xp[r * ldp + cc] = 0.0;
+      // phantom columns: whole 32-byte sectors (no partial-sector writes in DRAM), spread over the row's threads
+      for (int cc = B + L.c; cc < pad_vec_t<T>(B); cc += B) xp[r * ldp + cc] = T(0);
     }
   }
 }
@@ -160,13 +164,23 @@ int lz_grid(int64_t n, int B) {
 
 int lanczos_grid(int64_t n, int B) { return lz_grid(n, B); }
 
-void lanczos_vec(int phase, double* x, const double* y, const double* qm, int64_t n, int B, const double* sc,
-                 double* partials, cudaStream_t s, double* xp, int64_t ldp) {
-  WL_LAUNCH("lanczos_vec");
+template <class T>
+void lanczos_vec_t(int phase, T* x, const T* y, const T* qm, int64_t n, int B, const double* sc, double* partials,
+                   cudaStream_t s, T* xp, int64_t ldp) {
   const int G = lz_grid(n, B);
-  if (phase <= 1) lz_dot_kernel<<<G, kThreads, 0, s>>>(phase, x, y, n, B, partials);
-  else if (phase == 2) lz_update_kernel<<<G, kThreads, 0, s>>>(x, y, qm, n, B, sc, partials);
-  else lz_scale_kernel<<<G, kThreads, 0, s>>>(x, n, B, sc, xp, ldp);
+  if (phase <= 1) lz_dot_kernel<T><<<G, kThreads, 0, s>>>(phase, x, y, n, B, partials);
+  else if (phase == 2) lz_update_kernel<T><<<G, kThreads, 0, s>>>(x, y, qm, n, B, sc, partials);
+  else lz_scale_kernel<T><<<G, kThreads, 0, s>>>(x, n, B, sc, xp, ldp);
+}
+
+void lanczos_vec(int phase, double* x, const double* y, const double* qm, int64_t n, int B, const double* sc,
+                 double* partials, cudaStream_t s, double* xp, int64_t ldp, bool f32) {
+  WL_LAUNCH("lanczos_vec");
+  if (f32)
+    lanczos_vec_t<float>(phase, reinterpret_cast<float*>(x), reinterpret_cast<const float*>(y),
+                         reinterpret_cast<const float*>(qm), n, B, sc, partials, s, reinterpret_cast<float*>(xp), ldp);
+  else
+    lanczos_vec_t<double>(phase, x, y, qm, n, B, sc, partials, s, xp, ldp);
   WL_CUDA(cudaGetLastError());
 }
 

@@ -246,7 +246,8 @@ int lanczos_grid(int64_t n, int B);
 // phase 0: partials of Σ x²; 1: Σ x·y; 2: x = x − α y − β qm with partials of ‖x‖²; 3: x *= scale (and, with
 // xp, its row-padded copy xp with ld ldp for the SpMM's 32-byte lane gathers)
 void lanczos_vec(int phase, double* x, const double* y, const double* qm, int64_t n, int B, const double* sc,
-                 double* partials, cudaStream_t s, double* xp = nullptr, int64_t ldp = 0);
+                 double* partials, cudaStream_t s, double* xp = nullptr, int64_t ldp = 0,
+                 bool f32 = false);  // f32: x, y, qm, xp hold float (opts.fp32), sums double
 // which 0: β_0 = ‖u‖ (n0, scale); 1: α_j; 2: β_{j+1} (H, scale, breakdown -> keff)
 void lanczos_scalar(int which, int j, int64_t n, int presummed, const double* partials, double* sums, int B, int K,
                     double btol, double* sc, double* H, double* n0, int* keff, cudaStream_t s);
