@@ -235,3 +235,38 @@ def test_fp32_rational_midsize_road_fig7_shape(wl):
     g = gg.grid_lcc(60, 60, 0.3, 2002)
     p, e, po, eo = _rational_fp32(wl, g, 0.0, 30, np.linspace(0.0, 100.0, 90), 2026, inner_tol=1e-6)
     assert np.max(np.abs(p - po) / np.abs(po)) < TOL32
+
+
+def test_fp32_fuzz_small_graphs(wl):
+    """Randomised small cases (n <= 30, random density incl. isolated vertices, θ incl. 1 (Lanczos batches), walk
+    function, b; k = 64 >= 2n exhausts the Krylov space, so the only error is the float storage) in the fp32 mode
+    vs the dense oracle at 1e-4."""
+    rng = np.random.default_rng(4321)
+    for case in range(25):
+        n = int(rng.integers(2, 31))
+        p = float(rng.uniform(0.05, 0.6))
+        e = [(i, j) for i in range(n) for j in range(i + 1, n) if rng.random() < p]
+        if not e:
+            e = [(0, 1)]
+        g = gg.from_edges(n, e, f"fuzz32_{case}")
+        A = D.adjacency(g)
+        rA = max(D.rho_A(A), 1.0)
+        kind = ("exp", "resolvent", "series")[case % 3]
+        if kind == "exp":
+            f, fo = ("exp", 1.0 / rA), C.exp(1.0 / rA)
+        elif kind == "resolvent":
+            a = float(rng.uniform(0.05, 0.8)) / rA
+            f, fo = ("resolvent", a), C.resolvent(a)
+        else:
+            cs = list(rng.uniform(0.0, 1.0, size=int(rng.integers(2, 7))))
+            f, fo = ("series", cs), C.series(cs)
+        thetas = [1.0] if case % 4 == 0 else list(np.round(rng.uniform(0, 1, size=int(rng.integers(1, 4))), 3))
+        b = int(rng.integers(1, 4))
+        V = gg.vectors(n, b, 200 + case)
+        op = wl.Operator(g.n, g.row_ptr, g.col_idx, thetas=thetas, f=f, krylov_dim=64, fp32=1)
+        got = op.apply(torch.from_numpy(V).cuda()).cpu().numpy()
+        for i, th in enumerate(thetas):
+            ref = D.walk_laplacian(D.phi(A, 1.0 - th, fo)) @ V
+            err = relerr(got[:, i * b:(i + 1) * b], ref).max()
+            assert err < TOL32, (case, n, kind, th, b, err)
+        op.close()
