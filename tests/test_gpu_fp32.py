@@ -231,9 +231,11 @@ def test_fp32_rational_trace_every_pole_kind(wl):
 @pytest.mark.slow
 def test_fp32_rational_midsize_road_fig7_shape(wl):
     """The Fig. 7 shape (road-like grid, NBT, M = 30, 90 t in [0, 100], the library's AAA poles) with fp32 inner
-    actions and MINRES to 1e-6 (the paper's inner tolerance), vs the oracle: p̂ at the 1e-4 bar."""
+    actions, vs the oracle's exact shifted solves: p̂ at the 1e-4 bar.  MINRES to 1e-10: with the paper's 1e-6
+     the inexact solves alone move p̂(100) by 2e-3 relative in fp64 and fp32 alike (tools/fp32_trace_tol.py:
+    1e-7 -> 4e-4, 1e-8 -> 7e-6, 1e-10 -> 1.3e-7 (fp32) / 1.5e-7 (fp64))."""
     g = gg.grid_lcc(60, 60, 0.3, 2002)
-    p, e, po, eo = _rational_fp32(wl, g, 0.0, 30, np.linspace(0.0, 100.0, 90), 2026, inner_tol=1e-6)
+    p, e, po, eo = _rational_fp32(wl, g, 0.0, 30, np.linspace(0.0, 100.0, 90), 2026, inner_tol=1e-10)
     assert np.max(np.abs(p - po) / np.abs(po)) < TOL32
 
 
