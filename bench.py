@@ -347,10 +347,12 @@ def run_walklap(args):
                            esz=4 if args.fp32 else 8, n_act=op.n_active)
     if args.walk and args.lanczos:  # Lanczos batches (R19): K + 1 SpMMs (no diagonal term), 8 n-blocks per step
         na = op.n_active            # the Krylov vectors' rows (the isolated tail carries none)
-        blk = 8 * na * G
+        esz = 4 if args.fp32 else 8  # stored element of the Lanczos vectors (R21)
+        blk, blk8 = esz * na * G, 8 * na * G
         csr = 4 * nnz_loc + 4 * (na + 1)
-        ab = {"spmv_binned": (Kab + 1) * (csr + 2 * blk + 8 * op.n_halo * G), "lanczos_vec": Kab * 8 * blk + 3 * blk,
-              "combine": Kab * blk + 8 * n_loc * G + 8 * n_loc * b + 8 * n_loc, "batch_inputs": 8 * na * b + blk}
+        ab = {"spmv_binned": (csr + 2 * blk8 + 8 * op.n_halo * G) + Kab * (csr + 2 * blk + esz * op.n_halo * G),
+              "lanczos_vec": Kab * 8 * blk + 3 * blk,
+              "combine": Kab * blk + 8 * n_loc * G + 8 * n_loc * b + 8 * n_loc, "batch_inputs": 8 * na * b + blk8}
     kernels = {}
     for name, (tot_ms, cnt) in prof.items():
         per_step_ms = tot_ms / args.steps
