@@ -231,6 +231,9 @@ struct wl_operator {
   wl_opts opts{};
   DArr<double> tprime;  // n_loc x n_theta, internal row order: t - c_0 (φ1 minus its identity term)
   DArr<int32_t> perm;   // internal row -> user row (degree-sorted relabelling); empty = identity
+  // buffers of the spectral-radius estimates (0: ρ(A), 1: ρ(Z_θ)), kept between calls: a fresh workspace per
+  // call cost a cudaMalloc/cudaFree of k+3 outer vectors (~10 GB for ρ(Z) on C4) each time
+  mutable struct wl_workspace* est_ws[2] = {nullptr, nullptr};
 };
 
 struct wl_workspace {
@@ -1420,6 +1423,8 @@ void wl_operator_destroy(wl_operator* op) {
   if (!op) return;
   DeviceGuard dg(op->device);
   WL_CUDA(cudaDeviceSynchronize());
+  delete op->est_ws[0];
+  delete op->est_ws[1];
   delete op;
 }
 
@@ -1591,7 +1596,8 @@ wl_status wl_spectral_radius(const wl_operator* op, int32_t k, double* rho_out, 
     if (k < 2 || k > 128) throw Error(WL_EINVAL, "k must be in [2, 128]");
     DeviceGuard dg(op->device);
     cudaStream_t s = S_(stream);
-    wl_workspace ws;
+    if (!op->est_ws[0]) op->est_ws[0] = new wl_workspace;
+    wl_workspace& ws = *op->est_ws[0];
     ws.op = op;
     outer_alloc(op, &ws, k, 1);
     spmv_scratch(op, &ws, 1);
@@ -1620,7 +1626,8 @@ wl_status wl_spectral_radius_z(const wl_operator* op, int32_t theta_index, int32
     if (theta_index < 0 || theta_index >= op->n_theta) throw Error(WL_EINVAL, "theta_index out of range");
     DeviceGuard dg(op->device);
     cudaStream_t s = S_(stream);
-    wl_workspace ws;
+    if (!op->est_ws[1]) op->est_ws[1] = new wl_workspace;
+    wl_workspace& ws = *op->est_ws[1];
     ws.op = op;
     const int64_t np = outer_stride(op), len = 2 * np;  // Z vector = [top np ; bottom np], pad rows stay 0
     outer_alloc(op, &ws, k, 1, len);
