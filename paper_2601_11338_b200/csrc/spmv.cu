@@ -42,6 +42,10 @@
 #ifndef WL_SPMV_MINB_S
 #define WL_SPMV_MINB_S 3
 #endif
+// 1: column ids of the next round loaded before the current round's gathers are summed (tools/kernel_variants.sh)
+#ifndef WL_SPMV_PREFETCH
+#define WL_SPMV_PREFETCH 0
+#endif
 // fp32 storage (8-float lanes): unroll and min CTAs per SM of the row kernel
 #ifndef WL_SPMV_UW_F
 #define WL_SPMV_UW_F 4
@@ -198,6 +202,30 @@ struct Ctx {
   __device__ Vec<VW, Acc> strided_sum(int z0, int z1, int first, int step) const {
     Vec<VW, Acc> acc = vzero<VW, Acc>();
     int base = z0;
+#if WL_SPMV_PREFETCH
+    // the next full round's column ids are loaded before this round's gathers are consumed (one id latency
+    // hidden per round)
+    if (base + kU * step <= z1) {
+      int cl[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) cl[u] = col(base + first + u * step);
+      for (;;) {
+        const int nb = base + kU * step;
+        const bool more = nb + kU * step <= z1;  // warp-uniform (shared base)
+        int nx[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) nx[u] = more ? col(nb + first + u * step) : 0;
+        Vec<VW, T> v[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) v[u] = gather(cl[u]);
+        add_round(acc, v);
+        base = nb;
+        if (!more) break;
+#pragma unroll
+        for (int u = 0; u < kU; ++u) cl[u] = nx[u];
+      }
+    }
+#else
     for (; base + kU * step <= z1; base += kU * step) {
       int cl[kU];
 #pragma unroll
@@ -207,6 +235,7 @@ struct Ctx {
       for (int u = 0; u < kU; ++u) v[u] = gather(cl[u]);
       add_round(acc, v);
     }
+#endif
     const int z = base + first;
     if (base < z1) {  // predicated tail round
       int cl[kU];
