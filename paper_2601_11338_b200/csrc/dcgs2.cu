@@ -70,8 +70,14 @@ __host__ __device__ constexpr int stage_elems() { return 16384 / (int)sizeof(T);
 #ifndef WL_UPD_F_ACC32
 #define WL_UPD_F_ACC32 1
 #endif
+#ifndef WL_DOTS_F_CONSUMERS
+#define WL_DOTS_F_CONSUMERS 128
+#endif
 template <class T>
 __host__ __device__ constexpr int dots_per() { return sizeof(T) == 8 ? kDotsPer : WL_DOTS_F_PER; }
+template <class T>
+__host__ __device__ constexpr int dots_consumers() { return sizeof(T) == 8 ? kDotsConsumers : WL_DOTS_F_CONSUMERS; }
+static_assert(WL_DOTS_F_CONSUMERS * WL_DOTS_F_PER <= 2048, "float dots tiles fit a 2048-element stage");
 // toar_update with float storage: 480 consumers x 8 elements (15 KB tiles; 16 warps, so up to 128 registers
 // hold the 3 x 8 double accumulators without spilling), double: 512 x 4
 template <class T>
@@ -161,7 +167,8 @@ __device__ __forceinline__ void ring_init(uint64_t* full, uint64_t* empty, int c
 
 // pass A: items [P, w?, q_0..q_{nq-1}]; T = the storage type (values are converted and summed in double)
 template <class T>
-__global__ void __launch_bounds__(kDotsConsumers + 32, 1) dcgs2_dots_ring(Dcgs2Args a, int tpb) {
+__global__ void __launch_bounds__(dots_consumers<T>() + 32, 1) dcgs2_dots_ring(Dcgs2Args a, int tpb) {
+  constexpr int kCons = dots_consumers<T>();
   constexpr int SE = 2048;
   constexpr int kStages = ring_stages<T, SE>();
   extern __shared__ __align__(128) double ring_raw[];
@@ -174,7 +181,7 @@ __global__ void __launch_bounds__(kDotsConsumers + 32, 1) dcgs2_dots_ring(Dcgs2A
   const int E = tpb * PER;
   const int64_t N = a.len * a.B, h = a.split * a.B;
   const bool has_w = a.wa != nullptr;
-  ring_init(full, empty, kDotsConsumers / 32, kStages);
+  ring_init(full, empty, kCons / 32, kStages);
   // the basis loads below carry no bounds predicate (fewer instructions in the 32x-unrolled loop:
   // less icache pressure).  Entries they read past a ragged tile's end, or past E for a lane beyond
   // tpb, meet p = w = 0 and must be finite: zero [E, stage end) of every stage, and the whole ring in
@@ -190,7 +197,7 @@ __global__ void __launch_bounds__(kDotsConsumers + 32, 1) dcgs2_dots_ring(Dcgs2A
   double acc[2 * kMaxVecPerLaunch], alpha = 0.0, beta = 0.0, gamma = 0.0;
 #pragma unroll
   for (int v = 0; v < 2 * kMaxVecPerLaunch; ++v) acc[v] = 0.0;
-  if (warp == kDotsConsumers / 32) {
+  if (warp == kCons / 32) {
     if (lane == 0)
       ring_produce<T, SE>(a, reinterpret_cast<const T*>(a.P), has_w ? reinterpret_cast<const T*>(a.wa) : nullptr,
                       reinterpret_cast<const T*>(a.wb), h, E, ring, full, empty);
@@ -263,22 +270,22 @@ __global__ void __launch_bounds__(kDotsConsumers + 32, 1) dcgs2_dots_ring(Dcgs2A
   __syncthreads();  // every copy has landed and been consumed: the ring is free
   // epilogue: per (value, column) sum over the consumer threads of that column, fixed order
   const int nval = 2 * nq + 3;
-  double* red = ring_raw;  // [kRedBatch][kDotsConsumers]
+  double* red = ring_raw;  // [kRedBatch][kCons]
   for (int v0 = 0; v0 < nval; v0 += kRedBatch) {
-    if (t < kDotsConsumers) {
+    if (t < kCons) {
 #pragma unroll
       for (int u = 0; u < 2 * kMaxVecPerLaunch; ++u)
-        if (u < 2 * nq && u >= v0 && u < v0 + kRedBatch) red[(u - v0) * kDotsConsumers + t] = acc[u];
-      if (2 * nq >= v0 && 2 * nq < v0 + kRedBatch) red[(2 * nq - v0) * kDotsConsumers + t] = alpha;
-      if (2 * nq + 1 >= v0 && 2 * nq + 1 < v0 + kRedBatch) red[(2 * nq + 1 - v0) * kDotsConsumers + t] = beta;
-      if (2 * nq + 2 >= v0 && 2 * nq + 2 < v0 + kRedBatch) red[(2 * nq + 2 - v0) * kDotsConsumers + t] = gamma;
+        if (u < 2 * nq && u >= v0 && u < v0 + kRedBatch) red[(u - v0) * kCons + t] = acc[u];
+      if (2 * nq >= v0 && 2 * nq < v0 + kRedBatch) red[(2 * nq - v0) * kCons + t] = alpha;
+      if (2 * nq + 1 >= v0 && 2 * nq + 1 < v0 + kRedBatch) red[(2 * nq + 1 - v0) * kCons + t] = beta;
+      if (2 * nq + 2 >= v0 && 2 * nq + 2 < v0 + kRedBatch) red[(2 * nq + 2 - v0) * kCons + t] = gamma;
     }
     __syncthreads();
     const int nv = min(kRedBatch, nval - v0);
     for (int idx = warp; idx < nv * B; idx += blockDim.x / 32) {  // a warp per output, fixed-order tree
       const int vv = idx / B, c = idx - vv * B;
       double sum = 0.0;
-      for (int tt = c + lane * B; tt < tpb; tt += 32 * B) sum += red[vv * kDotsConsumers + tt];
+      for (int tt = c + lane * B; tt < tpb; tt += 32 * B) sum += red[vv * kCons + tt];
       for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
       if (lane == 0) a.partials[(int64_t)((v0 + vv) * B + c) * gridDim.x + blockIdx.x] = sum;
     }
@@ -501,12 +508,13 @@ int dcgs2_dots(Dcgs2Args a, cudaStream_t s) {
       WL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ring_smem()));
       attr[a.f32 ? 1 : 0] = true;
     }
-    const int tpb = kDotsConsumers / a.B * a.B;
+    const int nc = a.f32 ? dots_consumers<float>() : dots_consumers<double>();
+    const int tpb = nc / a.B * a.B;
     const int64_t N = a.len * a.B;
     // one persistent CTA per SM; an empty rank (N = 0) still launches one CTA so its partials are zeros
     const int E = tpb * (a.f32 ? dots_per<float>() : dots_per<double>());
     a.grid = (int)std::max<int64_t>(1, std::min<int64_t>(num_sms(), (N + E - 1) / E));
-    kern<<<a.grid, kDotsConsumers + 32, ring_smem(), s>>>(a, tpb);
+    kern<<<a.grid, nc + 32, ring_smem(), s>>>(a, tpb);
     WL_CUDA(cudaGetLastError());
     if (a.sums_out) {  // null: the consumer reduces the partials itself (a.grid of them per output)
       note_launch("gram_reduce");
