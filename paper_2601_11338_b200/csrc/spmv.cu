@@ -42,6 +42,10 @@
 #ifndef WL_SPMV_MINB_S
 #define WL_SPMV_MINB_S 3
 #endif
+// 1: the medium rows (several per warp) and the hub chunks of wide-lane kernels load their column ids 4 at a time
+#ifndef WL_SPMV_VEC4
+#define WL_SPMV_VEC4 0
+#endif
 // 1: column ids of the next round loaded before the current round's gathers are summed (tools/kernel_variants.sh)
 #ifndef WL_SPMV_PREFETCH
 #define WL_SPMV_PREFETCH 0
@@ -248,6 +252,27 @@ struct Ctx {
     }
     return acc;
   }
+  // Σ y[col[z]] over [z0, z1) with the column ids of the 4-aligned body loaded 4 at a time (one 16-byte load per
+  // 4 gathers: in the medium-row path a warp's id loads touched 5 rows' sectors 4 times per round, a quarter of
+  // the L1 wavefronts); group `first` of `step` groups takes the body's 4-id chunks first, first + step, ...; the
+  // unaligned head and the tail (< 4 ids each) go through strided_sum.  kU == 4.
+  __device__ Vec<VW, Acc> vec4_sum(int z0, int z1, int first, int step) const {
+    const int za = min(z1, (z0 + 3) & ~3);
+    Vec<VW, Acc> acc = strided_sum(z0, za, first, step);
+    const int nch = (z1 - za) >> 2;
+    const int4* c4 = reinterpret_cast<const int4*>(a.col + za);
+    for (int c = first; c < nch; c += step) {
+      const int4 id = __ldg(c4 + c);
+      Vec<VW, T> v[kU];
+      v[0] = gather(id.x);
+      v[1] = gather(id.y);
+      v[2] = gather(id.z);
+      v[3] = gather(id.w);
+      add_round(acc, v);
+    }
+    vadd(acc, strided_sum(za + 4 * nch, z1, first, step));
+    return acc;
+  }
   // one round of kU gathered rows into the double accumulator; fp32 storage sums the round in float first
   // (one conversion per round instead of per row: its rounding is that of the stored values)
   __device__ static void add_round(Vec<VW, Acc>& acc, const Vec<VW, T> (&v)[kU]) {
@@ -328,7 +353,11 @@ __global__ void __launch_bounds__(kThreads, VW == 1 ? 1 : (sizeof(T) == 4 ? WL_S
       const bool ok = rs < a.med_rpw && idx < a.n_medium;
       const int r = ok ? a.medium_rows[idx] : 0;
       const int z0 = ok ? __ldg(a.rowptr + r) : 0, z1 = ok ? __ldg(a.rowptr + r + 1) : 0;
-      const Vec<VW, Acc> part = ok ? ctx.strided_sum(z0, z1, gi2, G2) : vzero<VW, Acc>();
+      Vec<VW, Acc> part = vzero<VW, Acc>();
+      if (ok) {
+        if constexpr (WL_SPMV_VEC4 && VW > 1 && kU == 4) part = ctx.vec4_sum(z0, z1, gi2, G2);
+        else part = ctx.strided_sum(z0, z1, gi2, G2);
+      }
       Vec<VW, Acc> sum = part;
       for (int g = 1; g < G2; ++g) {
         const int src = base + ((lane - base) + g * W) % LR;
@@ -352,7 +381,11 @@ __global__ void __launch_bounds__(kThreads, VW == 1 ? 1 : (sizeof(T) == 4 ? WL_S
     const int idx = blk * kWarps + warp;
     if (idx >= a.n_chunks) return;
     const int4 ch = a.chunks[idx];  // (row, z0, z1, first chunk index of the row)
-    const Vec<VW, Acc> part = lane_ok ? ctx.strided_sum(ch.y, ch.z, gi, gpw) : vzero<VW, Acc>();
+    Vec<VW, Acc> part = vzero<VW, Acc>();
+    if (lane_ok) {
+      if constexpr (WL_SPMV_VEC4 && VW > 1 && kU == 4) part = ctx.vec4_sum(ch.y, ch.z, gi, gpw);
+      else part = ctx.strided_sum(ch.y, ch.z, gi, gpw);
+    }
     const Vec<VW, Acc> sum = group_reduce<VW>(part, W, gpw);
     const int ldp = W * VW;  // partial row: every column slot of the lane group
     if (gi == 0) {
