@@ -30,6 +30,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
+#include <cstring>
 #include <type_traits>
 
 // compile-time tuning knobs (tools/build_variants.sh): wide-lane unroll, min CTAs per SM of the rows kernel
@@ -640,6 +641,13 @@ void spmv(const SpmvArgs& a0, cudaStream_t s) {
   const int med_rpw = med_rpw_env ? med_rpw_env : (a.f32 ? 8 : 5);
   a.med_rpw = (W > 1 && med_rpw > 1 && gpw / med_rpw >= 1) ? med_rpw : 1;
   const int rows_per_warp = a.med_sub ? 32 / a.med_sub : a.med_rpw;
+  // profiling only (wrong results): WL_SPMV_ONLY = any of "s", "m", "h" launches only those row classes
+  static const char* only = getenv("WL_SPMV_ONLY");
+  if (only) {
+    if (!strchr(only, 's')) { a.n_small = 0; a.nblk_small = 0; }
+    if (!strchr(only, 'm')) a.n_medium = 0;
+    if (!strchr(only, 'h')) a.n_chunks = 0;
+  }
   a.nblk_medium = (a.n_medium + kWarps * rows_per_warp - 1) / (kWarps * rows_per_warp);
   const int nblk_hub = (a.n_chunks + kWarps - 1) / kWarps;
   const int grid = a.nblk_small + a.nblk_medium + nblk_hub;
