@@ -149,6 +149,7 @@ struct CsrPart {
   int64_t nnz = 0;
   int n_small = 0, n_medium = 0, n_chunks = 0;
   int small_first = -1;  // small rows form the contiguous id range [small_first, +n_small), or -1
+  int medium_first = -1; // medium rows form the contiguous id range [medium_first, +n_medium), or -1
   int n_iso = 0;          // the last n_iso rows of that range have no nonzeros
 
   void upload(const std::vector<int32_t>& rp, const std::vector<int32_t>& col_h, const std::vector<int32_t>* rows) {
@@ -170,6 +171,8 @@ struct CsrPart {
     n_medium = (int)md.size();
     // the batched small-row kernel needs contiguous ids and writes rows in place (no out_row)
     small_first = (!rows && !sm.empty() && sm.back() - sm.front() + 1 == (int32_t)sm.size()) ? sm.front() : -1;
+    // (the degree-sorted relabelling makes both ranges contiguous: the kernels then skip the row-list load)
+    medium_first = (!md.empty() && md.back() - md.front() + 1 == (int32_t)md.size()) ? md.front() : -1;
     // trailing rows of that range without nonzeros (isolated vertices sort last): a plain stream kernel
     n_iso = 0;
     if (small_first >= 0)
@@ -346,6 +349,7 @@ void spmv_part(const wl_operator* op, wl_workspace* ws, const CsrPart& part, boo
   a.small_rows = part.small_rows.p;
   a.n_small = part.n_small;
   a.small_first = part.small_first;
+  a.medium_first = part.medium_first;
   a.n_iso = part.n_iso;
   a.medium_rows = part.medium_rows.p;
   a.n_medium = part.n_medium;

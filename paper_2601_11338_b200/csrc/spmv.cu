@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(kThreads, VW == 1 ? 1 : (sizeof(T) == 4 ? WL_S
   if (blk < a.nblk_small) {  // ---- small rows: one lane group per row
     const int idx = (blk * kWarps + warp) * gpw + gi;
     if (!lane_ok || idx >= a.n_small) return;
-    const int r = a.small_rows[idx];
+    const int r = a.small_first >= 0 ? a.small_first + idx : a.small_rows[idx];  // contiguous: no list load
     const int z0 = __ldg(a.rowptr + r), z1 = __ldg(a.rowptr + r + 1);
     ctx.write(r, z1 - z0, ctx.strided_sum(z0, z1, 0, 1));
     return;
@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(kThreads, VW == 1 ? 1 : (sizeof(T) == 4 ? WL_S
       // and the tail round of a ~100-300-nonzero row wastes L lanes instead of 32
       const int L = a.med_sub;
       const int idx = (blk * kWarps + warp) * (32 / L) + lane / L, lg = lane % L;
-      const int r = idx < a.n_medium ? a.medium_rows[idx] : 0;
+      const int r = idx < a.n_medium ? (a.medium_first >= 0 ? a.medium_first + idx : a.medium_rows[idx]) : 0;
       const int z0 = idx < a.n_medium ? __ldg(a.rowptr + r) : 0, z1 = idx < a.n_medium ? __ldg(a.rowptr + r + 1) : 0;
       Vec<VW, Acc> part = ctx.strided_sum(z0, z1, lg, L);
 #pragma unroll
@@ -352,7 +352,7 @@ __global__ void __launch_bounds__(kThreads, VW == 1 ? 1 : (sizeof(T) == 4 ? WL_S
       const int rs = lane / LR, base = rs * LR, gi2 = (lane - base) / W;
       const int idx = (blk * kWarps + warp) * a.med_rpw + rs;
       const bool ok = rs < a.med_rpw && idx < a.n_medium;
-      const int r = ok ? a.medium_rows[idx] : 0;
+      const int r = ok ? (a.medium_first >= 0 ? a.medium_first + idx : a.medium_rows[idx]) : 0;
       const int z0 = ok ? __ldg(a.rowptr + r) : 0, z1 = ok ? __ldg(a.rowptr + r + 1) : 0;
       Vec<VW, Acc> part = vzero<VW, Acc>();
       if (ok) {
@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(kThreads, VW == 1 ? 1 : (sizeof(T) == 4 ? WL_S
     }
     const int idx = blk * kWarps + warp;
     if (idx >= a.n_medium) return;
-    const int r = a.medium_rows[idx];
+    const int r = a.medium_first >= 0 ? a.medium_first + idx : a.medium_rows[idx];
     const int z0 = __ldg(a.rowptr + r), z1 = __ldg(a.rowptr + r + 1);
     const Vec<VW, Acc> part = lane_ok ? ctx.strided_sum(z0, z1, gi, gpw) : vzero<VW, Acc>();
     const Vec<VW, Acc> sum = group_reduce<VW>(part, W, gpw);

@@ -109,6 +109,7 @@ struct SpmvArgs {
   int small_first;                   // small rows are ids [small_first, small_first + n_small), or -1
   int n_iso;                         // the last n_iso of them have no nonzeros (out = scale (g0 + g1 d) x)
   const int32_t* medium_rows; int n_medium;
+  int medium_first;                  // medium rows are ids [medium_first, medium_first + n_medium), or -1
   const int4* chunks; int n_chunks;  // (row, z0, z1, first chunk index of that row)
   double* chunk_part;                // n_chunks * B partial sums (scratch)
   unsigned int* row_ticket;          // n_chunks, zero between launches
