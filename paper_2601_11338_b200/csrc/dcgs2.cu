@@ -70,14 +70,19 @@ __host__ __device__ constexpr int stage_elems() { return 16384 / (int)sizeof(T);
 #ifndef WL_UPD_F_ACC32
 #define WL_UPD_F_ACC32 1
 #endif
+// float dot pass: 192 consumers x 16 elements in 16 KB stages (C4 fp32: 0.78 -> 0.98 of HBM; 128 x 16 in 8 KB
+// stages was issue/fetch bound — twice the ring operations per byte of the double pass)
 #ifndef WL_DOTS_F_CONSUMERS
-#define WL_DOTS_F_CONSUMERS 128
+#define WL_DOTS_F_CONSUMERS 192
+#endif
+#ifndef WL_DOTS_F_SE
+#define WL_DOTS_F_SE 4096  // float dot-pass stage (elements); the ring holds 192 KB / (4 SE) stages
 #endif
 template <class T>
 __host__ __device__ constexpr int dots_per() { return sizeof(T) == 8 ? kDotsPer : WL_DOTS_F_PER; }
 template <class T>
 __host__ __device__ constexpr int dots_consumers() { return sizeof(T) == 8 ? kDotsConsumers : WL_DOTS_F_CONSUMERS; }
-static_assert(WL_DOTS_F_CONSUMERS * WL_DOTS_F_PER <= 2048, "float dots tiles fit a 2048-element stage");
+static_assert(WL_DOTS_F_CONSUMERS * WL_DOTS_F_PER <= WL_DOTS_F_SE, "float dots tiles fit a stage");
 // toar_update with float storage: 480 consumers x 8 elements (15 KB tiles; 16 warps, so up to 128 registers
 // hold the 3 x 8 double accumulators without spilling), double: 512 x 4
 template <class T>
@@ -169,7 +174,7 @@ __device__ __forceinline__ void ring_init(uint64_t* full, uint64_t* empty, int c
 template <class T>
 __global__ void __launch_bounds__(dots_consumers<T>() + 32, 1) dcgs2_dots_ring(Dcgs2Args a, int tpb) {
   constexpr int kCons = dots_consumers<T>();
-  constexpr int SE = 2048;
+  constexpr int SE = sizeof(T) == 8 ? 2048 : WL_DOTS_F_SE;
   constexpr int kStages = ring_stages<T, SE>();
   extern __shared__ __align__(128) double ring_raw[];
   T* ring = reinterpret_cast<T*>(ring_raw);
