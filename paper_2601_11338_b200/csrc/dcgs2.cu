@@ -65,6 +65,13 @@ __host__ __device__ constexpr int stage_elems() { return 16384 / (int)sizeof(T);
 #ifndef WL_UPD_F_SE
 #define WL_UPD_F_SE 6144
 #endif
+// double toar_update: 512 consumers x WL_UPD_D_PER elements in WL_UPD_D_SE-element stages
+#ifndef WL_UPD_D_PER
+#define WL_UPD_D_PER 4
+#endif
+#ifndef WL_UPD_D_SE
+#define WL_UPD_D_SE 2048
+#endif
 // 1: the float update accumulates in float (coefficients rounded to float: one FFMA per element and output);
 // 0: in double (one float -> double conversion per element on the XU pipe, NOUT DFMA)
 #ifndef WL_UPD_F_ACC32
@@ -96,8 +103,8 @@ static_assert(WL_DOTS_F_CONSUMERS * WL_DOTS_F_PER <= WL_DOTS_F_SE, "float dots t
 template <class T>
 __host__ __device__ constexpr int upd_consumers() { return sizeof(T) == 8 ? kUpdConsumers : WL_UPD_F_CONSUMERS; }
 template <class T>
-__host__ __device__ constexpr int upd_per() { return sizeof(T) == 8 ? kUpdPer : WL_UPD_F_PER; }
-static_assert(WL_UPD_F_CONSUMERS * WL_UPD_F_PER <= WL_UPD_F_SE && 128 * WL_DOTS_F_PER <= 2048, "float tiles fit a stage");
+__host__ __device__ constexpr int upd_per() { return sizeof(T) == 8 ? WL_UPD_D_PER : WL_UPD_F_PER; }
+static_assert(WL_UPD_F_CONSUMERS * WL_UPD_F_PER <= WL_UPD_F_SE && kUpdConsumers * WL_UPD_D_PER <= WL_UPD_D_SE, "update tiles fit a stage");
 constexpr int kRedBatch = 24;                       // dots epilogue: values per smem round
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -385,7 +392,7 @@ __global__ void __launch_bounds__(kUpdConsumers + 32, 1) dcgs2_update_ring(Dcgs2
 constexpr int kToarMaxOut = 3;
 template <int NOUT, class T>
 __global__ void __launch_bounds__(upd_consumers<T>() + 32, 1) toar_update_ring(ToarArgs a, int tpb) {
-  constexpr int SE = sizeof(T) == 8 ? stage_elems<T>() : WL_UPD_F_SE;
+  constexpr int SE = sizeof(T) == 8 ? WL_UPD_D_SE : WL_UPD_F_SE;
   constexpr int kStages = ring_stages<T, SE>();
   constexpr int PER = upd_per<T>();
   extern __shared__ __align__(128) double ring_raw[];
